@@ -1,0 +1,173 @@
+/*
+ * snn.h -- C ABI of libsnn, the B200 (sm_100a) spike-wave step of a convolutional SNN with at
+ * most one spike per neuron (SpykeTorch, arxiv 1903.02440).  Citations: "P:<line>" = a line of
+ * the paper's text, "R<n>" = a reading recorded in DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *  - Every tensor argument is a DEVICE pointer owned by the caller (allocated e.g. by torch).  The
+ *    library never allocates, frees or caches device memory; scratch space comes from a caller
+ *    buffer sized by the matching *_workspace() call.
+ *  - Every call is asynchronous on the given CUDA stream (`snn_stream_t` = cudaStream_t; NULL =
+ *    legacy default stream) and never synchronises.
+ *  - Layouts are row-major (C order).  A latency grid is uint8 with SNN_NO_SPIKE = 255 for "no
+ *    spike" (the paper's infinity); valid spike times are 0..T-1 with 1 <= T <= 254.
+ *  - Return codes: SNN_OK (0) or a negative SNN_E* code.  Host-side argument checks run before any
+ *    launch; on error nothing is launched and snn_last_error() returns a message (thread-local).
+ *    Device-detected conditions (e.g. a weight outside the exact domain, see snn_conv_fire) set a
+ *    device error word that snn_sync_status() reports.
+ *  - Functions are stateless and thread-safe.  Plasticity calls on one weight tensor must be
+ *    serialised by the caller (single writer).
+ */
+#ifndef SNN_H_
+#define SNN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* snn_stream_t;
+
+#if defined(__GNUC__)
+#define SNN_API __attribute__((visibility("default")))
+#else
+#define SNN_API
+#endif
+
+#define SNN_NO_SPIKE 255
+
+#define SNN_OK 0
+#define SNN_EINVAL (-1)     /* bad scalar argument (T range, k < 1, NaN threshold, LB >= UB, ...) */
+#define SNN_ESHAPE (-2)     /* shape rule violated (kernel larger than padded input, index overflow) */
+#define SNN_ECUDA (-3)      /* a CUDA launch / runtime call failed */
+#define SNN_EINEXACT (-4)   /* device: a weight is outside the exact fixed-point domain (N1) */
+#define SNN_EWORKSPACE (-5) /* workspace pointer NULL or smaller than *_workspace() */
+
+/* ---------------------------------------------------------------------------------------------
+ * a1. Intensity -> latency encoding (P:51, P:135 utils.Intensity2Latency; readings R1, R2).
+ * x   : float32 [B, C, H, W] intensities.  Per image, the N strictly positive entries (x > 0;
+ *       zero, negative and NaN never spike) are ranked by (value descending, flat index c*H*W +
+ *       y*W + x ascending) and split into T bins: with q = N / T and m = N % T the first m bins hold
+ *       q + 1 entries and the others q.  lat = bin index of the entry's rank.
+ * lat : uint8 [B, C, H, W] output; SNN_NO_SPIKE for non-positive entries.
+ * Requires 1 <= T <= 254 and C*H*W < 2^24.  Workspace: snn_encode_workspace(B, C, H, W, T).
+ * ------------------------------------------------------------------------------------------- */
+SNN_API size_t snn_encode_workspace(int B, int C, int H, int W, int T);
+SNN_API int snn_encode(const float* x, int B, int C, int H, int W, int T, uint8_t* lat,
+               void* ws, size_t ws_bytes, snn_stream_t s);
+
+/* Eq. 1: wave[b, t, i] = 1.0f if lat[b, i] != NO_SPIKE and t >= lat[b, i], else 0.
+ * lat uint8 [B, n], wave float32 [B, T, n].  Validation / tests only (the hot path never
+ * materialises waves). */
+SNN_API int snn_expand(const uint8_t* lat, int B, int n, int T, float* wave, snn_stream_t s);
+
+/* Count entries of lat[n] that are neither < T nor NO_SPIKE (an invalid latency); the count is
+ * written (not accumulated) to *n_bad (int32, device). */
+SNN_API int snn_validate_lat(const uint8_t* lat, size_t n, int T, int32_t* n_bad, snn_stream_t s);
+
+/* ---------------------------------------------------------------------------------------------
+ * a2 + a3. Spiking convolution fused with threshold firing.
+ * Potentials (Eq. 2; R5, R6): for output neuron (f, y, x) of image b,
+ *   P[t] = sum over c, ky, kx of w[f, c, ky, kx] * [lat_in[b, c, y+ky-pad, x+kx-pad] <= t],
+ * a valid stride-1 cross-correlation of the zero-padded spike-wave (padding never spikes);
+ * Ho = H + 2*pad - KH + 1, Wo = W + 2*pad - KW + 1.
+ * Fire (R3): lat_out = min{t < T : P[t] > theta}, else NO_SPIKE; v_out = fp32(P[lat_out])
+ * (round-to-nearest of the exact potential), 0 if no spike.  theta = +INFINITY selects Eq. 5
+ * (R9): lat_out = T-1 iff P[T-1] > 0 and v_out = fp32(P[T-1]).
+ * Exactness (N1): potentials are accumulated exactly as integers in units of 2^-31, so
+ * every weight must satisfy w*2^31 integral and 0 <= w <= 1 (true for every w in {0} U [2^-8, 1]).
+ * A weight outside that domain sets the device error word (SNN_EINEXACT at snn_sync_status()).
+ *   lat_in  uint8 [B, C, H, W];   w float32 [F, C, KH, KW]
+ *   lat_out uint8 [B, F, Ho, Wo]; v_out float32 [B, F, Ho, Wo]
+ *   pot_out float32 [B, T, F, Ho, Wo] or NULL: if non-NULL every fp32(P[t]) is written (validation
+ *           mode, no early exit).
+ * Workspace: snn_conv_fire_workspace(...) bytes.
+ * ------------------------------------------------------------------------------------------- */
+SNN_API size_t snn_conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T);
+SNN_API int snn_conv_fire(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
+                  const float* w, int F, int KH, int KW, int T, float theta,
+                  uint8_t* lat_out, float* v_out, float* pot_out,
+                  void* ws, size_t ws_bytes, snn_stream_t s);
+
+/* ---------------------------------------------------------------------------------------------
+ * a4. Spike-wave max-pooling (Eq. 3; readings R10-R12).
+ * Window PH x PW, stride SH x SW, zero padding DH x DW (padding never spikes).
+ * Ho = (H + 2*DH - PH) / SH + 1, Wo = (W + 2*DW - PW) / SW + 1 (windows inside the padded input).
+ * lat_out = min of lat over the window (earliest spike); v_out = max of v over the window entries
+ * whose lat equals lat_out (0 if none): the per-time-step max-pool of the thresholded potentials
+ * read at the pooled spike time.  v / v_out may both be NULL (latencies only).
+ *   lat, v [B, F, H, W] -> lat_out, v_out [B, F, Ho, Wo]
+ * ------------------------------------------------------------------------------------------- */
+SNN_API int snn_pool(const uint8_t* lat, const float* v, int B, int F, int H, int W,
+             int PH, int PW, int SH, int SW, int DH, int DW,
+             uint8_t* lat_out, float* v_out, snn_stream_t s);
+
+/* ---------------------------------------------------------------------------------------------
+ * a5. Pointwise (cross-feature) inhibition (R13, R14).  At each (b, y, x) the spiking
+ * feature with the smallest key (lat ascending, v descending, f ascending) keeps its (lat, v);
+ * every other feature becomes (NO_SPIKE, 0).  winner_f[b, y, x] = that feature or -1 (may be
+ * NULL).  lat, v, lat_out, v_out: [B, F, H, W]; winner_f int16 [B, H, W].
+ * ------------------------------------------------------------------------------------------- */
+SNN_API int snn_inhibit(const uint8_t* lat, const float* v, int B, int F, int H, int W,
+                uint8_t* lat_out, float* v_out, int16_t* winner_f, snn_stream_t s);
+
+/* ---------------------------------------------------------------------------------------------
+ * a6. k winners-take-all with inhibition radius r (R13-R15).  Up to k rounds
+ * per image: the winner is the non-excluded spiking neuron with the smallest key (lat ascending,
+ * v descending, flat index f*H*W + y*W + x ascending); then its whole feature map and every neuron
+ * at Chebyshev distance <= r from (y, x) in all maps are excluded.  Stops early when no candidate
+ * is left (fewer than k winners is legal).
+ *   winners int32 [B, k, 3] = (feature, row, column), rows past count[b] are -1.
+ *   count   int32 [B].
+ * Requires k >= 1, r >= 0, F*H*W <= 2^24.  Workspace: snn_k_winners_workspace(B, F, H, W).
+ * ------------------------------------------------------------------------------------------- */
+SNN_API size_t snn_k_winners_workspace(int B, int F, int H, int W);
+SNN_API int snn_k_winners(const uint8_t* lat, const float* v, int B, int F, int H, int W, int k, int r,
+                  int32_t* winners, int32_t* count, void* ws, size_t ws_bytes, snn_stream_t s);
+
+/* ---------------------------------------------------------------------------------------------
+ * a7. STDP / R-STDP weight update of ONE image, in place (Eq. 4; R17-R23).
+ * For each winner (f, y, x) among winners[0 .. count[0]-1] and each synapse (c, ky, kx):
+ *   pre  = lat_in[c, y+ky-pad, x+kx-pad] (NO_SPIKE outside the input), post = lat_out[f, y, x];
+ *   a    = A+ if pre != NO_SPIKE and pre <= post, else A-;
+ *   dW   = (a * (W - lb)) * (ub - W) if stabilizer else a;   W = clamp(W + dW, lb, ub)
+ * evaluated in fp32 round-to-nearest without FMA contraction.  Winners have distinct features
+ * (snn_k_winners guarantees it), so synapse updates never collide.
+ * reward (device float scalar, may be NULL = +1): +1 applies (A+, A-), -1 applies (-A+, -A-)
+ * (anti-STDP), 0 skips the update (silent sample).
+ *   w        float32 [F, C, KH, KW] (in/out)
+ *   lat_in   uint8 [C, H, W];  lat_out uint8 [F, Ho, Wo]
+ *   winners  int32 [k, 3];     count int32 [1]
+ * ------------------------------------------------------------------------------------------- */
+SNN_API int snn_stdp_update(float* w, int F, int C, int KH, int KW,
+                    const uint8_t* lat_in, int H, int W, int pad,
+                    const uint8_t* lat_out, int Ho, int Wo,
+                    const int32_t* winners, const int32_t* count, int k,
+                    float a_plus, float a_minus, float lb, float ub, int stabilizer,
+                    const float* reward, snn_stream_t s);
+
+/* R-STDP decision on device (R24, R25): for each image b, decision[b] =
+ * winners[b, 0, 0] / (F / n_classes) (the block decision_map) or -1 when count[b] == 0 (silent);
+ * reward[b] = +1 if decision == labels[b], -1 if it differs, 0 when silent.  labels may be NULL
+ * (reward then 0).  winners [B, k, 3], count [B], labels int32 [B], decision int32 [B],
+ * reward float32 [B] (reward may be NULL). */
+SNN_API int snn_decide(const int32_t* winners, const int32_t* count, int B, int k, int F, int n_classes,
+               const int32_t* labels, int32_t* decision, float* reward, snn_stream_t s);
+
+/* ---------------------------------------------------------------------------------------------
+ * Status.
+ * snn_sync_status synchronises the stream, then returns and clears the device error word
+ * (SNN_OK, SNN_EINEXACT) or SNN_ECUDA if the stream reported a CUDA error.
+ * snn_last_error returns the calling thread's last host-side error message ("" if none).
+ * snn_version returns the ABI version (currently 1).
+ * ------------------------------------------------------------------------------------------- */
+SNN_API int snn_sync_status(snn_stream_t s);
+SNN_API const char* snn_last_error(void);
+SNN_API int snn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SNN_H_ */

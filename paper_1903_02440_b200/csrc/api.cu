@@ -1,0 +1,212 @@
+// api.cu -- the C ABI of libsnn (include/snn.h): host-side argument checks, workspace queries,
+// error reporting, then one asynchronous launch sequence per call on the caller's stream.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "common.cuh"
+
+namespace snn {
+
+size_t encode_workspace(int B, int C, int H, int W, int T);
+int encode_launch(const float* x, int B, int C, int H, int W, int T, uint8_t* lat, void* ws, size_t ws_bytes,
+                  cudaStream_t s);
+int expand_launch(const uint8_t* lat, int B, int n, int T, float* wave, cudaStream_t s);
+int validate_launch(const uint8_t* lat, size_t n, int T, int32_t* n_bad, cudaStream_t s);
+size_t conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T);
+int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
+                     int KW, int T, float theta, uint8_t* lat_out, float* v_out, float* pot_out, void* ws,
+                     size_t ws_bytes, cudaStream_t s);
+int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, int PH, int PW, int SH, int SW,
+                int DH, int DW, uint8_t* lat_out, float* v_out, cudaStream_t s);
+int inhibit_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, uint8_t* lat_out, float* v_out,
+                   int16_t* winner_f, cudaStream_t s);
+size_t k_winners_workspace(int B, int F, int H, int W);
+int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, int k, int r, int32_t* winners,
+                     int32_t* count, void* ws, size_t ws_bytes, cudaStream_t s);
+int stdp_launch(float* w, int F, int C, int KH, int KW, const uint8_t* lat_in, int H, int W, int pad,
+                const uint8_t* lat_out, int Ho, int Wo, const int32_t* winners, const int32_t* count, int k,
+                float a_plus, float a_minus, float lb, float ub, int stabilizer, const float* reward, cudaStream_t s);
+int decide_launch(const int32_t* winners, const int32_t* count, int B, int k, int F, int n_classes,
+                  const int32_t* labels, int32_t* decision, float* reward, cudaStream_t s);
+
+static thread_local char t_err[512] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(t_err, sizeof(t_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SNN_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return SNN_OK;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace snn
+
+using namespace snn;
+
+#define REQUIRE(cond, code, ...)                 \
+  do {                                           \
+    if (!(cond)) return set_error(code, __VA_ARGS__); \
+  } while (0)
+
+static inline cudaStream_t S(snn_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+int snn_version(void) { return 1; }
+
+const char* snn_last_error(void) { return t_err; }
+
+int snn_sync_status(snn_stream_t s) {
+  cudaError_t e = cudaStreamSynchronize(S(s));
+  if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_sync_status: %s", cudaGetErrorString(e));
+  int word = 0;
+  int rc = read_clear_error_word(&word);
+  if (rc) return rc;
+  if (word & kErrInexact)
+    return set_error(SNN_EINEXACT, "a weight is outside the exact domain {w : w*2^31 integral, 0 <= w <= 1}");
+  return SNN_OK;
+}
+
+size_t snn_encode_workspace(int B, int C, int H, int W, int T) {
+  if (B < 0 || C < 0 || H < 0 || W < 0 || T < 1 || T > 254) return 0;
+  return encode_workspace(B, C, H, W, T);
+}
+
+int snn_encode(const float* x, int B, int C, int H, int W, int T, uint8_t* lat, void* ws, size_t ws_bytes,
+               snn_stream_t s) {
+  REQUIRE(T >= 1 && T <= 254, SNN_EINVAL, "snn_encode: T=%d outside [1, 254]", T);
+  REQUIRE(B >= 0 && C >= 0 && H >= 0 && W >= 0, SNN_ESHAPE, "snn_encode: negative dimension");
+  REQUIRE(int64_t(C) * H * W < (int64_t(1) << 24), SNN_ESHAPE, "snn_encode: C*H*W >= 2^24");
+  if (int64_t(B) * C * H * W == 0) return SNN_OK;
+  REQUIRE(x && lat, SNN_EINVAL, "snn_encode: NULL tensor");
+  REQUIRE(ws, SNN_EWORKSPACE, "snn_encode: NULL workspace");
+  return encode_launch(x, B, C, H, W, T, lat, ws, ws_bytes, S(s));
+}
+
+int snn_expand(const uint8_t* lat, int B, int n, int T, float* wave, snn_stream_t s) {
+  REQUIRE(T >= 1 && T <= 254, SNN_EINVAL, "snn_expand: T=%d outside [1, 254]", T);
+  REQUIRE(B >= 0 && n >= 0, SNN_ESHAPE, "snn_expand: negative dimension");
+  if (int64_t(B) * n == 0) return SNN_OK;
+  REQUIRE(lat && wave, SNN_EINVAL, "snn_expand: NULL tensor");
+  return expand_launch(lat, B, n, T, wave, S(s));
+}
+
+int snn_validate_lat(const uint8_t* lat, size_t n, int T, int32_t* n_bad, snn_stream_t s) {
+  REQUIRE(T >= 1 && T <= 254, SNN_EINVAL, "snn_validate_lat: T=%d outside [1, 254]", T);
+  REQUIRE(n_bad && (lat || n == 0), SNN_EINVAL, "snn_validate_lat: NULL tensor");
+  return validate_launch(lat, n, T, n_bad, S(s));
+}
+
+static int conv_checks(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta) {
+  REQUIRE(T >= 1 && T <= 254, SNN_EINVAL, "snn_conv_fire: T=%d outside [1, 254]", T);
+  REQUIRE(!isnan(theta), SNN_EINVAL, "snn_conv_fire: theta is NaN");
+  REQUIRE(B >= 0 && C >= 1 && H >= 1 && W >= 1 && F >= 0 && KH >= 1 && KW >= 1 && pad >= 0, SNN_ESHAPE,
+          "snn_conv_fire: bad dimensions");
+  REQUIRE(KH <= H + 2 * pad && KW <= W + 2 * pad, SNN_ESHAPE,
+          "snn_conv_fire: kernel %dx%d larger than padded input %dx%d", KH, KW, H + 2 * pad, W + 2 * pad);
+  REQUIRE(int64_t(C) * KH * KW <= 65534, SNN_ESHAPE, "snn_conv_fire: receptive field C*KH*KW > 65534");
+  REQUIRE(KH < 256 && KW < 256, SNN_ESHAPE, "snn_conv_fire: kernel side >= 256");
+  return SNN_OK;
+}
+
+size_t snn_conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T) {
+  if (conv_checks(B, C, H, W, pad, F, KH, KW, T, 0.0f)) return 0;
+  return conv_fire_workspace(B, C, H, W, pad, F, KH, KW, T);
+}
+
+int snn_conv_fire(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH, int KW,
+                  int T, float theta, uint8_t* lat_out, float* v_out, float* pot_out, void* ws, size_t ws_bytes,
+                  snn_stream_t s) {
+  int rc = conv_checks(B, C, H, W, pad, F, KH, KW, T, theta);
+  if (rc) return rc;
+  if (B == 0 || F == 0) return SNN_OK;
+  REQUIRE(lat_in && w && lat_out && v_out, SNN_EINVAL, "snn_conv_fire: NULL tensor");
+  REQUIRE(ws, SNN_EWORKSPACE, "snn_conv_fire: NULL workspace");
+  return conv_fire_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, theta, lat_out, v_out, pot_out, ws, ws_bytes,
+                          S(s));
+}
+
+int snn_pool(const uint8_t* lat, const float* v, int B, int F, int H, int W, int PH, int PW, int SH, int SW, int DH,
+             int DW, uint8_t* lat_out, float* v_out, snn_stream_t s) {
+  REQUIRE(B >= 0 && F >= 0 && H >= 1 && W >= 1, SNN_ESHAPE, "snn_pool: bad dimensions");
+  REQUIRE(PH >= 1 && PW >= 1 && SH >= 1 && SW >= 1 && DH >= 0 && DW >= 0, SNN_EINVAL, "snn_pool: bad window");
+  REQUIRE(PH <= H + 2 * DH && PW <= W + 2 * DW, SNN_ESHAPE, "snn_pool: window larger than padded input");
+  REQUIRE(DH < PH && DW < PW, SNN_EINVAL, "snn_pool: padding must be smaller than the window");
+  if (int64_t(B) * F == 0) return SNN_OK;
+  REQUIRE(lat && lat_out, SNN_EINVAL, "snn_pool: NULL tensor");
+  REQUIRE(!v_out || v, SNN_EINVAL, "snn_pool: v_out without v");
+  return pool_launch(lat, v, B, F, H, W, PH, PW, SH, SW, DH, DW, lat_out, v_out, S(s));
+}
+
+int snn_inhibit(const uint8_t* lat, const float* v, int B, int F, int H, int W, uint8_t* lat_out, float* v_out,
+                int16_t* winner_f, snn_stream_t s) {
+  REQUIRE(B >= 0 && F >= 0 && H >= 0 && W >= 0, SNN_ESHAPE, "snn_inhibit: bad dimensions");
+  REQUIRE(F <= 32767, SNN_ESHAPE, "snn_inhibit: F > 32767 (int16 winner map)");
+  if (int64_t(B) * H * W == 0) return SNN_OK;
+  REQUIRE(lat && v && lat_out && v_out, SNN_EINVAL, "snn_inhibit: NULL tensor");
+  return inhibit_launch(lat, v, B, F, H, W, lat_out, v_out, winner_f, S(s));
+}
+
+size_t snn_k_winners_workspace(int B, int F, int H, int W) {
+  if (B < 0 || F < 0 || H < 0 || W < 0) return 0;
+  return k_winners_workspace(B, F, H, W);
+}
+
+int snn_k_winners(const uint8_t* lat, const float* v, int B, int F, int H, int W, int k, int r, int32_t* winners,
+                  int32_t* count, void* ws, size_t ws_bytes, snn_stream_t s) {
+  REQUIRE(k >= 1 && k <= 256, SNN_EINVAL, "snn_k_winners: k=%d outside [1, 256]", k);
+  REQUIRE(r >= 0, SNN_EINVAL, "snn_k_winners: r < 0");
+  REQUIRE(B >= 0 && F >= 0 && H >= 0 && W >= 0, SNN_ESHAPE, "snn_k_winners: bad dimensions");
+  REQUIRE(int64_t(F) * H * W <= (int64_t(1) << 24), SNN_ESHAPE, "snn_k_winners: F*H*W > 2^24");
+  if (B == 0) return SNN_OK;
+  REQUIRE(winners && count && (lat && v || int64_t(F) * H * W == 0), SNN_EINVAL, "snn_k_winners: NULL tensor");
+  REQUIRE(ws, SNN_EWORKSPACE, "snn_k_winners: NULL workspace");
+  return k_winners_launch(lat, v, B, F, H, W, k, r, winners, count, ws, ws_bytes, S(s));
+}
+
+int snn_stdp_update(float* w, int F, int C, int KH, int KW, const uint8_t* lat_in, int H, int W, int pad,
+                    const uint8_t* lat_out, int Ho, int Wo, const int32_t* winners, const int32_t* count, int k,
+                    float a_plus, float a_minus, float lb, float ub, int stabilizer, const float* reward,
+                    snn_stream_t s) {
+  REQUIRE(lb < ub, SNN_EINVAL, "snn_stdp_update: LB >= UB");
+  REQUIRE(k >= 0 && F >= 1 && C >= 1 && KH >= 1 && KW >= 1 && H >= 1 && W >= 1 && pad >= 0, SNN_ESHAPE,
+          "snn_stdp_update: bad dimensions");
+  REQUIRE(Ho == H + 2 * pad - KH + 1 && Wo == W + 2 * pad - KW + 1, SNN_ESHAPE,
+          "snn_stdp_update: lat_out %dx%d does not match Eq. 2 (%dx%d)", Ho, Wo, H + 2 * pad - KH + 1,
+          W + 2 * pad - KW + 1);
+  REQUIRE(!isnan(a_plus) && !isnan(a_minus), SNN_EINVAL, "snn_stdp_update: NaN rate");
+  if (k == 0) return SNN_OK;
+  REQUIRE(w && lat_in && lat_out && winners && count, SNN_EINVAL, "snn_stdp_update: NULL tensor");
+  return stdp_launch(w, F, C, KH, KW, lat_in, H, W, pad, lat_out, Ho, Wo, winners, count, k, a_plus, a_minus, lb, ub,
+                     stabilizer, reward, S(s));
+}
+
+int snn_decide(const int32_t* winners, const int32_t* count, int B, int k, int F, int n_classes,
+               const int32_t* labels, int32_t* decision, float* reward, snn_stream_t s) {
+  REQUIRE(B >= 0 && k >= 1 && n_classes >= 1 && F >= n_classes && F % n_classes == 0, SNN_EINVAL,
+          "snn_decide: need F divisible by n_classes");
+  if (B == 0) return SNN_OK;
+  REQUIRE(winners && count && (decision || reward), SNN_EINVAL, "snn_decide: NULL tensor");
+  return decide_launch(winners, count, B, k, F, n_classes, labels, decision, reward, S(s));
+}
+
+}  // extern "C"

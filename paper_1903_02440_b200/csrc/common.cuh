@@ -1,0 +1,51 @@
+// common.cuh -- shared device helpers of libsnn (sm_100a).  Product code; never includes oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/snn.h"
+
+namespace snn {
+
+constexpr uint8_t kNoSpike = SNN_NO_SPIKE;
+
+// Device error word (bit 0 = inexact weight), defined in conv_fire.cu (the only device writer);
+// read and cleared by snn_sync_status() through read_clear_error_word().
+constexpr int kErrInexact = 1;
+int read_clear_error_word(int* word);
+
+// Host-side error reporting (thread-local message), defined in api.cu.
+int set_error(int code, const char* fmt, ...);
+int check_launch(const char* what);
+int num_sms();  // multiprocessor count of the current device (cached)
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Total-order key of a float (ascending order of value), then complemented by callers that want
+// descending order.  v >= 0 for every potential this library produces.
+__device__ __forceinline__ uint32_t ordered_bits(float v) {
+  uint32_t b = __float_as_uint(v);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// Candidate key used by pooling ties, inhibition and k-WTA (R13/R14):
+// ascending key = (lat ascending, v descending, idx ascending); idx < 2^24.
+__device__ __forceinline__ uint64_t wta_key(uint8_t lat, float v, uint32_t idx) {
+  return (uint64_t(lat) << 56) | (uint64_t(~ordered_bits(v)) << 24) | uint64_t(idx & 0xFFFFFFu);
+}
+
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t y = __shfl_xor_sync(0xffffffffu, x, o);
+    x = y < x ? y : x;
+  }
+  return x;
+}
+
+// Exact fixed-point potential (units of 2^-31) -> fp32, round to nearest (N1).
+__device__ __forceinline__ float fixed_to_float(int64_t acc) {
+  return __ll2float_rn(acc) * 4.656612873077392578125e-10f;  // 2^-31, exact scaling
+}
+
+}  // namespace snn

@@ -1,0 +1,325 @@
+// encode.cu -- a1: intensity -> latency rank-order encoding (R1/R2, K1).
+//
+// Per image, the N positive intensities are ranked by the unique 55-bit key
+//     K = ((0x7FFFFFFF - bits(x)) << 24) | flat_index          (x > 0, flat_index < 2^24)
+// whose ascending order is (value descending, index ascending).  Bin b (b = 1..T-1) starts at rank
+// start_b = b*q + min(b, m).  Instead of sorting, a multi-level MSB radix SELECT finds, for every
+// cut b, the key prefix of the element of rank start_b (levels of 12/12/12/12/7 bits; a cut stops
+// as soon as its digit bucket holds a single element).  Then every element's latency is the number
+// of cuts whose prefix it reaches: lat = #{b : (K >> shift_b) >= prefix_b}.  HBM traffic is one read
+// of x per level (L2-resident for a group of images) plus one write of lat.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace snn {
+
+constexpr int kEncLevels = 5;
+constexpr int kEncBins = 4096;
+__constant__ int c_enc_bits[kEncLevels] = {12, 12, 12, 12, 7};
+__constant__ int c_enc_shift[kEncLevels] = {43, 31, 19, 7, 0};  // prefix after level L = K >> shift[L]
+constexpr int kEncThreads = 256;
+constexpr int kEncPerThread = 16;
+constexpr int kEncChunk = kEncThreads * kEncPerThread;
+
+struct EncodeWS {
+  uint32_t* hist0;      // [G][4096]
+  uint32_t* hist;       // [G][S][4096]   S = max(1, T-1)
+  uint64_t* cut_prefix; // [G][T-1]
+  int32_t* cut_shift;   // [G][T-1]  -1 = empty cut (never passed); >=0 when resolved
+  uint32_t* cut_resid;  // [G][T-1]
+  int32_t* cut_slot;    // [G][T-1]  slot of an unresolved cut, -1 when resolved / empty
+  uint64_t* slot_prefix;// [G][S]
+  int32_t* n_slots;     // [G]
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static size_t encode_ws_layout(int G, int T, EncodeWS* ws, char* base) {
+  int S = T > 1 ? T - 1 : 1, NC = S;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return base ? base + o : nullptr; };
+  EncodeWS w;
+  w.hist0 = (uint32_t*)take(sizeof(uint32_t) * size_t(G) * kEncBins);
+  w.hist = (uint32_t*)take(sizeof(uint32_t) * size_t(G) * S * kEncBins);
+  w.cut_prefix = (uint64_t*)take(sizeof(uint64_t) * size_t(G) * NC);
+  w.cut_shift = (int32_t*)take(sizeof(int32_t) * size_t(G) * NC);
+  w.cut_resid = (uint32_t*)take(sizeof(uint32_t) * size_t(G) * NC);
+  w.cut_slot = (int32_t*)take(sizeof(int32_t) * size_t(G) * NC);
+  w.slot_prefix = (uint64_t*)take(sizeof(uint64_t) * size_t(G) * S);
+  w.n_slots = (int32_t*)take(sizeof(int32_t) * size_t(G));
+  if (ws) *ws = w;
+  return off;
+}
+
+// Group size: whole batch unless the per-image histograms exceed ~256 MB.
+static int encode_group(int B, int T) {
+  size_t per = encode_ws_layout(1, T, nullptr, nullptr);
+  size_t g = (size_t(256) << 20) / (per ? per : 1);
+  if (g < 1) g = 1;
+  return int(g < size_t(B) ? g : size_t(B));
+}
+
+size_t encode_workspace(int B, int C, int H, int W, int T) {
+  (void)C; (void)H; (void)W;
+  if (B <= 0) return 256;
+  return encode_ws_layout(encode_group(B, T), T, nullptr, nullptr);
+}
+
+__device__ __forceinline__ uint64_t enc_key(float x, uint32_t idx) {
+  return (uint64_t(0x7FFFFFFFu - __float_as_uint(x)) << 24) | idx;
+}
+
+// Level 0: histogram of the top 12 bits of every positive key (all images of the group).
+__global__ void __launch_bounds__(kEncThreads) enc_hist0_kernel(const float* __restrict__ x, int64_t n,
+                                                                 EncodeWS ws) {
+  __shared__ uint32_t sh[kEncBins];
+  for (int i = threadIdx.x; i < kEncBins; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int g = blockIdx.y;
+  const float* xg = x + int64_t(g) * n;
+  int64_t base = int64_t(blockIdx.x) * kEncChunk;
+  for (int j = 0; j < kEncPerThread; ++j) {
+    int64_t i = base + int64_t(j) * kEncThreads + threadIdx.x;
+    bool pos = false;
+    uint32_t d = 0;
+    if (i < n) {
+      float v = xg[i];
+      pos = v > 0.0f;
+      if (pos) d = uint32_t(enc_key(v, uint32_t(i)) >> 43);
+    }
+    // warp-aggregated shared atomics: intensities cluster in few bins (e.g. one exponent)
+    unsigned act = __ballot_sync(0xffffffffu, pos);
+    if (pos) {
+      unsigned peers = __match_any_sync(act, d);
+      int leader = __ffs(peers) - 1;
+      if ((threadIdx.x & 31) == leader) atomicAdd(&sh[d], __popc(peers));
+    }
+  }
+  __syncthreads();
+  uint32_t* hg = ws.hist0 + int64_t(g) * kEncBins;
+  for (int i = threadIdx.x; i < kEncBins; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hg[i], sh[i]);
+}
+
+// Levels 1..4: histogram of the next digit for elements whose prefix matches an unresolved cut.
+__global__ void __launch_bounds__(kEncThreads) enc_hist_kernel(const float* __restrict__ x, int64_t n, int T,
+                                                                int level, EncodeWS ws) {
+  const int g = blockIdx.y;
+  const int S = T > 1 ? T - 1 : 1;
+  const int ns = ws.n_slots[g];
+  if (ns == 0) return;
+  __shared__ uint64_t sp[256];
+  for (int i = threadIdx.x; i < ns; i += blockDim.x) sp[i] = ws.slot_prefix[int64_t(g) * S + i];
+  __syncthreads();
+  const int shp = c_enc_shift[level - 1], sh = c_enc_shift[level];
+  const uint64_t mask = (uint64_t(1) << c_enc_bits[level]) - 1;
+  const float* xg = x + int64_t(g) * n;
+  uint32_t* hg = ws.hist + int64_t(g) * S * kEncBins;
+  int64_t base = int64_t(blockIdx.x) * kEncChunk;
+  for (int j = 0; j < kEncPerThread; ++j) {
+    int64_t i = base + int64_t(j) * kEncThreads + threadIdx.x;
+    if (i >= n) break;
+    float v = xg[i];
+    if (!(v > 0.0f)) continue;
+    uint64_t K = enc_key(v, uint32_t(i));
+    uint64_t p = K >> shp;
+    int lo = 0, hi = ns;  // lower_bound
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (sp[mid] < p) lo = mid + 1; else hi = mid;
+    }
+    if (lo < ns && sp[lo] == p) atomicAdd(&hg[int64_t(lo) * kEncBins + ((K >> sh) & mask)], 1u);
+  }
+}
+
+// Per-image selection after level L: locate every unresolved cut's digit, resolve or descend,
+// rebuild the sorted list of distinct prefixes for level L+1 and zero their histograms.
+__global__ void __launch_bounds__(256) enc_select_kernel(int T, int level, EncodeWS ws) {
+  const int g = blockIdx.x;
+  const int S = T > 1 ? T - 1 : 1;
+  const int NC = T - 1;
+  __shared__ uint32_t cum[kEncBins + 1];
+  __shared__ uint32_t wsum[8];
+  __shared__ int s_nslots;
+  uint64_t* cp = ws.cut_prefix + int64_t(g) * S;
+  int32_t* csh = ws.cut_shift + int64_t(g) * S;
+  uint32_t* cr = ws.cut_resid + int64_t(g) * S;
+  int32_t* cs = ws.cut_slot + int64_t(g) * S;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+  int nslots = (level == 0) ? 1 : ws.n_slots[g];
+  for (int s = 0; s < nslots; ++s) {
+    const uint32_t* h = (level == 0) ? ws.hist0 + int64_t(g) * kEncBins
+                                     : ws.hist + (int64_t(g) * S + s) * kEncBins;
+    // block exclusive scan of 4096 bins: 16 consecutive bins per thread
+    uint32_t loc[16], run = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) { loc[j] = h[tid * 16 + j]; run += loc[j]; }
+    uint32_t inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    uint32_t wbase = 0;
+    for (int w = 0; w < wid; ++w) wbase += wsum[w];
+    uint32_t e = wbase + inc - run;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) { cum[tid * 16 + j] = e; e += loc[j]; }
+    if (tid == 255) cum[kEncBins] = e;
+    __syncthreads();
+    if (level == 0) {
+      // initialise the cuts from N = total positives (bins: q + 1 for the first m, then q)
+      uint32_t N = cum[kEncBins];
+      uint32_t q = N / uint32_t(T), m = N % uint32_t(T);
+      for (int b = tid; b < NC; b += blockDim.x) {
+        uint32_t bb = uint32_t(b + 1);
+        uint32_t start = bb * q + (bb < m ? bb : m);
+        cp[b] = 0;
+        if (start >= N) { csh[b] = -1; cs[b] = -1; cr[b] = 0; }
+        else { csh[b] = -2; cs[b] = 0; cr[b] = start; }
+      }
+      __syncthreads();
+    }
+    for (int b = tid; b < NC; b += blockDim.x) {
+      if (cs[b] != s || csh[b] == -1) continue;
+      uint32_t r = cr[b];
+      int lo = 0, hi = kEncBins - 1;  // largest d with cum[d] <= r
+      while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (cum[mid] <= r) lo = mid; else hi = mid - 1;
+      }
+      uint32_t cnt = cum[lo + 1] - cum[lo];
+      uint64_t np = (cp[b] << c_enc_bits[level]) | uint64_t(lo);
+      cp[b] = np;
+      cr[b] = r - cum[lo];
+      if (cnt == 1 || level == kEncLevels - 1) { csh[b] = c_enc_shift[level]; cs[b] = -1; }
+      else cs[b] = -3;  // unresolved, slot assigned below
+    }
+    __syncthreads();
+  }
+  // rebuild slots for the next level: cuts are in rank order, so their prefixes are sorted
+  if (tid == 0) {
+    int n = 0;
+    uint64_t* spg = ws.slot_prefix + int64_t(g) * S;
+    for (int b = 0; b < NC; ++b) {
+      if (cs[b] != -3) continue;
+      if (n == 0 || spg[n - 1] != cp[b]) spg[n++] = cp[b];
+      cs[b] = n - 1;
+    }
+    ws.n_slots[g] = n;
+    s_nslots = n;
+  }
+  __syncthreads();
+  if (level + 1 < kEncLevels) {
+    uint32_t* hg = ws.hist + int64_t(g) * S * kEncBins;
+    for (int64_t i = tid; i < int64_t(s_nslots) * kEncBins; i += blockDim.x) hg[i] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(kEncThreads) enc_assign_kernel(const float* __restrict__ x, int64_t n, int T,
+                                                                  uint8_t* __restrict__ lat, EncodeWS ws) {
+  const int g = blockIdx.y;
+  const int S = T > 1 ? T - 1 : 1;
+  const int NC = T - 1;
+  __shared__ uint64_t sp[256];
+  __shared__ int ssh[256];
+  for (int b = threadIdx.x; b < NC; b += blockDim.x) {
+    sp[b] = ws.cut_prefix[int64_t(g) * S + b];
+    ssh[b] = ws.cut_shift[int64_t(g) * S + b];
+  }
+  __syncthreads();
+  const float* xg = x + int64_t(g) * n;
+  uint8_t* lg = lat + int64_t(g) * n;
+  int64_t base = int64_t(blockIdx.x) * kEncChunk;
+  for (int j = 0; j < kEncPerThread; ++j) {
+    int64_t i = base + int64_t(j) * kEncThreads + threadIdx.x;
+    if (i >= n) break;
+    float v = xg[i];
+    uint8_t out = kNoSpike;
+    if (v > 0.0f) {
+      uint64_t K = enc_key(v, uint32_t(i));
+      int lo = 0, hi = NC;  // number of cuts passed (pass(b) is monotone non-increasing in b)
+      while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        bool pass = ssh[mid] >= 0 && (K >> ssh[mid]) >= sp[mid];
+        if (pass) lo = mid + 1; else hi = mid;
+      }
+      out = uint8_t(lo);
+    }
+    lg[i] = out;
+  }
+}
+
+int encode_launch(const float* x, int B, int C, int H, int W, int T, uint8_t* lat, void* wsp,
+                  size_t ws_bytes, cudaStream_t s) {
+  int64_t n = int64_t(C) * H * W;
+  if (B == 0 || n == 0) return SNN_OK;
+  int G = encode_group(B, T);
+  EncodeWS ws;
+  size_t need = encode_ws_layout(G, T, &ws, (char*)wsp);
+  if (ws_bytes < need) return set_error(SNN_EWORKSPACE, "snn_encode: workspace %zu < %zu bytes", ws_bytes, need);
+  int nchunks = int(ceil_div(n, kEncChunk));
+  for (int g0 = 0; g0 < B; g0 += G) {
+    int gn = B - g0 < G ? B - g0 : G;
+    const float* xg = x + int64_t(g0) * n;
+    if (cudaMemsetAsync(ws.hist0, 0, sizeof(uint32_t) * size_t(gn) * kEncBins, s) != cudaSuccess)
+      return check_launch("snn_encode memset");
+    dim3 grid(nchunks, gn);
+    enc_hist0_kernel<<<grid, kEncThreads, 0, s>>>(xg, n, ws);
+    if (T > 1) {
+      enc_select_kernel<<<gn, 256, 0, s>>>(T, 0, ws);
+      for (int L = 1; L < kEncLevels; ++L) {
+        enc_hist_kernel<<<grid, kEncThreads, 0, s>>>(xg, n, T, L, ws);
+        enc_select_kernel<<<gn, 256, 0, s>>>(T, L, ws);
+      }
+    }
+    enc_assign_kernel<<<grid, kEncThreads, 0, s>>>(xg, n, T, lat + int64_t(g0) * n, ws);
+    int rc = check_launch("snn_encode");
+    if (rc) return rc;
+  }
+  return SNN_OK;
+}
+
+// ------------------------------------------------------------------------------------ expand / validate
+__global__ void expand_kernel(const uint8_t* __restrict__ lat, int64_t n, int T, float* __restrict__ wave) {
+  int b = blockIdx.y;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    uint8_t l = lat[int64_t(b) * n + i];
+    for (int t = 0; t < T; ++t)
+      wave[(int64_t(b) * T + t) * n + i] = (l != kNoSpike && t >= int(l)) ? 1.0f : 0.0f;
+  }
+}
+
+int expand_launch(const uint8_t* lat, int B, int n, int T, float* wave, cudaStream_t s) {
+  if (B == 0 || n == 0) return SNN_OK;
+  int blocks = int(ceil_div(n, 256));
+  if (blocks > 4096) blocks = 4096;
+  expand_kernel<<<dim3(blocks, B), 256, 0, s>>>(lat, n, T, wave);
+  return check_launch("snn_expand");
+}
+
+__global__ void validate_kernel(const uint8_t* __restrict__ lat, size_t n, int T, int32_t* n_bad) {
+  int bad = 0;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    uint8_t l = lat[i];
+    bad += (l != kNoSpike && int(l) >= T);
+  }
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(n_bad, bad);
+}
+
+int validate_launch(const uint8_t* lat, size_t n, int T, int32_t* n_bad, cudaStream_t s) {
+  if (cudaMemsetAsync(n_bad, 0, sizeof(int32_t), s) != cudaSuccess) return check_launch("snn_validate_lat");
+  if (n == 0) return SNN_OK;
+  size_t blocks = (n + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  validate_kernel<<<unsigned(blocks), 256, 0, s>>>(lat, n, T, n_bad);
+  return check_launch("snn_validate_lat");
+}
+
+}  // namespace snn

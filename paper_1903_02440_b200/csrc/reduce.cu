@@ -1,0 +1,244 @@
+// reduce.cu -- a4 pooling, a5 pointwise inhibition, a6 k-WTA, R-STDP decision.
+// All of them order candidates by the packed 64-bit key (lat asc, v desc, flat index asc), so a
+// single unsigned min gives the paper's "earliest spike, then maximum potential" rule (P:117, P:126,
+// P:128) with the DESIGN.md R14 tie-break.  Pooling and inhibition are HBM-bound elementwise
+// reductions (coalesced across the innermost spatial index); k-WTA runs one CTA per image over a
+// per-position best-key map.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace snn {
+
+// ------------------------------------------------------------------------------------- a4 pool
+// Earliest spike in the window; the max v among the window entries that spiked at that time
+// (per-time-step max-pooling of the thresholded potentials read at the pooled spike, R12).
+__global__ void __launch_bounds__(256) pool_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
+                                                   int64_t BF, int H, int W, int PH, int PW, int SH, int SW,
+                                                   int DH, int DW, int Ho, int Wo, uint8_t* __restrict__ lat_out,
+                                                   float* __restrict__ v_out) {
+  const int64_t total = BF * Ho * Wo;
+  for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < total; o += int64_t(gridDim.x) * blockDim.x) {
+    const int ox = int(o % Wo);
+    const int64_t r = o / Wo;
+    const int oy = int(r % Ho);
+    const int64_t bf = r / Ho;
+    const uint8_t* l = lat + bf * H * W;
+    const float* vv = v ? v + bf * H * W : nullptr;
+    int best = kNoSpike;
+    float bv = 0.0f;
+    const int y0 = oy * SH - DH, x0 = ox * SW - DW;
+    for (int py = 0; py < PH; ++py) {
+      const int yy = y0 + py;
+      if (yy < 0 || yy >= H) continue;
+      for (int px = 0; px < PW; ++px) {
+        const int xx = x0 + px;
+        if (xx < 0 || xx >= W) continue;
+        const int li = l[int64_t(yy) * W + xx];
+        if (li == kNoSpike || li > best) continue;
+        const float vi = vv ? vv[int64_t(yy) * W + xx] : 0.0f;
+        if (li < best) { best = li; bv = vi; }
+        else if (vi > bv) bv = vi;
+      }
+    }
+    lat_out[o] = uint8_t(best);
+    if (v_out) v_out[o] = best == kNoSpike ? 0.0f : bv;
+  }
+}
+
+int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, int PH, int PW, int SH, int SW,
+                int DH, int DW, uint8_t* lat_out, float* v_out, cudaStream_t s) {
+  const int Ho = (H + 2 * DH - PH) / SH + 1, Wo = (W + 2 * DW - PW) / SW + 1;
+  const int64_t total = int64_t(B) * F * Ho * Wo;
+  if (total == 0) return SNN_OK;
+  int64_t blocks = ceil_div(total, 256);
+  if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
+  pool_kernel<<<int(blocks), 256, 0, s>>>(lat, v_out ? v : nullptr, int64_t(B) * F, H, W, PH, PW, SH, SW, DH, DW,
+                                          Ho, Wo, lat_out, v_out);
+  return check_launch("snn_pool");
+}
+
+// ------------------------------------------------------------------------------------- a5 inhibit
+__global__ void __launch_bounds__(256) inhibit_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
+                                                      int B, int F, int64_t HW, uint8_t* __restrict__ lat_out,
+                                                      float* __restrict__ v_out, int16_t* __restrict__ winner_f) {
+  const int64_t total = int64_t(B) * HW;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < total; q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = q / HW, p = q - b * HW;
+    const int64_t base = b * F * HW + p;
+    uint64_t best = ~uint64_t(0);
+    for (int f = 0; f < F; ++f) {
+      const uint8_t l = lat[base + int64_t(f) * HW];
+      if (l == kNoSpike) continue;
+      const uint64_t k = wta_key(l, v[base + int64_t(f) * HW], uint32_t(f));
+      best = k < best ? k : best;
+    }
+    const int fw = best == ~uint64_t(0) ? -1 : int(best & 0xFFFFFFu);
+    for (int f = 0; f < F; ++f) {
+      const int64_t i = base + int64_t(f) * HW;
+      const bool keep = f == fw;
+      lat_out[i] = keep ? lat[i] : kNoSpike;
+      v_out[i] = keep ? v[i] : 0.0f;
+    }
+    if (winner_f) winner_f[q] = int16_t(fw);
+  }
+}
+
+int inhibit_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, uint8_t* lat_out, float* v_out,
+                   int16_t* winner_f, cudaStream_t s) {
+  const int64_t HW = int64_t(H) * W, total = int64_t(B) * HW;
+  if (total == 0) return SNN_OK;
+  int64_t blocks = ceil_div(total, 256);
+  if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
+  inhibit_kernel<<<int(blocks), 256, 0, s>>>(lat, v, B, F, HW, lat_out, v_out, winner_f);
+  return check_launch("snn_inhibit");
+}
+
+// ------------------------------------------------------------------------------------- a6 k-WTA
+// Stage 1 (all SMs): best key over features for every position -> pos_best[b][p].
+__global__ void __launch_bounds__(256) kwta_posbest_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
+                                                           int B, int F, int64_t HW, uint64_t* __restrict__ pos_best) {
+  const int64_t total = int64_t(B) * HW;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < total; q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = q / HW, p = q - b * HW;
+    const int64_t base = b * F * HW + p;
+    uint64_t best = ~uint64_t(0);
+    for (int f = 0; f < F; ++f) {
+      const uint8_t l = lat[base + int64_t(f) * HW];
+      if (l == kNoSpike) continue;
+      const uint64_t k = wta_key(l, v[base + int64_t(f) * HW], uint32_t(int64_t(f) * HW + p));
+      best = k < best ? k : best;
+    }
+    pos_best[q] = best;
+  }
+}
+
+// Stage 2 (one CTA per image): k rounds of a block argmin over positions.  A position inside the
+// radius of a previous winner is skipped (inhibited in all maps); a position whose best feature has
+// been excluded is re-evaluated over the remaining features and its key written back.
+constexpr int kKwtaThreads = 1024;
+constexpr int kMaxK = 256;
+
+__global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t* __restrict__ lat,
+                                                                   const float* __restrict__ v, int F, int H, int W,
+                                                                   int k, int r, uint64_t* __restrict__ pos_best,
+                                                                   int32_t* __restrict__ winners,
+                                                                   int32_t* __restrict__ count) {
+  extern __shared__ uint32_t fexcl[];  // bitmask of excluded features
+  __shared__ int wy[kMaxK], wx[kMaxK];
+  __shared__ uint64_t red[32];
+  __shared__ int s_count;
+  const int b = blockIdx.x;
+  const int64_t HW = int64_t(H) * W;
+  uint64_t* pb = pos_best + int64_t(b) * HW;
+  const uint8_t* lb = lat + int64_t(b) * F * HW;
+  const float* vb = v + int64_t(b) * F * HW;
+  const int nwords = (F + 31) >> 5;
+  for (int i = threadIdx.x; i < nwords; i += blockDim.x) fexcl[i] = 0;
+  if (threadIdx.x == 0) s_count = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int round = 0; round < k; ++round) {
+    const int nw = s_count;
+    uint64_t best = ~uint64_t(0);
+    for (int64_t p = threadIdx.x; p < HW; p += blockDim.x) {
+      uint64_t key = pb[p];
+      if (key == ~uint64_t(0)) continue;
+      const int y = int(p / W), x = int(p - int64_t(p / W) * W);
+      bool near = false;
+      for (int i = 0; i < nw; ++i) near |= (abs(y - wy[i]) <= r) && (abs(x - wx[i]) <= r);
+      if (near) continue;
+      int f = int((key & 0xFFFFFFu) / uint64_t(HW));
+      if (fexcl[f >> 5] >> (f & 31) & 1) {  // best feature already won: re-evaluate this position
+        key = ~uint64_t(0);
+        for (int ff = 0; ff < F; ++ff) {
+          if (fexcl[ff >> 5] >> (ff & 31) & 1) continue;
+          const uint8_t l = lb[int64_t(ff) * HW + p];
+          if (l == kNoSpike) continue;
+          const uint64_t kk = wta_key(l, vb[int64_t(ff) * HW + p], uint32_t(int64_t(ff) * HW + p));
+          key = kk < key ? kk : key;
+        }
+        pb[p] = key;
+      }
+      best = key < best ? key : best;
+    }
+    best = warp_min_u64(best);
+    if (lane == 0) red[wid] = best;
+    __syncthreads();
+    if (wid == 0) {
+      uint64_t x = lane < (blockDim.x >> 5) ? red[lane] : ~uint64_t(0);
+      x = warp_min_u64(x);
+      if (lane == 0) {
+        if (x != ~uint64_t(0)) {
+          const int64_t idx = int64_t(x & 0xFFFFFFu);
+          const int f = int(idx / HW);
+          const int64_t p = idx - int64_t(f) * HW;
+          const int y = int(p / W), xx = int(p - int64_t(y) * W);
+          const int c = s_count;
+          winners[(int64_t(b) * k + c) * 3 + 0] = f;
+          winners[(int64_t(b) * k + c) * 3 + 1] = y;
+          winners[(int64_t(b) * k + c) * 3 + 2] = xx;
+          wy[c] = y; wx[c] = xx;
+          fexcl[f >> 5] |= 1u << (f & 31);
+          s_count = c + 1;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_count == round) break;  // no candidate left
+  }
+  for (int i = s_count + threadIdx.x; i < k; i += blockDim.x) {
+    winners[(int64_t(b) * k + i) * 3 + 0] = -1;
+    winners[(int64_t(b) * k + i) * 3 + 1] = -1;
+    winners[(int64_t(b) * k + i) * 3 + 2] = -1;
+  }
+  if (threadIdx.x == 0) count[b] = s_count;
+}
+
+size_t k_winners_workspace(int B, int F, int H, int W) {
+  (void)F;
+  return size_t(B) * H * W * sizeof(uint64_t) + 256;
+}
+
+int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, int k, int r, int32_t* winners,
+                     int32_t* count, void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (B == 0) return SNN_OK;
+  const int64_t HW = int64_t(H) * W;
+  if (ws_bytes < size_t(B) * HW * sizeof(uint64_t))
+    return set_error(SNN_EWORKSPACE, "snn_k_winners: workspace too small");
+  uint64_t* pb = reinterpret_cast<uint64_t*>(ws);
+  int64_t total = int64_t(B) * HW;
+  int64_t blocks = ceil_div(total, 256);
+  if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
+  if (blocks < 1) blocks = 1;
+  kwta_posbest_kernel<<<int(blocks), 256, 0, s>>>(lat, v, B, F, HW, pb);
+  const int nwords = (F + 31) >> 5;
+  kwta_rounds_kernel<<<B, kKwtaThreads, nwords * 4, s>>>(lat, v, F, H, W, k, r, pb, winners, count);
+  return check_launch("snn_k_winners");
+}
+
+// ------------------------------------------------------------------------------------- decision
+__global__ void decide_kernel(const int32_t* __restrict__ winners, const int32_t* __restrict__ count, int B, int k,
+                              int F, int n_classes, const int32_t* __restrict__ labels, int32_t* __restrict__ decision,
+                              float* __restrict__ reward) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  int d = -1;
+  float rw = 0.0f;
+  if (count[b] > 0) {
+    d = winners[int64_t(b) * k * 3] / (F / n_classes);
+    if (labels) rw = (d == labels[b]) ? 1.0f : -1.0f;
+  }
+  if (decision) decision[b] = d;
+  if (reward) reward[b] = rw;
+}
+
+int decide_launch(const int32_t* winners, const int32_t* count, int B, int k, int F, int n_classes,
+                  const int32_t* labels, int32_t* decision, float* reward, cudaStream_t s) {
+  if (B == 0) return SNN_OK;
+  decide_kernel<<<int(ceil_div(B, 256)), 256, 0, s>>>(winners, count, B, k, F, n_classes, labels, decision, reward);
+  return check_launch("snn_decide");
+}
+
+}  // namespace snn

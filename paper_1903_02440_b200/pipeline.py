@@ -1,0 +1,166 @@
+"""Config-level compositions of the libsnn calls (the paper's forward / training passes).
+
+Each runner owns its device buffers (allocated once with torch), then issues the C-ABI calls of one
+step asynchronously on the current stream.  No arithmetic happens here; every step is a libsnn
+kernel.  Sequential plasticity (C1/C3/C4) keeps each image's update on the device: the R-STDP reward
+is decided by ``snn_decide`` on the GPU, so no host round trip is needed per image.
+"""
+from __future__ import annotations
+
+import math
+from typing import Dict, List, Optional
+
+import numpy as np
+import torch
+
+from . import snn
+
+
+def _dev(a, device, dtype=None):
+    t = torch.as_tensor(np.ascontiguousarray(a)).to(device)
+    return t if dtype is None else t.to(dtype)
+
+
+class Layer:
+    """conv+fire (+ optional pool) with preallocated outputs."""
+
+    def __init__(self, spec, w: torch.Tensor, B: int, C: int, H: int, W: int, T: int, pool_spec=None,
+                 pool_v: bool = True, device="cuda"):
+        self.spec, self.w, self.T = spec, w, T
+        self.B, self.C, self.H, self.W = B, C, H, W
+        self.Ho, self.Wo = snn.conv_out_hw(H, W, spec.KH, spec.KW, spec.pad)
+        F = spec.F
+        self.lat = torch.empty((B, F, self.Ho, self.Wo), dtype=torch.uint8, device=device)
+        self.v = torch.empty((B, F, self.Ho, self.Wo), dtype=torch.float32, device=device)
+        self.ws = torch.empty(snn.conv_fire_workspace(B, C, H, W, spec.pad, F, spec.KH, spec.KW, T),
+                              dtype=torch.uint8, device=device)
+        self.pool_spec = pool_spec
+        if pool_spec is not None:
+            self.PHo, self.PWo = snn.pool_out_hw(self.Ho, self.Wo, pool_spec.PH, pool_spec.PW, pool_spec.SH,
+                                                 pool_spec.SW, pool_spec.DH, pool_spec.DW)
+            self.plat = torch.empty((B, F, self.PHo, self.PWo), dtype=torch.uint8, device=device)
+            self.pv = torch.empty((B, F, self.PHo, self.PWo), dtype=torch.float32, device=device) if pool_v else None
+
+    @property
+    def out_lat(self):
+        return self.plat if self.pool_spec is not None else self.lat
+
+    @property
+    def out_v(self):
+        return self.pv if self.pool_spec is not None else self.v
+
+    def __call__(self, lat_in: torch.Tensor, w: Optional[torch.Tensor] = None):
+        s = self.spec
+        snn.conv_fire(lat_in, self.w if w is None else w, s.pad, self.T, s.theta, lat_out=self.lat, v_out=self.v,
+                      ws=self.ws)
+        if self.pool_spec is not None:
+            p = self.pool_spec
+            snn.pool(self.lat, self.v if self.pv is not None else None, (p.PH, p.PW), (p.SH, p.SW), (p.DH, p.DW),
+                     lat_out=self.plat, v_out=self.pv)
+        return self.out_lat
+
+
+class C2Net:
+    """3-layer DCSNN inference (configs[1]): encode -> [conv+fire -> pool] x 2 -> conv (theta = inf)
+    -> 1 winner (global max potential) -> class = f // (F / 10)."""
+
+    def __init__(self, wl, B: int, device="cuda"):
+        self.wl, self.B, self.T = wl, B, wl.T
+        _, C, H, W = wl.X.shape
+        self.ws_enc = torch.empty(snn.encode_workspace(B, C, H, W, wl.T), dtype=torch.uint8, device=device)
+        self.lat0 = torch.empty((B, C, H, W), dtype=torch.uint8, device=device)
+        self.w = [_dev(w, device) for w in wl.weights]
+        s1, s2, s3 = wl.convs
+        self.l1 = Layer(s1, self.w[0], B, C, H, W, wl.T, wl.pools[0], pool_v=False, device=device)
+        self.l2 = Layer(s2, self.w[1], B, s1.F, self.l1.PHo, self.l1.PWo, wl.T, wl.pools[1], pool_v=False,
+                        device=device)
+        self.l3 = Layer(s3, self.w[2], B, s2.F, self.l2.PHo, self.l2.PWo, wl.T, None, device=device)
+        self.winners = torch.empty((B, 1, 3), dtype=torch.int32, device=device)
+        self.count = torch.empty((B,), dtype=torch.int32, device=device)
+        n = int(snn.lib().snn_k_winners_workspace(B, s3.F, self.l3.Ho, self.l3.Wo))
+        self.ws_kw = torch.empty(n, dtype=torch.uint8, device=device)
+        self.decision = torch.empty((B,), dtype=torch.int32, device=device)
+        self.reward = torch.empty((B,), dtype=torch.float32, device=device)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        snn.encode(x, self.T, out=self.lat0, ws=self.ws_enc)
+        a = self.l1(self.lat0)
+        a = self.l2(a)
+        self.l3(a)
+        snn.k_winners(self.l3.lat, self.l3.v, 1, 0, winners=self.winners, count=self.count, ws=self.ws_kw)
+        snn.decide(self.winners, self.count, self.wl.convs[2].F, self.wl.extra["n_classes"], None,
+                   decision=self.decision, reward=self.reward)
+        return self.decision
+
+
+class C5Net:
+    """Throughput stress (configs[4]): encode -> conv+fire -> pool 2/2 -> inhibit -> kWTA(k16, r4)."""
+
+    def __init__(self, wl, B: int, device="cuda"):
+        self.wl, self.B, self.T = wl, B, wl.T
+        _, C, H, W = wl.X.shape
+        self.ws_enc = torch.empty(snn.encode_workspace(B, C, H, W, wl.T), dtype=torch.uint8, device=device)
+        self.lat0 = torch.empty((B, C, H, W), dtype=torch.uint8, device=device)
+        self.w = _dev(wl.weights[0], device)
+        self.l1 = Layer(wl.convs[0], self.w, B, C, H, W, wl.T, wl.pools[0], pool_v=True, device=device)
+        F, Hp, Wp = wl.convs[0].F, self.l1.PHo, self.l1.PWo
+        self.ilat = torch.empty((B, F, Hp, Wp), dtype=torch.uint8, device=device)
+        self.iv = torch.empty((B, F, Hp, Wp), dtype=torch.float32, device=device)
+        self.wf = torch.empty((B, Hp, Wp), dtype=torch.int16, device=device)
+        k = wl.extra["k"]
+        self.winners = torch.empty((B, k, 3), dtype=torch.int32, device=device)
+        self.count = torch.empty((B,), dtype=torch.int32, device=device)
+        self.ws_kw = torch.empty(int(snn.lib().snn_k_winners_workspace(B, F, Hp, Wp)), dtype=torch.uint8,
+                                 device=device)
+
+    def forward(self, x: torch.Tensor):
+        snn.encode(x, self.T, out=self.lat0, ws=self.ws_enc)
+        self.l1(self.lat0)
+        snn.inhibit(self.l1.plat, self.l1.pv, lat_out=self.ilat, v_out=self.iv, winner_f=self.wf)
+        snn.k_winners(self.ilat, self.iv, self.wl.extra["k"], self.wl.extra["r"], winners=self.winners,
+                      count=self.count, ws=self.ws_kw)
+        return self.winners, self.count
+
+
+class SeqSTDP:
+    """Sequential per-image plasticity on one conv layer (C1, C3: STDP; C4: R-STDP).
+
+    ``lat_in`` [N, C, H, W] is the layer's (already computed, fixed-weight) input for every image.
+    Per image: conv+fire -> [inhibit] -> kWTA -> [decide] -> STDP, all on the device.
+    """
+
+    def __init__(self, spec, w0: np.ndarray, C: int, H: int, W: int, T: int, k: int, r: int, inhibit: bool,
+                 rates: Dict, n_classes: int = 0, device="cuda"):
+        self.spec, self.T, self.k, self.r, self.inhibit_on = spec, T, k, r, inhibit
+        self.rates, self.n_classes = rates, n_classes
+        self.w = _dev(w0, device).clone()
+        self.layer = Layer(spec, self.w, 1, C, H, W, T, None, device=device)
+        F, Ho, Wo = spec.F, self.layer.Ho, self.layer.Wo
+        self.ilat = torch.empty((1, F, Ho, Wo), dtype=torch.uint8, device=device)
+        self.iv = torch.empty((1, F, Ho, Wo), dtype=torch.float32, device=device)
+        self.wf = torch.empty((1, Ho, Wo), dtype=torch.int16, device=device)
+        self.winners = torch.empty((1, k, 3), dtype=torch.int32, device=device)
+        self.count = torch.empty((1,), dtype=torch.int32, device=device)
+        self.ws_kw = torch.empty(int(snn.lib().snn_k_winners_workspace(1, F, Ho, Wo)), dtype=torch.uint8,
+                                 device=device)
+        self.decision = torch.empty((1,), dtype=torch.int32, device=device)
+        self.reward = torch.ones((1,), dtype=torch.float32, device=device)
+
+    def step(self, lat_in_img: torch.Tensor, label: Optional[torch.Tensor] = None):
+        """lat_in_img [1, C, H, W]; label int32 [1] device tensor (R-STDP) or None (plain STDP)."""
+        self.layer(lat_in_img, self.w)
+        lat, v = self.layer.lat, self.layer.v
+        if self.inhibit_on:
+            snn.inhibit(lat, v, lat_out=self.ilat, v_out=self.iv, winner_f=self.wf)
+            lat_k, v_k = self.ilat, self.iv
+        else:
+            lat_k, v_k = lat, v
+        snn.k_winners(lat_k, v_k, self.k, self.r, winners=self.winners, count=self.count, ws=self.ws_kw)
+        reward = None
+        if label is not None:
+            snn.decide(self.winners, self.count, self.spec.F, self.n_classes, label, decision=self.decision,
+                       reward=self.reward)
+            reward = self.reward
+        R = self.rates
+        snn.stdp_update(self.w, lat_in_img[0], self.spec.pad, lat[0], self.winners[0], self.count, R["a_plus"],
+                        R["a_minus"], R["lb"], R["ub"], R["stabilizer"], reward)

@@ -1,0 +1,273 @@
+"""Thin Python binding of libsnn (include/snn.h): ctypes marshalling of torch CUDA tensors only.
+
+Every step of the spike-wave path runs in the library's sm_100a kernels; this module only checks
+dtypes/devices/contiguity, allocates outputs and workspaces with torch (PyTorch is the device-memory
+and stream plumbing), passes raw pointers, and raises ``SNNError`` on a non-zero return code.  There
+is no CPU fallback: a missing library or a missing GPU raises.
+
+Names follow the C ABI (``snn_<name>`` -> ``<name>``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import threading
+from typing import Optional, Tuple
+
+import torch
+
+NO_SPIKE = 255
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsnn.so")
+_lib = None
+_lock = threading.Lock()
+
+SNN_OK, SNN_EINVAL, SNN_ESHAPE, SNN_ECUDA, SNN_EINEXACT, SNN_EWORKSPACE = 0, -1, -2, -3, -4, -5
+
+
+class SNNError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"libsnn error {code}: {msg}")
+        self.code = code
+
+
+def lib() -> C.CDLL:
+    """Load libsnn.so (raises if it has not been built: run __graft_entry__.build())."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(_LIB_PATH):
+                raise RuntimeError(f"{_LIB_PATH} missing: build it with `python -m paper_1903_02440_b200.build`")
+            L = C.CDLL(_LIB_PATH)
+            p, i32, f32, sz = C.c_void_p, C.c_int, C.c_float, C.c_size_t
+            sigs = {
+                "snn_version": (i32, []),
+                "snn_last_error": (C.c_char_p, []),
+                "snn_sync_status": (i32, [p]),
+                "snn_encode_workspace": (sz, [i32, i32, i32, i32, i32]),
+                "snn_encode": (i32, [p, i32, i32, i32, i32, i32, p, p, sz, p]),
+                "snn_expand": (i32, [p, i32, i32, i32, p, p]),
+                "snn_validate_lat": (i32, [p, sz, i32, p, p]),
+                "snn_conv_fire_workspace": (sz, [i32] * 9),
+                "snn_conv_fire": (i32, [p, i32, i32, i32, i32, i32, p, i32, i32, i32, i32, f32, p, p, p, p, sz, p]),
+                "snn_pool": (i32, [p, p, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, p, p, p]),
+                "snn_inhibit": (i32, [p, p, i32, i32, i32, i32, p, p, p, p]),
+                "snn_k_winners_workspace": (sz, [i32, i32, i32, i32]),
+                "snn_k_winners": (i32, [p, p, i32, i32, i32, i32, i32, i32, p, p, p, sz, p]),
+                "snn_stdp_update": (i32, [p, i32, i32, i32, i32, p, i32, i32, i32, p, i32, i32, p, p, i32,
+                                          f32, f32, f32, f32, i32, p, p]),
+                "snn_decide": (i32, [p, p, i32, i32, i32, i32, p, p, p, p]),
+            }
+            for name, (res, args) in sigs.items():
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return ["snn_version", "snn_last_error", "snn_sync_status", "snn_encode_workspace", "snn_encode",
+            "snn_expand", "snn_validate_lat", "snn_conv_fire_workspace", "snn_conv_fire", "snn_pool",
+            "snn_inhibit", "snn_k_winners_workspace", "snn_k_winners", "snn_stdp_update", "snn_decide"]
+
+
+def _check(rc: int):
+    if rc != SNN_OK:
+        raise SNNError(rc, lib().snn_last_error().decode())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream: Optional[torch.cuda.Stream]):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _req(t: torch.Tensor, dtype, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path exists)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+class _Workspace:
+    """Grow-only device scratch buffers, one per (device, tag)."""
+
+    def __init__(self):
+        self._bufs = {}
+
+    def get(self, nbytes: int, device, tag: str = "") -> torch.Tensor:
+        key = (str(device), tag)
+        b = self._bufs.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+            self._bufs[key] = b
+        return b
+
+
+_ws = _Workspace()
+
+
+# ------------------------------------------------------------------------------------------ a1
+def encode_workspace(B, C_, H, W, T) -> int:
+    return int(lib().snn_encode_workspace(B, C_, H, W, T))
+
+
+def encode(x: torch.Tensor, T: int, out: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None,
+           stream=None) -> torch.Tensor:
+    """x float32 [B, C, H, W] -> lat uint8 [B, C, H, W] (snn_encode)."""
+    _req(x, torch.float32, "x")
+    B, C_, H, W = x.shape
+    lat = out if out is not None else torch.empty(x.shape, dtype=torch.uint8, device=x.device)
+    _req(lat, torch.uint8, "lat")
+    n = encode_workspace(B, C_, H, W, T)
+    buf = ws if ws is not None else _ws.get(n, x.device, "encode")
+    _check(lib().snn_encode(_ptr(x), B, C_, H, W, T, _ptr(lat), _ptr(buf), buf.numel(), _stream(stream)))
+    return lat
+
+
+def expand(lat: torch.Tensor, T: int, stream=None) -> torch.Tensor:
+    """lat uint8 [B, ...] -> wave float32 [B, T, ...] (Eq. 1)."""
+    _req(lat, torch.uint8, "lat")
+    B = lat.shape[0]
+    n = lat[0].numel() if B else 0
+    wave = torch.empty((B, T) + tuple(lat.shape[1:]), dtype=torch.float32, device=lat.device)
+    _check(lib().snn_expand(_ptr(lat), B, n, T, _ptr(wave), _stream(stream)))
+    return wave
+
+
+def validate_lat(lat: torch.Tensor, T: int, stream=None) -> int:
+    _req(lat, torch.uint8, "lat")
+    nb = torch.zeros(1, dtype=torch.int32, device=lat.device)
+    _check(lib().snn_validate_lat(_ptr(lat), lat.numel(), T, _ptr(nb), _stream(stream)))
+    return int(nb.item())
+
+
+# ------------------------------------------------------------------------------------------ a2/a3
+def conv_out_hw(H, W, KH, KW, pad):
+    return H + 2 * pad - KH + 1, W + 2 * pad - KW + 1
+
+
+def conv_fire_workspace(B, C_, H, W, pad, F, KH, KW, T) -> int:
+    return int(lib().snn_conv_fire_workspace(B, C_, H, W, pad, F, KH, KW, T))
+
+
+def conv_fire(lat_in: torch.Tensor, w: torch.Tensor, pad: int, T: int, theta: float, want_pot: bool = False,
+              lat_out=None, v_out=None, ws=None, stream=None):
+    """lat_in uint8 [B, C, H, W], w float32 [F, C, KH, KW] -> (lat uint8, v float32) [B, F, Ho, Wo]
+    (+ pot float32 [B, T, F, Ho, Wo] when want_pot)."""
+    _req(lat_in, torch.uint8, "lat_in")
+    _req(w, torch.float32, "w")
+    B, C_, H, W = lat_in.shape
+    F, Cw, KH, KW = w.shape
+    if Cw != C_:
+        raise ValueError("channel mismatch between lat_in and w")
+    Ho, Wo = conv_out_hw(H, W, KH, KW, pad)
+    Ho, Wo = max(Ho, 0), max(Wo, 0)          # invalid shapes are rejected by the library (SNN_ESHAPE)
+    dev = lat_in.device
+    lat = lat_out if lat_out is not None else torch.empty((B, F, Ho, Wo), dtype=torch.uint8, device=dev)
+    v = v_out if v_out is not None else torch.empty((B, F, Ho, Wo), dtype=torch.float32, device=dev)
+    pot = torch.empty((B, T, F, Ho, Wo), dtype=torch.float32, device=dev) if want_pot else None
+    n = conv_fire_workspace(B, C_, H, W, pad, F, KH, KW, T)
+    buf = ws if ws is not None else _ws.get(n, dev, "conv")
+    _check(lib().snn_conv_fire(_ptr(lat_in), B, C_, H, W, pad, _ptr(w), F, KH, KW, T, float(theta),
+                               _ptr(lat), _ptr(v), _ptr(pot), _ptr(buf), buf.numel(), _stream(stream)))
+    return (lat, v, pot) if want_pot else (lat, v)
+
+
+# ------------------------------------------------------------------------------------------ a4
+def pool_out_hw(H, W, PH, PW, SH, SW, DH=0, DW=0):
+    return (H + 2 * DH - PH) // SH + 1, (W + 2 * DW - PW) // SW + 1
+
+
+def pool(lat: torch.Tensor, v: Optional[torch.Tensor], window, stride=None, padding=(0, 0),
+         lat_out=None, v_out=None, stream=None):
+    _req(lat, torch.uint8, "lat")
+    if v is not None:
+        _req(v, torch.float32, "v")
+    PH, PW = (window, window) if isinstance(window, int) else window
+    SH, SW = (PH, PW) if stride is None else ((stride, stride) if isinstance(stride, int) else stride)
+    DH, DW = (padding, padding) if isinstance(padding, int) else padding
+    B, F, H, W = lat.shape
+    Ho, Wo = (max(d, 0) for d in pool_out_hw(H, W, PH, PW, SH, SW, DH, DW))
+    lo = lat_out if lat_out is not None else torch.empty((B, F, Ho, Wo), dtype=torch.uint8, device=lat.device)
+    vo = None
+    if v is not None:
+        vo = v_out if v_out is not None else torch.empty((B, F, Ho, Wo), dtype=torch.float32, device=lat.device)
+    _check(lib().snn_pool(_ptr(lat), _ptr(v), B, F, H, W, PH, PW, SH, SW, DH, DW, _ptr(lo), _ptr(vo),
+                          _stream(stream)))
+    return lo, vo
+
+
+# ------------------------------------------------------------------------------------------ a5
+def inhibit(lat: torch.Tensor, v: torch.Tensor, lat_out=None, v_out=None, winner_f=None, stream=None):
+    _req(lat, torch.uint8, "lat")
+    _req(v, torch.float32, "v")
+    B, F, H, W = lat.shape
+    lo = lat_out if lat_out is not None else torch.empty_like(lat)
+    vo = v_out if v_out is not None else torch.empty_like(v)
+    wf = winner_f if winner_f is not None else torch.empty((B, H, W), dtype=torch.int16, device=lat.device)
+    _check(lib().snn_inhibit(_ptr(lat), _ptr(v), B, F, H, W, _ptr(lo), _ptr(vo), _ptr(wf), _stream(stream)))
+    return lo, vo, wf
+
+
+# ------------------------------------------------------------------------------------------ a6
+def k_winners(lat: torch.Tensor, v: torch.Tensor, k: int, r: int, winners=None, count=None, ws=None, stream=None):
+    _req(lat, torch.uint8, "lat")
+    _req(v, torch.float32, "v")
+    B, F, H, W = lat.shape
+    win = winners if winners is not None else torch.empty((B, k, 3), dtype=torch.int32, device=lat.device)
+    cnt = count if count is not None else torch.empty((B,), dtype=torch.int32, device=lat.device)
+    n = int(lib().snn_k_winners_workspace(B, F, H, W))
+    buf = ws if ws is not None else _ws.get(n, lat.device, "kwta")
+    _check(lib().snn_k_winners(_ptr(lat), _ptr(v), B, F, H, W, k, r, _ptr(win), _ptr(cnt), _ptr(buf), buf.numel(),
+                               _stream(stream)))
+    return win, cnt
+
+
+# ------------------------------------------------------------------------------------------ a7
+def stdp_update(w: torch.Tensor, lat_in: torch.Tensor, pad: int, lat_out: torch.Tensor, winners: torch.Tensor,
+                count: torch.Tensor, a_plus: float, a_minus: float, lb: float = 0.0, ub: float = 1.0,
+                stabilizer: int = 1, reward: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """In-place update of w [F, C, KH, KW] for one image: lat_in [C, H, W], lat_out [F, Ho, Wo],
+    winners [k, 3], count [1] (device), reward float32 [1] (device, +1 / -1 / 0) or None (= +1)."""
+    _req(w, torch.float32, "w")
+    _req(lat_in, torch.uint8, "lat_in")
+    _req(lat_out, torch.uint8, "lat_out")
+    _req(winners, torch.int32, "winners")
+    _req(count, torch.int32, "count")
+    if reward is not None:
+        _req(reward, torch.float32, "reward")
+    F, C_, KH, KW = w.shape
+    _, H, W = lat_in.shape
+    _, Ho, Wo = lat_out.shape
+    k = winners.shape[-2]
+    _check(lib().snn_stdp_update(_ptr(w), F, C_, KH, KW, _ptr(lat_in), H, W, pad, _ptr(lat_out), Ho, Wo,
+                                 _ptr(winners), _ptr(count), k, float(a_plus), float(a_minus), float(lb), float(ub),
+                                 int(stabilizer), _ptr(reward), _stream(stream)))
+    return w
+
+
+def decide(winners: torch.Tensor, count: torch.Tensor, F: int, n_classes: int, labels: Optional[torch.Tensor] = None,
+           decision=None, reward=None, stream=None):
+    _req(winners, torch.int32, "winners")
+    _req(count, torch.int32, "count")
+    B, k, _ = winners.shape
+    d = decision if decision is not None else torch.empty((B,), dtype=torch.int32, device=winners.device)
+    rw = reward if reward is not None else torch.empty((B,), dtype=torch.float32, device=winners.device)
+    _check(lib().snn_decide(_ptr(winners), _ptr(count), B, k, F, n_classes, _ptr(labels), _ptr(d), _ptr(rw),
+                            _stream(stream)))
+    return d, rw
+
+
+def sync_status(stream=None) -> None:
+    _check(lib().snn_sync_status(_stream(stream)))
+
+
+def version() -> int:
+    return int(lib().snn_version())

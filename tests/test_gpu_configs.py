@@ -1,0 +1,176 @@
+"""GPU parity at the five BASELINE.json configs (C1..C5) through the C ABI vs the oracle flows.
+
+Bit-exact comparison of every intermediate (latencies, v, pooled waves, inhibition maps, winners,
+weights).  The north_star tolerances (1e-5 rel + 1e-6 abs for potentials, 1e-6 abs for weights, a
+near-threshold allowance < 0.01 %) are therefore met with margin zero; near-threshold neurons
+(|P_oracle - theta| <= 1e-5 at some t) are still counted and reported.  C5 at its full size is
+checked on sampled neurons (the oracle computes them one by one) plus invariants; two images are
+compared in full.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+NS = 255
+
+
+@pytest.fixture(scope="module")
+def G():
+    assert torch.cuda.is_available()
+    from paper_1903_02440_b200 import build, snn
+    build.build()
+    return snn
+
+
+def cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def test_c1_full(G, orc):
+    from oracle import flows
+    from paper_1903_02440_b200 import pipeline
+    wl = synth.C1()
+    ref = flows.c1(wl)
+    x = cu(wl.X)
+    lat0 = G.encode(x, wl.T)
+    assert np.array_equal(host(lat0), ref["lat0"])
+    seq = pipeline.SeqSTDP(wl.convs[0], wl.weights[0], 2, 28, 28, wl.T, 5, 3, True, wl.extra["stdp"])
+    seq.step(lat0)
+    G.sync_status()
+    assert np.array_equal(host(seq.layer.lat), ref["lat1"])
+    assert np.array_equal(host(seq.layer.v), ref["v1"])
+    assert np.array_equal(host(seq.ilat), ref["inh_lat"])
+    assert np.array_equal(host(seq.wf), ref["winner_f"])
+    assert np.array_equal(host(seq.winners), ref["winners"])
+    assert np.array_equal(host(seq.w), ref["w_new"])
+
+
+def test_c2_parity(G, orc):
+    from oracle import flows
+    from paper_1903_02440_b200 import pipeline
+    n = 1000
+    wl = synth.C2(n=n)
+    ref = flows.c2(wl)
+    net = pipeline.C2Net(wl, n)
+    net.forward(cu(wl.X))
+    G.sync_status()
+    assert np.array_equal(host(net.lat0), ref["lat0"])
+    assert np.array_equal(host(net.l1.lat), ref["l1"]["lat"])
+    assert np.array_equal(host(net.l1.plat), ref["l1"]["pool_lat"])
+    assert np.array_equal(host(net.l2.lat), ref["l2"]["lat"])
+    assert np.array_equal(host(net.l2.v), ref["l2"]["v"])
+    assert np.array_equal(host(net.l2.plat), ref["l2"]["pool_lat"])
+    assert np.array_equal(host(net.l3.lat), ref["l3"]["lat"])
+    assert np.array_equal(host(net.l3.v), ref["l3"]["v"])
+    assert np.array_equal(host(net.winners), ref["winners"])
+    assert np.array_equal(host(net.decision), ref["decision"])
+
+
+@pytest.mark.parametrize("n", [300])
+def test_c3_sequential_stdp(G, orc, n):
+    from oracle import flows
+    from paper_1903_02440_b200 import pipeline
+    wl = synth.C3(n=n)
+    ref = flows.c3(wl, snapshot_every=100)
+    # layer 1 (fixed weights) for all images, then the sequential layer-2 loop
+    x = cu(wl.X)
+    lat0 = G.encode(x, wl.T)
+    l1 = pipeline.Layer(wl.convs[0], cu(wl.weights[0]), n, 6, 28, 28, wl.T, wl.pools[0], pool_v=False)
+    l1(lat0)
+    assert np.array_equal(host(l1.plat), ref["l1_pool_lat"])
+    s = wl.convs[1]
+    seq = pipeline.SeqSTDP(s, wl.weights[1], 30, 14, 14, wl.T, wl.extra["k"], wl.extra["r"], True, wl.extra["stdp"])
+    snaps = []
+    for b in range(n):
+        seq.step(l1.plat[b:b + 1])
+        assert np.array_equal(host(seq.winners[0]), ref["winners"][b]), f"image {b}"
+        if (b + 1) % 100 == 0:
+            snaps.append(host(seq.w).copy())
+    G.sync_status()
+    for a, r in zip(snaps, ref["snapshots"]):
+        assert np.array_equal(a, r)
+    assert np.array_equal(host(seq.w), ref["w2"])
+
+
+def test_c4_rstdp(G, orc):
+    from oracle import flows
+    from paper_1903_02440_b200 import pipeline
+    n = 40
+    wl = synth.C4(n=n)
+    ref = flows.c4(wl)
+    x = cu(wl.X)
+    lat0 = G.encode(x, wl.T)
+    l1 = pipeline.Layer(wl.convs[0], cu(wl.weights[0]), n, 4, 160, 250, wl.T, wl.pools[0], pool_v=False)
+    l1(lat0)
+    assert np.array_equal(host(l1.plat), ref["l1_pool_lat"])
+    s = wl.convs[1]
+    seq = pipeline.SeqSTDP(s, wl.weights[1], 20, 25, 40, wl.T, 1, 0, False, wl.extra["stdp"], n_classes=2)
+    labels = cu(wl.extra["labels"][:n].astype(np.int32))
+    dec = []
+    for b in range(n):
+        seq.step(l1.plat[b:b + 1], labels[b:b + 1])
+        dec.append(int(seq.decision.item()))
+    G.sync_status()
+    assert dec == ref["decision"].tolist()
+    assert np.array_equal(host(seq.w), ref["w2"])
+
+
+def test_c5_two_images_full(G, orc):
+    from oracle import flows
+    from paper_1903_02440_b200 import pipeline
+    wl = synth.C5(n=2)
+    ref = flows.c5(wl)
+    net = pipeline.C5Net(wl, 2)
+    net.forward(cu(wl.X))
+    G.sync_status()
+    assert np.array_equal(host(net.lat0), ref["lat0"])
+    assert np.array_equal(host(net.l1.lat), ref["l1"]["lat"])
+    assert np.array_equal(host(net.l1.v), ref["l1"]["v"])
+    assert np.array_equal(host(net.l1.plat), ref["l1"]["pool_lat"])
+    assert np.array_equal(host(net.l1.pv), ref["l1"]["pool_v"])
+    assert np.array_equal(host(net.ilat), ref["inh_lat"])
+    assert np.array_equal(host(net.winners), ref["winners"])
+
+
+def test_c5_full_batch_sampled(G, orc):
+    """All 64 images in the bench's launch configuration; 20k sampled neurons vs the oracle (one by
+    one), encode of every image in full, and the invariants at full size."""
+    from paper_1903_02440_b200 import pipeline
+    wl = synth.C5()
+    net = pipeline.C5Net(wl, 64)
+    net.forward(cu(wl.X))
+    G.sync_status()
+    lat0 = host(net.lat0)
+    assert np.array_equal(lat0, orc.encode(wl.X, wl.T))
+    lat, v = host(net.l1.lat), host(net.l1.v)
+    rng = np.random.default_rng(0)
+    idx = rng.choice(lat.size, 20000, replace=False)
+    s = wl.convs[0]
+    ol, ov, P = orc.conv_fire_sample(lat0, wl.weights[0], s.pad, wl.T, s.theta, idx, want_p=True)
+    near = np.any(np.abs(P - s.theta) <= 1e-5, axis=1)
+    mism = (lat.ravel()[idx] != ol) | (v.ravel()[idx] != ov)
+    assert int((mism & ~near).sum()) == 0
+    assert near.mean() < 1e-4
+    # invariants: <= 1 feature per position after inhibition; winners distinct, > r apart
+    il = host(net.ilat)
+    assert np.all((il != NS).sum(axis=1) <= 1)
+    win, cnt = host(net.winners), host(net.count)
+    for b in range(64):
+        ws = win[b, :cnt[b]]
+        assert len(set(ws[:, 0].tolist())) == len(ws)
+        for i in range(len(ws)):
+            for j in range(i):
+                assert max(abs(ws[i, 1] - ws[j, 1]), abs(ws[i, 2] - ws[j, 2])) > wl.extra["r"]
+    # pooled waves of two images in full
+    for b in (5, 63):
+        pl, pv = orc.pool(lat[b:b + 1], v[b:b + 1], 2, 2, 2, 2, 0, 0, wl.T)
+        assert np.array_equal(host(net.l1.plat[b:b + 1]), pl) and np.array_equal(host(net.l1.pv[b:b + 1]), pv)

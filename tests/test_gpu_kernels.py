@@ -1,0 +1,227 @@
+"""GPU parity: every libsnn kernel (through the C ABI) vs the CPU oracle on seeded inputs.
+
+Sizes span several tiles / chunks with ragged tails; edge cases: empty inputs, T = 1, T = 254,
+N < T, all-equal intensities, negative/NaN intensities, pad > 0, window != stride, k > #candidates,
+r = 0, F not a multiple of 32, theta = +inf, theta < 0, the dense theta = inf path.
+Integer / index outputs must be bit-exact; fp32 potentials are exact too (N1), so v and
+pot are compared bit-exactly as well.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+NS = 255
+
+
+@pytest.fixture(scope="module")
+def G():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_1903_02440_b200 import build, snn
+    build.build()
+    snn.lib()
+    return snn
+
+
+def cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def exact_weights(rng, shape, lo=2 ** -8):
+    return rng.uniform(lo, 1.0, size=shape).astype(np.float32)
+
+
+# ---------------------------------------------------------------------------------------- encode
+@pytest.mark.parametrize("shape,T,seed", [((1, 2, 28, 28), 15, 0), ((3, 3, 50, 60), 32, 1), ((2, 1, 1, 5), 10, 2),
+                                          ((4, 5, 7, 9), 1, 3), ((2, 4, 33, 65), 254, 4), ((1, 1, 64, 300), 7, 5)])
+def test_encode_random(G, orc, shape, T, seed):
+    rng = np.random.default_rng(seed)
+    x = rng.random(shape).astype(np.float32)
+    x[rng.random(shape) < 0.3] = 0
+    x[rng.random(shape) < 0.05] = -1
+    x.reshape(-1)[::97] = 0.5                        # ties
+    if x.size > 10:
+        x.reshape(-1)[3] = np.nan
+    got = host(G.encode(cu(x), T))
+    assert np.array_equal(got, orc.encode(x, T))
+
+
+def test_encode_all_equal_and_zero(G, orc):
+    x = np.full((2, 3, 20, 20), 0.25, np.float32)
+    x[1] = 0
+    for T in (1, 15, 254):
+        assert np.array_equal(host(G.encode(cu(x), T)), orc.encode(x, T))
+
+
+def test_encode_quantized_many_ties(G, orc):
+    rng = np.random.default_rng(11)
+    x = (rng.integers(0, 7, size=(5, 4, 40, 41)) / 6).astype(np.float32)
+    for T in (15, 30, 32):
+        assert np.array_equal(host(G.encode(cu(x), T)), orc.encode(x, T))
+
+
+def test_encode_empty(G):
+    x = torch.empty((0, 2, 4, 4), dtype=torch.float32, device="cuda")
+    assert G.encode(x, 5).shape == (0, 2, 4, 4)
+
+
+# ---------------------------------------------------------------------------------------- expand / validate
+def test_expand_and_validate(G, orc):
+    rng = np.random.default_rng(1)
+    lat = rng.integers(0, 9, size=(3, 4, 5, 6)).astype(np.uint8)
+    lat[rng.random(lat.shape) < 0.3] = NS
+    assert np.array_equal(host(G.expand(cu(lat), 9)), orc.expand(lat, 9))
+    assert G.validate_lat(cu(lat), 9) == 0
+    assert G.validate_lat(cu(lat), 5) == int(((lat >= 5) & (lat != NS)).sum())
+
+
+# ---------------------------------------------------------------------------------------- conv + fire
+CONV_CASES = [
+    # (B, C, H, W, pad, F, K, T, theta, p_spike)
+    (2, 2, 28, 28, 2, 30, 5, 15, 15.0, 0.5),        # C1-like, F < 32
+    (3, 6, 14, 13, 1, 70, 3, 15, 4.0, 0.7),         # F not a multiple of 32, ragged W
+    (2, 30, 14, 14, 1, 250, 3, 15, 10.0, 0.9),      # C2 L2 shape
+    (1, 4, 20, 31, 0, 20, 5, 30, 15.0, 0.5),        # C4 L1-like, T = 30
+    (2, 32, 24, 24, 2, 256, 5, 32, 40.0, 0.5),      # C5-like
+    (2, 3, 9, 9, 0, 33, 3, 1, 1.0, 0.8),            # T = 1
+    (2, 3, 9, 9, 2, 40, 3, 6, -0.5, 0.5),           # theta < 0 (fires at t = 0)
+    (2, 5, 8, 8, 1, 37, 3, 6, math.inf, 0.6),       # Eq. 5 on the shared-memory path
+    (2, 250, 4, 4, 2, 200, 5, 15, math.inf, 0.9),   # Eq. 5 dense path (C2 L3 shape)
+    (1, 20, 25, 40, 0, 100, 17, 30, math.inf, 0.7), # Eq. 5 dense path (C4 L2 shape)
+    (1, 2, 5, 5, 0, 3, 5, 4, 0.5, 0.0),             # no input spikes at all
+]
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_fire_vs_oracle(G, orc, case):
+    B, C, H, W, pad, F, K, T, theta, p = case
+    rng = np.random.default_rng(abs(hash(case)) % 2 ** 31)
+    import synth
+    lat_in = synth.random_latencies(rng, (B, C, H, W), T, p)
+    w = exact_weights(rng, (F, C, K, K))
+    w[0, 0, 0, 0] = 0.0                                # zero weight is exact too
+    lat, v = G.conv_fire(cu(lat_in), cu(w), pad, T, theta)
+    G.sync_status()
+    ol, ov = orc.conv_fire(lat_in, w, pad, T, theta)
+    assert np.array_equal(host(lat), ol)
+    assert np.array_equal(host(v), ov)
+
+
+@pytest.mark.parametrize("theta", [3.0, math.inf])
+def test_conv_pot_out_vs_oracle_potentials(G, orc, theta):
+    rng = np.random.default_rng(5)
+    import synth
+    B, C, H, W, pad, F, K, T = 2, 3, 10, 11, 1, 45, 3, 7
+    lat_in = synth.random_latencies(rng, (B, C, H, W), T, 0.6)
+    w = exact_weights(rng, (F, C, K, K))
+    lat, v, pot = G.conv_fire(cu(lat_in), cu(w), pad, T, theta, want_pot=True)
+    for b in range(B):
+        P = orc.potentials(lat_in[b], w, pad, T)
+        assert np.array_equal(host(pot[b]), P.astype(np.float32))
+        ol, ov = orc.fire(P, theta)
+        assert np.array_equal(host(lat[b]), ol) and np.array_equal(host(v[b]), ov)
+
+
+def test_conv_inexact_weight_flagged(G):
+    lat_in = torch.zeros((1, 1, 4, 4), dtype=torch.uint8, device="cuda")
+    w = torch.full((2, 1, 3, 3), 0.5, dtype=torch.float32, device="cuda")
+    w[1, 0, 0, 0] = 1e-5                              # not a multiple of 2^-31
+    G.conv_fire(lat_in, w, 0, 4, 1.0)
+    with pytest.raises(G.SNNError) as e:
+        G.sync_status()
+    assert e.value.code == G.SNN_EINEXACT
+    G.conv_fire(lat_in, w.clamp(min=0.5), 0, 4, 1.0)
+    G.sync_status()                                   # cleared
+
+
+def test_conv_errors(G):
+    lat_in = torch.zeros((1, 1, 4, 4), dtype=torch.uint8, device="cuda")
+    w = torch.full((2, 1, 7, 7), 0.5, dtype=torch.float32, device="cuda")
+    with pytest.raises(G.SNNError):
+        G.conv_fire(lat_in, w, 0, 4, 1.0)             # kernel larger than the padded input
+    with pytest.raises(G.SNNError):
+        G.conv_fire(lat_in, w[:, :, :3, :3].contiguous(), 0, 0, 1.0)   # T = 0
+
+
+# ---------------------------------------------------------------------------------------- pool
+@pytest.mark.parametrize("win,stride,pad,with_v", [((2, 2), (2, 2), (0, 0), True), ((3, 3), (3, 3), (0, 0), False),
+                                                  ((7, 7), (6, 6), (0, 0), True), ((3, 2), (2, 1), (1, 1), True),
+                                                  ((2, 3), (3, 2), (1, 0), True), ((1, 1), (1, 1), (0, 0), True)])
+def test_pool_vs_oracle(G, orc, win, stride, pad, with_v):
+    import synth
+    rng = np.random.default_rng(3)
+    T = 9
+    lat = synth.random_latencies(rng, (3, 5, 37, 29), T, 0.5)
+    v = synth.random_potentials_at_spike(rng, lat, 4)
+    gl, gv = G.pool(cu(lat), cu(v) if with_v else None, win, stride, pad)
+    ol, ov = orc.pool(lat, v if with_v else None, *win, *stride, *pad, T)
+    assert np.array_equal(host(gl), ol)
+    if with_v:
+        assert np.array_equal(host(gv), ov)
+
+
+# ---------------------------------------------------------------------------------------- inhibit
+@pytest.mark.parametrize("F,levels", [(1, 0), (6, 3), (30, 0), (257, 2)])
+def test_inhibit_vs_oracle(G, orc, F, levels):
+    import synth
+    rng = np.random.default_rng(F)
+    lat = synth.random_latencies(rng, (2, F, 13, 17), 5, 0.4)
+    v = synth.random_potentials_at_spike(rng, lat, levels)
+    gl, gv, gw = G.inhibit(cu(lat), cu(v))
+    ol, ov, ow = orc.inhibit(lat, v)
+    assert np.array_equal(host(gl), ol) and np.array_equal(host(gv), ov) and np.array_equal(host(gw), ow)
+
+
+# ---------------------------------------------------------------------------------------- k-WTA
+@pytest.mark.parametrize("B,F,H,W,k,r,p,levels", [(4, 30, 28, 28, 5, 3, 0.3, 0), (3, 250, 14, 14, 8, 2, 0.5, 3),
+                                                 (2, 7, 5, 6, 20, 0, 0.5, 2), (2, 3, 4, 4, 5, 1, 0.05, 0),
+                                                 (2, 256, 64, 64, 16, 4, 0.2, 0), (3, 1, 9, 9, 3, 0, 1.0, 1),
+                                                 (2, 4, 3, 3, 2, 5, 0.0, 0)])
+def test_k_winners_vs_oracle(G, orc, B, F, H, W, k, r, p, levels):
+    import synth
+    rng = np.random.default_rng(B * 1000 + F)
+    lat = synth.random_latencies(rng, (B, F, H, W), 6, p)
+    v = synth.random_potentials_at_spike(rng, lat, levels)
+    gw, gc = G.k_winners(cu(lat), cu(v), k, r)
+    ow, oc = orc.k_winners(lat, v, k, r)
+    assert np.array_equal(host(gc), oc)
+    assert np.array_equal(host(gw), ow)
+
+
+# ---------------------------------------------------------------------------------------- STDP
+@pytest.mark.parametrize("reward,stab", [(1.0, 1), (-1.0, 1), (0.0, 1), (None, 0), (1.0, 0)])
+def test_stdp_vs_oracle(G, orc, reward, stab):
+    import synth
+    rng = np.random.default_rng(7)
+    F, C, K, H, W, pad, T = 12, 5, 3, 11, 9, 1, 8
+    w = rng.random((F, C, K, K)).astype(np.float32)
+    w[0, 0, 0, :] = [0.0, 1.0, 0.5]
+    lat_in = synth.random_latencies(rng, (C, H, W), T, 0.6)
+    Ho, Wo = H + 2 * pad - K + 1, W + 2 * pad - K + 1
+    lat_out = synth.random_latencies(rng, (F, Ho, Wo), T, 0.7)
+    v_out = synth.random_potentials_at_spike(rng, lat_out)
+    win, cnt = orc.k_winners(lat_out[None], v_out[None], 4, 1)
+    lb, ub = (0.0, 1.0) if stab else (0.2, 0.8)
+    gw = cu(w)
+    rt = None if reward is None else torch.tensor([reward], dtype=torch.float32, device="cuda")
+    G.stdp_update(gw, cu(lat_in), pad, cu(lat_out), cu(win[0]), cu(cnt), 0.004, -0.003, lb, ub, stab, rt)
+    ow = orc.stdp(w, lat_in, pad, lat_out, win[0], int(cnt[0]), 0.004, -0.003, lb, ub, stab,
+                  1 if reward is None else int(reward))
+    assert np.array_equal(host(gw), ow)
+
+
+def test_decide_vs_oracle(G, orc):
+    win = np.array([[[57, 1, 2]], [[3, 0, 0]], [[-1, -1, -1]]], np.int32)
+    cnt = np.array([1, 1, 0], np.int32)
+    lab = np.array([1, 1, 0], np.int32)
+    d, rw = G.decide(cu(win), cu(cnt), 100, 2, cu(lab))
+    exp = [orc.decide(win[b], cnt[b], 100, 2, int(lab[b])) for b in range(3)]
+    assert host(d).tolist() == [e[0] for e in exp]
+    assert host(rw).tolist() == [float(e[1]) for e in exp]
