@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the B200 spike-wave step (SpykeTorch, arxiv 1903.02440).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
+
+Default workload = BASELINE.json configs[1] (C2): 3-layer DCSNN inference, T = 15, on a batch of
+1000 seeded synthetic 28x28 stroke images (DoG on/off, 6 channels).  One step = one pass of the hot
+path over the batch: encode -> conv+fire -> pool -> conv+fire -> pool -> conv (theta = inf) ->
+1-winner readout -> class.  Inputs are resident in HBM when the timed region starts; L2 is flushed
+(256 MiB write) between timed steps, outside the step's event pair.
+
+Multi-GPU (torchrun, one process per GPU, NCCL): every rank processes its own batch of the same size
+(weak scaling, images are independent -- no data-path collective); time = max over
+ranks of the summed step times; value = images of all ranks / that time.
+
+``--impl reference`` times the CPU oracle (oracle/, plain C, fp64) as it stands on the host cores,
+on a bounded sample of the same workload per step (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "images/sec & synaptic events/sec (3-layer DCSNN, T=15); % roofline"
+SMEM_BYTES_PER_CLK_SM = 128          # shared-memory crossbar (B300_MICROARCH.md "LDS/STS")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu: no flush/clocks/baselines")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm=d.get("hbm_gbs", 6650.0), bf16=d.get("bf16_tflops", 1590.0),
+                    bf16_sus=d.get("bf16_tflops_sustained", 1400.0), sm_max=d.get("sm_max_mhz", 1965.0),
+                    src="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, sm_max=1965.0, src="fallback")
+
+
+# --------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 10:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[6:10]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------------------- workloads
+class C2Step:
+    """configs[1]: 3-layer inference over a resident batch."""
+    name = "c2"
+
+    def __init__(self, torch, dev, batch=1000):
+        import synth
+        from paper_1903_02440_b200 import pipeline, snn
+        self.torch, self.snn = torch, snn
+        self.wl = synth.C2(n=batch)
+        self.B = batch
+        self.net = pipeline.C2Net(self.wl, batch, device=dev)
+        self.x = torch.from_numpy(self.wl.X).to(dev)
+        self.stages = ["encode", "conv1", "pool1", "conv2", "pool2", "conv3", "kwta", "decide"]
+
+    def run(self, ev=None):
+        n, snn, T = self.net, self.snn, self.wl.T
+        s1, s2, s3 = self.wl.convs
+
+        def mark(i):
+            if ev is not None:
+                ev[i].record()
+        mark(0)
+        snn.encode(self.x, T, out=n.lat0, ws=n.ws_enc); mark(1)
+        snn.conv_fire(n.lat0, n.w[0], s1.pad, T, s1.theta, lat_out=n.l1.lat, v_out=n.l1.v, ws=n.l1.ws); mark(2)
+        p = n.l1.pool_spec
+        snn.pool(n.l1.lat, None, (p.PH, p.PW), (p.SH, p.SW), (p.DH, p.DW), lat_out=n.l1.plat); mark(3)
+        snn.conv_fire(n.l1.plat, n.w[1], s2.pad, T, s2.theta, lat_out=n.l2.lat, v_out=n.l2.v, ws=n.l2.ws); mark(4)
+        p = n.l2.pool_spec
+        snn.pool(n.l2.lat, None, (p.PH, p.PW), (p.SH, p.SW), (p.DH, p.DW), lat_out=n.l2.plat); mark(5)
+        snn.conv_fire(n.l2.plat, n.w[2], s3.pad, T, s3.theta, lat_out=n.l3.lat, v_out=n.l3.v, ws=n.l3.ws); mark(6)
+        snn.k_winners(n.l3.lat, n.l3.v, 1, 0, winners=n.winners, count=n.count, ws=n.ws_kw); mark(7)
+        snn.decide(n.winners, n.count, s3.F, self.wl.extra["n_classes"], None, decision=n.decision,
+                   reward=n.reward); mark(8)
+
+    def e2e(self, x_host, out_host):
+        """Public-API path with host buffers: H2D of the inputs, the step, D2H of the decisions."""
+        self.x.copy_(x_host, non_blocking=True)
+        self.run()
+        out_host.copy_(self.net.decision, non_blocking=True)
+
+    def host_io(self):
+        xh = self.torch.from_numpy(self.wl.X).pin_memory()
+        oh = self.torch.empty((self.B,), dtype=self.torch.int32).pin_memory()
+        return xh, oh
+
+    def events(self):
+        """(paper events per batch, necessary events per conv layer) -- off the clock."""
+        n, snn, T = self.net, self.snn, self.wl.T
+        self.run()
+        out = {}
+        for name, lat_in, spec, lo in (("conv1", n.lat0, self.wl.convs[0], n.l1.lat),
+                                       ("conv2", n.l1.plat, self.wl.convs[1], n.l2.lat),
+                                       ("conv3", n.l2.plat, self.wl.convs[2], n.l3.lat)):
+            out[name] = snn.count_events(lat_in, spec.F, spec.KH, spec.KW, spec.pad, T, lo)
+        return out
+
+    def config(self):
+        return {"workload": "c2: BASELINE.json configs[1], 3-layer DCSNN inference, T=15",
+                "global_batch": self.B, "images": "28x28 strokes -> 6-ch DoG on/off (synthetic)",
+                "layers": "F30 5x5 p2 th15 -> pool2/2 -> F250 3x3 p1 th10 -> pool3/3 -> F200 5x5 p2 th=inf -> 1 winner",
+                "l2": "flushed between timed steps (256 MiB write, outside the step events)"}
+
+    def units(self):
+        return self.B
+
+    def oracle_step(self, n):
+        from oracle import flows
+        import synth
+        wl = self.wl if n == self.B else synth.Workload("c2", self.wl.T, self.wl.X[:n], self.wl.convs,
+                                                         self.wl.weights, self.wl.pools, self.wl.extra)
+        flows.c2(wl)
+
+
+class C5Step(C2Step):
+    name = "c5"
+
+    def __init__(self, torch, dev, batch=64):
+        import synth
+        from paper_1903_02440_b200 import pipeline, snn
+        self.torch, self.snn = torch, snn
+        self.wl = synth.C5(n=batch)
+        self.B = batch
+        self.net = pipeline.C5Net(self.wl, batch, device=dev)
+        self.x = torch.from_numpy(self.wl.X).to(dev)
+        self.stages = ["encode", "conv1", "pool1", "inhibit", "kwta"]
+
+    def run(self, ev=None):
+        n, snn, T = self.net, self.snn, self.wl.T
+        s = self.wl.convs[0]
+
+        def mark(i):
+            if ev is not None:
+                ev[i].record()
+        mark(0)
+        snn.encode(self.x, T, out=n.lat0, ws=n.ws_enc); mark(1)
+        snn.conv_fire(n.lat0, n.w, s.pad, T, s.theta, lat_out=n.l1.lat, v_out=n.l1.v, ws=n.l1.ws); mark(2)
+        p = n.l1.pool_spec
+        snn.pool(n.l1.lat, n.l1.v, (p.PH, p.PW), (p.SH, p.SW), (p.DH, p.DW), lat_out=n.l1.plat, v_out=n.l1.pv)
+        mark(3)
+        snn.inhibit(n.l1.plat, n.l1.pv, lat_out=n.ilat, v_out=n.iv, winner_f=n.wf); mark(4)
+        snn.k_winners(n.ilat, n.iv, self.wl.extra["k"], self.wl.extra["r"], winners=n.winners, count=n.count,
+                      ws=n.ws_kw); mark(5)
+
+    def e2e(self, x_host, out_host):
+        self.x.copy_(x_host, non_blocking=True)
+        self.run()
+        out_host.copy_(self.net.winners, non_blocking=True)
+
+    def host_io(self):
+        xh = self.torch.from_numpy(self.wl.X).pin_memory()
+        oh = self.torch.empty(tuple(self.net.winners.shape), dtype=self.torch.int32).pin_memory()
+        return xh, oh
+
+    def events(self):
+        n, snn, T = self.net, self.snn, self.wl.T
+        self.run()
+        s = self.wl.convs[0]
+        return {"conv1": snn.count_events(n.lat0, s.F, s.KH, s.KW, s.pad, T, n.l1.lat)}
+
+    def config(self):
+        return {"workload": "c5: BASELINE.json configs[4], throughput stress, T=32", "global_batch": self.B,
+                "layers": "F256 5x5 p2 th40 (32 ch 256x256) -> pool2/2 -> inhibit -> kWTA k16 r4",
+                "l2": "inputs (537 MB) larger than L2; also flushed between steps"}
+
+    def oracle_step(self, n):
+        from oracle import flows
+        import synth
+        flows.c5(synth.Workload("c5", self.wl.T, self.wl.X[:n], self.wl.convs, self.wl.weights, self.wl.pools,
+                                self.wl.extra))
+
+
+WORKLOADS = {"c2": C2Step, "c5": C5Step}
+
+
+# --------------------------------------------------------------------------------------- roofline
+def roofline(stage, t_ms, ev, wl, clocks, pk):
+    """Roofline of the dominant stage from its algorithmic work per launch."""
+    f_mhz = (clocks or {}).get("sm_mhz") or pk["sm_max"]
+    t = t_ms * 1e-3
+    if stage.startswith("conv"):
+        paper, need = ev[stage]
+        idx = int(stage[-1]) - 1
+        spec = wl.convs[idx]
+        if math.isinf(spec.theta):
+            # dense contraction of S[T-1]: int8 tensor-core work = 4 limbs x 2 ops per (position, feature,
+            # receptive-field entry); SIMT v1 reads one 4-byte weight per spiking event instead
+            return {"bound": "smem", "achieved": round(paper * 4 / t / 1e9, 1),
+                    "peak": round(SMEM_BYTES_PER_CLK_SM * 148 * f_mhz * 1e6 / 1e9, 1), "unit": "GB/s",
+                    "frac": round(paper * 4 / t / (SMEM_BYTES_PER_CLK_SM * 148 * f_mhz * 1e6), 4),
+                    "traffic": None, "kernel": stage, "work": f"{paper} events x 4 B (weight gathers)",
+                    "peak_src": f"128 B/clk/SM x 148 SMs x {f_mhz:.0f} MHz (measured SM clock)"}
+        peak = SMEM_BYTES_PER_CLK_SM * 148 * f_mhz * 1e6
+        ach = need * 4 / t
+        return {"bound": "smem", "achieved": round(ach / 1e9, 1), "peak": round(peak / 1e9, 1), "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": None, "kernel": stage,
+                "work": f"{need} necessary events x 4 B weight gather (of {paper} paper-definition events)",
+                "peak_src": f"128 B/clk/SM x 148 SMs x {f_mhz:.0f} MHz (measured SM clock)"}
+    return None
+
+
+# --------------------------------------------------------------------------------------- arms
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    import synth  # noqa: F401
+    import torch
+    step = WORKLOADS[args.workload].__new__(WORKLOADS[args.workload])
+    step.wl = {"c2": lambda: synth.C2(n=1000), "c5": lambda: synth.C5(n=2)}[args.workload]()
+    step.B = step.wl.X.shape[0]
+    sample = {"c2": 100, "c5": 1}[args.workload]
+    for _ in range(args.warmup):
+        step.oracle_step(sample)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step.oracle_step(sample)
+    dt = time.perf_counter() - t0
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
+    val = sample * args.steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "images/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "sample_images_per_step": sample},
+            "cpu_baseline": {"value": round(val, 3), "unit": "images/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{sample} images of the {args.workload} batch per step"},
+            "e2e": {"value": round(val, 3), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    from paper_1903_02440_b200 import snn
+    snn.lib()
+    step = WORKLOADS[args.workload](torch, dev)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if not args.profile else None
+    nst = len(step.stages)
+    for _ in range(args.warmup):
+        step.run()
+    snn.sync_status()
+    # ---------------- timed region ----------------
+    sampler = ClockSampler(local) if (rank == 0 and not args.no_clocks and not args.profile) else None
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 1)] for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    launches0 = snn.launch_count()
+    for k in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+        step.run(ev[k])
+    launches = snn.launch_count() - launches0
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop() if sampler else None
+    snn.sync_status()
+    step_ms = [ev[k][0].elapsed_time(ev[k][nst]) for k in range(args.steps)]
+    stage_ms = [statistics.mean(ev[k][i].elapsed_time(ev[k][i + 1]) for k in range(args.steps)) for i in range(nst)]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    units = step.B * args.steps * world
+    value = units / (total_ms * 1e-3)
+    # ---------------- off-clock: events, e2e, cpu baseline ----------------
+    ev_counts = step.events()
+    paper_events = sum(v[0] for v in ev_counts.values())
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        xh, oh = step.host_io()
+        for _ in range(2):
+            step.e2e(xh, oh)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            step.e2e(xh, oh)
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": round(step.B * args.steps * world / (e2e_ms * 1e-3), 3), "unit": "images/s",
+               "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
+               "d2h_bytes_per_step": int(oh.numel() * oh.element_size())}
+    if rank != 0:
+        return
+    pk = peaks()
+    dom = max(range(nst), key=lambda i: stage_ms[i])
+    roof = roofline(step.stages[dom], stage_ms[dom], ev_counts, step.wl, clocks, pk)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline and not args.profile:
+        n = {"c2": 1000, "c5": 1}[step.name]
+        t0 = time.perf_counter()
+        step.oracle_step(n)
+        dt = time.perf_counter() - t0
+        cpu = {"value": round(n / dt, 3), "unit": "images/s",
+               "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count())), "kind": "oracle",
+               "sample": f"{n} images of the {step.name} batch, one pass (OpenMP over images)"}
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "images/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic", "config": step.config(),
+            "events_per_sec": round(paper_events * args.steps * world / (total_ms * 1e-3), 1),
+            "events_per_step": paper_events,
+            "stages_ms": {s: round(m, 4) for s, m in zip(step.stages, stage_ms)},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": int(launches),
+            "peaks": {"src": pk["src"], "hbm_gbs": pk["hbm"], "bf16_tflops": pk["bf16"]}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        run_ours(args, rank, world, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -157,6 +157,21 @@ SNN_API int snn_decide(const int32_t* winners, const int32_t* count, int B, int 
                const int32_t* labels, int32_t* decision, float* reward, snn_stream_t s);
 
 /* ---------------------------------------------------------------------------------------------
+ * Measurement helpers (off the hot path).
+ * snn_count_events writes two uint64 counters to out[0..1] (device), overwriting them:
+ *   out[0] = synaptic events as the paper's delta contraction defines them: F * sum over output
+ *            positions of the number of spiking inputs in the receptive field;
+ *   out[1] = necessary events: sum over output neurons of the number of receptive-field inputs that
+ *            spiked at or before the neuron's first spike lat_out (all spiking inputs if it never
+ *            fires) -- the inputs any exact first-spike computation must add.  0 if lat_out is NULL.
+ *   lat_in uint8 [B, C, H, W], lat_out uint8 [B, F, Ho, Wo] or NULL.
+ * snn_launch_count returns the number of kernels this process has launched through libsnn.
+ * ------------------------------------------------------------------------------------------- */
+SNN_API int snn_count_events(const uint8_t* lat_in, int B, int C, int H, int W, int pad, int F, int KH, int KW,
+                             int T, const uint8_t* lat_out, unsigned long long* out, snn_stream_t s);
+SNN_API unsigned long long snn_launch_count(void);
+
+/* ---------------------------------------------------------------------------------------------
  * Status.
  * snn_sync_status synchronises the stream, then returns and clears the device error word
  * (SNN_OK, SNN_EINEXACT) or SNN_ECUDA if the stream reported a CUDA error.

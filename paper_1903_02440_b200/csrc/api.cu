@@ -6,6 +6,8 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace snn {
@@ -29,10 +31,15 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
 int stdp_launch(float* w, int F, int C, int KH, int KW, const uint8_t* lat_in, int H, int W, int pad,
                 const uint8_t* lat_out, int Ho, int Wo, const int32_t* winners, const int32_t* count, int k,
                 float a_plus, float a_minus, float lb, float ub, int stabilizer, const float* reward, cudaStream_t s);
+int count_events_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, int F, int KH, int KW, int T,
+                        const uint8_t* lat_out, unsigned long long* out, cudaStream_t s);
 int decide_launch(const int32_t* winners, const int32_t* count, int B, int k, int F, int n_classes,
                   const int32_t* labels, int32_t* decision, float* reward, cudaStream_t s);
 
 static thread_local char t_err[512] = "";
+static std::atomic<unsigned long long> g_launches{0};
+
+void note_launch(int n) { g_launches.fetch_add(uint64_t(n), std::memory_order_relaxed); }
 
 int set_error(int code, const char* fmt, ...) {
   va_list ap;
@@ -69,9 +76,31 @@ using namespace snn;
 
 static inline cudaStream_t S(snn_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
+static int conv_checks(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta) {
+  REQUIRE(T >= 1 && T <= 254, SNN_EINVAL, "snn_conv_fire: T=%d outside [1, 254]", T);
+  REQUIRE(!isnan(theta), SNN_EINVAL, "snn_conv_fire: theta is NaN");
+  REQUIRE(B >= 0 && C >= 1 && H >= 1 && W >= 1 && F >= 0 && KH >= 1 && KW >= 1 && pad >= 0, SNN_ESHAPE,
+          "snn_conv_fire: bad dimensions");
+  REQUIRE(KH <= H + 2 * pad && KW <= W + 2 * pad, SNN_ESHAPE,
+          "snn_conv_fire: kernel %dx%d larger than padded input %dx%d", KH, KW, H + 2 * pad, W + 2 * pad);
+  REQUIRE(int64_t(C) * KH * KW <= 65534, SNN_ESHAPE, "snn_conv_fire: receptive field C*KH*KW > 65534");
+  REQUIRE(KH < 256 && KW < 256, SNN_ESHAPE, "snn_conv_fire: kernel side >= 256");
+  return SNN_OK;
+}
+
 extern "C" {
 
 int snn_version(void) { return 1; }
+
+unsigned long long snn_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int snn_count_events(const uint8_t* lat_in, int B, int C, int H, int W, int pad, int F, int KH, int KW, int T,
+                     const uint8_t* lat_out, unsigned long long* out, snn_stream_t s) {
+  int rc = conv_checks(B, C, H, W, pad, F, KH, KW, T, 0.0f);
+  if (rc) return rc;
+  REQUIRE(out, SNN_EINVAL, "snn_count_events: NULL output");
+  return count_events_launch(lat_in, B, C, H, W, pad, F, KH, KW, T, lat_out, out, S(s));
+}
 
 const char* snn_last_error(void) { return t_err; }
 
@@ -116,17 +145,6 @@ int snn_validate_lat(const uint8_t* lat, size_t n, int T, int32_t* n_bad, snn_st
   return validate_launch(lat, n, T, n_bad, S(s));
 }
 
-static int conv_checks(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta) {
-  REQUIRE(T >= 1 && T <= 254, SNN_EINVAL, "snn_conv_fire: T=%d outside [1, 254]", T);
-  REQUIRE(!isnan(theta), SNN_EINVAL, "snn_conv_fire: theta is NaN");
-  REQUIRE(B >= 0 && C >= 1 && H >= 1 && W >= 1 && F >= 0 && KH >= 1 && KW >= 1 && pad >= 0, SNN_ESHAPE,
-          "snn_conv_fire: bad dimensions");
-  REQUIRE(KH <= H + 2 * pad && KW <= W + 2 * pad, SNN_ESHAPE,
-          "snn_conv_fire: kernel %dx%d larger than padded input %dx%d", KH, KW, H + 2 * pad, W + 2 * pad);
-  REQUIRE(int64_t(C) * KH * KW <= 65534, SNN_ESHAPE, "snn_conv_fire: receptive field C*KH*KW > 65534");
-  REQUIRE(KH < 256 && KW < 256, SNN_ESHAPE, "snn_conv_fire: kernel side >= 256");
-  return SNN_OK;
-}
 
 size_t snn_conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T) {
   if (conv_checks(B, C, H, W, pad, F, KH, KW, T, 0.0f)) return 0;

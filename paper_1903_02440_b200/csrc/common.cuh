@@ -18,6 +18,7 @@ int read_clear_error_word(int* word);
 int set_error(int code, const char* fmt, ...);
 int check_launch(const char* what);
 int num_sms();  // multiprocessor count of the current device (cached)
+void note_launch(int n = 1);  // diagnostic kernel-launch counter (snn_launch_count)
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

@@ -412,12 +412,14 @@ int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
     int blocks = int(ceil_div(total, 256));
     if (blocks > 2048) blocks = 2048;
     weight_prep_kernel<<<blocks, 256, 0, s>>>(w, F, a.R, pl.FGS, pl.n_groups, a.wq);
+    note_launch();
   }
   if (pl.dense) {
     int64_t items = npos * pl.n_groups;
     int64_t blocks = ceil_div(items, 8);
     if (blocks > int64_t(num_sms()) * 8) blocks = int64_t(num_sms()) * 8;
     conv_dense_kernel<<<int(blocks), 256, 0, s>>>(a);
+    note_launch();
     return check_launch("snn_conv_fire(dense)");
   }
   int occ = 1;
@@ -438,12 +440,15 @@ int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   switch (pl.fpl) {
     case 1:
       conv_fire_kernel<1><<<grid, pl.nwarps * 32, pl.smem, s>>>(a);
+      note_launch();
       break;
     case 2:
       conv_fire_kernel<2><<<grid, pl.nwarps * 32, pl.smem, s>>>(a);
+      note_launch();
       break;
     default:
       conv_fire_kernel<4><<<grid, pl.nwarps * 32, pl.smem, s>>>(a);
+      note_launch();
       break;
   }
   return check_launch("snn_conv_fire");

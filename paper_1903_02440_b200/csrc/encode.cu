@@ -271,14 +271,19 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, uint8_t* la
       return check_launch("snn_encode memset");
     dim3 grid(nchunks, gn);
     enc_hist0_kernel<<<grid, kEncThreads, 0, s>>>(xg, n, ws);
+    note_launch();
     if (T > 1) {
       enc_select_kernel<<<gn, 256, 0, s>>>(T, 0, ws);
+      note_launch();
       for (int L = 1; L < kEncLevels; ++L) {
         enc_hist_kernel<<<grid, kEncThreads, 0, s>>>(xg, n, T, L, ws);
+        note_launch();
         enc_select_kernel<<<gn, 256, 0, s>>>(T, L, ws);
+        note_launch();
       }
     }
     enc_assign_kernel<<<grid, kEncThreads, 0, s>>>(xg, n, T, lat + int64_t(g0) * n, ws);
+    note_launch();
     int rc = check_launch("snn_encode");
     if (rc) return rc;
   }
@@ -300,6 +305,7 @@ int expand_launch(const uint8_t* lat, int B, int n, int T, float* wave, cudaStre
   int blocks = int(ceil_div(n, 256));
   if (blocks > 4096) blocks = 4096;
   expand_kernel<<<dim3(blocks, B), 256, 0, s>>>(lat, n, T, wave);
+  note_launch();
   return check_launch("snn_expand");
 }
 
@@ -319,6 +325,7 @@ int validate_launch(const uint8_t* lat, size_t n, int T, int32_t* n_bad, cudaStr
   size_t blocks = (n + 255) / 256;
   if (blocks > 1184) blocks = 1184;
   validate_kernel<<<unsigned(blocks), 256, 0, s>>>(lat, n, T, n_bad);
+  note_launch();
   return check_launch("snn_validate_lat");
 }
 

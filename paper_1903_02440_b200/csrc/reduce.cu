@@ -56,6 +56,7 @@ int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, 
   if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
   pool_kernel<<<int(blocks), 256, 0, s>>>(lat, v_out ? v : nullptr, int64_t(B) * F, H, W, PH, PW, SH, SW, DH, DW,
                                           Ho, Wo, lat_out, v_out);
+  note_launch();
   return check_launch("snn_pool");
 }
 
@@ -92,6 +93,7 @@ int inhibit_launch(const uint8_t* lat, const float* v, int B, int F, int H, int 
   int64_t blocks = ceil_div(total, 256);
   if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
   inhibit_kernel<<<int(blocks), 256, 0, s>>>(lat, v, B, F, HW, lat_out, v_out, winner_f);
+  note_launch();
   return check_launch("snn_inhibit");
 }
 
@@ -213,8 +215,10 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
   if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
   if (blocks < 1) blocks = 1;
   kwta_posbest_kernel<<<int(blocks), 256, 0, s>>>(lat, v, B, F, HW, pb);
+  note_launch();
   const int nwords = (F + 31) >> 5;
   kwta_rounds_kernel<<<B, kKwtaThreads, nwords * 4, s>>>(lat, v, F, H, W, k, r, pb, winners, count);
+  note_launch();
   return check_launch("snn_k_winners");
 }
 
@@ -238,6 +242,7 @@ int decide_launch(const int32_t* winners, const int32_t* count, int B, int k, in
                   const int32_t* labels, int32_t* decision, float* reward, cudaStream_t s) {
   if (B == 0) return SNN_OK;
   decide_kernel<<<int(ceil_div(B, 256)), 256, 0, s>>>(winners, count, B, k, F, n_classes, labels, decision, reward);
+  note_launch();
   return check_launch("snn_decide");
 }
 

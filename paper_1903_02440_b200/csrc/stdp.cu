@@ -52,6 +52,7 @@ int stdp_launch(float* w, int F, int C, int KH, int KW, const uint8_t* lat_in, i
   if (k == 0) return SNN_OK;
   stdp_kernel<<<k, 256, 0, s>>>(w, C, KH, KW, lat_in, H, W, pad, lat_out, Ho, Wo, winners, count, a_plus, a_minus,
                                 lb, ub, stabilizer, reward);
+  note_launch();
   return check_launch("snn_stdp_update");
 }
 

@@ -57,6 +57,8 @@ def lib() -> C.CDLL:
                 "snn_stdp_update": (i32, [p, i32, i32, i32, i32, p, i32, i32, i32, p, i32, i32, p, p, i32,
                                           f32, f32, f32, f32, i32, p, p]),
                 "snn_decide": (i32, [p, p, i32, i32, i32, i32, p, p, p, p]),
+                "snn_count_events": (i32, [p, i32, i32, i32, i32, i32, i32, i32, i32, i32, p, p, p]),
+                "snn_launch_count": (C.c_ulonglong, []),
             }
             for name, (res, args) in sigs.items():
                 fn = getattr(L, name)
@@ -69,7 +71,8 @@ def lib() -> C.CDLL:
 def exported_symbols():
     return ["snn_version", "snn_last_error", "snn_sync_status", "snn_encode_workspace", "snn_encode",
             "snn_expand", "snn_validate_lat", "snn_conv_fire_workspace", "snn_conv_fire", "snn_pool",
-            "snn_inhibit", "snn_k_winners_workspace", "snn_k_winners", "snn_stdp_update", "snn_decide"]
+            "snn_inhibit", "snn_k_winners_workspace", "snn_k_winners", "snn_stdp_update", "snn_decide",
+            "snn_count_events", "snn_launch_count"]
 
 
 def _check(rc: int):
@@ -263,6 +266,22 @@ def decide(winners: torch.Tensor, count: torch.Tensor, F: int, n_classes: int, l
     _check(lib().snn_decide(_ptr(winners), _ptr(count), B, k, F, n_classes, _ptr(labels), _ptr(d), _ptr(rw),
                             _stream(stream)))
     return d, rw
+
+
+def count_events(lat_in: torch.Tensor, F: int, KH: int, KW: int, pad: int, T: int,
+                 lat_out: Optional[torch.Tensor] = None, stream=None) -> Tuple[int, int]:
+    """(paper-definition synaptic events, necessary events) of one conv layer (snn_count_events)."""
+    _req(lat_in, torch.uint8, "lat_in")
+    B, C_, H, W = lat_in.shape
+    out = torch.zeros(2, dtype=torch.int64, device=lat_in.device)
+    _check(lib().snn_count_events(_ptr(lat_in), B, C_, H, W, pad, F, KH, KW, T, _ptr(lat_out), _ptr(out),
+                                  _stream(stream)))
+    o = out.cpu().tolist()
+    return int(o[0]), int(o[1])
+
+
+def launch_count() -> int:
+    return int(lib().snn_launch_count())
 
 
 def sync_status(stream=None) -> None:
