@@ -83,9 +83,12 @@ SNN_API int snn_validate_lat(const uint8_t* lat, size_t n, int T, int32_t* n_bad
  *   lat_out uint8 [B, F, Ho, Wo]; v_out float32 [B, F, Ho, Wo]
  *   pot_out float32 [B, T, F, Ho, Wo] or NULL: if non-NULL every fp32(P[t]) is written (validation
  *           mode, no early exit).
- * Workspace: snn_conv_fire_workspace(...) bytes.
+ * Workspace: snn_conv_fire_workspace(..., theta) bytes.  theta = +inf without pot_out runs the
+ * tensor-core path (tcgen05 kind::i8, exact 4-limb split of the fixed-point weights); its workspace
+ * holds the binary im2col of S[T-1] (positions x C*KH*KW bytes) and the weight limbs.
  * ------------------------------------------------------------------------------------------- */
-SNN_API size_t snn_conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T);
+SNN_API size_t snn_conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T,
+                                       float theta);
 SNN_API int snn_conv_fire(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
                   const float* w, int F, int KH, int KW, int T, float theta,
                   uint8_t* lat_out, float* v_out, float* pot_out,

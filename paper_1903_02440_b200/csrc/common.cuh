@@ -13,6 +13,8 @@ constexpr uint8_t kNoSpike = SNN_NO_SPIKE;
 // read and cleared by snn_sync_status() through read_clear_error_word().
 constexpr int kErrInexact = 1;
 int read_clear_error_word(int* word);
+int* error_word_ptr();  // device address of the error word, for kernels of other translation units
+__device__ __forceinline__ void flag_error(int* err, int bit) { atomicOr(err, bit); }
 
 // Host-side error reporting (thread-local message), defined in api.cu.
 int set_error(int code, const char* fmt, ...);

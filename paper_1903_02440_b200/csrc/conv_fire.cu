@@ -24,6 +24,12 @@ namespace snn {
 
 __device__ int g_error_word = 0;
 
+int* error_word_ptr() {
+  static int* p = nullptr;
+  if (!p) cudaGetSymbolAddress(reinterpret_cast<void**>(&p), g_error_word);
+  return p;
+}
+
 int read_clear_error_word(int* word) {
   int zero = 0;
   cudaError_t e = cudaMemcpyFromSymbol(word, g_error_word, sizeof(int));
@@ -380,12 +386,19 @@ static void make_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
   pl->wq_bytes = size_t(pl->n_groups) * (R + 1) * pl->FGS * 4;
 }
 
-size_t conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T) {
+size_t conv_tc_workspace(int B, int Ho, int Wo, int R, int F);
+int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH, int KW,
+                   int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes, cudaStream_t s);
+
+size_t conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta) {
+  const bool inf = isinf(theta) && theta > 0;
   ConvPlan pl;
-  make_plan(B, C, H, W, pad, F, KH, KW, T, false, &pl);
-  ConvPlan pl2;
-  make_plan(B, C, H, W, pad, F, KH, KW, T, true, &pl2);
-  size_t m = pl.wq_bytes > pl2.wq_bytes ? pl.wq_bytes : pl2.wq_bytes;
+  make_plan(B, C, H, W, pad, F, KH, KW, T, inf, &pl);
+  size_t m = pl.wq_bytes;
+  if (inf) {  // tensor-core path (and the SIMT dense path for validation mode)
+    size_t t = conv_tc_workspace(B, pl.a.Ho, pl.a.Wo, pl.a.R, F);
+    m = m > t ? m : t;
+  }
   return ((m + 255) & ~size_t(255)) + 256;
 }
 
@@ -407,6 +420,8 @@ int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   } else a.thr = INT64_MAX;
   const int64_t npos = int64_t(B) * a.Ho * a.Wo;
   if (npos == 0 || F == 0) return SNN_OK;
+  if (inf && !pot_out)  // Eq. 5: dense contraction of S[T-1] on the tensor cores
+    return conv_tc_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, lat_out, v_out, ws, ws_bytes, s);
   {
     int64_t total = int64_t(pl.n_groups) * (a.R + 1) * pl.FGS;
     int blocks = int(ceil_div(total, 256));

@@ -1,0 +1,298 @@
+// conv_tc.cu -- a2 + a3 for an infinite threshold (Eq. 5) on the 5th-generation tensor
+// cores (tcgen05, sm_100a).  With theta = +inf only P[T-1] matters, and P[T-1] is a dense contraction
+// of the binary spike-wave at the last step, S[T-1] (every spiking input counts), with the weights:
+//     P[pos, f] = sum_k A[pos, k] * Wq[f, k],   A = im2col(S[T-1]) in {0, 1},  Wq = w * 2^31 (uint32)
+// Exactness (N1): Wq is split into four u8 limbs, Wq = sum_l L_l * 2^(8 l); each limb GEMM
+// runs as tcgen05.mma kind::i8 (u8 x u8 -> s32; max column sum 255 * 6250 < 2^31, exact) and the
+// epilogue recombines the four int32 accumulators in int64.  The limbs are interleaved feature-major
+// in the N dimension (n = 4 f + l), so one 16-column TMEM load yields 4 features x 4 limbs.
+//
+// Operands are staged by tiny prep kernels in the canonical K-major, no-swizzle UMMA layout: per
+// (row tile, 128-byte K tile) a block of 8x16-byte core matrices [row/8][k/16][row%8][16 B]
+// (LBO = 128 B between K-adjacent core matrices, SBO = 1024 B between 8-row groups), so the GEMM's
+// producer moves each stage with two contiguous cp.async.bulk copies completing on an mbarrier.
+// Warp roles: warp 0 = bulk-copy producer, warp 1 = MMA issuer (one elected thread), warp 2 = TMEM
+// allocator, warps 4..7 = epilogue (TMEM lane quadrant = warp % 4).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace snn {
+
+constexpr int kTcM = 128;          // UMMA M (one CTA)
+constexpr int kTcKT = 128;         // bytes (= int8 elements) of K per pipeline stage
+constexpr int kTcStages = 4;
+constexpr int kTcThreads = 256;
+
+struct TcPlan {
+  int M, K, Kp, Mt, Kt, nch, Fc, N;  // N = 4 * Fc (multiple of 16, <= 256)
+  size_t a_bytes, b_bytes;
+};
+
+static TcPlan tc_plan(int B, int Ho, int Wo, int R, int F) {
+  TcPlan p;
+  p.M = B * Ho * Wo;
+  p.K = R;
+  p.Kp = int(ceil_div(R, kTcKT)) * kTcKT;
+  p.Mt = int(ceil_div(p.M, kTcM));
+  p.Kt = p.Kp / kTcKT;
+  p.nch = int(ceil_div(F, 64));
+  p.Fc = int(ceil_div(ceil_div(F, p.nch), 4)) * 4;
+  p.N = 4 * p.Fc;
+  p.a_bytes = size_t(p.Mt) * p.Kt * kTcM * kTcKT;
+  p.b_bytes = size_t(p.nch) * p.Kt * p.N * kTcKT;
+  return p;
+}
+
+size_t conv_tc_workspace(int B, int Ho, int Wo, int R, int F) {
+  TcPlan p = tc_plan(B, Ho, Wo, R, F);
+  return ((p.a_bytes + 1023) & ~size_t(1023)) + p.b_bytes + 1024;
+}
+
+// byte offset of element (row, k) inside a [row tiles][K tiles] blocked core-matrix array
+__device__ __forceinline__ size_t tc_off(int row, int k, int rows_per_tile, int Kt) {
+  const int rt = row / rows_per_tile, r = row - rt * rows_per_tile;
+  const int kt = k / kTcKT, kk = k - kt * kTcKT;
+  return (size_t(rt) * Kt + kt) * size_t(rows_per_tile) * kTcKT + size_t(r >> 3) * 1024 + (kk >> 4) * 128 +
+         (r & 7) * 16 + (kk & 15);
+}
+
+// B operand: u8 limbs of the fixed-point weights, n = 4 * f_local + limb, one block per chunk.
+__global__ void tc_prep_b_kernel(const float* __restrict__ w, int F, int R, TcPlan p, uint8_t* __restrict__ bq,
+                                 int* err) {
+  const int64_t total = int64_t(p.nch) * p.N * p.Kp;
+  int bad = 0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int k = int(i % p.Kp);
+    const int64_t rest = i / p.Kp;
+    const int n = int(rest % p.N), ch = int(rest / p.N);
+    const int f = ch * p.Fc + (n >> 2), limb = n & 3;
+    uint8_t val = 0;
+    if (f < F && k < R) {
+      const float x = w[int64_t(f) * R + k];
+      const float s = x * 2147483648.0f;
+      if (!(x >= 0.0f && x <= 1.0f) || s != truncf(s)) bad = 1;
+      else val = uint8_t(uint32_t(s) >> (8 * limb));
+    }
+    bq[size_t(ch) * p.Kt * p.N * kTcKT + tc_off(n, k, p.N, p.Kt)] = val;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flag_error(err, kErrInexact);
+}
+
+// A operand: binary im2col of the spike-wave at T-1 (any spike, since every spike time is <= T-1).
+// One thread per 16-byte core-matrix row = 16 consecutive receptive-field entries of one position.
+__global__ void tc_prep_a_kernel(const uint8_t* __restrict__ lat_in, int C, int H, int W, int pad, int KH, int KW,
+                                 int Ho, int Wo, int T, TcPlan p, uint8_t* __restrict__ aq) {
+  const int KK = KH * KW;
+  const int64_t rows16 = int64_t(p.Mt) * kTcM * (p.Kp / 16);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < rows16; i += int64_t(gridDim.x) * blockDim.x) {
+    const int k0 = int(i % (p.Kp / 16)) * 16;
+    const int m = int(i / (p.Kp / 16));
+    uint32_t wv[4] = {0, 0, 0, 0};
+    if (m < p.M) {
+      const int HoWo = Ho * Wo;
+      const int b = m / HoWo, rem = m - b * HoWo, y = rem / Wo, x = rem - (rem / Wo) * Wo;
+      int c = k0 / KK, r = k0 - c * KK, ky = r / KW, kx = r - ky * KW;
+      const uint8_t* base = lat_in + int64_t(b) * C * H * W;
+      for (int j = 0; j < 16; ++j) {
+        const int k = k0 + j;
+        if (k < p.K) {
+          const int yy = y + ky - pad, xx = x + kx - pad;
+          if (yy >= 0 && yy < H && xx >= 0 && xx < W && base[(int64_t(c) * H + yy) * W + xx] < T)
+            wv[j >> 2] |= 1u << (8 * (j & 3));
+        }
+        if (++kx == KW) { kx = 0; if (++ky == KH) { ky = 0; ++c; } }
+      }
+    }
+    *reinterpret_cast<uint4*>(aq + tc_off(m, k0, kTcM, p.Kt)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+  }
+}
+
+// ------------------------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  // watchdog: a pipeline bug traps (the launch fails with an error) instead of hanging the GPU
+  for (uint32_t n = 0; !mbar_try(bar, parity); ++n)
+    if (n == (1u << 28)) __trap();
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  // K-major, SWIZZLE_NONE canonical layout; version 1 (sm_100) at bits [46,48)
+  return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46);
+}
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ------------------------------------------------------------------------------- the GEMM
+__global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* __restrict__ aq,
+                                                                 const uint8_t* __restrict__ bq, TcPlan p, int F,
+                                                                 int HoWo, int T, uint32_t tmem_cols,
+                                                                 uint8_t* __restrict__ lat_out,
+                                                                 float* __restrict__ v_out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t a_bytes = kTcM * kTcKT, b_bytes = uint32_t(p.N) * kTcKT, stage_bytes = a_bytes + b_bytes;
+  __shared__ __align__(8) uint64_t full_bar[kTcStages], empty_bar[kTcStages], done_bar;
+  __shared__ uint32_t tmem_base_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mt = blockIdx.x, ch = blockIdx.y;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(smem_u32(&full_bar[s]), 1);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
+    }
+    mbar_init(smem_u32(&done_bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = tmem_base_sh;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- producer: two bulk copies per stage ----------------
+    const uint8_t* a_src = aq + size_t(mt) * p.Kt * a_bytes;
+    const uint8_t* b_src = bq + size_t(ch) * p.Kt * b_bytes;
+    for (int kt = 0; kt < p.Kt; ++kt) {
+      const int s = kt % kTcStages, u = kt / kTcStages;
+      if (kt >= kTcStages) mbar_wait(smem_u32(&empty_bar[s]), (u - 1) & 1);
+      const uint32_t fb = smem_u32(&full_bar[s]);
+      mbar_expect_tx(fb, stage_bytes);
+      const uint32_t dst = smem_u32(smem + size_t(s) * stage_bytes);
+      bulk_g2s(dst, a_src + size_t(kt) * a_bytes, a_bytes, fb);
+      bulk_g2s(dst + a_bytes, b_src + size_t(kt) * b_bytes, b_bytes, fb);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = (2u << 4)                       // D format: s32
+                           | (0u << 7) | (0u << 10)        // A, B: unsigned 8-bit
+                           | (uint32_t(p.N >> 3) << 17)    // N
+                           | (uint32_t(kTcM >> 4) << 24);  // M = 128
+    for (int kt = 0; kt < p.Kt; ++kt) {
+      const int s = kt % kTcStages, u = kt / kTcStages;
+      mbar_wait(smem_u32(&full_bar[s]), u & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t a_base = smem_u32(smem + size_t(s) * stage_bytes);
+      const uint32_t b_base = a_base + a_bytes;
+#pragma unroll
+      for (int ks = 0; ks < kTcKT / 32; ++ks) {  // K = 32 bytes per tcgen05.mma (kind::i8)
+        const uint64_t da = umma_desc(a_base + ks * 256, 128, 1024);
+        const uint64_t db = umma_desc(b_base + ks * 256, 128, 1024);
+        umma_i8(tmem_base, da, db, idesc, (kt | ks) != 0);
+      }
+      umma_commit(smem_u32(&empty_bar[s]));  // frees the stage once these MMAs have read it
+    }
+    umma_commit(smem_u32(&done_bar));
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> registers -> exact recombination -> (lat, v) ----------------
+    mbar_wait(smem_u32(&done_bar), 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int m = mt * kTcM + row;
+    const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16);
+    const int b = m / HoWo, rem = m - (m / HoWo) * HoWo;
+    for (int g = 0; g < p.Fc / 4; ++g) {
+      uint32_t v[16];
+      tmem_ld16(trow + uint32_t(g * 16), v);  // warp-collective: every lane participates
+      if (m < p.M) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int f = ch * p.Fc + g * 4 + j;
+          if (f < F) {
+            const int64_t acc = int64_t(v[4 * j]) + (int64_t(v[4 * j + 1]) << 8) + (int64_t(v[4 * j + 2]) << 16) +
+                                (int64_t(v[4 * j + 3]) << 24);
+            const int64_t o = (int64_t(b) * F + f) * HoWo + rem;
+            lat_out[o] = acc > 0 ? uint8_t(T - 1) : kNoSpike;
+            v_out[o] = fixed_to_float(acc);
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols) : "memory");
+  }
+}
+
+int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH, int KW,
+                   int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const int Ho = H + 2 * pad - KH + 1, Wo = W + 2 * pad - KW + 1, R = C * KH * KW;
+  TcPlan p = tc_plan(B, Ho, Wo, R, F);
+  const size_t a_off = 0, b_off = (p.a_bytes + 1023) & ~size_t(1023);
+  if (ws_bytes < b_off + p.b_bytes) return set_error(SNN_EWORKSPACE, "snn_conv_fire(tc): workspace too small");
+  uint8_t* aq = reinterpret_cast<uint8_t*>(ws) + a_off;
+  uint8_t* bq = reinterpret_cast<uint8_t*>(ws) + b_off;
+  {
+    const int64_t total = int64_t(p.nch) * p.N * p.Kp;
+    int64_t blocks = ceil_div(total, 256);
+    if (blocks > int64_t(num_sms()) * 8) blocks = int64_t(num_sms()) * 8;
+    tc_prep_b_kernel<<<int(blocks), 256, 0, s>>>(w, F, R, p, bq, error_word_ptr());
+    note_launch();
+  }
+  {
+    const int64_t rows16 = int64_t(p.Mt) * kTcM * (p.Kp / 16);
+    int64_t blocks = ceil_div(rows16, 256);
+    if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
+    tc_prep_a_kernel<<<int(blocks), 256, 0, s>>>(lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p, aq);
+    note_launch();
+  }
+  uint32_t cols = 32;
+  while (cols < uint32_t(p.N)) cols <<= 1;
+  const int smem = kTcStages * (kTcM * kTcKT + p.N * kTcKT) + 1024;
+  cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_conv_fire(tc): %s", cudaGetErrorString(e));
+  conv_tc_kernel<<<dim3(p.Mt, p.nch), kTcThreads, smem, s>>>(aq, bq, p, F, Ho * Wo, T, cols, lat_out, v_out);
+  note_launch();
+  return check_launch("snn_conv_fire(tc)");
+}
+
+}  // namespace snn

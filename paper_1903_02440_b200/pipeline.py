@@ -32,7 +32,7 @@ class Layer:
         F = spec.F
         self.lat = torch.empty((B, F, self.Ho, self.Wo), dtype=torch.uint8, device=device)
         self.v = torch.empty((B, F, self.Ho, self.Wo), dtype=torch.float32, device=device)
-        self.ws = torch.empty(snn.conv_fire_workspace(B, C, H, W, spec.pad, F, spec.KH, spec.KW, T),
+        self.ws = torch.empty(snn.conv_fire_workspace(B, C, H, W, spec.pad, F, spec.KH, spec.KW, T, spec.theta),
                               dtype=torch.uint8, device=device)
         self.pool_spec = pool_spec
         if pool_spec is not None:

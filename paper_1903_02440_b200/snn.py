@@ -48,7 +48,7 @@ def lib() -> C.CDLL:
                 "snn_encode": (i32, [p, i32, i32, i32, i32, i32, p, p, sz, p]),
                 "snn_expand": (i32, [p, i32, i32, i32, p, p]),
                 "snn_validate_lat": (i32, [p, sz, i32, p, p]),
-                "snn_conv_fire_workspace": (sz, [i32] * 9),
+                "snn_conv_fire_workspace": (sz, [i32] * 9 + [f32]),
                 "snn_conv_fire": (i32, [p, i32, i32, i32, i32, i32, p, i32, i32, i32, i32, f32, p, p, p, p, sz, p]),
                 "snn_pool": (i32, [p, p, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, p, p, p]),
                 "snn_inhibit": (i32, [p, p, i32, i32, i32, i32, p, p, p, p]),
@@ -156,8 +156,8 @@ def conv_out_hw(H, W, KH, KW, pad):
     return H + 2 * pad - KH + 1, W + 2 * pad - KW + 1
 
 
-def conv_fire_workspace(B, C_, H, W, pad, F, KH, KW, T) -> int:
-    return int(lib().snn_conv_fire_workspace(B, C_, H, W, pad, F, KH, KW, T))
+def conv_fire_workspace(B, C_, H, W, pad, F, KH, KW, T, theta) -> int:
+    return int(lib().snn_conv_fire_workspace(B, C_, H, W, pad, F, KH, KW, T, float(theta)))
 
 
 def conv_fire(lat_in: torch.Tensor, w: torch.Tensor, pad: int, T: int, theta: float, want_pot: bool = False,
@@ -176,7 +176,7 @@ def conv_fire(lat_in: torch.Tensor, w: torch.Tensor, pad: int, T: int, theta: fl
     lat = lat_out if lat_out is not None else torch.empty((B, F, Ho, Wo), dtype=torch.uint8, device=dev)
     v = v_out if v_out is not None else torch.empty((B, F, Ho, Wo), dtype=torch.float32, device=dev)
     pot = torch.empty((B, T, F, Ho, Wo), dtype=torch.float32, device=dev) if want_pot else None
-    n = conv_fire_workspace(B, C_, H, W, pad, F, KH, KW, T)
+    n = conv_fire_workspace(B, C_, H, W, pad, F, KH, KW, T, theta)
     buf = ws if ws is not None else _ws.get(n, dev, "conv")
     _check(lib().snn_conv_fire(_ptr(lat_in), B, C_, H, W, pad, _ptr(w), F, KH, KW, T, float(theta),
                                _ptr(lat), _ptr(v), _ptr(pot), _ptr(buf), buf.numel(), _stream(stream)))

@@ -41,8 +41,9 @@ def test_version_and_workspaces(L):
     assert L.snn_version() == 1
     assert L.snn_encode_workspace(1000, 6, 28, 28, 15) > 0
     assert L.snn_encode_workspace(1, 1, 1, 1, 0) == 0            # T out of range
-    assert L.snn_conv_fire_workspace(64, 32, 256, 256, 2, 256, 5, 5, 32) > 0
-    assert L.snn_conv_fire_workspace(1, 1, 4, 4, 0, 1, 5, 5, 3) == 0   # kernel larger than input
+    assert L.snn_conv_fire_workspace(64, 32, 256, 256, 2, 256, 5, 5, 32, 40.0) > 0
+    assert L.snn_conv_fire_workspace(1000, 250, 4, 4, 2, 200, 5, 5, 15, float('inf')) > 16000 * 6250
+    assert L.snn_conv_fire_workspace(1, 1, 4, 4, 0, 1, 5, 5, 3, 1.0) == 0   # kernel larger than input
     assert L.snn_k_winners_workspace(64, 256, 128, 128) >= 64 * 128 * 128 * 8
 
 
