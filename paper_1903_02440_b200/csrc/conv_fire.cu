@@ -387,6 +387,20 @@ static void make_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
 }
 
 size_t conv_tc_workspace(int B, int Ho, int Wo, int R, int F);
+size_t conv_walk_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T);
+int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
+                     int KW, int T, float theta, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes,
+                     cudaStream_t s);
+
+int weight_prep_launch(const float* w, int F, int R, int FGS, int n_groups, uint32_t* wq, cudaStream_t s) {
+  const int64_t total = int64_t(n_groups) * (R + 1) * FGS;
+  int blocks = int(ceil_div(total, 256));
+  if (blocks > 2048) blocks = 2048;
+  if (blocks < 1) blocks = 1;
+  weight_prep_kernel<<<blocks, 256, 0, s>>>(w, F, R, FGS, n_groups, wq);
+  note_launch();
+  return check_launch("snn_conv_fire(weight prep)");
+}
 int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH, int KW,
                    int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes, cudaStream_t s);
 
@@ -397,6 +411,9 @@ size_t conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, i
   size_t m = pl.wq_bytes;
   if (inf) {  // tensor-core path (and the SIMT dense path for validation mode)
     size_t t = conv_tc_workspace(B, pl.a.Ho, pl.a.Wo, pl.a.R, F);
+    m = m > t ? m : t;
+  } else {
+    size_t t = conv_walk_workspace(B, C, H, W, pad, F, KH, KW, T);
     m = m > t ? m : t;
   }
   return ((m + 255) & ~size_t(255)) + 256;
@@ -422,6 +439,10 @@ int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   if (npos == 0 || F == 0) return SNN_OK;
   if (inf && !pot_out)  // Eq. 5: dense contraction of S[T-1] on the tensor cores
     return conv_tc_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, lat_out, v_out, ws, ws_bytes, s);
+  if (!inf && !pot_out) {  // throughput kernel (conv_walk.cu); the kernel below is the validation path
+    int rc = conv_walk_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, theta, lat_out, v_out, ws, ws_bytes, s);
+    if (rc != 1) return rc;
+  }
   {
     int64_t total = int64_t(pl.n_groups) * (a.R + 1) * pl.FGS;
     int blocks = int(ceil_div(total, 256));
