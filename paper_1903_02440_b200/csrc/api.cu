@@ -195,6 +195,7 @@ int snn_k_winners(const uint8_t* lat, const float* v, int B, int F, int H, int W
   REQUIRE(r >= 0, SNN_EINVAL, "snn_k_winners: r < 0");
   REQUIRE(B >= 0 && F >= 0 && H >= 0 && W >= 0, SNN_ESHAPE, "snn_k_winners: bad dimensions");
   REQUIRE(int64_t(F) * H * W <= (int64_t(1) << 24), SNN_ESHAPE, "snn_k_winners: F*H*W > 2^24");
+  REQUIRE(F <= 8192, SNN_ESHAPE, "snn_k_winners: F > 8192");
   if (B == 0) return SNN_OK;
   REQUIRE(winners && count && (lat && v || int64_t(F) * H * W == 0), SNN_EINVAL, "snn_k_winners: NULL tensor");
   REQUIRE(ws, SNN_EWORKSPACE, "snn_k_winners: NULL workspace");

@@ -86,9 +86,13 @@ __global__ void tc_prep_a_kernel(const uint8_t* __restrict__ lat_in, int C, int 
                                  int Ho, int Wo, int T, TcPlan p, uint8_t* __restrict__ aq) {
   const int KK = KH * KW;
   const int64_t rows16 = int64_t(p.Mt) * kTcM * (p.Kp / 16);
+  const int nk16 = p.Kp / 16;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < rows16; i += int64_t(gridDim.x) * blockDim.x) {
-    const int k0 = int(i % (p.Kp / 16)) * 16;
-    const int m = int(i / (p.Kp / 16));
+    // 8 consecutive threads fill the 8 rows of one 128-byte core matrix (coalesced 16-byte stores)
+    const int r8 = int(i & 7);
+    const int64_t rest = i >> 3;
+    const int k0 = int(rest % nk16) * 16;
+    const int m = int(rest / nk16) * 8 + r8;
     uint32_t wv[4] = {0, 0, 0, 0};
     if (m < p.M) {
       const int HoWo = Ho * Wo;

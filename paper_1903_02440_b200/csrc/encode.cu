@@ -255,10 +255,180 @@ __global__ void __launch_bounds__(kEncThreads) enc_assign_kernel(const float* __
   }
 }
 
+// Small images (C*H*W <= 16384, e.g. C1-C3): one CTA per image runs the same radix select with
+// everything in shared memory -- the image's 31-bit value keys, a 4096-bin level-0 histogram, then
+// 8-bit digit levels with one 256-bin histogram per distinct unresolved cut prefix.  Levels: key bits
+// 54..43 (12), then 8, 8, 8, 8, 8 and the last 3 (the index part of the key included).
+constexpr int kSmLevels = 7;
+__constant__ int c_sm_bits[kSmLevels] = {12, 8, 8, 8, 8, 8, 3};
+__constant__ int c_sm_shift[kSmLevels] = {43, 35, 27, 19, 11, 3, 0};
+constexpr int kSmThreads = 512;
+
+__device__ __forceinline__ uint64_t sm_key(uint32_t vk, int i) { return (uint64_t(vk) << 24) | uint32_t(i); }
+
+__global__ void __launch_bounds__(kSmThreads) enc_small_kernel(const float* __restrict__ x, int n, int T,
+                                                                uint8_t* __restrict__ lat) {
+  extern __shared__ uint32_t vk[];              // [n] 0x7FFFFFFF - bits(x), or ~0 for x <= 0
+  __shared__ uint32_t hist[4096];               // level 0: 4096 bins; later: slot * 256 + digit
+  __shared__ uint32_t slot_tot[16];
+  __shared__ uint64_t cut_prefix[256], slot_prefix[256];
+  __shared__ int cut_shift[256], cut_slot[256];
+  __shared__ uint32_t cut_resid[256];
+  __shared__ int s_nslots, s_N;
+  __shared__ uint32_t wsum[kSmThreads / 32];
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const float* xb = x + int64_t(b) * n;
+  uint8_t* lb = lat + int64_t(b) * n;
+  const int NC = T - 1;
+  for (int i = tid; i < 4096; i += kSmThreads) hist[i] = 0;
+  __syncthreads();
+  // ---- level 0: load keys, histogram of the top 12 bits ----
+  for (int i0 = 0; i0 < n; i0 += kSmThreads) {
+    const int i = i0 + tid;
+    bool pos = false;
+    uint32_t d = 0;
+    if (i < n) {
+      const float v = xb[i];
+      pos = v > 0.0f;
+      const uint32_t k = pos ? 0x7FFFFFFFu - __float_as_uint(v) : 0xFFFFFFFFu;
+      vk[i] = k;
+      if (pos) d = uint32_t(sm_key(k, i) >> 43);
+    }
+    const unsigned act = __ballot_sync(0xffffffffu, pos);
+    if (pos) {
+      const unsigned peers = __match_any_sync(act, d);
+      if (lane == __ffs(peers) - 1) atomicAdd(&hist[d], uint32_t(__popc(peers)));
+    }
+  }
+  __syncthreads();
+  {  // exclusive scan of 4096 bins (8 per thread) in place; N = total
+    uint32_t loc[8], run = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { loc[j] = hist[tid * 8 + j]; run += loc[j]; }
+    uint32_t inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    uint32_t base = 0, tot = 0;
+    for (int w = 0; w < kSmThreads / 32; ++w) { if (w < wid) base += wsum[w]; tot += wsum[w]; }
+    uint32_t e = base + inc - run;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { hist[tid * 8 + j] = e; e += loc[j]; }
+    if (tid == 0) s_N = int(tot);
+  }
+  __syncthreads();
+  const uint32_t N = uint32_t(s_N);
+  const uint32_t q = N / uint32_t(T), m = N % uint32_t(T);
+  for (int c = tid; c < NC; c += kSmThreads) {
+    const uint32_t bb = uint32_t(c + 1), start = bb * q + (bb < m ? bb : m);
+    if (start >= N) { cut_shift[c] = -1; cut_slot[c] = -1; continue; }
+    int lo = 0, hi = 4095;  // largest d with cum[d] <= start
+    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (hist[mid] <= start) lo = mid; else hi = mid - 1; }
+    const uint32_t next = lo == 4095 ? N : hist[lo + 1];
+    cut_prefix[c] = uint64_t(lo);
+    cut_resid[c] = start - hist[lo];
+    if (next - hist[lo] == 1) { cut_shift[c] = 43; cut_slot[c] = -1; }
+    else { cut_shift[c] = -2; cut_slot[c] = -3; }
+  }
+  __syncthreads();
+  // ---- levels 1..6 (a level is repeated while more than 16 distinct prefixes are pending) ----
+  for (int L = 1; L < kSmLevels;) {
+    if (tid == 0) {  // distinct prefixes of unresolved cuts (sorted, since cuts are in rank order)
+      int ns = 0;
+      for (int c = 0; c < NC; ++c) {
+        if (cut_slot[c] != -3) continue;
+        if (ns == 0 || slot_prefix[ns - 1] != cut_prefix[c]) slot_prefix[ns++] = cut_prefix[c];
+        cut_slot[c] = ns - 1 + 1000;  // tagged: slot index + 1000
+      }
+      s_nslots = ns;
+    }
+    __syncthreads();
+    const int ns = s_nslots;
+    if (ns == 0) break;
+    const int nsl = ns < 16 ? ns : 16;
+    for (int i = tid; i < nsl * 256; i += kSmThreads) hist[i] = 0;
+    __syncthreads();
+    const int shp = c_sm_shift[L - 1], sh = c_sm_shift[L];
+    const uint32_t mask = (1u << c_sm_bits[L]) - 1u;
+    for (int i = tid; i < n; i += kSmThreads) {
+      const uint32_t k32 = vk[i];
+      if (k32 == 0xFFFFFFFFu) continue;
+      const uint64_t K = sm_key(k32, i), pfx = K >> shp;
+      int lo = 0, hi = nsl;
+      while (lo < hi) { const int mid = (lo + hi) >> 1; if (slot_prefix[mid] < pfx) lo = mid + 1; else hi = mid; }
+      if (lo < nsl && slot_prefix[lo] == pfx) atomicAdd(&hist[lo * 256 + uint32_t((K >> sh) & mask)], 1u);
+    }
+    __syncthreads();
+    for (int sl = wid; sl < nsl; sl += kSmThreads / 32) {  // per-slot exclusive scan, one warp per slot
+      uint32_t loc[8], run = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { loc[j] = hist[sl * 256 + lane * 8 + j]; run += loc[j]; }
+      uint32_t inc = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      uint32_t e = inc - run;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { hist[sl * 256 + lane * 8 + j] = e; e += loc[j]; }
+      if (lane == 31) slot_tot[sl] = inc;
+    }
+    __syncthreads();
+    for (int c = tid; c < NC; c += kSmThreads) {
+      if (cut_slot[c] < 1000) continue;
+      const int sl = cut_slot[c] - 1000;
+      if (sl >= nsl) { cut_slot[c] = -3; continue; }  // beyond the first 16 prefixes: repeat the level
+      const uint32_t* h = hist + sl * 256;
+      const uint32_t r = cut_resid[c];
+      int lo = 0, hi = 255;
+      while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (h[mid] <= r) lo = mid; else hi = mid - 1; }
+      const uint32_t next = lo == 255 ? slot_tot[sl] : h[lo + 1];
+      cut_prefix[c] = (cut_prefix[c] << c_sm_bits[L]) | uint64_t(lo);
+      cut_resid[c] = r - h[lo];
+      if (next - h[lo] == 1 || L == kSmLevels - 1) { cut_shift[c] = c_sm_shift[L]; cut_slot[c] = -1; }
+      else cut_slot[c] = -4;  // descends to the next level
+    }
+    __syncthreads();
+    if (nsl == ns) {  // every pending prefix was handled at this level: advance
+      for (int c = tid; c < NC; c += kSmThreads)
+        if (cut_slot[c] == -4) cut_slot[c] = -3;
+      ++L;
+    }
+    __syncthreads();
+  }
+  // ---- assign: lat = number of cuts whose prefix the key reaches ----
+  for (int i = tid; i < n; i += kSmThreads) {
+    const uint32_t k32 = vk[i];
+    if (k32 == 0xFFFFFFFFu) { lb[i] = kNoSpike; continue; }
+    const uint64_t K = sm_key(k32, i);
+    int lo = 0, hi = NC;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const bool pass = cut_shift[mid] >= 0 && (K >> cut_shift[mid]) >= cut_prefix[mid];
+      if (pass) lo = mid + 1; else hi = mid;
+    }
+    lb[i] = uint8_t(lo);
+  }
+}
+
 int encode_launch(const float* x, int B, int C, int H, int W, int T, uint8_t* lat, void* wsp,
                   size_t ws_bytes, cudaStream_t s) {
   int64_t n = int64_t(C) * H * W;
   if (B == 0 || n == 0) return SNN_OK;
+  if (n <= 16384) {
+    const size_t smem = size_t(n) * sizeof(uint32_t);
+    cudaError_t e = cudaFuncSetAttribute(enc_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_encode: %s", cudaGetErrorString(e));
+    enc_small_kernel<<<B, kSmThreads, smem, s>>>(x, int(n), T, lat);
+    note_launch();
+    return check_launch("snn_encode(small)");
+  }
   int G = encode_group(B, T);
   EncodeWS ws;
   size_t need = encode_ws_layout(G, T, &ws, (char*)wsp);

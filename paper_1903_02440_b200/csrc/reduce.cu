@@ -99,17 +99,31 @@ int inhibit_launch(const uint8_t* lat, const float* v, int B, int F, int H, int 
 
 // ------------------------------------------------------------------------------------- a6 k-WTA
 // Stage 1 (all SMs): best key over features for every position -> pos_best[b][p].
+// 32-bit indexing (F*H*W <= 2^24 is checked at the ABI), 4 features in flight per thread.
 __global__ void __launch_bounds__(256) kwta_posbest_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
-                                                           int B, int F, int64_t HW, uint64_t* __restrict__ pos_best) {
+                                                           int B, int F, int HW, uint64_t* __restrict__ pos_best) {
   const int64_t total = int64_t(B) * HW;
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < total; q += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t b = q / HW, p = q - b * HW;
-    const int64_t base = b * F * HW + p;
+    const int b = int(q / HW), p = int(q - int64_t(b) * HW);
+    const uint8_t* lp = lat + int64_t(b) * F * HW + p;
+    const float* vp = v + int64_t(b) * F * HW + p;
     uint64_t best = ~uint64_t(0);
-    for (int f = 0; f < F; ++f) {
-      const uint8_t l = lat[base + int64_t(f) * HW];
+    int f = 0;
+    for (; f + 4 <= F; f += 4) {
+      uint8_t l[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) l[u] = lp[(f + u) * HW];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (l[u] == kNoSpike) continue;
+        const uint64_t k = wta_key(l[u], vp[(f + u) * HW], uint32_t((f + u) * HW + p));
+        best = k < best ? k : best;
+      }
+    }
+    for (; f < F; ++f) {
+      const uint8_t l = lp[f * HW];
       if (l == kNoSpike) continue;
-      const uint64_t k = wta_key(l, v[base + int64_t(f) * HW], uint32_t(int64_t(f) * HW + p));
+      const uint64_t k = wta_key(l, vp[f * HW], uint32_t(f * HW + p));
       best = k < best ? k : best;
     }
     pos_best[q] = best;
@@ -118,47 +132,53 @@ __global__ void __launch_bounds__(256) kwta_posbest_kernel(const uint8_t* __rest
 
 // Stage 2 (one CTA per image): k rounds of a block argmin over positions.  A position inside the
 // radius of a previous winner is skipped (inhibited in all maps); a position whose best feature has
-// been excluded is re-evaluated over the remaining features and its key written back.
+// been excluded is re-evaluated over the remaining features and its key written back.  The per-image
+// key map is staged in shared memory when it fits (<= 16384 positions).
 constexpr int kKwtaThreads = 1024;
 constexpr int kMaxK = 256;
+constexpr int kKwtaSmemPos = 16384;
 
 __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t* __restrict__ lat,
                                                                    const float* __restrict__ v, int F, int H, int W,
                                                                    int k, int r, uint64_t* __restrict__ pos_best,
                                                                    int32_t* __restrict__ winners,
-                                                                   int32_t* __restrict__ count) {
-  extern __shared__ uint32_t fexcl[];  // bitmask of excluded features
+                                                                   int32_t* __restrict__ count, int use_smem) {
+  extern __shared__ uint64_t dyn[];
+  __shared__ uint32_t fexcl[256];  // bitmask of excluded features (F <= 8192)
   __shared__ int wy[kMaxK], wx[kMaxK];
   __shared__ uint64_t red[32];
   __shared__ int s_count;
   const int b = blockIdx.x;
-  const int64_t HW = int64_t(H) * W;
-  uint64_t* pb = pos_best + int64_t(b) * HW;
+  const int HW = H * W;
+  uint64_t* pbg = pos_best + int64_t(b) * HW;
+  uint64_t* pb = use_smem ? dyn : pbg;
   const uint8_t* lb = lat + int64_t(b) * F * HW;
   const float* vb = v + int64_t(b) * F * HW;
   const int nwords = (F + 31) >> 5;
   for (int i = threadIdx.x; i < nwords; i += blockDim.x) fexcl[i] = 0;
+  if (use_smem)
+    for (int p = threadIdx.x; p < HW; p += blockDim.x) dyn[p] = pbg[p];
   if (threadIdx.x == 0) s_count = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int round = 0; round < k; ++round) {
     const int nw = s_count;
     uint64_t best = ~uint64_t(0);
-    for (int64_t p = threadIdx.x; p < HW; p += blockDim.x) {
+    for (int p = threadIdx.x; p < HW; p += blockDim.x) {
       uint64_t key = pb[p];
       if (key == ~uint64_t(0)) continue;
-      const int y = int(p / W), x = int(p - int64_t(p / W) * W);
+      const int y = p / W, x = p - (p / W) * W;
       bool near = false;
       for (int i = 0; i < nw; ++i) near |= (abs(y - wy[i]) <= r) && (abs(x - wx[i]) <= r);
       if (near) continue;
-      int f = int((key & 0xFFFFFFu) / uint64_t(HW));
+      const int f = int(uint32_t(key & 0xFFFFFFu) / uint32_t(HW));
       if (fexcl[f >> 5] >> (f & 31) & 1) {  // best feature already won: re-evaluate this position
         key = ~uint64_t(0);
         for (int ff = 0; ff < F; ++ff) {
           if (fexcl[ff >> 5] >> (ff & 31) & 1) continue;
-          const uint8_t l = lb[int64_t(ff) * HW + p];
+          const uint8_t l = lb[ff * HW + p];
           if (l == kNoSpike) continue;
-          const uint64_t kk = wta_key(l, vb[int64_t(ff) * HW + p], uint32_t(int64_t(ff) * HW + p));
+          const uint64_t kk = wta_key(l, vb[ff * HW + p], uint32_t(ff * HW + p));
           key = kk < key ? kk : key;
         }
         pb[p] = key;
@@ -171,20 +191,17 @@ __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t
     if (wid == 0) {
       uint64_t x = lane < (blockDim.x >> 5) ? red[lane] : ~uint64_t(0);
       x = warp_min_u64(x);
-      if (lane == 0) {
-        if (x != ~uint64_t(0)) {
-          const int64_t idx = int64_t(x & 0xFFFFFFu);
-          const int f = int(idx / HW);
-          const int64_t p = idx - int64_t(f) * HW;
-          const int y = int(p / W), xx = int(p - int64_t(y) * W);
-          const int c = s_count;
-          winners[(int64_t(b) * k + c) * 3 + 0] = f;
-          winners[(int64_t(b) * k + c) * 3 + 1] = y;
-          winners[(int64_t(b) * k + c) * 3 + 2] = xx;
-          wy[c] = y; wx[c] = xx;
-          fexcl[f >> 5] |= 1u << (f & 31);
-          s_count = c + 1;
-        }
+      if (lane == 0 && x != ~uint64_t(0)) {
+        const int idx = int(x & 0xFFFFFFu);
+        const int f = idx / HW, p = idx - f * HW;
+        const int y = p / W, xx = p - y * W;
+        const int c = s_count;
+        winners[(int64_t(b) * k + c) * 3 + 0] = f;
+        winners[(int64_t(b) * k + c) * 3 + 1] = y;
+        winners[(int64_t(b) * k + c) * 3 + 2] = xx;
+        wy[c] = y; wx[c] = xx;
+        fexcl[f >> 5] |= 1u << (f & 31);
+        s_count = c + 1;
       }
     }
     __syncthreads();
@@ -214,10 +231,13 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
   int64_t blocks = ceil_div(total, 256);
   if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
   if (blocks < 1) blocks = 1;
-  kwta_posbest_kernel<<<int(blocks), 256, 0, s>>>(lat, v, B, F, HW, pb);
+  kwta_posbest_kernel<<<int(blocks), 256, 0, s>>>(lat, v, B, F, int(HW), pb);
   note_launch();
-  const int nwords = (F + 31) >> 5;
-  kwta_rounds_kernel<<<B, kKwtaThreads, nwords * 4, s>>>(lat, v, F, H, W, k, r, pb, winners, count);
+  const int use_smem = HW <= kKwtaSmemPos;
+  const size_t smem = use_smem ? size_t(HW) * sizeof(uint64_t) : 0;
+  cudaError_t e = cudaFuncSetAttribute(kwta_rounds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_k_winners: %s", cudaGetErrorString(e));
+  kwta_rounds_kernel<<<B, kKwtaThreads, smem, s>>>(lat, v, F, H, W, k, r, pb, winners, count, use_smem);
   note_launch();
   return check_launch("snn_k_winners");
 }

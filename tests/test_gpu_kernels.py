@@ -53,6 +53,15 @@ def test_encode_random(G, orc, shape, T, seed):
     assert np.array_equal(got, orc.encode(x, T))
 
 
+@pytest.mark.parametrize("shape,T,seed", [((2, 3, 100, 70), 254, 6), ((3, 2, 129, 64), 32, 7), ((1, 1, 1, 16385), 15, 8)])
+def test_encode_large_path(G, orc, shape, T, seed):
+    """C*H*W > 16384 takes the multi-kernel radix-select path."""
+    rng = np.random.default_rng(seed)
+    x = (rng.integers(0, 50, size=shape) / 49).astype(np.float32)      # heavy ties
+    x[rng.random(shape) < 0.2] = 0
+    assert np.array_equal(host(G.encode(cu(x), T)), orc.encode(x, T))
+
+
 def test_encode_all_equal_and_zero(G, orc):
     x = np.full((2, 3, 20, 20), 0.25, np.float32)
     x[1] = 0
