@@ -246,7 +246,150 @@ class C5Step(C2Step):
                                 self.wl.extra))
 
 
-WORKLOADS = {"c2": C2Step, "c5": C5Step}
+class SeqBase(C2Step):
+    """Sequential plasticity configs: a batched fixed-weight prefix, then a CUDA graph of per-image
+    plasticity steps (conv+fire -> [inhibit] -> kWTA -> [decide] -> STDP), no host sync per image."""
+
+    def _prefix(self):
+        snn, T = self.snn, self.wl.T
+        snn.encode(self.x, T, out=self.lat0, ws=self.ws_enc)
+        if self.l1 is not None:
+            self.l1(self.lat0)
+
+    def run(self, ev=None):
+        def mark(i):
+            if ev is not None:
+                ev[i].record()
+        mark(0)
+        self._prefix(); mark(1)
+        self.graph.replay(); mark(2)
+
+    def e2e(self, x_host, out_host):
+        self.x.copy_(x_host, non_blocking=True)
+        self.run()
+        out_host.copy_(self.seq.w, non_blocking=True)
+
+    def host_io(self):
+        xh = self.torch.from_numpy(self.wl.X).pin_memory()
+        oh = self.torch.empty(tuple(self.seq.w.shape), dtype=self.torch.float32).pin_memory()
+        return xh, oh
+
+    def events(self):
+        self.run()
+        s = self.wl.convs[-1]
+        lat_in = self.l1.plat if self.l1 is not None else self.lat0
+        return {"seq": self.snn.count_events(lat_in, s.F, s.KH, s.KW, s.pad, self.wl.T, None)}
+
+
+class C3Step(SeqBase):
+    name = "c3"
+
+    def __init__(self, torch, dev, batch=2000):
+        import synth
+        from paper_1903_02440_b200 import pipeline, snn
+        self.torch, self.snn = torch, snn
+        self.wl = wl = synth.C3(n=batch)
+        self.B = batch
+        self.x = torch.from_numpy(wl.X).to(dev)
+        _, C, H, W = wl.X.shape
+        self.ws_enc = torch.empty(snn.encode_workspace(batch, C, H, W, wl.T), dtype=torch.uint8, device=dev)
+        self.lat0 = torch.empty(wl.X.shape, dtype=torch.uint8, device=dev)
+        self.l1 = pipeline.Layer(wl.convs[0], torch.from_numpy(wl.weights[0]).to(dev), batch, C, H, W, wl.T,
+                                 wl.pools[0], pool_v=False, device=dev)
+        self.seq = pipeline.SeqSTDP(wl.convs[1], wl.weights[1], wl.convs[0].F, self.l1.PHo, self.l1.PWo, wl.T,
+                                    wl.extra["k"], wl.extra["r"], True, wl.extra["stdp"], device=dev)
+        self._prefix()
+        self.graph = pipeline.SeqGraph(self.seq, self.l1.plat, batch, snapshot_every=wl.extra["snapshot_every"])
+        self.stages = ["l1_prefix", "seq_stdp"]
+
+    def config(self):
+        return {"workload": "c3: BASELINE.json configs[2], sequential STDP on layer 2, 2000 images",
+                "global_batch": self.B, "layers": "C2 L1 (fixed) -> pool -> L2 F250 3x3 th10 -> inhibit -> kWTA k8 r2 -> STDP",
+                "plasticity": "per-image CUDA graph, no host sync", "l2": "flushed between timed steps"}
+
+    def oracle_step(self, n):
+        from oracle import flows
+        import synth
+        flows.c3(synth.Workload("c3", self.wl.T, self.wl.X[:n], self.wl.convs, self.wl.weights, self.wl.pools,
+                                self.wl.extra), snapshot_every=10 ** 9)
+
+
+class C4Step(SeqBase):
+    name = "c4"
+
+    def __init__(self, torch, dev, batch=1000):
+        import synth
+        from paper_1903_02440_b200 import pipeline, snn
+        self.torch, self.snn = torch, snn
+        self.wl = wl = synth.C4(n=batch)
+        self.B = batch
+        self.x = torch.from_numpy(wl.X).to(dev)
+        _, C, H, W = wl.X.shape
+        self.ws_enc = torch.empty(snn.encode_workspace(batch, C, H, W, wl.T), dtype=torch.uint8, device=dev)
+        self.lat0 = torch.empty(wl.X.shape, dtype=torch.uint8, device=dev)
+        self.l1 = pipeline.Layer(wl.convs[0], torch.from_numpy(wl.weights[0]).to(dev), batch, C, H, W, wl.T,
+                                 wl.pools[0], pool_v=False, device=dev)
+        self.seq = pipeline.SeqSTDP(wl.convs[1], wl.weights[1], wl.convs[0].F, self.l1.PHo, self.l1.PWo, wl.T,
+                                    1, 0, False, wl.extra["stdp"], n_classes=wl.extra["n_classes"], device=dev)
+        self.labels = torch.from_numpy(wl.extra["labels"].astype(np.int32)).to(dev)
+        self._prefix()
+        self.graph = pipeline.SeqGraph(self.seq, self.l1.plat, batch, labels=self.labels)
+        self.stages = ["l1_prefix", "seq_rstdp"]
+
+    def config(self):
+        return {"workload": "c4: BASELINE.json configs[3], Caltech-shaped R-STDP, 1000 sequential images, T=30",
+                "global_batch": self.B,
+                "layers": "F20 5x5 th15 (4x160x250) -> pool7/6 -> F100 17x17 th=inf (tcgen05) -> 1 winner -> decide -> R-STDP",
+                "plasticity": "per-image CUDA graph, reward decided on device", "l2": "flushed between timed steps"}
+
+    def oracle_step(self, n):
+        from oracle import flows
+        import synth
+        ex = dict(self.wl.extra)
+        flows.c4(synth.Workload("c4", self.wl.T, self.wl.X[:n], self.wl.convs, self.wl.weights, self.wl.pools, ex))
+
+
+class C1Step(SeqBase):
+    name = "c1"
+
+    def __init__(self, torch, dev, batch=1):
+        import synth
+        from paper_1903_02440_b200 import pipeline, snn
+        self.torch, self.snn = torch, snn
+        self.wl = wl = synth.C1()
+        self.B = 1
+        self.x = torch.from_numpy(wl.X).to(dev)
+        self.ws_enc = torch.empty(snn.encode_workspace(1, 2, 28, 28, wl.T), dtype=torch.uint8, device=dev)
+        self.lat0 = torch.empty(wl.X.shape, dtype=torch.uint8, device=dev)
+        self.l1 = None
+        self.seq = pipeline.SeqSTDP(wl.convs[0], wl.weights[0], 2, 28, 28, wl.T, wl.extra["k"], wl.extra["r"], True,
+                                    wl.extra["stdp"], device=dev)
+        w0 = self.seq.w.clone()
+
+        def body():
+            self.seq.w.copy_(w0)
+            self._prefix()
+            self.seq.step(self.lat0)
+        self.graph = pipeline.StepGraph(body)
+        self.stages = ["step"]
+
+    def run(self, ev=None):
+        if ev is not None:
+            ev[0].record()
+        self.graph.replay()
+        if ev is not None:
+            ev[1].record()
+
+    def config(self):
+        return {"workload": "c1: BASELINE.json configs[0], single layer, batch 1: encode -> conv+fire -> inhibit -> kWTA k5 r3 -> STDP",
+                "global_batch": 1, "plasticity": "whole step as one CUDA graph", "l2": "flushed between timed steps"}
+
+    def oracle_step(self, n):
+        from oracle import flows
+        flows.c1(self.wl)
+
+
+WORKLOADS = {"c1": C1Step, "c2": C2Step, "c3": C3Step, "c4": C4Step, "c5": C5Step}
 
 
 # --------------------------------------------------------------------------------------- roofline
@@ -272,6 +415,10 @@ def roofline(stage, t_ms, ev, wl, clocks, pk):
                 "frac": round(ach / peak, 4), "traffic": None, "kernel": stage,
                 "work": f"{need} necessary events x 4 B weight gather (of {paper} paper-definition events)",
                 "peak_src": f"128 B/clk/SM x 148 SMs x {f_mhz:.0f} MHz (measured SM clock)"}
+    if stage.startswith("seq") or stage == "step":
+        return {"bound": "latency", "achieved": round(t_ms * 1e3 / max(1, wl.X.shape[0]), 3), "peak": None,
+                "unit": "us/image", "frac": None, "traffic": None, "kernel": stage,
+                "work": "sequential per-image plasticity chain (each image's weights feed the next, P:95)"}
     return None
 
 
@@ -282,9 +429,10 @@ def run_reference(args, rank):
     import synth  # noqa: F401
     import torch
     step = WORKLOADS[args.workload].__new__(WORKLOADS[args.workload])
-    step.wl = {"c2": lambda: synth.C2(n=1000), "c5": lambda: synth.C5(n=2)}[args.workload]()
+    step.wl = {"c1": synth.C1, "c2": lambda: synth.C2(n=1000), "c3": lambda: synth.C3(n=200),
+               "c4": lambda: synth.C4(n=20), "c5": lambda: synth.C5(n=2)}[args.workload]()
     step.B = step.wl.X.shape[0]
-    sample = {"c2": 100, "c5": 1}[args.workload]
+    sample = {"c1": 1, "c2": 100, "c3": 20, "c4": 5, "c5": 1}[args.workload]
     for _ in range(args.warmup):
         step.oracle_step(sample)
     t0 = time.perf_counter()
@@ -337,6 +485,8 @@ def run_ours(args, rank, world, local):
             flush.zero_()
         step.run(ev[k])
     launches = snn.launch_count() - launches0
+    if getattr(step, "graph", None) is not None:      # kernels replayed from a captured CUDA graph
+        launches += args.steps * step.graph.launches
     torch.cuda.synchronize()
     barrier()
     clocks = sampler.stop() if sampler else None
@@ -381,7 +531,7 @@ def run_ours(args, rank, world, local):
     roof = roofline(step.stages[dom], stage_ms[dom], ev_counts, step.wl, clocks, pk)
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
-        n = {"c2": 1000, "c5": 1}[step.name]
+        n = {"c1": 1, "c2": 1000, "c3": 200, "c4": 30, "c5": 1}[step.name]
         t0 = time.perf_counter()
         step.oracle_step(n)
         dt = time.perf_counter() - t0

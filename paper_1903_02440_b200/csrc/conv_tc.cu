@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
   __shared__ __align__(8) uint64_t full_bar[kTcStages], empty_bar[kTcStages], done_bar;
   __shared__ uint32_t tmem_base_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt = blockIdx.x, ch = blockIdx.y;
+  const int ch = blockIdx.x, mt = blockIdx.y;  // N chunks fastest: CTAs sharing an A tile run together
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTcStages; ++s) {
@@ -294,7 +294,7 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
   const int smem = kTcStages * (kTcM * kTcKT + p.N * kTcKT) + 1024;
   cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_conv_fire(tc): %s", cudaGetErrorString(e));
-  conv_tc_kernel<<<dim3(p.Mt, p.nch), kTcThreads, smem, s>>>(aq, bq, p, F, Ho * Wo, T, cols, lat_out, v_out);
+  conv_tc_kernel<<<dim3(p.nch, p.Mt), kTcThreads, smem, s>>>(aq, bq, p, F, Ho * Wo, T, cols, lat_out, v_out);
   note_launch();
   return check_launch("snn_conv_fire(tc)");
 }

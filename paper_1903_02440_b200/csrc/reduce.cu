@@ -86,10 +86,47 @@ __global__ void __launch_bounds__(256) inhibit_kernel(const uint8_t* __restrict_
   }
 }
 
+// Small maps (batch-1 plasticity steps): one warp per position, lanes over features, so the
+// per-position latency is one round of loads instead of F dependent ones.
+constexpr int64_t kWarpPerPosMax = 16384;
+
+__global__ void __launch_bounds__(256) inhibit_warp_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
+                                                           int B, int F, int64_t HW, uint8_t* __restrict__ lat_out,
+                                                           float* __restrict__ v_out, int16_t* __restrict__ winner_f) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = int64_t(B) * HW;
+  for (int64_t q = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; q < total;
+       q += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t b = q / HW, p = q - b * HW;
+    const int64_t base = b * F * HW + p;
+    uint64_t best = ~uint64_t(0);
+    for (int f = lane; f < F; f += 32) {
+      const uint8_t l = lat[base + int64_t(f) * HW];
+      if (l == kNoSpike) continue;
+      const uint64_t k = wta_key(l, v[base + int64_t(f) * HW], uint32_t(f));
+      best = k < best ? k : best;
+    }
+    best = warp_min_u64(best);
+    const int fw = best == ~uint64_t(0) ? -1 : int(best & 0xFFFFFFu);
+    for (int f = lane; f < F; f += 32) {
+      const int64_t i = base + int64_t(f) * HW;
+      const bool keep = f == fw;
+      lat_out[i] = keep ? lat[i] : kNoSpike;
+      v_out[i] = keep ? v[i] : 0.0f;
+    }
+    if (winner_f && lane == 0) winner_f[q] = int16_t(fw);
+  }
+}
+
 int inhibit_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, uint8_t* lat_out, float* v_out,
                    int16_t* winner_f, cudaStream_t s) {
   const int64_t HW = int64_t(H) * W, total = int64_t(B) * HW;
   if (total == 0) return SNN_OK;
+  if (total <= kWarpPerPosMax) {
+    inhibit_warp_kernel<<<int(ceil_div(total, 8)), 256, 0, s>>>(lat, v, B, F, HW, lat_out, v_out, winner_f);
+    note_launch();
+    return check_launch("snn_inhibit");
+  }
   int64_t blocks = ceil_div(total, 256);
   if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
   inhibit_kernel<<<int(blocks), 256, 0, s>>>(lat, v, B, F, HW, lat_out, v_out, winner_f);
@@ -130,6 +167,28 @@ __global__ void __launch_bounds__(256) kwta_posbest_kernel(const uint8_t* __rest
   }
 }
 
+__global__ void __launch_bounds__(256) kwta_posbest_warp_kernel(const uint8_t* __restrict__ lat,
+                                                                const float* __restrict__ v, int B, int F, int HW,
+                                                                uint64_t* __restrict__ pos_best) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = int64_t(B) * HW;
+  for (int64_t q = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; q < total;
+       q += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    const int b = int(q / HW), p = int(q - int64_t(b) * HW);
+    const uint8_t* lp = lat + int64_t(b) * F * HW + p;
+    const float* vp = v + int64_t(b) * F * HW + p;
+    uint64_t best = ~uint64_t(0);
+    for (int f = lane; f < F; f += 32) {
+      const uint8_t l = lp[f * HW];
+      if (l == kNoSpike) continue;
+      const uint64_t k = wta_key(l, vp[f * HW], uint32_t(f * HW + p));
+      best = k < best ? k : best;
+    }
+    best = warp_min_u64(best);
+    if (lane == 0) pos_best[q] = best;
+  }
+}
+
 // Stage 2 (one CTA per image): k rounds of a block argmin over positions.  A position inside the
 // radius of a previous winner is skipped (inhibited in all maps); a position whose best feature has
 // been excluded is re-evaluated over the remaining features and its key written back.  The per-image
@@ -137,6 +196,7 @@ __global__ void __launch_bounds__(256) kwta_posbest_kernel(const uint8_t* __rest
 constexpr int kKwtaThreads = 1024;
 constexpr int kMaxK = 256;
 constexpr int kKwtaSmemPos = 16384;
+constexpr int kKwtaQueue = 4096;
 
 __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t* __restrict__ lat,
                                                                    const float* __restrict__ v, int F, int H, int W,
@@ -147,7 +207,8 @@ __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t
   __shared__ uint32_t fexcl[256];  // bitmask of excluded features (F <= 8192)
   __shared__ int wy[kMaxK], wx[kMaxK];
   __shared__ uint64_t red[32];
-  __shared__ int s_count;
+  __shared__ int s_count, s_qn;
+  __shared__ int queue[kKwtaQueue];
   const int b = blockIdx.x;
   const int HW = H * W;
   uint64_t* pbg = pos_best + int64_t(b) * HW;
@@ -164,26 +225,52 @@ __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t
   for (int round = 0; round < k; ++round) {
     const int nw = s_count;
     uint64_t best = ~uint64_t(0);
+    if (threadIdx.x == 0) s_qn = 0;
+    __syncthreads();
     for (int p = threadIdx.x; p < HW; p += blockDim.x) {
-      uint64_t key = pb[p];
+      const uint64_t key = pb[p];
       if (key == ~uint64_t(0)) continue;
       const int y = p / W, x = p - (p / W) * W;
       bool near = false;
       for (int i = 0; i < nw; ++i) near |= (abs(y - wy[i]) <= r) && (abs(x - wx[i]) <= r);
       if (near) continue;
       const int f = int(uint32_t(key & 0xFFFFFFu) / uint32_t(HW));
-      if (fexcl[f >> 5] >> (f & 31) & 1) {  // best feature already won: re-evaluate this position
-        key = ~uint64_t(0);
-        for (int ff = 0; ff < F; ++ff) {
+      if (fexcl[f >> 5] >> (f & 31) & 1) {  // its best feature already won: re-evaluate below
+        const int slot = atomicAdd(&s_qn, 1);
+        if (slot < kKwtaQueue) queue[slot] = p;
+        else {  // queue overflow (rare): serial re-evaluation by this thread
+          uint64_t kk2 = ~uint64_t(0);
+          for (int ff = 0; ff < F; ++ff) {
+            if (fexcl[ff >> 5] >> (ff & 31) & 1) continue;
+            const uint8_t l = lb[ff * HW + p];
+            if (l == kNoSpike) continue;
+            const uint64_t kk = wta_key(l, vb[ff * HW + p], uint32_t(ff * HW + p));
+            kk2 = kk < kk2 ? kk : kk2;
+          }
+          pb[p] = kk2;
+          best = kk2 < best ? kk2 : best;
+        }
+        continue;
+      }
+      best = key < best ? key : best;
+    }
+    __syncthreads();
+    {  // one warp per queued position: lanes scan the features, warp-min, write the key back
+      const int qn = s_qn < kKwtaQueue ? s_qn : kKwtaQueue;
+      for (int qi = wid; qi < qn; qi += (blockDim.x >> 5)) {
+        const int p = queue[qi];
+        uint64_t key = ~uint64_t(0);
+        for (int ff = lane; ff < F; ff += 32) {
           if (fexcl[ff >> 5] >> (ff & 31) & 1) continue;
           const uint8_t l = lb[ff * HW + p];
           if (l == kNoSpike) continue;
           const uint64_t kk = wta_key(l, vb[ff * HW + p], uint32_t(ff * HW + p));
           key = kk < key ? kk : key;
         }
-        pb[p] = key;
+        key = warp_min_u64(key);
+        if (lane == 0) pb[p] = key;
+        best = key < best ? key : best;
       }
-      best = key < best ? key : best;
     }
     best = warp_min_u64(best);
     if (lane == 0) red[wid] = best;
@@ -231,7 +318,10 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
   int64_t blocks = ceil_div(total, 256);
   if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
   if (blocks < 1) blocks = 1;
-  kwta_posbest_kernel<<<int(blocks), 256, 0, s>>>(lat, v, B, F, int(HW), pb);
+  if (total <= kWarpPerPosMax)
+    kwta_posbest_warp_kernel<<<int(ceil_div(total, 8)), 256, 0, s>>>(lat, v, B, F, int(HW), pb);
+  else
+    kwta_posbest_kernel<<<int(blocks), 256, 0, s>>>(lat, v, B, F, int(HW), pb);
   note_launch();
   const int use_smem = HW <= kKwtaSmemPos;
   const size_t smem = use_smem ? size_t(HW) * sizeof(uint64_t) : 0;

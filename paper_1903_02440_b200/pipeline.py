@@ -164,3 +164,65 @@ class SeqSTDP:
         R = self.rates
         snn.stdp_update(self.w, lat_in_img[0], self.spec.pad, lat[0], self.winners[0], self.count, R["a_plus"],
                         R["a_minus"], R["lb"], R["ub"], R["stabilizer"], reward)
+
+
+class SeqGraph:
+    """A CUDA graph of n sequential plasticity steps: one kernel chain per image, replayed without any
+    host synchronisation (the paper's residual per-image CPU-GPU interaction, removed).
+
+    ``replay()`` restores the initial weights first, so every replay is one training pass over the
+    same n images.  ``snapshot_every`` adds device copies of the weights after every that many images.
+    """
+
+    def __init__(self, seq: "SeqSTDP", lat_in_all: torch.Tensor, n: int, labels: Optional[torch.Tensor] = None,
+                 snapshot_every: int = 0):
+        self.seq, self.lat, self.n, self.labels = seq, lat_in_all, n, labels
+        self.w0 = seq.w.clone()
+        self.snaps = [torch.empty_like(seq.w) for _ in range(n // snapshot_every)] if snapshot_every else []
+        self.every = snapshot_every
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):          # warm-up outside capture (lazy attribute setup)
+            self._body(1)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.seq.w.copy_(self.w0)
+        self.graph = torch.cuda.CUDAGraph()
+        c0 = snn.launch_count()
+        with torch.cuda.graph(self.graph, capture_error_mode="relaxed"):
+            self.seq.w.copy_(self.w0)
+            self._body(n)
+        self.launches = snn.launch_count() - c0  # libsnn kernel nodes per replay
+
+    def _body(self, n: int):
+        si = 0
+        for b in range(n):
+            lab = None if self.labels is None else self.labels[b:b + 1]
+            self.seq.step(self.lat[b:b + 1], lab)
+            if self.every and (b + 1) % self.every == 0 and si < len(self.snaps):
+                self.snaps[si].copy_(self.seq.w)
+                si += 1
+
+    def replay(self):
+        self.graph.replay()
+
+
+class StepGraph:
+    """CUDA graph of one fixed sequence of libsnn calls (``fn``) on preallocated buffers."""
+
+    def __init__(self, fn):
+        self.fn = fn
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            fn()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        c0 = snn.launch_count()
+        with torch.cuda.graph(self.graph, capture_error_mode="relaxed"):
+            fn()
+        self.launches = snn.launch_count() - c0  # libsnn kernel nodes per replay
+
+    def replay(self):
+        self.graph.replay()

@@ -177,11 +177,13 @@ def test_pool_vs_oracle(G, orc, win, stride, pad, with_v):
 
 
 # ---------------------------------------------------------------------------------------- inhibit
-@pytest.mark.parametrize("F,levels", [(1, 0), (6, 3), (30, 0), (257, 2)])
-def test_inhibit_vs_oracle(G, orc, F, levels):
+@pytest.mark.parametrize("F,levels,hw", [(1, 0, (13, 17)), (6, 3, (13, 17)), (30, 0, (13, 17)), (257, 2, (13, 17)),
+                                         (7, 2, (131, 129))])
+def test_inhibit_vs_oracle(G, orc, F, levels, hw):
+    """Small maps take the warp-per-position kernel, large ones (> 16384 positions) the thread one."""
     import synth
     rng = np.random.default_rng(F)
-    lat = synth.random_latencies(rng, (2, F, 13, 17), 5, 0.4)
+    lat = synth.random_latencies(rng, (2, F) + hw, 5, 0.4)
     v = synth.random_potentials_at_spike(rng, lat, levels)
     gl, gv, gw = G.inhibit(cu(lat), cu(v))
     ol, ov, ow = orc.inhibit(lat, v)
@@ -192,7 +194,7 @@ def test_inhibit_vs_oracle(G, orc, F, levels):
 @pytest.mark.parametrize("B,F,H,W,k,r,p,levels", [(4, 30, 28, 28, 5, 3, 0.3, 0), (3, 250, 14, 14, 8, 2, 0.5, 3),
                                                  (2, 7, 5, 6, 20, 0, 0.5, 2), (2, 3, 4, 4, 5, 1, 0.05, 0),
                                                  (2, 256, 64, 64, 16, 4, 0.2, 0), (3, 1, 9, 9, 3, 0, 1.0, 1),
-                                                 (2, 4, 3, 3, 2, 5, 0.0, 0)])
+                                                 (2, 4, 3, 3, 2, 5, 0.0, 0), (1, 9, 140, 141, 6, 3, 0.3, 2)])
 def test_k_winners_vs_oracle(G, orc, B, F, H, W, k, r, p, levels):
     import synth
     rng = np.random.default_rng(B * 1000 + F)
