@@ -462,9 +462,8 @@ def run_ours(args, rank, world, local):
     step = WORKLOADS[args.workload](torch, dev)
     torch.cuda.synchronize()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
+    from paper_1903_02440_b200 import dist as sdist
+    barrier = sdist.barrier
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if not args.profile else None
     nst = len(step.stages)
@@ -493,11 +492,7 @@ def run_ours(args, rank, world, local):
     snn.sync_status()
     step_ms = [ev[k][0].elapsed_time(ev[k][nst]) for k in range(args.steps)]
     stage_ms = [statistics.mean(ev[k][i].elapsed_time(ev[k][i + 1]) for k in range(args.steps)) for i in range(nst)]
-    total_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = sdist.max_over_ranks(sum(step_ms), dev)   # the job's time = the slowest rank
     units = step.B * args.steps * world
     value = units / (total_ms * 1e-3)
     # ---------------- off-clock: events, e2e, cpu baseline ----------------
@@ -516,11 +511,7 @@ def run_ours(args, rank, world, local):
             step.e2e(xh, oh)
         e1.record()
         torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        e2e_ms = sdist.max_over_ranks(e0.elapsed_time(e1), dev)
         e2e = {"value": round(step.B * args.steps * world / (e2e_ms * 1e-3), 3), "unit": "images/s",
                "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
                "d2h_bytes_per_step": int(oh.numel() * oh.element_size())}
@@ -561,9 +552,9 @@ def main():
         return
     if world > 1:
         import torch
-        import torch.distributed as dist
+        from paper_1903_02440_b200 import dist as sdist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        sdist.init("nccl", torch.device("cuda", local))
     try:
         run_ours(args, rank, world, local)
     finally:
