@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 
@@ -388,6 +390,21 @@ static void make_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
 
 size_t conv_tc_workspace(int B, int Ho, int Wo, int R, int F);
 size_t conv_walk_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T);
+size_t conv_tct_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW);
+int conv_tct_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
+                    int KW, int T, float theta, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes,
+                    cudaStream_t s);
+
+// Finite-threshold path selection.  Default: the SIMT delta walk (conv_walk.cu).  SNN_CONV_PATH=tct
+// selects the tensor-core time-stepped kernel (conv_tct.cu; exact, but slower on every config so far,
+// DESIGN.md §7), SNN_CONV_PATH=ref the validation kernel below.
+static int conv_path_override() {
+  const char* e = getenv("SNN_CONV_PATH");
+  if (!e) return 1;
+  if (!strcmp(e, "tct")) return 0;
+  if (!strcmp(e, "ref")) return 2;
+  return 1;
+}
 int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
                      int KW, int T, float theta, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes,
                      cudaStream_t s);
@@ -415,6 +432,8 @@ size_t conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, i
   } else {
     size_t t = conv_walk_workspace(B, C, H, W, pad, F, KH, KW, T);
     m = m > t ? m : t;
+    t = conv_tct_workspace(B, C, H, W, pad, F, KH, KW);
+    m = m > t ? m : t;
   }
   return ((m + 255) & ~size_t(255)) + 256;
 }
@@ -439,7 +458,12 @@ int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   if (npos == 0 || F == 0) return SNN_OK;
   if (inf && !pot_out)  // Eq. 5: dense contraction of S[T-1] on the tensor cores
     return conv_tc_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, lat_out, v_out, ws, ws_bytes, s);
-  if (!inf && !pot_out) {  // throughput kernel (conv_walk.cu); the kernel below is the validation path
+  const int path = conv_path_override();
+  if (!inf && !pot_out && path == 0) {  // tensor cores, time step by time step (conv_tct.cu)
+    int rc = conv_tct_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, theta, lat_out, v_out, ws, ws_bytes, s);
+    if (rc != 1) return rc;
+  }
+  if (!inf && !pot_out && path <= 1) {  // SIMT delta walk (conv_walk.cu); the kernel below validates
     int rc = conv_walk_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, theta, lat_out, v_out, ws, ws_bytes, s);
     if (rc != 1) return rc;
   }

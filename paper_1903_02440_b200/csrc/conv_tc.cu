@@ -17,6 +17,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "tc_ptx.cuh"
 
 namespace snn {
 
@@ -113,58 +114,6 @@ __global__ void tc_prep_a_kernel(const uint8_t* __restrict__ lat_in, int C, int 
   }
 }
 
-// ------------------------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  // watchdog: a pipeline bug traps (the launch fails with an error) instead of hanging the GPU
-  for (uint32_t n = 0; !mbar_try(bar, parity); ++n)
-    if (n == (1u << 28)) __trap();
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
-}
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  // K-major, SWIZZLE_NONE canonical layout; version 1 (sm_100) at bits [46,48)
-  return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
-         (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46);
-}
-__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(accum)
-      : "memory");
-}
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
-        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
 // ------------------------------------------------------------------------------- the GEMM
 __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* __restrict__ aq,
                                                                  const uint8_t* __restrict__ bq, TcPlan p, int F,
@@ -177,7 +126,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
   __shared__ __align__(8) uint64_t full_bar[kTcStages], empty_bar[kTcStages], done_bar;
   __shared__ uint32_t tmem_base_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ch = blockIdx.x, mt = blockIdx.y;  // N chunks fastest: CTAs sharing an A tile run together
+  const int ch = int(blockIdx.x % unsigned(p.nch)), mt = int(blockIdx.x / unsigned(p.nch));  // chunks fastest
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTcStages; ++s) {
@@ -294,7 +243,7 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
   const int smem = kTcStages * (kTcM * kTcKT + p.N * kTcKT) + 1024;
   cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_conv_fire(tc): %s", cudaGetErrorString(e));
-  conv_tc_kernel<<<dim3(p.nch, p.Mt), kTcThreads, smem, s>>>(aq, bq, p, F, Ho * Wo, T, cols, lat_out, v_out);
+  conv_tc_kernel<<<unsigned(int64_t(p.Mt) * p.nch), kTcThreads, smem, s>>>(aq, bq, p, F, Ho * Wo, T, cols, lat_out, v_out);
   note_launch();
   return check_launch("snn_conv_fire(tc)");
 }

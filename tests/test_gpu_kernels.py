@@ -105,11 +105,17 @@ CONV_CASES = [
     (2, 250, 4, 4, 2, 200, 5, 15, math.inf, 0.9),   # Eq. 5 dense path (C2 L3 shape)
     (1, 20, 25, 40, 0, 100, 17, 30, math.inf, 0.7), # Eq. 5 dense path (C4 L2 shape)
     (1, 2, 5, 5, 0, 3, 5, 4, 0.5, 0.0),             # no input spikes at all
+    (3, 7, 21, 19, 2, 130, 5, 9, 6.0, 0.7),         # 3 feature chunks, ragged M tile
+    (1, 4, 20, 31, 0, 20, 5, 254, 2.0, 0.3),        # T = 254
 ]
 
 
+@pytest.mark.parametrize("path", ["walk", "tct", "ref"])
 @pytest.mark.parametrize("case", CONV_CASES)
-def test_conv_fire_vs_oracle(G, orc, case):
+def test_conv_fire_vs_oracle(G, orc, case, path, monkeypatch):
+    """walk = default SIMT delta walk for finite theta (tcgen05 GEMM for theta = inf);
+    tct = tensor-core time-stepped kernel (SNN_CONV_PATH=tct); ref = validation kernel."""
+    monkeypatch.setenv("SNN_CONV_PATH", path)
     B, C, H, W, pad, F, K, T, theta, p = case
     rng = np.random.default_rng(abs(hash(case)) % 2 ** 31)
     import synth
