@@ -173,9 +173,9 @@ __global__ void __launch_bounds__(512) rf_sort_kernel(const WalkArgs a) {
   for (int64_t wi = int64_t(blockIdx.x) * nwarps + warp; wi * PPW < a.np; wi += int64_t(gridDim.x) * nwarps) {
     const int64_t q = wi * PPW + grp;  // chunk-relative position
     const bool pv = q < a.np;
-    const int64_t p = a.p0 + q;
-    const int b = pv ? int(p / HoWo) : 0;
-    const int rem = pv ? int(p - int64_t(b) * HoWo) : 0;
+    const int p = int(a.p0 + q);
+    const int b = pv ? p / int(HoWo) : 0;
+    const int rem = pv ? p - b * int(HoWo) : 0;
     const int y = rem / a.Wo, x = rem - (rem / a.Wo) * a.Wo;
     const int y0 = y - a.pad, x0 = x - a.pad;
     const uint8_t* in = a.lat_in + int64_t(b) * CHW + int64_t(y0) * a.W + x0;
@@ -235,9 +235,9 @@ __global__ void __launch_bounds__(WalkThreads<FPL>::v, 1) conv_walk_kernel(const
   for (int64_t wi = int64_t(blockIdx.x) * nwarps + warp; wi * PPW < a.np; wi += stride_w) {
     const int64_t q = wi * PPW + grp;
     const bool pv = q < a.np;
-    const int64_t p = a.p0 + q;
-    const int b = pv ? int(p / HoWo) : 0;
-    const int rem = pv ? int(p - int64_t(b) * HoWo) : 0;
+    const int p = int(a.p0 + q);  // npos < 2^31 (checked by the planner)
+    const int b = pv ? p / int(HoWo) : 0;
+    const int rem = pv ? p - b * int(HoWo) : 0;
     const uint16_t* rec = nullptr;
     if constexpr (PRE) {
       rec = a.lists + (pv ? q : 0) * a.rec;
@@ -351,6 +351,7 @@ static int pos_scratch_bytes(int T, int R, int lpp, int rw, WalkArgs* a) {
 static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, WalkPlan* pl) {
   WalkArgs& a = pl->a;
   a = WalkArgs{};
+  if (int64_t(B) * (H + 2 * pad - KH + 1) * (W + 2 * pad - KW + 1) >= (int64_t(1) << 31)) return false;
   a.B = B; a.C = C; a.H = H; a.W = W; a.pad = pad; a.F = F; a.KH = KH; a.KW = KW; a.T = T;
   a.Ho = H + 2 * pad - KH + 1; a.Wo = W + 2 * pad - KW + 1; a.R = C * KH * KW;
   const int R = a.R;
@@ -433,7 +434,7 @@ size_t conv_walk_workspace(int B, int C, int H, int W, int pad, int F, int KH, i
   if (!walk_plan(B, C, H, W, pad, F, KH, KW, T, &pl)) return 0;
   size_t n = size_t(pl.n_groups) * (pl.a.R + 1) * pl.FGS * 4;
   n = (n + 255) & ~size_t(255);
-  if (pl.pre) n += size_t(pl.chunk) * pl.a.rec * 2 + 64;  // + slack for the prefetch past the end
+  if (pl.pre) n += size_t(pl.chunk) * pl.a.rec * 2 + 256;  // + slack for the prefetch past the end
   return n + 256;
 }
 
@@ -478,7 +479,7 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   if (!walk_plan(B, C, H, W, pad, F, KH, KW, T, &pl)) return 1;
   WalkArgs a = pl.a;
   size_t wq_bytes = (size_t(pl.n_groups) * (a.R + 1) * pl.FGS * 4 + 255) & ~size_t(255);
-  const size_t need = wq_bytes + (pl.pre ? size_t(pl.chunk) * a.rec * 2 + 64 : 0);
+  const size_t need = wq_bytes + (pl.pre ? size_t(pl.chunk) * a.rec * 2 + 256 : 0);
   if (ws_bytes < need) return set_error(SNN_EWORKSPACE, "snn_conv_fire: workspace %zu < %zu", ws_bytes, need);
   a.lat_in = lat_in; a.lat_out = lat_out; a.v_out = v_out;
   a.wq = reinterpret_cast<const uint32_t*>(ws);
