@@ -110,6 +110,7 @@ int snn_sync_status(snn_stream_t s) {
   int word = 0;
   int rc = read_clear_error_word(&word);
   if (rc) return rc;
+  if (word & kErrInternal) return set_error(SNN_ECUDA, "internal error: a kernel consistency trap fired");
   if (word & kErrInexact)
     return set_error(SNN_EINEXACT, "a weight is outside the exact domain {w : w*2^31 integral, 0 <= w <= 1}");
   return SNN_OK;

@@ -12,6 +12,7 @@ constexpr uint8_t kNoSpike = SNN_NO_SPIKE;
 // Device error word (bit 0 = inexact weight), defined in conv_fire.cu (the only device writer);
 // read and cleared by snn_sync_status() through read_clear_error_word().
 constexpr int kErrInexact = 1;
+constexpr int kErrInternal = 2;  // a kernel's internal consistency trap fired (a library bug)
 int read_clear_error_word(int* word);
 int* error_word_ptr();  // device address of the error word, for kernels of other translation units
 __device__ __forceinline__ void flag_error(int* err, int bit) { atomicOr(err, bit); }

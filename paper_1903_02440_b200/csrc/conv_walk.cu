@@ -4,23 +4,33 @@
 //
 //  * Receptive-field sort.  Each output position's C*KH*KW inputs are counting-sorted by spike time
 //    (lane-private u16 counters per (bucket, lane), rows scanned with 16-byte loads, bucket starts by a
-//    segmented warp scan; buckets padded to an even length with the zero-weight dummy row R).
+//    segmented warp scan).  The sorted list holds u32 BYTE OFFSETS of the inputs' weight rows in the
+//    shared-memory weight slice (so the walk's gather address is one add); every bucket is padded to
+//    an even length with the zero-weight row R (bucket ends fall on pair boundaries) and the tail to
+//    whole 8-entry blocks.
 //  * Walk.  PPW output positions per warp, LPP = 32/PPW lanes per position, FPL features per lane:
-//    a group of LPP lanes covers FGS = LPP*FPL features of its position.  All groups advance in
-//    lockstep, one pair of list entries per iteration: each lane gathers its FPL fixed-point weights
-//    per input (one conflict-free LDS.64/128) and accumulates exactly in int64 (units of 2^-31); at
-//    the end of every non-empty bucket it tests the threshold and records (lat, v); a group stops as
+//    a group of LPP lanes covers FGS = LPP*FPL features of its position.  The list is consumed in
+//    blocks of 8 inputs; each lane gathers its FPL fixed-point weights per input (one conflict-free
+//    LDS.64/128) and sums the block exactly (int64, units of 2^-31, three-input adds).  Because every
+//    weight is >= 0 the potential is monotone along the list, so a threshold test inside a block can
+//    only fire if the potential at the block END exceeds the threshold for an unfired feature; and a
+//    test is only due at a bucket end.  Blocks with no crossing, or with no bucket end strictly
+//    inside, are therefore added whole (a test at most at the block end); only a block with both is
+//    walked pair by pair with the exact test at each bucket end (K3).  A group stops as
 //    soon as all its features fired or its list is exhausted.
 //  * Two schedules.  If the layer fits one feature group (weights of all F features in shared
 //    memory), sort and walk are fused in one kernel (no list traffic).  Otherwise the sort runs ONCE
 //    per position in rf_sort_kernel, which writes compact bucketed lists to a workspace chunk that
-//    stays L2-resident, and conv_walk_kernel<PRE=true> streams them (16-byte prefetched loads) for
-//    every feature group -- the sort is not repeated per group.
+//    stays L2-resident, and conv_walk_kernel<PRE=true> streams them (16-byte loads, one block ahead)
+//    for every feature group -- the sort is not repeated per group.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "common.cuh"
+#include "tc_ptx.cuh"
 
 namespace snn {
 
@@ -28,6 +38,10 @@ int weight_prep_launch(const float* w, int F, int R, int FGS, int n_groups, uint
 
 constexpr int kWalkSmemLimit = 227 * 1024;
 constexpr size_t kListChunkBytes = size_t(48) << 20;  // sorted lists per chunk (L2-resident)
+constexpr int kBlk = 8;                               // list entries per gather block
+constexpr int kIt = 16;                               // list entries per walk iteration (lists padded to this)
+constexpr int kRing = 4;                              // per-warp list ring (PRE): iterations in flight + 1
+constexpr int kListSlack = kRing * kIt * 4;           // bytes read past the last record (prefetch)
 
 struct WalkArgs {
   const uint8_t* lat_in;
@@ -38,11 +52,13 @@ struct WalkArgs {
   uint8_t* lat_out;
   float* v_out;
   int off_eoff, off_ekk, off_warps, warp_bytes, pos_bytes;
-  int cnt_off, start_off, size_off, list_off, row_words;
-  // presorted lists: record of position p (chunk-relative) at lists + (p - p0) * rec (u16 units)
-  uint16_t* lists;
-  int rec, hdr;       // u16 per record; u16 of the header (bucket starts), multiple of 8
+  int cnt_off, start_off, list_off;
+  int row_bytes;      // bytes per weight row of the walk's slice (FGS * 4): list entries are row * row_bytes
+  // presorted lists: record of position p (chunk-relative) at lists + (p - p0) * rec bytes
+  unsigned char* lists;
+  int rec, hdr;       // bytes per record; bytes of its header (T+1 u16 bucket starts, 16-aligned)
   int64_t p0, np;     // chunk of positions [p0, p0 + np)
+  int* err;           // device error word
 };
 
 static inline int al16(int x) { return (x + 15) & ~15; }
@@ -53,7 +69,7 @@ template <> struct WalkVec<2> { typedef uint2 T; };
 template <> struct WalkVec<4> { typedef uint4 T; };
 
 template <int FPL>
-__device__ __forceinline__ void wgather(const uint32_t* p, uint32_t (&o)[FPL]) {
+__device__ __forceinline__ void wgather(const unsigned char* p, uint32_t (&o)[FPL]) {
   typedef typename WalkVec<FPL>::T V;
   const V v = *reinterpret_cast<const V*>(p);
   if constexpr (FPL == 1) { o[0] = v; }
@@ -70,35 +86,34 @@ __device__ __forceinline__ uint8_t rf_lat(const WalkArgs& a, const int32_t* eoff
 }
 
 // Counting sort of one position's receptive field by a group of LPP lanes into (start, list).
+// Pass 1 counts the spiking inputs of each bucket with shared-memory atomics (independent, no
+// read-modify-write chains in the lane); the counts are scanned (each bucket padded to an even
+// length with the zero-weight row R, so every bucket end is on a pair boundary) into the bucket
+// starts; pass 2 re-reads the latencies (L1-resident) and takes each entry's slot with an atomic on
+// the bucket's running position.  Entries are weight-row byte offsets e * row_bytes; the tail is
+// padded to a whole walk iteration.  The order inside a bucket is whatever the atomics gave: it does
+// not change any result (the sum at a bucket end is exact and order-free).
 template <int LPP>
 __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, const int32_t* eoff, const uint16_t* ekk, bool pv,
                                               const uint8_t* in, bool interior, int y0, int x0, int gl,
-                                              uint16_t* cnt, uint16_t* start, uint16_t* bsize, uint16_t* list) {
-  const int R = a.R, T = a.T, rw = a.row_words;
-  for (int t = 0; t < T; ++t) cnt[t * rw * 2 + gl] = 0;
+                                              uint32_t* cnt, uint16_t* start, uint32_t* list) {
+  const int R = a.R, T = a.T;
+  const uint32_t rb = uint32_t(a.row_bytes);
+  for (int t = gl; t < T; t += LPP) cnt[t] = 0;
   __syncwarp();
-  if (pv)
+  if (pv) {
+#pragma unroll 4
     for (int e = gl; e < R; e += LPP) {
-      const uint8_t l = rf_lat(a, eoff, ekk, in, interior, y0, x0, e);
-      if (l < T) cnt[l * rw * 2 + gl] += 1;
+      const int l = rf_lat(a, eoff, ekk, in, interior, y0, x0, e);
+      if (l < T) atomicAdd(&cnt[l], 1u);
     }
+  }
   __syncwarp();
   int carry = 0;
   for (int tb = 0; tb < T; tb += LPP) {
     const int t = tb + gl;
-    uint32_t words[LPP / 2];
-    int tot = 0;
-    if (t < T) {
-      const uint32_t* row = reinterpret_cast<const uint32_t*>(cnt + t * rw * 2);
-#pragma unroll
-      for (int q = 0; q < LPP / 2; q += 4) {
-        const uint4 v4 = *reinterpret_cast<const uint4*>(row + q);
-        words[q] = v4.x; words[q + 1] = v4.y; words[q + 2] = v4.z; words[q + 3] = v4.w;
-      }
-#pragma unroll
-      for (int q = 0; q < LPP / 2; ++q) tot += int(words[q] & 0xFFFFu) + int(words[q] >> 16);
-    }
-    const int padded = tot + (tot & 1);
+    const int tot = t < T ? int(cnt[t]) : 0;
+    const int padded = tot + (tot & 1);  // buckets padded to even length: every bucket end is on a pair boundary
     int inc = padded;
 #pragma unroll
     for (int o = 1; o < LPP; o <<= 1) {
@@ -108,37 +123,23 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, const int32_t* 
     const int st = carry + inc - padded;
     if (t < T) {
       start[t] = uint16_t(st);
-      bsize[t] = uint16_t(tot);
-      int run = st;
-      uint32_t* row = reinterpret_cast<uint32_t*>(cnt + t * rw * 2);
-#pragma unroll
-      for (int q = 0; q < LPP / 2; ++q) {
-        const int c0 = int(words[q] & 0xFFFFu), c1 = int(words[q] >> 16);
-        words[q] = uint32_t(run) | (uint32_t(run + c0) << 16);
-        run += c0 + c1;
-      }
-#pragma unroll
-      for (int q = 0; q < LPP / 2; q += 4)
-        *reinterpret_cast<uint4*>(row + q) = make_uint4(words[q], words[q + 1], words[q + 2], words[q + 3]);
+      cnt[t] = uint32_t(st);                           // pass 2: running slot of the bucket
+      if (tot & 1) list[st + tot] = uint32_t(R) * rb;  // the pad entry: zero-weight row
     }
     carry += __shfl_sync(0xffffffffu, inc, LPP - 1, LPP);
   }
   if (gl == 0) start[T] = uint16_t(carry);
   __syncwarp();
-  if (pv)
+  if (pv) {
+#pragma unroll 4
     for (int e = gl; e < R; e += LPP) {
-      const uint8_t l = rf_lat(a, eoff, ekk, in, interior, y0, x0, e);
-      if (l < T) {
-        const int c = cnt[l * rw * 2 + gl];
-        cnt[l * rw * 2 + gl] = uint16_t(c + 1);
-        list[c] = uint16_t(e);
-      }
+      const int l = rf_lat(a, eoff, ekk, in, interior, y0, x0, e);
+      if (l < T) list[atomicAdd(&cnt[l], 1u)] = uint32_t(e) * rb;
     }
-  for (int t = gl; t < T; t += LPP)
-    if (bsize[t] & 1) list[start[t] + bsize[t]] = uint16_t(R);
-  {  // pad the tail to a whole 8-entry block (the walk consumes blocks of 4 pairs)
+  }
+  {  // pad the tail to a whole walk iteration with the zero-weight row R
     const int n = carry;
-    for (int k = n + gl; k < ((n + 7) & ~7); k += LPP) list[k] = uint16_t(R);
+    for (int k = n + gl; k < ((n + kIt - 1) & ~(kIt - 1)); k += LPP) list[k] = uint32_t(R) * rb;
   }
   __syncwarp();
 }
@@ -162,56 +163,116 @@ __global__ void __launch_bounds__(512) rf_sort_kernel(const WalkArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int grp = lane / LPP, gl = lane - grp * LPP;
   unsigned char* pb = smem + a.off_warps + warp * a.warp_bytes + grp * a.pos_bytes;
-  uint16_t* cnt = reinterpret_cast<uint16_t*>(pb + a.cnt_off);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(pb + a.cnt_off);
   uint16_t* start = reinterpret_cast<uint16_t*>(pb + a.start_off);
-  uint16_t* bsize = reinterpret_cast<uint16_t*>(pb + a.size_off);
-  uint16_t* list = reinterpret_cast<uint16_t*>(pb + a.list_off);
+  uint32_t* list = reinterpret_cast<uint32_t*>(pb + a.list_off);
   rf_tables(a, eoff, ekk);
   __syncthreads();
-  const int64_t HoWo = int64_t(a.Ho) * a.Wo;
+  const int HoWo = a.Ho * a.Wo;
   const int64_t CHW = int64_t(a.C) * a.H * a.W;
   for (int64_t wi = int64_t(blockIdx.x) * nwarps + warp; wi * PPW < a.np; wi += int64_t(gridDim.x) * nwarps) {
     const int64_t q = wi * PPW + grp;  // chunk-relative position
     const bool pv = q < a.np;
     const int p = int(a.p0 + q);
-    const int b = pv ? p / int(HoWo) : 0;
-    const int rem = pv ? p - b * int(HoWo) : 0;
+    const int b = pv ? p / HoWo : 0;
+    const int rem = pv ? p - b * HoWo : 0;
     const int y = rem / a.Wo, x = rem - (rem / a.Wo) * a.Wo;
     const int y0 = y - a.pad, x0 = x - a.pad;
     const uint8_t* in = a.lat_in + int64_t(b) * CHW + int64_t(y0) * a.W + x0;
     const bool interior = y0 >= 0 && x0 >= 0 && y0 + a.KH <= a.H && x0 + a.KW <= a.W;
-    rf_sort_group<LPP>(a, eoff, ekk, pv, in, interior, y0, x0, gl, cnt, start, bsize, list);
-    if (pv) {  // record = [header (T+1 starts, padded to hdr)][entries (start[T] of them)]
-      uint16_t* rec = a.lists + q * a.rec;
-      for (int t = gl; t <= a.T; t += LPP) rec[t] = start[t];
-      const int n8 = (int(start[a.T]) + 7) >> 3;  // whole 8-entry blocks (tail padded with R)
+    rf_sort_group<LPP>(a, eoff, ekk, pv, in, interior, y0, x0, gl, cnt, start, list);
+    if (pv) {  // record = [header: T+1 u16 starts, 16-aligned][entries: u32, whole blocks]
+      unsigned char* rec = a.lists + q * a.rec;
+      uint16_t* hdr = reinterpret_cast<uint16_t*>(rec);
+      for (int t = gl; t <= a.T; t += LPP) hdr[t] = start[t];
+      const int n4 = ((int(start[a.T]) + kIt - 1) / kIt) * (kIt / 4);  // uint4 per walk iteration
       const uint4* src = reinterpret_cast<const uint4*>(list);
       uint4* dst = reinterpret_cast<uint4*>(rec + a.hdr);
-      for (int k = gl; k < n8; k += LPP) dst[k] = src[k];
+      for (int k = gl; k < n4; k += LPP) dst[k] = src[k];
     }
     __syncwarp();
   }
 }
 
 // ------------------------------------------------------------------------------------- walk
-template <int FPL> struct WalkThreads { static constexpr int v = FPL == 4 ? 768 : 1024; };
+template <int FPL> struct WalkThreads { static constexpr int v = FPL == 4 ? 640 : 1024; };
+
+// Fire every unfired feature whose potential at the end of bucket t exceeds the threshold.
+template <int FPL>
+__device__ __forceinline__ void fire_at(const uint64_t (&acc)[FPL], int64_t thr, int t, unsigned& fired,
+                                        uint32_t& lo, float (&vo)[FPL]) {
+#pragma unroll
+  for (int j = 0; j < FPL; ++j) {
+    if (!(fired >> j & 1) && int64_t(acc[j]) > thr) {
+      fired |= 1u << j;
+      lo = (lo & ~(0xFFu << (8 * j))) | (uint32_t(t) << (8 * j));
+      vo[j] = fixed_to_float(int64_t(acc[j]));
+    }
+  }
+}
+
+// One 8-input block of the walk (entries e0, e1: weight-row byte offsets).  The bucket ends inside
+// the block are known to the whole group beforehand (endm: bit m = a bucket ends after pair m, its
+// first-spike index in byte m of tpk).  Each lane sums its features' 8 weights exactly; if no
+// unfired feature of the lane then exceeds the threshold, no test inside the block could fire
+// (potentials only grow along the list) and the block is taken whole; otherwise the lane re-adds it
+// pair by pair from the same registers and tests at every bucket end (K3).  Lanes decide
+// independently (no vote): the group's bookkeeping does not depend on the branch taken.
+template <int FPL>
+__device__ __forceinline__ void walk_block(const unsigned char* wl, const uint4& e0, const uint4& e1, unsigned endm,
+                                           uint32_t tpk, int64_t thr, uint64_t (&acc)[FPL], unsigned& fired,
+                                           uint32_t& lo, float (&vo)[FPL]) {
+  const uint32_t off[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+  uint32_t wv[8][FPL];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) wgather<FPL>(wl + off[k], wv[k]);
+  uint64_t s[FPL];
+  bool hit = false;
+#pragma unroll
+  for (int j = 0; j < FPL; ++j) {
+    s[j] = acc[j] + (uint64_t(wv[0][j]) + wv[1][j]) + (uint64_t(wv[2][j]) + wv[3][j]) +
+           (uint64_t(wv[4][j]) + wv[5][j]) + (uint64_t(wv[6][j]) + wv[7][j]);
+    hit |= !(fired >> j & 1) && int64_t(s[j]) > thr;
+  }
+  if (hit && endm) {
+    if (endm & 7u) {  // a bucket ends strictly inside the block: pair by pair
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+#pragma unroll
+        for (int j = 0; j < FPL; ++j) acc[j] += uint64_t(wv[2 * m][j]) + wv[2 * m + 1][j];
+        if (endm >> m & 1) fire_at<FPL>(acc, thr, int((tpk >> (8 * m)) & 0xFFu), fired, lo, vo);
+      }
+    } else {  // the only bucket end is the block end
+      fire_at<FPL>(s, thr, int(tpk >> 24), fired, lo, vo);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < FPL; ++j) acc[j] = s[j];
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int FPL, int PPW, bool PRE>
 __global__ void __launch_bounds__(WalkThreads<FPL>::v, 1) conv_walk_kernel(const WalkArgs a) {
   constexpr int LPP = 32 / PPW;
   constexpr int FGS = LPP * FPL;
+  constexpr unsigned kAll = (1u << FPL) - 1;
+  static_assert(!PRE || PPW == 1, "presorted walk: one position per warp");
   extern __shared__ __align__(16) unsigned char smem[];
   const int R = a.R, T = a.T;
-  const uint32_t* Ws = reinterpret_cast<const uint32_t*>(smem);
   int32_t* eoff = reinterpret_cast<int32_t*>(smem + a.off_eoff);
   uint16_t* ekk = reinterpret_cast<uint16_t*>(smem + a.off_ekk);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int grp = lane / LPP, gl = lane - grp * LPP;
   unsigned char* pb = smem + a.off_warps + warp * a.warp_bytes + grp * a.pos_bytes;
-  uint16_t* cnt = reinterpret_cast<uint16_t*>(pb + a.cnt_off);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(pb + a.cnt_off);
   uint16_t* start = reinterpret_cast<uint16_t*>(pb + a.start_off);
-  uint16_t* bsize = reinterpret_cast<uint16_t*>(pb + a.size_off);
-  uint16_t* list = reinterpret_cast<uint16_t*>(pb + a.list_off);
+  uint32_t* list = reinterpret_cast<uint32_t*>(pb + a.list_off);  // fused: the sorted list; PRE: the ring
   const int g = blockIdx.y;
   {
     const uint4* src = reinterpret_cast<const uint4*>(a.wq + int64_t(g) * (R + 1) * FGS);
@@ -222,95 +283,104 @@ __global__ void __launch_bounds__(WalkThreads<FPL>::v, 1) conv_walk_kernel(const
   }
   __syncthreads();
 
-  const int64_t HoWo = int64_t(a.Ho) * a.Wo;
+  const int HoWo = a.Ho * a.Wo;
   const int64_t CHW = int64_t(a.C) * a.H * a.W;
   const int fbase = g * FGS + gl * FPL;
   unsigned valid = 0;
 #pragma unroll
   for (int j = 0; j < FPL; ++j) valid |= (fbase + j < a.F) ? (1u << j) : 0u;
-  constexpr unsigned kAll = (1u << FPL) - 1;
   const unsigned gmask = (LPP == 32) ? 0xffffffffu : (((1u << LPP) - 1u) << (grp * LPP));
   const int64_t stride_w = int64_t(gridDim.x) * nwarps;
+  const int64_t thr = a.thr;
+  const unsigned char* wl = smem + gl * FPL * 4;  // this lane's features in weight row 0
 
   for (int64_t wi = int64_t(blockIdx.x) * nwarps + warp; wi * PPW < a.np; wi += stride_w) {
     const int64_t q = wi * PPW + grp;
     const bool pv = q < a.np;
     const int p = int(a.p0 + q);  // npos < 2^31 (checked by the planner)
-    const int b = pv ? p / int(HoWo) : 0;
-    const int rem = pv ? p - b * int(HoWo) : 0;
-    const uint16_t* rec = nullptr;
+    const int b = pv ? p / HoWo : 0;
+    const int rem = pv ? p - b * HoWo : 0;
+    const unsigned char* ent = nullptr;  // PRE: this position's entries in global memory (L2)
     if constexpr (PRE) {
-      rec = a.lists + (pv ? q : 0) * a.rec;
-      for (int t = gl; t <= T; t += LPP) start[t] = pv ? rec[t] : 0;
+      const unsigned char* rec = a.lists + (pv ? q : 0) * a.rec;
+      ent = rec + a.hdr;
+      cp_async_wait<0>();  // the previous position's copies into the ring have landed
+      __syncwarp();
+      if (lane < 4)  // the first kRing-1 iterations of entries -> ring, ahead of the header
+        for (int r = 0; r < kRing - 1; ++r) cp_async16(list + r * kIt + lane * 4, ent + r * kIt * 4 + lane * 16);
+      for (int r = 0; r < kRing - 1; ++r) cp_async_commit();
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(rec);
+      for (int t = gl; t <= T; t += LPP) start[t] = pv ? h[t] : 0;
       __syncwarp();
     } else {
       const int y = rem / a.Wo, x = rem - (rem / a.Wo) * a.Wo;
       const int y0 = y - a.pad, x0 = x - a.pad;
       const uint8_t* in = a.lat_in + int64_t(b) * CHW + int64_t(y0) * a.W + x0;
       const bool interior = y0 >= 0 && x0 >= 0 && y0 + a.KH <= a.H && x0 + a.KW <= a.W;
-      rf_sort_group<LPP>(a, eoff, ekk, pv, in, interior, y0, x0, gl, cnt, start, bsize, list);
+      rf_sort_group<LPP>(a, eoff, ekk, pv, in, interior, y0, x0, gl, cnt, start, list);
     }
 
     uint64_t acc[FPL];
-    uint8_t lo[FPL];
+    uint32_t lo = 0xFFFFFFFFu;  // byte j = lat of feature j (255 = no spike)
     float vo[FPL];
 #pragma unroll
-    for (int j = 0; j < FPL; ++j) { acc[j] = 0; lo[j] = kNoSpike; vo[j] = 0.0f; }
+    for (int j = 0; j < FPL; ++j) { acc[j] = 0; vo[j] = 0.0f; }
     unsigned fired = ~valid & kAll;
     const int total = pv ? int(start[T]) : 0;
-    int i = 0, t = 0;
-    int bend = start[1];
-    if (bend == 0) {  // bucket 0 empty: P[0] = 0 may still exceed a negative threshold
-      if (int64_t(0) > a.thr) {
+    if (pv && int(start[1]) == 0 && int64_t(0) > thr) {  // empty bucket 0: P[0] = 0 > a negative threshold
 #pragma unroll
-        for (int j = 0; j < FPL; ++j)
-          if (!(fired >> j & 1)) { fired |= 1u << j; lo[j] = 0; vo[j] = 0.0f; }
-      }
-      while (t < T && int(start[t + 1]) == 0) ++t;
-      bend = t < T ? int(start[t + 1]) : 0;
+      for (int j = 0; j < FPL; ++j)
+        if (!(fired >> j & 1)) lo &= ~(0xFFu << (8 * j));
+      fired = kAll;
     }
-    bool done = (t >= T) || (i >= total) || !pv || __all_sync(gmask, fired == kAll);
-    const uint32_t* wl = Ws + gl * FPL;
-    const uint4* list4 = reinterpret_cast<const uint4*>(list);
-    const uint4* gl4 = PRE ? reinterpret_cast<const uint4*>(rec + a.hdr) : nullptr;
-    uint4 cur = make_uint4(0, 0, 0, 0), nxt = make_uint4(0, 0, 0, 0);
-    if (PRE && !done) { cur = gl4[0]; nxt = gl4[1]; }
-    while (__any_sync(0xffffffffu, !done)) {
-      if (!done) {
-        // one block = 4 pairs = 8 inputs: all 8 gathers are issued before the ordered
-        // accumulate / threshold sequence (buckets end on pair boundaries)
-        uint4 blk;
-        if constexpr (PRE) { blk = cur; cur = nxt; nxt = gl4[(i >> 3) + 2]; }
-        else blk = list4[i >> 3];
-        const uint32_t prs[4] = {blk.x, blk.y, blk.z, blk.w};
-        uint32_t wv[8][FPL];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          wgather<FPL>(wl + (prs[k] & 0xFFFFu) * FGS, wv[2 * k]);
-          wgather<FPL>(wl + (prs[k] >> 16) * FGS, wv[2 * k + 1]);
+    bool done = !pv || total == 0;  // group-uniform, like every later update of done
+    {
+      const unsigned nd = __ballot_sync(0xffffffffu, fired != kAll);
+      if ((nd & gmask) == 0) done = true;  // all features of the group fired (or are padding)
+    }
+    int i = 0, t = 0, it = 0;
+    while (t < T && int(start[t + 1]) == 0) ++t;  // leading empty buckets (handled above)
+    int bend = t < T ? int(start[t + 1]) : 0x7FFFFFFF;  // end of the current non-empty bucket t
+    int guard = (total + kIt - 1) / kIt + 2;  // iterations this group can take (a bug trap, never hit)
+    // Every vote below is a full-warp ballot at a converged point; done is group-uniform.
+    while (true) {
+      if (__ballot_sync(0xffffffffu, !done) == 0) break;
+      const uint4* cur;  // this iteration's 16 entries, in shared memory
+      if constexpr (PRE) cur = reinterpret_cast<const uint4*>(list + (it % kRing) * kIt);
+      else cur = reinterpret_cast<const uint4*>(list + it * kIt);
+      if constexpr (PRE) {  // keep kRing-1 iterations of list entries in flight
+        if (!done) {
+          if (lane < 4)
+            cp_async16(list + ((it + kRing - 1) % kRing) * kIt + lane * 4, ent + (it + kRing - 1) * kIt * 4 + lane * 16);
+          cp_async_commit();
+          cp_async_wait<kRing - 1>();
         }
+        __syncwarp();
+      }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (!done) {
-#pragma unroll
-            for (int j = 0; j < FPL; ++j) acc[j] += uint64_t(wv[2 * k][j]) + uint64_t(wv[2 * k + 1][j]);
-            i += 2;
-            if (i == bend) {  // end of the non-empty bucket t: exact threshold test
-#pragma unroll
-              for (int j = 0; j < FPL; ++j) {
-                if (!(fired >> j & 1) && int64_t(acc[j]) > a.thr) {
-                  fired |= 1u << j;
-                  lo[j] = uint8_t(t);
-                  vo[j] = fixed_to_float(int64_t(acc[j]));
-                }
-              }
-              ++t;
-              while (t < T && int(start[t + 1]) == i) ++t;  // skip empty buckets
-              bend = t < T ? int(start[t + 1]) : 0;
-              done = (t >= T) || __all_sync(gmask, fired == kAll);
-            }
+      for (int h = 0; h < 2; ++h) {
+        if (!done) {
+          // group-uniform: bucket ends inside this block (pair m ends bucket t_m)
+          unsigned endm = 0;
+          uint32_t tpk = 0;
+          i += kBlk;
+          while (bend <= i) {
+            const int m = ((bend - (i - kBlk)) >> 1) - 1;
+            endm |= 1u << m;
+            tpk |= uint32_t(t) << (8 * m);
+            ++t;
+            while (t < T && int(start[t + 1]) == bend) ++t;  // empty buckets add nothing
+            bend = t < T ? int(start[t + 1]) : 0x7FFFFFFF;
           }
+          walk_block<FPL>(wl, cur[2 * h], cur[2 * h + 1], endm, tpk, thr, acc, fired, lo, vo);
         }
+        const unsigned nf = __ballot_sync(0xffffffffu, !done && fired != kAll);
+        if (!done && ((nf & gmask) == 0 || i >= total)) done = true;
+      }
+      ++it;
+      if (!done && --guard < 0) {
+        flag_error(a.err, kErrInternal);
+        done = true;
       }
     }
     if (pv) {
@@ -318,13 +388,14 @@ __global__ void __launch_bounds__(WalkThreads<FPL>::v, 1) conv_walk_kernel(const
       for (int j = 0; j < FPL; ++j) {
         if (valid >> j & 1) {
           const int64_t o = (int64_t(b) * a.F + fbase + j) * HoWo + rem;
-          a.lat_out[o] = lo[j];
+          a.lat_out[o] = uint8_t(lo >> (8 * j));
           a.v_out[o] = vo[j];
         }
       }
     }
     __syncwarp();
   }
+  if constexpr (PRE) cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------------------------- host
@@ -332,19 +403,17 @@ struct WalkPlan {
   int fpl, ppw, FGS, n_groups, nwarps, smem;  // walk kernel
   int sort_ppw, sort_nwarps, sort_smem;        // sort kernel (presorted mode)
   bool pre;
-  int64_t chunk;                               // positions per list chunk
-  WalkArgs a;                                  // walk kernel arguments / smem layout
-  WalkArgs sa;                                 // sort kernel arguments / smem layout
+  int64_t chunk;                                   // positions per list chunk
+  WalkArgs a;                                      // walk kernel arguments / smem layout
+  WalkArgs sa;                                     // sort kernel arguments / smem layout
 };
 
-static int pos_scratch_bytes(int T, int R, int lpp, int rw, WalkArgs* a) {
-  int o = 0, c0, c1, c2, c3;
-  c0 = o; o += al16(T * rw * 4);
-  c1 = o; o += al16((T + 1) * 2);
-  c2 = o; o += al16(T * 2);
-  c3 = o; o += al16((R + T + 8) * 2);
-  (void)lpp;
-  if (a) { a->cnt_off = c0; a->start_off = c1; a->size_off = c2; a->list_off = c3; a->pos_bytes = o; }
+static int pos_scratch_bytes(int T, int R, WalkArgs* a) {
+  int o = 0, c0, c1, c3;
+  c0 = o; o += al16(T * 4);                // bucket counters (u32, shared-memory atomics)
+  c1 = o; o += al16((T + 1) * 2);          // bucket starts
+  c3 = o; o += al16((R + T + kIt) * 4);    // entries + one pad per bucket + tail
+  if (a) { a->cnt_off = c0; a->start_off = c1; a->list_off = c3; a->pos_bytes = o; }
   return o;
 }
 
@@ -355,6 +424,7 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
   a.B = B; a.C = C; a.H = H; a.W = W; a.pad = pad; a.F = F; a.KH = KH; a.KW = KW; a.T = T;
   a.Ho = H + 2 * pad - KH + 1; a.Wo = W + 2 * pad - KW + 1; a.R = C * KH * KW;
   const int R = a.R;
+  if (R + T + kIt >= 65536) return false;  // u16 bucket starts
   const long tables = al16(R * 4) + al16(R * 2);
   struct Cand { int ppw, fpl; };
   const Cand cands[] = {{4, 4}, {2, 4}, {1, 4}, {4, 2}, {2, 2}, {1, 2}, {1, 1}};
@@ -364,12 +434,11 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
     const int lpp = 32 / c.ppw, fgs = lpp * c.fpl;
     if (fgs < F) continue;
     if (fgs > 32 && F <= fgs / 2) continue;
-    const int rw = lpp <= 16 ? 12 : 20;
-    const int wb = c.ppw * pos_scratch_bytes(T, R, lpp, rw, nullptr);
+    const int wb = c.ppw * pos_scratch_bytes(T, R, nullptr);
     const long fixed = al16(int(long(R + 1) * fgs * 4)) + tables;
     if (fixed + 8L * wb > kWalkSmemLimit) continue;
     long warps = (kWalkSmemLimit - fixed) / wb;
-    const int wcap = c.fpl == 4 ? 24 : 32;
+    const int wcap = c.fpl == 4 ? 20 : 32;
     if (warps > wcap) warps = wcap;
     if (best < 0 || warps > best_warps + 8) { best = int(&c - cands); best_warps = int(warps); }
   }
@@ -378,8 +447,8 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
     pl->ppw = cands[best].ppw; pl->fpl = cands[best].fpl;
     const int lpp = 32 / pl->ppw;
     pl->FGS = lpp * pl->fpl; pl->n_groups = 1; pl->nwarps = best_warps;
-    a.row_words = lpp <= 16 ? 12 : 20;
-    pos_scratch_bytes(T, R, lpp, a.row_words, &a);
+    a.row_bytes = pl->FGS * 4;
+    pos_scratch_bytes(T, R, &a);
     a.warp_bytes = pl->ppw * a.pos_bytes;
     a.off_eoff = al16(int(long(R + 1) * pl->FGS * 4));
     a.off_ekk = a.off_eoff + al16(R * 4);
@@ -396,32 +465,30 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
     if (fgs > 32 && F <= fgs / 2) continue;
     const long wsb = long(R + 1) * fgs * 4;
     const int hdr_bytes = al16((T + 1) * 2);
-    if (al16(int(wsb)) + 32L * hdr_bytes > kWalkSmemLimit) continue;
+    if (al16(int(wsb)) + 32L * (hdr_bytes + kRing * kIt * 4) > kWalkSmemLimit) continue;
+    pl->sort_ppw = R <= 256 ? 4 : 1;  // 4 positions per warp for small receptive fields
     pl->pre = true;
     pl->ppw = 1; pl->fpl = fpl; pl->FGS = fgs;
     pl->n_groups = int(ceil_div(F, fgs));
-    pl->nwarps = fpl == 4 ? 24 : 32;
-    a.cnt_off = 0; a.start_off = 0; a.size_off = 0; a.list_off = 0;
-    a.pos_bytes = hdr_bytes; a.warp_bytes = hdr_bytes;
+    pl->nwarps = fpl == 4 ? 20 : 32;
+    a.row_bytes = fgs * 4;
+    a.cnt_off = 0; a.start_off = 0; a.list_off = hdr_bytes;  // per warp: bucket starts, then the list ring
+    a.pos_bytes = hdr_bytes + kRing * kIt * 4; a.warp_bytes = a.pos_bytes;
     a.off_eoff = al16(int(wsb)); a.off_ekk = a.off_eoff; a.off_warps = a.off_eoff;
     pl->smem = a.off_warps + pl->nwarps * a.warp_bytes;
-    a.hdr = int(ceil_div(T + 1, 8)) * 8;
-    a.rec = a.hdr + int(ceil_div(R + T + 8, 8)) * 8;
-    // sort kernel: 16 warps, 1 position per warp (PPW 1) or 4 per warp for small receptive fields
-    pl->sort_ppw = R <= 256 ? 4 : 1;
+    a.hdr = hdr_bytes;
+    a.rec = hdr_bytes + int(ceil_div(R + T, kIt)) * kIt * 4;
     pl->sort_nwarps = 16;
-    const int slpp = 32 / pl->sort_ppw;
     WalkArgs& sa = pl->sa;
     sa = a;
-    sa.row_words = slpp <= 16 ? 12 : 20;
-    pos_scratch_bytes(T, R, slpp, sa.row_words, &sa);
+    pos_scratch_bytes(T, R, &sa);
     sa.warp_bytes = pl->sort_ppw * sa.pos_bytes;
     sa.off_eoff = 0;
     sa.off_ekk = al16(R * 4);
     sa.off_warps = sa.off_ekk + al16(R * 2);
     pl->sort_smem = sa.off_warps + pl->sort_nwarps * sa.warp_bytes;
     const int64_t npos = int64_t(B) * a.Ho * a.Wo;
-    int64_t ch = int64_t(kListChunkBytes / (size_t(a.rec) * 2));
+    int64_t ch = int64_t(kListChunkBytes / size_t(a.rec));
     if (ch < 1024) ch = 1024;
     pl->chunk = ch < npos ? ch : npos;
     return true;
@@ -434,7 +501,7 @@ size_t conv_walk_workspace(int B, int C, int H, int W, int pad, int F, int KH, i
   if (!walk_plan(B, C, H, W, pad, F, KH, KW, T, &pl)) return 0;
   size_t n = size_t(pl.n_groups) * (pl.a.R + 1) * pl.FGS * 4;
   n = (n + 255) & ~size_t(255);
-  if (pl.pre) n += size_t(pl.chunk) * pl.a.rec * 2 + 256;  // + slack for the prefetch past the end
+  if (pl.pre) n += size_t(pl.chunk) * pl.a.rec + kListSlack;
   return n + 256;
 }
 
@@ -479,14 +546,20 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   if (!walk_plan(B, C, H, W, pad, F, KH, KW, T, &pl)) return 1;
   WalkArgs a = pl.a;
   size_t wq_bytes = (size_t(pl.n_groups) * (a.R + 1) * pl.FGS * 4 + 255) & ~size_t(255);
-  const size_t need = wq_bytes + (pl.pre ? size_t(pl.chunk) * a.rec * 2 + 256 : 0);
+  const size_t need = wq_bytes + (pl.pre ? size_t(pl.chunk) * a.rec + kListSlack : 0);
   if (ws_bytes < need) return set_error(SNN_EWORKSPACE, "snn_conv_fire: workspace %zu < %zu", ws_bytes, need);
   a.lat_in = lat_in; a.lat_out = lat_out; a.v_out = v_out;
+  a.err = error_word_ptr();
   a.wq = reinterpret_cast<const uint32_t*>(ws);
-  a.lists = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(ws) + wq_bytes);
+  a.lists = reinterpret_cast<unsigned char*>(ws) + wq_bytes;
   const double tt = floor(double(theta) * 2147483648.0);
   a.thr = tt >= 9.0e18 ? INT64_MAX : (tt < -1.0 ? -1 : int64_t(tt));
   const int64_t npos = int64_t(B) * a.Ho * a.Wo;
+  if (getenv("SNN_DEBUG_PLAN"))
+    fprintf(stderr, "walk plan: pre %d fpl %d ppw %d FGS %d groups %d warps %d smem %d | sort ppw %d "
+            "warps %d smem %d | rec %d hdr %d chunk %lld npos %lld\n", int(pl.pre), pl.fpl, pl.ppw, pl.FGS,
+            pl.n_groups, pl.nwarps, pl.smem, pl.sort_ppw, pl.sort_nwarps, pl.sort_smem, a.rec,
+            a.hdr, (long long)pl.chunk, (long long)npos);
   int rc = weight_prep_launch(w, F, a.R, pl.FGS, pl.n_groups, reinterpret_cast<uint32_t*>(ws), s);
   if (rc) return rc;
   if (!pl.pre) {

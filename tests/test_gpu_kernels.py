@@ -107,6 +107,11 @@ CONV_CASES = [
     (1, 2, 5, 5, 0, 3, 5, 4, 0.5, 0.0),             # no input spikes at all
     (3, 7, 21, 19, 2, 130, 5, 9, 6.0, 0.7),         # 3 feature chunks, ragged M tile
     (1, 4, 20, 31, 0, 20, 5, 254, 2.0, 0.3),        # T = 254
+    (2, 32, 12, 12, 2, 100, 5, 2, 40.0, 0.6),       # 2 huge buckets: crossings pend across walk blocks
+    (2, 16, 10, 10, 1, 64, 3, 3, 20.0, 0.9),        # T = 3, 64 features (one FPL=2 group)
+    (1, 9, 11, 7, 1, 256, 3, 5, 5.0, 0.5),          # 256 features on a small receptive field
+    (3, 8, 10, 10, 1, 130, 3, 40, 30.0, 1.0),       # every input spikes, T > R/2: many odd buckets (list padding)
+    (2, 8, 10, 10, 1, 30, 3, 40, 30.0, 1.0),        # the same on the fused sort+walk schedule
 ]
 
 
