@@ -390,14 +390,15 @@ static void make_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
 
 size_t conv_tc_workspace(int B, int Ho, int Wo, int R, int F);
 size_t conv_walk_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T);
-size_t conv_tct_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW);
+size_t conv_tct_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T);
 int conv_tct_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
                     int KW, int T, float theta, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes,
                     cudaStream_t s);
 
 // Finite-threshold path selection.  Default: the SIMT delta walk (conv_walk.cu).  SNN_CONV_PATH=tct
-// selects the tensor-core time-stepped kernel (conv_tct.cu; exact, but slower on every config so far,
-// DESIGN.md §7), SNN_CONV_PATH=ref the validation kernel below.
+// selects the tensor-core time-stepped kernel (conv_tct.cu; exact, parity-tested, but slower than the
+// walk on every config so far: its epilogue re-reads 16 bytes of TMEM per neuron and step, DESIGN.md
+// §7), SNN_CONV_PATH=ref the validation kernel below.
 static int conv_path_override() {
   const char* e = getenv("SNN_CONV_PATH");
   if (!e) return 1;
@@ -432,7 +433,7 @@ size_t conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, i
   } else {
     size_t t = conv_walk_workspace(B, C, H, W, pad, F, KH, KW, T);
     m = m > t ? m : t;
-    t = conv_tct_workspace(B, C, H, W, pad, F, KH, KW);
+    t = conv_tct_workspace(B, C, H, W, pad, F, KH, KW, T);
     m = m > t ? m : t;
   }
   return ((m + 255) & ~size_t(255)) + 256;

@@ -12,18 +12,30 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  // potentially blocking: the thread is suspended (up to ~1 ms, the hint in ns) until the phase completes,
+  // instead of spinning on issue slots the other warps of the SM need
   uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(bar), "r"(parity)
+      : "r"(bar), "r"(parity), "r"(0x100000u)
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// watchdog: a wait longer than 4 s is a pipeline bug; trap (the launch fails with an error) instead of
+// hanging the GPU
+__device__ __forceinline__ void watchdog(uint64_t t0) {
+  if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  // watchdog: a pipeline bug traps (the launch fails with an error) instead of hanging the GPU
-  for (uint32_t n = 0; !mbar_try(bar, parity); ++n)
-    if (n == (1u << 28)) __trap();
+  if (mbar_try(bar, parity)) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (!mbar_try(bar, parity)) watchdog(t0);
 }
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),

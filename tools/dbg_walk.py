@@ -7,9 +7,9 @@ import numpy as np, torch
 import oracle, synth
 from paper_1903_02440_b200 import snn as G
 from test_gpu_kernels import CONV_CASES, exact_weights
-sel = [int(x) for x in sys.argv[1:]] or range(len(CONV_CASES))
+sel = [eval(x) if x.startswith('(') else int(x) for x in sys.argv[1:]] or range(len(CONV_CASES))
 for ci in sel:
-    case = CONV_CASES[ci]
+    case = ci if isinstance(ci, tuple) else CONV_CASES[ci]
     B, C, H, W, pad, F, K, T, theta, p = case
     rng = np.random.default_rng(abs(hash(case)) % 2 ** 31)
     lat_in = synth.random_latencies(rng, (B, C, H, W), T, p)
