@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(512) rf_sort_kernel(const WalkArgs a) {
 }
 
 // ------------------------------------------------------------------------------------- walk
-template <int FPL> struct WalkThreads { static constexpr int v = FPL == 4 ? 640 : 1024; };
+template <int FPL, bool PRE> struct WalkThreads { static constexpr int v = FPL == 4 ? (PRE ? 640 : 768) : 1024; };
 
 // Fire every unfired feature whose potential at the end of bucket t exceeds the threshold.
 template <int FPL>
@@ -258,7 +258,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int FPL, int PPW, bool PRE>
-__global__ void __launch_bounds__(WalkThreads<FPL>::v, 1) conv_walk_kernel(const WalkArgs a) {
+__global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(const WalkArgs a) {
   constexpr int LPP = 32 / PPW;
   constexpr int FGS = LPP * FPL;
   constexpr unsigned kAll = (1u << FPL) - 1;
@@ -438,9 +438,22 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
     const long fixed = al16(int(long(R + 1) * fgs * 4)) + tables;
     if (fixed + 8L * wb > kWalkSmemLimit) continue;
     long warps = (kWalkSmemLimit - fixed) / wb;
-    const int wcap = c.fpl == 4 ? 20 : 32;
+    const int wcap = c.fpl == 4 ? 24 : 32;
     if (warps > wcap) warps = wcap;
-    if (best < 0 || warps > best_warps + 8) { best = int(&c - cands); best_warps = int(warps); }
+    if (best < 0) { best = int(&c - cands); best_warps = int(warps); }  // the first (widest FPL) that fits
+  }
+  if (const char* e = getenv("SNN_WALK_FUSED")) {  // tuning experiments: force "ppw,fpl"
+    int ppw = 0, fpl = 0;
+    if (sscanf(e, "%d,%d", &ppw, &fpl) == 2)
+      for (const Cand& c : cands)
+        if (c.ppw == ppw && c.fpl == fpl && (32 / ppw) * fpl >= F) {
+          best = int(&c - cands);
+          const int wb = c.ppw * pos_scratch_bytes(T, R, nullptr);
+          const long fixed = al16(int(long(R + 1) * (32 / ppw) * fpl * 4)) + tables;
+          long warps = (kWalkSmemLimit - fixed) / wb;
+          const int wcap = c.fpl == 4 ? 24 : 32;
+          best_warps = int(warps > wcap ? wcap : warps);
+        }
   }
   if (best >= 0) {
     pl->pre = false;
