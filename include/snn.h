@@ -169,10 +169,17 @@ SNN_API int snn_decide(const int32_t* winners, const int32_t* count, int B, int 
  *            fires) -- the inputs any exact first-spike computation must add.  0 if lat_out is NULL.
  *   lat_in uint8 [B, C, H, W], lat_out uint8 [B, F, Ho, Wo] or NULL.
  * snn_launch_count returns the number of kernels this process has launched through libsnn.
+ * snn_conv_fire_plan (host only, no GPU needed) describes what one snn_conv_fire call with the same
+ *   scalars (pot_out NULL) launches: *path = 0 fused sort+walk, 1 presorted walk (a sort and a walk
+ *   kernel per list chunk, *chunks of them), 2 tensor-core Eq. 5 (theta = +inf), 3 tensor-core
+ *   time-stepped (SNN_CONV_PATH=tct), 4 validation kernel; *launches = kernels per call.  Same
+ *   argument errors as snn_conv_fire.
  * ------------------------------------------------------------------------------------------- */
 SNN_API int snn_count_events(const uint8_t* lat_in, int B, int C, int H, int W, int pad, int F, int KH, int KW,
                              int T, const uint8_t* lat_out, unsigned long long* out, snn_stream_t s);
 SNN_API unsigned long long snn_launch_count(void);
+SNN_API int snn_conv_fire_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta,
+                               int* path, int* launches, int* chunks);
 
 /* ---------------------------------------------------------------------------------------------
  * Status.

@@ -18,6 +18,8 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, uint8_t* la
 int expand_launch(const uint8_t* lat, int B, int n, int T, float* wave, cudaStream_t s);
 int validate_launch(const uint8_t* lat, size_t n, int T, int32_t* n_bad, cudaStream_t s);
 size_t conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta);
+int conv_fire_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta, int* path,
+                   int* launches, int* chunks);
 int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
                      int KW, int T, float theta, uint8_t* lat_out, float* v_out, float* pot_out, void* ws,
                      size_t ws_bytes, cudaStream_t s);
@@ -150,6 +152,14 @@ int snn_validate_lat(const uint8_t* lat, size_t n, int T, int32_t* n_bad, snn_st
 size_t snn_conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta) {
   if (conv_checks(B, C, H, W, pad, F, KH, KW, T, theta)) return 0;
   return conv_fire_workspace(B, C, H, W, pad, F, KH, KW, T, theta);
+}
+
+int snn_conv_fire_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta, int* path,
+                       int* launches, int* chunks) {
+  int rc = conv_checks(B, C, H, W, pad, F, KH, KW, T, theta);
+  if (rc) return rc;
+  REQUIRE(path && launches && chunks, SNN_EINVAL, "snn_conv_fire_plan: NULL output");
+  return conv_fire_plan(B, C, H, W, pad, F, KH, KW, T, theta, path, launches, chunks);
 }
 
 int snn_conv_fire(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH, int KW,

@@ -410,6 +410,31 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
                      int KW, int T, float theta, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes,
                      cudaStream_t s);
 
+static int conv_path_override();
+int conv_walk_describe(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, int* pre, int* chunks);
+bool conv_tct_applies(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta);
+
+// Which kernels one snn_conv_fire call (pot_out == NULL) launches, for measurement: path 0 = fused
+// sort+walk, 1 = presorted walk (sort + walk per list chunk), 2 = tensor-core Eq. 5 (theta = inf),
+// 3 = tensor-core time-stepped (SNN_CONV_PATH=tct), 4 = validation kernel.
+int conv_fire_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta, int* path,
+                   int* launches, int* chunks) {
+  const bool inf = isinf(theta) && theta > 0;
+  *chunks = 1;
+  if (inf) { *path = 2; *launches = 3; return SNN_OK; }
+  const int ov = conv_path_override();
+  if (ov == 0 && conv_tct_applies(B, C, H, W, pad, F, KH, KW, T, theta)) { *path = 3; *launches = 2; return SNN_OK; }
+  int pre = 0, ch = 1;
+  if (ov <= 1 && conv_walk_describe(B, C, H, W, pad, F, KH, KW, T, &pre, &ch)) {
+    *path = pre ? 1 : 0;
+    *chunks = ch;
+    *launches = pre ? 1 + 2 * ch : 2;
+    return SNN_OK;
+  }
+  *path = 4; *launches = 2;
+  return SNN_OK;
+}
+
 int weight_prep_launch(const float* w, int F, int R, int FGS, int n_groups, uint32_t* wq, cudaStream_t s) {
   const int64_t total = int64_t(n_groups) * (R + 1) * FGS;
   int blocks = int(ceil_div(total, 256));

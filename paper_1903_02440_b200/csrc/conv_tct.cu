@@ -98,6 +98,11 @@ static bool t2_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW, 
   return true;
 }
 
+bool conv_tct_applies(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta) {
+  T2Plan p;
+  return theta >= 0.0f && t2_plan(B, C, H, W, pad, F, KH, KW, T, &p);
+}
+
 size_t conv_tct_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T) {
   T2Plan p;
   if (!t2_plan(B, C, H, W, pad, F, KH, KW, T, &p)) return 0;

@@ -20,9 +20,10 @@
 //    soon as all its features fired or its list is exhausted.
 //  * Two schedules.  If the layer fits one feature group (weights of all F features in shared
 //    memory), sort and walk are fused in one kernel (no list traffic).  Otherwise the sort runs ONCE
-//    per position in rf_sort_kernel, which writes compact bucketed lists to a workspace chunk that
-//    stays L2-resident, and conv_walk_kernel<PRE=true> streams them (16-byte loads, one block ahead)
-//    for every feature group -- the sort is not repeated per group.
+//    per position in rf_sort_kernel, which writes compact bucketed lists to a workspace chunk (up to
+//    512 MB: fewer, larger chunks measured faster than L2-sized ones, whose per-launch tails cost more
+//    than the HBM round trip saves), and conv_walk_kernel<PRE=true> streams them through a per-warp
+//    cp.async ring for every feature group -- the sort is not repeated per group.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -37,7 +38,8 @@ namespace snn {
 int weight_prep_launch(const float* w, int F, int R, int FGS, int n_groups, uint32_t* wq, cudaStream_t s);
 
 constexpr int kWalkSmemLimit = 227 * 1024;
-constexpr size_t kListChunkBytes = size_t(48) << 20;  // sorted lists per chunk (L2-resident)
+constexpr size_t kListChunkBytes = size_t(512) << 20;  // sorted lists per chunk (measured: fewer, larger chunks win;
+                                                        // the lists stream from HBM either way)
 constexpr int kBlk = 8;                               // list entries per gather block
 constexpr int kIt = 16;                               // list entries per walk iteration (lists padded to this)
 constexpr int kRing = 4;                              // per-warp list ring (PRE): iterations in flight + 1
@@ -501,7 +503,9 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
     sa.off_warps = sa.off_ekk + al16(R * 2);
     pl->sort_smem = sa.off_warps + pl->sort_nwarps * sa.warp_bytes;
     const int64_t npos = int64_t(B) * a.Ho * a.Wo;
-    int64_t ch = int64_t(kListChunkBytes / size_t(a.rec));
+    size_t chunk_bytes = kListChunkBytes;
+    if (const char* e = getenv("SNN_LIST_CHUNK_MB")) chunk_bytes = size_t(atoi(e)) << 20;  // tuning experiments
+    int64_t ch = int64_t(chunk_bytes / size_t(a.rec));
     if (ch < 1024) ch = 1024;
     pl->chunk = ch < npos ? ch : npos;
     return true;
@@ -549,6 +553,15 @@ static int sort_go(const WalkPlan& pl, const WalkArgs& a, cudaStream_t s) {
   k<<<int(blocks), pl.sort_nwarps * 32, pl.sort_smem, s>>>(a);
   note_launch();
   return check_launch("snn_conv_fire(sort)");
+}
+
+// Plan description for snn_conv_fire_plan: 0 if the walk does not apply, else 1 (+ *pre, *chunks).
+int conv_walk_describe(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, int* pre, int* chunks) {
+  WalkPlan pl;
+  if (!walk_plan(B, C, H, W, pad, F, KH, KW, T, &pl)) return 0;
+  *pre = pl.pre ? 1 : 0;
+  *chunks = int(ceil_div(int64_t(B) * pl.a.Ho * pl.a.Wo, pl.chunk));
+  return 1;
 }
 
 // Returns 1 if this path does not apply (caller falls back), else an SNN code.

@@ -59,6 +59,7 @@ def lib() -> C.CDLL:
                 "snn_decide": (i32, [p, p, i32, i32, i32, i32, p, p, p, p]),
                 "snn_count_events": (i32, [p, i32, i32, i32, i32, i32, i32, i32, i32, i32, p, p, p]),
                 "snn_launch_count": (C.c_ulonglong, []),
+                "snn_conv_fire_plan": (i32, [i32] * 9 + [f32, p, p, p]),
             }
             for name, (res, args) in sigs.items():
                 fn = getattr(L, name)
@@ -72,7 +73,7 @@ def exported_symbols():
     return ["snn_version", "snn_last_error", "snn_sync_status", "snn_encode_workspace", "snn_encode",
             "snn_expand", "snn_validate_lat", "snn_conv_fire_workspace", "snn_conv_fire", "snn_pool",
             "snn_inhibit", "snn_k_winners_workspace", "snn_k_winners", "snn_stdp_update", "snn_decide",
-            "snn_count_events", "snn_launch_count"]
+            "snn_count_events", "snn_launch_count", "snn_conv_fire_plan"]
 
 
 def _check(rc: int):
@@ -278,6 +279,16 @@ def count_events(lat_in: torch.Tensor, F: int, KH: int, KW: int, pad: int, T: in
                                   _stream(stream)))
     o = out.cpu().tolist()
     return int(o[0]), int(o[1])
+
+
+def conv_fire_plan(B: int, Cin: int, H: int, W: int, pad: int, F: int, KH: int, KW: int, T: int,
+                   theta: float) -> dict:
+    """What one conv_fire call launches (snn_conv_fire_plan): path, kernel launches, list chunks."""
+    path, launches, chunks = C.c_int(), C.c_int(), C.c_int()
+    _check(lib().snn_conv_fire_plan(B, Cin, H, W, pad, F, KH, KW, T, theta, C.byref(path), C.byref(launches),
+                                    C.byref(chunks)))
+    names = {0: "walk_fused", 1: "walk_presorted", 2: "tc_inf", 3: "tct", 4: "ref"}
+    return {"path": names[path.value], "launches": launches.value, "chunks": chunks.value}
 
 
 def launch_count() -> int:
