@@ -169,6 +169,7 @@ class C2Step:
                                        ("conv2", n.l1.plat, self.wl.convs[1], n.l2.lat),
                                        ("conv3", n.l2.plat, self.wl.convs[2], n.l3.lat)):
             out[name] = snn.count_events(lat_in, spec.F, spec.KH, spec.KW, spec.pad, T, lo)
+            out["_shape_" + name] = (int(lat_in.shape[1]), int(lo.shape[0] * lo.shape[2] * lo.shape[3]))
         return out
 
     def config(self):
@@ -393,26 +394,41 @@ WORKLOADS = {"c1": C1Step, "c2": C2Step, "c3": C3Step, "c4": C4Step, "c5": C5Ste
 
 
 # --------------------------------------------------------------------------------------- roofline
-def roofline(stage, t_ms, ev, wl, clocks, pk):
-    """Roofline of the dominant stage from its algorithmic work per launch."""
+def _traffic(wl_name, stage):
+    """DRAM bytes per step of the stage from the committed ncu capture (profiles/*_traffic.json), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+    if not files:
+        return None, None
+    d = json.load(open(files[-1]))
+    v = d.get(f"{wl_name}:{stage}")
+    return (int(v) if v is not None else None), os.path.relpath(files[-1], ROOT)
+
+
+def roofline(stage, t_ms, ev, wl, clocks, pk, wl_name="c2"):
+    """Roofline of the dominant stage from its algorithmic work per step."""
     f_mhz = (clocks or {}).get("sm_mhz") or pk["sm_max"]
     t = t_ms * 1e-3
     if stage.startswith("conv"):
         paper, need = ev[stage]
         idx = int(stage[-1]) - 1
         spec = wl.convs[idx]
+        traffic, tsrc = _traffic(wl_name, stage)
         if math.isinf(spec.theta):
-            # dense contraction of S[T-1]: int8 tensor-core work = 4 limbs x 2 ops per (position, feature,
-            # receptive-field entry); SIMT v1 reads one 4-byte weight per spiking event instead
-            return {"bound": "smem", "achieved": round(paper * 4 / t / 1e9, 1),
-                    "peak": round(SMEM_BYTES_PER_CLK_SM * 148 * f_mhz * 1e6 / 1e9, 1), "unit": "GB/s",
-                    "frac": round(paper * 4 / t / (SMEM_BYTES_PER_CLK_SM * 148 * f_mhz * 1e6), 4),
-                    "traffic": None, "kernel": stage, "work": f"{paper} events x 4 B (weight gathers)",
-                    "peak_src": f"128 B/clk/SM x 148 SMs x {f_mhz:.0f} MHz (measured SM clock)"}
+            # Eq. 5: one dense contraction of S[T-1] on the int8 tensor pipe, 4 exact u8 limbs per weight:
+            # 2 ops x 4 limbs x positions x F x R (algorithmic, unpadded); peak = measured bf16 x 2 (int8 rate)
+            C_in, M = ev["_shape_" + stage]  # input channels, output positions per step
+            R = C_in * spec.KH * spec.KW
+            ops = 2.0 * 4 * M * spec.F * R
+            peak = pk["bf16"] * 2e12
+            return {"bound": "tensor", "achieved": round(ops / t / 1e12, 1), "peak": round(peak / 1e12, 1),
+                    "unit": "TFLOP/s", "frac": round(ops / t / peak, 4), "traffic": traffic, "traffic_src": tsrc,
+                    "kernel": stage, "work": f"{ops:.3e} int8 ops (4 limbs x 2 x {M} positions x {spec.F} x {R})",
+                    "peak_src": f"measured bf16 {pk['bf16']} TFLOP/s x 2 (int8:bf16 nominal ratio)"}
         peak = SMEM_BYTES_PER_CLK_SM * 148 * f_mhz * 1e6
         ach = need * 4 / t
         return {"bound": "smem", "achieved": round(ach / 1e9, 1), "peak": round(peak / 1e9, 1), "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": None, "kernel": stage,
+                "frac": round(ach / peak, 4), "traffic": traffic, "traffic_src": tsrc, "kernel": stage,
                 "work": f"{need} necessary events x 4 B weight gather (of {paper} paper-definition events)",
                 "peak_src": f"128 B/clk/SM x 148 SMs x {f_mhz:.0f} MHz (measured SM clock)"}
     if stage.startswith("seq") or stage == "step":
@@ -497,7 +513,7 @@ def run_ours(args, rank, world, local):
     value = units / (total_ms * 1e-3)
     # ---------------- off-clock: events, e2e, cpu baseline ----------------
     ev_counts = step.events()
-    paper_events = sum(v[0] for v in ev_counts.values())
+    paper_events = sum(v[0] for k, v in ev_counts.items() if not k.startswith("_"))
     e2e = None
     if not args.no_e2e and not args.profile:
         xh, oh = step.host_io()
@@ -519,7 +535,12 @@ def run_ours(args, rank, world, local):
         return
     pk = peaks()
     dom = max(range(nst), key=lambda i: stage_ms[i])
-    roof = roofline(step.stages[dom], stage_ms[dom], ev_counts, step.wl, clocks, pk)
+    roof = roofline(step.stages[dom], stage_ms[dom], ev_counts, step.wl, clocks, pk, step.name)
+    stage_roofs = {}
+    for i, st in enumerate(step.stages):  # every conv stage, for context (the dominant one is "roofline")
+        if st.startswith("conv") and st in ev_counts:
+            r_ = roofline(st, stage_ms[i], ev_counts, step.wl, clocks, pk, step.name)
+            stage_roofs[st] = {k: r_[k] for k in ("bound", "achieved", "unit", "frac", "traffic")}
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
         n = {"c1": 1, "c2": 1000, "c3": 200, "c4": 30, "c5": 1}[step.name]
@@ -536,7 +557,7 @@ def run_ours(args, rank, world, local):
             "events_per_sec": round(paper_events * args.steps * world / (total_ms * 1e-3), 1),
             "events_per_step": paper_events,
             "stages_ms": {s: round(m, 4) for s, m in zip(step.stages, stage_ms)},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "roofline": roof, "stage_rooflines": stage_roofs, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": int(launches),
             "peaks": {"src": pk["src"], "hbm_gbs": pk["hbm"], "bf16_tflops": pk["bf16"]}}
     print(json.dumps(line), flush=True)

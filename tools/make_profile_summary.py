@@ -1,6 +1,6 @@
 """Summarise a GPU measurement session (gpurun_out/) into profiles/: bench lines, per-kernel launch
 shares (ncu gpu__time_duration list) and DRAM traffic of the captured kernels (ncu --set full).
-usage: python tools/make_profile_summary.py <tag>      (writes profiles/<tag>_summary.md, _traffic.json)"""
+usage: python tools/make_profile_summary.py <tag>      (writes profiles/<tag>_summary.md, _kernel_dram.json)"""
 import collections, csv, io, json, os, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -63,6 +63,6 @@ for rep in sorted(f for f in os.listdir(G) if f.endswith(".ncu-rep")):
                    f"{f('l1tex__data_pipe_lsu_wavefronts_mem_shared.sum')/f('sm__cycles_elapsed.avg')/148:.2f} | "
                    f"{f('sm__warps_active.avg.pct_of_peak_sustained_active'):.1f} | {x.get('launch__registers_per_thread')} |")
 open(os.path.join(ROOT, "profiles", f"{tag}_summary.md"), "w").write("\n".join(out) + "\n")
-json.dump({k: sum(v) / len(v) for k, v in traffic.items()}, open(os.path.join(ROOT, "profiles", f"{tag}_traffic.json"), "w"),
+json.dump({k: sum(v) / len(v) for k, v in traffic.items()}, open(os.path.join(ROOT, "profiles", f"{tag}_kernel_dram.json"), "w"),
           indent=1)
 print("\n".join(out[:40]))
