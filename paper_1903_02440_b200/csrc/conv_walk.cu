@@ -42,8 +42,7 @@ constexpr size_t kListChunkBytes = size_t(512) << 20;  // sorted lists per chunk
                                                         // the lists stream from HBM either way)
 constexpr int kBlk = 8;                               // list entries per gather block
 constexpr int kIt = 16;                               // list entries per walk iteration (lists padded to this)
-constexpr int kRing = 4;                              // per-warp list ring (PRE): iterations in flight + 1
-constexpr int kListSlack = kRing * kIt * 4;           // bytes read past the last record (prefetch)
+constexpr int kListSlack = 2048;                      // bytes read past the last record (prefetch)
 
 struct WalkArgs {
   const uint8_t* lat_in;
@@ -61,6 +60,7 @@ struct WalkArgs {
   int rec, hdr;       // bytes per record; bytes of its header (T+1 u16 bucket starts, 16-aligned)
   int64_t p0, np;     // chunk of positions [p0, p0 + np)
   int* err;           // device error word
+  int npre, buf_bytes; // PRE: list entries prefetched per position (one bulk copy), bytes of one buffer
 };
 
 static inline int al16(int x) { return (x + 15) & ~15; }
@@ -252,13 +252,6 @@ __device__ __forceinline__ void walk_block(const unsigned char* wl, const uint4&
   for (int j = 0; j < FPL; ++j) acc[j] = s[j];
 }
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
 template <int FPL, int PPW, bool PRE>
 __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(const WalkArgs a) {
   constexpr int LPP = 32 / PPW;
@@ -296,24 +289,44 @@ __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(
   const int64_t thr = a.thr;
   const unsigned char* wl = smem + gl * FPL * 4;  // this lane's features in weight row 0
 
-  for (int64_t wi = int64_t(blockIdx.x) * nwarps + warp; wi * PPW < a.np; wi += stride_w) {
+  // PRE: two per-warp position buffers [header | first npre entries], each filled by one bulk copy
+  // (TMA, mbarrier completion) issued one position ahead, so the list of the next position streams in
+  // while this one is walked; entries past npre (rare long walks) are read from global memory
+  uint64_t* pmb = reinterpret_cast<uint64_t*>(pb);
+  unsigned char* pbuf = pb + 16;
+  if constexpr (PRE) {
+    if (lane == 0) {
+      mbar_init(smem_u32(&pmb[0]), 1);
+      mbar_init(smem_u32(&pmb[1]), 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      const int64_t w0 = int64_t(blockIdx.x) * nwarps + warp;
+      if (w0 < a.np) {
+        mbar_expect_tx(smem_u32(&pmb[0]), uint32_t(a.buf_bytes));
+        bulk_g2s(smem_u32(pbuf), a.lists + w0 * a.rec, uint32_t(a.buf_bytes), smem_u32(&pmb[0]));
+      }
+    }
+    __syncwarp();
+  }
+  int npos_done = 0;
+  for (int64_t wi = int64_t(blockIdx.x) * nwarps + warp; wi * PPW < a.np; wi += stride_w, ++npos_done) {
     const int64_t q = wi * PPW + grp;
     const bool pv = q < a.np;
     const int p = int(a.p0 + q);  // npos < 2^31 (checked by the planner)
     const int b = pv ? p / HoWo : 0;
     const int rem = pv ? p - b * HoWo : 0;
-    const unsigned char* ent = nullptr;  // PRE: this position's entries in global memory (L2)
+    const unsigned char* ent = nullptr;   // PRE: this position's entries in global memory
+    const unsigned char* sent = nullptr;  // PRE: its first npre entries in shared memory
     if constexpr (PRE) {
-      const unsigned char* rec = a.lists + (pv ? q : 0) * a.rec;
-      ent = rec + a.hdr;
-      cp_async_wait<0>();  // the previous position's copies into the ring have landed
-      __syncwarp();
-      if (lane < 4)  // the first kRing-1 iterations of entries -> ring, ahead of the header
-        for (int r = 0; r < kRing - 1; ++r) cp_async16(list + r * kIt + lane * 4, ent + r * kIt * 4 + lane * 16);
-      for (int r = 0; r < kRing - 1; ++r) cp_async_commit();
-      const uint16_t* h = reinterpret_cast<const uint16_t*>(rec);
-      for (int t = gl; t <= T; t += LPP) start[t] = pv ? h[t] : 0;
-      __syncwarp();
+      const int bi = npos_done & 1;
+      if (lane == 0 && (wi + stride_w) * PPW < a.np) {  // prefetch the next position into the other buffer
+        mbar_expect_tx(smem_u32(&pmb[bi ^ 1]), uint32_t(a.buf_bytes));
+        bulk_g2s(smem_u32(pbuf + (bi ^ 1) * a.buf_bytes), a.lists + (wi + stride_w) * a.rec, uint32_t(a.buf_bytes),
+                 smem_u32(&pmb[bi ^ 1]));
+      }
+      mbar_wait(smem_u32(&pmb[bi]), (npos_done >> 1) & 1);
+      start = reinterpret_cast<uint16_t*>(pbuf + bi * a.buf_bytes);
+      sent = pbuf + bi * a.buf_bytes + a.hdr;
+      ent = a.lists + q * a.rec + a.hdr;
     } else {
       const int y = rem / a.Wo, x = rem - (rem / a.Wo) * a.Wo;
       const int y0 = y - a.pad, x0 = x - a.pad;
@@ -347,18 +360,9 @@ __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(
     // Every vote below is a full-warp ballot at a converged point; done is group-uniform.
     while (true) {
       if (__ballot_sync(0xffffffffu, !done) == 0) break;
-      const uint4* cur;  // this iteration's 16 entries, in shared memory
-      if constexpr (PRE) cur = reinterpret_cast<const uint4*>(list + (it % kRing) * kIt);
+      const uint4* cur;  // this iteration's 16 entries (shared memory; PRE past npre: global memory)
+      if constexpr (PRE) cur = reinterpret_cast<const uint4*>(it * kIt < a.npre ? sent + it * kIt * 4 : ent + it * kIt * 4);
       else cur = reinterpret_cast<const uint4*>(list + it * kIt);
-      if constexpr (PRE) {  // keep kRing-1 iterations of list entries in flight
-        if (!done) {
-          if (lane < 4)
-            cp_async16(list + ((it + kRing - 1) % kRing) * kIt + lane * 4, ent + (it + kRing - 1) * kIt * 4 + lane * 16);
-          cp_async_commit();
-          cp_async_wait<kRing - 1>();
-        }
-        __syncwarp();
-      }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         if (!done) {
@@ -397,7 +401,6 @@ __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(
     }
     __syncwarp();
   }
-  if constexpr (PRE) cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------------------------- host
@@ -475,20 +478,30 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
   }
   // 2) presorted: sort once per position, walk per feature group (PPW = 1, the largest FPL that fits)
   const int fpls[3] = {4, 2, 1};
+  const char* fe = getenv("SNN_WALK_PRE_FPL");  // tuning experiments: force the presorted FPL
+  const int force_fpl = fe ? atoi(fe) : 0;
   for (int k = 0; k < 3; ++k) {
     const int fpl = fpls[k], fgs = 32 * fpl;
-    if (fgs > 32 && F <= fgs / 2) continue;
+    if (force_fpl && fpl != force_fpl) continue;
+    if (!force_fpl && fgs > 32 && F <= fgs / 2) continue;
     const long wsb = long(R + 1) * fgs * 4;
     const int hdr_bytes = al16((T + 1) * 2);
-    if (al16(int(wsb)) + 32L * (hdr_bytes + kRing * kIt * 4) > kWalkSmemLimit) continue;
+    if (al16(int(wsb)) + 20L * (16 + 2 * (hdr_bytes + kIt * 4)) > kWalkSmemLimit) continue;
     pl->sort_ppw = R <= 256 ? 4 : 1;  // 4 positions per warp for small receptive fields
     pl->pre = true;
     pl->ppw = 1; pl->fpl = fpl; pl->FGS = fgs;
     pl->n_groups = int(ceil_div(F, fgs));
     pl->nwarps = fpl == 4 ? 20 : 32;
     a.row_bytes = fgs * 4;
-    a.cnt_off = 0; a.start_off = 0; a.list_off = hdr_bytes;  // per warp: bucket starts, then the list ring
-    a.pos_bytes = hdr_bytes + kRing * kIt * 4; a.warp_bytes = a.pos_bytes;
+    // per warp: 2 mbarriers, then two position buffers [header | npre entries]
+    const long left = (kWalkSmemLimit - al16(int(wsb))) / pl->nwarps - 16;
+    int npre = int(((left / 2 - hdr_bytes) / 4) / kIt) * kIt;
+    if (npre > 256) npre = 256;
+    if (npre < kIt) continue;
+    a.npre = npre;
+    a.buf_bytes = hdr_bytes + npre * 4;
+    a.cnt_off = 0; a.start_off = 0; a.list_off = 0;
+    a.pos_bytes = 16 + 2 * a.buf_bytes; a.warp_bytes = a.pos_bytes;
     a.off_eoff = al16(int(wsb)); a.off_ekk = a.off_eoff; a.off_warps = a.off_eoff;
     pl->smem = a.off_warps + pl->nwarps * a.warp_bytes;
     a.hdr = hdr_bytes;
