@@ -360,9 +360,20 @@ __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(
     // Every vote below is a full-warp ballot at a converged point; done is group-uniform.
     while (true) {
       if (__ballot_sync(0xffffffffu, !done) == 0) break;
-      const uint4* cur;  // this iteration's 16 entries (shared memory; PRE past npre: global memory)
-      if constexpr (PRE) cur = reinterpret_cast<const uint4*>(it * kIt < a.npre ? sent + it * kIt * 4 : ent + it * kIt * 4);
-      else cur = reinterpret_cast<const uint4*>(list + it * kIt);
+      uint4 cur[4];  // this iteration's 16 entries: shared memory (PRE past npre: global memory)
+      if (PRE && it * kIt >= a.npre) {
+        const uint4* g4 = reinterpret_cast<const uint4*>(ent + it * kIt * 4);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cur[u] = __ldg(g4 + u);
+      } else {
+        const uint32_t sa = smem_u32(PRE ? static_cast<const void*>(sent + it * kIt * 4)
+                                         : static_cast<const void*>(list + it * kIt));
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(cur[u].x), "=r"(cur[u].y), "=r"(cur[u].z), "=r"(cur[u].w)
+                       : "r"(sa + 16 * u));
+      }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         if (!done) {
