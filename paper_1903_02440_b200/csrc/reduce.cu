@@ -100,6 +100,35 @@ __global__ void __launch_bounds__(256) inhibit_warp_kernel(const uint8_t* __rest
     const int64_t b = q / HW, p = q - b * HW;
     const int64_t base = b * F * HW + p;
     uint64_t best = ~uint64_t(0);
+    if (F <= 256) {  // all of the lane's (lat, v) loads in flight at once, kept for the write-back
+      uint32_t l[8];
+      float vv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int f = lane + 32 * j;
+        l[j] = f < F ? lat[base + int64_t(f) * HW] : kNoSpike;
+        vv[j] = f < F ? v[base + int64_t(f) * HW] : 0.0f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (l[j] != kNoSpike) {
+          const uint64_t k = wta_key(uint8_t(l[j]), vv[j], uint32_t(lane + 32 * j));
+          best = k < best ? k : best;
+        }
+      best = warp_min_u64(best);
+      const int fw = best == ~uint64_t(0) ? -1 : int(best & 0xFFFFFFu);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int f = lane + 32 * j;
+        if (f < F) {
+          const int64_t i = base + int64_t(f) * HW;
+          lat_out[i] = f == fw ? uint8_t(l[j]) : kNoSpike;
+          v_out[i] = f == fw ? vv[j] : 0.0f;
+        }
+      }
+      if (winner_f && lane == 0) winner_f[q] = int16_t(fw);
+      continue;
+    }
     for (int f = lane; f < F; f += 32) {
       const uint8_t l = lat[base + int64_t(f) * HW];
       if (l == kNoSpike) continue;
@@ -178,14 +207,60 @@ __global__ void __launch_bounds__(256) kwta_posbest_warp_kernel(const uint8_t* _
     const uint8_t* lp = lat + int64_t(b) * F * HW + p;
     const float* vp = v + int64_t(b) * F * HW + p;
     uint64_t best = ~uint64_t(0);
+#pragma unroll 4
     for (int f = lane; f < F; f += 32) {
       const uint8_t l = lp[f * HW];
+      const float vf = vp[f * HW];
       if (l == kNoSpike) continue;
-      const uint64_t k = wta_key(l, vp[f * HW], uint32_t(f * HW + p));
+      const uint64_t k = wta_key(l, vf, uint32_t(f * HW + p));
       best = k < best ? k : best;
     }
     best = warp_min_u64(best);
     if (lane == 0) pos_best[q] = best;
+  }
+}
+
+// Stage 1 with candidate lists (k + 1 <= kTopM, F <= 512, H*W <= kKwtaSmemPos): one warp per
+// position keeps its features' keys in registers and extracts the M = k + 1 smallest in ascending
+// order.  A position can lose at most k - 1 features to earlier winners before its last use, so its
+// best remaining candidate is always in the list (or the list holds all its spiking features): the
+// rounds never rescan the maps.
+constexpr int kTopM = 17;
+__global__ void __launch_bounds__(256) kwta_topk_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
+                                                        int B, int F, int HW, int M, uint64_t* __restrict__ pos_best,
+                                                        uint64_t* __restrict__ topk) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = int64_t(B) * HW;
+  for (int64_t q = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; q < total;
+       q += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    const int b = int(q / HW), p = int(q - int64_t(b) * HW);
+    const uint8_t* lp = lat + int64_t(b) * F * HW + p;
+    const float* vp = v + int64_t(b) * F * HW + p;
+    uint64_t key[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int f = lane + 32 * j;
+      key[j] = ~uint64_t(0);
+      if (f < F) {  // lat and v loads independent: all in flight
+        const uint8_t l = lp[int64_t(f) * HW];
+        const float vf = vp[int64_t(f) * HW];
+        if (l != kNoSpike) key[j] = wta_key(l, vf, uint32_t(f * HW + p));
+      }
+    }
+    uint64_t prev = 0;
+    bool first = true;
+    for (int m = 0; m < M; ++m) {
+      uint64_t mn = ~uint64_t(0);
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if ((first || key[j] > prev) && key[j] < mn) mn = key[j];
+      mn = warp_min_u64(mn);
+      if (lane == 0) topk[q * M + m] = mn;
+      if (m == 0 && lane == 0) pos_best[q] = mn;
+      prev = mn;
+      first = false;
+      if (mn == ~uint64_t(0)) break;  // fewer than M spiking features: ~0 ends the list (read no further)
+    }
   }
 }
 
@@ -201,9 +276,10 @@ constexpr int kKwtaQueue = 4096;
 __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t* __restrict__ lat,
                                                                    const float* __restrict__ v, int F, int H, int W,
                                                                    int k, int r, uint64_t* __restrict__ pos_best,
+                                                                   const uint64_t* __restrict__ topk, int M,
                                                                    int32_t* __restrict__ winners,
                                                                    int32_t* __restrict__ count, int use_smem) {
-  extern __shared__ uint64_t dyn[];
+  extern __shared__ uint64_t dyn[];  // [HW] current keys, then (topk) [HW] list cursors (u8)
   __shared__ uint32_t fexcl[256];  // bitmask of excluded features (F <= 8192)
   __shared__ int wy[kMaxK], wx[kMaxK];
   __shared__ uint64_t red[32];
@@ -217,8 +293,13 @@ __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t
   const float* vb = v + int64_t(b) * F * HW;
   const int nwords = (F + 31) >> 5;
   for (int i = threadIdx.x; i < nwords; i += blockDim.x) fexcl[i] = 0;
+  uint8_t* cur = reinterpret_cast<uint8_t*>(dyn + HW);
+  const uint64_t* tk = topk ? topk + int64_t(b) * HW * M : nullptr;
   if (use_smem)
-    for (int p = threadIdx.x; p < HW; p += blockDim.x) dyn[p] = pbg[p];
+    for (int p = threadIdx.x; p < HW; p += blockDim.x) {
+      dyn[p] = pbg[p];
+      if (topk) cur[p] = 0;
+    }
   if (threadIdx.x == 0) s_count = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -235,6 +316,21 @@ __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t
       for (int i = 0; i < nw; ++i) near |= (abs(y - wy[i]) <= r) && (abs(x - wx[i]) <= r);
       if (near) continue;
       const int f = int(uint32_t(key & 0xFFFFFFu) / uint32_t(HW));
+      if (tk && (fexcl[f >> 5] >> (f & 31) & 1)) {  // its best feature already won: next in its list
+        int c = cur[p];
+        uint64_t kk = key;
+        for (;;) {
+          ++c;
+          kk = c < M ? tk[int64_t(p) * M + c] : ~uint64_t(0);
+          if (kk == ~uint64_t(0)) break;
+          const int ff = int(uint32_t(kk & 0xFFFFFFu) / uint32_t(HW));
+          if (!(fexcl[ff >> 5] >> (ff & 31) & 1)) break;
+        }
+        cur[p] = uint8_t(c < M ? c : M);
+        pb[p] = kk;
+        best = kk < best ? kk : best;
+        continue;
+      }
       if (fexcl[f >> 5] >> (f & 31) & 1) {  // its best feature already won: re-evaluate below
         const int slot = atomicAdd(&s_qn, 1);
         if (slot < kKwtaQueue) queue[slot] = p;
@@ -304,7 +400,9 @@ __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t
 
 size_t k_winners_workspace(int B, int F, int H, int W) {
   (void)F;
-  return size_t(B) * H * W * sizeof(uint64_t) + 256;
+  // current key per position + (maps up to kKwtaSmemPos positions) candidate lists of up to kTopM keys
+  const size_t per = (size_t(H) * W <= size_t(kKwtaSmemPos)) ? 1 + size_t(kTopM) : 1;
+  return size_t(B) * H * W * sizeof(uint64_t) * per + 256;
 }
 
 int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, int k, int r, int32_t* winners,
@@ -318,16 +416,25 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
   int64_t blocks = ceil_div(total, 256);
   if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
   if (blocks < 1) blocks = 1;
-  if (total <= kWarpPerPosMax)
-    kwta_posbest_warp_kernel<<<int(ceil_div(total, 8)), 256, 0, s>>>(lat, v, B, F, int(HW), pb);
-  else
-    kwta_posbest_kernel<<<int(blocks), 256, 0, s>>>(lat, v, B, F, int(HW), pb);
-  note_launch();
   const int use_smem = HW <= kKwtaSmemPos;
-  const size_t smem = use_smem ? size_t(HW) * sizeof(uint64_t) : 0;
+  const int M = k + 1;
+  const bool lists = k >= 2 && total <= kWarpPerPosMax && use_smem && M <= kTopM && F <= 512 &&
+                     ws_bytes >= size_t(B) * HW * sizeof(uint64_t) * (1 + size_t(M));
+  uint64_t* topk = lists ? pb + total : nullptr;
+  if (lists) {
+    int64_t wb = ceil_div(total, 8);
+    if (wb > int64_t(num_sms()) * 32) wb = int64_t(num_sms()) * 32;
+    kwta_topk_kernel<<<int(wb), 256, 0, s>>>(lat, v, B, F, int(HW), M, pb, topk);
+  } else if (total <= kWarpPerPosMax) {
+    kwta_posbest_warp_kernel<<<int(ceil_div(total, 8)), 256, 0, s>>>(lat, v, B, F, int(HW), pb);
+  } else {
+    kwta_posbest_kernel<<<int(blocks), 256, 0, s>>>(lat, v, B, F, int(HW), pb);
+  }
+  note_launch();
+  const size_t smem = use_smem ? size_t(HW) * sizeof(uint64_t) + (lists ? size_t(HW) : 0) : 0;
   cudaError_t e = cudaFuncSetAttribute(kwta_rounds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_k_winners: %s", cudaGetErrorString(e));
-  kwta_rounds_kernel<<<B, kKwtaThreads, smem, s>>>(lat, v, F, H, W, k, r, pb, winners, count, use_smem);
+  kwta_rounds_kernel<<<B, kKwtaThreads, smem, s>>>(lat, v, F, H, W, k, r, pb, topk, M, winners, count, use_smem);
   note_launch();
   return check_launch("snn_k_winners");
 }

@@ -205,7 +205,9 @@ def test_inhibit_vs_oracle(G, orc, F, levels, hw):
 @pytest.mark.parametrize("B,F,H,W,k,r,p,levels", [(4, 30, 28, 28, 5, 3, 0.3, 0), (3, 250, 14, 14, 8, 2, 0.5, 3),
                                                  (2, 7, 5, 6, 20, 0, 0.5, 2), (2, 3, 4, 4, 5, 1, 0.05, 0),
                                                  (2, 256, 64, 64, 16, 4, 0.2, 0), (3, 1, 9, 9, 3, 0, 1.0, 1),
-                                                 (2, 4, 3, 3, 2, 5, 0.0, 0), (1, 9, 140, 141, 6, 3, 0.3, 2)])
+                                                 (2, 4, 3, 3, 2, 5, 0.0, 0), (1, 9, 140, 141, 6, 3, 0.3, 2),
+                                                 (2, 500, 12, 12, 16, 1, 0.7, 3),   # candidate lists, F near 512
+                                                 (2, 600, 10, 10, 6, 1, 0.6, 2)])   # F > 512: rescan path
 def test_k_winners_vs_oracle(G, orc, B, F, H, W, k, r, p, levels):
     import synth
     rng = np.random.default_rng(B * 1000 + F)
