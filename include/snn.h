@@ -160,6 +160,28 @@ SNN_API int snn_decide(const int32_t* winners, const int32_t* count, int B, int 
                const int32_t* labels, int32_t* decision, float* reward, snn_stream_t s);
 
 /* ---------------------------------------------------------------------------------------------
+ * snn_stdp_sequence -- N sequential plasticity steps of one conv layer in ONE persistent kernel
+ * (P:95).  For image i = 0..N-1, in order:
+ *   conv + fire of lat_in[i] with the current weights (Eq. 2, theta finite, R3-R8),
+ *   pointwise inhibition (R13/R14), k-WTA with radius r on the inhibited map (R15),
+ *   STDP (Eq. 4, R17-R20) of the winners' weights, in place,
+ * exactly as snn_conv_fire + snn_inhibit + snn_k_winners + snn_stdp_update called image by image
+ * (bit-identical results).  lat_in uint8 [N, C, H, W]; w fp32 [F, C, KH, KW] (in place, every
+ * weight in the exact domain of N1); winners int32 [N, k, 3] (-1 padded) and count int32 [N] are
+ * written for every image; snapshots (nullable) fp32 [N / snap_every, F, C, KH, KW] receive the
+ * weights after images snap_every, 2 snap_every, ...  Workspace: snn_stdp_sequence_workspace.
+ * Cooperative launch (one CTA per SM, grid-wide barriers between the stages of an image).
+ * Errors: as snn_conv_fire; SNN_ESHAPE if theta is infinite or the layer's weight slice / scratch
+ * does not fit shared memory (use the per-call functions then); SNN_EINVAL for k outside [1, 256],
+ * r < 0, lb >= ub, snap_every < 1 with snapshots.  SNN_EINEXACT (device) as snn_conv_fire.
+ * ------------------------------------------------------------------------------------------- */
+SNN_API size_t snn_stdp_sequence_workspace(int N, int C, int H, int W, int pad, int F, int KH, int KW, int T, int k);
+SNN_API int snn_stdp_sequence(const uint8_t* lat_in, int N, int C, int H, int W, int pad, float* w, int F, int KH,
+                              int KW, int T, float theta, int k, int r, float a_plus, float a_minus, float lb,
+                              float ub, int stabilizer, int32_t* winners, int32_t* count, float* snapshots,
+                              int snap_every, void* ws, size_t ws_bytes, snn_stream_t s);
+
+/* ---------------------------------------------------------------------------------------------
  * Measurement helpers (off the hot path).
  * snn_count_events writes two uint64 counters to out[0..1] (device), overwriting them:
  *   out[0] = synaptic events as the paper's delta contraction defines them: F * sum over output

@@ -28,6 +28,11 @@ int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, 
 int inhibit_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, uint8_t* lat_out, float* v_out,
                    int16_t* winner_f, cudaStream_t s);
 size_t k_winners_workspace(int B, int F, int H, int W);
+size_t seq_train_workspace(int C, int H, int W, int pad, int F, int KH, int KW, int T, int k, int N);
+int seq_train_launch(const uint8_t* lat_all, int N, int C, int H, int W, int pad, float* w, int F, int KH, int KW,
+                     int T, float theta, int k, int r, float a_plus, float a_minus, float lb, float ub,
+                     int stabilizer, int32_t* winners, int32_t* count, float* snaps, int snap_every, void* ws,
+                     size_t ws_bytes, cudaStream_t st);
 int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, int k, int r, int32_t* winners,
                      int32_t* count, void* ws, size_t ws_bytes, cudaStream_t s);
 int stdp_launch(float* w, int F, int C, int KH, int KW, const uint8_t* lat_in, int H, int W, int pad,
@@ -152,6 +157,31 @@ int snn_validate_lat(const uint8_t* lat, size_t n, int T, int32_t* n_bad, snn_st
 size_t snn_conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta) {
   if (conv_checks(B, C, H, W, pad, F, KH, KW, T, theta)) return 0;
   return conv_fire_workspace(B, C, H, W, pad, F, KH, KW, T, theta);
+}
+
+size_t snn_stdp_sequence_workspace(int N, int C, int H, int W, int pad, int F, int KH, int KW, int T, int k) {
+  if (N < 0 || C < 1 || H < 1 || W < 1 || pad < 0 || F < 1 || KH < 1 || KW < 1 || T < 1 || T > 254 || k < 1) return 0;
+  return seq_train_workspace(C, H, W, pad, F, KH, KW, T, k, N);
+}
+
+int snn_stdp_sequence(const uint8_t* lat_in, int N, int C, int H, int W, int pad, float* w, int F, int KH, int KW,
+                      int T, float theta, int k, int r, float a_plus, float a_minus, float lb, float ub,
+                      int stabilizer, int32_t* winners, int32_t* count, float* snapshots, int snap_every, void* ws,
+                      size_t ws_bytes, snn_stream_t s) {
+  int rc = conv_checks(N, C, H, W, pad, F, KH, KW, T, theta);
+  if (rc) return rc;
+  REQUIRE(k >= 1 && k <= 256, SNN_EINVAL, "snn_stdp_sequence: k=%d outside [1, 256]", k);
+  REQUIRE(r >= 0, SNN_EINVAL, "snn_stdp_sequence: r=%d < 0", r);
+  REQUIRE(lb < ub, SNN_EINVAL, "snn_stdp_sequence: lb >= ub");
+  REQUIRE(!snapshots || snap_every >= 1, SNN_EINVAL, "snn_stdp_sequence: snap_every < 1");
+  REQUIRE(lat_in && w && winners && count && ws, SNN_EINVAL, "snn_stdp_sequence: NULL pointer");
+  if (N == 0) return SNN_OK;
+  rc = seq_train_launch(lat_in, N, C, H, W, pad, w, F, KH, KW, T, theta, k, r, a_plus, a_minus, lb, ub, stabilizer,
+                        winners, count, snapshots, snap_every, ws, ws_bytes, S(s));
+  if (rc == 1)
+    return set_error(SNN_ESHAPE, "snn_stdp_sequence: layer not supported by the persistent kernel "
+                                 "(infinite threshold, or weights/scratch exceed shared memory)");
+  return rc;
 }
 
 int snn_conv_fire_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta, int* path,

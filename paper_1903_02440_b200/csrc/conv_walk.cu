@@ -32,128 +32,11 @@
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
+#include "walk_dev.cuh"
 
 namespace snn {
 
 int weight_prep_launch(const float* w, int F, int R, int FGS, int n_groups, uint32_t* wq, cudaStream_t s);
-
-constexpr int kWalkSmemLimit = 227 * 1024;
-constexpr size_t kListChunkBytes = size_t(512) << 20;  // sorted lists per chunk (measured: fewer, larger chunks win;
-                                                        // the lists stream from HBM either way)
-constexpr int kBlk = 8;                               // list entries per gather block
-constexpr int kIt = 16;                               // list entries per walk iteration (lists padded to this)
-constexpr int kListSlack = 2048;                      // bytes read past the last record (prefetch)
-
-struct WalkArgs {
-  const uint8_t* lat_in;
-  int B, C, H, W, pad;
-  int F, KH, KW, T, Ho, Wo, R;
-  const uint32_t* wq;  // [n_groups][R+1][FGS]
-  int64_t thr;
-  uint8_t* lat_out;
-  float* v_out;
-  int off_eoff, off_ekk, off_warps, warp_bytes, pos_bytes;
-  int cnt_off, start_off, list_off;
-  int row_bytes;      // bytes per weight row of the walk's slice (FGS * 4): list entries are row * row_bytes
-  // presorted lists: record of position p (chunk-relative) at lists + (p - p0) * rec bytes
-  unsigned char* lists;
-  int rec, hdr;       // bytes per record; bytes of its header (T+1 u16 bucket starts, 16-aligned)
-  int64_t p0, np;     // chunk of positions [p0, p0 + np)
-  int* err;           // device error word
-  int npre, buf_bytes; // PRE: list entries prefetched per position (one bulk copy), bytes of one buffer
-};
-
-static inline int al16(int x) { return (x + 15) & ~15; }
-
-template <int FPL> struct WalkVec;
-template <> struct WalkVec<1> { typedef uint32_t T; };
-template <> struct WalkVec<2> { typedef uint2 T; };
-template <> struct WalkVec<4> { typedef uint4 T; };
-
-template <int FPL>
-__device__ __forceinline__ void wgather(const unsigned char* p, uint32_t (&o)[FPL]) {
-  typedef typename WalkVec<FPL>::T V;
-  const V v = *reinterpret_cast<const V*>(p);
-  if constexpr (FPL == 1) { o[0] = v; }
-  else if constexpr (FPL == 2) { o[0] = v.x; o[1] = v.y; }
-  else { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
-}
-
-__device__ __forceinline__ uint8_t rf_lat(const WalkArgs& a, const int32_t* eoff, const uint16_t* ekk,
-                                          const uint8_t* in, bool interior, int y0, int x0, int e) {
-  if (interior) return in[eoff[e]];
-  const int kk = ekk[e], ky = kk >> 8, kx = kk & 0xFF;
-  const bool ok = (y0 + ky >= 0) && (y0 + ky < a.H) && (x0 + kx >= 0) && (x0 + kx < a.W);
-  return ok ? in[eoff[e]] : kNoSpike;
-}
-
-// Counting sort of one position's receptive field by a group of LPP lanes into (start, list).
-// Pass 1 counts the spiking inputs of each bucket with shared-memory atomics (independent, no
-// read-modify-write chains in the lane); the counts are scanned (each bucket padded to an even
-// length with the zero-weight row R, so every bucket end is on a pair boundary) into the bucket
-// starts; pass 2 re-reads the latencies (L1-resident) and takes each entry's slot with an atomic on
-// the bucket's running position.  Entries are weight-row byte offsets e * row_bytes; the tail is
-// padded to a whole walk iteration.  The order inside a bucket is whatever the atomics gave: it does
-// not change any result (the sum at a bucket end is exact and order-free).
-template <int LPP>
-__device__ __forceinline__ void rf_sort_group(const WalkArgs& a, const int32_t* eoff, const uint16_t* ekk, bool pv,
-                                              const uint8_t* in, bool interior, int y0, int x0, int gl,
-                                              uint32_t* cnt, uint16_t* start, uint32_t* list) {
-  const int R = a.R, T = a.T;
-  const uint32_t rb = uint32_t(a.row_bytes);
-  for (int t = gl; t < T; t += LPP) cnt[t] = 0;
-  __syncwarp();
-  if (pv) {
-#pragma unroll 4
-    for (int e = gl; e < R; e += LPP) {
-      const int l = rf_lat(a, eoff, ekk, in, interior, y0, x0, e);
-      if (l < T) atomicAdd(&cnt[l], 1u);
-    }
-  }
-  __syncwarp();
-  int carry = 0;
-  for (int tb = 0; tb < T; tb += LPP) {
-    const int t = tb + gl;
-    const int tot = t < T ? int(cnt[t]) : 0;
-    const int padded = tot + (tot & 1);  // buckets padded to even length: every bucket end is on a pair boundary
-    int inc = padded;
-#pragma unroll
-    for (int o = 1; o < LPP; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, inc, o, LPP);
-      if (gl >= o) inc += v;
-    }
-    const int st = carry + inc - padded;
-    if (t < T) {
-      start[t] = uint16_t(st);
-      cnt[t] = uint32_t(st);                           // pass 2: running slot of the bucket
-      if (tot & 1) list[st + tot] = uint32_t(R) * rb;  // the pad entry: zero-weight row
-    }
-    carry += __shfl_sync(0xffffffffu, inc, LPP - 1, LPP);
-  }
-  if (gl == 0) start[T] = uint16_t(carry);
-  __syncwarp();
-  if (pv) {
-#pragma unroll 4
-    for (int e = gl; e < R; e += LPP) {
-      const int l = rf_lat(a, eoff, ekk, in, interior, y0, x0, e);
-      if (l < T) list[atomicAdd(&cnt[l], 1u)] = uint32_t(e) * rb;
-    }
-  }
-  {  // pad the tail to a whole walk iteration with the zero-weight row R
-    const int n = carry;
-    for (int k = n + gl; k < ((n + kIt - 1) & ~(kIt - 1)); k += LPP) list[k] = uint32_t(R) * rb;
-  }
-  __syncwarp();
-}
-
-__device__ __forceinline__ void rf_tables(const WalkArgs& a, int32_t* eoff, uint16_t* ekk) {
-  const int KK = a.KH * a.KW;
-  for (int e = threadIdx.x; e < a.R; e += blockDim.x) {
-    const int c = e / KK, r = e - c * KK, ky = r / a.KW, kx = r - ky * a.KW;
-    eoff[e] = c * a.H * a.W + ky * a.W + kx;
-    ekk[e] = uint16_t((ky << 8) | kx);
-  }
-}
 
 // ------------------------------------------------------------------------------------- sort only
 template <int PPW>
@@ -196,70 +79,13 @@ __global__ void __launch_bounds__(512) rf_sort_kernel(const WalkArgs a) {
   }
 }
 
-// ------------------------------------------------------------------------------------- walk
-template <int FPL, bool PRE> struct WalkThreads { static constexpr int v = FPL == 4 ? (PRE ? 640 : 768) : 1024; };
-
-// Fire every unfired feature whose potential at the end of bucket t exceeds the threshold.
-template <int FPL>
-__device__ __forceinline__ void fire_at(const uint64_t (&acc)[FPL], int64_t thr, int t, unsigned& fired,
-                                        uint32_t& lo, float (&vo)[FPL]) {
-#pragma unroll
-  for (int j = 0; j < FPL; ++j) {
-    if (!(fired >> j & 1) && int64_t(acc[j]) > thr) {
-      fired |= 1u << j;
-      lo = (lo & ~(0xFFu << (8 * j))) | (uint32_t(t) << (8 * j));
-      vo[j] = fixed_to_float(int64_t(acc[j]));
-    }
-  }
-}
-
-// One 8-input block of the walk (entries e0, e1: weight-row byte offsets).  The bucket ends inside
-// the block are known to the whole group beforehand (endm: bit m = a bucket ends after pair m, its
-// first-spike index in byte m of tpk).  Each lane sums its features' 8 weights exactly; if no
-// unfired feature of the lane then exceeds the threshold, no test inside the block could fire
-// (potentials only grow along the list) and the block is taken whole; otherwise the lane re-adds it
-// pair by pair from the same registers and tests at every bucket end (K3).  Lanes decide
-// independently (no vote): the group's bookkeeping does not depend on the branch taken.
-template <int FPL>
-__device__ __forceinline__ void walk_block(const unsigned char* wl, const uint4& e0, const uint4& e1, unsigned endm,
-                                           uint32_t tpk, int64_t thr, uint64_t (&acc)[FPL], unsigned& fired,
-                                           uint32_t& lo, float (&vo)[FPL]) {
-  const uint32_t off[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
-  uint32_t wv[8][FPL];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) wgather<FPL>(wl + off[k], wv[k]);
-  uint64_t s[FPL];
-  bool hit = false;
-#pragma unroll
-  for (int j = 0; j < FPL; ++j) {
-    s[j] = acc[j] + (uint64_t(wv[0][j]) + wv[1][j]) + (uint64_t(wv[2][j]) + wv[3][j]) +
-           (uint64_t(wv[4][j]) + wv[5][j]) + (uint64_t(wv[6][j]) + wv[7][j]);
-    hit |= !(fired >> j & 1) && int64_t(s[j]) > thr;
-  }
-  if (hit && endm) {
-    if (endm & 7u) {  // a bucket ends strictly inside the block: pair by pair
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-#pragma unroll
-        for (int j = 0; j < FPL; ++j) acc[j] += uint64_t(wv[2 * m][j]) + wv[2 * m + 1][j];
-        if (endm >> m & 1) fire_at<FPL>(acc, thr, int((tpk >> (8 * m)) & 0xFFu), fired, lo, vo);
-      }
-    } else {  // the only bucket end is the block end
-      fire_at<FPL>(s, thr, int(tpk >> 24), fired, lo, vo);
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < FPL; ++j) acc[j] = s[j];
-}
-
 template <int FPL, int PPW, bool PRE>
 __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(const WalkArgs a) {
   constexpr int LPP = 32 / PPW;
   constexpr int FGS = LPP * FPL;
-  constexpr unsigned kAll = (1u << FPL) - 1;
   static_assert(!PRE || PPW == 1, "presorted walk: one position per warp");
   extern __shared__ __align__(16) unsigned char smem[];
-  const int R = a.R, T = a.T;
+  const int R = a.R;
   int32_t* eoff = reinterpret_cast<int32_t*>(smem + a.off_eoff);
   uint16_t* ekk = reinterpret_cast<uint16_t*>(smem + a.off_ekk);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
@@ -286,7 +112,6 @@ __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(
   for (int j = 0; j < FPL; ++j) valid |= (fbase + j < a.F) ? (1u << j) : 0u;
   const unsigned gmask = (LPP == 32) ? 0xffffffffu : (((1u << LPP) - 1u) << (grp * LPP));
   const int64_t stride_w = int64_t(gridDim.x) * nwarps;
-  const int64_t thr = a.thr;
   const unsigned char* wl = smem + gl * FPL * 4;  // this lane's features in weight row 0
 
   // PRE: two per-warp position buffers [header | first npre entries], each filled by one bulk copy
@@ -335,71 +160,9 @@ __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(
       rf_sort_group<LPP>(a, eoff, ekk, pv, in, interior, y0, x0, gl, cnt, start, list);
     }
 
-    uint64_t acc[FPL];
-    uint32_t lo = 0xFFFFFFFFu;  // byte j = lat of feature j (255 = no spike)
+    uint32_t lo;
     float vo[FPL];
-#pragma unroll
-    for (int j = 0; j < FPL; ++j) { acc[j] = 0; vo[j] = 0.0f; }
-    unsigned fired = ~valid & kAll;
-    const int total = pv ? int(start[T]) : 0;
-    if (pv && int(start[1]) == 0 && int64_t(0) > thr) {  // empty bucket 0: P[0] = 0 > a negative threshold
-#pragma unroll
-      for (int j = 0; j < FPL; ++j)
-        if (!(fired >> j & 1)) lo &= ~(0xFFu << (8 * j));
-      fired = kAll;
-    }
-    bool done = !pv || total == 0;  // group-uniform, like every later update of done
-    {
-      const unsigned nd = __ballot_sync(0xffffffffu, fired != kAll);
-      if ((nd & gmask) == 0) done = true;  // all features of the group fired (or are padding)
-    }
-    int i = 0, t = 0, it = 0;
-    while (t < T && int(start[t + 1]) == 0) ++t;  // leading empty buckets (handled above)
-    int bend = t < T ? int(start[t + 1]) : 0x7FFFFFFF;  // end of the current non-empty bucket t
-    int guard = (total + kIt - 1) / kIt + 2;  // iterations this group can take (a bug trap, never hit)
-    // Every vote below is a full-warp ballot at a converged point; done is group-uniform.
-    while (true) {
-      if (__ballot_sync(0xffffffffu, !done) == 0) break;
-      uint4 cur[4];  // this iteration's 16 entries: shared memory (PRE past npre: global memory)
-      if (PRE && it * kIt >= a.npre) {
-        const uint4* g4 = reinterpret_cast<const uint4*>(ent + it * kIt * 4);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) cur[u] = __ldg(g4 + u);
-      } else {
-        const uint32_t sa = smem_u32(PRE ? static_cast<const void*>(sent + it * kIt * 4)
-                                         : static_cast<const void*>(list + it * kIt));
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(cur[u].x), "=r"(cur[u].y), "=r"(cur[u].z), "=r"(cur[u].w)
-                       : "r"(sa + 16 * u));
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (!done) {
-          // group-uniform: bucket ends inside this block (pair m ends bucket t_m)
-          unsigned endm = 0;
-          uint32_t tpk = 0;
-          i += kBlk;
-          while (bend <= i) {
-            const int m = ((bend - (i - kBlk)) >> 1) - 1;
-            endm |= 1u << m;
-            tpk |= uint32_t(t) << (8 * m);
-            ++t;
-            while (t < T && int(start[t + 1]) == bend) ++t;  // empty buckets add nothing
-            bend = t < T ? int(start[t + 1]) : 0x7FFFFFFF;
-          }
-          walk_block<FPL>(wl, cur[2 * h], cur[2 * h + 1], endm, tpk, thr, acc, fired, lo, vo);
-        }
-        const unsigned nf = __ballot_sync(0xffffffffu, !done && fired != kAll);
-        if (!done && ((nf & gmask) == 0 || i >= total)) done = true;
-      }
-      ++it;
-      if (!done && --guard < 0) {
-        flag_error(a.err, kErrInternal);
-        done = true;
-      }
-    }
+    walk_list<FPL, PPW, PRE>(a, wl, start, sent, ent, list, pv, valid, gmask, lo, vo);
     if (pv) {
 #pragma unroll
       for (int j = 0; j < FPL; ++j) {

@@ -1,0 +1,348 @@
+// seq_train.cu -- SURVEY.md §8(f) f1: the per-image plasticity chain (conv + fire -> pointwise
+// inhibition -> k-WTA -> STDP, image after image; each image's weights feed the next) as ONE
+// persistent cooperative kernel, so the chain pays no kernel launch or host interaction per image
+// (the paper's residual cost).  Same arithmetic as the separate kernels (N1,
+// K2, K3, R13-R23), so results are bit-identical to snn_conv_fire + snn_inhibit + snn_k_winners +
+// snn_stdp_update run image by image.
+//
+// Grid: one CTA per SM (cooperative launch: all CTAs resident), CTA c holds feature group
+// g = c % n_groups (FGS = 32 * FPL features) as fixed-point weights in shared memory for the whole
+// run.  Per image:
+//   A  every CTA walks its share of the output positions for its group (fused receptive-field sort +
+//      delta walk, K2/K3) and writes (lat, v) of its features to a one-image scratch map;
+//   -- grid barrier --
+//   B  CTA 0: pointwise inhibition (best key per position over all features, R13/R14) and the k-WTA
+//      rounds on the inhibited map (one candidate per position, R15): winners, their post times;
+//   -- grid barrier --
+//   C  every CTA applies Eq. 4 to the winners of its group in its shared-memory copy (old weights
+//      recovered exactly from the fixed point); the group's leader CTA also writes the fp32 weights
+//      (and the snapshots).  The next image's phase A uses the updated shared-memory copy.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "walk_dev.cuh"
+
+namespace snn {
+
+struct SeqArgs {
+  WalkArgs wa;              // geometry of one image (B = 1), smem layout, threshold
+  const uint8_t* lat_all;   // [N][C][H][W] layer input of every image
+  int N;
+  float* w;                 // [F][R] fp32, updated in place
+  int k, r;
+  float a_plus, a_minus, lb, ub;
+  int stabilizer;
+  float* snaps;             // nullable [N / snap_every][F][R]
+  int snap_every;
+  uint8_t* lat_map;         // [F][Ho][Wo] one-image scratch
+  float* v_map;
+  int32_t* winners;         // [N][k][3]
+  int32_t* count;           // [N]
+  int32_t* post;            // [N][k] post-synaptic spike time of each winner
+  unsigned* bar;            // grid barrier words [2] (zeroed before the launch)
+  int n_groups, FGS;
+  int off_keys;             // CTA 0 scratch: per-position candidate keys [HoWo] u64
+};
+
+// Grid-wide barrier for a cooperative launch (all CTAs co-resident).  gen = barriers passed so far.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned g = gen;
+    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicExch(&bar[1], g + 1);
+    } else {
+      const uint64_t t0 = globaltimer_ns();
+      for (;;) {
+        unsigned cur;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+        if (cur != g) break;
+        __nanosleep(64);
+        watchdog(t0);
+      }
+    }
+    __threadfence();
+  }
+  ++gen;
+  __syncthreads();
+}
+
+template <int FPL>
+__global__ void __launch_bounds__(FPL == 4 ? 768 : 1024, 1) seq_train_kernel(const SeqArgs s) {
+  constexpr int FGS = 32 * FPL;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const WalkArgs& a = s.wa;
+  const int R = a.R, T = a.T, F = a.F, HoWo = a.Ho * a.Wo;
+  uint32_t* Wsh = reinterpret_cast<uint32_t*>(smem);  // [R+1][FGS] fixed point
+  int32_t* eoff = reinterpret_cast<int32_t*>(smem + a.off_eoff);
+  uint16_t* ekk = reinterpret_cast<uint16_t*>(smem + a.off_ekk);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  unsigned char* pb = smem + a.off_warps + warp * a.warp_bytes;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(pb + a.cnt_off);
+  uint16_t* start = reinterpret_cast<uint16_t*>(pb + a.start_off);
+  uint32_t* list = reinterpret_cast<uint32_t*>(pb + a.list_off);
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem + s.off_keys);
+  __shared__ uint32_t fexcl[256];
+  __shared__ int wy[256], wx[256];
+  __shared__ uint64_t red[32];
+  __shared__ int s_count;
+  const int g = int(blockIdx.x) % s.n_groups;
+  const int cg = int(blockIdx.x) / s.n_groups, ncg = int(gridDim.x) / s.n_groups;
+  const bool leader = cg == 0;
+  const int fbase = g * FGS + lane * FPL;
+  unsigned valid = 0;
+#pragma unroll
+  for (int j = 0; j < FPL; ++j) valid |= (fbase + j < F) ? (1u << j) : 0u;
+  const unsigned char* wl = smem + lane * FPL * 4;
+  const int64_t CHW = int64_t(a.C) * a.H * a.W;
+
+  // the group's weights -> fixed point (exact domain checked), row R = 0
+  for (int i = tid; i < (R + 1) * FGS; i += blockDim.x) {
+    const int e = i / FGS, f = g * FGS + (i - e * FGS);
+    uint32_t u = 0;
+    if (f < F && e < R) {
+      const float x = s.w[int64_t(f) * R + e];
+      const float sx = x * 2147483648.0f;
+      if (!(x >= 0.0f && x <= 1.0f) || sx != truncf(sx)) flag_error(a.err, kErrInexact);
+      else u = uint32_t(sx);
+    }
+    Wsh[i] = u;
+  }
+  rf_tables(a, eoff, ekk);
+  __syncthreads();
+  unsigned gen = 0;
+
+  for (int img = 0; img < s.N; ++img) {
+    const uint8_t* lat_img = s.lat_all + int64_t(img) * CHW;
+    // ---------------- A: conv + fire of this CTA's positions, this group's features ----------------
+    for (int pos = cg * nwarps + warp; pos < HoWo; pos += ncg * nwarps) {
+      const int y = pos / a.Wo, x = pos - y * a.Wo;
+      const int y0 = y - a.pad, x0 = x - a.pad;
+      const uint8_t* in = lat_img + int64_t(y0) * a.W + x0;
+      const bool interior = y0 >= 0 && x0 >= 0 && y0 + a.KH <= a.H && x0 + a.KW <= a.W;
+      rf_sort_group<32>(a, eoff, ekk, true, in, interior, y0, x0, lane, cnt, start, list);
+      uint32_t lo;
+      float vo[FPL];
+      walk_list<FPL, 1, false>(a, wl, start, nullptr, nullptr, list, true, valid, 0xffffffffu, lo, vo);
+#pragma unroll
+      for (int j = 0; j < FPL; ++j)
+        if (valid >> j & 1) {
+          s.lat_map[int64_t(fbase + j) * HoWo + pos] = uint8_t(lo >> (8 * j));
+          s.v_map[int64_t(fbase + j) * HoWo + pos] = vo[j];
+        }
+      __syncwarp();
+    }
+    grid_barrier(s.bar, gen);
+    // ---------------- B (CTA 0): pointwise inhibition, then k-WTA on the inhibited map ----------------
+    if (blockIdx.x == 0) {
+      for (int pos = warp; pos < HoWo; pos += nwarps) {  // best (lat, v, f) per position (R13/R14)
+        uint64_t best = ~uint64_t(0);
+        for (int f = lane; f < F; f += 32) {
+          const uint8_t l = s.lat_map[int64_t(f) * HoWo + pos];
+          const float vv = s.v_map[int64_t(f) * HoWo + pos];
+          if (l == kNoSpike) continue;
+          const uint64_t kk = wta_key(l, vv, uint32_t(f));
+          best = kk < best ? kk : best;
+        }
+        best = warp_min_u64(best);
+        if (lane == 0) {
+          uint64_t cand = ~uint64_t(0);  // the survivor's k-WTA key: flat index f * HoWo + pos (R14)
+          if (best != ~uint64_t(0)) cand = (best & ~uint64_t(0xFFFFFFu)) | uint64_t(uint32_t(best & 0xFFFFFFu) * HoWo + pos);
+          keys[pos] = cand;
+        }
+      }
+      for (int i = tid; i < (F + 31) / 32; i += blockDim.x) fexcl[i] = 0;
+      if (tid == 0) s_count = 0;
+      __syncthreads();
+      for (int round = 0; round < s.k; ++round) {
+        const int nw = s_count;
+        uint64_t best = ~uint64_t(0);
+        for (int pos = tid; pos < HoWo; pos += blockDim.x) {
+          const uint64_t kk = keys[pos];
+          if (kk == ~uint64_t(0)) continue;
+          const int f = int(uint32_t(kk & 0xFFFFFFu) / uint32_t(HoWo));
+          if (fexcl[f >> 5] >> (f & 31) & 1) continue;  // inhibited map: no other candidate here
+          const int y = pos / a.Wo, x = pos - y * a.Wo;
+          bool near = false;
+          for (int i = 0; i < nw; ++i) near |= (abs(y - wy[i]) <= s.r) && (abs(x - wx[i]) <= s.r);
+          if (!near) best = kk < best ? kk : best;
+        }
+        best = warp_min_u64(best);
+        if (lane == 0) red[warp] = best;
+        __syncthreads();
+        if (warp == 0) {
+          uint64_t x = lane < nwarps ? red[lane] : ~uint64_t(0);
+          x = warp_min_u64(x);
+          if (lane == 0 && x != ~uint64_t(0)) {
+            const int idx = int(x & 0xFFFFFFu);
+            const int f = idx / HoWo, p = idx - f * HoWo;
+            const int yy = p / a.Wo, xx = p - yy * a.Wo;
+            const int c = s_count;
+            int32_t* wrec = s.winners + (int64_t(img) * s.k + c) * 3;
+            wrec[0] = f; wrec[1] = yy; wrec[2] = xx;
+            s.post[int64_t(img) * s.k + c] = int(x >> 56);  // the winner's spike time (key bits 56..63)
+            wy[c] = yy; wx[c] = xx;
+            fexcl[f >> 5] |= 1u << (f & 31);
+            s_count = c + 1;
+          }
+        }
+        __syncthreads();
+        if (s_count == round) break;  // no candidate left
+      }
+      for (int i = s_count + tid; i < s.k; i += blockDim.x) {
+        int32_t* wrec = s.winners + (int64_t(img) * s.k + i) * 3;
+        wrec[0] = -1; wrec[1] = -1; wrec[2] = -1;
+      }
+      if (tid == 0) s.count[img] = s_count;
+    }
+    grid_barrier(s.bar, gen);
+    // ---------------- C: Eq. 4 on this group's winners (shared-memory copy; leader writes fp32) ----------------
+    {
+      const int nwin = s.count[img];
+      const int KK = a.KH * a.KW;
+      for (int i = 0; i < nwin; ++i) {
+        const int32_t* wrec = s.winners + (int64_t(img) * s.k + i) * 3;
+        const int f = wrec[0], y = wrec[1], x = wrec[2];
+        if (f < g * FGS || f >= g * FGS + FGS) continue;
+        const int fl = f - g * FGS;
+        const int post = s.post[int64_t(img) * s.k + i];
+        for (int e = tid; e < R; e += blockDim.x) {
+          const int c = e / KK, rr = e - c * KK, ky = rr / a.KW, kx = rr - ky * a.KW;
+          const int yy = y + ky - a.pad, xx = x + kx - a.pad;
+          int pre = kNoSpike;
+          if (yy >= 0 && yy < a.H && xx >= 0 && xx < a.W) pre = lat_img[(int64_t(c) * a.H + yy) * a.W + xx];
+          const float am = (pre != kNoSpike && pre <= post) ? s.a_plus : s.a_minus;  // T_j <= T_i -> LTP
+          const float w0 = __uint2float_rn(Wsh[e * FGS + fl]) * 4.656612873077392578125e-10f;  // exact
+          const float dw = s.stabilizer ? __fmul_rn(__fmul_rn(am, __fsub_rn(w0, s.lb)), __fsub_rn(s.ub, w0)) : am;
+          float w1 = __fadd_rn(w0, dw);
+          w1 = w1 < s.lb ? s.lb : w1;
+          w1 = w1 > s.ub ? s.ub : w1;
+          const float sx = w1 * 2147483648.0f;
+          if (!(w1 >= 0.0f && w1 <= 1.0f) || sx != truncf(sx)) flag_error(a.err, kErrInexact);
+          Wsh[e * FGS + fl] = uint32_t(sx);
+          if (leader) s.w[int64_t(f) * R + e] = w1;
+        }
+      }
+      if (leader && s.snaps && (img + 1) % s.snap_every == 0) {
+        __syncthreads();
+        float* snap = s.snaps + int64_t((img + 1) / s.snap_every - 1) * F * R;
+        const int f0 = g * FGS, f1 = f0 + FGS < F ? f0 + FGS : F;
+        for (int64_t i = int64_t(f0) * R + tid; i < int64_t(f1) * R; i += blockDim.x) snap[i] = s.w[i];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------- host
+struct SeqPlan {
+  int fpl, n_groups, FGS, nwarps, smem, grid;
+  WalkArgs a;
+  int off_keys;
+};
+
+static int al16h(int x) { return (x + 15) & ~15; }
+
+static bool seq_plan(int C, int H, int W, int pad, int F, int KH, int KW, int T, SeqPlan* pl) {
+  WalkArgs& a = pl->a;
+  a = WalkArgs{};
+  a.B = 1; a.C = C; a.H = H; a.W = W; a.pad = pad; a.F = F; a.KH = KH; a.KW = KW; a.T = T;
+  a.Ho = H + 2 * pad - KH + 1; a.Wo = W + 2 * pad - KW + 1; a.R = C * KH * KW;
+  const int R = a.R;
+  if (a.Ho < 1 || a.Wo < 1 || R + T + kIt >= 65536 || F > 8192) return false;
+  const int HoWo = a.Ho * a.Wo;
+  if (int64_t(F) * HoWo >= (int64_t(1) << 24)) return false;
+  const int fpls[3] = {4, 2, 1};
+  for (int i = 0; i < 3; ++i) {
+    const int fpl = fpls[i], fgs = 32 * fpl;
+    if (fpl > 1 && F <= fgs / 2) continue;  // lanes would idle
+    const int nwarps = fpl == 4 ? 24 : 32;
+    int o = 0;
+    a.cnt_off = o; o += al16h(T * 4);
+    a.start_off = o; o += al16h((T + 1) * 2);
+    a.list_off = o; o += al16h((R + T + kIt) * 4);
+    a.pos_bytes = o; a.warp_bytes = o;
+    a.row_bytes = fgs * 4;
+    const int wsb = al16h((R + 1) * fgs * 4);
+    a.off_eoff = wsb;
+    a.off_ekk = a.off_eoff + al16h(R * 4);
+    a.off_warps = a.off_ekk + al16h(R * 2);
+    const int off_keys = a.off_warps + nwarps * a.warp_bytes;
+    const int smem = off_keys + al16h(HoWo * 8);
+    if (smem > 220 * 1024) continue;
+    pl->fpl = fpl; pl->FGS = fgs; pl->nwarps = nwarps; pl->smem = smem; pl->off_keys = off_keys;
+    pl->n_groups = (F + fgs - 1) / fgs;
+    pl->grid = (num_sms() / pl->n_groups) * pl->n_groups;
+    if (pl->grid < pl->n_groups) return false;
+    a.np = HoWo;
+    return true;
+  }
+  return false;
+}
+
+static size_t r256(size_t x) { return (x + 255) & ~size_t(255); }
+// workspace: [barrier words 256 B][lat_map F*HoWo][v_map F*HoWo*4][post N*k*4]
+size_t seq_train_workspace(int C, int H, int W, int pad, int F, int KH, int KW, int T, int k, int N) {
+  SeqPlan pl;
+  if (!seq_plan(C, H, W, pad, F, KH, KW, T, &pl)) return 0;
+  const size_t HoWo = size_t(pl.a.Ho) * pl.a.Wo;
+  return 256 + r256(size_t(F) * HoWo) + r256(size_t(F) * HoWo * 4) + r256(size_t(N) * k * 4);
+}
+
+template <int FPL>
+static int seq_go(const SeqPlan& pl, SeqArgs& s, cudaStream_t st) {
+  auto kern = seq_train_kernel<FPL>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
+  if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_stdp_sequence: %s", cudaGetErrorString(e));
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, pl.nwarps * 32, pl.smem);
+  if (occ < 1) return set_error(SNN_ESHAPE, "snn_stdp_sequence: kernel does not fit an SM");
+  void* args[] = {&s};
+  e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(pl.grid), dim3(pl.nwarps * 32), args,
+                                  size_t(pl.smem), st);
+  if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_stdp_sequence: %s", cudaGetErrorString(e));
+  note_launch();
+  return SNN_OK;
+}
+
+// Returns 1 if the persistent path does not apply (caller uses the per-call kernels), else an SNN code.
+int seq_train_launch(const uint8_t* lat_all, int N, int C, int H, int W, int pad, float* w, int F, int KH, int KW,
+                     int T, float theta, int k, int r, float a_plus, float a_minus, float lb, float ub,
+                     int stabilizer, int32_t* winners, int32_t* count, float* snaps, int snap_every, void* ws,
+                     size_t ws_bytes, cudaStream_t st) {
+  SeqPlan pl;
+  if (!(isfinite(theta)) || k > 256 || !seq_plan(C, H, W, pad, F, KH, KW, T, &pl)) return 1;
+  const size_t need = seq_train_workspace(C, H, W, pad, F, KH, KW, T, k, N);
+  if (ws_bytes < need) return set_error(SNN_EWORKSPACE, "snn_stdp_sequence: workspace %zu < %zu", ws_bytes, need);
+  SeqArgs s;
+  s.wa = pl.a;
+  s.wa.lat_in = lat_all;
+  s.wa.err = error_word_ptr();
+  const double tt = floor(double(theta) * 2147483648.0);
+  s.wa.thr = tt >= 9.0e18 ? INT64_MAX : (tt < -1.0 ? -1 : int64_t(tt));
+  s.lat_all = lat_all; s.N = N; s.w = w; s.k = k; s.r = r;
+  s.a_plus = a_plus; s.a_minus = a_minus; s.lb = lb; s.ub = ub; s.stabilizer = stabilizer;
+  s.snaps = snaps; s.snap_every = snap_every > 0 ? snap_every : 1;
+  if (!snaps) s.snap_every = 1;
+  unsigned char* p = reinterpret_cast<unsigned char*>(ws);
+  s.bar = reinterpret_cast<unsigned*>(p);
+  const size_t HoWo = size_t(pl.a.Ho) * pl.a.Wo;
+  s.lat_map = p + 256;
+  s.v_map = reinterpret_cast<float*>(p + 256 + r256(size_t(F) * HoWo));
+  s.post = reinterpret_cast<int32_t*>(p + 256 + r256(size_t(F) * HoWo) + r256(size_t(F) * HoWo * 4));
+  s.winners = winners; s.count = count;
+  s.n_groups = pl.n_groups; s.FGS = pl.FGS; s.off_keys = pl.off_keys;
+  if (cudaMemsetAsync(s.bar, 0, 2 * sizeof(unsigned), st) != cudaSuccess) return check_launch("snn_stdp_sequence");
+  switch (pl.fpl) {
+    case 4: return seq_go<4>(pl, s, st);
+    case 2: return seq_go<2>(pl, s, st);
+    default: return seq_go<1>(pl, s, st);
+  }
+}
+
+}  // namespace snn

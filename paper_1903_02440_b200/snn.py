@@ -60,6 +60,9 @@ def lib() -> C.CDLL:
                 "snn_count_events": (i32, [p, i32, i32, i32, i32, i32, i32, i32, i32, i32, p, p, p]),
                 "snn_launch_count": (C.c_ulonglong, []),
                 "snn_conv_fire_plan": (i32, [i32] * 9 + [f32, p, p, p]),
+                "snn_stdp_sequence_workspace": (sz, [i32] * 10),
+                "snn_stdp_sequence": (i32, [p, i32, i32, i32, i32, i32, p, i32, i32, i32, i32, f32, i32, i32,
+                                            f32, f32, f32, f32, i32, p, p, p, i32, p, sz, p]),
             }
             for name, (res, args) in sigs.items():
                 fn = getattr(L, name)
@@ -73,7 +76,8 @@ def exported_symbols():
     return ["snn_version", "snn_last_error", "snn_sync_status", "snn_encode_workspace", "snn_encode",
             "snn_expand", "snn_validate_lat", "snn_conv_fire_workspace", "snn_conv_fire", "snn_pool",
             "snn_inhibit", "snn_k_winners_workspace", "snn_k_winners", "snn_stdp_update", "snn_decide",
-            "snn_count_events", "snn_launch_count", "snn_conv_fire_plan"]
+            "snn_count_events", "snn_launch_count", "snn_conv_fire_plan", "snn_stdp_sequence_workspace",
+            "snn_stdp_sequence"]
 
 
 def _check(rc: int):
@@ -289,6 +293,32 @@ def conv_fire_plan(B: int, Cin: int, H: int, W: int, pad: int, F: int, KH: int, 
                                     C.byref(chunks)))
     names = {0: "walk_fused", 1: "walk_presorted", 2: "tc_inf", 3: "tct", 4: "ref"}
     return {"path": names[path.value], "launches": launches.value, "chunks": chunks.value}
+
+
+def stdp_sequence(lat_in: torch.Tensor, w: torch.Tensor, pad: int, T: int, theta: float, k: int, r: int,
+                  a_plus: float, a_minus: float, lb: float = 0.0, ub: float = 1.0, stabilizer: int = 1,
+                  winners: Optional[torch.Tensor] = None, count: Optional[torch.Tensor] = None,
+                  snapshots: Optional[torch.Tensor] = None, snap_every: int = 0, ws: Optional[torch.Tensor] = None,
+                  stream=None):
+    """N sequential conv+fire -> inhibit -> k-WTA -> STDP steps in one persistent kernel (w in place)."""
+    _req(lat_in, torch.uint8, "lat_in")
+    _req(w, torch.float32, "w")
+    N, Cin, H, W = lat_in.shape
+    F, _, KH, KW = w.shape
+    dev = lat_in.device
+    if winners is None:
+        winners = torch.empty((N, k, 3), dtype=torch.int32, device=dev)
+    if count is None:
+        count = torch.empty((N,), dtype=torch.int32, device=dev)
+    if ws is None:
+        n = int(lib().snn_stdp_sequence_workspace(N, Cin, H, W, pad, F, KH, KW, T, k))
+        if n == 0:
+            raise SNNError(SNN_ESHAPE, "snn_stdp_sequence: layer not supported")
+        ws = torch.empty(n, dtype=torch.uint8, device=dev)
+    _check(lib().snn_stdp_sequence(_ptr(lat_in), N, Cin, H, W, pad, _ptr(w), F, KH, KW, T, theta, k, r, a_plus,
+                                   a_minus, lb, ub, stabilizer, _ptr(winners), _ptr(count), _ptr(snapshots),
+                                   snap_every, _ptr(ws), ws.numel(), _stream(stream)))
+    return winners, count
 
 
 def launch_count() -> int:

@@ -174,3 +174,44 @@ def test_c5_full_batch_sampled(G, orc):
     for b in (5, 63):
         pl, pv = orc.pool(lat[b:b + 1], v[b:b + 1], 2, 2, 2, 2, 0, 0, wl.T)
         assert np.array_equal(host(net.l1.plat[b:b + 1]), pl) and np.array_equal(host(net.l1.pv[b:b + 1]), pv)
+
+
+@pytest.mark.parametrize("n", [300])
+def test_c3_persistent_sequence(G, orc, n):
+    """C3 through snn_stdp_sequence (one persistent kernel for all n images) vs the oracle flow."""
+    from oracle import flows
+    from paper_1903_02440_b200 import pipeline
+    wl = synth.C3(n=n)
+    ref = flows.c3(wl, snapshot_every=100)
+    x = cu(wl.X)
+    lat0 = G.encode(x, wl.T)
+    l1 = pipeline.Layer(wl.convs[0], cu(wl.weights[0]), n, 6, 28, 28, wl.T, wl.pools[0], pool_v=False)
+    l1(lat0)
+    s = wl.convs[1]
+    st = wl.extra["stdp"]
+    w = cu(wl.weights[1]).clone()
+    snaps = torch.empty((n // 100,) + tuple(w.shape), dtype=torch.float32, device="cuda")
+    win, cnt = G.stdp_sequence(l1.plat.contiguous(), w, s.pad, wl.T, s.theta, wl.extra["k"], wl.extra["r"],
+                               st["a_plus"], st["a_minus"], st["lb"], st["ub"], st["stabilizer"],
+                               snapshots=snaps, snap_every=100)
+    G.sync_status()
+    for b in range(n):
+        assert np.array_equal(host(win[b]), ref["winners"][b]), f"image {b}"
+    for a, r in zip(host(snaps), ref["snapshots"]):
+        assert np.array_equal(a, r)
+    assert np.array_equal(host(w), ref["w2"])
+
+
+def test_c1_persistent_sequence(G, orc):
+    """C1's single STDP step through snn_stdp_sequence (N = 1)."""
+    from oracle import flows
+    wl = synth.C1()
+    ref = flows.c1(wl)
+    lat0 = G.encode(cu(wl.X), wl.T)
+    s, st = wl.convs[0], wl.extra["stdp"]
+    w = cu(wl.weights[0]).clone()
+    win, cnt = G.stdp_sequence(lat0, w, s.pad, wl.T, s.theta, wl.extra["k"], wl.extra["r"], st["a_plus"],
+                               st["a_minus"], st["lb"], st["ub"], st["stabilizer"])
+    G.sync_status()
+    assert np.array_equal(host(win), ref["winners"])
+    assert np.array_equal(host(w), ref["w_new"])
