@@ -297,16 +297,25 @@ class C3Step(SeqBase):
         self.lat0 = torch.empty(wl.X.shape, dtype=torch.uint8, device=dev)
         self.l1 = pipeline.Layer(wl.convs[0], torch.from_numpy(wl.weights[0]).to(dev), batch, C, H, W, wl.T,
                                  wl.pools[0], pool_v=False, device=dev)
-        self.seq = pipeline.SeqSTDP(wl.convs[1], wl.weights[1], wl.convs[0].F, self.l1.PHo, self.l1.PWo, wl.T,
-                                    wl.extra["k"], wl.extra["r"], True, wl.extra["stdp"], device=dev)
         self._prefix()
-        self.graph = pipeline.SeqGraph(self.seq, self.l1.plat, batch, snapshot_every=wl.extra["snapshot_every"])
+        s2 = wl.convs[1]
+        if pipeline.SeqPersistent.supported(s2, tuple(self.l1.plat.shape), wl.weights[1].shape, wl.T, wl.extra["k"]):
+            # all 2000 plasticity steps in one persistent kernel (snn_stdp_sequence)
+            self.seq = self.graph = pipeline.SeqPersistent(s2, wl.weights[1], self.l1.plat, wl.T, wl.extra["k"],
+                                                           wl.extra["r"], wl.extra["stdp"],
+                                                           snapshot_every=wl.extra["snapshot_every"], device=dev)
+            self.mode = "one persistent kernel (snn_stdp_sequence)"
+        else:
+            self.seq = pipeline.SeqSTDP(s2, wl.weights[1], wl.convs[0].F, self.l1.PHo, self.l1.PWo, wl.T,
+                                        wl.extra["k"], wl.extra["r"], True, wl.extra["stdp"], device=dev)
+            self.graph = pipeline.SeqGraph(self.seq, self.l1.plat, batch, snapshot_every=wl.extra["snapshot_every"])
+            self.mode = "per-image CUDA graph, no host sync"
         self.stages = ["l1_prefix", "seq_stdp"]
 
     def config(self):
         return {"workload": "c3: BASELINE.json configs[2], sequential STDP on layer 2, 2000 images",
                 "global_batch": self.B, "layers": "C2 L1 (fixed) -> pool -> L2 F250 3x3 th10 -> inhibit -> kWTA k8 r2 -> STDP",
-                "plasticity": "per-image CUDA graph, no host sync", "l2": "flushed between timed steps"}
+                "plasticity": self.mode, "l2": "flushed between timed steps"}
 
     def oracle_step(self, n):
         from oracle import flows
@@ -363,14 +372,29 @@ class C1Step(SeqBase):
         self.ws_enc = torch.empty(snn.encode_workspace(1, 2, 28, 28, wl.T), dtype=torch.uint8, device=dev)
         self.lat0 = torch.empty(wl.X.shape, dtype=torch.uint8, device=dev)
         self.l1 = None
-        self.seq = pipeline.SeqSTDP(wl.convs[0], wl.weights[0], 2, 28, 28, wl.T, wl.extra["k"], wl.extra["r"], True,
-                                    wl.extra["stdp"], device=dev)
-        w0 = self.seq.w.clone()
+        s1 = wl.convs[0]
+        # one image: the per-call kernels in one CUDA graph beat the persistent kernel's fixed cost
+        # (list presort + cooperative launch + grid barriers); SNN_C1_PERSISTENT=1 selects it anyway
+        if os.environ.get("SNN_C1_PERSISTENT") == "1" and pipeline.SeqPersistent.supported(
+                s1, tuple(self.lat0.shape), wl.weights[0].shape, wl.T, wl.extra["k"]):
+            # encode + the plasticity step (one persistent kernel, N = 1), captured as one CUDA graph
+            self.seq = pipeline.SeqPersistent(s1, wl.weights[0], self.lat0, wl.T, wl.extra["k"], wl.extra["r"],
+                                              wl.extra["stdp"], device=dev)
 
-        def body():
-            self.seq.w.copy_(w0)
-            self._prefix()
-            self.seq.step(self.lat0)
+            def body():
+                self._prefix()
+                self.seq.replay()
+            self.mode = "encode + snn_stdp_sequence as one CUDA graph"
+        else:
+            self.seq = pipeline.SeqSTDP(s1, wl.weights[0], 2, 28, 28, wl.T, wl.extra["k"], wl.extra["r"], True,
+                                        wl.extra["stdp"], device=dev)
+            w0 = self.seq.w.clone()
+
+            def body():
+                self.seq.w.copy_(w0)
+                self._prefix()
+                self.seq.step(self.lat0)
+            self.mode = "whole step as one CUDA graph"
         self.graph = pipeline.StepGraph(body)
         self.stages = ["step"]
 
@@ -383,7 +407,7 @@ class C1Step(SeqBase):
 
     def config(self):
         return {"workload": "c1: BASELINE.json configs[0], single layer, batch 1: encode -> conv+fire -> inhibit -> kWTA k5 r3 -> STDP",
-                "global_batch": 1, "plasticity": "whole step as one CUDA graph", "l2": "flushed between timed steps"}
+                "global_batch": 1, "plasticity": self.mode, "l2": "flushed between timed steps"}
 
     def oracle_step(self, n):
         from oracle import flows

@@ -342,6 +342,31 @@ static int sort_go(const WalkPlan& pl, const WalkArgs& a, cudaStream_t s) {
   return check_launch("snn_conv_fire(sort)");
 }
 
+// Sorted receptive-field lists of every output position of B images, in the presorted record format
+// (header + u32 weight-row byte offsets for weight rows of row_bytes), one record of rec bytes per
+// position, no chunking: the input of the persistent plasticity chain (seq_train.cu).
+int rf_sort_lists_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, int KH, int KW, int T,
+                         int row_bytes, unsigned char* lists, int rec, int hdr, cudaStream_t s) {
+  WalkPlan pl;
+  WalkArgs& sa = pl.sa;
+  sa = WalkArgs{};
+  sa.B = B; sa.C = C; sa.H = H; sa.W = W; sa.pad = pad; sa.KH = KH; sa.KW = KW; sa.T = T;
+  sa.Ho = H + 2 * pad - KH + 1; sa.Wo = W + 2 * pad - KW + 1; sa.R = C * KH * KW;
+  sa.row_bytes = row_bytes; sa.lists = lists; sa.rec = rec; sa.hdr = hdr;
+  sa.lat_in = lat_in; sa.p0 = 0; sa.np = int64_t(B) * sa.Ho * sa.Wo;
+  const int R = sa.R;
+  pl.sort_ppw = R <= 256 ? 4 : 1;
+  pl.sort_nwarps = 16;
+  pos_scratch_bytes(T, R, &sa);
+  sa.warp_bytes = pl.sort_ppw * sa.pos_bytes;
+  sa.off_eoff = 0;
+  sa.off_ekk = al16(R * 4);
+  sa.off_warps = sa.off_ekk + al16(R * 2);
+  pl.sort_smem = sa.off_warps + pl.sort_nwarps * sa.warp_bytes;
+  if (pl.sort_smem > kWalkSmemLimit) return set_error(SNN_ESHAPE, "rf_sort_lists: receptive field too large");
+  return pl.sort_ppw == 4 ? sort_go<4>(pl, sa, s) : sort_go<1>(pl, sa, s);
+}
+
 // Plan description for snn_conv_fire_plan: 0 if the walk does not apply, else 1 (+ *pre, *chunks).
 int conv_walk_describe(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, int* pre, int* chunks) {
   WalkPlan pl;

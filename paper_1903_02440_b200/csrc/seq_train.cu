@@ -11,8 +11,9 @@
 //   A  every CTA walks its share of the output positions for its group (fused receptive-field sort +
 //      delta walk, K2/K3) and writes (lat, v) of its features to a one-image scratch map;
 //   -- grid barrier --
-//   B  CTA 0: pointwise inhibition (best key per position over all features, R13/R14) and the k-WTA
-//      rounds on the inhibited map (one candidate per position, R15): winners, their post times;
+//   B  CTA 0: pointwise inhibition (best key per position over all features, R13/R14: the minimum of
+//      the per-group bests phase A left) and the k-WTA rounds on the inhibited map (one candidate per
+//      position, R15): winners, their post times;
 //   -- grid barrier --
 //   C  every CTA applies Eq. 4 to the winners of its group in its shared-memory copy (old weights
 //      recovered exactly from the fixed point); the group's leader CTA also writes the fp32 weights
@@ -20,6 +21,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "walk_dev.cuh"
@@ -41,9 +43,14 @@ struct SeqArgs {
   int32_t* winners;         // [N][k][3]
   int32_t* count;           // [N]
   int32_t* post;            // [N][k] post-synaptic spike time of each winner
+  uint64_t* gbest;          // [n_groups][HoWo] best inhibition key of each group at each position
+  uint64_t* stamps;         // [N][6] CTA-0 phase timestamps (globaltimer ns), timing diagnostics
   unsigned* bar;            // grid barrier words [2] (zeroed before the launch)
   int n_groups, FGS;
   int off_keys;             // CTA 0 scratch: per-position candidate keys [HoWo] u64
+  int dbg;                  // timing experiments only (SNN_SEQ_DBG): 1 = skip conv, 2 = skip inhibit/kWTA, 4 = skip STDP
+  const unsigned char* lists;  // [N][HoWo] presorted receptive-field records (rf_sort_lists_launch)
+  int rec, hdr, npre, buf_bytes;
 };
 
 // Grid-wide barrier for a cooperative launch (all CTAs co-resident).  gen = barriers passed so far.
@@ -77,19 +84,18 @@ __global__ void __launch_bounds__(FPL == 4 ? 768 : 1024, 1) seq_train_kernel(con
   constexpr int FGS = 32 * FPL;
   extern __shared__ __align__(16) unsigned char smem[];
   const WalkArgs& a = s.wa;
-  const int R = a.R, T = a.T, F = a.F, HoWo = a.Ho * a.Wo;
+  const int R = a.R, F = a.F, HoWo = a.Ho * a.Wo;
   uint32_t* Wsh = reinterpret_cast<uint32_t*>(smem);  // [R+1][FGS] fixed point
   int32_t* eoff = reinterpret_cast<int32_t*>(smem + a.off_eoff);
   uint16_t* ekk = reinterpret_cast<uint16_t*>(smem + a.off_ekk);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  unsigned char* pb = smem + a.off_warps + warp * a.warp_bytes;
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(pb + a.cnt_off);
-  uint16_t* start = reinterpret_cast<uint16_t*>(pb + a.start_off);
-  uint32_t* list = reinterpret_cast<uint32_t*>(pb + a.list_off);
-  uint64_t* keys = reinterpret_cast<uint64_t*>(smem + s.off_keys);
-  __shared__ uint32_t fexcl[256];
-  __shared__ int wy[256], wx[256];
-  __shared__ uint64_t red[32];
+  unsigned char* pb = smem + a.off_warps + warp * a.warp_bytes;  // [2 mbarriers][2 record buffers]
+  uint64_t* pmb = reinterpret_cast<uint64_t*>(pb);
+  unsigned char* pbuf = pb + 16;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem + s.off_keys);  // [HoWo] candidate keys
+  uint16_t* fpos = reinterpret_cast<uint16_t*>(keys + HoWo);           // [HoWo] candidate features
+  uint16_t* ypos = fpos + HoWo;                                         // [HoWo] row, column of each position
+  uint16_t* xpos = ypos + HoWo;
   __shared__ int s_count;
   const int g = int(blockIdx.x) % s.n_groups;
   const int cg = int(blockIdx.x) / s.n_groups, ncg = int(gridDim.x) / s.n_groups;
@@ -113,97 +119,165 @@ __global__ void __launch_bounds__(FPL == 4 ? 768 : 1024, 1) seq_train_kernel(con
     }
     Wsh[i] = u;
   }
-  rf_tables(a, eoff, ekk);
+  (void)eoff; (void)ekk;
+  for (int pos = tid; pos < HoWo; pos += blockDim.x) {  // (row, col) of every position, for phase B
+    ypos[pos] = uint16_t(pos / a.Wo);
+    xpos[pos] = uint16_t(pos - (pos / a.Wo) * a.Wo);
+  }
+  // this warp's positions: pos0 + j * pstride (the same every image); records prefetched one item ahead
+  const int pstride = ncg * nwarps, pos0 = cg + ncg * warp;
+  auto rec_of = [&](int im, int pos) { return s.lists + (int64_t(im) * HoWo + pos) * s.rec; };
+  if (lane == 0) {
+    mbar_init(smem_u32(&pmb[0]), 1);
+    mbar_init(smem_u32(&pmb[1]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (pos0 < HoWo && s.N > 0) {
+      mbar_expect_tx(smem_u32(&pmb[0]), uint32_t(s.buf_bytes));
+      bulk_g2s(smem_u32(pbuf), rec_of(0, pos0), uint32_t(s.buf_bytes), smem_u32(&pmb[0]));
+    }
+  }
   __syncthreads();
   unsigned gen = 0;
+  int item = 0;  // walks done by this warp (buffer / phase bookkeeping)
 
   for (int img = 0; img < s.N; ++img) {
     const uint8_t* lat_img = s.lat_all + int64_t(img) * CHW;
+    if (blockIdx.x == 0 && tid == 0) s.stamps[img * 6 + 0] = globaltimer_ns();
+    if (img == 100 && tid == 0) s.stamps[int64_t(s.N) * 6 + blockIdx.x * 2] = globaltimer_ns();
     // ---------------- A: conv + fire of this CTA's positions, this group's features ----------------
-    for (int pos = cg * nwarps + warp; pos < HoWo; pos += ncg * nwarps) {
-      const int y = pos / a.Wo, x = pos - y * a.Wo;
-      const int y0 = y - a.pad, x0 = x - a.pad;
-      const uint8_t* in = lat_img + int64_t(y0) * a.W + x0;
-      const bool interior = y0 >= 0 && x0 >= 0 && y0 + a.KH <= a.H && x0 + a.KW <= a.W;
-      rf_sort_group<32>(a, eoff, ekk, true, in, interior, y0, x0, lane, cnt, start, list);
+    // positions round-robin over the group's CTAs first, so a small map spreads over all SMs
+    for (int pos = pos0; pos < ((s.dbg & 1) ? 0 : HoWo); pos += pstride, ++item) {
+      const int bi = item & 1;
+      if (lane == 0) {  // prefetch this warp's next (image, position) record into the other buffer
+        int nim = img, npos = pos + pstride;
+        if (npos >= HoWo) { ++nim; npos = pos0; }
+        if (nim < s.N) {
+          mbar_expect_tx(smem_u32(&pmb[bi ^ 1]), uint32_t(s.buf_bytes));
+          bulk_g2s(smem_u32(pbuf + (bi ^ 1) * s.buf_bytes), rec_of(nim, npos), uint32_t(s.buf_bytes),
+                   smem_u32(&pmb[bi ^ 1]));
+        }
+      }
+      mbar_wait(smem_u32(&pmb[bi]), (item >> 1) & 1);
+      const uint16_t* start = reinterpret_cast<const uint16_t*>(pbuf + bi * s.buf_bytes);
       uint32_t lo;
       float vo[FPL];
-      walk_list<FPL, 1, false>(a, wl, start, nullptr, nullptr, list, true, valid, 0xffffffffu, lo, vo);
+      walk_list<FPL, 1, true>(a, wl, start, pbuf + bi * s.buf_bytes + s.hdr, rec_of(img, pos) + s.hdr, nullptr,
+                              true, valid, 0xffffffffu, lo, vo);
+      uint64_t best = ~uint64_t(0);  // this group's inhibition candidate at pos (R13/R14: key over f)
 #pragma unroll
       for (int j = 0; j < FPL; ++j)
         if (valid >> j & 1) {
-          s.lat_map[int64_t(fbase + j) * HoWo + pos] = uint8_t(lo >> (8 * j));
+          const uint8_t l = uint8_t(lo >> (8 * j));
+          s.lat_map[int64_t(fbase + j) * HoWo + pos] = l;
           s.v_map[int64_t(fbase + j) * HoWo + pos] = vo[j];
-        }
-      __syncwarp();
-    }
-    grid_barrier(s.bar, gen);
-    // ---------------- B (CTA 0): pointwise inhibition, then k-WTA on the inhibited map ----------------
-    if (blockIdx.x == 0) {
-      for (int pos = warp; pos < HoWo; pos += nwarps) {  // best (lat, v, f) per position (R13/R14)
-        uint64_t best = ~uint64_t(0);
-        for (int f = lane; f < F; f += 32) {
-          const uint8_t l = s.lat_map[int64_t(f) * HoWo + pos];
-          const float vv = s.v_map[int64_t(f) * HoWo + pos];
-          if (l == kNoSpike) continue;
-          const uint64_t kk = wta_key(l, vv, uint32_t(f));
-          best = kk < best ? kk : best;
-        }
-        best = warp_min_u64(best);
-        if (lane == 0) {
-          uint64_t cand = ~uint64_t(0);  // the survivor's k-WTA key: flat index f * HoWo + pos (R14)
-          if (best != ~uint64_t(0)) cand = (best & ~uint64_t(0xFFFFFFu)) | uint64_t(uint32_t(best & 0xFFFFFFu) * HoWo + pos);
-          keys[pos] = cand;
-        }
-      }
-      for (int i = tid; i < (F + 31) / 32; i += blockDim.x) fexcl[i] = 0;
-      if (tid == 0) s_count = 0;
-      __syncthreads();
-      for (int round = 0; round < s.k; ++round) {
-        const int nw = s_count;
-        uint64_t best = ~uint64_t(0);
-        for (int pos = tid; pos < HoWo; pos += blockDim.x) {
-          const uint64_t kk = keys[pos];
-          if (kk == ~uint64_t(0)) continue;
-          const int f = int(uint32_t(kk & 0xFFFFFFu) / uint32_t(HoWo));
-          if (fexcl[f >> 5] >> (f & 31) & 1) continue;  // inhibited map: no other candidate here
-          const int y = pos / a.Wo, x = pos - y * a.Wo;
-          bool near = false;
-          for (int i = 0; i < nw; ++i) near |= (abs(y - wy[i]) <= s.r) && (abs(x - wx[i]) <= s.r);
-          if (!near) best = kk < best ? kk : best;
-        }
-        best = warp_min_u64(best);
-        if (lane == 0) red[warp] = best;
-        __syncthreads();
-        if (warp == 0) {
-          uint64_t x = lane < nwarps ? red[lane] : ~uint64_t(0);
-          x = warp_min_u64(x);
-          if (lane == 0 && x != ~uint64_t(0)) {
-            const int idx = int(x & 0xFFFFFFu);
-            const int f = idx / HoWo, p = idx - f * HoWo;
-            const int yy = p / a.Wo, xx = p - yy * a.Wo;
-            const int c = s_count;
-            int32_t* wrec = s.winners + (int64_t(img) * s.k + c) * 3;
-            wrec[0] = f; wrec[1] = yy; wrec[2] = xx;
-            s.post[int64_t(img) * s.k + c] = int(x >> 56);  // the winner's spike time (key bits 56..63)
-            wy[c] = yy; wx[c] = xx;
-            fexcl[f >> 5] |= 1u << (f & 31);
-            s_count = c + 1;
+          if (l != kNoSpike) {
+            const uint64_t kk = wta_key(l, vo[j], uint32_t(fbase + j));
+            best = kk < best ? kk : best;
           }
         }
-        __syncthreads();
-        if (s_count == round) break;  // no candidate left
+      best = warp_min_u64(best);
+      if (lane == 0) s.gbest[int64_t(g) * HoWo + pos] = best;
+      __syncwarp();
+    }
+    if (blockIdx.x == 0) { __syncthreads(); if (tid == 0) s.stamps[img * 6 + 1] = globaltimer_ns(); }
+    if (img == 100) { __syncthreads(); if (tid == 0) s.stamps[int64_t(s.N) * 6 + blockIdx.x * 2 + 1] = globaltimer_ns(); }
+    grid_barrier(s.bar, gen);
+    if (blockIdx.x == 0 && tid == 0) s.stamps[img * 6 + 2] = globaltimer_ns();
+    // ---------------- B (CTA 0): pointwise inhibition, then k-WTA on the inhibited map ----------------
+    if (blockIdx.x == 0 && !(s.dbg & 2)) {
+      for (int pos = tid; pos < HoWo; pos += blockDim.x) {  // best (lat, v, f) per position over the groups
+        uint64_t best = ~uint64_t(0);
+        for (int gg = 0; gg < s.n_groups; ++gg) {
+          const uint64_t kk = s.gbest[int64_t(gg) * HoWo + pos];
+          best = kk < best ? kk : best;
+        }
+        uint64_t cand = ~uint64_t(0);  // the survivor's k-WTA key: flat index f * HoWo + pos (R14)
+        if (best != ~uint64_t(0)) cand = (best & ~uint64_t(0xFFFFFFu)) | uint64_t(uint32_t(best & 0xFFFFFFu) * HoWo + pos);
+        keys[pos] = cand;
+        fpos[pos] = best != ~uint64_t(0) ? uint16_t(best & 0xFFFFFFu) : uint16_t(0xFFFF);
       }
-      for (int i = s_count + tid; i < s.k; i += blockDim.x) {
+      __syncthreads();
+      if (img == 100 && tid == 0) s.stamps[int64_t(s.N) * 6 + 400] = globaltimer_ns();
+      if (warp == 0) {  // k-WTA rounds by one warp (no block barriers)
+        // inhibited map: one candidate key per position; a round's winner kills the positions of its
+        // feature and those within Chebyshev distance r (R15), so each round is a plain warp min
+        int nwin = 0;
+        auto emit = [&](uint64_t best, int f, int yy, int xx) {
+          if (lane == 0) {
+            int32_t* wrec = s.winners + (int64_t(img) * s.k + nwin) * 3;
+            wrec[0] = f; wrec[1] = yy; wrec[2] = xx;
+            s.post[int64_t(img) * s.k + nwin] = int(best >> 56);  // the winner's spike time (key bits 56..63)
+          }
+        };
+        if (HoWo <= 32 * 8 && a.Ho <= 256 && a.Wo <= 256) {
+          // small maps: every lane keeps its <= 8 positions' keys and (f, y, x) in registers
+          uint64_t kr[8];
+          uint32_t fxy[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int pos = lane + 32 * j;
+            kr[j] = pos < HoWo ? keys[pos] : ~uint64_t(0);
+            fxy[j] = pos < HoWo ? (uint32_t(fpos[pos]) << 16 | uint32_t(ypos[pos]) << 8 | uint32_t(xpos[pos])) : 0u;
+          }
+          for (int round = 0; round < s.k; ++round) {
+            uint64_t mine = ~uint64_t(0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) mine = kr[j] < mine ? kr[j] : mine;
+            const uint32_t hi = __reduce_min_sync(0xffffffffu, uint32_t(mine >> 32));
+            const uint32_t lo = __reduce_min_sync(0xffffffffu, uint32_t(mine >> 32) == hi ? uint32_t(mine) : ~0u);
+            const uint64_t best = uint64_t(hi) << 32 | lo;
+            if (best == ~uint64_t(0)) break;  // no candidate left
+            uint32_t w = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) w = kr[j] == best ? fxy[j] : w;
+            const int src = __ffs(__ballot_sync(0xffffffffu, mine == best)) - 1;
+            w = __shfl_sync(0xffffffffu, w, src);
+            const int f = int(w >> 16), yy = int(w >> 8 & 0xFFu), xx = int(w & 0xFFu);
+            emit(best, f, yy, xx);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int fj = int(fxy[j] >> 16), yj = int(fxy[j] >> 8 & 0xFFu), xj = int(fxy[j] & 0xFFu);
+              if (fj == f || (abs(yj - yy) <= s.r && abs(xj - xx) <= s.r)) kr[j] = ~uint64_t(0);
+            }
+            ++nwin;
+          }
+        } else {
+          for (int round = 0; round < s.k; ++round) {
+            uint64_t best = ~uint64_t(0);
+            for (int pos = lane; pos < HoWo; pos += 32) {
+              const uint64_t kk = keys[pos];
+              best = kk < best ? kk : best;
+            }
+            best = warp_min_u64(best);
+            if (best == ~uint64_t(0)) break;  // no candidate left
+            const int idx = int(best & 0xFFFFFFu);
+            const int f = idx / HoWo, p = idx - f * HoWo;
+            const int yy = p / a.Wo, xx = p - yy * a.Wo;
+            emit(best, f, yy, xx);
+            for (int pos = lane; pos < HoWo; pos += 32)
+              if (int(fpos[pos]) == f || (abs(int(ypos[pos]) - yy) <= s.r && abs(int(xpos[pos]) - xx) <= s.r))
+                keys[pos] = ~uint64_t(0);
+            __syncwarp();
+            ++nwin;
+          }
+        }
+        if (lane == 0) s_count = nwin;
+      }
+      __syncthreads();
+      if (img == 100 && tid == 0) s.stamps[int64_t(s.N) * 6 + 401] = globaltimer_ns();
+      for (int i = s_count + tid; i < s.k; i += blockDim.x) {  // unused winner slots: -1
         int32_t* wrec = s.winners + (int64_t(img) * s.k + i) * 3;
         wrec[0] = -1; wrec[1] = -1; wrec[2] = -1;
       }
       if (tid == 0) s.count[img] = s_count;
+      __syncthreads();
+      if (tid == 0) s.stamps[img * 6 + 3] = globaltimer_ns();
     }
     grid_barrier(s.bar, gen);
+    if (blockIdx.x == 0 && tid == 0) s.stamps[img * 6 + 4] = globaltimer_ns();
     // ---------------- C: Eq. 4 on this group's winners (shared-memory copy; leader writes fp32) ----------------
     {
-      const int nwin = s.count[img];
+      const int nwin = (s.dbg & 4) ? 0 : s.count[img];
       const int KK = a.KH * a.KW;
       for (int i = 0; i < nwin; ++i) {
         const int32_t* wrec = s.winners + (int64_t(img) * s.k + i) * 3;
@@ -235,6 +309,7 @@ __global__ void __launch_bounds__(FPL == 4 ? 768 : 1024, 1) seq_train_kernel(con
         for (int64_t i = int64_t(f0) * R + tid; i < int64_t(f1) * R; i += blockDim.x) snap[i] = s.w[i];
       }
       __syncthreads();
+      if (blockIdx.x == 0 && tid == 0) s.stamps[img * 6 + 5] = globaltimer_ns();
     }
   }
 }
@@ -244,6 +319,7 @@ struct SeqPlan {
   int fpl, n_groups, FGS, nwarps, smem, grid;
   WalkArgs a;
   int off_keys;
+  int rec, hdr, npre, buf_bytes;  // presorted records and the per-warp prefetch buffers
 };
 
 static int al16h(int x) { return (x + 15) & ~15; }
@@ -262,18 +338,24 @@ static bool seq_plan(int C, int H, int W, int pad, int F, int KH, int KW, int T,
     const int fpl = fpls[i], fgs = 32 * fpl;
     if (fpl > 1 && F <= fgs / 2) continue;  // lanes would idle
     const int nwarps = fpl == 4 ? 24 : 32;
-    int o = 0;
-    a.cnt_off = o; o += al16h(T * 4);
-    a.start_off = o; o += al16h((T + 1) * 2);
-    a.list_off = o; o += al16h((R + T + kIt) * 4);
-    a.pos_bytes = o; a.warp_bytes = o;
     a.row_bytes = fgs * 4;
     const int wsb = al16h((R + 1) * fgs * 4);
-    a.off_eoff = wsb;
-    a.off_ekk = a.off_eoff + al16h(R * 4);
-    a.off_warps = a.off_ekk + al16h(R * 2);
+    pl->hdr = al16h((T + 1) * 2);
+    pl->rec = pl->hdr + int((R + T + kIt - 1) / kIt) * kIt * 4;
+    // per warp: 2 mbarriers + 2 record buffers [header | up to 256 prefetched entries]
+    const long left = (220L * 1024 - wsb - al16h(HoWo * 8) - al16h(HoWo * 6)) / nwarps - 16;
+    int npre = int(((left / 2 - pl->hdr) / 4) / kIt) * kIt;
+    const int full = pl->rec - pl->hdr;
+    if (npre > full / 4) npre = full / 4;
+    if (npre > 256) npre = 256;
+    if (npre < kIt) continue;
+    pl->npre = npre;
+    pl->buf_bytes = pl->hdr + npre * 4;
+    a.off_eoff = wsb; a.off_ekk = wsb;
+    a.off_warps = wsb;
+    a.warp_bytes = 16 + 2 * pl->buf_bytes;
     const int off_keys = a.off_warps + nwarps * a.warp_bytes;
-    const int smem = off_keys + al16h(HoWo * 8);
+    const int smem = off_keys + al16h(HoWo * 8) + al16h(HoWo * 6);
     if (smem > 220 * 1024) continue;
     pl->fpl = fpl; pl->FGS = fgs; pl->nwarps = nwarps; pl->smem = smem; pl->off_keys = off_keys;
     pl->n_groups = (F + fgs - 1) / fgs;
@@ -286,13 +368,18 @@ static bool seq_plan(int C, int H, int W, int pad, int F, int KH, int KW, int T,
 }
 
 static size_t r256(size_t x) { return (x + 255) & ~size_t(255); }
-// workspace: [barrier words 256 B][lat_map F*HoWo][v_map F*HoWo*4][post N*k*4]
+// workspace: [barrier words 256 B][lat_map F*HoWo][v_map F*HoWo*4][post N*k*4][gbest n_groups*HoWo*8]
+//            [stamps N*48][presorted records N*HoWo*rec][slack]
 size_t seq_train_workspace(int C, int H, int W, int pad, int F, int KH, int KW, int T, int k, int N) {
   SeqPlan pl;
   if (!seq_plan(C, H, W, pad, F, KH, KW, T, &pl)) return 0;
   const size_t HoWo = size_t(pl.a.Ho) * pl.a.Wo;
-  return 256 + r256(size_t(F) * HoWo) + r256(size_t(F) * HoWo * 4) + r256(size_t(N) * k * 4);
+  return 256 + r256(size_t(F) * HoWo) + r256(size_t(F) * HoWo * 4) + r256(size_t(N) * k * 4) +
+         r256(size_t(pl.n_groups) * HoWo * 8) + r256(size_t(N) * 48 + 16384) + r256(size_t(N) * HoWo * pl.rec) + 4096;
 }
+
+int rf_sort_lists_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, int KH, int KW, int T,
+                         int row_bytes, unsigned char* lists, int rec, int hdr, cudaStream_t s);
 
 template <int FPL>
 static int seq_go(const SeqPlan& pl, SeqArgs& s, cudaStream_t st) {
@@ -335,8 +422,17 @@ int seq_train_launch(const uint8_t* lat_all, int N, int C, int H, int W, int pad
   s.lat_map = p + 256;
   s.v_map = reinterpret_cast<float*>(p + 256 + r256(size_t(F) * HoWo));
   s.post = reinterpret_cast<int32_t*>(p + 256 + r256(size_t(F) * HoWo) + r256(size_t(F) * HoWo * 4));
+  s.gbest = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(s.post) + r256(size_t(N) * k * 4));
+  s.stamps = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(s.gbest) + r256(size_t(pl.n_groups) * HoWo * 8));
+  unsigned char* lists = reinterpret_cast<unsigned char*>(s.stamps) + r256(size_t(N) * 48 + 16384);
+  s.lists = lists; s.rec = pl.rec; s.hdr = pl.hdr; s.npre = pl.npre; s.buf_bytes = pl.buf_bytes;
+  s.wa.npre = pl.npre;
+  // every image's receptive fields sorted up front (they do not depend on the weights)
+  int rc = rf_sort_lists_launch(lat_all, N, C, H, W, pad, KH, KW, T, pl.a.row_bytes, lists, pl.rec, pl.hdr, st);
+  if (rc) return rc;
   s.winners = winners; s.count = count;
   s.n_groups = pl.n_groups; s.FGS = pl.FGS; s.off_keys = pl.off_keys;
+  s.dbg = getenv("SNN_SEQ_DBG") ? atoi(getenv("SNN_SEQ_DBG")) : 0;
   if (cudaMemsetAsync(s.bar, 0, 2 * sizeof(unsigned), st) != cudaSuccess) return check_launch("snn_stdp_sequence");
   switch (pl.fpl) {
     case 4: return seq_go<4>(pl, s, st);

@@ -207,6 +207,47 @@ class SeqGraph:
         self.graph.replay()
 
 
+class SeqPersistent:
+    """All n sequential plasticity steps of one conv layer (conv+fire -> inhibit -> k-WTA -> STDP) in
+    one persistent kernel (snn_stdp_sequence).  ``replay()`` restores the initial
+    weights first, so every replay is one training pass over the same n images (like SeqGraph)."""
+
+    def __init__(self, spec, w0, lat_in_all: torch.Tensor, T: int, k: int, r: int, rates: Dict,
+                 snapshot_every: int = 0, device="cuda"):
+        self.spec, self.T, self.k, self.r, self.rates = spec, T, k, r, rates
+        self.w = _dev(w0, device).clone()
+        self.w0 = self.w.clone()
+        self.lat = lat_in_all.contiguous()
+        n = self.lat.shape[0]
+        self.every = snapshot_every
+        self.snaps = (torch.empty((n // snapshot_every,) + tuple(self.w.shape), dtype=torch.float32, device=device)
+                      if snapshot_every else None)
+        self.winners = torch.empty((n, k, 3), dtype=torch.int32, device=device)
+        self.count = torch.empty((n,), dtype=torch.int32, device=device)
+        N, C, H, W = self.lat.shape
+        F, _, KH, KW = self.w.shape
+        nb = int(snn.lib().snn_stdp_sequence_workspace(N, C, H, W, spec.pad, F, KH, KW, T, k))
+        self.ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=device)
+        self.launches = 0  # replay() launches through libsnn (counted by snn_launch_count itself)
+
+    @staticmethod
+    def supported(spec, lat_shape, w_shape, T: int, k: int) -> bool:
+        N, C, H, W = lat_shape
+        F, _, KH, KW = w_shape
+        return not math.isinf(spec.theta) and \
+            int(snn.lib().snn_stdp_sequence_workspace(N, C, H, W, spec.pad, F, KH, KW, T, k)) > 0
+
+    def run(self):
+        R = self.rates
+        snn.stdp_sequence(self.lat, self.w, self.spec.pad, self.T, self.spec.theta, self.k, self.r, R["a_plus"],
+                          R["a_minus"], R["lb"], R["ub"], R["stabilizer"], winners=self.winners, count=self.count,
+                          snapshots=self.snaps, snap_every=self.every, ws=self.ws)
+
+    def replay(self):
+        self.w.copy_(self.w0)
+        self.run()
+
+
 class StepGraph:
     """CUDA graph of one fixed sequence of libsnn calls (``fn``) on preallocated buffers."""
 
