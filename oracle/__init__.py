@@ -48,6 +48,9 @@ def lib():
             p = C.c_void_p
             i64, i32, f32 = C.c_int64, C.c_int, C.c_float
             sig = {
+                "orc_filter_bank": (None, [p, i64, i32, i32, p, i32, i32, i32, C.c_double, i32, p]),
+                "orc_local_norm": (None, [p, i64, i32, i32, i32, i32, C.c_double, p]),
+                "orc_lateral_inhibition": (None, [p, i64, i32, i32, i32, p, i32, p]),
                 "orc_encode": (None, [p, i64, i64, i32, p]),
                 "orc_expand": (None, [p, i64, i64, i32, p]),
                 "orc_potentials": (None, [p, i32, i32, i32, i32, p, i32, i32, i32, i32, p]),
@@ -242,3 +245,37 @@ def decide(winners: np.ndarray, count: int, F: int, n_classes: int, label: int):
     d = C.c_int(0)
     rw = lib().orc_decide(_ptr(winners), int(count), F, n_classes, int(label), C.byref(d))
     return int(d.value), int(rw)
+
+
+# ------------------------------------------------------------------------------ f2 front end
+def filter_bank(img: np.ndarray, kernels: np.ndarray, pad: int, mode: int = 0,
+                threshold: float = -math.inf) -> np.ndarray:
+    """[B,H,W] fp64 images * [K,S,S] fp64 kernels -> fp32 [B,Kout,Ho,Wo] (R33; mode 0 thresholded,
+    1 DoG on/off split, 2 rectified)."""
+    img = np.ascontiguousarray(img, dtype=np.float64)
+    ker = np.ascontiguousarray(kernels, dtype=np.float64)
+    B, H, W = img.shape
+    K, S, _ = ker.shape
+    Ho, Wo = H + 2 * pad - S + 1, W + 2 * pad - S + 1
+    out = np.zeros((B, 2 * K if mode == 1 else K, Ho, Wo), dtype=np.float32)
+    lib().orc_filter_bank(_ptr(img), B, H, W, _ptr(ker), K, S, pad, float(threshold), mode, _ptr(out))
+    return out
+
+
+def local_norm(x: np.ndarray, radius: int, eps: float = 1e-12) -> np.ndarray:
+    """x / max(regional mean, eps), border windows truncated (R34)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    B, Cc, H, W = x.shape
+    out = np.empty_like(x)
+    lib().orc_local_norm(_ptr(x), B, Cc, H, W, radius, float(eps), _ptr(out))
+    return out
+
+
+def lateral_inhibition(x: np.ndarray, factors) -> np.ndarray:
+    """Intensity lateral inhibition, SPEC's descending-intensity sweep (R35)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    f = np.ascontiguousarray(np.asarray(factors, dtype=np.float32))
+    B, Cc, H, W = x.shape
+    out = np.empty_like(x)
+    lib().orc_lateral_inhibition(_ptr(x), B, Cc, H, W, _ptr(f), len(f), _ptr(out))
+    return out

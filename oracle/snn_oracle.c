@@ -391,3 +391,123 @@ int orc_decide(const int32_t* winners, int count, int F, int n_classes, int labe
     *decision = winners[0] / (F / n_classes);
     return (*decision == label) ? 1 : -1;
 }
+
+/* ------------------------------------------------------------------------- */
+/* f2: the input-transform front end of the paper's pipeline  */
+/* ("utils.Filter ... DoG and Gabor kernels", "intensity_lateral_   */
+/* inhibition ... local_normalization", P:232 InputTransform).  The paper gives   */
+/* intent only; the readings R33-R35 follow SPEC.md's definitions.    */
+/* ------------------------------------------------------------------------- */
+
+/* R33: zero-padded cross-correlation of [B][H][W] fp64 images with [K][S][S] fp64
+ * kernels, fp64 sum over (dy, dx) in row-major kernel order, one multiply
+ * and one add per term (no fused multiply-add), then per mode:
+ *   mode 0: out[b][k] = r, values below `threshold` set to 0 (SPEC apply_filter_bank);
+ *   mode 1: DoG on/off split, out[b][2k] = max(r, 0), out[b][2k+1] = max(-r, 0);
+ *   mode 2: rectified, out[b][k] = max(r, 0) (Gabor).
+ * Output fp32 (round to nearest), [B][Kout][Ho][Wo], Ho = H + 2 pad - S + 1.       */
+void orc_filter_bank(const double* img, int64_t B, int H, int W, const double* ker, int K, int S, int pad,
+                     double threshold, int mode, float* out) {
+    const int Ho = H + 2 * pad - S + 1, Wo = W + 2 * pad - S + 1;
+    const int Kout = mode == 1 ? 2 * K : K;
+#pragma omp parallel for schedule(static)
+    for (int64_t b = 0; b < B; ++b) {
+        const double* im = img + b * (int64_t)H * W;
+        for (int k = 0; k < K; ++k) {
+            const double* kk = ker + (int64_t)k * S * S;
+            for (int y = 0; y < Ho; ++y) {
+                for (int x = 0; x < Wo; ++x) {
+                    double r = 0.0;
+                    for (int dy = 0; dy < S; ++dy) {
+                        for (int dx = 0; dx < S; ++dx) {
+                            const int yy = y + dy - pad, xx = x + dx - pad;
+                            const double p = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? im[(int64_t)yy * W + xx] : 0.0;
+                            const double term = p * kk[dy * S + dx];
+                            r = r + term;
+                        }
+                    }
+                    const int64_t o = (int64_t)y * Wo + x;
+                    if (mode == 0) {
+                        out[((b * Kout) + k) * (int64_t)Ho * Wo + o] = (float)(r < threshold ? 0.0 : r);
+                    } else if (mode == 1) {
+                        out[((b * Kout) + 2 * k) * (int64_t)Ho * Wo + o] = (float)(r > 0.0 ? r : 0.0);
+                        out[((b * Kout) + 2 * k + 1) * (int64_t)Ho * Wo + o] = (float)(-r > 0.0 ? -r : 0.0);
+                    } else {
+                        out[((b * Kout) + k) * (int64_t)Ho * Wo + o] = (float)(r > 0.0 ? r : 0.0);
+                    }
+                }
+            }
+        }
+    }
+}
+
+/* R34: local normalization ("uses regional mean for normalizing intensity
+ * values"): out = x / max(mean of the (2 radius + 1)^2 window around it, eps), the
+ * window truncated at the borders (SPEC); fp64 window sum in row-major order, the
+ * mean as sum / count, the division in fp64, output fp32.                           */
+void orc_local_norm(const float* x, int64_t B, int C, int H, int W, int radius, double eps, float* out) {
+#pragma omp parallel for schedule(static)
+    for (int64_t bc = 0; bc < B * C; ++bc) {
+        const float* xc = x + bc * (int64_t)H * W;
+        float* oc = out + bc * (int64_t)H * W;
+        for (int y = 0; y < H; ++y) {
+            for (int xx = 0; xx < W; ++xx) {
+                double s = 0.0;
+                int cnt = 0;
+                for (int yy = y - radius; yy <= y + radius; ++yy) {
+                    if (yy < 0 || yy >= H) continue;
+                    for (int x2 = xx - radius; x2 <= xx + radius; ++x2) {
+                        if (x2 < 0 || x2 >= W) continue;
+                        s = s + (double)xc[(int64_t)yy * W + x2];
+                        ++cnt;
+                    }
+                }
+                double m = s / (double)cnt;
+                if (m < eps) m = eps;
+                oc[(int64_t)y * W + xx] = (float)((double)xc[(int64_t)y * W + xx] / m);
+            }
+        }
+    }
+}
+
+/* R35: intensity lateral inhibition ("decreases the surrounding intensities
+ * ... of each salient point"), SPEC's sweep: locations are processed in descending
+ * order of their ORIGINAL intensity (ties: row-major index ascending); each processed
+ * location multiplies every strictly weaker location of the same channel within
+ * Chebyshev distance n (1 <= d <= n) by factors[d - 1].  Done literally: sort, sweep,
+ * fp32 multiplications in sweep order.                                                */
+typedef struct { float v; int idx; } orc_li_item;
+static int orc_li_cmp(const void* a, const void* b) {
+    const orc_li_item* p = (const orc_li_item*)a;
+    const orc_li_item* q = (const orc_li_item*)b;
+    if (p->v > q->v) return -1;
+    if (p->v < q->v) return 1;
+    return (p->idx < q->idx) ? -1 : (p->idx > q->idx);
+}
+void orc_lateral_inhibition(const float* x, int64_t B, int C, int H, int W, const float* factors, int n,
+                            float* out) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t bc = 0; bc < B * C; ++bc) {
+        const float* xc = x + bc * (int64_t)H * W;
+        float* oc = out + bc * (int64_t)H * W;
+        orc_li_item* it = (orc_li_item*)malloc(sizeof(orc_li_item) * (size_t)H * W);
+        for (int i = 0; i < H * W; ++i) { it[i].v = xc[i]; it[i].idx = i; oc[i] = xc[i]; }
+        qsort(it, (size_t)H * W, sizeof(orc_li_item), orc_li_cmp);
+        for (int s = 0; s < H * W; ++s) {
+            const int p = it[s].idx, py = p / W, px = p % W;
+            const float vp = xc[p];
+            for (int yy = py - n; yy <= py + n; ++yy) {
+                if (yy < 0 || yy >= H) continue;
+                for (int x2 = px - n; x2 <= px + n; ++x2) {
+                    if (x2 < 0 || x2 >= W || (yy == py && x2 == px)) continue;
+                    const int q = yy * W + x2;
+                    if (!(xc[q] < vp)) continue; /* only strictly weaker neighbours */
+                    const int dy = yy > py ? yy - py : py - yy, dx = x2 > px ? x2 - px : px - x2;
+                    const int d = dy > dx ? dy : dx;
+                    oc[q] = oc[q] * factors[d - 1];
+                }
+            }
+        }
+        free(it);
+    }
+}
