@@ -127,36 +127,41 @@ class C2Step:
         self.B = batch
         self.net = pipeline.C2Net(self.wl, batch, device=dev)
         self.x = torch.from_numpy(self.wl.X).to(dev)
-        self.stages = ["encode", "conv1", "pool1", "conv2", "pool2", "conv3", "kwta", "decide"]
+        # f2 front end: the step starts from the raw fp64 images and filters them on the GPU (R33)
+        self.raw = torch.from_numpy(self.wl.extra["raw"]).to(dev)
+        self.bank = torch.from_numpy(self.wl.extra["bank"]).to(dev)
+        self.stages = ["dog", "encode", "conv1", "pool1", "conv2", "pool2", "conv3", "kwta", "decide"]
 
     def run(self, ev=None):
         n, snn, T = self.net, self.snn, self.wl.T
         s1, s2, s3 = self.wl.convs
+        fr = self.wl.extra["front"]
 
         def mark(i):
             if ev is not None:
                 ev[i].record()
         mark(0)
-        snn.encode(self.x, T, out=n.lat0, ws=n.ws_enc); mark(1)
-        snn.conv_fire(n.lat0, n.w[0], s1.pad, T, s1.theta, lat_out=n.l1.lat, v_out=n.l1.v, ws=n.l1.ws); mark(2)
+        snn.filter_bank(self.raw, self.bank, fr["pad"], mode=fr["mode"], out=self.x); mark(1)
+        snn.encode(self.x, T, out=n.lat0, ws=n.ws_enc); mark(2)
+        snn.conv_fire(n.lat0, n.w[0], s1.pad, T, s1.theta, lat_out=n.l1.lat, v_out=n.l1.v, ws=n.l1.ws); mark(3)
         p = n.l1.pool_spec
-        snn.pool(n.l1.lat, None, (p.PH, p.PW), (p.SH, p.SW), (p.DH, p.DW), lat_out=n.l1.plat); mark(3)
-        snn.conv_fire(n.l1.plat, n.w[1], s2.pad, T, s2.theta, lat_out=n.l2.lat, v_out=n.l2.v, ws=n.l2.ws); mark(4)
+        snn.pool(n.l1.lat, None, (p.PH, p.PW), (p.SH, p.SW), (p.DH, p.DW), lat_out=n.l1.plat); mark(4)
+        snn.conv_fire(n.l1.plat, n.w[1], s2.pad, T, s2.theta, lat_out=n.l2.lat, v_out=n.l2.v, ws=n.l2.ws); mark(5)
         p = n.l2.pool_spec
-        snn.pool(n.l2.lat, None, (p.PH, p.PW), (p.SH, p.SW), (p.DH, p.DW), lat_out=n.l2.plat); mark(5)
-        snn.conv_fire(n.l2.plat, n.w[2], s3.pad, T, s3.theta, lat_out=n.l3.lat, v_out=n.l3.v, ws=n.l3.ws); mark(6)
-        snn.k_winners(n.l3.lat, n.l3.v, 1, 0, winners=n.winners, count=n.count, ws=n.ws_kw); mark(7)
+        snn.pool(n.l2.lat, None, (p.PH, p.PW), (p.SH, p.SW), (p.DH, p.DW), lat_out=n.l2.plat); mark(6)
+        snn.conv_fire(n.l2.plat, n.w[2], s3.pad, T, s3.theta, lat_out=n.l3.lat, v_out=n.l3.v, ws=n.l3.ws); mark(7)
+        snn.k_winners(n.l3.lat, n.l3.v, 1, 0, winners=n.winners, count=n.count, ws=n.ws_kw); mark(8)
         snn.decide(n.winners, n.count, s3.F, self.wl.extra["n_classes"], None, decision=n.decision,
-                   reward=n.reward); mark(8)
+                   reward=n.reward); mark(9)
 
     def e2e(self, x_host, out_host):
-        """Public-API path with host buffers: H2D of the inputs, the step, D2H of the decisions."""
-        self.x.copy_(x_host, non_blocking=True)
+        """Public-API path with host buffers: H2D of the raw images, the step, D2H of the decisions."""
+        self.raw.copy_(x_host, non_blocking=True)
         self.run()
         out_host.copy_(self.net.decision, non_blocking=True)
 
     def host_io(self):
-        xh = self.torch.from_numpy(self.wl.X).pin_memory()
+        xh = self.torch.from_numpy(self.wl.extra["raw"]).pin_memory()
         oh = self.torch.empty((self.B,), dtype=self.torch.int32).pin_memory()
         return xh, oh
 
@@ -174,7 +179,7 @@ class C2Step:
 
     def config(self):
         return {"workload": "c2: BASELINE.json configs[1], 3-layer DCSNN inference, T=15",
-                "global_batch": self.B, "images": "28x28 strokes -> 6-ch DoG on/off (synthetic)",
+                "global_batch": self.B, "images": "raw 28x28 fp64 strokes (synthetic) -> GPU DoG bank on/off (6 ch)",
                 "layers": "F30 5x5 p2 th15 -> pool2/2 -> F250 3x3 p1 th10 -> pool3/3 -> F200 5x5 p2 th=inf -> 1 winner",
                 "l2": "flushed between timed steps (256 MiB write, outside the step events)"}
 
@@ -185,8 +190,9 @@ class C2Step:
         from oracle import flows
         import synth
         wl = self.wl if n == self.B else synth.Workload("c2", self.wl.T, self.wl.X[:n], self.wl.convs,
-                                                         self.wl.weights, self.wl.pools, self.wl.extra)
-        flows.c2(wl)
+                                                         self.wl.weights, self.wl.pools,
+                                                         dict(self.wl.extra, raw=self.wl.extra["raw"][:n]))
+        flows.c2(wl, front=True)
 
 
 class C5Step(C2Step):

@@ -46,6 +46,37 @@ typedef void* snn_stream_t;
 #define SNN_EWORKSPACE (-5) /* workspace pointer NULL or smaller than *_workspace() */
 
 /* ---------------------------------------------------------------------------------------------
+ * f2. Front end: the preprocessing ahead of a1.  Each output is bit-identical
+ * to the definition stated (explicitly rounded operations in the stated order, no FMA).  Outputs
+ * must not alias inputs.  No workspace.
+ *
+ * snn_filter_bank (P:133 utils.Filter; DoG P:223, Gabor P:232; reading R33):
+ *   img fp64 [B, H, W] grayscale images; kernels fp64 [K, S, S] (the DoG/Gabor taps, built by the
+ *   caller); out fp32 [B, Kout, Ho, Wo], Ho = H + 2 pad - S + 1, Wo likewise.  For each kernel k,
+ *   r = sum over (dy, dx) in row-major order of img[y + dy - pad, x + dx - pad] * kernels[k, dy, dx]
+ *   (cross-correlation, zero outside the image) accumulated in fp64.  mode 0: out[k] = r < threshold
+ *   ? 0 : r (Kout = K); mode 1 (on/off DoG): out[2k] = max(r, 0), out[2k+1] = max(-r, 0) (Kout = 2K);
+ *   mode 2: out[k] = max(r, 0) (Kout = K).  Each cast to fp32 rounds to nearest.
+ *   Requires 1 <= S <= 31, 0 <= pad < S, Ho, Wo >= 1, K >= 1, the taps and the 8 x 32 tile's halo
+ *   within 200 KB of shared memory (SNN_ESHAPE otherwise); mode in {0, 1, 2} (SNN_EINVAL).
+ * snn_local_norm ("uses regional mean for normalizing intensity values"; reading R34):
+ *   x, out fp32 [B, C, H, W]; out = x / max(m, eps) with m = (fp64 sum, row-major, of the window
+ *   [y - radius, y + radius] x [x - radius, x + radius] truncated at the borders) / (its size),
+ *   the division in fp64.  Requires 0 <= radius <= 32, eps > 0.
+ * snn_lateral_inhibition (P:126 intensity lateral inhibition; reading R35):
+ *   x, out fp32 [B, C, H, W]; factors fp32 [n] (device).  Per (b, c) plane, locations are visited in
+ *   (x descending, flat index y W + x ascending) order; visiting p multiplies (fp32) the running value
+ *   of every location q with x[q] < x[p] and Chebyshev distance d = max(|dy|, |dx|) in [1, n] by
+ *   factors[d - 1].  out starts as x.  Requires 0 <= n <= 32 (n = 0 copies).
+ * ------------------------------------------------------------------------------------------- */
+SNN_API int snn_filter_bank(const double* img, int B, int H, int W, const double* kernels, int K, int S, int pad,
+                            double threshold, int mode, float* out, snn_stream_t s);
+SNN_API int snn_local_norm(const float* x, int B, int C, int H, int W, int radius, double eps, float* out,
+                           snn_stream_t s);
+SNN_API int snn_lateral_inhibition(const float* x, int B, int C, int H, int W, const float* factors, int n,
+                                   float* out, snn_stream_t s);
+
+/* ---------------------------------------------------------------------------------------------
  * a1. Intensity -> latency encoding (P:51, P:135 utils.Intensity2Latency; readings R1, R2).
  * x   : float32 [B, C, H, W] intensities.  Per image, the N strictly positive entries (x > 0;
  *       zero, negative and NaN never spike) are ranked by (value descending, flat index c*H*W +

@@ -12,7 +12,7 @@ from typing import Dict, List
 
 import numpy as np
 
-from . import conv_fire, decide, encode, inhibit, k_winners, pool, stdp
+from . import conv_fire, decide, encode, filter_bank, inhibit, k_winners, pool, stdp
 
 
 def layer(lat_in, w, spec, T, pool_spec=None):
@@ -40,9 +40,14 @@ def c1(wl) -> Dict[str, np.ndarray]:
                 winners=win, count=cnt, w_new=w_new)
 
 
-def c2(wl, n: int = None) -> Dict[str, np.ndarray]:
-    """3-layer inference: encode -> [conv+fire -> pool] x2 -> conv (theta=inf) -> 1 winner -> class."""
+def c2(wl, n: int = None, front: bool = False) -> Dict[str, np.ndarray]:
+    """3-layer inference: encode -> [conv+fire -> pool] x2 -> conv (theta=inf) -> 1 winner -> class.
+    front=True starts from the raw images (extra["raw"]) through the f2 filter bank (R33) instead of X."""
     X = wl.X if n is None else wl.X[:n]
+    if front:
+        fr = wl.extra["front"]
+        raw = wl.extra["raw"] if n is None else wl.extra["raw"][:n]
+        X = filter_bank(raw, wl.extra["bank"], fr["pad"], mode=fr["mode"])
     T = wl.T
     lat0 = encode(X, T)
     l1 = layer(lat0, wl.weights[0], wl.convs[0], T, wl.pools[0])

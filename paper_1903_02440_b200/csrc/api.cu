@@ -40,6 +40,13 @@ int stdp_launch(float* w, int F, int C, int KH, int KW, const uint8_t* lat_in, i
                 float a_plus, float a_minus, float lb, float ub, int stabilizer, const float* reward, cudaStream_t s);
 int count_events_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, int F, int KH, int KW, int T,
                         const uint8_t* lat_out, unsigned long long* out, cudaStream_t s);
+size_t filter_bank_smem(int K, int S);
+size_t stencil_smem(int r, int extra);
+int filter_bank_launch(const double* img, int B, int H, int W, const double* ker, int K, int S, int pad, double thr,
+                       int mode, float* out, cudaStream_t s);
+int local_norm_launch(const float* x, int B, int C, int H, int W, int R, double eps, float* out, cudaStream_t s);
+int lateral_inhibition_launch(const float* x, int B, int C, int H, int W, const float* factors, int n, float* out,
+                              cudaStream_t s);
 int decide_launch(const int32_t* winners, const int32_t* count, int B, int k, int F, int n_classes,
                   const int32_t* labels, int32_t* decision, float* reward, cudaStream_t s);
 
@@ -126,6 +133,40 @@ int snn_sync_status(snn_stream_t s) {
 size_t snn_encode_workspace(int B, int C, int H, int W, int T) {
   if (B < 0 || C < 0 || H < 0 || W < 0 || T < 1 || T > 254) return 0;
   return encode_workspace(B, C, H, W, T);
+}
+
+int snn_filter_bank(const double* img, int B, int H, int W, const double* kernels, int K, int ksize, int pad,
+                    double threshold, int mode, float* out, snn_stream_t s) {
+  REQUIRE(mode >= 0 && mode <= 2, SNN_EINVAL, "snn_filter_bank: mode=%d not in {0, 1, 2}", mode);
+  REQUIRE(!(threshold != threshold), SNN_EINVAL, "snn_filter_bank: NaN threshold");
+  REQUIRE(B >= 0 && H >= 1 && W >= 1 && K >= 1, SNN_ESHAPE, "snn_filter_bank: bad dimension");
+  REQUIRE(ksize >= 1 && ksize <= 31 && pad >= 0 && pad < ksize, SNN_ESHAPE, "snn_filter_bank: S=%d pad=%d", ksize, pad);
+  REQUIRE(H + 2 * pad - ksize + 1 >= 1 && W + 2 * pad - ksize + 1 >= 1, SNN_ESHAPE, "snn_filter_bank: kernel larger than input");
+  REQUIRE(int64_t(H) * W < (int64_t(1) << 31), SNN_ESHAPE, "snn_filter_bank: H*W >= 2^31");
+  REQUIRE(snn::filter_bank_smem(K, ksize) <= 200 * 1024, SNN_ESHAPE, "snn_filter_bank: %d taps of %dx%d exceed shared memory", K, ksize, ksize);
+  if (B == 0) return SNN_OK;
+  REQUIRE(img && kernels && out, SNN_EINVAL, "snn_filter_bank: NULL tensor");
+  return snn::filter_bank_launch(img, B, H, W, kernels, K, ksize, pad, threshold, mode, out, S(s));
+}
+
+int snn_local_norm(const float* x, int B, int C, int H, int W, int radius, double eps, float* out, snn_stream_t s) {
+  REQUIRE(radius >= 0 && radius <= 32, SNN_EINVAL, "snn_local_norm: radius=%d outside [0, 32]", radius);
+  REQUIRE(eps > 0, SNN_EINVAL, "snn_local_norm: eps must be > 0");
+  REQUIRE(B >= 0 && C >= 0 && H >= 0 && W >= 0, SNN_ESHAPE, "snn_local_norm: negative dimension");
+  REQUIRE(int64_t(H) * W < (int64_t(1) << 31), SNN_ESHAPE, "snn_local_norm: H*W >= 2^31");
+  if (int64_t(B) * C * H * W == 0) return SNN_OK;
+  REQUIRE(x && out && x != out, SNN_EINVAL, "snn_local_norm: NULL or aliased tensor");
+  return snn::local_norm_launch(x, B, C, H, W, radius, eps, out, S(s));
+}
+
+int snn_lateral_inhibition(const float* x, int B, int C, int H, int W, const float* factors, int n, float* out,
+                           snn_stream_t s) {
+  REQUIRE(n >= 0 && n <= 32, SNN_EINVAL, "snn_lateral_inhibition: n=%d outside [0, 32]", n);
+  REQUIRE(B >= 0 && C >= 0 && H >= 0 && W >= 0, SNN_ESHAPE, "snn_lateral_inhibition: negative dimension");
+  REQUIRE(int64_t(H) * W < (int64_t(1) << 31), SNN_ESHAPE, "snn_lateral_inhibition: H*W >= 2^31");
+  if (int64_t(B) * C * H * W == 0) return SNN_OK;
+  REQUIRE(x && out && x != out && (factors || n == 0), SNN_EINVAL, "snn_lateral_inhibition: NULL or aliased tensor");
+  return snn::lateral_inhibition_launch(x, B, C, H, W, factors, n, out, S(s));
 }
 
 int snn_encode(const float* x, int B, int C, int H, int W, int T, uint8_t* lat, void* ws, size_t ws_bytes,

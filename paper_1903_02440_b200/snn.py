@@ -59,6 +59,9 @@ def lib() -> C.CDLL:
                 "snn_decide": (i32, [p, p, i32, i32, i32, i32, p, p, p, p]),
                 "snn_count_events": (i32, [p, i32, i32, i32, i32, i32, i32, i32, i32, i32, p, p, p]),
                 "snn_launch_count": (C.c_ulonglong, []),
+                "snn_filter_bank": (i32, [p, i32, i32, i32, p, i32, i32, i32, C.c_double, i32, p, p]),
+                "snn_local_norm": (i32, [p, i32, i32, i32, i32, i32, C.c_double, p, p]),
+                "snn_lateral_inhibition": (i32, [p, i32, i32, i32, i32, p, i32, p, p]),
                 "snn_conv_fire_plan": (i32, [i32] * 9 + [f32, p, p, p]),
                 "snn_stdp_sequence_workspace": (sz, [i32] * 10),
                 "snn_stdp_sequence": (i32, [p, i32, i32, i32, i32, i32, p, i32, i32, i32, i32, f32, i32, i32,
@@ -77,7 +80,7 @@ def exported_symbols():
             "snn_expand", "snn_validate_lat", "snn_conv_fire_workspace", "snn_conv_fire", "snn_pool",
             "snn_inhibit", "snn_k_winners_workspace", "snn_k_winners", "snn_stdp_update", "snn_decide",
             "snn_count_events", "snn_launch_count", "snn_conv_fire_plan", "snn_stdp_sequence_workspace",
-            "snn_stdp_sequence"]
+            "snn_stdp_sequence", "snn_filter_bank", "snn_local_norm", "snn_lateral_inhibition"]
 
 
 def _check(rc: int):
@@ -137,6 +140,45 @@ def encode(x: torch.Tensor, T: int, out: Optional[torch.Tensor] = None, ws: Opti
     buf = ws if ws is not None else _ws.get(n, x.device, "encode")
     _check(lib().snn_encode(_ptr(x), B, C_, H, W, T, _ptr(lat), _ptr(buf), buf.numel(), _stream(stream)))
     return lat
+
+
+def filter_bank(img: torch.Tensor, kernels: torch.Tensor, pad: int, mode: int = 0, threshold: float = float("-inf"),
+                out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """img float64 [B, H, W], kernels float64 [K, S, S] -> float32 [B, Kout, Ho, Wo] (snn_filter_bank, R33)."""
+    _req(img, torch.float64, "img")
+    _req(kernels, torch.float64, "kernels")
+    B, H, W = img.shape
+    K, S, S2 = kernels.shape
+    if S != S2:
+        raise ValueError("kernels must be square")
+    Ho, Wo = H + 2 * pad - S + 1, W + 2 * pad - S + 1
+    shape = (B, 2 * K if mode == 1 else K, Ho, Wo)
+    o = out if out is not None else torch.empty(shape, dtype=torch.float32, device=img.device)
+    _req(o, torch.float32, "out")
+    _check(lib().snn_filter_bank(_ptr(img), B, H, W, _ptr(kernels), K, S, pad, float(threshold), mode, _ptr(o),
+                                 _stream(stream)))
+    return o
+
+
+def local_norm(x: torch.Tensor, radius: int, eps: float = 1e-12, out: Optional[torch.Tensor] = None,
+               stream=None) -> torch.Tensor:
+    """x float32 [B, C, H, W] -> x / max(regional mean, eps) (snn_local_norm, R34)."""
+    _req(x, torch.float32, "x")
+    o = out if out is not None else torch.empty_like(x)
+    _req(o, torch.float32, "out")
+    _check(lib().snn_local_norm(_ptr(x), *x.shape, radius, float(eps), _ptr(o), _stream(stream)))
+    return o
+
+
+def lateral_inhibition(x: torch.Tensor, factors: torch.Tensor, out: Optional[torch.Tensor] = None,
+                       stream=None) -> torch.Tensor:
+    """x float32 [B, C, H, W], factors float32 [n] (device) -> inhibited intensities (snn_lateral_inhibition, R35)."""
+    _req(x, torch.float32, "x")
+    _req(factors, torch.float32, "factors")
+    o = out if out is not None else torch.empty_like(x)
+    _req(o, torch.float32, "out")
+    _check(lib().snn_lateral_inhibition(_ptr(x), *x.shape, _ptr(factors), factors.numel(), _ptr(o), _stream(stream)))
+    return o
 
 
 def expand(lat: torch.Tensor, T: int, stream=None) -> torch.Tensor:

@@ -220,12 +220,13 @@ def _c2_weights():
 
 def C2(n: int = 1000) -> Workload:
     X = _dog_input(1002, n)
+    raw = stroke_images(1002, n)                            # the images X was filtered from (f2 front end)
     return Workload("c2", 15, X,
                     [ConvSpec(30, 6, 5, 5, 2, 15.0), ConvSpec(250, 30, 3, 3, 1, 10.0),
                      ConvSpec(200, 250, 5, 5, 2, math.inf)],
                     _c2_weights(),
                     [PoolSpec(2, 2, 2, 2), PoolSpec(3, 3, 3, 3), None],
-                    dict(k=1, r=0, n_classes=10))
+                    dict(k=1, r=0, n_classes=10, raw=raw, bank=dog_bank(), front=dict(pad=3, mode=1)))
 
 
 def C3(n: int = 2000) -> Workload:
