@@ -152,7 +152,7 @@ def filter_bank(img: torch.Tensor, kernels: torch.Tensor, pad: int, mode: int = 
     if S != S2:
         raise ValueError("kernels must be square")
     Ho, Wo = H + 2 * pad - S + 1, W + 2 * pad - S + 1
-    shape = (B, 2 * K if mode == 1 else K, Ho, Wo)
+    shape = (B, 2 * K if mode == 1 else K, max(Ho, 0), max(Wo, 0))  # the C call rejects a bad shape
     o = out if out is not None else torch.empty(shape, dtype=torch.float32, device=img.device)
     _req(o, torch.float32, "out")
     _check(lib().snn_filter_bank(_ptr(img), B, H, W, _ptr(kernels), K, S, pad, float(threshold), mode, _ptr(o),
