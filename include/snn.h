@@ -89,6 +89,17 @@ SNN_API size_t snn_encode_workspace(int B, int C, int H, int W, int T);
 SNN_API int snn_encode(const float* x, int B, int C, int H, int W, int T, uint8_t* lat,
                void* ws, size_t ws_bytes, snn_stream_t s);
 
+/* f3 variant of a1 (the paper's "pre-defined number of spike bins", leaves the bin
+ * sizes open).  bins: SNN_BINS_R1 = snn_encode; SNN_BINS_PROPORTIONAL = the entry of rank r gets
+ * floor(r T / N); SNN_BINS_FLOOR = every bin holds q = N / T entries and ranks >= T q never spike
+ * (N < T: nothing spikes).  Same workspace, arguments and errors as snn_encode (bins unknown:
+ * SNN_EINVAL). */
+#define SNN_BINS_R1 0
+#define SNN_BINS_PROPORTIONAL 1
+#define SNN_BINS_FLOOR 2
+SNN_API int snn_encode_ex(const float* x, int B, int C, int H, int W, int T, int bins, uint8_t* lat,
+                          void* ws, size_t ws_bytes, snn_stream_t s);
+
 /* Eq. 1: wave[b, t, i] = 1.0f if lat[b, i] != NO_SPIKE and t >= lat[b, i], else 0.
  * lat uint8 [B, n], wave float32 [B, T, n].  Validation / tests only (the hot path never
  * materialises waves). */
@@ -138,6 +149,18 @@ SNN_API int snn_pool(const uint8_t* lat, const float* v, int B, int F, int H, in
              int PH, int PW, int SH, int SW, int DH, int DW,
              uint8_t* lat_out, float* v_out, snn_stream_t s);
 
+/* f3 variants of a4.  flags (bitwise or):
+ *   SNN_POOL_EQ3    output size per Eq. 3 literally: Ho = (H + 2 DH) / SH,
+ *                   Wo = (W + 2 DW) / SW; windows reaching past the padded input are truncated.
+ *                   Requires H + 2 DH >= SH and W + 2 DW >= SW instead of the window rule.
+ *   SNN_POOL_VFINAL v_out = max of v over EVERY spiking entry of the window (the pooled potentials
+ *                   tensor at t = T - 1, for v = final potentials: the A13 tie-break variant).
+ * flags = 0 is snn_pool.  Unknown bits: SNN_EINVAL. */
+#define SNN_POOL_EQ3 1
+#define SNN_POOL_VFINAL 2
+SNN_API int snn_pool_ex(const uint8_t* lat, const float* v, int B, int F, int H, int W, int PH, int PW, int SH,
+                        int SW, int DH, int DW, int flags, uint8_t* lat_out, float* v_out, snn_stream_t s);
+
 /* ---------------------------------------------------------------------------------------------
  * a5. Pointwise (cross-feature) inhibition (R13, R14).  At each (b, y, x) the spiking
  * feature with the smallest key (lat ascending, v descending, f ascending) keeps its (lat, v);
@@ -167,7 +190,8 @@ SNN_API int snn_k_winners(const uint8_t* lat, const float* v, int B, int F, int 
  *   pre  = lat_in[c, y+ky-pad, x+kx-pad] (NO_SPIKE outside the input), post = lat_out[f, y, x];
  *   a    = A+ if pre != NO_SPIKE and pre <= post, else A-;
  *   dW   = (a * (W - lb)) * (ub - W) if stabilizer else a;   W = clamp(W + dW, lb, ub)
- * evaluated in fp32 round-to-nearest without FMA contraction.  Winners have distinct features
+ * stabilizer: 0 off, 1 on, 2 on WITHOUT the clamp (f3 variant A20, "clamp only when the stabilizer
+ * is off"); other values SNN_EINVAL.  Evaluated in fp32 round-to-nearest without FMA contraction.  Winners have distinct features
  * (snn_k_winners guarantees it), so synapse updates never collide.
  * reward (device float scalar, may be NULL = +1): +1 applies (A+, A-), -1 applies (-A+, -A-)
  * (anti-STDP), 0 skips the update (silent sample).

@@ -48,6 +48,8 @@ def lib():
             p = C.c_void_p
             i64, i32, f32 = C.c_int64, C.c_int, C.c_float
             sig = {
+                "orc_pool_ex": (None, [p, p, i64, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, p, p]),
+                "orc_encode_bins": (None, [p, i64, i64, i32, i32, p]),
                 "orc_filter_bank": (None, [p, i64, i32, i32, p, i32, i32, i32, C.c_double, i32, p]),
                 "orc_local_norm": (None, [p, i64, i32, i32, i32, i32, C.c_double, p]),
                 "orc_lateral_inhibition": (None, [p, i64, i32, i32, i32, p, i32, p]),
@@ -88,13 +90,13 @@ def set_threads(n: int) -> None:
 
 
 # ----------------------------------------------------------------------------- a1
-def encode(x: np.ndarray, T: int) -> np.ndarray:
-    """x fp32 [B, C, H, W] (or [B, n]) -> lat uint8 same shape."""
+def encode(x: np.ndarray, T: int, bins: int = 0) -> np.ndarray:
+    """x fp32 [B, C, H, W] (or [B, n]) -> lat uint8 same shape; bins = bin-size rule (orc_encode_bins)."""
     x = _c(x, np.float32)
     B = x.shape[0]
     n = int(np.prod(x.shape[1:])) if x.ndim > 1 else 0
     lat = np.empty(x.shape, dtype=np.uint8)
-    lib().orc_encode(_ptr(x), B, n, T, _ptr(lat))
+    lib().orc_encode_bins(_ptr(x), B, n, T, int(bins), _ptr(lat))
     return lat
 
 
@@ -182,19 +184,22 @@ def events(lat_in: np.ndarray, F: int, KH: int, KW: int, pad: int) -> int:
 
 
 # ----------------------------------------------------------------------------- a4
-def pool_out_hw(H, W, PH, PW, SH, SW, DH=0, DW=0):
-    """Reading R10: windows fully inside the padded input."""
+def pool_out_hw(H, W, PH, PW, SH, SW, DH=0, DW=0, eq3=False):
+    """Reading R10: windows fully inside the padded input; eq3: Eq. 3 literally (f3 variant)."""
+    if eq3:
+        return (H + 2 * DH) // SH, (W + 2 * DW) // SW
     return (H + 2 * DH - PH) // SH + 1, (W + 2 * DW - PW) // SW + 1
 
 
-def pool(lat: np.ndarray, v, PH, PW, SH, SW, DH=0, DW=0, T=254):
+def pool(lat: np.ndarray, v, PH, PW, SH, SW, DH=0, DW=0, T=254, eq3=False, vfinal=False):
     lat = _c(lat, np.uint8)
     B, F, H, W = lat.shape
     v = None if v is None else _c(v, np.float32)
-    Ho, Wo = pool_out_hw(H, W, PH, PW, SH, SW, DH, DW)
+    Ho, Wo = pool_out_hw(H, W, PH, PW, SH, SW, DH, DW, eq3)
     lo = np.empty((B, F, Ho, Wo), dtype=np.uint8)
     vo = np.empty((B, F, Ho, Wo), dtype=np.float32) if v is not None else None
-    lib().orc_pool(_ptr(lat), _ptr(v), B, F, H, W, PH, PW, SH, SW, DH, DW, T, _ptr(lo), _ptr(vo))
+    lib().orc_pool_ex(_ptr(lat), _ptr(v), B, F, H, W, PH, PW, SH, SW, DH, DW, T, int(eq3), int(vfinal),
+                      _ptr(lo), _ptr(vo))
     return lo, vo
 
 

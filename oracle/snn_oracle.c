@@ -37,7 +37,12 @@ static int orc_item_cmp(const void* a, const void* b) {
     return (p->idx < q->idx) ? -1 : (p->idx > q->idx); /* then flat index ascending */
 }
 
-void orc_encode(const float* x, int64_t B, int64_t n, int T, uint8_t* lat) {
+/* bins selects the bin-size rule ("pre-defined number of spike bins"; the paper does not fix
+ * the sizes -- DESIGN.md R1 and the f3 variants):
+ *   0 (R1, default): q = N / T, m = N % T; the first m bins hold q + 1 ranks, the rest q;
+ *   1 (proportional): the entry of rank r gets bin floor(r * T / N);
+ *   2 (floor): every bin holds q = N / T ranks; ranks >= T q never spike.                       */
+void orc_encode_bins(const float* x, int64_t B, int64_t n, int T, int bins, uint8_t* lat) {
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t b = 0; b < B; ++b) {
         const float* xb = x + b * n;
@@ -49,15 +54,20 @@ void orc_encode(const float* x, int64_t B, int64_t n, int T, uint8_t* lat) {
             if (xb[i] > 0.0f) { items[N].v = xb[i]; items[N].idx = i; ++N; }
         }
         qsort(items, (size_t)N, sizeof(orc_item), orc_item_cmp);
-        /* bin sizes: q+1 for the first m bins, q for the rest (R1) */
         int64_t q = N / T, m = N % T, rank = 0;
-        for (int t = 0; t < T; ++t) {
-            int64_t size = q + (t < m ? 1 : 0);
-            for (int64_t j = 0; j < size; ++j, ++rank) lb[items[rank].idx] = (uint8_t)t;
+        if (bins == 1) {
+            for (rank = 0; rank < N; ++rank) lb[items[rank].idx] = (uint8_t)((rank * T) / N);
+        } else {
+            for (int t = 0; t < T; ++t) {
+                int64_t size = q + ((bins == 0 && t < m) ? 1 : 0);
+                for (int64_t j = 0; j < size; ++j, ++rank) lb[items[rank].idx] = (uint8_t)t;
+            }
         }
         free(items);
     }
 }
+
+void orc_encode(const float* x, int64_t B, int64_t n, int T, uint8_t* lat) { orc_encode_bins(x, B, n, T, 0, lat); }
 
 /* Eq. 1: S[t,i] = 0 if t < T_i else 1; NO_SPIKE rows all zero. */
 void orc_expand(const uint8_t* lat, int64_t B, int64_t n, int T, float* wave /* [B][T][n] */) {
@@ -234,10 +244,16 @@ int64_t orc_events(const uint8_t* lat_in, int64_t B, int C, int H, int W, int pa
  * that spiked by t (none spiked earlier, since t is the first).  Padding = no
  * spike (R11).  Output size per R10.                                        */
 /* ------------------------------------------------------------------------- */
-void orc_pool(const uint8_t* lat, const float* v, int64_t B, int F, int H, int W,
-              int PH, int PW, int SH, int SW, int DH, int DW, int T,
-              uint8_t* lat_out, float* v_out) {
-    int Ho = (H + 2 * DH - PH) / SH + 1, Wo = (W + 2 * DW - PW) / SW + 1;
+/* f3 variants: eq3 = 1 takes Eq. 3's output size literally,
+ * Ho = floor((H + 2 DH) / SH), the last windows truncated at the
+ * edge of the padded input (outside it nothing spikes, like the padding);
+ * vfinal = 1 reads the pooled thresholded potentials at t = T-1 instead of at
+ * the pooled spike time: the max of v over every window entry that spiked.     */
+void orc_pool_ex(const uint8_t* lat, const float* v, int64_t B, int F, int H, int W,
+                 int PH, int PW, int SH, int SW, int DH, int DW, int T, int eq3, int vfinal,
+                 uint8_t* lat_out, float* v_out) {
+    int Ho = eq3 ? (H + 2 * DH) / SH : (H + 2 * DH - PH) / SH + 1;
+    int Wo = eq3 ? (W + 2 * DW) / SW : (W + 2 * DW - PW) / SW + 1;
 #pragma omp parallel for schedule(static)
     for (int64_t bf = 0; bf < B * F; ++bf) {
         const uint8_t* l = lat + bf * H * W;
@@ -255,11 +271,12 @@ void orc_pool(const uint8_t* lat, const float* v, int64_t B, int F, int H, int W
                         }
                     if (s) {
                         lo = (uint8_t)t;
+                        const int tr = vfinal ? T - 1 : t; /* time at which the pooled potential is read */
                         for (int py = 0; py < PH; ++py)
                             for (int px = 0; px < PW; ++px) {
                                 int yy = oy * SH + py - DH, xx = ox * SW + px - DW;
                                 uint8_t li = orc_lat_at(l, H, W, yy, xx);
-                                if (li != ORC_NO_SPIKE && t >= li && vv) {
+                                if (li != ORC_NO_SPIKE && tr >= li && vv) {
                                     float c = vv[(int64_t)yy * W + xx];
                                     if (c > vo) vo = c;
                                 }
@@ -270,6 +287,12 @@ void orc_pool(const uint8_t* lat, const float* v, int64_t B, int F, int H, int W
                 if (v_out) v_out[(bf * Ho + oy) * Wo + ox] = vo;
             }
     }
+}
+
+void orc_pool(const uint8_t* lat, const float* v, int64_t B, int F, int H, int W,
+              int PH, int PW, int SH, int SW, int DH, int DW, int T,
+              uint8_t* lat_out, float* v_out) {
+    orc_pool_ex(lat, v, B, F, H, W, PH, PW, SH, SW, DH, DW, T, 0, 0, lat_out, v_out);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -345,7 +368,8 @@ void orc_k_winners_batch(const uint8_t* lat, const float* v, int64_t B, int F, i
 /* a7: STDP, Eq. 4.  For winner i (post) and each synapse j of its
  * receptive field: dW = A+ (W-LB)(UB-W) if T_j <= T_i else A- (W-LB)(UB-W);
  * NO_SPIKE / padded pre counts as T_j > T_i (R17); stabilizer off => dW = A;
- * then clamp to [LB, UB] (R20).  fp32, Eq. 4 left-to-right, no FMA (R19).
+ * then clamp to [LB, UB] (R20) -- except stabilizer == 2 (stabilizer on, no clamp:
+ * the A20 variant "clamp only when the stabilizer is off").  fp32, Eq. 4 left-to-right, no FMA (R19).
  * R-STDP: reward = +1 applies (A+, A-), -1 applies the negated
  * rates (anti-STDP), 0 = no update (silent, R25).                            */
 /* ------------------------------------------------------------------------- */
@@ -376,8 +400,10 @@ void orc_stdp(float* w, int F, int C, int KH, int KW,
                         dw = a;
                     }
                     float w1 = W0 + dw;
-                    if (w1 < lb) w1 = lb;
-                    if (w1 > ub) w1 = ub;
+                    if (stabilizer != 2) { /* 2: stabilizer on, no clamp (A20 variant) */
+                        if (w1 < lb) w1 = lb;
+                        if (w1 > ub) w1 = ub;
+                    }
                     *wp = w1;
                 }
     }

@@ -13,7 +13,7 @@
 namespace snn {
 
 size_t encode_workspace(int B, int C, int H, int W, int T);
-int encode_launch(const float* x, int B, int C, int H, int W, int T, uint8_t* lat, void* ws, size_t ws_bytes,
+int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, uint8_t* lat, void* ws, size_t ws_bytes,
                   cudaStream_t s);
 int expand_launch(const uint8_t* lat, int B, int n, int T, float* wave, cudaStream_t s);
 int validate_launch(const uint8_t* lat, size_t n, int T, int32_t* n_bad, cudaStream_t s);
@@ -24,7 +24,7 @@ int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
                      int KW, int T, float theta, uint8_t* lat_out, float* v_out, float* pot_out, void* ws,
                      size_t ws_bytes, cudaStream_t s);
 int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, int PH, int PW, int SH, int SW,
-                int DH, int DW, uint8_t* lat_out, float* v_out, cudaStream_t s);
+                int DH, int DW, int flags, uint8_t* lat_out, float* v_out, cudaStream_t s);
 int inhibit_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, uint8_t* lat_out, float* v_out,
                    int16_t* winner_f, cudaStream_t s);
 size_t k_winners_workspace(int B, int F, int H, int W);
@@ -169,15 +169,21 @@ int snn_lateral_inhibition(const float* x, int B, int C, int H, int W, const flo
   return snn::lateral_inhibition_launch(x, B, C, H, W, factors, n, out, S(s));
 }
 
-int snn_encode(const float* x, int B, int C, int H, int W, int T, uint8_t* lat, void* ws, size_t ws_bytes,
-               snn_stream_t s) {
+int snn_encode_ex(const float* x, int B, int C, int H, int W, int T, int bins, uint8_t* lat, void* ws,
+                  size_t ws_bytes, snn_stream_t s) {
   REQUIRE(T >= 1 && T <= 254, SNN_EINVAL, "snn_encode: T=%d outside [1, 254]", T);
+  REQUIRE(bins >= SNN_BINS_R1 && bins <= SNN_BINS_FLOOR, SNN_EINVAL, "snn_encode: bins=%d unknown", bins);
   REQUIRE(B >= 0 && C >= 0 && H >= 0 && W >= 0, SNN_ESHAPE, "snn_encode: negative dimension");
   REQUIRE(int64_t(C) * H * W < (int64_t(1) << 24), SNN_ESHAPE, "snn_encode: C*H*W >= 2^24");
   if (int64_t(B) * C * H * W == 0) return SNN_OK;
   REQUIRE(x && lat, SNN_EINVAL, "snn_encode: NULL tensor");
   REQUIRE(ws, SNN_EWORKSPACE, "snn_encode: NULL workspace");
-  return encode_launch(x, B, C, H, W, T, lat, ws, ws_bytes, S(s));
+  return encode_launch(x, B, C, H, W, T, bins, lat, ws, ws_bytes, S(s));
+}
+
+int snn_encode(const float* x, int B, int C, int H, int W, int T, uint8_t* lat, void* ws, size_t ws_bytes,
+               snn_stream_t s) {
+  return snn_encode_ex(x, B, C, H, W, T, SNN_BINS_R1, lat, ws, ws_bytes, s);
 }
 
 int snn_expand(const uint8_t* lat, int B, int n, int T, float* wave, snn_stream_t s) {
@@ -209,6 +215,7 @@ int snn_stdp_sequence(const uint8_t* lat_in, int N, int C, int H, int W, int pad
                       int T, float theta, int k, int r, float a_plus, float a_minus, float lb, float ub,
                       int stabilizer, int32_t* winners, int32_t* count, float* snapshots, int snap_every, void* ws,
                       size_t ws_bytes, snn_stream_t s) {
+  REQUIRE(stabilizer >= 0 && stabilizer <= 2, SNN_EINVAL, "snn_stdp_sequence: stabilizer=%d not in {0, 1, 2}", stabilizer);
   int rc = conv_checks(N, C, H, W, pad, F, KH, KW, T, theta);
   if (rc) return rc;
   REQUIRE(k >= 1 && k <= 256, SNN_EINVAL, "snn_stdp_sequence: k=%d outside [1, 256]", k);
@@ -245,16 +252,23 @@ int snn_conv_fire(const uint8_t* lat_in, int B, int C, int H, int W, int pad, co
                           S(s));
 }
 
-int snn_pool(const uint8_t* lat, const float* v, int B, int F, int H, int W, int PH, int PW, int SH, int SW, int DH,
-             int DW, uint8_t* lat_out, float* v_out, snn_stream_t s) {
+int snn_pool_ex(const uint8_t* lat, const float* v, int B, int F, int H, int W, int PH, int PW, int SH, int SW,
+                int DH, int DW, int flags, uint8_t* lat_out, float* v_out, snn_stream_t s) {
   REQUIRE(B >= 0 && F >= 0 && H >= 1 && W >= 1, SNN_ESHAPE, "snn_pool: bad dimensions");
   REQUIRE(PH >= 1 && PW >= 1 && SH >= 1 && SW >= 1 && DH >= 0 && DW >= 0, SNN_EINVAL, "snn_pool: bad window");
-  REQUIRE(PH <= H + 2 * DH && PW <= W + 2 * DW, SNN_ESHAPE, "snn_pool: window larger than padded input");
+  REQUIRE((flags & ~(SNN_POOL_EQ3 | SNN_POOL_VFINAL)) == 0, SNN_EINVAL, "snn_pool: unknown flags 0x%x", flags);
+  REQUIRE((flags & SNN_POOL_EQ3) ? (H + 2 * DH >= SH && W + 2 * DW >= SW) : (PH <= H + 2 * DH && PW <= W + 2 * DW),
+          SNN_ESHAPE, "snn_pool: window larger than padded input");
   REQUIRE(DH < PH && DW < PW, SNN_EINVAL, "snn_pool: padding must be smaller than the window");
   if (int64_t(B) * F == 0) return SNN_OK;
   REQUIRE(lat && lat_out, SNN_EINVAL, "snn_pool: NULL tensor");
   REQUIRE(!v_out || v, SNN_EINVAL, "snn_pool: v_out without v");
-  return pool_launch(lat, v, B, F, H, W, PH, PW, SH, SW, DH, DW, lat_out, v_out, S(s));
+  return pool_launch(lat, v, B, F, H, W, PH, PW, SH, SW, DH, DW, flags, lat_out, v_out, S(s));
+}
+
+int snn_pool(const uint8_t* lat, const float* v, int B, int F, int H, int W, int PH, int PW, int SH, int SW, int DH,
+             int DW, uint8_t* lat_out, float* v_out, snn_stream_t s) {
+  return snn_pool_ex(lat, v, B, F, H, W, PH, PW, SH, SW, DH, DW, 0, lat_out, v_out, s);
 }
 
 int snn_inhibit(const uint8_t* lat, const float* v, int B, int F, int H, int W, uint8_t* lat_out, float* v_out,
@@ -288,6 +302,7 @@ int snn_stdp_update(float* w, int F, int C, int KH, int KW, const uint8_t* lat_i
                     const uint8_t* lat_out, int Ho, int Wo, const int32_t* winners, const int32_t* count, int k,
                     float a_plus, float a_minus, float lb, float ub, int stabilizer, const float* reward,
                     snn_stream_t s) {
+  REQUIRE(stabilizer >= 0 && stabilizer <= 2, SNN_EINVAL, "snn_stdp_update: stabilizer=%d not in {0, 1, 2}", stabilizer);
   REQUIRE(lb < ub, SNN_EINVAL, "snn_stdp_update: LB >= UB");
   REQUIRE(k >= 0 && F >= 1 && C >= 1 && KH >= 1 && KW >= 1 && H >= 1 && W >= 1 && pad >= 0, SNN_ESHAPE,
           "snn_stdp_update: bad dimensions");

@@ -25,11 +25,11 @@ constexpr int kEncChunk = kEncThreads * kEncPerThread;
 
 struct EncodeWS {
   uint32_t* hist0;      // [G][4096]
-  uint32_t* hist;       // [G][S][4096]   S = max(1, T-1)
-  uint64_t* cut_prefix; // [G][T-1]
-  int32_t* cut_shift;   // [G][T-1]  -1 = empty cut (never passed); >=0 when resolved
-  uint32_t* cut_resid;  // [G][T-1]
-  int32_t* cut_slot;    // [G][T-1]  slot of an unresolved cut, -1 when resolved / empty
+  uint32_t* hist;       // [G][S][4096]   S = T (>= the number of cuts)
+  uint64_t* cut_prefix; // [G][S]
+  int32_t* cut_shift;   // [G][S]  -1 = empty cut (never passed); >=0 when resolved
+  uint32_t* cut_resid;  // [G][S]
+  int32_t* cut_slot;    // [G][S]  slot of an unresolved cut, -1 when resolved / empty
   uint64_t* slot_prefix;// [G][S]
   int32_t* n_slots;     // [G]
 };
@@ -37,7 +37,7 @@ struct EncodeWS {
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static size_t encode_ws_layout(int G, int T, EncodeWS* ws, char* base) {
-  int S = T > 1 ? T - 1 : 1, NC = S;
+  int S = T, NC = S;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return base ? base + o : nullptr; };
   EncodeWS w;
@@ -69,6 +69,17 @@ size_t encode_workspace(int B, int C, int H, int W, int T) {
 
 __device__ __forceinline__ uint64_t enc_key(float x, uint32_t idx) {
   return (uint64_t(0x7FFFFFFFu - __float_as_uint(x)) << 24) | idx;
+}
+
+// Number of cuts and the rank at which bin b (b = 1..ncuts) starts, per bin-size rule (snn_encode_ex):
+// 0 (R1) q + 1 ranks for the first N % T bins, q for the rest; 1 proportional, bin = floor(r T / N);
+// 2 floor, q ranks per bin and a T-th cut at T q past which nothing spikes (lat = T -> no spike).
+__host__ __device__ __forceinline__ int enc_ncuts(int T, int bins) { return T - 1 + (bins == 2 ? 1 : 0); }
+__device__ __forceinline__ uint32_t enc_cut_start(uint32_t b, uint32_t N, uint32_t T, int bins) {
+  const uint32_t q = N / T, m = N % T;
+  if (bins == 1) return uint32_t((uint64_t(b) * N + T - 1) / T);
+  if (bins == 2) return b * q;
+  return b * q + (b < m ? b : m);
 }
 
 // Level 0: histogram of the top 12 bits of every positive key (all images of the group).
@@ -107,7 +118,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_hist0_kernel(const float* __r
 __global__ void __launch_bounds__(kEncThreads) enc_hist_kernel(const float* __restrict__ x, int64_t n, int T,
                                                                 int level, EncodeWS ws) {
   const int g = blockIdx.y;
-  const int S = T > 1 ? T - 1 : 1;
+  const int S = T;
   const int ns = ws.n_slots[g];
   if (ns == 0) return;
   __shared__ uint64_t sp[256];
@@ -136,10 +147,10 @@ __global__ void __launch_bounds__(kEncThreads) enc_hist_kernel(const float* __re
 
 // Per-image selection after level L: locate every unresolved cut's digit, resolve or descend,
 // rebuild the sorted list of distinct prefixes for level L+1 and zero their histograms.
-__global__ void __launch_bounds__(256) enc_select_kernel(int T, int level, EncodeWS ws) {
+__global__ void __launch_bounds__(256) enc_select_kernel(int T, int bins, int level, EncodeWS ws) {
   const int g = blockIdx.x;
-  const int S = T > 1 ? T - 1 : 1;
-  const int NC = T - 1;
+  const int S = T;
+  const int NC = enc_ncuts(T, bins);
   __shared__ uint32_t cum[kEncBins + 1];
   __shared__ uint32_t wsum[8];
   __shared__ int s_nslots;
@@ -173,12 +184,10 @@ __global__ void __launch_bounds__(256) enc_select_kernel(int T, int level, Encod
     if (tid == 255) cum[kEncBins] = e;
     __syncthreads();
     if (level == 0) {
-      // initialise the cuts from N = total positives (bins: q + 1 for the first m, then q)
+      // initialise the cuts from N = total positives
       uint32_t N = cum[kEncBins];
-      uint32_t q = N / uint32_t(T), m = N % uint32_t(T);
       for (int b = tid; b < NC; b += blockDim.x) {
-        uint32_t bb = uint32_t(b + 1);
-        uint32_t start = bb * q + (bb < m ? bb : m);
+        uint32_t start = enc_cut_start(uint32_t(b + 1), N, uint32_t(T), bins);
         cp[b] = 0;
         if (start >= N) { csh[b] = -1; cs[b] = -1; cr[b] = 0; }
         else { csh[b] = -2; cs[b] = 0; cr[b] = start; }
@@ -222,10 +231,10 @@ __global__ void __launch_bounds__(256) enc_select_kernel(int T, int level, Encod
 }
 
 __global__ void __launch_bounds__(kEncThreads) enc_assign_kernel(const float* __restrict__ x, int64_t n, int T,
-                                                                  uint8_t* __restrict__ lat, EncodeWS ws) {
+                                                                  int bins, uint8_t* __restrict__ lat, EncodeWS ws) {
   const int g = blockIdx.y;
-  const int S = T > 1 ? T - 1 : 1;
-  const int NC = T - 1;
+  const int S = T;
+  const int NC = enc_ncuts(T, bins);
   __shared__ uint64_t sp[256];
   __shared__ int ssh[256];
   for (int b = threadIdx.x; b < NC; b += blockDim.x) {
@@ -249,7 +258,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_assign_kernel(const float* __
         bool pass = ssh[mid] >= 0 && (K >> ssh[mid]) >= sp[mid];
         if (pass) lo = mid + 1; else hi = mid;
       }
-      out = uint8_t(lo);
+      out = lo >= T ? kNoSpike : uint8_t(lo);
     }
     lg[i] = out;
   }
@@ -266,7 +275,7 @@ constexpr int kSmThreads = 512;
 
 __device__ __forceinline__ uint64_t sm_key(uint32_t vk, int i) { return (uint64_t(vk) << 24) | uint32_t(i); }
 
-__global__ void __launch_bounds__(kSmThreads) enc_small_kernel(const float* __restrict__ x, int n, int T,
+__global__ void __launch_bounds__(kSmThreads) enc_small_kernel(const float* __restrict__ x, int n, int T, int bins,
                                                                 uint8_t* __restrict__ lat) {
   extern __shared__ uint32_t vk[];              // [n] 0x7FFFFFFF - bits(x), or ~0 for x <= 0
   __shared__ uint32_t hist[4096];               // level 0: 4096 bins; later: slot * 256 + digit
@@ -279,7 +288,7 @@ __global__ void __launch_bounds__(kSmThreads) enc_small_kernel(const float* __re
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const float* xb = x + int64_t(b) * n;
   uint8_t* lb = lat + int64_t(b) * n;
-  const int NC = T - 1;
+  const int NC = enc_ncuts(T, bins);
   for (int i = tid; i < 4096; i += kSmThreads) hist[i] = 0;
   __syncthreads();
   // ---- level 0: load keys, histogram of the top 12 bits ----
@@ -323,9 +332,8 @@ __global__ void __launch_bounds__(kSmThreads) enc_small_kernel(const float* __re
   }
   __syncthreads();
   const uint32_t N = uint32_t(s_N);
-  const uint32_t q = N / uint32_t(T), m = N % uint32_t(T);
   for (int c = tid; c < NC; c += kSmThreads) {
-    const uint32_t bb = uint32_t(c + 1), start = bb * q + (bb < m ? bb : m);
+    const uint32_t start = enc_cut_start(uint32_t(c + 1), N, uint32_t(T), bins);
     if (start >= N) { cut_shift[c] = -1; cut_slot[c] = -1; continue; }
     int lo = 0, hi = 4095;  // largest d with cum[d] <= start
     while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (hist[mid] <= start) lo = mid; else hi = mid - 1; }
@@ -413,11 +421,11 @@ __global__ void __launch_bounds__(kSmThreads) enc_small_kernel(const float* __re
       const bool pass = cut_shift[mid] >= 0 && (K >> cut_shift[mid]) >= cut_prefix[mid];
       if (pass) lo = mid + 1; else hi = mid;
     }
-    lb[i] = uint8_t(lo);
+    lb[i] = lo >= T ? kNoSpike : uint8_t(lo);
   }
 }
 
-int encode_launch(const float* x, int B, int C, int H, int W, int T, uint8_t* lat, void* wsp,
+int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, uint8_t* lat, void* wsp,
                   size_t ws_bytes, cudaStream_t s) {
   int64_t n = int64_t(C) * H * W;
   if (B == 0 || n == 0) return SNN_OK;
@@ -425,7 +433,7 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, uint8_t* la
     const size_t smem = size_t(n) * sizeof(uint32_t);
     cudaError_t e = cudaFuncSetAttribute(enc_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_encode: %s", cudaGetErrorString(e));
-    enc_small_kernel<<<B, kSmThreads, smem, s>>>(x, int(n), T, lat);
+    enc_small_kernel<<<B, kSmThreads, smem, s>>>(x, int(n), T, bins, lat);
     note_launch();
     return check_launch("snn_encode(small)");
   }
@@ -442,17 +450,17 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, uint8_t* la
     dim3 grid(nchunks, gn);
     enc_hist0_kernel<<<grid, kEncThreads, 0, s>>>(xg, n, ws);
     note_launch();
-    if (T > 1) {
-      enc_select_kernel<<<gn, 256, 0, s>>>(T, 0, ws);
+    if (enc_ncuts(T, bins) > 0) {
+      enc_select_kernel<<<gn, 256, 0, s>>>(T, bins, 0, ws);
       note_launch();
       for (int L = 1; L < kEncLevels; ++L) {
         enc_hist_kernel<<<grid, kEncThreads, 0, s>>>(xg, n, T, L, ws);
         note_launch();
-        enc_select_kernel<<<gn, 256, 0, s>>>(T, L, ws);
+        enc_select_kernel<<<gn, 256, 0, s>>>(T, bins, L, ws);
         note_launch();
       }
     }
-    enc_assign_kernel<<<grid, kEncThreads, 0, s>>>(xg, n, T, lat + int64_t(g0) * n, ws);
+    enc_assign_kernel<<<grid, kEncThreads, 0, s>>>(xg, n, T, bins, lat + int64_t(g0) * n, ws);
     note_launch();
     int rc = check_launch("snn_encode");
     if (rc) return rc;

@@ -16,8 +16,8 @@ namespace snn {
 // (per-time-step max-pooling of the thresholded potentials read at the pooled spike, R12).
 __global__ void __launch_bounds__(256) pool_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
                                                    int64_t BF, int H, int W, int PH, int PW, int SH, int SW,
-                                                   int DH, int DW, int Ho, int Wo, uint8_t* __restrict__ lat_out,
-                                                   float* __restrict__ v_out) {
+                                                   int DH, int DW, int Ho, int Wo, int vfinal,
+                                                   uint8_t* __restrict__ lat_out, float* __restrict__ v_out) {
   const int64_t total = BF * Ho * Wo;
   for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < total; o += int64_t(gridDim.x) * blockDim.x) {
     const int ox = int(o % Wo);
@@ -36,9 +36,12 @@ __global__ void __launch_bounds__(256) pool_kernel(const uint8_t* __restrict__ l
         const int xx = x0 + px;
         if (xx < 0 || xx >= W) continue;
         const int li = l[int64_t(yy) * W + xx];
-        if (li == kNoSpike || li > best) continue;
+        if (li == kNoSpike || (li > best && !vfinal)) continue;
         const float vi = vv ? vv[int64_t(yy) * W + xx] : 0.0f;
-        if (li < best) { best = li; bv = vi; }
+        if (vfinal) {  // SNN_POOL_VFINAL: max over every spiking entry (the pooled potentials at T - 1)
+          if (best == kNoSpike || vi > bv) bv = vi;
+          if (li < best) best = li;
+        } else if (li < best) { best = li; bv = vi; }
         else if (vi > bv) bv = vi;
       }
     }
@@ -48,14 +51,17 @@ __global__ void __launch_bounds__(256) pool_kernel(const uint8_t* __restrict__ l
 }
 
 int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, int PH, int PW, int SH, int SW,
-                int DH, int DW, uint8_t* lat_out, float* v_out, cudaStream_t s) {
-  const int Ho = (H + 2 * DH - PH) / SH + 1, Wo = (W + 2 * DW - PW) / SW + 1;
+                int DH, int DW, int flags, uint8_t* lat_out, float* v_out, cudaStream_t s) {
+  // R10 (windows inside the padded input), or Eq. 3 literally (last window truncated at the edge)
+  const bool eq3 = flags & SNN_POOL_EQ3;
+  const int Ho = eq3 ? (H + 2 * DH) / SH : (H + 2 * DH - PH) / SH + 1;
+  const int Wo = eq3 ? (W + 2 * DW) / SW : (W + 2 * DW - PW) / SW + 1;
   const int64_t total = int64_t(B) * F * Ho * Wo;
   if (total == 0) return SNN_OK;
   int64_t blocks = ceil_div(total, 256);
   if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
   pool_kernel<<<int(blocks), 256, 0, s>>>(lat, v_out ? v : nullptr, int64_t(B) * F, H, W, PH, PW, SH, SW, DH, DW,
-                                          Ho, Wo, lat_out, v_out);
+                                          Ho, Wo, (flags & SNN_POOL_VFINAL) ? 1 : 0, lat_out, v_out);
   note_launch();
   return check_launch("snn_pool");
 }

@@ -294,8 +294,10 @@ __global__ void __launch_bounds__(FPL == 4 ? 768 : 1024, 1) seq_train_kernel(con
           const float w0 = __uint2float_rn(Wsh[e * FGS + fl]) * 4.656612873077392578125e-10f;  // exact
           const float dw = s.stabilizer ? __fmul_rn(__fmul_rn(am, __fsub_rn(w0, s.lb)), __fsub_rn(s.ub, w0)) : am;
           float w1 = __fadd_rn(w0, dw);
-          w1 = w1 < s.lb ? s.lb : w1;
-          w1 = w1 > s.ub ? s.ub : w1;
+          if (s.stabilizer != 2) {  // 2 = stabilized without the clamp (A20 variant)
+            w1 = w1 < s.lb ? s.lb : w1;
+            w1 = w1 > s.ub ? s.ub : w1;
+          }
           const float sx = w1 * 2147483648.0f;
           if (!(w1 >= 0.0f && w1 <= 1.0f) || sx != truncf(sx)) flag_error(a.err, kErrInexact);
           Wsh[e * FGS + fl] = uint32_t(sx);

@@ -4,7 +4,7 @@
 // The winners of k-WTA have distinct features, so their kernels are disjoint (no write races).
 // Arithmetic is fp32 round-to-nearest with explicit intrinsics so no FMA is contracted:
 //   dW = (a * (W - lb)) * (ub - W)   (stabilizer on, Eq. 4 left to right)  or  dW = a
-//   W  = min(max(W + dW, lb), ub)
+//   W  = min(max(W + dW, lb), ub)   (no clamp for stabilizer == 2, the A20 variant)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -38,8 +38,10 @@ __global__ void __launch_bounds__(256) stdp_kernel(float* __restrict__ w, int C,
     const float w0 = wf[e];
     const float dw = stabilizer ? __fmul_rn(__fmul_rn(a, __fsub_rn(w0, lb)), __fsub_rn(ub, w0)) : a;
     float w1 = __fadd_rn(w0, dw);
-    w1 = w1 < lb ? lb : w1;
-    w1 = w1 > ub ? ub : w1;
+    if (stabilizer != 2) {  // 2 = stabilized without the clamp (A20 variant, "clamp only when the stabilizer is off")
+      w1 = w1 < lb ? lb : w1;
+      w1 = w1 > ub ? ub : w1;
+    }
     wf[e] = w1;
   }
 }

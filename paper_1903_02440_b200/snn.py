@@ -51,6 +51,8 @@ def lib() -> C.CDLL:
                 "snn_conv_fire_workspace": (sz, [i32] * 9 + [f32]),
                 "snn_conv_fire": (i32, [p, i32, i32, i32, i32, i32, p, i32, i32, i32, i32, f32, p, p, p, p, sz, p]),
                 "snn_pool": (i32, [p, p, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, p, p, p]),
+                "snn_pool_ex": (i32, [p, p] + [i32] * 11 + [p, p, p]),
+                "snn_encode_ex": (i32, [p, i32, i32, i32, i32, i32, i32, p, p, sz, p]),
                 "snn_inhibit": (i32, [p, p, i32, i32, i32, i32, p, p, p, p]),
                 "snn_k_winners_workspace": (sz, [i32, i32, i32, i32]),
                 "snn_k_winners": (i32, [p, p, i32, i32, i32, i32, i32, i32, p, p, p, sz, p]),
@@ -80,7 +82,8 @@ def exported_symbols():
             "snn_expand", "snn_validate_lat", "snn_conv_fire_workspace", "snn_conv_fire", "snn_pool",
             "snn_inhibit", "snn_k_winners_workspace", "snn_k_winners", "snn_stdp_update", "snn_decide",
             "snn_count_events", "snn_launch_count", "snn_conv_fire_plan", "snn_stdp_sequence_workspace",
-            "snn_stdp_sequence", "snn_filter_bank", "snn_local_norm", "snn_lateral_inhibition"]
+            "snn_stdp_sequence", "snn_filter_bank", "snn_local_norm", "snn_lateral_inhibition",
+            "snn_encode_ex", "snn_pool_ex"]
 
 
 def _check(rc: int):
@@ -130,15 +133,19 @@ def encode_workspace(B, C_, H, W, T) -> int:
 
 
 def encode(x: torch.Tensor, T: int, out: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None,
-           stream=None) -> torch.Tensor:
-    """x float32 [B, C, H, W] -> lat uint8 [B, C, H, W] (snn_encode)."""
+           stream=None, bins: int = 0) -> torch.Tensor:
+    """x float32 [B, C, H, W] -> lat uint8 [B, C, H, W] (snn_encode; bins != 0: snn_encode_ex variant)."""
     _req(x, torch.float32, "x")
     B, C_, H, W = x.shape
     lat = out if out is not None else torch.empty(x.shape, dtype=torch.uint8, device=x.device)
     _req(lat, torch.uint8, "lat")
     n = encode_workspace(B, C_, H, W, T)
     buf = ws if ws is not None else _ws.get(n, x.device, "encode")
-    _check(lib().snn_encode(_ptr(x), B, C_, H, W, T, _ptr(lat), _ptr(buf), buf.numel(), _stream(stream)))
+    if bins:
+        _check(lib().snn_encode_ex(_ptr(x), B, C_, H, W, T, bins, _ptr(lat), _ptr(buf), buf.numel(),
+                                   _stream(stream)))
+    else:
+        _check(lib().snn_encode(_ptr(x), B, C_, H, W, T, _ptr(lat), _ptr(buf), buf.numel(), _stream(stream)))
     return lat
 
 
@@ -231,12 +238,17 @@ def conv_fire(lat_in: torch.Tensor, w: torch.Tensor, pad: int, T: int, theta: fl
 
 
 # ------------------------------------------------------------------------------------------ a4
-def pool_out_hw(H, W, PH, PW, SH, SW, DH=0, DW=0):
+def pool_out_hw(H, W, PH, PW, SH, SW, DH=0, DW=0, eq3=False):
+    if eq3:  # Eq. 3 literally (snn_pool_ex SNN_POOL_EQ3)
+        return (H + 2 * DH) // SH, (W + 2 * DW) // SW
     return (H + 2 * DH - PH) // SH + 1, (W + 2 * DW - PW) // SW + 1
 
 
+POOL_EQ3, POOL_VFINAL = 1, 2  # snn_pool_ex flags (f3 variants)
+
+
 def pool(lat: torch.Tensor, v: Optional[torch.Tensor], window, stride=None, padding=(0, 0),
-         lat_out=None, v_out=None, stream=None):
+         lat_out=None, v_out=None, stream=None, flags: int = 0):
     _req(lat, torch.uint8, "lat")
     if v is not None:
         _req(v, torch.float32, "v")
@@ -244,13 +256,17 @@ def pool(lat: torch.Tensor, v: Optional[torch.Tensor], window, stride=None, padd
     SH, SW = (PH, PW) if stride is None else ((stride, stride) if isinstance(stride, int) else stride)
     DH, DW = (padding, padding) if isinstance(padding, int) else padding
     B, F, H, W = lat.shape
-    Ho, Wo = (max(d, 0) for d in pool_out_hw(H, W, PH, PW, SH, SW, DH, DW))
+    Ho, Wo = (max(d, 0) for d in pool_out_hw(H, W, PH, PW, SH, SW, DH, DW, bool(flags & POOL_EQ3)))
     lo = lat_out if lat_out is not None else torch.empty((B, F, Ho, Wo), dtype=torch.uint8, device=lat.device)
     vo = None
     if v is not None:
         vo = v_out if v_out is not None else torch.empty((B, F, Ho, Wo), dtype=torch.float32, device=lat.device)
-    _check(lib().snn_pool(_ptr(lat), _ptr(v), B, F, H, W, PH, PW, SH, SW, DH, DW, _ptr(lo), _ptr(vo),
-                          _stream(stream)))
+    if flags:
+        _check(lib().snn_pool_ex(_ptr(lat), _ptr(v), B, F, H, W, PH, PW, SH, SW, DH, DW, flags, _ptr(lo), _ptr(vo),
+                                 _stream(stream)))
+    else:
+        _check(lib().snn_pool(_ptr(lat), _ptr(v), B, F, H, W, PH, PW, SH, SW, DH, DW, _ptr(lo), _ptr(vo),
+                              _stream(stream)))
     return lo, vo
 
 
