@@ -94,7 +94,7 @@ def test_final_potential_flow(G, pooled):
 
 @pytest.mark.parametrize("stab,lb,ub,reward", [(2, 0.2, 0.8, 1), (0, 0.2, 0.8, -1), (0, 0.2, 0.8, 1), (2, 0.0, 1.0, -1)])
 def test_stdp_variants(G, stab, lb, ub, reward):
-    rng = np.random.default_rng(stab * 10 + reward)
+    rng = np.random.default_rng(stab * 10 + reward + 5)
     C, H, W, F, KH, T = 6, 14, 14, 20, 5, 15
     w = np.clip(rng.normal(0.8, 0.05, (F, C, KH, KH)), 0, 1).astype(np.float32)
     lat_in = rng.integers(0, T, (C, H, W)).astype(np.uint8)
