@@ -237,6 +237,37 @@ SNN_API int snn_stdp_sequence(const uint8_t* lat_in, int N, int C, int H, int W,
                               int snap_every, void* ws, size_t ws_bytes, snn_stream_t s);
 
 /* ---------------------------------------------------------------------------------------------
+ * f4. Feature sharding across GPUs.  Each rank owns the
+ * contiguous features [f_offset, f_offset + F) of a layer.  Per image: snn_conv_fire on the rank's
+ * weights -> snn_position_keys -> all-reduce(MIN) of the int64 keys over ranks (NCCL, by the caller)
+ * -> snn_k_winners_keys (identical on every rank) -> snn_stdp_update_shard.  Bit-identical to the
+ * unsharded snn_inhibit + snn_k_winners + snn_stdp_update.
+ *
+ * snn_position_keys: keys int64 [B, H, W] = min over the rank's features of the packed key
+ *   (lat << 55) | (~order(v) << 23) | (f_offset + f)   -- ascending = (lat asc, v desc, f asc), the
+ *   pointwise-inhibition order (R13/R14); SNN_KEY_NONE where none of them spikes.  Keys are
+ *   non-negative, so a signed MIN reduction combines ranks.  lat, v [B, F, H, W].
+ *   Requires f_offset + F <= 2^23.
+ * snn_k_winners_keys: k-WTA (R15) on the inhibited map the keys describe (at most one candidate
+ *   per position): winners int32 [B, k, 3] (global f, y, x; -1 padded), count int32 [B]; F = the
+ *   layer's total feature count (for the F*H*W <= 2^24 index check).  Workspace
+ *   snn_k_winners_keys_workspace(B, H, W) (used when H*W*8 B exceeds shared memory).
+ * snn_stdp_update_shard: snn_stdp_update on the rank's weights w [F_local, C, KH, KW] and lat_out
+ *   [F_local, Ho, Wo]; winners carry global features, those outside [f_offset, f_offset + F_local)
+ *   are skipped (another rank owns them).
+ * ------------------------------------------------------------------------------------------- */
+#define SNN_KEY_NONE INT64_MAX
+SNN_API int snn_position_keys(const uint8_t* lat, const float* v, int B, int F, int H, int W, int f_offset,
+                              int64_t* keys, snn_stream_t s);
+SNN_API size_t snn_k_winners_keys_workspace(int B, int H, int W);
+SNN_API int snn_k_winners_keys(const int64_t* keys, int B, int F, int H, int W, int k, int r, int32_t* winners,
+                               int32_t* count, void* ws, size_t ws_bytes, snn_stream_t s);
+SNN_API int snn_stdp_update_shard(float* w, int F_local, int f_offset, int C, int KH, int KW, const uint8_t* lat_in,
+                                  int H, int W, int pad, const uint8_t* lat_out, int Ho, int Wo,
+                                  const int32_t* winners, const int32_t* count, int k, float a_plus, float a_minus,
+                                  float lb, float ub, int stabilizer, const float* reward, snn_stream_t s);
+
+/* ---------------------------------------------------------------------------------------------
  * Measurement helpers (off the hot path).
  * snn_count_events writes two uint64 counters to out[0..1] (device), overwriting them:
  *   out[0] = synaptic events as the paper's delta contraction defines them: F * sum over output

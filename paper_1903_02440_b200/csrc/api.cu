@@ -37,7 +37,13 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
                      int32_t* count, void* ws, size_t ws_bytes, cudaStream_t s);
 int stdp_launch(float* w, int F, int C, int KH, int KW, const uint8_t* lat_in, int H, int W, int pad,
                 const uint8_t* lat_out, int Ho, int Wo, const int32_t* winners, const int32_t* count, int k,
-                float a_plus, float a_minus, float lb, float ub, int stabilizer, const float* reward, cudaStream_t s);
+                float a_plus, float a_minus, float lb, float ub, int stabilizer, const float* reward, int f0,
+                cudaStream_t s);
+int position_keys_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, int f0, int64_t* keys,
+                         cudaStream_t s);
+size_t k_winners_keys_workspace(int B, int H, int W);
+int k_winners_keys_launch(const int64_t* keys, int B, int H, int W, int k, int r, int32_t* winners, int32_t* count,
+                          void* ws, size_t ws_bytes, cudaStream_t s);
 int count_events_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, int F, int KH, int KW, int T,
                         const uint8_t* lat_out, unsigned long long* out, cudaStream_t s);
 size_t filter_bank_smem(int K, int S);
@@ -298,12 +304,14 @@ int snn_k_winners(const uint8_t* lat, const float* v, int B, int F, int H, int W
   return k_winners_launch(lat, v, B, F, H, W, k, r, winners, count, ws, ws_bytes, S(s));
 }
 
-int snn_stdp_update(float* w, int F, int C, int KH, int KW, const uint8_t* lat_in, int H, int W, int pad,
-                    const uint8_t* lat_out, int Ho, int Wo, const int32_t* winners, const int32_t* count, int k,
-                    float a_plus, float a_minus, float lb, float ub, int stabilizer, const float* reward,
-                    snn_stream_t s) {
+int snn_stdp_update_shard(float* w, int F_local, int f_offset, int C, int KH, int KW, const uint8_t* lat_in, int H,
+                          int W, int pad, const uint8_t* lat_out, int Ho, int Wo, const int32_t* winners,
+                          const int32_t* count, int k, float a_plus, float a_minus, float lb, float ub, int stabilizer,
+                          const float* reward, snn_stream_t s) {
+  const int F = F_local;
   REQUIRE(stabilizer >= 0 && stabilizer <= 2, SNN_EINVAL, "snn_stdp_update: stabilizer=%d not in {0, 1, 2}", stabilizer);
   REQUIRE(lb < ub, SNN_EINVAL, "snn_stdp_update: LB >= UB");
+  REQUIRE(f_offset >= 0, SNN_EINVAL, "snn_stdp_update: f_offset < 0");
   REQUIRE(k >= 0 && F >= 1 && C >= 1 && KH >= 1 && KW >= 1 && H >= 1 && W >= 1 && pad >= 0, SNN_ESHAPE,
           "snn_stdp_update: bad dimensions");
   REQUIRE(Ho == H + 2 * pad - KH + 1 && Wo == W + 2 * pad - KW + 1, SNN_ESHAPE,
@@ -313,7 +321,42 @@ int snn_stdp_update(float* w, int F, int C, int KH, int KW, const uint8_t* lat_i
   if (k == 0) return SNN_OK;
   REQUIRE(w && lat_in && lat_out && winners && count, SNN_EINVAL, "snn_stdp_update: NULL tensor");
   return stdp_launch(w, F, C, KH, KW, lat_in, H, W, pad, lat_out, Ho, Wo, winners, count, k, a_plus, a_minus, lb, ub,
-                     stabilizer, reward, S(s));
+                     stabilizer, reward, f_offset, S(s));
+}
+
+int snn_stdp_update(float* w, int F, int C, int KH, int KW, const uint8_t* lat_in, int H, int W, int pad,
+                    const uint8_t* lat_out, int Ho, int Wo, const int32_t* winners, const int32_t* count, int k,
+                    float a_plus, float a_minus, float lb, float ub, int stabilizer, const float* reward,
+                    snn_stream_t s) {
+  return snn_stdp_update_shard(w, F, 0, C, KH, KW, lat_in, H, W, pad, lat_out, Ho, Wo, winners, count, k, a_plus,
+                               a_minus, lb, ub, stabilizer, reward, s);
+}
+
+int snn_position_keys(const uint8_t* lat, const float* v, int B, int F, int H, int W, int f_offset, int64_t* keys,
+                      snn_stream_t s) {
+  REQUIRE(B >= 0 && F >= 0 && H >= 0 && W >= 0, SNN_ESHAPE, "snn_position_keys: negative dimension");
+  REQUIRE(f_offset >= 0 && int64_t(f_offset) + F <= (int64_t(1) << 23), SNN_ESHAPE,
+          "snn_position_keys: global feature index >= 2^23");
+  REQUIRE(int64_t(H) * W < (int64_t(1) << 31), SNN_ESHAPE, "snn_position_keys: H*W >= 2^31");
+  if (int64_t(B) * H * W == 0) return SNN_OK;
+  REQUIRE(keys && (F == 0 || (lat && v)), SNN_EINVAL, "snn_position_keys: NULL tensor");
+  return position_keys_launch(lat, v, B, F, H, W, f_offset, keys, S(s));
+}
+
+size_t snn_k_winners_keys_workspace(int B, int H, int W) {
+  if (B < 0 || H < 0 || W < 0) return 0;
+  return k_winners_keys_workspace(B, H, W);
+}
+
+int snn_k_winners_keys(const int64_t* keys, int B, int F, int H, int W, int k, int r, int32_t* winners,
+                       int32_t* count, void* ws, size_t ws_bytes, snn_stream_t s) {
+  REQUIRE(k >= 1 && k <= 256, SNN_EINVAL, "snn_k_winners_keys: k=%d outside [1, 256]", k);
+  REQUIRE(r >= 0, SNN_EINVAL, "snn_k_winners_keys: r < 0");
+  REQUIRE(B >= 0 && F >= 0 && H >= 0 && W >= 0, SNN_ESHAPE, "snn_k_winners_keys: bad dimensions");
+  REQUIRE(int64_t(F) * H * W <= (int64_t(1) << 24), SNN_ESHAPE, "snn_k_winners_keys: F*H*W > 2^24");
+  if (B == 0) return SNN_OK;
+  REQUIRE(winners && count && (keys || int64_t(H) * W == 0), SNN_EINVAL, "snn_k_winners_keys: NULL tensor");
+  return k_winners_keys_launch(keys, B, H, W, k, r, winners, count, ws, ws_bytes, S(s));
 }
 
 int snn_decide(const int32_t* winners, const int32_t* count, int B, int k, int F, int n_classes,

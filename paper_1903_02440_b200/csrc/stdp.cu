@@ -18,14 +18,15 @@ __global__ void __launch_bounds__(256) stdp_kernel(float* __restrict__ w, int C,
                                                    const int32_t* __restrict__ winners,
                                                    const int32_t* __restrict__ count, float a_plus, float a_minus,
                                                    float lb, float ub, int stabilizer,
-                                                   const float* __restrict__ reward) {
+                                                   const float* __restrict__ reward, int f0, int Floc) {
   const int i = blockIdx.x;
   if (i >= count[0]) return;
+  if (winners[i * 3] < f0 || winners[i * 3] >= f0 + Floc) return;  // another rank's feature (f4 sharding)
   float rw = reward ? reward[0] : 1.0f;
   if (rw == 0.0f) return;  // silent sample: no plasticity
   const float ap = rw > 0.0f ? a_plus : -a_plus;   // anti-STDP = negated rates
   const float am = rw > 0.0f ? a_minus : -a_minus;
-  const int f = winners[i * 3 + 0], y = winners[i * 3 + 1], x = winners[i * 3 + 2];
+  const int f = winners[i * 3 + 0] - f0, y = winners[i * 3 + 1], x = winners[i * 3 + 2];
   const int post = lat_out[(int64_t(f) * Ho + y) * Wo + x];
   const int KK = KH * KW, R = C * KK;
   float* wf = w + int64_t(f) * R;
@@ -49,11 +50,10 @@ __global__ void __launch_bounds__(256) stdp_kernel(float* __restrict__ w, int C,
 int stdp_launch(float* w, int F, int C, int KH, int KW, const uint8_t* lat_in, int H, int W, int pad,
                 const uint8_t* lat_out, int Ho, int Wo, const int32_t* winners, const int32_t* count, int k,
                 float a_plus, float a_minus, float lb, float ub, int stabilizer, const float* reward,
-                cudaStream_t s) {
-  (void)F;
+                int f0, cudaStream_t s) {
   if (k == 0) return SNN_OK;
   stdp_kernel<<<k, 256, 0, s>>>(w, C, KH, KW, lat_in, H, W, pad, lat_out, Ho, Wo, winners, count, a_plus, a_minus,
-                                lb, ub, stabilizer, reward);
+                                lb, ub, stabilizer, reward, f0, F);
   note_launch();
   return check_launch("snn_stdp_update");
 }

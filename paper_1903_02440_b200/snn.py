@@ -53,6 +53,11 @@ def lib() -> C.CDLL:
                 "snn_pool": (i32, [p, p, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, p, p, p]),
                 "snn_pool_ex": (i32, [p, p] + [i32] * 11 + [p, p, p]),
                 "snn_encode_ex": (i32, [p, i32, i32, i32, i32, i32, i32, p, p, sz, p]),
+                "snn_position_keys": (i32, [p, p, i32, i32, i32, i32, i32, p, p]),
+                "snn_k_winners_keys_workspace": (sz, [i32, i32, i32]),
+                "snn_k_winners_keys": (i32, [p, i32, i32, i32, i32, i32, i32, p, p, p, sz, p]),
+                "snn_stdp_update_shard": (i32, [p, i32, i32, i32, i32, i32, p, i32, i32, i32, p, i32, i32, p, p, i32,
+                                                f32, f32, f32, f32, i32, p, p]),
                 "snn_inhibit": (i32, [p, p, i32, i32, i32, i32, p, p, p, p]),
                 "snn_k_winners_workspace": (sz, [i32, i32, i32, i32]),
                 "snn_k_winners": (i32, [p, p, i32, i32, i32, i32, i32, i32, p, p, p, sz, p]),
@@ -83,7 +88,8 @@ def exported_symbols():
             "snn_inhibit", "snn_k_winners_workspace", "snn_k_winners", "snn_stdp_update", "snn_decide",
             "snn_count_events", "snn_launch_count", "snn_conv_fire_plan", "snn_stdp_sequence_workspace",
             "snn_stdp_sequence", "snn_filter_bank", "snn_local_norm", "snn_lateral_inhibition",
-            "snn_encode_ex", "snn_pool_ex"]
+            "snn_encode_ex", "snn_pool_ex", "snn_position_keys", "snn_k_winners_keys_workspace",
+            "snn_k_winners_keys", "snn_stdp_update_shard"]
 
 
 def _check(rc: int):
@@ -299,7 +305,8 @@ def k_winners(lat: torch.Tensor, v: torch.Tensor, k: int, r: int, winners=None, 
 # ------------------------------------------------------------------------------------------ a7
 def stdp_update(w: torch.Tensor, lat_in: torch.Tensor, pad: int, lat_out: torch.Tensor, winners: torch.Tensor,
                 count: torch.Tensor, a_plus: float, a_minus: float, lb: float = 0.0, ub: float = 1.0,
-                stabilizer: int = 1, reward: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+                stabilizer: int = 1, reward: Optional[torch.Tensor] = None, stream=None,
+                f_offset: Optional[int] = None) -> torch.Tensor:
     """In-place update of w [F, C, KH, KW] for one image: lat_in [C, H, W], lat_out [F, Ho, Wo],
     winners [k, 3], count [1] (device), reward float32 [1] (device, +1 / -1 / 0) or None (= +1)."""
     _req(w, torch.float32, "w")
@@ -313,10 +320,44 @@ def stdp_update(w: torch.Tensor, lat_in: torch.Tensor, pad: int, lat_out: torch.
     _, H, W = lat_in.shape
     _, Ho, Wo = lat_out.shape
     k = winners.shape[-2]
+    if f_offset is not None:  # f4: w holds the features [f_offset, f_offset + F) of the layer
+        _check(lib().snn_stdp_update_shard(_ptr(w), F, int(f_offset), C_, KH, KW, _ptr(lat_in), H, W, pad,
+                                           _ptr(lat_out), Ho, Wo, _ptr(winners), _ptr(count), k, float(a_plus),
+                                           float(a_minus), float(lb), float(ub), int(stabilizer), _ptr(reward),
+                                           _stream(stream)))
+        return w
     _check(lib().snn_stdp_update(_ptr(w), F, C_, KH, KW, _ptr(lat_in), H, W, pad, _ptr(lat_out), Ho, Wo,
                                  _ptr(winners), _ptr(count), k, float(a_plus), float(a_minus), float(lb), float(ub),
                                  int(stabilizer), _ptr(reward), _stream(stream)))
     return w
+
+
+# ------------------------------------------------------------------------------------------ f4
+KEY_NONE = (1 << 63) - 1  # SNN_KEY_NONE
+
+
+def position_keys(lat: torch.Tensor, v: torch.Tensor, f_offset: int = 0, out=None, stream=None) -> torch.Tensor:
+    """lat/v [B, F, H, W] of the rank's features -> int64 [B, H, W] min packed key (snn_position_keys)."""
+    _req(lat, torch.uint8, "lat")
+    _req(v, torch.float32, "v")
+    B, F, H, W = lat.shape
+    keys = out if out is not None else torch.empty((B, H, W), dtype=torch.int64, device=lat.device)
+    _req(keys, torch.int64, "keys")
+    _check(lib().snn_position_keys(_ptr(lat), _ptr(v), B, F, H, W, int(f_offset), _ptr(keys), _stream(stream)))
+    return keys
+
+
+def k_winners_keys(keys: torch.Tensor, F: int, k: int, r: int, winners=None, count=None, ws=None, stream=None):
+    """k-WTA on the inhibited map given by reduced position keys [B, H, W] (snn_k_winners_keys)."""
+    _req(keys, torch.int64, "keys")
+    B, H, W = keys.shape
+    win = winners if winners is not None else torch.empty((B, k, 3), dtype=torch.int32, device=keys.device)
+    cnt = count if count is not None else torch.empty((B,), dtype=torch.int32, device=keys.device)
+    n = int(lib().snn_k_winners_keys_workspace(B, H, W))
+    buf = ws if ws is not None else _ws.get(n, keys.device, "kwta_keys")
+    _check(lib().snn_k_winners_keys(_ptr(keys), B, int(F), H, W, k, r, _ptr(win), _ptr(cnt), _ptr(buf), buf.numel(),
+                                    _stream(stream)))
+    return win, cnt
 
 
 def decide(winners: torch.Tensor, count: torch.Tensor, F: int, n_classes: int, labels: Optional[torch.Tensor] = None,
