@@ -114,6 +114,92 @@ __global__ void tc_prep_a_kernel(const uint8_t* __restrict__ lat_in, int C, int 
   }
 }
 
+// B operand, vectorised: one thread per (chunk, feature, 16 consecutive k): 16 weights -> the four
+// 16-byte limb rows n = 4 f_local + limb of one core-matrix column.
+__global__ void tc_prep_b16_kernel(const float* __restrict__ w, int F, int R, TcPlan p, uint8_t* __restrict__ bq,
+                                   int* err) {
+  const int nk16 = p.Kp / 16;
+  const int64_t total = int64_t(p.nch) * p.Fc * nk16;
+  int bad = 0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int k16 = int(i % nk16);
+    const int64_t rest = i / nk16;
+    const int fl = int(rest % p.Fc), ch = int(rest / p.Fc);
+    const int f = ch * p.Fc + fl, k0 = k16 * 16;
+    uint32_t limb[4][4] = {};
+    if (f < F) {
+      for (int j = 0; j < 16; ++j) {
+        const int k = k0 + j;
+        if (k >= R) break;
+        const float x = __ldg(w + int64_t(f) * R + k);
+        const float s = x * 2147483648.0f;
+        if (!(x >= 0.0f && x <= 1.0f) || s != truncf(s)) { bad = 1; continue; }
+        const uint32_t q = uint32_t(s);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) limb[l][j >> 2] |= ((q >> (8 * l)) & 0xFFu) << (8 * (j & 3));
+      }
+    }
+    uint8_t* base = bq + size_t(ch) * p.Kt * p.N * kTcKT;
+#pragma unroll
+    for (int l = 0; l < 4; ++l)
+      *reinterpret_cast<uint4*>(base + tc_off(4 * fl + l, k0, p.N, p.Kt)) =
+          make_uint4(limb[l][0], limb[l][1], limb[l][2], limb[l][3]);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flag_error(err, kErrInexact);
+}
+
+// A operand from a shared-memory band: one CTA per (image, band of RB output rows) stages the binary
+// spike-wave S[T-1] of the band's input rows (zero padded, [C][RB + KH - 1][W + 2 pad]) once, then
+// writes the band's core-matrix rows (16 receptive-field entries of one position per thread,
+// consecutive threads = consecutive positions, so 8 threads fill one 128-byte core matrix).  KS CTAs
+// share a band (each stages it and writes every KS-th 16-byte K column), so small batches still fill
+// the GPU.  The last CTA zero-fills the padding rows M .. Mt * 128.
+__global__ void __launch_bounds__(256) tc_prep_a_band_kernel(const uint8_t* __restrict__ lat_in, int C, int H, int W,
+                                                             int pad, int KH, int KW, int Ho, int Wo, int T,
+                                                             TcPlan p, int RB, int nbands, int B, int KS,
+                                                             uint8_t* __restrict__ aq) {
+  extern __shared__ uint8_t band[];
+  const int Wp = W + 2 * pad, TR = RB + KH - 1, KK = KH * KW, nk16 = p.Kp / 16;
+  if (int(blockIdx.x) == B * nbands * KS) {  // padding rows
+    const int64_t rows = (int64_t(p.Mt) * kTcM - p.M) * nk16;
+    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+      const int m = p.M + int(i % (p.Mt * kTcM - p.M)), k16 = int(i / (p.Mt * kTcM - p.M));
+      *reinterpret_cast<uint4*>(aq + tc_off(m, k16 * 16, kTcM, p.Kt)) = make_uint4(0, 0, 0, 0);
+    }
+    return;
+  }
+  const int ks = blockIdx.x % KS, bb = blockIdx.x / KS;
+  const int b = bb / nbands, ya = (bb % nbands) * RB;
+  const int yb = ya + RB < Ho ? ya + RB : Ho;
+  const uint8_t* lb = lat_in + int64_t(b) * C * H * W;
+  {  // zero the band (padding never spikes), then scatter the band's input rows (coalesced per channel)
+    uint4* b16 = reinterpret_cast<uint4*>(band);
+    for (int i = threadIdx.x; i < (C * TR * Wp + 15) / 16; i += blockDim.x) b16[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const int top = ya - pad;  // input row of band row 0
+    const int iy0 = top > 0 ? top : 0, iy1 = (top + TR - 1 < H - 1 ? top + TR - 1 : H - 1);
+    const int nr = iy1 - iy0 + 1, per_c = nr * W;
+    for (int i = threadIdx.x; i < C * per_c; i += blockDim.x) {
+      const int c = i / per_c, r = i - c * per_c, ry = r / W, ix = r - ry * W;
+      band[(c * TR + iy0 + ry - top) * Wp + ix + pad] = __ldg(lb + (int64_t(c) * H + iy0 + ry) * W + ix) < T ? 1 : 0;
+    }
+  }
+  const int mcount = (yb - ya) * Wo, m0 = b * Ho * Wo + ya * Wo;
+  const int nks = (nk16 - ks + KS - 1) / KS;  // this CTA's K columns: ks, ks + KS, ...
+  for (int i = threadIdx.x; i < mcount * nks; i += blockDim.x) {
+    const int k16 = ks + (i / mcount) * KS, mi = i - (i / mcount) * mcount;
+    const int yl = mi / Wo, x = mi - yl * Wo, k0 = k16 * 16;
+    int c = k0 / KK, r = k0 - c * KK, ky = r / KW, kx = r - ky * KW;
+    uint32_t wv[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (k0 + j < p.K) wv[j >> 2] |= uint32_t(band[(c * TR + yl + ky) * Wp + x + kx]) << (8 * (j & 3));
+      if (++kx == KW) { kx = 0; if (++ky == KH) { ky = 0; ++c; } }
+    }
+    *reinterpret_cast<uint4*>(aq + tc_off(m0 + mi, k0, kTcM, p.Kt)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+  }
+}
+
 // ------------------------------------------------------------------------------- the GEMM
 __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* __restrict__ aq,
                                                                  const uint8_t* __restrict__ bq, TcPlan p, int F,
@@ -216,6 +302,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
   }
 }
 
+static inline int64_t al16c(int64_t x) { return (x + 15) & ~int64_t(15); }
+
 int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH, int KW,
                    int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes, cudaStream_t s) {
   const int Ho = H + 2 * pad - KH + 1, Wo = W + 2 * pad - KW + 1, R = C * KH * KW;
@@ -225,17 +313,30 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
   uint8_t* aq = reinterpret_cast<uint8_t*>(ws) + a_off;
   uint8_t* bq = reinterpret_cast<uint8_t*>(ws) + b_off;
   {
-    const int64_t total = int64_t(p.nch) * p.N * p.Kp;
+    const int64_t total = int64_t(p.nch) * p.Fc * (p.Kp / 16);
     int64_t blocks = ceil_div(total, 256);
     if (blocks > int64_t(num_sms()) * 8) blocks = int64_t(num_sms()) * 8;
-    tc_prep_b_kernel<<<int(blocks), 256, 0, s>>>(w, F, R, p, bq, error_word_ptr());
+    tc_prep_b16_kernel<<<int(blocks), 256, 0, s>>>(w, F, R, p, bq, error_word_ptr());
     note_launch();
   }
   {
-    const int64_t rows16 = int64_t(p.Mt) * kTcM * (p.Kp / 16);
-    int64_t blocks = ceil_div(rows16, 256);
-    if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
-    tc_prep_a_kernel<<<int(blocks), 256, 0, s>>>(lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p, aq);
+    // the largest band of output rows whose padded input rows fit 48 KB of shared memory
+    const int Wp = W + 2 * pad;
+    int RB = Ho;
+    while (RB > 1 && int64_t(C) * (RB + KH - 1) * Wp > 48 * 1024) RB = (RB + 1) / 2;
+    // (a batch too small to give every SM two bands keeps the per-row gather kernel)
+    if (int64_t(C) * (RB + KH - 1) * Wp + 16 <= 48 * 1024 && int64_t(B) * ceil_div(Ho, RB) >= 2 * num_sms()) {
+      const int nbands = int(ceil_div(Ho, RB));
+      const int smem_a = int(al16c(C * (RB + KH - 1) * Wp));
+      const int64_t KS = 1;
+      tc_prep_a_band_kernel<<<unsigned(int64_t(B) * nbands * KS + 1), 256, smem_a, s>>>(
+          lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p, RB, nbands, B, int(KS), aq);
+    } else {
+      const int64_t rows16 = int64_t(p.Mt) * kTcM * (p.Kp / 16);
+      int64_t blocks = ceil_div(rows16, 256);
+      if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
+      tc_prep_a_kernel<<<int(blocks), 256, 0, s>>>(lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p, aq);
+    }
     note_launch();
   }
   uint32_t cols = 32;

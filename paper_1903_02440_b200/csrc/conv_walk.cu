@@ -43,29 +43,19 @@ template <int PPW>
 __global__ void __launch_bounds__(512) rf_sort_kernel(const WalkArgs a) {
   constexpr int LPP = 32 / PPW;
   extern __shared__ __align__(16) unsigned char smem[];
-  int32_t* eoff = reinterpret_cast<int32_t*>(smem + a.off_eoff);
-  uint16_t* ekk = reinterpret_cast<uint16_t*>(smem + a.off_ekk);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int grp = lane / LPP, gl = lane - grp * LPP;
-  unsigned char* pb = smem + a.off_warps + warp * a.warp_bytes + grp * a.pos_bytes;
+  unsigned char* wbase = smem + a.off_warps + warp * a.warp_bytes;
+  unsigned char* pb = wbase + grp * a.pos_bytes;
   uint32_t* cnt = reinterpret_cast<uint32_t*>(pb + a.cnt_off);
   uint16_t* start = reinterpret_cast<uint16_t*>(pb + a.start_off);
   uint32_t* list = reinterpret_cast<uint32_t*>(pb + a.list_off);
-  rf_tables(a, eoff, ekk);
+  rf_tables(a, smem);
   __syncthreads();
-  const int HoWo = a.Ho * a.Wo;
-  const int64_t CHW = int64_t(a.C) * a.H * a.W;
   for (int64_t wi = int64_t(blockIdx.x) * nwarps + warp; wi * PPW < a.np; wi += int64_t(gridDim.x) * nwarps) {
     const int64_t q = wi * PPW + grp;  // chunk-relative position
     const bool pv = q < a.np;
-    const int p = int(a.p0 + q);
-    const int b = pv ? p / HoWo : 0;
-    const int rem = pv ? p - b * HoWo : 0;
-    const int y = rem / a.Wo, x = rem - (rem / a.Wo) * a.Wo;
-    const int y0 = y - a.pad, x0 = x - a.pad;
-    const uint8_t* in = a.lat_in + int64_t(b) * CHW + int64_t(y0) * a.W + x0;
-    const bool interior = y0 >= 0 && x0 >= 0 && y0 + a.KH <= a.H && x0 + a.KW <= a.W;
-    rf_sort_group<LPP>(a, eoff, ekk, pv, in, interior, y0, x0, gl, cnt, start, list);
+    rf_sort_warp<PPW>(a, smem, wbase, wi * PPW, lane, grp, gl, pv, cnt, start, list);
     if (pv) {  // record = [header: T+1 u16 starts, 16-aligned][entries: u32, whole blocks]
       unsigned char* rec = a.lists + q * a.rec;
       uint16_t* hdr = reinterpret_cast<uint16_t*>(rec);
@@ -86,11 +76,10 @@ __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(
   static_assert(!PRE || PPW == 1, "presorted walk: one position per warp");
   extern __shared__ __align__(16) unsigned char smem[];
   const int R = a.R;
-  int32_t* eoff = reinterpret_cast<int32_t*>(smem + a.off_eoff);
-  uint16_t* ekk = reinterpret_cast<uint16_t*>(smem + a.off_ekk);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int grp = lane / LPP, gl = lane - grp * LPP;
-  unsigned char* pb = smem + a.off_warps + warp * a.warp_bytes + grp * a.pos_bytes;
+  unsigned char* wbase = smem + a.off_warps + warp * a.warp_bytes;
+  unsigned char* pb = wbase + grp * a.pos_bytes;
   uint32_t* cnt = reinterpret_cast<uint32_t*>(pb + a.cnt_off);
   uint16_t* start = reinterpret_cast<uint16_t*>(pb + a.start_off);
   uint32_t* list = reinterpret_cast<uint32_t*>(pb + a.list_off);  // fused: the sorted list; PRE: the ring
@@ -100,12 +89,11 @@ __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(
     uint4* dst = reinterpret_cast<uint4*>(smem);
     const int n4 = (R + 1) * FGS / 4;
     for (int i = tid; i < n4; i += blockDim.x) dst[i] = src[i];
-    if (!PRE) rf_tables(a, eoff, ekk);
+    if (!PRE) rf_tables(a, smem);
   }
   __syncthreads();
 
   const int HoWo = a.Ho * a.Wo;
-  const int64_t CHW = int64_t(a.C) * a.H * a.W;
   const int fbase = g * FGS + gl * FPL;
   unsigned valid = 0;
 #pragma unroll
@@ -153,11 +141,7 @@ __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(
       sent = pbuf + bi * a.buf_bytes + a.hdr;
       ent = a.lists + q * a.rec + a.hdr;
     } else {
-      const int y = rem / a.Wo, x = rem - (rem / a.Wo) * a.Wo;
-      const int y0 = y - a.pad, x0 = x - a.pad;
-      const uint8_t* in = a.lat_in + int64_t(b) * CHW + int64_t(y0) * a.W + x0;
-      const bool interior = y0 >= 0 && x0 >= 0 && y0 + a.KH <= a.H && x0 + a.KW <= a.W;
-      rf_sort_group<LPP>(a, eoff, ekk, pv, in, interior, y0, x0, gl, cnt, start, list);
+      rf_sort_warp<PPW>(a, smem, wbase, wi * PPW, lane, grp, gl, pv, cnt, start, list);
     }
 
     uint32_t lo;
@@ -196,6 +180,36 @@ static int pos_scratch_bytes(int T, int R, WalkArgs* a) {
   return o;
 }
 
+// Layout of the sort's tables (from byte `base`) and per-warp scratch (PPW position scratches + the
+// input patch, rf_sort_warp); a.pos_bytes must be set.  Returns the offset of the warps' regions.
+static int sort_layout(WalkArgs& a, int ppw, int base) {
+  a.patch_w = a.KW + ppw - 1;
+  const long pn = long(a.C) * a.KH * a.patch_w;
+  // the patch pays when several positions share it; one position per warp (or a large receptive
+  // field) reads its latencies from global memory (measured C5: 47.6 ms without, 50.4 ms with)
+  a.patch_n = (ppw > 1 && pn <= 4096) ? int(pn) : 0;
+  a.off_eoff = base;
+  a.off_ekk = a.off_eoff + al16(a.R * 4);
+  a.off_eoffp = a.off_ekk + al16(a.R * 2);
+  a.off_ptab = a.off_eoffp + al16(a.R * 2);
+  a.off_pkk = a.off_ptab + al16(a.patch_n * 4);
+  a.off_warps = a.off_pkk + al16(a.patch_n * 2);
+  a.patch_off = ppw * a.pos_bytes;
+  a.warp_bytes = a.patch_off + al16(a.patch_n);
+  return a.off_warps;
+}
+
+// positions per warp of the sort kernel (more independent positions per warp hide the gather latency;
+// measured C2 conv2 (R 270): 1.20 ms at 1, 1.14 ms at 4; C5 (R 800): 50 ms at 1, 64 ms at 4);
+// SNN_SORT_PPW overrides: 1, 2, 4
+static int sort_ppw_for(int R) {
+  if (const char* e = getenv("SNN_SORT_PPW")) {
+    const int v = atoi(e);
+    if (v == 1 || v == 2 || v == 4) return v;
+  }
+  return R <= 512 ? 4 : 1;
+}
+
 static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, WalkPlan* pl) {
   WalkArgs& a = pl->a;
   a = WalkArgs{};
@@ -204,8 +218,13 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
   a.Ho = H + 2 * pad - KH + 1; a.Wo = W + 2 * pad - KW + 1; a.R = C * KH * KW;
   const int R = a.R;
   if (R + T + kIt >= 65536) return false;  // u16 bucket starts
-  const long tables = al16(R * 4) + al16(R * 2);
   struct Cand { int ppw, fpl; };
+  auto sort_cost = [&](int ppw, long* tables) {  // (tables bytes, per-warp bytes) of a fused candidate
+    WalkArgs t = a;
+    pos_scratch_bytes(T, R, &t);
+    *tables = sort_layout(t, ppw, 0);
+    return long(t.warp_bytes);
+  };
   const Cand cands[] = {{4, 4}, {2, 4}, {1, 4}, {4, 2}, {2, 2}, {1, 2}, {1, 1}};
   // 1) fused: all features in one group with >= 8 warps of sort scratch
   int best = -1, best_warps = 0;
@@ -213,7 +232,8 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
     const int lpp = 32 / c.ppw, fgs = lpp * c.fpl;
     if (fgs < F) continue;
     if (fgs > 32 && F <= fgs / 2) continue;
-    const int wb = c.ppw * pos_scratch_bytes(T, R, nullptr);
+    long tables;
+    const long wb = sort_cost(c.ppw, &tables);
     const long fixed = al16(int(long(R + 1) * fgs * 4)) + tables;
     if (fixed + 8L * wb > kWalkSmemLimit) continue;
     long warps = (kWalkSmemLimit - fixed) / wb;
@@ -227,7 +247,8 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
       for (const Cand& c : cands)
         if (c.ppw == ppw && c.fpl == fpl && (32 / ppw) * fpl >= F) {
           best = int(&c - cands);
-          const int wb = c.ppw * pos_scratch_bytes(T, R, nullptr);
+          long tables;
+          const long wb = sort_cost(c.ppw, &tables);
           const long fixed = al16(int(long(R + 1) * (32 / ppw) * fpl * 4)) + tables;
           long warps = (kWalkSmemLimit - fixed) / wb;
           const int wcap = c.fpl == 4 ? 24 : 32;
@@ -241,10 +262,7 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
     pl->FGS = lpp * pl->fpl; pl->n_groups = 1; pl->nwarps = best_warps;
     a.row_bytes = pl->FGS * 4;
     pos_scratch_bytes(T, R, &a);
-    a.warp_bytes = pl->ppw * a.pos_bytes;
-    a.off_eoff = al16(int(long(R + 1) * pl->FGS * 4));
-    a.off_ekk = a.off_eoff + al16(R * 4);
-    a.off_warps = a.off_ekk + al16(R * 2);
+    sort_layout(a, pl->ppw, al16(int(long(R + 1) * pl->FGS * 4)));
     pl->smem = a.off_warps + pl->nwarps * a.warp_bytes;
     a.np = int64_t(B) * a.Ho * a.Wo;
     pl->chunk = a.np;
@@ -261,7 +279,7 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
     const long wsb = long(R + 1) * fgs * 4;
     const int hdr_bytes = al16((T + 1) * 2);
     if (al16(int(wsb)) + 20L * (16 + 2 * (hdr_bytes + kIt * 4)) > kWalkSmemLimit) continue;
-    pl->sort_ppw = R <= 256 ? 4 : 1;  // 4 positions per warp for small receptive fields
+    pl->sort_ppw = sort_ppw_for(R);
     pl->pre = true;
     pl->ppw = 1; pl->fpl = fpl; pl->FGS = fgs;
     pl->n_groups = int(ceil_div(F, fgs));
@@ -284,10 +302,8 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
     WalkArgs& sa = pl->sa;
     sa = a;
     pos_scratch_bytes(T, R, &sa);
-    sa.warp_bytes = pl->sort_ppw * sa.pos_bytes;
-    sa.off_eoff = 0;
-    sa.off_ekk = al16(R * 4);
-    sa.off_warps = sa.off_ekk + al16(R * 2);
+    sort_layout(sa, pl->sort_ppw, 0);
+    while (pl->sort_nwarps > 1 && sa.off_warps + pl->sort_nwarps * sa.warp_bytes > kWalkSmemLimit) pl->sort_nwarps /= 2;
     pl->sort_smem = sa.off_warps + pl->sort_nwarps * sa.warp_bytes;
     const int64_t npos = int64_t(B) * a.Ho * a.Wo;
     size_t chunk_bytes = kListChunkBytes;
@@ -355,16 +371,13 @@ int rf_sort_lists_launch(const uint8_t* lat_in, int B, int C, int H, int W, int 
   sa.row_bytes = row_bytes; sa.lists = lists; sa.rec = rec; sa.hdr = hdr;
   sa.lat_in = lat_in; sa.p0 = 0; sa.np = int64_t(B) * sa.Ho * sa.Wo;
   const int R = sa.R;
-  pl.sort_ppw = R <= 256 ? 4 : 1;
+  pl.sort_ppw = sort_ppw_for(R);
   pl.sort_nwarps = 16;
   pos_scratch_bytes(T, R, &sa);
-  sa.warp_bytes = pl.sort_ppw * sa.pos_bytes;
-  sa.off_eoff = 0;
-  sa.off_ekk = al16(R * 4);
-  sa.off_warps = sa.off_ekk + al16(R * 2);
+  sort_layout(sa, pl.sort_ppw, 0);
   pl.sort_smem = sa.off_warps + pl.sort_nwarps * sa.warp_bytes;
   if (pl.sort_smem > kWalkSmemLimit) return set_error(SNN_ESHAPE, "rf_sort_lists: receptive field too large");
-  return pl.sort_ppw == 4 ? sort_go<4>(pl, sa, s) : sort_go<1>(pl, sa, s);
+  return pl.sort_ppw == 4 ? sort_go<4>(pl, sa, s) : pl.sort_ppw == 2 ? sort_go<2>(pl, sa, s) : sort_go<1>(pl, sa, s);
 }
 
 // Plan description for snn_conv_fire_plan: 0 if the walk does not apply, else 1 (+ *pre, *chunks).
@@ -418,7 +431,7 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
     a.p0 = p0;
     a.np = npos - p0 < pl.chunk ? npos - p0 : pl.chunk;
     sa.p0 = a.p0; sa.np = a.np;
-    rc = pl.sort_ppw == 4 ? sort_go<4>(pl, sa, s) : sort_go<1>(pl, sa, s);
+    rc = pl.sort_ppw == 4 ? sort_go<4>(pl, sa, s) : pl.sort_ppw == 2 ? sort_go<2>(pl, sa, s) : sort_go<1>(pl, sa, s);
     if (rc) return rc;
     switch (pl.fpl) {
       case 4: rc = walk_go<4, 1, true>(pl, a, s); break;

@@ -17,7 +17,6 @@ namespace {
 
 constexpr int kKeyThreads = 256;
 constexpr int kWtaThreads = 512;
-constexpr int kMaxK = 256;
 
 __device__ __forceinline__ int64_t pos_key(uint8_t lat, float v, int f) {
   return int64_t((uint64_t(lat) << 55) | (uint64_t(~ordered_bits(v)) << 23) | uint64_t(f));
@@ -55,7 +54,6 @@ __global__ void __launch_bounds__(kWtaThreads) k_winners_keys_kernel(const int64
                                                                      int32_t* __restrict__ count) {
   extern __shared__ uint64_t skey[];
   __shared__ uint64_t red[kWtaThreads / 32];
-  __shared__ int s_n;
   const int b = blockIdx.x, HW = H * W;
   uint64_t* kk = use_smem ? skey : scratch + int64_t(b) * HW;
   const int64_t* kb = keys + int64_t(b) * HW;
@@ -65,7 +63,6 @@ __global__ void __launch_bounds__(kWtaThreads) k_winners_keys_kernel(const int64
     const uint64_t f = uint64_t(pk) & 0x7FFFFFu;
     kk[p] = ((uint64_t(pk) >> 23) << 24) | (f * uint64_t(HW) + uint64_t(p));
   }
-  if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int n = 0;

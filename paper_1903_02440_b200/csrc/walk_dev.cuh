@@ -34,6 +34,11 @@ struct WalkArgs {
   int64_t p0, np;     // chunk of positions [p0, p0 + np)
   int* err;           // device error word
   int npre, buf_bytes; // PRE: list entries prefetched per position (one bulk copy), bytes of one buffer
+  // sort from a per-warp shared-memory patch of the input (the union of the warp's PPW receptive fields
+  // when its positions share an output row): C x KH x patch_w latencies, patch_w = KW + PPW - 1;
+  // patch_n = 0 disables it.  Tables: ptab (patch index -> input offset), pkk (ky << 8 | kx),
+  // eoffp (receptive-field entry -> patch index); the patch sits at warp base + patch_off.
+  int patch_w, patch_n, patch_off, off_ptab, off_pkk, off_eoffp;
 };
 
 static inline int al16(int x) { return (x + 15) & ~15; }
@@ -68,10 +73,9 @@ __device__ __forceinline__ uint8_t rf_lat(const WalkArgs& a, const int32_t* eoff
 // the bucket's running position.  Entries are weight-row byte offsets e * row_bytes; the tail is
 // padded to a whole walk iteration.  The order inside a bucket is whatever the atomics gave: it does
 // not change any result (the sum at a bucket end is exact and order-free).
-template <int LPP>
-__device__ __forceinline__ void rf_sort_group(const WalkArgs& a, const int32_t* eoff, const uint16_t* ekk, bool pv,
-                                              const uint8_t* in, bool interior, int y0, int x0, int gl,
-                                              uint32_t* cnt, uint16_t* start, uint32_t* list) {
+template <int LPP, class Lat>
+__device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl, uint32_t* cnt, uint16_t* start,
+                                              uint32_t* list, Lat lat_of) {
   const int R = a.R, T = a.T;
   const uint32_t rb = uint32_t(a.row_bytes);
   for (int t = gl; t < T; t += LPP) cnt[t] = 0;
@@ -79,7 +83,7 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, const int32_t* 
   if (pv) {
 #pragma unroll 4
     for (int e = gl; e < R; e += LPP) {
-      const int l = rf_lat(a, eoff, ekk, in, interior, y0, x0, e);
+      const int l = lat_of(e);
       if (l < T) atomicAdd(&cnt[l], 1u);
     }
   }
@@ -108,7 +112,7 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, const int32_t* 
   if (pv) {
 #pragma unroll 4
     for (int e = gl; e < R; e += LPP) {
-      const int l = rf_lat(a, eoff, ekk, in, interior, y0, x0, e);
+      const int l = lat_of(e);
       if (l < T) list[atomicAdd(&cnt[l], 1u)] = uint32_t(e) * rb;
     }
   }
@@ -119,12 +123,71 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, const int32_t* 
   __syncwarp();
 }
 
-__device__ __forceinline__ void rf_tables(const WalkArgs& a, int32_t* eoff, uint16_t* ekk) {
+// Sort the receptive field of each of the warp's PPW consecutive positions (group grp = position
+// q0 + grp).  When the warp's valid positions share an output row, the union of their receptive
+// fields is first staged once into the warp's shared-memory patch (one coalesced-ish byte gather,
+// bounds checked once per patch element); both sort passes then read latencies from the patch.
+// Otherwise (a warp straddling a row end) each group reads its latencies from global memory.
+template <int PPW>
+__device__ __forceinline__ void rf_sort_warp(const WalkArgs& a, const unsigned char* tabs, unsigned char* wbase,
+                                             int64_t q0, int lane, int grp, int gl, bool pv, uint32_t* cnt,
+                                             uint16_t* start, uint32_t* list) {
+  constexpr int LPP = 32 / PPW;
+  const int HoWo = a.Ho * a.Wo;
+  const int64_t CHW = int64_t(a.C) * a.H * a.W;
+  const int64_t qlast = (q0 + PPW - 1 < a.np ? q0 + PPW - 1 : a.np - 1);
+  const int pf = int(a.p0 + q0), pl = int(a.p0 + qlast);
+  if (a.patch_n > 0 && pf / a.Wo == pl / a.Wo) {  // warp-uniform
+    const int32_t* ptab = reinterpret_cast<const int32_t*>(tabs + a.off_ptab);
+    const uint16_t* pkk = reinterpret_cast<const uint16_t*>(tabs + a.off_pkk);
+    const uint16_t* eoffp = reinterpret_cast<const uint16_t*>(tabs + a.off_eoffp);
+    uint8_t* patch = wbase + a.patch_off;
+    const int b = pf / HoWo, rem = pf - b * HoWo, y = rem / a.Wo, x = rem - (rem / a.Wo) * a.Wo;
+    const int y0 = y - a.pad, x0 = x - a.pad;
+    const uint8_t* in0 = a.lat_in + int64_t(b) * CHW + int64_t(y0) * a.W + x0;
+    const bool interior = y0 >= 0 && x0 >= 0 && y0 + a.KH <= a.H && x0 + a.patch_w <= a.W;
+    if (interior) {
+      for (int i = lane; i < a.patch_n; i += 32) patch[i] = __ldg(in0 + ptab[i]);
+    } else {
+      for (int i = lane; i < a.patch_n; i += 32) {
+        const int kk = pkk[i], yy = y0 + (kk >> 8), xx = x0 + (kk & 0xFF);
+        patch[i] = (yy >= 0 && yy < a.H && xx >= 0 && xx < a.W) ? __ldg(in0 + ptab[i]) : kNoSpike;
+      }
+    }
+    __syncwarp();
+    const uint8_t* pg = patch + grp;
+    rf_sort_group<LPP>(a, pv, gl, cnt, start, list, [&](int e) { return int(pg[eoffp[e]]); });
+  } else {
+    const int32_t* eoff = reinterpret_cast<const int32_t*>(tabs + a.off_eoff);
+    const uint16_t* ekk = reinterpret_cast<const uint16_t*>(tabs + a.off_ekk);
+    const int p = int(a.p0 + q0 + grp);
+    const int b = pv ? p / HoWo : 0;
+    const int rem = pv ? p - b * HoWo : 0;
+    const int y = rem / a.Wo, x = rem - (rem / a.Wo) * a.Wo;
+    const int y0 = y - a.pad, x0 = x - a.pad;
+    const uint8_t* in = a.lat_in + int64_t(b) * CHW + int64_t(y0) * a.W + x0;
+    const bool interior = y0 >= 0 && x0 >= 0 && y0 + a.KH <= a.H && x0 + a.KW <= a.W;
+    rf_sort_group<LPP>(a, pv, gl, cnt, start, list,
+                       [&](int e) { return int(rf_lat(a, eoff, ekk, in, interior, y0, x0, e)); });
+  }
+}
+
+__device__ __forceinline__ void rf_tables(const WalkArgs& a, unsigned char* tabs) {
+  int32_t* eoff = reinterpret_cast<int32_t*>(tabs + a.off_eoff);
+  uint16_t* ekk = reinterpret_cast<uint16_t*>(tabs + a.off_ekk);
   const int KK = a.KH * a.KW;
   for (int e = threadIdx.x; e < a.R; e += blockDim.x) {
     const int c = e / KK, r = e - c * KK, ky = r / a.KW, kx = r - ky * a.KW;
     eoff[e] = c * a.H * a.W + ky * a.W + kx;
     ekk[e] = uint16_t((ky << 8) | kx);
+    if (a.patch_n > 0)
+      reinterpret_cast<uint16_t*>(tabs + a.off_eoffp)[e] = uint16_t((c * a.KH + ky) * a.patch_w + kx);
+  }
+  const int PK = a.KH * a.patch_w;
+  for (int i = threadIdx.x; i < a.patch_n; i += blockDim.x) {
+    const int c = i / PK, r = i - c * PK, ky = r / a.patch_w, kx = r - ky * a.patch_w;
+    reinterpret_cast<int32_t*>(tabs + a.off_ptab)[i] = c * a.H * a.W + ky * a.W + kx;
+    reinterpret_cast<uint16_t*>(tabs + a.off_pkk)[i] = uint16_t((ky << 8) | kx);
   }
 }
 
