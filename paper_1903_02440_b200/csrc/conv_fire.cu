@@ -388,7 +388,7 @@ static void make_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
   pl->wq_bytes = size_t(pl->n_groups) * (R + 1) * pl->FGS * 4;
 }
 
-size_t conv_tc_workspace(int B, int Ho, int Wo, int R, int F);
+size_t conv_tc_workspace(int B, int C, int H, int W, int pad, int KH, int KW, int F);
 size_t conv_walk_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T);
 size_t conv_tct_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T);
 int conv_tct_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
@@ -453,7 +453,7 @@ size_t conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, i
   make_plan(B, C, H, W, pad, F, KH, KW, T, inf, &pl);
   size_t m = pl.wq_bytes;
   if (inf) {  // tensor-core path (and the SIMT dense path for validation mode)
-    size_t t = conv_tc_workspace(B, pl.a.Ho, pl.a.Wo, pl.a.R, F);
+    size_t t = conv_tc_workspace(B, C, H, W, pad, KH, KW, F);
     m = m > t ? m : t;
   } else {
     size_t t = conv_walk_workspace(B, C, H, W, pad, F, KH, KW, T);

@@ -29,13 +29,30 @@ constexpr int kTcThreads = 256;
 struct TcPlan {
   int M, K, Kp, Mt, Kt, nch, Fc, N;  // N = 4 * Fc (multiple of 16, <= 256)
   size_t a_bytes, b_bytes;
+  // A from a shared-memory band of RB output rows (nbands per image) when band = 1; with hwc = 1 the
+  // K order is (ky, kx, c) with channels padded to Cp (a multiple of 16), so every 16-byte core-matrix
+  // row of A is 16 channels of one input pixel: one 16-byte shared-memory load per row.  Otherwise K
+  // is the receptive-field order (c, ky, kx).
+  int band, hwc, Cp, RB, nbands, band_smem;
 };
 
-static TcPlan tc_plan(int B, int Ho, int Wo, int R, int F) {
+static TcPlan tc_plan(int B, int C, int H, int W, int pad, int KH, int KW, int F, int sms) {
   TcPlan p;
+  const int Ho = H + 2 * pad - KH + 1, Wo = W + 2 * pad - KW + 1, Wp = W + 2 * pad;
+  const int R = C * KH * KW;
   p.M = B * Ho * Wo;
-  p.K = R;
-  p.Kp = int(ceil_div(R, kTcKT)) * kTcKT;
+  // bands: the largest band of output rows whose padded input rows fit 48 KB of shared memory; a batch
+  // too small to give every SM two bands keeps the per-row gather kernel (and the (c, ky, kx) order)
+  const int Cp16 = int(ceil_div(C, 16)) * 16;
+  p.RB = Ho;
+  while (p.RB > 1 && int64_t(Cp16) * (p.RB + KH - 1) * Wp > 48 * 1024) p.RB = (p.RB + 1) / 2;
+  p.nbands = int(ceil_div(Ho, p.RB));
+  p.band = int64_t(Cp16) * (p.RB + KH - 1) * Wp <= 48 * 1024 && int64_t(B) * p.nbands >= 2 * sms;
+  p.hwc = p.band && (C % 16 == 0 || (C >= 64 && int64_t(Cp16) * 100 <= int64_t(C) * 104));
+  p.Cp = p.hwc ? Cp16 : C;
+  p.band_smem = int((int64_t(p.Cp) * (p.RB + KH - 1) * Wp + 15) & ~int64_t(15));
+  p.K = p.hwc ? KH * KW * p.Cp : R;
+  p.Kp = int(ceil_div(p.K, kTcKT)) * kTcKT;
   p.Mt = int(ceil_div(p.M, kTcM));
   p.Kt = p.Kp / kTcKT;
   p.nch = int(ceil_div(F, 64));
@@ -46,8 +63,8 @@ static TcPlan tc_plan(int B, int Ho, int Wo, int R, int F) {
   return p;
 }
 
-size_t conv_tc_workspace(int B, int Ho, int Wo, int R, int F) {
-  TcPlan p = tc_plan(B, Ho, Wo, R, F);
+size_t conv_tc_workspace(int B, int C, int H, int W, int pad, int KH, int KW, int F) {
+  TcPlan p = tc_plan(B, C, H, W, pad, KH, KW, F, num_sms());
   return ((p.a_bytes + 1023) & ~size_t(1023)) + p.b_bytes + 1024;
 }
 
@@ -116,8 +133,8 @@ __global__ void tc_prep_a_kernel(const uint8_t* __restrict__ lat_in, int C, int 
 
 // B operand, vectorised: one thread per (chunk, feature, 16 consecutive k): 16 weights -> the four
 // 16-byte limb rows n = 4 f_local + limb of one core-matrix column.
-__global__ void tc_prep_b16_kernel(const float* __restrict__ w, int F, int R, TcPlan p, uint8_t* __restrict__ bq,
-                                   int* err) {
+__global__ void tc_prep_b16_kernel(const float* __restrict__ w, int F, int R, int KK, TcPlan p,
+                                   uint8_t* __restrict__ bq, int* err) {
   const int nk16 = p.Kp / 16;
   const int64_t total = int64_t(p.nch) * p.Fc * nk16;
   int bad = 0;
@@ -127,11 +144,20 @@ __global__ void tc_prep_b16_kernel(const float* __restrict__ w, int F, int R, Tc
     const int fl = int(rest % p.Fc), ch = int(rest / p.Fc);
     const int f = ch * p.Fc + fl, k0 = k16 * 16;
     uint32_t limb[4][4] = {};
-    if (f < F) {
+    if (f < F && k0 < p.K) {
+      // weight index of GEMM column k: (c, ky, kx) order = k itself; (ky, kx, c) order = c * KK + kyx
+      const int kyx = p.hwc ? k0 / p.Cp : 0, c0 = p.hwc ? k0 - kyx * p.Cp : 0;
+      const int C = R / KK;
       for (int j = 0; j < 16; ++j) {
-        const int k = k0 + j;
-        if (k >= R) break;
-        const float x = __ldg(w + int64_t(f) * R + k);
+        int widx;
+        if (p.hwc) {
+          if (c0 + j >= C) break;
+          widx = (c0 + j) * KK + kyx;
+        } else {
+          if (k0 + j >= R) break;
+          widx = k0 + j;
+        }
+        const float x = __ldg(w + int64_t(f) * R + widx);
         const float s = x * 2147483648.0f;
         if (!(x >= 0.0f && x <= 1.0f) || s != truncf(s)) { bad = 1; continue; }
         const uint32_t q = uint32_t(s);
@@ -197,6 +223,53 @@ __global__ void __launch_bounds__(256) tc_prep_a_band_kernel(const uint8_t* __re
       if (++kx == KW) { kx = 0; if (++ky == KH) { ky = 0; ++c; } }
     }
     *reinterpret_cast<uint4*>(aq + tc_off(m0 + mi, k0, kTcM, p.Kt)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+  }
+}
+
+// A operand, (ky, kx, c) order: the band is staged channel-innermost ([RB + KH - 1][W + 2 pad][Cp],
+// binary S[T-1], zero padded), so each core-matrix row (16 channels of one input pixel) is one 16-byte
+// shared-memory load and one 16-byte global store.
+__global__ void __launch_bounds__(256) tc_prep_a_hwc_kernel(const uint8_t* __restrict__ lat_in, int C, int H, int W,
+                                                            int pad, int KH, int KW, int Ho, int Wo, int T, TcPlan p,
+                                                            int B, uint8_t* __restrict__ aq) {
+  extern __shared__ __align__(16) uint8_t hband[];
+  const int Wp = W + 2 * pad, TR = p.RB + KH - 1, Cp = p.Cp, nk16 = p.Kp / 16;
+  if (int(blockIdx.x) == B * p.nbands) {  // padding rows
+    const int pr = p.Mt * kTcM - p.M;
+    for (int64_t i = threadIdx.x; i < int64_t(pr) * nk16; i += blockDim.x) {
+      const int m = p.M + int(i % pr), k16 = int(i / pr);
+      *reinterpret_cast<uint4*>(aq + tc_off(m, k16 * 16, kTcM, p.Kt)) = make_uint4(0, 0, 0, 0);
+    }
+    return;
+  }
+  const int b = blockIdx.x / p.nbands, ya = (blockIdx.x % p.nbands) * p.RB;
+  const int yb = ya + p.RB < Ho ? ya + p.RB : Ho;
+  const uint8_t* lb = lat_in + int64_t(b) * C * H * W;
+  {
+    uint4* b16 = reinterpret_cast<uint4*>(hband);
+    for (int i = threadIdx.x; i < p.band_smem / 16; i += blockDim.x) b16[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const int top = ya - pad;
+    const int iy0 = top > 0 ? top : 0, iy1 = (top + TR - 1 < H - 1 ? top + TR - 1 : H - 1);
+    const int npx = (iy1 - iy0 + 1) * W;
+    for (int i = threadIdx.x; i < C * npx; i += blockDim.x) {  // channel fastest: conflict-free byte stores
+      const int px = i / C, c = i - px * C, ry = px / W, ix = px - ry * W;
+      hband[((iy0 + ry - top) * Wp + ix + pad) * Cp + c] =
+          __ldg(lb + (int64_t(c) * H + iy0 + ry) * W + ix) < T ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  const int mcount = (yb - ya) * Wo, m0 = b * Ho * Wo + ya * Wo;
+  const int kcols = p.K / 16;  // columns >= K / 16 are zero (K = KH KW Cp is a multiple of 16)
+  for (int i = threadIdx.x; i < mcount * nk16; i += blockDim.x) {
+    const int k16 = i / mcount, mi = i - k16 * mcount;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (k16 < kcols) {
+      const int k0 = k16 * 16, kyx = k0 / Cp, c0 = k0 - kyx * Cp, ky = kyx / KW, kx = kyx - ky * KW;
+      const int yl = mi / Wo, x = mi - yl * Wo;
+      v = *reinterpret_cast<const uint4*>(hband + ((yl + ky) * Wp + x + kx) * Cp + c0);
+    }
+    *reinterpret_cast<uint4*>(aq + tc_off(m0 + mi, k16 * 16, kTcM, p.Kt)) = v;
   }
 }
 
@@ -302,12 +375,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
   }
 }
 
-static inline int64_t al16c(int64_t x) { return (x + 15) & ~int64_t(15); }
-
 int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH, int KW,
                    int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes, cudaStream_t s) {
   const int Ho = H + 2 * pad - KH + 1, Wo = W + 2 * pad - KW + 1, R = C * KH * KW;
-  TcPlan p = tc_plan(B, Ho, Wo, R, F);
+  TcPlan p = tc_plan(B, C, H, W, pad, KH, KW, F, num_sms());
   const size_t a_off = 0, b_off = (p.a_bytes + 1023) & ~size_t(1023);
   if (ws_bytes < b_off + p.b_bytes) return set_error(SNN_EWORKSPACE, "snn_conv_fire(tc): workspace too small");
   uint8_t* aq = reinterpret_cast<uint8_t*>(ws) + a_off;
@@ -316,21 +387,16 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
     const int64_t total = int64_t(p.nch) * p.Fc * (p.Kp / 16);
     int64_t blocks = ceil_div(total, 256);
     if (blocks > int64_t(num_sms()) * 8) blocks = int64_t(num_sms()) * 8;
-    tc_prep_b16_kernel<<<int(blocks), 256, 0, s>>>(w, F, R, p, bq, error_word_ptr());
+    tc_prep_b16_kernel<<<int(blocks), 256, 0, s>>>(w, F, R, KH * KW, p, bq, error_word_ptr());
     note_launch();
   }
   {
-    // the largest band of output rows whose padded input rows fit 48 KB of shared memory
-    const int Wp = W + 2 * pad;
-    int RB = Ho;
-    while (RB > 1 && int64_t(C) * (RB + KH - 1) * Wp > 48 * 1024) RB = (RB + 1) / 2;
-    // (a batch too small to give every SM two bands keeps the per-row gather kernel)
-    if (int64_t(C) * (RB + KH - 1) * Wp + 16 <= 48 * 1024 && int64_t(B) * ceil_div(Ho, RB) >= 2 * num_sms()) {
-      const int nbands = int(ceil_div(Ho, RB));
-      const int smem_a = int(al16c(C * (RB + KH - 1) * Wp));
-      const int64_t KS = 1;
-      tc_prep_a_band_kernel<<<unsigned(int64_t(B) * nbands * KS + 1), 256, smem_a, s>>>(
-          lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p, RB, nbands, B, int(KS), aq);
+    if (p.hwc) {
+      tc_prep_a_hwc_kernel<<<unsigned(int64_t(B) * p.nbands + 1), 256, p.band_smem, s>>>(lat_in, C, H, W, pad, KH, KW,
+                                                                                      Ho, Wo, T, p, B, aq);
+    } else if (p.band) {
+      tc_prep_a_band_kernel<<<unsigned(int64_t(B) * p.nbands + 1), 256, p.band_smem, s>>>(
+          lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p, p.RB, p.nbands, B, 1, aq);
     } else {
       const int64_t rows16 = int64_t(p.Mt) * kTcM * (p.Kp / 16);
       int64_t blocks = ceil_div(rows16, 256);
