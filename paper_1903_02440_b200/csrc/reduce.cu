@@ -14,18 +14,21 @@ namespace snn {
 // ------------------------------------------------------------------------------------- a4 pool
 // Earliest spike in the window; the max v among the window entries that spiked at that time
 // (per-time-step max-pooling of the thresholded potentials read at the pooled spike, R12).
+// IDX = uint32_t when the output count fits 32 bits (the index arithmetic is then 32-bit: a 64-bit
+// division per output made this HBM-light kernel instruction-bound), int64_t otherwise.
+template <class IDX>
 __global__ void __launch_bounds__(256) pool_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
                                                    int64_t BF, int H, int W, int PH, int PW, int SH, int SW,
                                                    int DH, int DW, int Ho, int Wo, int vfinal,
                                                    uint8_t* __restrict__ lat_out, float* __restrict__ v_out) {
-  const int64_t total = BF * Ho * Wo;
-  for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < total; o += int64_t(gridDim.x) * blockDim.x) {
-    const int ox = int(o % Wo);
-    const int64_t r = o / Wo;
-    const int oy = int(r % Ho);
-    const int64_t bf = r / Ho;
-    const uint8_t* l = lat + bf * H * W;
-    const float* vv = v ? v + bf * H * W : nullptr;
+  const IDX total = IDX(BF) * IDX(Ho) * IDX(Wo);
+  const IDX HoWo = IDX(Ho) * IDX(Wo), HW = IDX(H) * IDX(W);
+  for (IDX o = IDX(blockIdx.x) * IDX(blockDim.x) + threadIdx.x; o < total; o += IDX(gridDim.x) * blockDim.x) {
+    const IDX bf = o / HoWo;
+    const int rem = int(o - bf * HoWo);
+    const int oy = rem / Wo, ox = rem - oy * Wo;
+    const uint8_t* l = lat + bf * HW;
+    const float* vv = v ? v + bf * HW : nullptr;
     int best = kNoSpike;
     float bv = 0.0f;
     const int y0 = oy * SH - DH, x0 = ox * SW - DW;
@@ -35,9 +38,9 @@ __global__ void __launch_bounds__(256) pool_kernel(const uint8_t* __restrict__ l
       for (int px = 0; px < PW; ++px) {
         const int xx = x0 + px;
         if (xx < 0 || xx >= W) continue;
-        const int li = l[int64_t(yy) * W + xx];
+        const int li = l[yy * W + xx];
         if (li == kNoSpike || (li > best && !vfinal)) continue;
-        const float vi = vv ? vv[int64_t(yy) * W + xx] : 0.0f;
+        const float vi = vv ? vv[yy * W + xx] : 0.0f;
         if (vfinal) {  // SNN_POOL_VFINAL: max over every spiking entry (the pooled potentials at T - 1)
           if (best == kNoSpike || vi > bv) bv = vi;
           if (li < best) best = li;
@@ -47,6 +50,33 @@ __global__ void __launch_bounds__(256) pool_kernel(const uint8_t* __restrict__ l
     }
     lat_out[o] = uint8_t(best);
     if (v_out) v_out[o] = best == kNoSpike ? 0.0f : bv;
+  }
+}
+
+// Latency-only pooling (no v): one thread per output ROW of one plane walks its Wo windows left to
+// right -- no per-output index arithmetic, every input byte of a stride = window layer loaded once
+// (through L1), consecutive threads on consecutive rows.
+__global__ void __launch_bounds__(256) pool_rows_kernel(const uint8_t* __restrict__ lat, uint32_t rows, int H, int W,
+                                                        int PH, int PW, int SH, int SW, int DH, int DW, int Ho,
+                                                        int Wo, uint8_t* __restrict__ lat_out) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    const uint32_t bf = r / uint32_t(Ho);
+    const int oy = int(r - bf * uint32_t(Ho));
+    const uint8_t* l = lat + size_t(bf) * H * W;
+    uint8_t* out = lat_out + size_t(r) * Wo;
+    const int y0 = oy * SH - DH;
+    const int ya = y0 < 0 ? 0 : y0, yb = (y0 + PH < H ? y0 + PH : H);
+    for (int ox = 0; ox < Wo; ++ox) {
+      const int x0 = ox * SW - DW;
+      const int xa = x0 < 0 ? 0 : x0, xb = (x0 + PW < W ? x0 + PW : W);
+      unsigned best = kNoSpike;
+      for (int yy = ya; yy < yb; ++yy)
+        for (int xx = xa; xx < xb; ++xx) {
+          const unsigned li = __ldg(l + yy * W + xx);
+          best = li < best ? li : best;
+        }
+      out[ox] = uint8_t(best);
+    }
   }
 }
 
@@ -60,8 +90,18 @@ int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, 
   if (total == 0) return SNN_OK;
   int64_t blocks = ceil_div(total, 256);
   if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
-  pool_kernel<<<int(blocks), 256, 0, s>>>(lat, v_out ? v : nullptr, int64_t(B) * F, H, W, PH, PW, SH, SW, DH, DW,
-                                          Ho, Wo, (flags & SNN_POOL_VFINAL) ? 1 : 0, lat_out, v_out);
+  const bool small = total < (int64_t(1) << 32) && int64_t(B) * F * H * W < (int64_t(1) << 32);
+  if (small && !v_out) {
+    const uint32_t rows = uint32_t(int64_t(B) * F * Ho);
+    int64_t rb = ceil_div(rows, 256);
+    if (rb > int64_t(num_sms()) * 16) rb = int64_t(num_sms()) * 16;
+    pool_rows_kernel<<<int(rb), 256, 0, s>>>(lat, rows, H, W, PH, PW, SH, SW, DH, DW, Ho, Wo, lat_out);
+  } else if (small)
+    pool_kernel<uint32_t><<<int(blocks), 256, 0, s>>>(lat, v_out ? v : nullptr, int64_t(B) * F, H, W, PH, PW, SH, SW,
+                                                      DH, DW, Ho, Wo, (flags & SNN_POOL_VFINAL) ? 1 : 0, lat_out, v_out);
+  else
+    pool_kernel<int64_t><<<int(blocks), 256, 0, s>>>(lat, v_out ? v : nullptr, int64_t(B) * F, H, W, PH, PW, SH, SW,
+                                                     DH, DW, Ho, Wo, (flags & SNN_POOL_VFINAL) ? 1 : 0, lat_out, v_out);
   note_launch();
   return check_launch("snn_pool");
 }
