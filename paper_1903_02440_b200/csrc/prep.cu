@@ -5,9 +5,9 @@
 // rounded operations (__dmul_rn/__dadd_rn/__fmul_rn, never contracted to FMA), so results are
 // bit-identical to the definitions.
 //
-// All three are HBM/latency-light stencils: one CTA per 8 x 32 output tile of one (image, channel)
-// plane, the input tile plus halo staged once in shared memory (zero padded), the filter taps in
-// shared memory (read as warp broadcasts), one output pixel per thread, coalesced fp32 stores.
+// All three are light stencils: one CTA per output tile of one (image, channel) plane (32 x 32 for the
+// filter bank, 4 outputs per thread; 8 x 32 for the others, one per thread), the input tile plus halo
+// staged once in shared memory (zero padded), filter taps in shared memory (warp broadcasts).
 #include "common.cuh"
 
 namespace snn {
@@ -18,17 +18,21 @@ constexpr int kTH = 8, kTW = 32, kThreads = kTH * kTW;
 // R33: out[b, k] = sum over (dy, dx) in row-major order of img[y + dy - pad, x + dx - pad] * ker[k, dy, dx]
 // in fp64 (zero outside the image), then mode 0 -> r < threshold ? 0 : r; mode 1 -> channel 2k =
 // max(r, 0), channel 2k+1 = max(-r, 0); mode 2 -> max(r, 0); cast to fp32 (round to nearest).
+// One CTA per 32 x 32 output tile; each thread computes 4 horizontally adjacent outputs, so a row of
+// S + 3 image values in registers serves 4 outputs per tap and each tap weight (a shared-memory
+// broadcast) is read once per 4 outputs.  Every output keeps its own (dy, dx) summation order.
+constexpr int kFB = 32, kFBX = 4;
 __global__ void __launch_bounds__(kThreads) filter_bank_kernel(const double* __restrict__ img, int H, int W,
                                                                const double* __restrict__ ker, int K, int S,
                                                                int pad, double thr, int mode, float* __restrict__ out,
                                                                int Ho, int Wo, int tiles_x, int tiles) {
   extern __shared__ double fsm[];
-  const int SW = kTW + S - 1, SH = kTH + S - 1;
+  const int SW = kFB + S - 1, SH = kFB + S - 1;
   double* tile = fsm;
   double* kk = fsm + SH * SW;
   const int64_t b = blockIdx.x / tiles;
   const int t = blockIdx.x % tiles;
-  const int ty0 = (t / tiles_x) * kTH, tx0 = (t % tiles_x) * kTW;
+  const int ty0 = (t / tiles_x) * kFB, tx0 = (t % tiles_x) * kFB;
   const double* im = img + b * H * W;
   for (int i = threadIdx.x; i < SH * SW; i += kThreads) {
     const int yy = ty0 + i / SW - pad, xx = tx0 + i % SW - pad;
@@ -36,26 +40,41 @@ __global__ void __launch_bounds__(kThreads) filter_bank_kernel(const double* __r
   }
   for (int i = threadIdx.x; i < K * S * S; i += kThreads) kk[i] = __ldg(ker + i);
   __syncthreads();
-  const int ly = threadIdx.x / kTW, lx = threadIdx.x % kTW;
+  const int ly = threadIdx.x / (kFB / kFBX), lx = (threadIdx.x % (kFB / kFBX)) * kFBX;
   const int y = ty0 + ly, x = tx0 + lx;
   if (y >= Ho || x >= Wo) return;
   const int Kout = mode == 1 ? 2 * K : K;
   const int64_t HWo = int64_t(Ho) * Wo;
   float* o = out + b * Kout * HWo + int64_t(y) * Wo + x;
+  const int nx = Wo - x < kFBX ? Wo - x : kFBX;
   for (int k = 0; k < K; ++k) {
     const double* kw = kk + k * S * S;
-    double r = 0.0;
+    double r[kFBX] = {0.0, 0.0, 0.0, 0.0};
     for (int dy = 0; dy < S; ++dy) {
       const double* row = tile + (ly + dy) * SW + lx;
-      for (int dx = 0; dx < S; ++dx) r = __dadd_rn(r, __dmul_rn(row[dx], kw[dy * S + dx]));
+      double win[kFBX];
+#pragma unroll
+      for (int i = 0; i < kFBX - 1; ++i) win[i + 1] = row[i];
+      for (int dx = 0; dx < S; ++dx) {
+#pragma unroll
+        for (int i = 0; i < kFBX - 1; ++i) win[i] = win[i + 1];
+        win[kFBX - 1] = row[dx + kFBX - 1];
+        const double wt = kw[dy * S + dx];
+#pragma unroll
+        for (int i = 0; i < kFBX; ++i) r[i] = __dadd_rn(r[i], __dmul_rn(win[i], wt));
+      }
     }
-    if (mode == 0) {
-      o[k * HWo] = __double2float_rn(r < thr ? 0.0 : r);
-    } else if (mode == 1) {
-      o[(2 * k) * HWo] = __double2float_rn(r > 0.0 ? r : 0.0);
-      o[(2 * k + 1) * HWo] = __double2float_rn(-r > 0.0 ? -r : 0.0);
-    } else {
-      o[k * HWo] = __double2float_rn(r > 0.0 ? r : 0.0);
+#pragma unroll
+    for (int i = 0; i < kFBX; ++i) {
+      if (i >= nx) break;
+      if (mode == 0) {
+        o[k * HWo + i] = __double2float_rn(r[i] < thr ? 0.0 : r[i]);
+      } else if (mode == 1) {
+        o[(2 * k) * HWo + i] = __double2float_rn(r[i] > 0.0 ? r[i] : 0.0);
+        o[(2 * k + 1) * HWo + i] = __double2float_rn(-r[i] > 0.0 ? -r[i] : 0.0);
+      } else {
+        o[k * HWo + i] = __double2float_rn(r[i] > 0.0 ? r[i] : 0.0);
+      }
     }
   }
 }
@@ -164,14 +183,23 @@ int launch_tiles(Kern kern, const char* what, int64_t planes, int Ho, int Wo, si
 
 }  // namespace
 
-size_t filter_bank_smem(int K, int S) { return sizeof(double) * (size_t(kTH + S - 1) * (kTW + S - 1) + size_t(K) * S * S); }
+size_t filter_bank_smem(int K, int S) { return sizeof(double) * (size_t(kFB + S - 1) * (kFB + S - 1) + size_t(K) * S * S); }
 size_t stencil_smem(int r, int extra) { return sizeof(float) * (size_t(kTH + 2 * r) * (kTW + 2 * r) + extra); }
 
 int filter_bank_launch(const double* img, int B, int H, int W, const double* ker, int K, int S, int pad, double thr,
                        int mode, float* out, cudaStream_t s) {
   const int Ho = H + 2 * pad - S + 1, Wo = W + 2 * pad - S + 1;
-  return launch_tiles(filter_bank_kernel, "filter_bank", B, Ho, Wo, filter_bank_smem(K, S), s, img, H, W, ker, K, S,
-                      pad, thr, mode, out, Ho, Wo);
+  const int tiles_x = int(ceil_div(Wo, kFB)), tiles = tiles_x * int(ceil_div(Ho, kFB));
+  const int64_t grid = int64_t(B) * tiles;
+  const size_t smem = filter_bank_smem(K, S);
+  if (grid > 0x7fffffff) return set_error(SNN_ESHAPE, "filter_bank: %lld tiles exceed the grid limit", (long long)grid);
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(filter_bank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+    return set_error(SNN_ECUDA, "filter_bank: cannot opt in to %zu B of shared memory", smem);
+  filter_bank_kernel<<<unsigned(grid), kThreads, smem, s>>>(img, H, W, ker, K, S, pad, thr, mode, out, Ho, Wo, tiles_x,
+                                                             tiles);
+  note_launch();
+  return check_launch("filter_bank");
 }
 
 int local_norm_launch(const float* x, int B, int C, int H, int W, int R, double eps, float* out, cudaStream_t s) {
