@@ -255,6 +255,7 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
           best_warps = int(warps > wcap ? wcap : warps);
         }
   }
+  if (getenv("SNN_WALK_NOFUSE")) best = -1;  // tuning experiments: force the presorted schedule
   if (best >= 0) {
     pl->pre = false;
     pl->ppw = cands[best].ppw; pl->fpl = cands[best].fpl;
@@ -288,7 +289,9 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
     // per warp: 2 mbarriers, then two position buffers [header | npre entries]
     const long left = (kWalkSmemLimit - al16(int(wsb))) / pl->nwarps - 16;
     int npre = int(((left / 2 - hdr_bytes) / 4) / kIt) * kIt;
-    if (npre > 256) npre = 256;
+    int npre_cap = 256;
+    if (const char* e = getenv("SNN_WALK_NPRE")) npre_cap = atoi(e) / kIt * kIt;  // tuning experiments
+    if (npre > npre_cap) npre = npre_cap;
     if (npre < kIt) continue;
     a.npre = npre;
     a.buf_bytes = hdr_bytes + npre * 4;
