@@ -53,6 +53,48 @@ __global__ void __launch_bounds__(256) pool_kernel(const uint8_t* __restrict__ l
   }
 }
 
+// 2 x 2 windows, stride 2, no padding, with potentials (C5's pool): one thread per pair of adjacent
+// outputs, each input row read as one 4-byte latency word and one 16-byte potential vector
+// (consecutive threads on consecutive column pairs: coalesced).  Requires W % 4 == 0.
+__device__ __forceinline__ void pool4(uint32_t l0, uint32_t l1, uint32_t l2, uint32_t l3, float v0, float v1,
+                                      float v2, float v3, int vfinal, uint32_t& lo, float& vo) {
+  const uint32_t la[4] = {l0, l1, l2, l3};
+  const float va[4] = {v0, v1, v2, v3};
+  uint32_t best = kNoSpike;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) best = la[j] < best ? la[j] : best;
+  float bv = 0.0f;
+  bool have = false;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool take = la[j] != kNoSpike && (vfinal || la[j] == best);
+    if (take && (!have || va[j] > bv)) { bv = va[j]; have = true; }
+  }
+  lo = best;
+  vo = best == kNoSpike ? 0.0f : bv;
+}
+
+__global__ void __launch_bounds__(256) pool2x2_v_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
+                                                        uint32_t pairs, int H, int W, int Ho, int Wo, int vfinal,
+                                                        uint8_t* __restrict__ lat_out, float* __restrict__ v_out) {
+  const uint32_t Wo2 = uint32_t(Wo) >> 1, per_plane = uint32_t(Ho) * Wo2;
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < pairs; q += gridDim.x * blockDim.x) {
+    const uint32_t bf = q / per_plane, rem = q - bf * per_plane, oy = rem / Wo2, ox2 = rem - oy * Wo2;
+    const uint32_t i0 = bf * uint32_t(H) * W + 2 * oy * W + 4 * ox2;
+    const uint32_t a = __ldg(reinterpret_cast<const uint32_t*>(lat + i0));
+    const uint32_t c = __ldg(reinterpret_cast<const uint32_t*>(lat + i0 + W));
+    const float4 va = __ldg(reinterpret_cast<const float4*>(v + i0));
+    const float4 vc = __ldg(reinterpret_cast<const float4*>(v + i0 + W));
+    uint32_t l0, l1;
+    float o0, o1;
+    pool4(a & 0xFF, (a >> 8) & 0xFF, c & 0xFF, (c >> 8) & 0xFF, va.x, va.y, vc.x, vc.y, vfinal, l0, o0);
+    pool4((a >> 16) & 0xFF, a >> 24, (c >> 16) & 0xFF, c >> 24, va.z, va.w, vc.z, vc.w, vfinal, l1, o1);
+    const uint32_t o = bf * per_plane * 2 + oy * uint32_t(Wo) + 2 * ox2;
+    *reinterpret_cast<uint16_t*>(lat_out + o) = uint16_t(l0 | (l1 << 8));
+    *reinterpret_cast<float2*>(v_out + o) = make_float2(o0, o1);
+  }
+}
+
 // Latency-only pooling (no v): one thread per output ROW of one plane walks its Wo windows left to
 // right -- no per-output index arithmetic, every input byte of a stride = window layer loaded once
 // (through L1), consecutive threads on consecutive rows.
@@ -91,7 +133,14 @@ int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, 
   int64_t blocks = ceil_div(total, 256);
   if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
   const bool small = total < (int64_t(1) << 32) && int64_t(B) * F * H * W < (int64_t(1) << 32);
-  if (small && !v_out) {
+  if (small && v_out && PH == 2 && PW == 2 && SH == 2 && SW == 2 && DH == 0 && DW == 0 && W % 4 == 0 &&
+      H % 2 == 0 && Wo % 2 == 0) {
+    const uint32_t pairs = uint32_t(total / 2);
+    int64_t pb = ceil_div(pairs, 256);
+    if (pb > int64_t(num_sms()) * 16) pb = int64_t(num_sms()) * 16;
+    pool2x2_v_kernel<<<int(pb), 256, 0, s>>>(lat, v, pairs, H, W, Ho, Wo, (flags & SNN_POOL_VFINAL) ? 1 : 0, lat_out,
+                                              v_out);
+  } else if (small && !v_out) {
     const uint32_t rows = uint32_t(int64_t(B) * F * Ho);
     int64_t rb = ceil_div(rows, 256);
     if (rb > int64_t(num_sms()) * 16) rb = int64_t(num_sms()) * 16;
@@ -107,26 +156,45 @@ int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, 
 }
 
 // ------------------------------------------------------------------------------------- a5 inhibit
+// Large maps: one thread per position, 8 features' loads in flight at a time (the v load only where
+// the neuron spiked), then the write-back from the winning key alone (lat and v are recovered exactly
+// from it, so nothing is read twice).  IDX = uint32_t when B*F*H*W < 2^32.
+__device__ __forceinline__ float key_v(uint64_t key) {  // inverse of ordered_bits on the key's v field
+  const uint32_t o = ~uint32_t(key >> 24);
+  return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
+}
+
+template <class IDX>
 __global__ void __launch_bounds__(256) inhibit_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
-                                                      int B, int F, int64_t HW, uint8_t* __restrict__ lat_out,
+                                                      int B, int F, int64_t HW64, uint8_t* __restrict__ lat_out,
                                                       float* __restrict__ v_out, int16_t* __restrict__ winner_f) {
-  const int64_t total = int64_t(B) * HW;
-  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < total; q += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t b = q / HW, p = q - b * HW;
-    const int64_t base = b * F * HW + p;
+  const IDX HW = IDX(HW64), total = IDX(B) * HW;
+  for (IDX q = IDX(blockIdx.x) * blockDim.x + threadIdx.x; q < total; q += IDX(gridDim.x) * blockDim.x) {
+    const IDX b = q / HW, p = q - b * HW;
+    const IDX base = b * IDX(F) * HW + p;
     uint64_t best = ~uint64_t(0);
-    for (int f = 0; f < F; ++f) {
-      const uint8_t l = lat[base + int64_t(f) * HW];
-      if (l == kNoSpike) continue;
-      const uint64_t k = wta_key(l, v[base + int64_t(f) * HW], uint32_t(f));
-      best = k < best ? k : best;
+    for (int f0 = 0; f0 < F; f0 += 8) {
+      uint32_t l[8];
+      float vv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) l[j] = f0 + j < F ? lat[base + IDX(f0 + j) * HW] : kNoSpike;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) vv[j] = l[j] != kNoSpike ? v[base + IDX(f0 + j) * HW] : 0.0f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (l[j] != kNoSpike) {
+          const uint64_t k = wta_key(uint8_t(l[j]), vv[j], uint32_t(f0 + j));
+          best = k < best ? k : best;
+        }
     }
-    const int fw = best == ~uint64_t(0) ? -1 : int(best & 0xFFFFFFu);
+    const bool any = best != ~uint64_t(0);
+    const int fw = any ? int(best & 0xFFFFFFu) : -1;
+    const uint8_t lw = any ? uint8_t(best >> 56) : kNoSpike;
+    const float vw = any ? key_v(best) : 0.0f;
     for (int f = 0; f < F; ++f) {
-      const int64_t i = base + int64_t(f) * HW;
-      const bool keep = f == fw;
-      lat_out[i] = keep ? lat[i] : kNoSpike;
-      v_out[i] = keep ? v[i] : 0.0f;
+      const IDX i = base + IDX(f) * HW;
+      lat_out[i] = f == fw ? lw : kNoSpike;
+      v_out[i] = f == fw ? vw : 0.0f;
     }
     if (winner_f) winner_f[q] = int16_t(fw);
   }
@@ -204,7 +272,10 @@ int inhibit_launch(const uint8_t* lat, const float* v, int B, int F, int H, int 
   }
   int64_t blocks = ceil_div(total, 256);
   if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
-  inhibit_kernel<<<int(blocks), 256, 0, s>>>(lat, v, B, F, HW, lat_out, v_out, winner_f);
+  if (int64_t(B) * F * HW < (int64_t(1) << 32))
+    inhibit_kernel<uint32_t><<<int(blocks), 256, 0, s>>>(lat, v, B, F, HW, lat_out, v_out, winner_f);
+  else
+    inhibit_kernel<int64_t><<<int(blocks), 256, 0, s>>>(lat, v, B, F, HW, lat_out, v_out, winner_f);
   note_launch();
   return check_launch("snn_inhibit");
 }
