@@ -192,7 +192,7 @@ __device__ __forceinline__ void rf_tables(const WalkArgs& a, unsigned char* tabs
 }
 
 // ------------------------------------------------------------------------------------- walk
-template <int FPL, bool PRE> struct WalkThreads { static constexpr int v = FPL == 4 ? (PRE ? 640 : 768) : 1024; };
+template <int FPL, bool PRE> struct WalkThreads { static constexpr int v = FPL == 4 ? 768 : 1024; };
 
 // Fire every unfired feature whose potential at the end of bucket t exceeds the threshold.
 template <int FPL>
