@@ -57,6 +57,19 @@ __device__ __forceinline__ void wgather(const unsigned char* p, uint32_t (&o)[FP
   else { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
 }
 
+// The same gather from a 32-bit shared-window address (lane base + row offset): one LDS, no generic
+// address arithmetic.  The weights do not change during a walk, so the load needs no ordering.
+template <int FPL>
+__device__ __forceinline__ void wgather_s(uint32_t a, uint32_t (&o)[FPL]) {
+  if constexpr (FPL == 1) {
+    asm("ld.shared.u32 %0, [%1];" : "=r"(o[0]) : "r"(a));
+  } else if constexpr (FPL == 2) {
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(o[0]), "=r"(o[1]) : "r"(a));
+  } else {
+    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]) : "r"(a));
+  }
+}
+
 __device__ __forceinline__ uint8_t rf_lat(const WalkArgs& a, const int32_t* eoff, const uint16_t* ekk,
                                           const uint8_t* in, bool interior, int y0, int x0, int e) {
   if (interior) return in[eoff[e]];
@@ -216,13 +229,13 @@ __device__ __forceinline__ void fire_at(const uint64_t (&acc)[FPL], int64_t thr,
 // pair by pair from the same registers and tests at every bucket end (K3).  Lanes decide
 // independently (no vote): the group's bookkeeping does not depend on the branch taken.
 template <int FPL>
-__device__ __forceinline__ void walk_block(const unsigned char* wl, const uint4& e0, const uint4& e1, unsigned endm,
+__device__ __forceinline__ void walk_block(uint32_t wls, const uint4& e0, const uint4& e1, unsigned endm,
                                            uint32_t tpk, int64_t thr, uint64_t (&acc)[FPL], unsigned& fired,
                                            uint32_t& lo, float (&vo)[FPL]) {
   const uint32_t off[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
   uint32_t wv[8][FPL];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) wgather<FPL>(wl + off[k], wv[k]);
+  for (int k = 0; k < 8; ++k) wgather_s<FPL>(wls + off[k], wv[k]);
   uint64_t s[FPL];
   bool hit = false;
 #pragma unroll
@@ -257,6 +270,8 @@ __device__ __forceinline__ void walk_list(const WalkArgs& a, const unsigned char
   constexpr unsigned kAll = (1u << FPL) - 1;
   const int T = a.T;
   const int64_t thr = a.thr;
+  uint32_t wls;  // the lane's weight base as a shared-window address, opaque so it stays in a register
+  asm volatile("mov.u32 %0, %1;" : "=r"(wls) : "r"(smem_u32(wl)));
     uint64_t acc[FPL];
     lo = 0xFFFFFFFFu;  // byte j = lat of feature j (255 = no spike)
 #pragma unroll
@@ -310,7 +325,7 @@ __device__ __forceinline__ void walk_list(const WalkArgs& a, const unsigned char
             while (t < T && int(start[t + 1]) == bend) ++t;  // empty buckets add nothing
             bend = t < T ? int(start[t + 1]) : 0x7FFFFFFF;
           }
-          walk_block<FPL>(wl, cur[2 * h], cur[2 * h + 1], endm, tpk, thr, acc, fired, lo, vo);
+          walk_block<FPL>(wls, cur[2 * h], cur[2 * h + 1], endm, tpk, thr, acc, fired, lo, vo);
         }
         const unsigned nf = __ballot_sync(0xffffffffu, !done && fired != kAll);
         if (!done && ((nf & gmask) == 0 || i >= total)) done = true;
