@@ -277,7 +277,10 @@ __device__ __forceinline__ uint64_t sm_key(uint32_t vk, int i) { return (uint64_
 
 __global__ void __launch_bounds__(kSmThreads) enc_small_kernel(const float* __restrict__ x, int n, int T, int bins,
                                                                 uint8_t* __restrict__ lat) {
-  extern __shared__ uint32_t vk[];              // [n] 0x7FFFFFFF - bits(x), or ~0 for x <= 0
+  extern __shared__ uint32_t vk[];              // [n] 0x7FFFFFFF - bits(x), or ~0 for x <= 0; then [n] u16 candidates
+  uint16_t* cand = reinterpret_cast<uint16_t*>(vk + n);
+  __shared__ uint8_t bin_lat[4096];             // level-0 bin -> latency of its elements, 0xFF = a cut inside
+  __shared__ int s_ncand;
   __shared__ uint32_t hist[4096];               // level 0: 4096 bins; later: slot * 256 + digit
   __shared__ uint32_t slot_tot[16];
   __shared__ uint64_t cut_prefix[256], slot_prefix[256];
@@ -344,6 +347,32 @@ __global__ void __launch_bounds__(kSmThreads) enc_small_kernel(const float* __re
     else { cut_shift[c] = -2; cut_slot[c] = -3; }
   }
   __syncthreads();
+  // ---- per-bin latencies: an element of a level-0 bin without a cut passes exactly the cuts of the
+  // lower bins; only elements of bins holding a cut (the candidates) take part in the finer levels ----
+  for (int d = tid; d < 4096; d += kSmThreads) {
+    int lo = 0, hi = NC;  // cuts with digit < d (empty cuts, never passed, count as digit +inf)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const int dm = cut_shift[mid] == -1 ? 4096 : int(cut_prefix[mid]);
+      if (dm < d) lo = mid + 1; else hi = mid;
+    }
+    const bool inside = lo < NC && cut_shift[lo] != -1 && int(cut_prefix[lo]) == d;
+    bin_lat[d] = inside ? uint8_t(0xFF) : uint8_t(lo);
+  }
+  if (tid == 0) s_ncand = 0;
+  __syncthreads();
+  for (int i0 = 0; i0 < n; i0 += kSmThreads) {  // warp-uniform trip count (the ballot needs every lane)
+    const int i = i0 + tid;
+    const uint32_t k32 = i < n ? vk[i] : 0xFFFFFFFFu;
+    const bool c = k32 != 0xFFFFFFFFu && bin_lat[uint32_t(sm_key(k32, i) >> 43)] == 0xFF;
+    const unsigned m = __ballot_sync(0xffffffffu, c);  // warp-aggregated append
+    int base = 0;
+    if ((tid & 31) == 0 && m) base = atomicAdd(&s_ncand, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (c) cand[base + __popc(m & ((1u << (tid & 31)) - 1u))] = uint16_t(i);
+  }
+  __syncthreads();
+  const int ncand = s_ncand;
   // ---- levels 1..6 (a level is repeated while more than 16 distinct prefixes are pending) ----
   for (int L = 1; L < kSmLevels;) {
     if (tid == 0) {  // distinct prefixes of unresolved cuts (sorted, since cuts are in rank order)
@@ -363,9 +392,9 @@ __global__ void __launch_bounds__(kSmThreads) enc_small_kernel(const float* __re
     __syncthreads();
     const int shp = c_sm_shift[L - 1], sh = c_sm_shift[L];
     const uint32_t mask = (1u << c_sm_bits[L]) - 1u;
-    for (int i = tid; i < n; i += kSmThreads) {
+    for (int j = tid; j < ncand; j += kSmThreads) {
+      const int i = cand[j];
       const uint32_t k32 = vk[i];
-      if (k32 == 0xFFFFFFFFu) continue;
       const uint64_t K = sm_key(k32, i), pfx = K >> shp;
       int lo = 0, hi = nsl;
       while (lo < hi) { const int mid = (lo + hi) >> 1; if (slot_prefix[mid] < pfx) lo = mid + 1; else hi = mid; }
@@ -415,6 +444,8 @@ __global__ void __launch_bounds__(kSmThreads) enc_small_kernel(const float* __re
     const uint32_t k32 = vk[i];
     if (k32 == 0xFFFFFFFFu) { lb[i] = kNoSpike; continue; }
     const uint64_t K = sm_key(k32, i);
+    const int bl = bin_lat[uint32_t(K >> 43)];
+    if (bl != 0xFF) { lb[i] = bl >= T ? kNoSpike : uint8_t(bl); continue; }
     int lo = 0, hi = NC;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
@@ -430,7 +461,7 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, u
   int64_t n = int64_t(C) * H * W;
   if (B == 0 || n == 0) return SNN_OK;
   if (n <= 16384) {
-    const size_t smem = size_t(n) * sizeof(uint32_t);
+    const size_t smem = size_t(n) * (sizeof(uint32_t) + sizeof(uint16_t)) + 16;
     cudaError_t e = cudaFuncSetAttribute(enc_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_encode: %s", cudaGetErrorString(e));
     enc_small_kernel<<<B, kSmThreads, smem, s>>>(x, int(n), T, bins, lat);
