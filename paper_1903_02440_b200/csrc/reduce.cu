@@ -140,7 +140,7 @@ int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, 
     if (pb > int64_t(num_sms()) * 16) pb = int64_t(num_sms()) * 16;
     pool2x2_v_kernel<<<int(pb), 256, 0, s>>>(lat, v, pairs, H, W, Ho, Wo, (flags & SNN_POOL_VFINAL) ? 1 : 0, lat_out,
                                               v_out);
-  } else if (small && !v_out) {
+  } else if (small && !v_out && PH * PW <= 16) {  // small windows: one thread per output row
     const uint32_t rows = uint32_t(int64_t(B) * F * Ho);
     int64_t rb = ceil_div(rows, 256);
     if (rb > int64_t(num_sms()) * 16) rb = int64_t(num_sms()) * 16;
