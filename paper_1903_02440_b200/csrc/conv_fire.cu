@@ -389,6 +389,7 @@ static void make_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
 }
 
 size_t conv_tc_workspace(int B, int C, int H, int W, int pad, int KH, int KW, int F);
+int conv_tc_launches(int B, int C, int H, int W, int pad, int KH, int KW, int F);
 size_t conv_walk_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T);
 size_t conv_tct_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T);
 int conv_tct_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
@@ -421,7 +422,7 @@ int conv_fire_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW, i
                    int* launches, int* chunks) {
   const bool inf = isinf(theta) && theta > 0;
   *chunks = 1;
-  if (inf) { *path = 2; *launches = 3; return SNN_OK; }
+  if (inf) { *path = 2; *launches = conv_tc_launches(B, C, H, W, pad, KH, KW, F); return SNN_OK; }
   const int ov = conv_path_override();
   if (ov == 0 && conv_tct_applies(B, C, H, W, pad, F, KH, KW, T, theta)) { *path = 3; *launches = 2; return SNN_OK; }
   int pre = 0, ch = 1;

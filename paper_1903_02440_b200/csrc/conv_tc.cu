@@ -34,6 +34,11 @@ struct TcPlan {
   // row of A is 16 channels of one input pixel: one 16-byte shared-memory load per row.  Otherwise K
   // is the receptive-field order (c, ky, kx).
   int band, hwc, Cp, RB, nbands, band_smem;
+  // split-K for grids too small to fill the GPU (C4's one-image layer: 2 x 2 tiles): KS CTAs share an
+  // output tile, each adds its exact integer partial sums into part[M][F] (int64, atomics; integer
+  // addition is order-free, so the result stays exact) and a finalize kernel writes (lat, v)
+  int KS;
+  size_t part_bytes;
 };
 
 static TcPlan tc_plan(int B, int C, int H, int W, int pad, int KH, int KW, int F, int sms) {
@@ -60,12 +65,23 @@ static TcPlan tc_plan(int B, int C, int H, int W, int pad, int KH, int KW, int F
   p.N = 4 * p.Fc;
   p.a_bytes = size_t(p.Mt) * p.Kt * kTcM * kTcKT;
   p.b_bytes = size_t(p.nch) * p.Kt * p.N * kTcKT;
+  const int tiles = p.Mt * p.nch;
+  p.KS = 1;
+  if (tiles * 2 < sms) {  // at least 4 K tiles per slice (pipeline depth, atomic traffic)
+    p.KS = sms / tiles < p.Kt / 4 ? sms / tiles : p.Kt / 4;
+    if (p.KS < 1) p.KS = 1;
+  }
+  p.part_bytes = p.KS > 1 ? size_t(p.M) * F * sizeof(int64_t) : 0;
   return p;
+}
+
+int conv_tc_launches(int B, int C, int H, int W, int pad, int KH, int KW, int F) {
+  return tc_plan(B, C, H, W, pad, KH, KW, F, num_sms()).KS > 1 ? 4 : 3;  // prep B, prep A, GEMM (+ finalize)
 }
 
 size_t conv_tc_workspace(int B, int C, int H, int W, int pad, int KH, int KW, int F) {
   TcPlan p = tc_plan(B, C, H, W, pad, KH, KW, F, num_sms());
-  return ((p.a_bytes + 1023) & ~size_t(1023)) + p.b_bytes + 1024;
+  return ((p.a_bytes + 1023) & ~size_t(1023)) + ((p.b_bytes + 1023) & ~size_t(1023)) + p.part_bytes + 1024;
 }
 
 // byte offset of element (row, k) inside a [row tiles][K tiles] blocked core-matrix array
@@ -278,14 +294,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
                                                                  const uint8_t* __restrict__ bq, TcPlan p, int F,
                                                                  int HoWo, int T, uint32_t tmem_cols,
                                                                  uint8_t* __restrict__ lat_out,
-                                                                 float* __restrict__ v_out) {
+                                                                 float* __restrict__ v_out,
+                                                                 unsigned long long* __restrict__ part) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t a_bytes = kTcM * kTcKT, b_bytes = uint32_t(p.N) * kTcKT, stage_bytes = a_bytes + b_bytes;
   __shared__ __align__(8) uint64_t full_bar[kTcStages], empty_bar[kTcStages], done_bar;
   __shared__ uint32_t tmem_base_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ch = int(blockIdx.x % unsigned(p.nch)), mt = int(blockIdx.x / unsigned(p.nch));  // chunks fastest
+  const int ksi = int(blockIdx.x % unsigned(p.KS)), tile = int(blockIdx.x / unsigned(p.KS));  // K slices fastest
+  const int ch = tile % p.nch, mt = tile / p.nch;  // then feature chunks
+  const int kt0 = int(int64_t(ksi) * p.Kt / p.KS), kt1 = int(int64_t(ksi + 1) * p.Kt / p.KS);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTcStages; ++s) {
@@ -310,9 +329,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
     // ---------------- producer: two bulk copies per stage ----------------
     const uint8_t* a_src = aq + size_t(mt) * p.Kt * a_bytes;
     const uint8_t* b_src = bq + size_t(ch) * p.Kt * b_bytes;
-    for (int kt = 0; kt < p.Kt; ++kt) {
-      const int s = kt % kTcStages, u = kt / kTcStages;
-      if (kt >= kTcStages) mbar_wait(smem_u32(&empty_bar[s]), (u - 1) & 1);
+    for (int kt = kt0; kt < kt1; ++kt) {
+      const int s = (kt - kt0) % kTcStages, u = (kt - kt0) / kTcStages;
+      if (kt - kt0 >= kTcStages) mbar_wait(smem_u32(&empty_bar[s]), (u - 1) & 1);
       const uint32_t fb = smem_u32(&full_bar[s]);
       mbar_expect_tx(fb, stage_bytes);
       const uint32_t dst = smem_u32(smem + size_t(s) * stage_bytes);
@@ -325,8 +344,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
                            | (0u << 7) | (0u << 10)        // A, B: unsigned 8-bit
                            | (uint32_t(p.N >> 3) << 17)    // N
                            | (uint32_t(kTcM >> 4) << 24);  // M = 128
-    for (int kt = 0; kt < p.Kt; ++kt) {
-      const int s = kt % kTcStages, u = kt / kTcStages;
+    for (int kt = kt0; kt < kt1; ++kt) {
+      const int s = (kt - kt0) % kTcStages, u = (kt - kt0) / kTcStages;
       mbar_wait(smem_u32(&full_bar[s]), u & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t a_base = smem_u32(smem + size_t(s) * stage_bytes);
@@ -335,7 +354,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
       for (int ks = 0; ks < kTcKT / 32; ++ks) {  // K = 32 bytes per tcgen05.mma (kind::i8)
         const uint64_t da = umma_desc(a_base + ks * 256, 128, 1024);
         const uint64_t db = umma_desc(b_base + ks * 256, 128, 1024);
-        umma_i8(tmem_base, da, db, idesc, (kt | ks) != 0);
+        umma_i8(tmem_base, da, db, idesc, ((kt - kt0) | ks) != 0);
       }
       umma_commit(smem_u32(&empty_bar[s]));  // frees the stage once these MMAs have read it
     }
@@ -359,6 +378,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
           if (f < F) {
             const int64_t acc = int64_t(v[4 * j]) + (int64_t(v[4 * j + 1]) << 8) + (int64_t(v[4 * j + 2]) << 16) +
                                 (int64_t(v[4 * j + 3]) << 24);
+            if (part) {  // split-K: exact partial sum of this K slice
+              atomicAdd(part + int64_t(m) * F + f, (unsigned long long)acc);
+              continue;
+            }
             const int64_t o = (int64_t(b) * F + f) * HoWo + rem;
             lat_out[o] = acc > 0 ? uint8_t(T - 1) : kNoSpike;
             v_out[o] = fixed_to_float(acc);
@@ -375,12 +398,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
   }
 }
 
+// split-K finalize: the summed fixed-point potentials -> (lat, v) (Eq. 5).
+__global__ void conv_tc_finalize_kernel(const unsigned long long* __restrict__ part, int M, int F, int HoWo, int T,
+                                        uint8_t* __restrict__ lat_out, float* __restrict__ v_out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < int64_t(M) * F;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int m = int(i / F), f = int(i - int64_t(m) * F);
+    const int b = m / HoWo, rem = m - b * HoWo;
+    const int64_t acc = int64_t(part[i]);
+    const int64_t o = (int64_t(b) * F + f) * HoWo + rem;
+    lat_out[o] = acc > 0 ? uint8_t(T - 1) : kNoSpike;
+    v_out[o] = fixed_to_float(acc);
+  }
+}
+
 int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH, int KW,
                    int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes, cudaStream_t s) {
   const int Ho = H + 2 * pad - KH + 1, Wo = W + 2 * pad - KW + 1, R = C * KH * KW;
   TcPlan p = tc_plan(B, C, H, W, pad, KH, KW, F, num_sms());
   const size_t a_off = 0, b_off = (p.a_bytes + 1023) & ~size_t(1023);
-  if (ws_bytes < b_off + p.b_bytes) return set_error(SNN_EWORKSPACE, "snn_conv_fire(tc): workspace too small");
+  const size_t part_off = b_off + ((p.b_bytes + 1023) & ~size_t(1023));
+  if (ws_bytes < part_off + p.part_bytes) return set_error(SNN_EWORKSPACE, "snn_conv_fire(tc): workspace too small");
+  unsigned long long* part =
+      p.KS > 1 ? reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(ws) + part_off) : nullptr;
+  if (part && cudaMemsetAsync(part, 0, p.part_bytes, s) != cudaSuccess) return check_launch("snn_conv_fire(tc) memset");
   uint8_t* aq = reinterpret_cast<uint8_t*>(ws) + a_off;
   uint8_t* bq = reinterpret_cast<uint8_t*>(ws) + b_off;
   {
@@ -410,8 +451,16 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
   const int smem = kTcStages * (kTcM * kTcKT + p.N * kTcKT) + 1024;
   cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_conv_fire(tc): %s", cudaGetErrorString(e));
-  conv_tc_kernel<<<unsigned(int64_t(p.Mt) * p.nch), kTcThreads, smem, s>>>(aq, bq, p, F, Ho * Wo, T, cols, lat_out, v_out);
+  conv_tc_kernel<<<unsigned(int64_t(p.Mt) * p.nch * p.KS), kTcThreads, smem, s>>>(aq, bq, p, F, Ho * Wo, T, cols,
+                                                                               lat_out, v_out, part);
   note_launch();
+  if (part) {
+    const int64_t n = int64_t(p.M) * F;
+    int blocks = int(ceil_div(n, 256));
+    if (blocks > num_sms() * 8) blocks = num_sms() * 8;
+    conv_tc_finalize_kernel<<<blocks, 256, 0, s>>>(part, p.M, F, Ho * Wo, T, lat_out, v_out);
+    note_launch();
+  }
   return check_launch("snn_conv_fire(tc)");
 }
 

@@ -1,5 +1,5 @@
 // stdp.cu -- a7: STDP / R-STDP weight update of one image, in place (Eq. 4, P:161;
-// DESIGN.md R17-R23).  One CTA per winner slot, one thread per synapse of the winner's kernel:
+// DESIGN.md R17-R23).  One CTA per (winner slot, slice of 256 synapses), one thread per synapse:
 // a gather of the winner's receptive field (pre spike times) and an elementwise fp32 update.
 // The winners of k-WTA have distinct features, so their kernels are disjoint (no write races).
 // Arithmetic is fp32 round-to-nearest with explicit intrinsics so no FMA is contracted:
@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(256) stdp_kernel(float* __restrict__ w, int C,
                                                    const int32_t* __restrict__ count, float a_plus, float a_minus,
                                                    float lb, float ub, int stabilizer,
                                                    const float* __restrict__ reward, int f0, int Floc) {
-  const int i = blockIdx.x;
+  const int i = blockIdx.x;  // winner slot; blockIdx.y = slice of its synapses (gridDim.y slices)
   if (i >= count[0]) return;
   if (winners[i * 3] < f0 || winners[i * 3] >= f0 + Floc) return;  // another rank's feature (f4 sharding)
   float rw = reward ? reward[0] : 1.0f;
@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(256) stdp_kernel(float* __restrict__ w, int C,
   const int post = lat_out[(int64_t(f) * Ho + y) * Wo + x];
   const int KK = KH * KW, R = C * KK;
   float* wf = w + int64_t(f) * R;
-  for (int e = threadIdx.x; e < R; e += blockDim.x) {
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < R; e += gridDim.y * blockDim.x) {
     const int c = e / KK, rr = e - c * KK, ky = rr / KW, kx = rr - ky * KW;
     const int yy = y + ky - pad, xx = x + kx - pad;
     int pre = kNoSpike;
@@ -52,7 +52,12 @@ int stdp_launch(float* w, int F, int C, int KH, int KW, const uint8_t* lat_in, i
                 float a_plus, float a_minus, float lb, float ub, int stabilizer, const float* reward,
                 int f0, cudaStream_t s) {
   if (k == 0) return SNN_OK;
-  stdp_kernel<<<k, 256, 0, s>>>(w, C, KH, KW, lat_in, H, W, pad, lat_out, Ho, Wo, winners, count, a_plus, a_minus,
+  // one CTA per (winner, slice of 256 synapses): a large kernel (C4: 5,780 synapses) is updated by many
+  // SMs at once instead of one CTA looping over it
+  const int R = C * KH * KW;
+  int slices = int(ceil_div(R, 256));
+  if (slices > 64) slices = 64;
+  stdp_kernel<<<dim3(k, slices), 256, 0, s>>>(w, C, KH, KW, lat_in, H, W, pad, lat_out, Ho, Wo, winners, count, a_plus, a_minus,
                                 lb, ub, stabilizer, reward, f0, F);
   note_launch();
   return check_launch("snn_stdp_update");
