@@ -249,3 +249,31 @@ def test_decide_vs_oracle(G, orc):
     exp = [orc.decide(win[b], cnt[b], 100, 2, int(lab[b])) for b in range(3)]
     assert host(d).tolist() == [e[0] for e in exp]
     assert host(rw).tolist() == [float(e[1]) for e in exp]
+
+
+@pytest.mark.parametrize("shape", [(2, 3, 16, 24), (1, 2, 8, 4), (3, 5, 36, 40), (2, 4, 6, 12)])
+@pytest.mark.parametrize("flags", [0, 2])
+def test_pool_2x2_vector_path(G, orc, shape, flags):
+    """2 x 2 / stride 2 pooling with potentials on W % 4 == 0 maps (the vectorised pair kernel), with
+    latency ties inside windows, plain (R12) and final-potential (SNN_POOL_VFINAL) readings."""
+    rng = np.random.default_rng(sum(shape) + flags)
+    lat = rng.integers(0, 4, shape).astype(np.uint8)
+    lat[rng.random(shape) < 0.4] = NS
+    v = (rng.integers(1, 9, shape) / 8).astype(np.float32)
+    gl, gv = G.pool(cu(lat), cu(v), 2, 2, 0, flags=flags)
+    ol, ov = orc.pool(lat, v, 2, 2, 2, 2, 0, 0, T=4, vfinal=bool(flags & 2))
+    assert np.array_equal(host(gl), ol) and np.array_equal(host(gv), ov)
+
+
+@pytest.mark.parametrize("B,C,H,W,F,K,pad", [(1, 20, 25, 40, 100, 17, 0), (2, 64, 12, 12, 70, 5, 2)])
+def test_conv_inf_split_k(G, orc, B, C, H, W, F, K, pad):
+    """theta = inf on a grid too small to fill the GPU: the split-K GEMM (exact int64 partial sums)."""
+    plan = G.conv_fire_plan(B, C, H, W, pad, F, K, K, 30, float("inf"))
+    assert plan["launches"] == 4, plan  # prep B, prep A, split GEMM, finalize
+    rng = np.random.default_rng(B + C)
+    lat = rng.integers(0, 30, (B, C, H, W)).astype(np.uint8)
+    lat[rng.random(lat.shape) < 0.5] = NS
+    w = exact_weights(rng, (F, C, K, K))
+    gl, gv = G.conv_fire(cu(lat), cu(w), pad, 30, float("inf"))
+    ol, ov = orc.conv_fire(lat, w, pad, 30, float("inf"))
+    assert np.array_equal(host(gl), ol) and np.array_equal(host(gv), ov)
