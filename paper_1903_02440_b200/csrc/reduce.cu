@@ -522,12 +522,69 @@ size_t k_winners_workspace(int B, int F, int H, int W) {
   return size_t(B) * H * W * sizeof(uint64_t) * per + 256;
 }
 
+// k = 1 (C2's decision layer, C4's R-STDP winner): the single winner is the minimum key over every
+// neuron of the image -- a plain reduction, spread over cpi CTAs per image for large maps (each writes
+// its block minimum to the workspace), then one thread per image reduces them and decodes (f, y, x).
+__global__ void __launch_bounds__(256) kwta_k1_min_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
+                                                          int n, int cpi, uint64_t* __restrict__ part_min) {
+  __shared__ uint64_t red[8];
+  const int b = blockIdx.x / cpi, part = blockIdx.x - b * cpi;
+  const uint8_t* lb = lat + int64_t(b) * n;
+  const float* vb = v + int64_t(b) * n;
+  uint64_t m = ~uint64_t(0);
+  for (int i = part * 256 + threadIdx.x; i < n; i += cpi * 256) {
+    const uint8_t l = lb[i];
+    if (l != kNoSpike) {
+      const uint64_t k = wta_key(l, vb[i], uint32_t(i));  // i = f * H * W + p: the R14 flat index
+      m = k < m ? k : m;
+    }
+  }
+  m = warp_min_u64(m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < 8 ? red[threadIdx.x] : ~uint64_t(0);
+    m = warp_min_u64(m);
+    if (threadIdx.x == 0) part_min[blockIdx.x] = m;
+  }
+}
+
+__global__ void kwta_k1_emit_kernel(const uint64_t* __restrict__ part_min, int B, int cpi, int HW, int W,
+                                    int32_t* __restrict__ winners, int32_t* __restrict__ count) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  uint64_t m = ~uint64_t(0);
+  for (int c = 0; c < cpi; ++c) {
+    const uint64_t x = part_min[int64_t(b) * cpi + c];
+    m = x < m ? x : m;
+  }
+  if (m == ~uint64_t(0)) {
+    winners[b * 3 + 0] = -1; winners[b * 3 + 1] = -1; winners[b * 3 + 2] = -1;
+    count[b] = 0;
+    return;
+  }
+  const int idx = int(m & 0xFFFFFFu), f = idx / HW, p = idx - f * HW;
+  winners[b * 3 + 0] = f; winners[b * 3 + 1] = p / W; winners[b * 3 + 2] = p - (p / W) * W;
+  count[b] = 1;
+}
+
 int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, int k, int r, int32_t* winners,
                      int32_t* count, void* ws, size_t ws_bytes, cudaStream_t s) {
   if (B == 0) return SNN_OK;
   const int64_t HW = int64_t(H) * W;
-  if (ws_bytes < size_t(B) * HW * sizeof(uint64_t))
+  if (ws_bytes < size_t(B) * HW * sizeof(uint64_t) || ws_bytes < size_t(B) * sizeof(uint64_t))
     return set_error(SNN_EWORKSPACE, "snn_k_winners: workspace too small");
+  if (k == 1) {
+    uint64_t* part_min = reinterpret_cast<uint64_t*>(ws);
+    const int n = int(int64_t(F) * HW);
+    int cpi = int(ceil_div(n, 256 * 8));  // >= 8 neurons per thread
+    if (cpi < 1) cpi = 1;
+    while (cpi > 1 && size_t(B) * cpi * sizeof(uint64_t) > ws_bytes) cpi /= 2;
+    kwta_k1_min_kernel<<<unsigned(int64_t(B) * cpi), 256, 0, s>>>(lat, v, n, cpi, part_min);
+    kwta_k1_emit_kernel<<<int(ceil_div(B, 128)), 128, 0, s>>>(part_min, B, cpi, int(HW), W, winners, count);
+    note_launch(2);
+    return check_launch("snn_k_winners(k=1)");
+  }
   uint64_t* pb = reinterpret_cast<uint64_t*>(ws);
   int64_t total = int64_t(B) * HW;
   int64_t blocks = ceil_div(total, 256);

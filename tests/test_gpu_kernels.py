@@ -207,7 +207,10 @@ def test_inhibit_vs_oracle(G, orc, F, levels, hw):
                                                  (2, 256, 64, 64, 16, 4, 0.2, 0), (3, 1, 9, 9, 3, 0, 1.0, 1),
                                                  (2, 4, 3, 3, 2, 5, 0.0, 0), (1, 9, 140, 141, 6, 3, 0.3, 2),
                                                  (2, 500, 12, 12, 16, 1, 0.7, 3),   # candidate lists, F near 512
-                                                 (2, 600, 10, 10, 6, 1, 0.6, 2)])   # F > 512: rescan path
+                                                 (2, 600, 10, 10, 6, 1, 0.6, 2),    # F > 512: rescan path
+                                                 (5, 200, 4, 4, 1, 0, 0.3, 3),      # k = 1: reduction path
+                                                 (1, 100, 9, 24, 1, 0, 0.5, 2), (3, 40, 70, 70, 1, 2, 0.1, 1),
+                                                 (2, 8, 5, 5, 1, 0, 0.0, 0)])       # k = 1, nothing spikes
 def test_k_winners_vs_oracle(G, orc, B, F, H, W, k, r, p, levels):
     import synth
     rng = np.random.default_rng(B * 1000 + F)
