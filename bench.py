@@ -289,6 +289,7 @@ class C5Step(C2Step):
 class SeqBase(C2Step):
     """Sequential plasticity configs: a batched fixed-weight prefix, then a CUDA graph of per-image
     plasticity steps (conv+fire -> [inhibit] -> kWTA -> [decide] -> STDP), no host sync per image."""
+    e2e_pipelined = None  # one step is the whole sequential pass: its e2e copies stay in line
 
     def _prefix(self):
         snn, T = self.snn, self.wl.T
