@@ -235,9 +235,10 @@ __global__ void __launch_bounds__(FPL == 4 ? 768 : 1024, 1) seq_train_kernel(con
             const int f = int(w >> 16), yy = int(w >> 8 & 0xFFu), xx = int(w & 0xFFu);
             emit(best, f, yy, xx);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < 8; ++j) {  // branchless: one select per slot
               const int fj = int(fxy[j] >> 16), yj = int(fxy[j] >> 8 & 0xFFu), xj = int(fxy[j] & 0xFFu);
-              if (fj == f || (abs(yj - yy) <= s.r && abs(xj - xx) <= s.r)) kr[j] = ~uint64_t(0);
+              const bool kill = (fj == f) | ((abs(yj - yy) <= s.r) & (abs(xj - xx) <= s.r));
+              kr[j] = kill ? ~uint64_t(0) : kr[j];
             }
             ++nwin;
           }
