@@ -336,10 +336,16 @@ static bool seq_plan(int C, int H, int W, int pad, int F, int KH, int KW, int T,
   if (a.Ho < 1 || a.Wo < 1 || R + T + kIt >= 65536 || F > 8192) return false;
   const int HoWo = a.Ho * a.Wo;
   if (int64_t(F) * HoWo >= (int64_t(1) << 24)) return false;
-  const int fpls[3] = {4, 2, 1};
+  // Latency-bound (one image at a time): when one walk per (position, 32-feature group) fits in a wave
+  // of warps, the narrowest groups give the shortest critical walk (measured C3: FPL 4 43.1k, 2 49.7k,
+  // 1 50.1k img/s); larger maps take the widest groups that fit.
+  const bool one_wave = int64_t(HoWo) * ceil_div(F, 32) <= int64_t(num_sms()) * 32;
+  const int fpls[3] = {one_wave ? 1 : 4, 2, one_wave ? 4 : 1};
   for (int i = 0; i < 3; ++i) {
     const int fpl = fpls[i], fgs = 32 * fpl;
     if (fpl > 1 && F <= fgs / 2) continue;  // lanes would idle
+    if (const char* e = getenv("SNN_SEQ_FPL"))  // tuning experiments: force the features per lane
+      if (atoi(e) != fpl) continue;
     const int nwarps = fpl == 4 ? 24 : 32;
     a.row_bytes = fgs * 4;
     const int wsb = al16h((R + 1) * fgs * 4);

@@ -15,7 +15,8 @@ for _ in range(3):
 torch.cuda.synchronize()
 F, HoWo, N, k = 250, 196, 2000, wl.extra["k"]
 r256 = lambda x: (x + 255) // 256 * 256
-off = 256 + r256(F * HoWo) + r256(F * HoWo * 4) + r256(N * k * 4) + r256(2 * HoWo * 8)
+G = int(os.environ.get("SEQ_GROUPS", "8"))  # feature groups of the plan (ceil(F / (32 * FPL))); C3 default FPL 1
+off = 256 + r256(F * HoWo) + r256(F * HoWo * 4) + r256(N * k * 4) + r256(G * HoWo * 8)
 st = seq.ws[off:off + N * 48].view(torch.int64).cpu().numpy().reshape(N, 6).astype(np.float64)
 d = np.diff(st, axis=1)[100:]
 ca = seq.ws[off + N * 48: off + N * 48 + 148 * 16].view(torch.int64).cpu().numpy().reshape(148, 2).astype(np.float64)
