@@ -456,10 +456,68 @@ __global__ void __launch_bounds__(kSmThreads) enc_small_kernel(const float* __re
   }
 }
 
+// Latency path for a handful of small images (C1: one image per plasticity step): one CTA of 1024
+// threads per image sorts the image's unique 55-bit keys (value desc, index asc) with a shared-memory
+// bitonic network, then every sorted rank r maps to its bin directly -- a few microseconds where the
+// multi-level select, built for throughput over many images, needs tens of them for one.
+constexpr int kBtThreads = 1024;
+__global__ void __launch_bounds__(kBtThreads) enc_bitonic_kernel(const float* __restrict__ x, int n, int np2, int T,
+                                                                 int bins, uint8_t* __restrict__ lat) {
+  extern __shared__ uint64_t bk[];  // [np2] keys; ~0 = not positive / padding
+  __shared__ int s_n;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const float* xb = x + int64_t(b) * n;
+  uint8_t* lb = lat + int64_t(b) * n;
+  if (tid == 0) s_n = 0;
+  __syncthreads();
+  int cnt = 0;
+  for (int i = tid; i < np2; i += kBtThreads) {
+    uint64_t k = ~uint64_t(0);
+    if (i < n) {
+      const float v = xb[i];
+      if (v > 0.0f) { k = (uint64_t(0x7FFFFFFFu - __float_as_uint(v)) << 24) | uint32_t(i); ++cnt; }
+      else lb[i] = kNoSpike;
+    }
+    bk[i] = k;
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((tid & 31) == 0 && cnt) atomicAdd(&s_n, cnt);
+  __syncthreads();
+  for (int size = 2; size <= np2; size <<= 1) {  // bitonic sort, ascending
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < (np2 >> 1); i += kBtThreads) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint64_t a = bk[lo], c = bk[hi];
+        if ((a > c) == up) { bk[lo] = c; bk[hi] = a; }
+      }
+      __syncthreads();
+    }
+  }
+  const uint32_t N = uint32_t(s_n), q = N / uint32_t(T), m = N % uint32_t(T);
+  for (uint32_t r = tid; r < N; r += kBtThreads) {
+    uint32_t bin;
+    if (bins == 1) bin = uint32_t((uint64_t(r) * T) / N);
+    else if (bins == 2) bin = q ? (r < q * uint32_t(T) ? r / q : 255u) : 255u;
+    else bin = r < m * (q + 1) ? r / (q + 1) : m + (r - m * (q + 1)) / q;  // R1
+    lb[uint32_t(bk[r] & 0xFFFFFFu)] = bin >= uint32_t(T) ? kNoSpike : uint8_t(bin);
+  }
+}
+
 int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, uint8_t* lat, void* wsp,
                   size_t ws_bytes, cudaStream_t s) {
   int64_t n = int64_t(C) * H * W;
   if (B == 0 || n == 0) return SNN_OK;
+  if (n <= 8192 && B * 2 <= num_sms()) {  // a few small images: latency path
+    int np2 = 2;
+    while (np2 < n) np2 <<= 1;
+    const size_t smem = size_t(np2) * sizeof(uint64_t);
+    cudaError_t e = cudaFuncSetAttribute(enc_bitonic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_encode: %s", cudaGetErrorString(e));
+    enc_bitonic_kernel<<<B, kBtThreads, smem, s>>>(x, int(n), np2, T, bins, lat);
+    note_launch();
+    return check_launch("snn_encode(bitonic)");
+  }
   if (n <= 16384) {
     const size_t smem = size_t(n) * (sizeof(uint32_t) + sizeof(uint16_t)) + 16;
     cudaError_t e = cudaFuncSetAttribute(enc_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
