@@ -6,6 +6,7 @@
 // per-position best-key map.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -608,7 +609,9 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
   const size_t smem = use_smem ? size_t(HW) * sizeof(uint64_t) + (lists ? size_t(HW) : 0) : 0;
   cudaError_t e = cudaFuncSetAttribute(kwta_rounds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_k_winners: %s", cudaGetErrorString(e));
-  kwta_rounds_kernel<<<B, kKwtaThreads, smem, s>>>(lat, v, F, H, W, k, r, pb, topk, M, winners, count, use_smem);
+  int nthr = kKwtaThreads;  // measured C1 (784 positions): 1024 threads 59 us step, 512 67, 256 70
+  if (const char* e = getenv("SNN_KWTA_THREADS")) nthr = atoi(e);  // tuning experiments
+  kwta_rounds_kernel<<<B, nthr, smem, s>>>(lat, v, F, H, W, k, r, pb, topk, M, winners, count, use_smem);
   note_launch();
   return check_launch("snn_k_winners");
 }
