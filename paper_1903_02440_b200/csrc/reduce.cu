@@ -533,12 +533,20 @@ __global__ void __launch_bounds__(256) kwta_k1_min_kernel(const uint8_t* __restr
   const uint8_t* lb = lat + int64_t(b) * n;
   const float* vb = v + int64_t(b) * n;
   uint64_t m = ~uint64_t(0);
-  for (int i = part * 256 + threadIdx.x; i < n; i += cpi * 256) {
-    const uint8_t l = lb[i];
-    if (l != kNoSpike) {
-      const uint64_t k = wta_key(l, vb[i], uint32_t(i));  // i = f * H * W + p: the R14 flat index
-      m = k < m ? k : m;
-    }
+  const int stride = cpi * 256;
+  for (int i0 = part * 256 + threadIdx.x; i0 < n; i0 += 4 * stride) {  // 4 neurons' loads in flight
+    uint32_t l[4];
+    float vv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) l[u] = i0 + u * stride < n ? lb[i0 + u * stride] : kNoSpike;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) vv[u] = l[u] != kNoSpike ? vb[i0 + u * stride] : 0.0f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (l[u] != kNoSpike) {
+        const uint64_t k = wta_key(uint8_t(l[u]), vv[u], uint32_t(i0 + u * stride));  // flat index (R14)
+        m = k < m ? k : m;
+      }
   }
   m = warp_min_u64(m);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
@@ -578,7 +586,7 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
   if (k == 1) {
     uint64_t* part_min = reinterpret_cast<uint64_t*>(ws);
     const int n = int(int64_t(F) * HW);
-    int cpi = int(ceil_div(n, 256 * 8));  // >= 8 neurons per thread
+    int cpi = int(ceil_div(n, 256 * 4));  // ~4 neurons per thread, loaded together
     if (cpi < 1) cpi = 1;
     while (cpi > 1 && size_t(B) * cpi * sizeof(uint64_t) > ws_bytes) cpi /= 2;
     kwta_k1_min_kernel<<<unsigned(int64_t(B) * cpi), 256, 0, s>>>(lat, v, n, cpi, part_min);
