@@ -133,15 +133,17 @@ __global__ void tc_prep_a_kernel(const uint8_t* __restrict__ lat_in, int C, int 
       const int b = m / HoWo, rem = m - b * HoWo, y = rem / Wo, x = rem - (rem / Wo) * Wo;
       int c = k0 / KK, r = k0 - c * KK, ky = r / KW, kx = r - ky * KW;
       const uint8_t* base = lat_in + int64_t(b) * C * H * W;
-      for (int j = 0; j < 16; ++j) {
-        const int k = k0 + j;
-        if (k < p.K) {
-          const int yy = y + ky - pad, xx = x + kx - pad;
-          if (yy >= 0 && yy < H && xx >= 0 && xx < W && base[(int64_t(c) * H + yy) * W + xx] < T)
-            wv[j >> 2] |= 1u << (8 * (j & 3));
-        }
+      uint32_t lv[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {  // addresses and predicates first, then all loads in flight
+        const int yy = y + ky - pad, xx = x + kx - pad;
+        const bool in = k0 + j < p.K && yy >= 0 && yy < H && xx >= 0 && xx < W;
+        lv[j] = in ? base[(int64_t(c) * H + yy) * W + xx] : 0xFFu;
         if (++kx == KW) { kx = 0; if (++ky == KH) { ky = 0; ++c; } }
       }
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (lv[j] < uint32_t(T)) wv[j >> 2] |= 1u << (8 * (j & 3));
     }
     *reinterpret_cast<uint4*>(aq + tc_off(m, k0, kTcM, p.Kt)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
   }
@@ -164,16 +166,16 @@ __global__ void tc_prep_b16_kernel(const float* __restrict__ w, int F, int R, in
       // weight index of GEMM column k: (c, ky, kx) order = k itself; (ky, kx, c) order = c * KK + kyx
       const int kyx = p.hwc ? k0 / p.Cp : 0, c0 = p.hwc ? k0 - kyx * p.Cp : 0;
       const int C = R / KK;
+      float xs[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {  // all 16 loads issued before any use
+        const bool in = p.hwc ? (c0 + j < C) : (k0 + j < R);
+        const int widx = p.hwc ? (c0 + j) * KK + kyx : k0 + j;
+        xs[j] = in ? __ldg(w + int64_t(f) * R + widx) : 0.0f;
+      }
+#pragma unroll
       for (int j = 0; j < 16; ++j) {
-        int widx;
-        if (p.hwc) {
-          if (c0 + j >= C) break;
-          widx = (c0 + j) * KK + kyx;
-        } else {
-          if (k0 + j >= R) break;
-          widx = k0 + j;
-        }
-        const float x = __ldg(w + int64_t(f) * R + widx);
+        const float x = xs[j];
         const float s = x * 2147483648.0f;
         if (!(x >= 0.0f && x <= 1.0f) || s != truncf(s)) { bad = 1; continue; }
         const uint32_t q = uint32_t(s);
