@@ -47,6 +47,33 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t x) {
   return x;
 }
 
+// Programmatic dependent launch: every chained kernel first waits for its predecessor grid (so no
+// read or write can race it), then lets its own dependent start launching; launches go through
+// launch_k with the programmatic-serialization attribute (SNN_PDL=0 turns it off).  Without the
+// attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// Large resident kernels (the walk and the sort, one CTA per SM with most of the shared memory) only
+// wait: letting their dependents launch early would park waiting CTAs next to them (C5: -1.6 %).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 // Exact fixed-point potential (units of 2^-31) -> fp32, round to nearest (N1).
 __device__ __forceinline__ float fixed_to_float(int64_t acc) {
   return __ll2float_rn(acc) * 4.656612873077392578125e-10f;  // 2^-31, exact scaling

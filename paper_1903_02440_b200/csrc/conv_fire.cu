@@ -63,6 +63,7 @@ static inline int align16(int x) { return (x + 15) & ~15; }
 // not an integer multiple of 2^-31 in [0, 1] (outside the exact domain, N1).
 __global__ void weight_prep_kernel(const float* __restrict__ w, int F, int R, int FGS, int n_groups,
                                    uint32_t* __restrict__ wq) {
+  pdl_begin();
   int64_t total = int64_t(n_groups) * (R + 1) * FGS;
   int bad = 0;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
@@ -441,7 +442,7 @@ int weight_prep_launch(const float* w, int F, int R, int FGS, int n_groups, uint
   int blocks = int(ceil_div(total, 256));
   if (blocks > 2048) blocks = 2048;
   if (blocks < 1) blocks = 1;
-  weight_prep_kernel<<<blocks, 256, 0, s>>>(w, F, R, FGS, n_groups, wq);
+  launch_k(weight_prep_kernel, dim3(blocks), dim3(256), 0, s, w, F, R, FGS, n_groups, wq);
   note_launch();
   return check_launch("snn_conv_fire(weight prep)");
 }

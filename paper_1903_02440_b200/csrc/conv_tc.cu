@@ -95,6 +95,7 @@ __device__ __forceinline__ size_t tc_off(int row, int k, int rows_per_tile, int 
 // B operand: u8 limbs of the fixed-point weights, n = 4 * f_local + limb, one block per chunk.
 __global__ void tc_prep_b_kernel(const float* __restrict__ w, int F, int R, TcPlan p, uint8_t* __restrict__ bq,
                                  int* err) {
+  pdl_begin();
   const int64_t total = int64_t(p.nch) * p.N * p.Kp;
   int bad = 0;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
@@ -118,6 +119,7 @@ __global__ void tc_prep_b_kernel(const float* __restrict__ w, int F, int R, TcPl
 // One thread per 16-byte core-matrix row = 16 consecutive receptive-field entries of one position.
 __global__ void tc_prep_a_kernel(const uint8_t* __restrict__ lat_in, int C, int H, int W, int pad, int KH, int KW,
                                  int Ho, int Wo, int T, TcPlan p, uint8_t* __restrict__ aq) {
+  pdl_begin();
   const int KK = KH * KW;
   const int64_t rows16 = int64_t(p.Mt) * kTcM * (p.Kp / 16);
   const int nk16 = p.Kp / 16;
@@ -153,6 +155,7 @@ __global__ void tc_prep_a_kernel(const uint8_t* __restrict__ lat_in, int C, int 
 // 16-byte limb rows n = 4 f_local + limb of one core-matrix column.
 __global__ void tc_prep_b16_kernel(const float* __restrict__ w, int F, int R, int KK, TcPlan p,
                                    uint8_t* __restrict__ bq, int* err) {
+  pdl_begin();
   const int nk16 = p.Kp / 16;
   const int64_t total = int64_t(p.nch) * p.Fc * nk16;
   int bad = 0;
@@ -202,6 +205,7 @@ __global__ void __launch_bounds__(256) tc_prep_a_band_kernel(const uint8_t* __re
                                                              int pad, int KH, int KW, int Ho, int Wo, int T,
                                                              TcPlan p, int RB, int nbands, int B, int KS,
                                                              uint8_t* __restrict__ aq) {
+  pdl_begin();
   extern __shared__ uint8_t band[];
   const int Wp = W + 2 * pad, TR = RB + KH - 1, KK = KH * KW, nk16 = p.Kp / 16;
   if (int(blockIdx.x) == B * nbands * KS) {  // padding rows
@@ -250,6 +254,7 @@ __global__ void __launch_bounds__(256) tc_prep_a_band_kernel(const uint8_t* __re
 __global__ void __launch_bounds__(256) tc_prep_a_hwc_kernel(const uint8_t* __restrict__ lat_in, int C, int H, int W,
                                                             int pad, int KH, int KW, int Ho, int Wo, int T, TcPlan p,
                                                             int B, uint8_t* __restrict__ aq) {
+  pdl_begin();
   extern __shared__ __align__(16) uint8_t hband[];
   const int Wp = W + 2 * pad, TR = p.RB + KH - 1, Cp = p.Cp, nk16 = p.Kp / 16;
   if (int(blockIdx.x) == B * p.nbands) {  // padding rows
@@ -298,6 +303,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
                                                                  uint8_t* __restrict__ lat_out,
                                                                  float* __restrict__ v_out,
                                                                  unsigned long long* __restrict__ part) {
+  pdl_begin();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t a_bytes = kTcM * kTcKT, b_bytes = uint32_t(p.N) * kTcKT, stage_bytes = a_bytes + b_bytes;
@@ -403,6 +409,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
 // split-K finalize: the summed fixed-point potentials -> (lat, v) (Eq. 5).
 __global__ void conv_tc_finalize_kernel(const unsigned long long* __restrict__ part, int M, int F, int HoWo, int T,
                                         uint8_t* __restrict__ lat_out, float* __restrict__ v_out) {
+  pdl_begin();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < int64_t(M) * F;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int m = int(i / F), f = int(i - int64_t(m) * F);
@@ -430,21 +437,21 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
     const int64_t total = int64_t(p.nch) * p.Fc * (p.Kp / 16);
     int64_t blocks = ceil_div(total, 256);
     if (blocks > int64_t(num_sms()) * 8) blocks = int64_t(num_sms()) * 8;
-    tc_prep_b16_kernel<<<int(blocks), 256, 0, s>>>(w, F, R, KH * KW, p, bq, error_word_ptr());
+    launch_k(tc_prep_b16_kernel, dim3(int(blocks)), dim3(256), 0, s, w, F, R, KH * KW, p, bq, error_word_ptr());
     note_launch();
   }
   {
     if (p.hwc) {
-      tc_prep_a_hwc_kernel<<<unsigned(int64_t(B) * p.nbands + 1), 256, p.band_smem, s>>>(lat_in, C, H, W, pad, KH, KW,
+      launch_k(tc_prep_a_hwc_kernel, dim3(unsigned(int64_t(B) * p.nbands + 1)), dim3(256), p.band_smem, s, lat_in, C, H, W, pad, KH, KW,
                                                                                       Ho, Wo, T, p, B, aq);
     } else if (p.band) {
-      tc_prep_a_band_kernel<<<unsigned(int64_t(B) * p.nbands + 1), 256, p.band_smem, s>>>(
+      launch_k(tc_prep_a_band_kernel, dim3(unsigned(int64_t(B) * p.nbands + 1)), dim3(256), p.band_smem, s, 
           lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p, p.RB, p.nbands, B, 1, aq);
     } else {
       const int64_t rows16 = int64_t(p.Mt) * kTcM * (p.Kp / 16);
       int64_t blocks = ceil_div(rows16, 256);
       if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
-      tc_prep_a_kernel<<<int(blocks), 256, 0, s>>>(lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p, aq);
+      launch_k(tc_prep_a_kernel, dim3(int(blocks)), dim3(256), 0, s, lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p, aq);
     }
     note_launch();
   }
@@ -453,14 +460,14 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
   const int smem = kTcStages * (kTcM * kTcKT + p.N * kTcKT) + 1024;
   cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_conv_fire(tc): %s", cudaGetErrorString(e));
-  conv_tc_kernel<<<unsigned(int64_t(p.Mt) * p.nch * p.KS), kTcThreads, smem, s>>>(aq, bq, p, F, Ho * Wo, T, cols,
+  launch_k(conv_tc_kernel, dim3(unsigned(int64_t(p.Mt) * p.nch * p.KS)), dim3(kTcThreads), smem, s, aq, bq, p, F, Ho * Wo, T, cols,
                                                                                lat_out, v_out, part);
   note_launch();
   if (part) {
     const int64_t n = int64_t(p.M) * F;
     int blocks = int(ceil_div(n, 256));
     if (blocks > num_sms() * 8) blocks = num_sms() * 8;
-    conv_tc_finalize_kernel<<<blocks, 256, 0, s>>>(part, p.M, F, Ho * Wo, T, lat_out, v_out);
+    launch_k(conv_tc_finalize_kernel, dim3(blocks), dim3(256), 0, s, part, p.M, F, Ho * Wo, T, lat_out, v_out);
     note_launch();
   }
   return check_launch("snn_conv_fire(tc)");

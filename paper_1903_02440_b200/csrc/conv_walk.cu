@@ -41,6 +41,7 @@ int weight_prep_launch(const float* w, int F, int R, int FGS, int n_groups, uint
 // ------------------------------------------------------------------------------------- sort only
 template <int PPW>
 __global__ void __launch_bounds__(512) rf_sort_kernel(const WalkArgs a) {
+  pdl_wait();
   constexpr int LPP = 32 / PPW;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -71,6 +72,7 @@ __global__ void __launch_bounds__(512) rf_sort_kernel(const WalkArgs a) {
 
 template <int FPL, int PPW, bool PRE>
 __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(const WalkArgs a) {
+  pdl_wait();
   constexpr int LPP = 32 / PPW;
   constexpr int FGS = LPP * FPL;
   static_assert(!PRE || PPW == 1, "presorted walk: one position per warp");
@@ -344,7 +346,7 @@ static int walk_go(const WalkPlan& pl, const WalkArgs& a, cudaStream_t s) {
   const int64_t want = ceil_div(int64_t(num_sms()) * occ, pl.n_groups);
   int gx = int(per_group < want ? per_group : want);
   if (gx < 1) gx = 1;
-  k<<<dim3(gx, pl.n_groups), pl.nwarps * 32, pl.smem, s>>>(a);
+  launch_k(k, dim3(dim3(gx, pl.n_groups)), dim3(pl.nwarps * 32), pl.smem, s, a);
   note_launch();
   return check_launch("snn_conv_fire(walk)");
 }
@@ -360,7 +362,7 @@ static int sort_go(const WalkPlan& pl, const WalkArgs& a, cudaStream_t s) {
   int64_t blocks = ceil_div(ceil_div(a.np, PPW), pl.sort_nwarps);
   const int64_t cap = int64_t(num_sms()) * occ;
   if (blocks > cap) blocks = cap;
-  k<<<int(blocks), pl.sort_nwarps * 32, pl.sort_smem, s>>>(a);
+  launch_k(k, dim3(int(blocks)), dim3(pl.sort_nwarps * 32), pl.sort_smem, s, a);
   note_launch();
   return check_launch("snn_conv_fire(sort)");
 }

@@ -85,6 +85,7 @@ __device__ __forceinline__ uint32_t enc_cut_start(uint32_t b, uint32_t N, uint32
 // Level 0: histogram of the top 12 bits of every positive key (all images of the group).
 __global__ void __launch_bounds__(kEncThreads) enc_hist0_kernel(const float* __restrict__ x, int64_t n,
                                                                  EncodeWS ws) {
+  pdl_begin();
   __shared__ uint32_t sh[kEncBins];
   for (int i = threadIdx.x; i < kEncBins; i += blockDim.x) sh[i] = 0;
   __syncthreads();
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_hist0_kernel(const float* __r
 // Levels 1..4: histogram of the next digit for elements whose prefix matches an unresolved cut.
 __global__ void __launch_bounds__(kEncThreads) enc_hist_kernel(const float* __restrict__ x, int64_t n, int T,
                                                                 int level, EncodeWS ws) {
+  pdl_begin();
   const int g = blockIdx.y;
   const int S = T;
   const int ns = ws.n_slots[g];
@@ -148,6 +150,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_hist_kernel(const float* __re
 // Per-image selection after level L: locate every unresolved cut's digit, resolve or descend,
 // rebuild the sorted list of distinct prefixes for level L+1 and zero their histograms.
 __global__ void __launch_bounds__(256) enc_select_kernel(int T, int bins, int level, EncodeWS ws) {
+  pdl_begin();
   const int g = blockIdx.x;
   const int S = T;
   const int NC = enc_ncuts(T, bins);
@@ -232,6 +235,7 @@ __global__ void __launch_bounds__(256) enc_select_kernel(int T, int bins, int le
 
 __global__ void __launch_bounds__(kEncThreads) enc_assign_kernel(const float* __restrict__ x, int64_t n, int T,
                                                                   int bins, uint8_t* __restrict__ lat, EncodeWS ws) {
+  pdl_begin();
   const int g = blockIdx.y;
   const int S = T;
   const int NC = enc_ncuts(T, bins);
@@ -277,6 +281,7 @@ __device__ __forceinline__ uint64_t sm_key(uint32_t vk, int i) { return (uint64_
 
 __global__ void __launch_bounds__(kSmThreads) enc_small_kernel(const float* __restrict__ x, int n, int T, int bins,
                                                                 uint8_t* __restrict__ lat) {
+  pdl_begin();
   extern __shared__ uint32_t vk[];              // [n] 0x7FFFFFFF - bits(x), or ~0 for x <= 0; then [n] u16 candidates
   uint16_t* cand = reinterpret_cast<uint16_t*>(vk + n);
   __shared__ uint8_t bin_lat[4096];             // level-0 bin -> latency of its elements, 0xFF = a cut inside
@@ -463,6 +468,7 @@ __global__ void __launch_bounds__(kSmThreads) enc_small_kernel(const float* __re
 constexpr int kBtThreads = 1024;
 __global__ void __launch_bounds__(kBtThreads) enc_bitonic_kernel(const float* __restrict__ x, int n, int np2, int T,
                                                                  int bins, uint8_t* __restrict__ lat) {
+  pdl_begin();
   extern __shared__ uint64_t bk[];  // [np2] keys; ~0 = not positive / padding
   __shared__ int s_n;
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -514,7 +520,7 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, u
     const size_t smem = size_t(np2) * sizeof(uint64_t);
     cudaError_t e = cudaFuncSetAttribute(enc_bitonic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_encode: %s", cudaGetErrorString(e));
-    enc_bitonic_kernel<<<B, kBtThreads, smem, s>>>(x, int(n), np2, T, bins, lat);
+    launch_k(enc_bitonic_kernel, dim3(B), dim3(kBtThreads), smem, s, x, int(n), np2, T, bins, lat);
     note_launch();
     return check_launch("snn_encode(bitonic)");
   }
@@ -522,7 +528,7 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, u
     const size_t smem = size_t(n) * (sizeof(uint32_t) + sizeof(uint16_t)) + 16;
     cudaError_t e = cudaFuncSetAttribute(enc_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_encode: %s", cudaGetErrorString(e));
-    enc_small_kernel<<<B, kSmThreads, smem, s>>>(x, int(n), T, bins, lat);
+    launch_k(enc_small_kernel, dim3(B), dim3(kSmThreads), smem, s, x, int(n), T, bins, lat);
     note_launch();
     return check_launch("snn_encode(small)");
   }
@@ -537,19 +543,19 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, u
     if (cudaMemsetAsync(ws.hist0, 0, sizeof(uint32_t) * size_t(gn) * kEncBins, s) != cudaSuccess)
       return check_launch("snn_encode memset");
     dim3 grid(nchunks, gn);
-    enc_hist0_kernel<<<grid, kEncThreads, 0, s>>>(xg, n, ws);
+    launch_k(enc_hist0_kernel, dim3(grid), dim3(kEncThreads), 0, s, xg, n, ws);
     note_launch();
     if (enc_ncuts(T, bins) > 0) {
-      enc_select_kernel<<<gn, 256, 0, s>>>(T, bins, 0, ws);
+      launch_k(enc_select_kernel, dim3(gn), dim3(256), 0, s, T, bins, 0, ws);
       note_launch();
       for (int L = 1; L < kEncLevels; ++L) {
-        enc_hist_kernel<<<grid, kEncThreads, 0, s>>>(xg, n, T, L, ws);
+        launch_k(enc_hist_kernel, dim3(grid), dim3(kEncThreads), 0, s, xg, n, T, L, ws);
         note_launch();
-        enc_select_kernel<<<gn, 256, 0, s>>>(T, bins, L, ws);
+        launch_k(enc_select_kernel, dim3(gn), dim3(256), 0, s, T, bins, L, ws);
         note_launch();
       }
     }
-    enc_assign_kernel<<<grid, kEncThreads, 0, s>>>(xg, n, T, bins, lat + int64_t(g0) * n, ws);
+    launch_k(enc_assign_kernel, dim3(grid), dim3(kEncThreads), 0, s, xg, n, T, bins, lat + int64_t(g0) * n, ws);
     note_launch();
     int rc = check_launch("snn_encode");
     if (rc) return rc;
@@ -559,6 +565,7 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, u
 
 // ------------------------------------------------------------------------------------ expand / validate
 __global__ void expand_kernel(const uint8_t* __restrict__ lat, int64_t n, int T, float* __restrict__ wave) {
+  pdl_begin();
   int b = blockIdx.y;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     uint8_t l = lat[int64_t(b) * n + i];
@@ -571,12 +578,13 @@ int expand_launch(const uint8_t* lat, int B, int n, int T, float* wave, cudaStre
   if (B == 0 || n == 0) return SNN_OK;
   int blocks = int(ceil_div(n, 256));
   if (blocks > 4096) blocks = 4096;
-  expand_kernel<<<dim3(blocks, B), 256, 0, s>>>(lat, n, T, wave);
+  launch_k(expand_kernel, dim3(dim3(blocks, B)), dim3(256), 0, s, lat, n, T, wave);
   note_launch();
   return check_launch("snn_expand");
 }
 
 __global__ void validate_kernel(const uint8_t* __restrict__ lat, size_t n, int T, int32_t* n_bad) {
+  pdl_begin();
   int bad = 0;
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
     uint8_t l = lat[i];
@@ -591,7 +599,7 @@ int validate_launch(const uint8_t* lat, size_t n, int T, int32_t* n_bad, cudaStr
   if (n == 0) return SNN_OK;
   size_t blocks = (n + 255) / 256;
   if (blocks > 1184) blocks = 1184;
-  validate_kernel<<<unsigned(blocks), 256, 0, s>>>(lat, n, T, n_bad);
+  launch_k(validate_kernel, dim3(unsigned(blocks)), dim3(256), 0, s, lat, n, T, n_bad);
   note_launch();
   return check_launch("snn_validate_lat");
 }

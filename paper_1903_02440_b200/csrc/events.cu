@@ -13,6 +13,7 @@ __global__ void __launch_bounds__(256) count_events_kernel(const uint8_t* __rest
                                                            int W, int pad, int F, int KH, int KW, int T, int Ho,
                                                            int Wo, const uint8_t* __restrict__ lat_out,
                                                            unsigned long long* __restrict__ out) {
+  pdl_begin();
   extern __shared__ uint32_t hist[];  // [warps][T + 1]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   uint32_t* h = hist + warp * (T + 1);
@@ -66,7 +67,7 @@ int count_events_launch(const uint8_t* lat_in, int B, int C, int H, int W, int p
   if (npos == 0) return SNN_OK;
   int64_t blocks = ceil_div(npos, 8);
   if (blocks > int64_t(num_sms()) * 8) blocks = int64_t(num_sms()) * 8;
-  count_events_kernel<<<int(blocks), 256, 8 * (T + 1) * sizeof(uint32_t), s>>>(lat_in, B, C, H, W, pad, F, KH, KW, T,
+  launch_k(count_events_kernel, dim3(int(blocks)), dim3(256), 8 * (T + 1) * sizeof(uint32_t), s, lat_in, B, C, H, W, pad, F, KH, KW, T,
                                                                                 Ho, Wo, lat_out, out);
   note_launch();
   return check_launch("snn_count_events");

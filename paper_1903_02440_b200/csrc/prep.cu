@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(kThreads) filter_bank_kernel(const double* __r
                                                                const double* __restrict__ ker, int K, int S,
                                                                int pad, double thr, int mode, float* __restrict__ out,
                                                                int Ho, int Wo, int tiles_x, int tiles) {
+  pdl_begin();
   extern __shared__ double fsm[];
   const int SW = kFB + S - 1, SH = kFB + S - 1;
   double* tile = fsm;
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(kThreads) filter_bank_kernel(const double* __r
 __global__ void __launch_bounds__(kThreads) local_norm_kernel(const float* __restrict__ x, int H, int W, int R,
                                                               double eps, float* __restrict__ out, int tiles_x,
                                                               int tiles) {
+  pdl_begin();
   extern __shared__ float lsm[];
   const int SW = kTW + 2 * R, SH = kTH + 2 * R;
   const int64_t bc = blockIdx.x / tiles;
@@ -118,6 +120,7 @@ __global__ void __launch_bounds__(kThreads) lateral_inhibition_kernel(const floa
                                                                       const float* __restrict__ factors, int n,
                                                                       float* __restrict__ out, int tiles_x,
                                                                       int tiles) {
+  pdl_begin();
   extern __shared__ float isms[];
   const int SW = kTW + 2 * n, SH = kTH + 2 * n;
   float* fac = isms + SH * SW;
@@ -176,7 +179,7 @@ int launch_tiles(Kern kern, const char* what, int64_t planes, int Ho, int Wo, si
   if (grid > 0x7fffffff) return set_error(SNN_ESHAPE, "%s: %lld tiles exceed the grid limit", what, (long long)grid);
   if (smem > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
     return set_error(SNN_ECUDA, "%s: cannot opt in to %zu B of shared memory", what, smem);
-  kern<<<unsigned(grid), kThreads, smem, s>>>(args..., tiles_x, tiles);
+  launch_k(kern, dim3(unsigned(grid)), dim3(kThreads), smem, s, args..., tiles_x, tiles);
   note_launch();
   return check_launch(what);
 }
@@ -196,7 +199,7 @@ int filter_bank_launch(const double* img, int B, int H, int W, const double* ker
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(filter_bank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
     return set_error(SNN_ECUDA, "filter_bank: cannot opt in to %zu B of shared memory", smem);
-  filter_bank_kernel<<<unsigned(grid), kThreads, smem, s>>>(img, H, W, ker, K, S, pad, thr, mode, out, Ho, Wo, tiles_x,
+  launch_k(filter_bank_kernel, dim3(unsigned(grid)), dim3(kThreads), smem, s, img, H, W, ker, K, S, pad, thr, mode, out, Ho, Wo, tiles_x,
                                                              tiles);
   note_launch();
   return check_launch("filter_bank");

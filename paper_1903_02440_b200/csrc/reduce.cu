@@ -22,6 +22,7 @@ __global__ void __launch_bounds__(256) pool_kernel(const uint8_t* __restrict__ l
                                                    int64_t BF, int H, int W, int PH, int PW, int SH, int SW,
                                                    int DH, int DW, int Ho, int Wo, int vfinal,
                                                    uint8_t* __restrict__ lat_out, float* __restrict__ v_out) {
+  pdl_begin();
   const IDX total = IDX(BF) * IDX(Ho) * IDX(Wo);
   const IDX HoWo = IDX(Ho) * IDX(Wo), HW = IDX(H) * IDX(W);
   for (IDX o = IDX(blockIdx.x) * IDX(blockDim.x) + threadIdx.x; o < total; o += IDX(gridDim.x) * blockDim.x) {
@@ -78,6 +79,7 @@ __device__ __forceinline__ void pool4(uint32_t l0, uint32_t l1, uint32_t l2, uin
 __global__ void __launch_bounds__(256) pool2x2_v_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
                                                         uint32_t pairs, int H, int W, int Ho, int Wo, int vfinal,
                                                         uint8_t* __restrict__ lat_out, float* __restrict__ v_out) {
+  pdl_begin();
   const uint32_t Wo2 = uint32_t(Wo) >> 1, per_plane = uint32_t(Ho) * Wo2;
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < pairs; q += gridDim.x * blockDim.x) {
     const uint32_t bf = q / per_plane, rem = q - bf * per_plane, oy = rem / Wo2, ox2 = rem - oy * Wo2;
@@ -102,6 +104,7 @@ __global__ void __launch_bounds__(256) pool2x2_v_kernel(const uint8_t* __restric
 __global__ void __launch_bounds__(256) pool_rows_kernel(const uint8_t* __restrict__ lat, uint32_t rows, int H, int W,
                                                         int PH, int PW, int SH, int SW, int DH, int DW, int Ho,
                                                         int Wo, uint8_t* __restrict__ lat_out) {
+  pdl_begin();
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
     const uint32_t bf = r / uint32_t(Ho);
     const int oy = int(r - bf * uint32_t(Ho));
@@ -139,18 +142,18 @@ int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, 
     const uint32_t pairs = uint32_t(total / 2);
     int64_t pb = ceil_div(pairs, 256);
     if (pb > int64_t(num_sms()) * 16) pb = int64_t(num_sms()) * 16;
-    pool2x2_v_kernel<<<int(pb), 256, 0, s>>>(lat, v, pairs, H, W, Ho, Wo, (flags & SNN_POOL_VFINAL) ? 1 : 0, lat_out,
+    launch_k(pool2x2_v_kernel, dim3(int(pb)), dim3(256), 0, s, lat, v, pairs, H, W, Ho, Wo, (flags & SNN_POOL_VFINAL) ? 1 : 0, lat_out,
                                               v_out);
   } else if (small && !v_out && PH * PW <= 16) {  // small windows: one thread per output row
     const uint32_t rows = uint32_t(int64_t(B) * F * Ho);
     int64_t rb = ceil_div(rows, 256);
     if (rb > int64_t(num_sms()) * 16) rb = int64_t(num_sms()) * 16;
-    pool_rows_kernel<<<int(rb), 256, 0, s>>>(lat, rows, H, W, PH, PW, SH, SW, DH, DW, Ho, Wo, lat_out);
+    launch_k(pool_rows_kernel, dim3(int(rb)), dim3(256), 0, s, lat, rows, H, W, PH, PW, SH, SW, DH, DW, Ho, Wo, lat_out);
   } else if (small)
-    pool_kernel<uint32_t><<<int(blocks), 256, 0, s>>>(lat, v_out ? v : nullptr, int64_t(B) * F, H, W, PH, PW, SH, SW,
+    launch_k(pool_kernel<uint32_t>, dim3(int(blocks)), dim3(256), 0, s, lat, v_out ? v : nullptr, int64_t(B) * F, H, W, PH, PW, SH, SW,
                                                       DH, DW, Ho, Wo, (flags & SNN_POOL_VFINAL) ? 1 : 0, lat_out, v_out);
   else
-    pool_kernel<int64_t><<<int(blocks), 256, 0, s>>>(lat, v_out ? v : nullptr, int64_t(B) * F, H, W, PH, PW, SH, SW,
+    launch_k(pool_kernel<int64_t>, dim3(int(blocks)), dim3(256), 0, s, lat, v_out ? v : nullptr, int64_t(B) * F, H, W, PH, PW, SH, SW,
                                                      DH, DW, Ho, Wo, (flags & SNN_POOL_VFINAL) ? 1 : 0, lat_out, v_out);
   note_launch();
   return check_launch("snn_pool");
@@ -169,6 +172,7 @@ template <class IDX>
 __global__ void __launch_bounds__(256) inhibit_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
                                                       int B, int F, int64_t HW64, uint8_t* __restrict__ lat_out,
                                                       float* __restrict__ v_out, int16_t* __restrict__ winner_f) {
+  pdl_begin();
   const IDX HW = IDX(HW64), total = IDX(B) * HW;
   for (IDX q = IDX(blockIdx.x) * blockDim.x + threadIdx.x; q < total; q += IDX(gridDim.x) * blockDim.x) {
     const IDX b = q / HW, p = q - b * HW;
@@ -208,6 +212,7 @@ constexpr int64_t kWarpPerPosMax = 16384;
 __global__ void __launch_bounds__(256) inhibit_warp_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
                                                            int B, int F, int64_t HW, uint8_t* __restrict__ lat_out,
                                                            float* __restrict__ v_out, int16_t* __restrict__ winner_f) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const int64_t total = int64_t(B) * HW;
   for (int64_t q = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; q < total;
@@ -267,16 +272,16 @@ int inhibit_launch(const uint8_t* lat, const float* v, int B, int F, int H, int 
   const int64_t HW = int64_t(H) * W, total = int64_t(B) * HW;
   if (total == 0) return SNN_OK;
   if (total <= kWarpPerPosMax) {
-    inhibit_warp_kernel<<<int(ceil_div(total, 8)), 256, 0, s>>>(lat, v, B, F, HW, lat_out, v_out, winner_f);
+    launch_k(inhibit_warp_kernel, dim3(int(ceil_div(total, 8))), dim3(256), 0, s, lat, v, B, F, HW, lat_out, v_out, winner_f);
     note_launch();
     return check_launch("snn_inhibit");
   }
   int64_t blocks = ceil_div(total, 256);
   if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
   if (int64_t(B) * F * HW < (int64_t(1) << 32))
-    inhibit_kernel<uint32_t><<<int(blocks), 256, 0, s>>>(lat, v, B, F, HW, lat_out, v_out, winner_f);
+    launch_k(inhibit_kernel<uint32_t>, dim3(int(blocks)), dim3(256), 0, s, lat, v, B, F, HW, lat_out, v_out, winner_f);
   else
-    inhibit_kernel<int64_t><<<int(blocks), 256, 0, s>>>(lat, v, B, F, HW, lat_out, v_out, winner_f);
+    launch_k(inhibit_kernel<int64_t>, dim3(int(blocks)), dim3(256), 0, s, lat, v, B, F, HW, lat_out, v_out, winner_f);
   note_launch();
   return check_launch("snn_inhibit");
 }
@@ -286,6 +291,7 @@ int inhibit_launch(const uint8_t* lat, const float* v, int B, int F, int H, int 
 // 32-bit indexing (F*H*W <= 2^24 is checked at the ABI), 4 features in flight per thread.
 __global__ void __launch_bounds__(256) kwta_posbest_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
                                                            int B, int F, int HW, uint64_t* __restrict__ pos_best) {
+  pdl_begin();
   const int64_t total = int64_t(B) * HW;
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < total; q += int64_t(gridDim.x) * blockDim.x) {
     const int b = int(q / HW), p = int(q - int64_t(b) * HW);
@@ -317,6 +323,7 @@ __global__ void __launch_bounds__(256) kwta_posbest_kernel(const uint8_t* __rest
 __global__ void __launch_bounds__(256) kwta_posbest_warp_kernel(const uint8_t* __restrict__ lat,
                                                                 const float* __restrict__ v, int B, int F, int HW,
                                                                 uint64_t* __restrict__ pos_best) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const int64_t total = int64_t(B) * HW;
   for (int64_t q = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; q < total;
@@ -347,6 +354,7 @@ constexpr int kTopM = 17;
 __global__ void __launch_bounds__(256) kwta_topk_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
                                                         int B, int F, int HW, int M, uint64_t* __restrict__ pos_best,
                                                         uint64_t* __restrict__ topk) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const int64_t total = int64_t(B) * HW;
   for (int64_t q = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; q < total;
@@ -397,6 +405,7 @@ __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t
                                                                    const uint64_t* __restrict__ topk, int M,
                                                                    int32_t* __restrict__ winners,
                                                                    int32_t* __restrict__ count, int use_smem) {
+  pdl_begin();
   extern __shared__ uint64_t dyn[];  // [HW] current keys, then (topk) [HW] list cursors (u8)
   __shared__ uint32_t fexcl[256];  // bitmask of excluded features (F <= 8192)
   __shared__ int wy[kMaxK], wx[kMaxK];
@@ -528,6 +537,7 @@ size_t k_winners_workspace(int B, int F, int H, int W) {
 // its block minimum to the workspace), then one thread per image reduces them and decodes (f, y, x).
 __global__ void __launch_bounds__(256) kwta_k1_min_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
                                                           int n, int cpi, uint64_t* __restrict__ part_min) {
+  pdl_begin();
   __shared__ uint64_t red[8];
   const int b = blockIdx.x / cpi, part = blockIdx.x - b * cpi;
   const uint8_t* lb = lat + int64_t(b) * n;
@@ -560,6 +570,7 @@ __global__ void __launch_bounds__(256) kwta_k1_min_kernel(const uint8_t* __restr
 
 __global__ void kwta_k1_emit_kernel(const uint64_t* __restrict__ part_min, int B, int cpi, int HW, int W,
                                     int32_t* __restrict__ winners, int32_t* __restrict__ count) {
+  pdl_begin();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   uint64_t m = ~uint64_t(0);
@@ -589,8 +600,8 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
     int cpi = int(ceil_div(n, 256 * 4));  // ~4 neurons per thread, loaded together
     if (cpi < 1) cpi = 1;
     while (cpi > 1 && size_t(B) * cpi * sizeof(uint64_t) > ws_bytes) cpi /= 2;
-    kwta_k1_min_kernel<<<unsigned(int64_t(B) * cpi), 256, 0, s>>>(lat, v, n, cpi, part_min);
-    kwta_k1_emit_kernel<<<int(ceil_div(B, 128)), 128, 0, s>>>(part_min, B, cpi, int(HW), W, winners, count);
+    launch_k(kwta_k1_min_kernel, dim3(unsigned(int64_t(B) * cpi)), dim3(256), 0, s, lat, v, n, cpi, part_min);
+    launch_k(kwta_k1_emit_kernel, dim3(int(ceil_div(B, 128))), dim3(128), 0, s, part_min, B, cpi, int(HW), W, winners, count);
     note_launch(2);
     return check_launch("snn_k_winners(k=1)");
   }
@@ -607,11 +618,11 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
   if (lists) {
     int64_t wb = ceil_div(total, 8);
     if (wb > int64_t(num_sms()) * 32) wb = int64_t(num_sms()) * 32;
-    kwta_topk_kernel<<<int(wb), 256, 0, s>>>(lat, v, B, F, int(HW), M, pb, topk);
+    launch_k(kwta_topk_kernel, dim3(int(wb)), dim3(256), 0, s, lat, v, B, F, int(HW), M, pb, topk);
   } else if (total <= kWarpPerPosMax) {
-    kwta_posbest_warp_kernel<<<int(ceil_div(total, 8)), 256, 0, s>>>(lat, v, B, F, int(HW), pb);
+    launch_k(kwta_posbest_warp_kernel, dim3(int(ceil_div(total, 8))), dim3(256), 0, s, lat, v, B, F, int(HW), pb);
   } else {
-    kwta_posbest_kernel<<<int(blocks), 256, 0, s>>>(lat, v, B, F, int(HW), pb);
+    launch_k(kwta_posbest_kernel, dim3(int(blocks)), dim3(256), 0, s, lat, v, B, F, int(HW), pb);
   }
   note_launch();
   const size_t smem = use_smem ? size_t(HW) * sizeof(uint64_t) + (lists ? size_t(HW) : 0) : 0;
@@ -619,7 +630,7 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_k_winners: %s", cudaGetErrorString(e));
   int nthr = kKwtaThreads;  // measured C1 (784 positions): 1024 threads 59 us step, 512 67, 256 70
   if (const char* e = getenv("SNN_KWTA_THREADS")) nthr = atoi(e);  // tuning experiments
-  kwta_rounds_kernel<<<B, nthr, smem, s>>>(lat, v, F, H, W, k, r, pb, topk, M, winners, count, use_smem);
+  launch_k(kwta_rounds_kernel, dim3(B), dim3(nthr), smem, s, lat, v, F, H, W, k, r, pb, topk, M, winners, count, use_smem);
   note_launch();
   return check_launch("snn_k_winners");
 }
@@ -628,6 +639,7 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
 __global__ void decide_kernel(const int32_t* __restrict__ winners, const int32_t* __restrict__ count, int B, int k,
                               int F, int n_classes, const int32_t* __restrict__ labels, int32_t* __restrict__ decision,
                               float* __restrict__ reward) {
+  pdl_begin();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   int d = -1;
@@ -643,7 +655,7 @@ __global__ void decide_kernel(const int32_t* __restrict__ winners, const int32_t
 int decide_launch(const int32_t* winners, const int32_t* count, int B, int k, int F, int n_classes,
                   const int32_t* labels, int32_t* decision, float* reward, cudaStream_t s) {
   if (B == 0) return SNN_OK;
-  decide_kernel<<<int(ceil_div(B, 256)), 256, 0, s>>>(winners, count, B, k, F, n_classes, labels, decision, reward);
+  launch_k(decide_kernel, dim3(int(ceil_div(B, 256))), dim3(256), 0, s, winners, count, B, k, F, n_classes, labels, decision, reward);
   note_launch();
   return check_launch("snn_decide");
 }

@@ -27,6 +27,7 @@ __device__ __forceinline__ int64_t pos_key(uint8_t lat, float v, int f) {
 __global__ void __launch_bounds__(kKeyThreads) position_keys_kernel(const uint8_t* __restrict__ lat,
                                                                     const float* __restrict__ v, int64_t B, int F,
                                                                     int HW, int f0, int64_t* __restrict__ keys) {
+  pdl_begin();
   const int64_t total = B * HW;
   for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < total; o += int64_t(gridDim.x) * blockDim.x) {
     const int64_t b = o / HW;
@@ -52,6 +53,7 @@ __global__ void __launch_bounds__(kWtaThreads) k_winners_keys_kernel(const int64
                                                                      int k, int r, uint64_t* __restrict__ scratch,
                                                                      int use_smem, int32_t* __restrict__ winners,
                                                                      int32_t* __restrict__ count) {
+  pdl_begin();
   extern __shared__ uint64_t skey[];
   __shared__ uint64_t red[kWtaThreads / 32];
   const int b = blockIdx.x, HW = H * W;
@@ -105,7 +107,7 @@ int position_keys_launch(const uint8_t* lat, const float* v, int B, int F, int H
   const int64_t total = int64_t(B) * H * W;
   int64_t blocks = ceil_div(total, kKeyThreads);
   if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
-  position_keys_kernel<<<unsigned(blocks), kKeyThreads, 0, s>>>(lat, v, B, F, H * W, f0, keys);
+  launch_k(position_keys_kernel, dim3(unsigned(blocks)), dim3(kKeyThreads), 0, s, lat, v, B, F, H * W, f0, keys);
   note_launch();
   return check_launch("snn_position_keys");
 }
@@ -123,7 +125,7 @@ int k_winners_keys_launch(const int64_t* keys, int B, int H, int W, int k, int r
   if (dyn > 48 * 1024 &&
       cudaFuncSetAttribute(k_winners_keys_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn)) != cudaSuccess)
     return set_error(SNN_ECUDA, "snn_k_winners_keys: cannot opt in to %zu B of shared memory", dyn);
-  k_winners_keys_kernel<<<B, kWtaThreads, dyn, s>>>(keys, H, W, k, r, static_cast<uint64_t*>(ws), use_smem, winners,
+  launch_k(k_winners_keys_kernel, dim3(B), dim3(kWtaThreads), dyn, s, keys, H, W, k, r, static_cast<uint64_t*>(ws), use_smem, winners,
                                                     count);
   note_launch();
   return check_launch("snn_k_winners_keys");

@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(256) stdp_kernel(float* __restrict__ w, int C,
                                                    const int32_t* __restrict__ count, float a_plus, float a_minus,
                                                    float lb, float ub, int stabilizer,
                                                    const float* __restrict__ reward, int f0, int Floc) {
+  pdl_begin();
   const int i = blockIdx.x;  // winner slot; blockIdx.y = slice of its synapses (gridDim.y slices)
   if (i >= count[0]) return;
   if (winners[i * 3] < f0 || winners[i * 3] >= f0 + Floc) return;  // another rank's feature (f4 sharding)
@@ -57,7 +58,7 @@ int stdp_launch(float* w, int F, int C, int KH, int KW, const uint8_t* lat_in, i
   const int R = C * KH * KW;
   int slices = int(ceil_div(R, 256));
   if (slices > 64) slices = 64;
-  stdp_kernel<<<dim3(k, slices), 256, 0, s>>>(w, C, KH, KW, lat_in, H, W, pad, lat_out, Ho, Wo, winners, count, a_plus, a_minus,
+  launch_k(stdp_kernel, dim3(dim3(k, slices)), dim3(256), 0, s, w, C, KH, KW, lat_in, H, W, pad, lat_out, Ho, Wo, winners, count, a_plus, a_minus,
                                 lb, ub, stabilizer, reward, f0, F);
   note_launch();
   return check_launch("snn_stdp_update");
