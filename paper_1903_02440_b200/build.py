@@ -37,6 +37,9 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, extra=()) -> str:
+    env_extra = os.environ.get("SNN_NVCC_EXTRA", "").split()  # tuning experiments, e.g. -DSNN_SORT_UNROLL=8
+    if env_extra:
+        extra, force = list(extra) + env_extra, True
     if not force and not needs_build():
         return LIB
     objdir = os.path.join(PKG, "build")

@@ -15,7 +15,11 @@ constexpr size_t kListChunkBytes = size_t(512) << 20;  // sorted lists per chunk
                                                         // the lists stream from HBM either way)
 constexpr int kBlk = 8;                               // list entries per gather block
 constexpr int kIt = 16;                               // list entries per walk iteration (lists padded to this)
-constexpr int kListSlack = 2048;                      // bytes read past the last record (prefetch)
+constexpr int kListSlack = 2048;
+#ifndef SNN_SORT_UNROLL
+#define SNN_SORT_UNROLL 4  // receptive-field entries per lane whose latency loads are in flight together
+#endif
+constexpr int kSortUnroll = SNN_SORT_UNROLL;                      // bytes read past the last record (prefetch)
 
 struct WalkArgs {
   const uint8_t* lat_in;
@@ -94,7 +98,7 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl
   for (int t = gl; t < T; t += LPP) cnt[t] = 0;
   __syncwarp();
   if (pv) {
-#pragma unroll 4
+#pragma unroll kSortUnroll
     for (int e = gl; e < R; e += LPP) {
       const int l = lat_of(e);
       if (l < T) atomicAdd(&cnt[l], 1u);
@@ -123,7 +127,7 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl
   if (gl == 0) start[T] = uint16_t(carry);
   __syncwarp();
   if (pv) {
-#pragma unroll 4
+#pragma unroll kSortUnroll
     for (int e = gl; e < R; e += LPP) {
       const int l = lat_of(e);
       if (l < T) list[atomicAdd(&cnt[l], 1u)] = uint32_t(e) * rb;
