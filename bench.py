@@ -296,6 +296,9 @@ class SeqBase(C2Step):
         snn.encode(self.x, T, out=self.lat0, ws=self.ws_enc)
         if self.l1 is not None:
             self.l1(self.lat0)
+        if getattr(self, "prep", None) is not None:  # C4: the theta = +inf layer's A operands, all images
+            s2 = self.wl.convs[1]
+            snn.conv_inf_prepare(self.l1.plat, s2.F, s2.KH, s2.KW, s2.pad, T, out=self.prep)
 
     def run(self, ev=None):
         def mark(i):
@@ -382,8 +385,13 @@ class C4Step(SeqBase):
         self.seq = pipeline.SeqSTDP(wl.convs[1], wl.weights[1], wl.convs[0].F, self.l1.PHo, self.l1.PWo, wl.T,
                                     1, 0, False, wl.extra["stdp"], n_classes=wl.extra["n_classes"], device=dev)
         self.labels = torch.from_numpy(wl.extra["labels"].astype(np.int32)).to(dev)
+        s2 = wl.convs[1]
+        _, C2, H2, W2 = self.l1.plat.shape
+        # theta = +inf layer: its A operands (weight-independent) for all images, built in the prefix
+        self.prep = torch.empty(max(snn.lib().snn_conv_inf_prepare_bytes(batch, C2, H2, W2, s2.pad, s2.F, s2.KH, s2.KW), 1),
+                                dtype=torch.uint8, device=dev)
         self._prefix()
-        self.graph = pipeline.SeqGraph(self.seq, self.l1.plat, batch, labels=self.labels)
+        self.graph = pipeline.SeqGraph(self.seq, self.l1.plat, batch, labels=self.labels, prep=self.prep)
         self.stages = ["l1_prefix", "seq_rstdp"]
 
     def config(self):

@@ -136,6 +136,21 @@ SNN_API int snn_conv_fire(const uint8_t* lat_in, int B, int C, int H, int W, int
                   uint8_t* lat_out, float* v_out, float* pot_out,
                   void* ws, size_t ws_bytes, snn_stream_t s);
 
+/* Sequential theta = +inf layers (C4's R-STDP layer: one image at a time, new weights every image).
+ * The A operand of Eq. 5 (the binary im2col of each image's S[T-1]) does not depend on the weights, so
+ * snn_conv_inf_prepare builds it for all B images of lat_in [B, C, H, W] at once into `prep`
+ * (snn_conv_inf_prepare_bytes(B, ...) bytes, caller-owned); snn_conv_fire_prepared then runs the
+ * conv of image b of that batch with the current weights w: exactly snn_conv_fire(lat_in[b], w, pad, T,
+ * +inf, ...) (bit-identical), minus the A preparation.  lat_out, v_out [1, F, Ho, Wo]; workspace
+ * snn_conv_fire_workspace(1, C, H, W, pad, F, KH, KW, T, +inf).  Same argument errors as snn_conv_fire;
+ * prep smaller than required: SNN_EWORKSPACE. */
+SNN_API size_t snn_conv_inf_prepare_bytes(int B, int C, int H, int W, int pad, int F, int KH, int KW);
+SNN_API int snn_conv_inf_prepare(const uint8_t* lat_in, int B, int C, int H, int W, int pad, int F, int KH, int KW,
+                                 int T, void* prep, size_t prep_bytes, snn_stream_t s);
+SNN_API int snn_conv_fire_prepared(const void* prep, int b, int C, int H, int W, int pad, const float* w, int F,
+                                   int KH, int KW, int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes,
+                                   snn_stream_t s);
+
 /* ---------------------------------------------------------------------------------------------
  * a4. Spike-wave max-pooling (Eq. 3; readings R10-R12).
  * Window PH x PW, stride SH x SW, zero padding DH x DW (padding never spikes).

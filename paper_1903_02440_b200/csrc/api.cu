@@ -54,6 +54,12 @@ int filter_bank_launch(const double* img, int B, int H, int W, const double* ker
 int local_norm_launch(const float* x, int B, int C, int H, int W, int R, double eps, float* out, cudaStream_t s);
 int lateral_inhibition_launch(const float* x, int B, int C, int H, int W, const float* factors, int n, float* out,
                               cudaStream_t s);
+size_t conv_inf_prepare_bytes(int B, int C, int H, int W, int pad, int F, int KH, int KW);
+int conv_inf_prepare_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, int F, int KH, int KW, int T,
+                            void* prep, size_t prep_bytes, cudaStream_t s);
+int conv_fire_prepared_launch(const void* prep, int b, int C, int H, int W, int pad, const float* w, int F, int KH,
+                              int KW, int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes,
+                              cudaStream_t s);
 int decide_launch(const int32_t* winners, const int32_t* count, int B, int k, int F, int n_classes,
                   const int32_t* labels, int32_t* decision, float* reward, cudaStream_t s);
 
@@ -220,6 +226,31 @@ int snn_validate_lat(const uint8_t* lat, size_t n, int T, int32_t* n_bad, snn_st
 size_t snn_conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta) {
   if (conv_checks(B, C, H, W, pad, F, KH, KW, T, theta)) return 0;
   return conv_fire_workspace(B, C, H, W, pad, F, KH, KW, T, theta);
+}
+
+size_t snn_conv_inf_prepare_bytes(int B, int C, int H, int W, int pad, int F, int KH, int KW) {
+  if (conv_checks(B, C, H, W, pad, F, KH, KW, 1, INFINITY)) return 0;
+  return conv_inf_prepare_bytes(B, C, H, W, pad, F, KH, KW);
+}
+
+int snn_conv_inf_prepare(const uint8_t* lat_in, int B, int C, int H, int W, int pad, int F, int KH, int KW, int T,
+                         void* prep, size_t prep_bytes, snn_stream_t s) {
+  int rc = conv_checks(B, C, H, W, pad, F, KH, KW, T, INFINITY);
+  if (rc) return rc;
+  if (B == 0 || F == 0) return SNN_OK;
+  REQUIRE(lat_in && prep, SNN_EINVAL, "snn_conv_inf_prepare: NULL tensor");
+  return conv_inf_prepare_launch(lat_in, B, C, H, W, pad, F, KH, KW, T, prep, prep_bytes, S(s));
+}
+
+int snn_conv_fire_prepared(const void* prep, int b, int C, int H, int W, int pad, const float* w, int F, int KH,
+                           int KW, int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes, snn_stream_t s) {
+  int rc = conv_checks(1, C, H, W, pad, F, KH, KW, T, INFINITY);
+  if (rc) return rc;
+  REQUIRE(b >= 0, SNN_EINVAL, "snn_conv_fire_prepared: b < 0");
+  if (F == 0) return SNN_OK;
+  REQUIRE(prep && w && lat_out && v_out, SNN_EINVAL, "snn_conv_fire_prepared: NULL tensor");
+  REQUIRE(ws, SNN_EWORKSPACE, "snn_conv_fire_prepared: NULL workspace");
+  return conv_fire_prepared_launch(prep, b, C, H, W, pad, w, F, KH, KW, T, lat_out, v_out, ws, ws_bytes, S(s));
 }
 
 size_t snn_stdp_sequence_workspace(int N, int C, int H, int W, int pad, int F, int KH, int KW, int T, int k) {

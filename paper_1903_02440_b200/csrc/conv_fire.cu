@@ -447,7 +447,8 @@ int weight_prep_launch(const float* w, int F, int R, int FGS, int n_groups, uint
   return check_launch("snn_conv_fire(weight prep)");
 }
 int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH, int KW,
-                   int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes, cudaStream_t s);
+                   int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes, cudaStream_t s,
+                   const uint8_t* aq_pre = nullptr);
 
 size_t conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta) {
   const bool inf = isinf(theta) && theta > 0;

@@ -117,9 +117,13 @@ __global__ void tc_prep_b_kernel(const float* __restrict__ w, int F, int R, TcPl
 
 // A operand: binary im2col of the spike-wave at T-1 (any spike, since every spike time is <= T-1).
 // One thread per 16-byte core-matrix row = 16 consecutive receptive-field entries of one position.
+// grid.y > 1: blockIdx.y is an image of a batch prepared image by image (snn_conv_inf_prepare), each
+// with its own one-image plan p and an A block of img_bytes.
 __global__ void tc_prep_a_kernel(const uint8_t* __restrict__ lat_in, int C, int H, int W, int pad, int KH, int KW,
-                                 int Ho, int Wo, int T, TcPlan p, uint8_t* __restrict__ aq) {
+                                 int Ho, int Wo, int T, TcPlan p, uint8_t* __restrict__ aq, size_t img_bytes) {
   pdl_begin();
+  lat_in += int64_t(blockIdx.y) * C * H * W;
+  aq += size_t(blockIdx.y) * img_bytes;
   const int KK = KH * KW;
   const int64_t rows16 = int64_t(p.Mt) * kTcM * (p.Kp / 16);
   const int nk16 = p.Kp / 16;
@@ -422,7 +426,40 @@ __global__ void conv_tc_finalize_kernel(const unsigned long long* __restrict__ p
 }
 
 int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH, int KW,
-                   int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes, cudaStream_t s) {
+                   int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes, cudaStream_t s,
+                   const uint8_t* aq_pre = nullptr);
+
+// A operands of B images, one one-image block each (tc_plan(1, ...)), for later snn_conv_fire_prepared.
+size_t conv_inf_prepare_bytes(int B, int C, int H, int W, int pad, int F, int KH, int KW) {
+  return size_t(B) * tc_plan(1, C, H, W, pad, KH, KW, F, num_sms()).a_bytes;
+}
+
+int conv_inf_prepare_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, int F, int KH, int KW, int T,
+                            void* prep, size_t prep_bytes, cudaStream_t s) {
+  const TcPlan p = tc_plan(1, C, H, W, pad, KH, KW, F, num_sms());
+  if (prep_bytes < size_t(B) * p.a_bytes)
+    return set_error(SNN_EWORKSPACE, "snn_conv_inf_prepare: %zu < %zu bytes", prep_bytes, size_t(B) * p.a_bytes);
+  const int Ho = H + 2 * pad - KH + 1, Wo = W + 2 * pad - KW + 1;
+  const int64_t rows16 = int64_t(p.Mt) * kTcM * (p.Kp / 16);
+  const int blocks = int(ceil_div(rows16, 256));
+  if (B > 65535) return set_error(SNN_ESHAPE, "snn_conv_inf_prepare: B > 65535");
+  launch_k(tc_prep_a_kernel, dim3(blocks, B), dim3(256), 0, s, lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p,
+           static_cast<uint8_t*>(prep), p.a_bytes);
+  note_launch();
+  return check_launch("snn_conv_inf_prepare");
+}
+
+int conv_fire_prepared_launch(const void* prep, int b, int C, int H, int W, int pad, const float* w, int F, int KH,
+                              int KW, int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes,
+                              cudaStream_t s) {
+  const TcPlan p = tc_plan(1, C, H, W, pad, KH, KW, F, num_sms());
+  const uint8_t* aq = static_cast<const uint8_t*>(prep) + size_t(b) * p.a_bytes;
+  return conv_tc_launch(nullptr, 1, C, H, W, pad, w, F, KH, KW, T, lat_out, v_out, ws, ws_bytes, s, aq);
+}
+
+int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH, int KW,
+                   int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes, cudaStream_t s,
+                   const uint8_t* aq_pre) {
   const int Ho = H + 2 * pad - KH + 1, Wo = W + 2 * pad - KW + 1, R = C * KH * KW;
   TcPlan p = tc_plan(B, C, H, W, pad, KH, KW, F, num_sms());
   const size_t a_off = 0, b_off = (p.a_bytes + 1023) & ~size_t(1023);
@@ -440,7 +477,9 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
     launch_k(tc_prep_b16_kernel, dim3(int(blocks)), dim3(256), 0, s, w, F, R, KH * KW, p, bq, error_word_ptr());
     note_launch();
   }
-  {
+  if (aq_pre) {  // prepared by snn_conv_inf_prepare
+    aq = const_cast<uint8_t*>(aq_pre);
+  } else {
     if (p.hwc) {
       launch_k(tc_prep_a_hwc_kernel, dim3(unsigned(int64_t(B) * p.nbands + 1)), dim3(256), p.band_smem, s, lat_in, C, H, W, pad, KH, KW,
                                                                                       Ho, Wo, T, p, B, aq);
@@ -451,7 +490,8 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
       const int64_t rows16 = int64_t(p.Mt) * kTcM * (p.Kp / 16);
       int64_t blocks = ceil_div(rows16, 256);
       if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
-      launch_k(tc_prep_a_kernel, dim3(int(blocks)), dim3(256), 0, s, lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p, aq);
+      launch_k(tc_prep_a_kernel, dim3(int(blocks)), dim3(256), 0, s, lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p, aq,
+               size_t(0));
     }
     note_launch();
   }

@@ -146,9 +146,15 @@ class SeqSTDP:
         self.decision = torch.empty((1,), dtype=torch.int32, device=device)
         self.reward = torch.ones((1,), dtype=torch.float32, device=device)
 
-    def step(self, lat_in_img: torch.Tensor, label: Optional[torch.Tensor] = None):
-        """lat_in_img [1, C, H, W]; label int32 [1] device tensor (R-STDP) or None (plain STDP)."""
-        self.layer(lat_in_img, self.w)
+    def step(self, lat_in_img: torch.Tensor, label: Optional[torch.Tensor] = None, prep=None, b: int = 0):
+        """lat_in_img [1, C, H, W]; label int32 [1] device tensor (R-STDP) or None (plain STDP).
+        prep: for a theta = +inf layer, the batch's A operands (snn_conv_inf_prepare), image index b."""
+        if prep is not None:
+            L = self.layer
+            snn.conv_fire_prepared(prep, b, L.C, L.H, L.W, self.w, self.spec.pad, self.T, lat_out=L.lat, v_out=L.v,
+                                   ws=L.ws)
+        else:
+            self.layer(lat_in_img, self.w)
         lat, v = self.layer.lat, self.layer.v
         if self.inhibit_on:
             snn.inhibit(lat, v, lat_out=self.ilat, v_out=self.iv, winner_f=self.wf)
@@ -175,8 +181,10 @@ class SeqGraph:
     """
 
     def __init__(self, seq: "SeqSTDP", lat_in_all: torch.Tensor, n: int, labels: Optional[torch.Tensor] = None,
-                 snapshot_every: int = 0):
-        self.seq, self.lat, self.n, self.labels = seq, lat_in_all, n, labels
+                 snapshot_every: int = 0, prep: Optional[torch.Tensor] = None):
+        """prep: A operands of lat_in_all for a theta = +inf layer (snn_conv_inf_prepare), refreshed by the
+        caller before each replay whenever lat_in_all changes."""
+        self.seq, self.lat, self.n, self.labels, self.prep = seq, lat_in_all, n, labels, prep
         self.w0 = seq.w.clone()
         self.snaps = [torch.empty_like(seq.w) for _ in range(n // snapshot_every)] if snapshot_every else []
         self.every = snapshot_every
@@ -198,7 +206,7 @@ class SeqGraph:
         si = 0
         for b in range(n):
             lab = None if self.labels is None else self.labels[b:b + 1]
-            self.seq.step(self.lat[b:b + 1], lab)
+            self.seq.step(self.lat[b:b + 1], lab, prep=self.prep, b=b)
             if self.every and (b + 1) % self.every == 0 and si < len(self.snaps):
                 self.snaps[si].copy_(self.seq.w)
                 si += 1

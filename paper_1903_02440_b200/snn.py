@@ -53,6 +53,9 @@ def lib() -> C.CDLL:
                 "snn_pool": (i32, [p, p, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, p, p, p]),
                 "snn_pool_ex": (i32, [p, p] + [i32] * 11 + [p, p, p]),
                 "snn_encode_ex": (i32, [p, i32, i32, i32, i32, i32, i32, p, p, sz, p]),
+                "snn_conv_inf_prepare_bytes": (sz, [i32] * 8),
+                "snn_conv_inf_prepare": (i32, [p] + [i32] * 9 + [p, sz, p]),
+                "snn_conv_fire_prepared": (i32, [p, i32, i32, i32, i32, i32, p, i32, i32, i32, i32, p, p, p, sz, p]),
                 "snn_position_keys": (i32, [p, p, i32, i32, i32, i32, i32, p, p]),
                 "snn_k_winners_keys_workspace": (sz, [i32, i32, i32]),
                 "snn_k_winners_keys": (i32, [p, i32, i32, i32, i32, i32, i32, p, p, p, sz, p]),
@@ -89,7 +92,8 @@ def exported_symbols():
             "snn_count_events", "snn_launch_count", "snn_conv_fire_plan", "snn_stdp_sequence_workspace",
             "snn_stdp_sequence", "snn_filter_bank", "snn_local_norm", "snn_lateral_inhibition",
             "snn_encode_ex", "snn_pool_ex", "snn_position_keys", "snn_k_winners_keys_workspace",
-            "snn_k_winners_keys", "snn_stdp_update_shard"]
+            "snn_k_winners_keys", "snn_stdp_update_shard", "snn_conv_inf_prepare_bytes", "snn_conv_inf_prepare",
+            "snn_conv_fire_prepared"]
 
 
 def _check(rc: int):
@@ -241,6 +245,33 @@ def conv_fire(lat_in: torch.Tensor, w: torch.Tensor, pad: int, T: int, theta: fl
     _check(lib().snn_conv_fire(_ptr(lat_in), B, C_, H, W, pad, _ptr(w), F, KH, KW, T, float(theta),
                                _ptr(lat), _ptr(v), _ptr(pot), _ptr(buf), buf.numel(), _stream(stream)))
     return (lat, v, pot) if want_pot else (lat, v)
+
+
+def conv_inf_prepare(lat_in: torch.Tensor, F: int, KH: int, KW: int, pad: int, T: int, out=None, stream=None):
+    """A operands of every image of lat_in [B, C, H, W] for theta = +inf (snn_conv_inf_prepare)."""
+    _req(lat_in, torch.uint8, "lat_in")
+    B, C_, H, W = lat_in.shape
+    n = int(lib().snn_conv_inf_prepare_bytes(B, C_, H, W, pad, F, KH, KW))
+    buf = out if out is not None else torch.empty(max(n, 1), dtype=torch.uint8, device=lat_in.device)
+    _check(lib().snn_conv_inf_prepare(_ptr(lat_in), B, C_, H, W, pad, F, KH, KW, T, _ptr(buf), buf.numel(),
+                                      _stream(stream)))
+    return buf
+
+
+def conv_fire_prepared(prep: torch.Tensor, b: int, C_: int, H: int, W: int, w: torch.Tensor, pad: int, T: int,
+                       lat_out=None, v_out=None, ws=None, stream=None):
+    """theta = +inf conv of image b of a snn_conv_inf_prepare batch with weights w (snn_conv_fire_prepared)."""
+    _req(w, torch.float32, "w")
+    F, _, KH, KW = w.shape
+    Ho, Wo = conv_out_hw(H, W, KH, KW, pad)
+    dev = w.device
+    lat = lat_out if lat_out is not None else torch.empty((1, F, Ho, Wo), dtype=torch.uint8, device=dev)
+    v = v_out if v_out is not None else torch.empty((1, F, Ho, Wo), dtype=torch.float32, device=dev)
+    n = conv_fire_workspace(1, C_, H, W, pad, F, KH, KW, T, float("inf"))
+    buf = ws if ws is not None else _ws.get(n, dev, "conv")
+    _check(lib().snn_conv_fire_prepared(_ptr(prep), int(b), C_, H, W, pad, _ptr(w), F, KH, KW, T, _ptr(lat), _ptr(v),
+                                        _ptr(buf), buf.numel(), _stream(stream)))
+    return lat, v
 
 
 # ------------------------------------------------------------------------------------------ a4

@@ -280,3 +280,18 @@ def test_conv_inf_split_k(G, orc, B, C, H, W, F, K, pad):
     gl, gv = G.conv_fire(cu(lat), cu(w), pad, 30, float("inf"))
     ol, ov = orc.conv_fire(lat, w, pad, 30, float("inf"))
     assert np.array_equal(host(gl), ol) and np.array_equal(host(gv), ov)
+
+
+@pytest.mark.parametrize("B,C,H,W,F,K,pad", [(5, 20, 25, 40, 100, 17, 0), (3, 6, 9, 11, 12, 3, 1)])
+def test_conv_inf_prepared(G, orc, B, C, H, W, F, K, pad):
+    """snn_conv_inf_prepare + snn_conv_fire_prepared (image by image) == the theta = inf conv per image."""
+    rng = np.random.default_rng(B * 7 + C)
+    lat = rng.integers(0, 30, (B, C, H, W)).astype(np.uint8)
+    lat[rng.random(lat.shape) < 0.5] = NS
+    w = exact_weights(rng, (F, C, K, K))
+    prep = G.conv_inf_prepare(cu(lat), F, K, K, pad, 30)
+    ol, ov = orc.conv_fire(lat, w, pad, 30, float("inf"))
+    gw = cu(w)
+    for b in range(B):
+        gl, gv = G.conv_fire_prepared(prep, b, C, H, W, gw, pad, 30)
+        assert np.array_equal(host(gl)[0], ol[b]) and np.array_equal(host(gv)[0], ov[b]), b
