@@ -92,29 +92,6 @@ __device__ __forceinline__ size_t tc_off(int row, int k, int rows_per_tile, int 
          (r & 7) * 16 + (kk & 15);
 }
 
-// B operand: u8 limbs of the fixed-point weights, n = 4 * f_local + limb, one block per chunk.
-__global__ void tc_prep_b_kernel(const float* __restrict__ w, int F, int R, TcPlan p, uint8_t* __restrict__ bq,
-                                 int* err) {
-  pdl_begin();
-  const int64_t total = int64_t(p.nch) * p.N * p.Kp;
-  int bad = 0;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int k = int(i % p.Kp);
-    const int64_t rest = i / p.Kp;
-    const int n = int(rest % p.N), ch = int(rest / p.N);
-    const int f = ch * p.Fc + (n >> 2), limb = n & 3;
-    uint8_t val = 0;
-    if (f < F && k < R) {
-      const float x = w[int64_t(f) * R + k];
-      const float s = x * 2147483648.0f;
-      if (!(x >= 0.0f && x <= 1.0f) || s != truncf(s)) bad = 1;
-      else val = uint8_t(uint32_t(s) >> (8 * limb));
-    }
-    bq[size_t(ch) * p.Kt * p.N * kTcKT + tc_off(n, k, p.N, p.Kt)] = val;
-  }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flag_error(err, kErrInexact);
-}
-
 // A operand: binary im2col of the spike-wave at T-1 (any spike, since every spike time is <= T-1).
 // One thread per 16-byte core-matrix row = 16 consecutive receptive-field entries of one position.
 // grid.y > 1: blockIdx.y is an image of a batch prepared image by image (snn_conv_inf_prepare), each
