@@ -466,47 +466,94 @@ __global__ void __launch_bounds__(kSmThreads) enc_small_kernel(const float* __re
 // bitonic network, then every sorted rank r maps to its bin directly -- a few microseconds where the
 // multi-level select, built for throughput over many images, needs tens of them for one.
 constexpr int kBtThreads = 1024;
-__global__ void __launch_bounds__(kBtThreads) enc_bitonic_kernel(const float* __restrict__ x, int n, int np2, int T,
-                                                                 int bins, uint8_t* __restrict__ lat) {
+__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
+  const uint32_t lo = __shfl_xor_sync(0xffffffffu, uint32_t(v), m);
+  const uint32_t hi = __shfl_xor_sync(0xffffffffu, uint32_t(v >> 32), m);
+  return (uint64_t(hi) << 32) | lo;
+}
+
+// EPT keys per thread (np2 = 1024 EPT): each warp owns 32 EPT consecutive keys, lane l keys
+// [l EPT, l EPT + EPT); compare-exchange partners closer than 32 EPT are in the same thread or a
+// shuffle away (no barrier), farther ones go through shared memory (one barrier per stride).
+template <int EPT>
+__global__ void __launch_bounds__(kBtThreads) enc_bitonic_kernel(const float* __restrict__ x, int n, int T, int bins,
+                                                                 uint8_t* __restrict__ lat) {
   pdl_begin();
-  extern __shared__ uint64_t bk[];  // [np2] keys; ~0 = not positive / padding
+  constexpr int np2 = kBtThreads * EPT, WCH = 32 * EPT;
+  extern __shared__ uint64_t bk[];  // [np2] keys for the long strides
   __shared__ int s_n;
-  const int b = blockIdx.x, tid = threadIdx.x;
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const int base = (tid >> 5) * WCH + lane * EPT;
   const float* xb = x + int64_t(b) * n;
   uint8_t* lb = lat + int64_t(b) * n;
   if (tid == 0) s_n = 0;
   __syncthreads();
+  uint64_t v[EPT];
   int cnt = 0;
-  for (int i = tid; i < np2; i += kBtThreads) {
-    uint64_t k = ~uint64_t(0);
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int i = base + k;
+    v[k] = ~uint64_t(0);  // not positive / padding: sorts last
     if (i < n) {
-      const float v = xb[i];
-      if (v > 0.0f) { k = (uint64_t(0x7FFFFFFFu - __float_as_uint(v)) << 24) | uint32_t(i); ++cnt; }
+      const float xv = xb[i];
+      if (xv > 0.0f) { v[k] = (uint64_t(0x7FFFFFFFu - __float_as_uint(xv)) << 24) | uint32_t(i); ++cnt; }
       else lb[i] = kNoSpike;
     }
-    bk[i] = k;
   }
   cnt = __reduce_add_sync(0xffffffffu, cnt);
-  if ((tid & 31) == 0 && cnt) atomicAdd(&s_n, cnt);
-  __syncthreads();
+  if (lane == 0 && cnt) atomicAdd(&s_n, cnt);
   for (int size = 2; size <= np2; size <<= 1) {  // bitonic sort, ascending
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = tid; i < (np2 >> 1); i += kBtThreads) {
-        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
-        const bool up = (lo & size) == 0;
-        const uint64_t a = bk[lo], c = bk[hi];
-        if ((a > c) == up) { bk[lo] = c; bk[hi] = a; }
-      }
+    int stride = size >> 1;
+    if (stride >= WCH) {  // long strides: through shared memory
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) bk[base + k] = v[k];
       __syncthreads();
+      for (; stride >= WCH; stride >>= 1) {
+        for (int i = tid; i < (np2 >> 1); i += kBtThreads) {
+          const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+          const bool up = (lo & size) == 0;
+          const uint64_t a = bk[lo], c = bk[hi];
+          if ((a > c) == up) { bk[lo] = c; bk[hi] = a; }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) v[k] = bk[base + k];
+      __syncthreads();  // bk is rewritten by the next size's long strides
+    }
+    for (; stride >= EPT; stride >>= 1) {  // partner in lane ^ (stride / EPT), same slot
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const int i = base + k;
+        const uint64_t o = shfl_xor_u64(v[k], stride / EPT);
+        const bool up = (i & size) == 0, lower = (i & stride) == 0;
+        const uint64_t mn = v[k] < o ? v[k] : o, mx = v[k] < o ? o : v[k];
+        v[k] = (lower == up) ? mn : mx;
+      }
+    }
+    for (; stride > 0; stride >>= 1) {  // partner in the same thread
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const int pk = k ^ stride;
+        if (pk > k) {
+          const bool up = ((base + k) & size) == 0;
+          const uint64_t a = v[k], c = v[pk];
+          if ((a > c) == up) { v[k] = c; v[pk] = a; }
+        }
+      }
     }
   }
+  __syncthreads();  // s_n complete
   const uint32_t N = uint32_t(s_n), q = N / uint32_t(T), m = N % uint32_t(T);
-  for (uint32_t r = tid; r < N; r += kBtThreads) {
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const uint32_t r = uint32_t(base + k);
+    if (r >= N) continue;
     uint32_t bin;
     if (bins == 1) bin = uint32_t((uint64_t(r) * T) / N);
     else if (bins == 2) bin = q ? (r < q * uint32_t(T) ? r / q : 255u) : 255u;
     else bin = r < m * (q + 1) ? r / (q + 1) : m + (r - m * (q + 1)) / q;  // R1
-    lb[uint32_t(bk[r] & 0xFFFFFFu)] = bin >= uint32_t(T) ? kNoSpike : uint8_t(bin);
+    lb[uint32_t(v[k] & 0xFFFFFFu)] = bin >= uint32_t(T) ? kNoSpike : uint8_t(bin);
   }
 }
 
@@ -515,12 +562,12 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, u
   int64_t n = int64_t(C) * H * W;
   if (B == 0 || n == 0) return SNN_OK;
   if (n <= 8192 && B * 2 <= num_sms()) {  // a few small images: latency path
-    int np2 = 2;
-    while (np2 < n) np2 <<= 1;
-    const size_t smem = size_t(np2) * sizeof(uint64_t);
-    cudaError_t e = cudaFuncSetAttribute(enc_bitonic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    const int ept = n <= 2048 ? 2 : n <= 4096 ? 4 : 8;
+    const size_t smem = size_t(kBtThreads) * ept * sizeof(uint64_t);
+    auto k = ept == 2 ? enc_bitonic_kernel<2> : ept == 4 ? enc_bitonic_kernel<4> : enc_bitonic_kernel<8>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_encode: %s", cudaGetErrorString(e));
-    launch_k(enc_bitonic_kernel, dim3(B), dim3(kBtThreads), smem, s, x, int(n), np2, T, bins, lat);
+    launch_k(k, dim3(B), dim3(kBtThreads), smem, s, x, int(n), T, bins, lat);
     note_launch();
     return check_launch("snn_encode(bitonic)");
   }
