@@ -532,6 +532,58 @@ size_t k_winners_workspace(int B, int F, int H, int W) {
   return size_t(B) * H * W * sizeof(uint64_t) * per + 256;
 }
 
+// Stage 2 for small maps with candidate lists (H*W <= 1024: one position per thread): one barrier
+// per round.  Every warp reduces the same per-warp minima (double-buffered, so the next round's writes
+// cannot race a slow reader), every thread learns the winner and updates only its own position --
+// killed inside the winner's Chebyshev-r neighbourhood (R15), else advanced along its list past features
+// that have won (each thread keeps its own copy of that set by writing the same bits).
+__global__ void __launch_bounds__(1024) kwta_rounds_small_kernel(int F, int H, int W, int k, int r,
+                                                                 const uint64_t* __restrict__ pos_best,
+                                                                 const uint64_t* __restrict__ topk, int M,
+                                                                 int32_t* __restrict__ winners,
+                                                                 int32_t* __restrict__ count) {
+  pdl_begin();
+  __shared__ uint64_t red[2][32];
+  __shared__ uint32_t fexcl[256];  // F <= 8192
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
+  const int HW = H * W;
+  for (int i = tid; i < 256; i += blockDim.x) fexcl[i] = 0;
+  const int p = tid;
+  uint64_t key = p < HW ? pos_best[int64_t(b) * HW + p] : ~uint64_t(0);
+  const int py = p / W, px = p - (p / W) * W;
+  int cur = 0, nwin = 0;
+  __syncthreads();
+  for (int round = 0; round < k; ++round) {
+    uint64_t m = warp_min_u64(key);
+    if (lane == 0) red[round & 1][wid] = m;
+    __syncthreads();
+    m = lane < nwarps ? red[round & 1][lane] : ~uint64_t(0);
+    m = warp_min_u64(m);
+    if (m == ~uint64_t(0)) break;  // block-uniform
+    const int idx = int(m & 0xFFFFFFu), f = idx / HW, pw = idx - f * HW, wy = pw / W, wx = pw - (pw / W) * W;
+    if (tid == 0) {
+      int32_t* wr = winners + (int64_t(b) * k + nwin) * 3;
+      wr[0] = f; wr[1] = wy; wr[2] = wx;
+    }
+    atomicOr(&fexcl[f >> 5], 1u << (f & 31));
+    ++nwin;
+    if (key == ~uint64_t(0)) continue;
+    if (abs(py - wy) <= r && abs(px - wx) <= r) { key = ~uint64_t(0); continue; }
+    int ff = int(uint32_t(key & 0xFFFFFFu) / uint32_t(HW));
+    while (fexcl[ff >> 5] >> (ff & 31) & 1) {  // its feature has won: next list entry
+      ++cur;
+      key = cur < M ? topk[(int64_t(b) * HW + p) * M + cur] : ~uint64_t(0);
+      if (key == ~uint64_t(0)) break;
+      ff = int(uint32_t(key & 0xFFFFFFu) / uint32_t(HW));
+    }
+  }
+  for (int i = nwin + tid; i < k; i += blockDim.x) {
+    int32_t* wr = winners + (int64_t(b) * k + i) * 3;
+    wr[0] = -1; wr[1] = -1; wr[2] = -1;
+  }
+  if (tid == 0) count[b] = nwin;
+}
+
 // k = 1 (C2's decision layer, C4's R-STDP winner): the single winner is the minimum key over every
 // neuron of the image -- a plain reduction, spread over cpi CTAs per image for large maps (each writes
 // its block minimum to the workspace), then one thread per image reduces them and decodes (f, y, x).
@@ -625,6 +677,12 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
     launch_k(kwta_posbest_kernel, dim3(int(blocks)), dim3(256), 0, s, lat, v, B, F, int(HW), pb);
   }
   note_launch();
+  if (lists && HW <= 1024 && !getenv("SNN_KWTA_NOSMALL")) {
+    launch_k(kwta_rounds_small_kernel, dim3(B), dim3(int(ceil_div(HW, 32)) * 32), 0, s, F, H, W, k, r, pb, topk, M,
+             winners, count);
+    note_launch();
+    return check_launch("snn_k_winners");
+  }
   const size_t smem = use_smem ? size_t(HW) * sizeof(uint64_t) + (lists ? size_t(HW) : 0) : 0;
   cudaError_t e = cudaFuncSetAttribute(kwta_rounds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_k_winners: %s", cudaGetErrorString(e));
