@@ -475,11 +475,11 @@ __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
 // EPT keys per thread (np2 = 1024 EPT): each warp owns 32 EPT consecutive keys, lane l keys
 // [l EPT, l EPT + EPT); compare-exchange partners closer than 32 EPT are in the same thread or a
 // shuffle away (no barrier), farther ones go through shared memory (one barrier per stride).
-template <int EPT>
-__global__ void __launch_bounds__(kBtThreads) enc_bitonic_kernel(const float* __restrict__ x, int n, int T, int bins,
-                                                                 uint8_t* __restrict__ lat) {
+template <int EPT, int NT = kBtThreads>
+__global__ void __launch_bounds__(NT) enc_bitonic_kernel(const float* __restrict__ x, int n, int T, int bins,
+                                                         uint8_t* __restrict__ lat) {
   pdl_begin();
-  constexpr int np2 = kBtThreads * EPT, WCH = 32 * EPT;
+  constexpr int np2 = NT * EPT, WCH = 32 * EPT;
   extern __shared__ uint64_t bk[];  // [np2] keys for the long strides
   __shared__ int s_n;
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kBtThreads) enc_bitonic_kernel(const float* __
       for (int k = 0; k < EPT; ++k) bk[base + k] = v[k];
       __syncthreads();
       for (; stride >= WCH; stride >>= 1) {
-        for (int i = tid; i < (np2 >> 1); i += kBtThreads) {
+        for (int i = tid; i < (np2 >> 1); i += NT) {
           const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
           const bool up = (lo & size) == 0;
           const uint64_t a = bk[lo], c = bk[hi];
@@ -562,12 +562,22 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, u
   int64_t n = int64_t(C) * H * W;
   if (B == 0 || n == 0) return SNN_OK;
   if (n <= 8192 && B * 2 <= num_sms()) {  // a few small images: latency path
-    const int ept = n <= 2048 ? 2 : n <= 4096 ? 4 : 8;
-    const size_t smem = size_t(kBtThreads) * ept * sizeof(uint64_t);
-    auto k = ept == 2 ? enc_bitonic_kernel<2> : ept == 4 ? enc_bitonic_kernel<4> : enc_bitonic_kernel<8>;
+    // keys per thread x threads = the padded key count (measured C1: 1024 threads 53 us per step, 512 56,
+    // 256 63; SNN_BITONIC_NT = 256 / 512 / 1024 for tuning)
+    int nt = 1024;
+    if (const char* e = getenv("SNN_BITONIC_NT")) nt = atoi(e);
+    const int keys = n <= 2048 ? 2048 : n <= 4096 ? 4096 : 8192;
+    if (nt != 256 && nt != 512 && nt != 1024) nt = 1024;
+    if (keys / nt > 16) nt = keys / 16;
+    const int ept = keys / nt;
+    void (*k)(const float*, int, int, int, uint8_t*) = nullptr;
+    if (nt == 256) k = ept == 8 ? enc_bitonic_kernel<8, 256> : enc_bitonic_kernel<16, 256>;
+    else if (nt == 512) k = ept == 4 ? enc_bitonic_kernel<4, 512> : ept == 8 ? enc_bitonic_kernel<8, 512> : enc_bitonic_kernel<16, 512>;
+    else k = ept == 2 ? enc_bitonic_kernel<2, 1024> : ept == 4 ? enc_bitonic_kernel<4, 1024> : enc_bitonic_kernel<8, 1024>;
+    const size_t smem = size_t(keys) * sizeof(uint64_t);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_encode: %s", cudaGetErrorString(e));
-    launch_k(k, dim3(B), dim3(kBtThreads), smem, s, x, int(n), T, bins, lat);
+    launch_k(k, dim3(B), dim3(nt), smem, s, x, int(n), T, bins, lat);
     note_launch();
     return check_launch("snn_encode(bitonic)");
   }
