@@ -241,7 +241,11 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
     long warps = (kWalkSmemLimit - fixed) / wb;
     const int wcap = c.fpl == 4 ? 24 : 32;
     if (warps > wcap) warps = wcap;
-    if (best < 0) { best = int(&c - cands); best_warps = int(warps); }  // the first (widest FPL) that fits
+    // the first (widest FPL) that fits; a map of few positions (one image: latency, not throughput)
+    // takes the first one-position-per-warp candidate instead -- all lanes sort its receptive field
+    // (measured C1: PPW 4 / FPL 4 53.1 us per step, PPW 1 / FPL 1 50.9 us)
+    const bool latency = int64_t(B) * a.Ho * a.Wo <= int64_t(num_sms()) * 16;
+    if (best < 0 || (latency && c.ppw == 1 && cands[best].ppw != 1)) { best = int(&c - cands); best_warps = int(warps); }
   }
   if (const char* e = getenv("SNN_WALK_FUSED")) {  // tuning experiments: force "ppw,fpl"
     int ppw = 0, fpl = 0;
