@@ -640,12 +640,66 @@ __global__ void kwta_k1_emit_kernel(const uint64_t* __restrict__ part_min, int B
   count[b] = 1;
 }
 
+// k = 1 with one CTA per image (up to ~64 neurons per thread): reduction and decode in one kernel.
+template <int NT>
+__global__ void __launch_bounds__(NT) kwta_k1_block_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
+                                                           int n, int HW, int W, int32_t* __restrict__ winners,
+                                                           int32_t* __restrict__ count) {
+  pdl_begin();
+  __shared__ uint64_t red[NT / 32];
+  const int b = blockIdx.x;
+  const uint8_t* lb = lat + int64_t(b) * n;
+  const float* vb = v + int64_t(b) * n;
+  uint64_t m = ~uint64_t(0);
+  for (int i0 = threadIdx.x; i0 < n; i0 += 4 * NT) {  // 4 neurons' loads in flight
+    uint32_t l[4];
+    float vv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) l[u] = i0 + u * NT < n ? lb[i0 + u * NT] : kNoSpike;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) vv[u] = l[u] != kNoSpike ? vb[i0 + u * NT] : 0.0f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (l[u] != kNoSpike) {
+        const uint64_t k = wta_key(uint8_t(l[u]), vv[u], uint32_t(i0 + u * NT));
+        m = k < m ? k : m;
+      }
+  }
+  m = warp_min_u64(m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < NT / 32 ? red[threadIdx.x] : ~uint64_t(0);
+    m = warp_min_u64(m);
+    if (threadIdx.x == 0) {
+      if (m == ~uint64_t(0)) {
+        winners[b * 3 + 0] = -1; winners[b * 3 + 1] = -1; winners[b * 3 + 2] = -1;
+        count[b] = 0;
+      } else {
+        const int idx = int(m & 0xFFFFFFu), f = idx / HW, p = idx - f * HW;
+        winners[b * 3 + 0] = f; winners[b * 3 + 1] = p / W; winners[b * 3 + 2] = p - (p / W) * W;
+        count[b] = 1;
+      }
+    }
+  }
+}
+
 int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, int k, int r, int32_t* winners,
                      int32_t* count, void* ws, size_t ws_bytes, cudaStream_t s) {
   if (B == 0) return SNN_OK;
   const int64_t HW = int64_t(H) * W;
   if (ws_bytes < size_t(B) * HW * sizeof(uint64_t) || ws_bytes < size_t(B) * sizeof(uint64_t))
     return set_error(SNN_EWORKSPACE, "snn_k_winners: workspace too small");
+  if (k == 1 && int64_t(F) * HW <= 1024 * 8) {  // one CTA per image suffices: no separate decode kernel
+    // (larger maps of one image -- C4: 21,600 neurons -- are faster spread over several CTAs below)
+    const int n = int(int64_t(F) * HW);
+    if (n > 256 * 16 || B < num_sms())
+      launch_k(kwta_k1_block_kernel<1024>, dim3(B), dim3(1024), 0, s, lat, v, n, int(HW), W, winners, count);
+    else
+      launch_k(kwta_k1_block_kernel<256>, dim3(B), dim3(256), 0, s, lat, v, n, int(HW), W, winners, count);
+    note_launch();
+    return check_launch("snn_k_winners(k=1)");
+  }
   if (k == 1) {
     uint64_t* part_min = reinterpret_cast<uint64_t*>(ws);
     const int n = int(int64_t(F) * HW);
