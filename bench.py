@@ -289,29 +289,31 @@ class C5Step(C2Step):
 class SeqBase(C2Step):
     """Sequential plasticity configs: a batched fixed-weight prefix, then a CUDA graph of per-image
     plasticity steps (conv+fire -> [inhibit] -> kWTA -> [decide] -> STDP), no host sync per image."""
-    e2e_pipelined = None  # one step is the whole sequential pass: its e2e copies stay in line
-
-    def _prefix(self):
+    def _prefix(self, src=None):
         snn, T = self.snn, self.wl.T
-        snn.encode(self.x, T, out=self.lat0, ws=self.ws_enc)
+        snn.encode(self.x if src is None else src, T, out=self.lat0, ws=self.ws_enc)
         if self.l1 is not None:
             self.l1(self.lat0)
         if getattr(self, "prep", None) is not None:  # C4: the theta = +inf layer's A operands, all images
             s2 = self.wl.convs[1]
             snn.conv_inf_prepare(self.l1.plat, s2.F, s2.KH, s2.KW, s2.pad, T, out=self.prep)
 
-    def run(self, ev=None):
+    def run(self, ev=None, src=None):
         def mark(i):
             if ev is not None:
                 ev[i].record()
         mark(0)
-        self._prefix(); mark(1)
+        self._prefix(src); mark(1)
         self.graph.replay(); mark(2)
 
     def e2e(self, x_host, out_host):
         self.x.copy_(x_host, non_blocking=True)
         self.run()
         out_host.copy_(self.seq.w, non_blocking=True)
+
+    def e2e_pipelined(self, x_host, out_host, steps):
+        """Each step's images copied on a second stream while the previous step trains (2 buffers)."""
+        return _pipelined(self, self.x, x_host, out_host, lambda: self.seq.w, steps)
 
     def host_io(self):
         xh = self.torch.from_numpy(self.wl.X).pin_memory()
@@ -446,9 +448,11 @@ class C1Step(SeqBase):
         self.graph = pipeline.StepGraph(body)
         self.stages = ["step"]
 
-    def run(self, ev=None):
+    def run(self, ev=None, src=None):
         if ev is not None:
             ev[0].record()
+        if src is not None and src.data_ptr() != self.x.data_ptr():
+            self.x.copy_(src)  # the captured graph reads self.x (a 6 KB device copy)
         self.graph.replay()
         if ev is not None:
             ev[1].record()
