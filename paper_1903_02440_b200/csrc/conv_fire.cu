@@ -413,7 +413,8 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
                      cudaStream_t s);
 
 static int conv_path_override();
-int conv_walk_describe(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, int* pre, int* chunks);
+int conv_walk_describe(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, int* pre, int* chunks,
+                       int* launches);
 bool conv_tct_applies(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta);
 
 // Which kernels one snn_conv_fire call (pot_out == NULL) launches, for measurement: path 0 = fused
@@ -426,11 +427,11 @@ int conv_fire_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW, i
   if (inf) { *path = 2; *launches = conv_tc_launches(B, C, H, W, pad, KH, KW, F); return SNN_OK; }
   const int ov = conv_path_override();
   if (ov == 0 && conv_tct_applies(B, C, H, W, pad, F, KH, KW, T, theta)) { *path = 3; *launches = 2; return SNN_OK; }
-  int pre = 0, ch = 1;
-  if (ov <= 1 && conv_walk_describe(B, C, H, W, pad, F, KH, KW, T, &pre, &ch)) {
+  int pre = 0, ch = 1, nl = 0;
+  if (ov <= 1 && conv_walk_describe(B, C, H, W, pad, F, KH, KW, T, &pre, &ch, &nl)) {
     *path = pre ? 1 : 0;
     *chunks = ch;
-    *launches = pre ? 1 + 2 * ch : 2;
+    *launches = nl;  // weight prep + walk (latency mode: the walk converts the weights itself), or per chunk
     return SNN_OK;
   }
   *path = 4; *launches = 2;

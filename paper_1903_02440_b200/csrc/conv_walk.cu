@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(512) rf_sort_kernel(const WalkArgs a) {
   }
 }
 
-template <int FPL, int PPW, bool PRE>
+template <int FPL, int PPW, bool PRE, bool WCONV = false>
 __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(const WalkArgs a) {
   pdl_wait();
   constexpr int LPP = 32 / PPW;
@@ -86,7 +86,21 @@ __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(
   uint16_t* start = reinterpret_cast<uint16_t*>(pb + a.start_off);
   uint32_t* list = reinterpret_cast<uint32_t*>(pb + a.list_off);  // fused: the sorted list; PRE: the ring
   const int g = blockIdx.y;
-  {
+  if constexpr (WCONV) {  // fixed point straight from the fp32 weights (exact domain checked, N1)
+    uint32_t* dst = reinterpret_cast<uint32_t*>(smem);
+    for (int i = tid; i < (R + 1) * FGS; i += blockDim.x) {
+      const int e = i / FGS, f = g * FGS + (i - (i / FGS) * FGS);
+      uint32_t u = 0;
+      if (f < a.F && e < R) {
+        const float x = __ldg(a.wf32 + int64_t(f) * R + e);
+        const float sx = x * 2147483648.0f;  // exact power-of-two scaling
+        if (!(x >= 0.0f && x <= 1.0f) || sx != truncf(sx)) flag_error(a.err, kErrInexact);
+        else u = uint32_t(sx);
+      }
+      dst[i] = u;
+    }
+    rf_tables(a, smem);
+  } else {
     const uint4* src = reinterpret_cast<const uint4*>(a.wq + int64_t(g) * (R + 1) * FGS);
     uint4* dst = reinterpret_cast<uint4*>(smem);
     const int n4 = (R + 1) * FGS / 4;
@@ -338,9 +352,9 @@ size_t conv_walk_workspace(int B, int C, int H, int W, int pad, int F, int KH, i
   return n + 256;
 }
 
-template <int FPL, int PPW, bool PRE>
+template <int FPL, int PPW, bool PRE, bool WCONV = false>
 static int walk_go(const WalkPlan& pl, const WalkArgs& a, cudaStream_t s) {
-  auto k = conv_walk_kernel<FPL, PPW, PRE>;
+  auto k = conv_walk_kernel<FPL, PPW, PRE, WCONV>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_conv_fire(walk): %s", cudaGetErrorString(e));
   int occ = 1;
@@ -394,10 +408,12 @@ int rf_sort_lists_launch(const uint8_t* lat_in, int B, int C, int H, int W, int 
 }
 
 // Plan description for snn_conv_fire_plan: 0 if the walk does not apply, else 1 (+ *pre, *chunks).
-int conv_walk_describe(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, int* pre, int* chunks) {
+int conv_walk_describe(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, int* pre, int* chunks,
+                       int* launches) {
   WalkPlan pl;
   if (!walk_plan(B, C, H, W, pad, F, KH, KW, T, &pl)) return 0;
   *pre = pl.pre ? 1 : 0;
+  *launches = pl.pre ? 1 + 2 * int(ceil_div(int64_t(B) * pl.a.Ho * pl.a.Wo, pl.chunk)) : (pl.ppw == 1 ? 1 : 2);
   *chunks = int(ceil_div(int64_t(B) * pl.a.Ho * pl.a.Wo, pl.chunk));
   return 1;
 }
@@ -424,6 +440,15 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
             "warps %d smem %d | rec %d hdr %d chunk %lld npos %lld\n", int(pl.pre), pl.fpl, pl.ppw, pl.FGS,
             pl.n_groups, pl.nwarps, pl.smem, pl.sort_ppw, pl.sort_nwarps, pl.sort_smem, a.rec,
             a.hdr, (long long)pl.chunk, (long long)npos);
+  if (!pl.pre && pl.ppw == 1) {  // latency mode (few positions): the walk converts the weights itself
+    a.wf32 = w;
+    a.p0 = 0; a.np = npos;
+    switch (pl.fpl) {
+      case 4: return walk_go<4, 1, false, true>(pl, a, s);
+      case 2: return walk_go<2, 1, false, true>(pl, a, s);
+      default: return walk_go<1, 1, false, true>(pl, a, s);
+    }
+  }
   int rc = weight_prep_launch(w, F, a.R, pl.FGS, pl.n_groups, reinterpret_cast<uint32_t*>(ws), s);
   if (rc) return rc;
   if (!pl.pre) {
@@ -431,9 +456,9 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
     switch (pl.ppw * 10 + pl.fpl) {
       case 44: return walk_go<4, 4, false>(pl, a, s);
       case 24: return walk_go<4, 2, false>(pl, a, s);
-      case 14: return walk_go<4, 1, false>(pl, a, s);
       case 42: return walk_go<2, 4, false>(pl, a, s);
       case 22: return walk_go<2, 2, false>(pl, a, s);
+      case 14: return walk_go<4, 1, false>(pl, a, s);
       case 12: return walk_go<2, 1, false>(pl, a, s);
       default: return walk_go<1, 1, false>(pl, a, s);
     }

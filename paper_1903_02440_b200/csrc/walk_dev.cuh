@@ -43,6 +43,9 @@ struct WalkArgs {
   // patch_n = 0 disables it.  Tables: ptab (patch index -> input offset), pkk (ky << 8 | kx),
   // eoffp (receptive-field entry -> patch index); the patch sits at warp base + patch_off.
   int patch_w, patch_n, patch_off, off_ptab, off_pkk, off_eoffp;
+  // fused schedule: the fp32 weights [F][R], converted to fixed point while staged into shared memory
+  // (no separate weight-prep launch); nullptr = copy the prepared wq
+  const float* wf32;
 };
 
 static inline int al16(int x) { return (x + 15) & ~15; }
