@@ -98,6 +98,25 @@ __global__ void __launch_bounds__(256) pool2x2_v_kernel(const uint8_t* __restric
   }
 }
 
+// 2 x 2 / stride 2, latencies only, W % 4 == 0 (C2's first pool): one thread per 4-byte word of a
+// row pair, the window minima by byte-wise SIMD (__vminu4), two outputs per 16-bit store; consecutive
+// threads on consecutive words (coalesced).
+__global__ void __launch_bounds__(256) pool2x2_lat_kernel(const uint8_t* __restrict__ lat, uint32_t words, int H,
+                                                          int W, int Ho, uint8_t* __restrict__ lat_out) {
+  pdl_begin();
+  const uint32_t wpr = uint32_t(W) >> 2;  // words per input row
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < words; q += gridDim.x * blockDim.x) {
+    const uint32_t row = q / wpr, w = q - row * wpr;  // row = bf * Ho + oy
+    const uint32_t bf = row / uint32_t(Ho), oy = row - bf * uint32_t(Ho);
+    const uint8_t* in = lat + (size_t(bf) * H + 2 * oy) * W + 4 * w;
+    const uint32_t a = __ldg(reinterpret_cast<const uint32_t*>(in));
+    const uint32_t c = __ldg(reinterpret_cast<const uint32_t*>(in + W));
+    const uint32_t m = __vminu4(a, c);
+    const uint32_t p = __vminu4(m, m >> 8);  // bytes 0 and 2: the two windows' minima
+    *reinterpret_cast<uint16_t*>(lat_out + size_t(row) * (W >> 1) + 2 * w) = uint16_t((p & 0xFFu) | ((p >> 8) & 0xFF00u));
+  }
+}
+
 // Latency-only pooling (no v): one thread per output ROW of one plane walks its Wo windows left to
 // right -- no per-output index arithmetic, every input byte of a stride = window layer loaded once
 // (through L1), consecutive threads on consecutive rows.
@@ -144,6 +163,12 @@ int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, 
     if (pb > int64_t(num_sms()) * 16) pb = int64_t(num_sms()) * 16;
     launch_k(pool2x2_v_kernel, dim3(int(pb)), dim3(256), 0, s, lat, v, pairs, H, W, Ho, Wo, (flags & SNN_POOL_VFINAL) ? 1 : 0, lat_out,
                                               v_out);
+  } else if (small && !v_out && PH == 2 && PW == 2 && SH == 2 && SW == 2 && DH == 0 && DW == 0 && W % 4 == 0 &&
+             Wo * 2 == W) {
+    const uint32_t words = uint32_t(int64_t(B) * F * Ho * (W / 4));
+    int64_t wb = ceil_div(words, 256);
+    if (wb > int64_t(num_sms()) * 16) wb = int64_t(num_sms()) * 16;
+    launch_k(pool2x2_lat_kernel, dim3(int(wb)), dim3(256), 0, s, lat, words, H, W, Ho, lat_out);
   } else if (small && !v_out && PH * PW <= 16) {  // small windows: one thread per output row
     const uint32_t rows = uint32_t(int64_t(B) * F * Ho);
     int64_t rb = ceil_div(rows, 256);

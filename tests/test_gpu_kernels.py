@@ -295,3 +295,14 @@ def test_conv_inf_prepared(G, orc, B, C, H, W, F, K, pad):
     for b in range(B):
         gl, gv = G.conv_fire_prepared(prep, b, C, H, W, gw, pad, 30)
         assert np.array_equal(host(gl)[0], ol[b]) and np.array_equal(host(gv)[0], ov[b]), b
+
+
+@pytest.mark.parametrize("shape", [(2, 3, 16, 24), (1, 30, 28, 28), (2, 2, 7, 8)])
+def test_pool_2x2_latency_only(G, orc, shape):
+    """2 x 2 / stride 2 pooling of latencies alone on W % 4 == 0 maps (the byte-SIMD word kernel)."""
+    rng = np.random.default_rng(sum(shape))
+    lat = rng.integers(0, 9, shape).astype(np.uint8)
+    lat[rng.random(shape) < 0.5] = NS
+    gl, _ = G.pool(cu(lat), None, 2)
+    ol, _ = orc.pool(lat, None, 2, 2, 2, 2, 0, 0, T=9)
+    assert np.array_equal(host(gl), ol)
