@@ -306,3 +306,15 @@ def test_pool_2x2_latency_only(G, orc, shape):
     gl, _ = G.pool(cu(lat), None, 2)
     ol, _ = orc.pool(lat, None, 2, 2, 2, 2, 0, 0, T=9)
     assert np.array_equal(host(gl), ol)
+
+
+@pytest.mark.parametrize("shape,win,stride", [((3, 7, 14, 14), 3, 3), ((2, 4, 12, 10), 2, 1), ((2, 3, 8, 8), 3, 2),
+                                              ((1, 250, 14, 14), 3, 3)])
+def test_pool_small_planes(G, orc, shape, win, stride):
+    """Latency-only pooling of planes of <= 256 entries (one thread per plane through shared memory)."""
+    rng = np.random.default_rng(sum(shape) + win)
+    lat = rng.integers(0, 9, shape).astype(np.uint8)
+    lat[rng.random(shape) < 0.5] = NS
+    gl, _ = G.pool(cu(lat), None, win, stride)
+    ol, _ = orc.pool(lat, None, win, win, stride, stride, 0, 0, T=9)
+    assert np.array_equal(host(gl), ol)
