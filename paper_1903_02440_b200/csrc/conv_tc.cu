@@ -15,6 +15,7 @@
 // allocator, warps 4..7 = epilogue (TMEM lane quadrant = warp % 4).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -23,7 +24,10 @@ namespace snn {
 
 constexpr int kTcM = 128;          // UMMA M (one CTA)
 constexpr int kTcKT = 128;         // bytes (= int8 elements) of K per pipeline stage
-constexpr int kTcStages = 4;
+#ifndef SNN_TC_STAGES
+#define SNN_TC_STAGES 4
+#endif
+constexpr int kTcStages = SNN_TC_STAGES;
 constexpr int kTcThreads = 256;
 
 struct TcPlan {
@@ -61,6 +65,10 @@ static TcPlan tc_plan(int B, int C, int H, int W, int pad, int KH, int KW, int F
   p.Mt = int(ceil_div(p.M, kTcM));
   p.Kt = p.Kp / kTcKT;
   p.nch = int(ceil_div(F, 64));
+  if (const char* e = getenv("SNN_TC_NCH")) {  // tuning experiments: feature chunks (N = 4 * ceil(F / nch) <= 256)
+    const int v = atoi(e);
+    if (v >= p.nch && v <= F) p.nch = v;
+  }
   p.Fc = int(ceil_div(ceil_div(F, p.nch), 4)) * 4;
   p.N = 4 * p.Fc;
   p.a_bytes = size_t(p.Mt) * p.Kt * kTcM * kTcKT;
