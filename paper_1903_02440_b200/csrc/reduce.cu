@@ -415,12 +415,11 @@ __global__ void __launch_bounds__(256) kwta_topk_kernel(const uint8_t* __restric
   }
 }
 
-// Stage 2 (one CTA per image): k rounds of a block argmin over positions.  A position inside the
-// radius of a previous winner is skipped (inhibited in all maps); a position whose best feature has
-// been excluded is re-evaluated over the remaining features and its key written back.  The per-image
-// key map is staged in shared memory when it fits (<= 16384 positions).
+// Stage 2 (one CTA per image): k rounds of a block argmin over positions.  After each round the
+// winner's (2r+1)^2 window is cleared (inhibited in all maps) and the positions whose best feature
+// won are re-evaluated over the remaining features.  The per-image key map is staged in shared
+// memory when it fits (<= 16384 positions).
 constexpr int kKwtaThreads = 1024;
-constexpr int kMaxK = 256;
 constexpr int kKwtaSmemPos = 16384;
 constexpr int kKwtaQueue = 4096;
 
@@ -433,9 +432,8 @@ __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t
   pdl_begin();
   extern __shared__ uint64_t dyn[];  // [HW] current keys, then (topk) [HW] list cursors (u8)
   __shared__ uint32_t fexcl[256];  // bitmask of excluded features (F <= 8192)
-  __shared__ int wy[kMaxK], wx[kMaxK];
   __shared__ uint64_t red[32];
-  __shared__ int s_count, s_qn;
+  __shared__ int s_count, s_qn, s_wf, s_wy, s_wx;
   __shared__ int queue[kKwtaQueue];
   const int b = blockIdx.x;
   const int HW = H * W;
@@ -452,60 +450,20 @@ __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t
       dyn[p] = pbg[p];
       if (topk) cur[p] = 0;
     }
-  if (threadIdx.x == 0) s_count = 0;
+  if (threadIdx.x == 0) { s_count = 0; s_qn = 0; }
   __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  // Invariant between rounds: every live key in pb[] is a valid candidate -- its position is outside
+  // the radius of every winner so far and its feature has not won.  The winner of a round therefore
+  // is a plain argmin, and only the round's own winner has to be applied afterwards: its (2r+1)^2
+  // window is killed directly and the positions whose key carries the winning feature (an index
+  // range test, no division) move to their next candidate.  Those re-evaluations are folded into the
+  // next round's argmin, so a round costs three barriers and O(H*W / threads) shared loads.
   for (int round = 0; round < k; ++round) {
-    const int nw = s_count;
     uint64_t best = ~uint64_t(0);
-    if (threadIdx.x == 0) s_qn = 0;
-    __syncthreads();
-    for (int p = threadIdx.x; p < HW; p += blockDim.x) {
-      const uint64_t key = pb[p];
-      if (key == ~uint64_t(0)) continue;
-      const int y = p / W, x = p - (p / W) * W;
-      bool near = false;
-      for (int i = 0; i < nw; ++i) near |= (abs(y - wy[i]) <= r) && (abs(x - wx[i]) <= r);
-      if (near) continue;
-      const int f = int(uint32_t(key & 0xFFFFFFu) / uint32_t(HW));
-      if (tk && (fexcl[f >> 5] >> (f & 31) & 1)) {  // its best feature already won: next in its list
-        int c = cur[p];
-        uint64_t kk = key;
-        for (;;) {
-          ++c;
-          kk = c < M ? tk[int64_t(p) * M + c] : ~uint64_t(0);
-          if (kk == ~uint64_t(0)) break;
-          const int ff = int(uint32_t(kk & 0xFFFFFFu) / uint32_t(HW));
-          if (!(fexcl[ff >> 5] >> (ff & 31) & 1)) break;
-        }
-        cur[p] = uint8_t(c < M ? c : M);
-        pb[p] = kk;
-        best = kk < best ? kk : best;
-        continue;
-      }
-      if (fexcl[f >> 5] >> (f & 31) & 1) {  // its best feature already won: re-evaluate below
-        const int slot = atomicAdd(&s_qn, 1);
-        if (slot < kKwtaQueue) queue[slot] = p;
-        else {  // queue overflow (rare): serial re-evaluation by this thread
-          uint64_t kk2 = ~uint64_t(0);
-          for (int ff = 0; ff < F; ++ff) {
-            if (fexcl[ff >> 5] >> (ff & 31) & 1) continue;
-            const uint8_t l = lb[ff * HW + p];
-            if (l == kNoSpike) continue;
-            const uint64_t kk = wta_key(l, vb[ff * HW + p], uint32_t(ff * HW + p));
-            kk2 = kk < kk2 ? kk : kk2;
-          }
-          pb[p] = kk2;
-          best = kk2 < best ? kk2 : best;
-        }
-        continue;
-      }
-      best = key < best ? key : best;
-    }
-    __syncthreads();
-    {  // one warp per queued position: lanes scan the features, warp-min, write the key back
+    {  // positions queued by the previous round: one warp each, lanes scan the features
       const int qn = s_qn < kKwtaQueue ? s_qn : kKwtaQueue;
-      for (int qi = wid; qi < qn; qi += (blockDim.x >> 5)) {
+      for (int qi = wid; qi < qn; qi += nwarps) {
         const int p = queue[qi];
         uint64_t key = ~uint64_t(0);
         for (int ff = lane; ff < F; ff += 32) {
@@ -520,27 +478,82 @@ __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t
         best = key < best ? key : best;
       }
     }
+    for (int p = threadIdx.x; p < HW; p += blockDim.x) {
+      const uint64_t key = pb[p];  // a queued position reads ~0 or its new key: both are counted
+      best = key < best ? key : best;
+    }
     best = warp_min_u64(best);
     if (lane == 0) red[wid] = best;
     __syncthreads();
     if (wid == 0) {
-      uint64_t x = lane < (blockDim.x >> 5) ? red[lane] : ~uint64_t(0);
+      uint64_t x = lane < nwarps ? red[lane] : ~uint64_t(0);
       x = warp_min_u64(x);
-      if (lane == 0 && x != ~uint64_t(0)) {
-        const int idx = int(x & 0xFFFFFFu);
-        const int f = idx / HW, p = idx - f * HW;
-        const int y = p / W, xx = p - y * W;
-        const int c = s_count;
-        winners[(int64_t(b) * k + c) * 3 + 0] = f;
-        winners[(int64_t(b) * k + c) * 3 + 1] = y;
-        winners[(int64_t(b) * k + c) * 3 + 2] = xx;
-        wy[c] = y; wx[c] = xx;
-        fexcl[f >> 5] |= 1u << (f & 31);
-        s_count = c + 1;
+      if (lane == 0) {
+        s_qn = 0;
+        if (x != ~uint64_t(0)) {
+          const int idx = int(x & 0xFFFFFFu);
+          const int f = idx / HW, p = idx - f * HW;
+          const int y = p / W, xx = p - y * W;
+          const int c = s_count;
+          winners[(int64_t(b) * k + c) * 3 + 0] = f;
+          winners[(int64_t(b) * k + c) * 3 + 1] = y;
+          winners[(int64_t(b) * k + c) * 3 + 2] = xx;
+          s_wf = f; s_wy = y; s_wx = xx;
+          fexcl[f >> 5] |= 1u << (f & 31);
+          s_count = c + 1;
+        }
       }
     }
     __syncthreads();
     if (s_count == round) break;  // no candidate left
+    if (round + 1 == k) break;
+    const int wf = s_wf, wyy = s_wy, wxx = s_wx;
+    {  // the winner's window (clipped to the map) leaves every map
+      const int y0 = max(wyy - r, 0), y1 = min(wyy + r, H - 1);
+      const int x0 = max(wxx - r, 0), x1 = min(wxx + r, W - 1);
+      const int ww = x1 - x0 + 1, n = (y1 - y0 + 1) * ww;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int dy = i / ww;
+        pb[(y0 + dy) * W + x0 + (i - dy * ww)] = ~uint64_t(0);
+      }
+    }
+    const uint32_t lo = uint32_t(wf) * uint32_t(HW);
+    for (int p = threadIdx.x; p < HW; p += blockDim.x) {
+      const uint64_t key = pb[p];
+      if (key == ~uint64_t(0) || uint32_t(key & 0xFFFFFFu) - lo >= uint32_t(HW)) continue;
+      const int y = p / W, x = p - y * W;
+      if (abs(y - wyy) <= r && abs(x - wxx) <= r) continue;  // killed by the window above
+      if (tk) {  // next entry of the position's candidate list whose feature has not won
+        int c = cur[p];
+        uint64_t kk;
+        for (;;) {
+          ++c;
+          kk = c < M ? tk[int64_t(p) * M + c] : ~uint64_t(0);
+          if (kk == ~uint64_t(0)) break;
+          const int ff = int(uint32_t(kk & 0xFFFFFFu) / uint32_t(HW));
+          if (!(fexcl[ff >> 5] >> (ff & 31) & 1)) break;
+        }
+        cur[p] = uint8_t(c < M ? c : M);
+        pb[p] = kk;
+        continue;
+      }
+      const int slot = atomicAdd(&s_qn, 1);
+      if (slot < kKwtaQueue) {
+        pb[p] = ~uint64_t(0);
+        queue[slot] = p;
+      } else {  // queue overflow (rare): serial re-evaluation by this thread
+        uint64_t kk2 = ~uint64_t(0);
+        for (int ff = 0; ff < F; ++ff) {
+          if (fexcl[ff >> 5] >> (ff & 31) & 1) continue;
+          const uint8_t l = lb[ff * HW + p];
+          if (l == kNoSpike) continue;
+          const uint64_t kk = wta_key(l, vb[ff * HW + p], uint32_t(ff * HW + p));
+          kk2 = kk < kk2 ? kk : kk2;
+        }
+        pb[p] = kk2;
+      }
+    }
+    __syncthreads();
   }
   for (int i = s_count + threadIdx.x; i < k; i += blockDim.x) {
     winners[(int64_t(b) * k + i) * 3 + 0] = -1;
