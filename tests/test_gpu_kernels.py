@@ -210,7 +210,10 @@ def test_inhibit_vs_oracle(G, orc, F, levels, hw):
                                                  (2, 600, 10, 10, 6, 1, 0.6, 2),    # F > 512: rescan path
                                                  (5, 200, 4, 4, 1, 0, 0.3, 3),      # k = 1: reduction path
                                                  (1, 100, 9, 24, 1, 0, 0.5, 2), (3, 40, 70, 70, 1, 2, 0.1, 1),
-                                                 (2, 8, 5, 5, 1, 0, 0.0, 0)])       # k = 1, nothing spikes
+                                                 (2, 8, 5, 5, 1, 0, 0.0, 0),        # k = 1, nothing spikes
+                                                 (4, 64, 64, 64, 8, 40, 0.3, 2),    # rescan path, window clipped
+                                                 (1, 2, 128, 128, 3, 0, 0.9, 1),    # requeue overflow (smem map)
+                                                 (1, 3, 150, 150, 4, 1, 0.9, 0)])   # requeue overflow (global map)
 def test_k_winners_vs_oracle(G, orc, B, F, H, W, k, r, p, levels):
     import synth
     rng = np.random.default_rng(B * 1000 + F)
