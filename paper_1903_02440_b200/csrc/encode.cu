@@ -124,7 +124,14 @@ __global__ void __launch_bounds__(kEncThreads) enc_hist_kernel(const float* __re
   const int ns = ws.n_slots[g];
   if (ns == 0) return;
   __shared__ uint64_t sp[256];
-  for (int i = threadIdx.x; i < ns; i += blockDim.x) sp[i] = ws.slot_prefix[int64_t(g) * S + i];
+  __shared__ uint32_t dmask[kEncBins / 32];  // previous-level digits of the unresolved prefixes
+  for (int i = threadIdx.x; i < kEncBins / 32; i += blockDim.x) dmask[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+    const uint64_t q = ws.slot_prefix[int64_t(g) * S + i];
+    sp[i] = q;
+    atomicOr(&dmask[uint32_t(q >> 5) & (kEncBins / 32 - 1)], 1u << (uint32_t(q) & 31));
+  }
   __syncthreads();
   const int shp = c_enc_shift[level - 1], sh = c_enc_shift[level];
   const uint64_t mask = (uint64_t(1) << c_enc_bits[level]) - 1;
@@ -138,6 +145,8 @@ __global__ void __launch_bounds__(kEncThreads) enc_hist_kernel(const float* __re
     if (!(v > 0.0f)) continue;
     uint64_t K = enc_key(v, uint32_t(i));
     uint64_t p = K >> shp;
+    const uint32_t dg = uint32_t(p) & (kEncBins - 1);  // a 12-bit digit: most elements leave here
+    if (!(dmask[dg >> 5] >> (dg & 31) & 1)) continue;
     int lo = 0, hi = ns;  // lower_bound
     while (lo < hi) {
       int mid = (lo + hi) >> 1;

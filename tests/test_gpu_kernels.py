@@ -62,6 +62,15 @@ def test_encode_large_path(G, orc, shape, T, seed):
     assert np.array_equal(host(G.encode(cu(x), T)), orc.encode(x, T))
 
 
+@pytest.mark.parametrize("shape,T,seed", [((2, 2, 150, 150), 32, 9), ((1, 3, 90, 91), 15, 10)])
+def test_encode_large_path_continuous(G, orc, shape, T, seed):
+    """Large path, distinct values (every radix level decides on value bits, few elements per cut bin)."""
+    rng = np.random.default_rng(seed)
+    x = rng.random(shape, dtype=np.float32)
+    x[rng.random(shape) < 0.1] = 0
+    assert np.array_equal(host(G.encode(cu(x), T)), orc.encode(x, T))
+
+
 def test_encode_all_equal_and_zero(G, orc):
     x = np.full((2, 3, 20, 20), 0.25, np.float32)
     x[1] = 0
