@@ -312,6 +312,41 @@ int inhibit_launch(const uint8_t* lat, const float* v, int B, int F, int H, int 
 }
 
 // ------------------------------------------------------------------------------------- a6 k-WTA
+// Stage 1 for H*W % 4 == 0: one thread per 4 consecutive positions, one 4-byte latency load per
+// feature (a warp reads 128 contiguous bytes per feature plane), 8 features in flight -- the map is
+// far larger than L2 on the throughput configs, so bytes in flight set the speed.
+__global__ void __launch_bounds__(256) kwta_posbest4_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
+                                                            int B, int F, int HW, uint64_t* __restrict__ pos_best) {
+  pdl_begin();
+  const int HW4 = HW >> 2;
+  const int64_t total = int64_t(B) * HW4;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < total; q += int64_t(gridDim.x) * blockDim.x) {
+    const int b = int(q / HW4), p = (int(q - int64_t(b) * HW4)) << 2;
+    const uint32_t* lp = reinterpret_cast<const uint32_t*>(lat + int64_t(b) * F * HW + p);
+    const float* vp = v + int64_t(b) * F * HW + p;
+    uint64_t best[4] = {~uint64_t(0), ~uint64_t(0), ~uint64_t(0), ~uint64_t(0)};
+    for (int f = 0; f < F; f += 8) {
+      uint32_t l[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) l[u] = f + u < F ? __ldg(lp + (f + u) * HW4) : 0xFFFFFFFFu;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (l[u] == 0xFFFFFFFFu) continue;  // none of the 4 positions spikes in this plane
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint8_t lj = uint8_t(l[u] >> (8 * j));
+          if (lj == kNoSpike) continue;
+          const uint64_t k = wta_key(lj, vp[(f + u) * HW + j], uint32_t((f + u) * HW + p + j));
+          best[j] = k < best[j] ? k : best[j];
+        }
+      }
+    }
+    uint64_t* out = pos_best + int64_t(b) * HW + p;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) out[j] = best[j];
+  }
+}
+
 // Stage 1 (all SMs): best key over features for every position -> pos_best[b][p].
 // 32-bit indexing (F*H*W <= 2^24 is checked at the ABI), 4 features in flight per thread.
 __global__ void __launch_bounds__(256) kwta_posbest_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
@@ -466,12 +501,17 @@ __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t
       for (int qi = wid; qi < qn; qi += nwarps) {
         const int p = queue[qi];
         uint64_t key = ~uint64_t(0);
-        for (int ff = lane; ff < F; ff += 32) {
-          if (fexcl[ff >> 5] >> (ff & 31) & 1) continue;
-          const uint8_t l = lb[ff * HW + p];
-          if (l == kNoSpike) continue;
-          const uint64_t kk = wta_key(l, vb[ff * HW + p], uint32_t(ff * HW + p));
-          key = kk < key ? kk : key;
+        for (int f0 = lane; f0 < F; f0 += 32 * 8) {  // 8 strided latency loads in flight per lane
+          uint8_t l[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) l[u] = f0 + 32 * u < F ? lb[(f0 + 32 * u) * HW + p] : kNoSpike;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int ff = f0 + 32 * u;
+            if (l[u] == kNoSpike || (fexcl[ff >> 5] >> (ff & 31) & 1)) continue;
+            const uint64_t kk = wta_key(l[u], vb[ff * HW + p], uint32_t(ff * HW + p));
+            key = kk < key ? kk : key;
+          }
         }
         key = warp_min_u64(key);
         if (lane == 0) pb[p] = key;
@@ -766,7 +806,13 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
   } else if (total <= kWarpPerPosMax) {
     launch_k(kwta_posbest_warp_kernel, dim3(int(ceil_div(total, 8))), dim3(256), 0, s, lat, v, B, F, int(HW), pb);
   } else {
-    launch_k(kwta_posbest_kernel, dim3(int(blocks)), dim3(256), 0, s, lat, v, B, F, int(HW), pb);
+    if (HW % 4 == 0 && (reinterpret_cast<uintptr_t>(lat) & 3) == 0 && !getenv("SNN_KWTA_POSBEST1")) {
+      int64_t b4 = ceil_div(total / 4, 256);
+      if (b4 > int64_t(num_sms()) * 8) b4 = int64_t(num_sms()) * 8;
+      launch_k(kwta_posbest4_kernel, dim3(int(b4)), dim3(256), 0, s, lat, v, B, F, int(HW), pb);
+    } else {
+      launch_k(kwta_posbest_kernel, dim3(int(blocks)), dim3(256), 0, s, lat, v, B, F, int(HW), pb);
+    }
   }
   note_launch();
   if (lists && HW <= 1024 && !getenv("SNN_KWTA_NOSMALL")) {

@@ -222,7 +222,9 @@ def test_inhibit_vs_oracle(G, orc, F, levels, hw):
                                                  (2, 8, 5, 5, 1, 0, 0.0, 0),        # k = 1, nothing spikes
                                                  (4, 64, 64, 64, 8, 40, 0.3, 2),    # rescan path, window clipped
                                                  (1, 2, 128, 128, 3, 0, 0.9, 1),    # requeue overflow (smem map)
-                                                 (1, 3, 150, 150, 4, 1, 0.9, 0)])   # requeue overflow (global map)
+                                                 (1, 3, 150, 150, 4, 1, 0.9, 0),    # requeue overflow (global map)
+                                                 (2, 20, 100, 100, 6, 2, 0.4, 1),   # 4-position best-key stage
+                                                 (2, 5, 99, 101, 4, 1, 0.5, 2)])    # H*W odd: 1-position stage
 def test_k_winners_vs_oracle(G, orc, B, F, H, W, k, r, p, levels):
     import synth
     rng = np.random.default_rng(B * 1000 + F)
