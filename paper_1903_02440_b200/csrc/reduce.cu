@@ -292,12 +292,82 @@ __global__ void __launch_bounds__(256) inhibit_warp_kernel(const uint8_t* __rest
   }
 }
 
+// H*W % 4 == 0 (aligned maps): one thread per 4 consecutive positions -- 4-byte latency loads and
+// stores, 16-byte potential loads (only for planes where one of the 4 spikes) and stores; 64-bit
+// indexing (B*F*H*W may exceed 2^32: C5 is 2^28 neurons, larger batches are legal).
+__global__ void __launch_bounds__(256) inhibit4_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
+                                                       int B, int F, int64_t HW, uint8_t* __restrict__ lat_out,
+                                                       float* __restrict__ v_out, int16_t* __restrict__ winner_f) {
+  pdl_begin();
+  const int64_t HW4 = HW >> 2, total = int64_t(B) * HW4;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < total; q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = q / HW4, p = (q - b * HW4) << 2;
+    const int64_t base = b * F * HW + p;
+    uint64_t best[4] = {~uint64_t(0), ~uint64_t(0), ~uint64_t(0), ~uint64_t(0)};
+    for (int f0 = 0; f0 < F; f0 += 8) {
+      uint32_t l[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        l[u] = f0 + u < F ? __ldg(reinterpret_cast<const uint32_t*>(lat + base + int64_t(f0 + u) * HW)) : 0xFFFFFFFFu;
+      float4 vv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        vv[u] = l[u] != 0xFFFFFFFFu ? __ldg(reinterpret_cast<const float4*>(v + base + int64_t(f0 + u) * HW))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (l[u] == 0xFFFFFFFFu) continue;
+        const float vj[4] = {vv[u].x, vv[u].y, vv[u].z, vv[u].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint8_t lj = uint8_t(l[u] >> (8 * j));
+          if (lj == kNoSpike) continue;
+          const uint64_t k = wta_key(lj, vj[j], uint32_t(f0 + u));
+          best[j] = k < best[j] ? k : best[j];
+        }
+      }
+    }
+    int fw[4];
+    uint32_t lw[4];
+    float vw[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool any = best[j] != ~uint64_t(0);
+      fw[j] = any ? int(best[j] & 0xFFFFFFu) : -1;
+      lw[j] = any ? uint32_t(best[j] >> 56) : kNoSpike;
+      vw[j] = any ? key_v(best[j]) : 0.0f;
+    }
+    for (int f = 0; f < F; ++f) {
+      const int64_t i = base + int64_t(f) * HW;
+      uint32_t lo = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) lo |= (f == fw[j] ? lw[j] : uint32_t(kNoSpike)) << (8 * j);
+      *reinterpret_cast<uint32_t*>(lat_out + i) = lo;
+      *reinterpret_cast<float4*>(v_out + i) =
+          make_float4(f == fw[0] ? vw[0] : 0.f, f == fw[1] ? vw[1] : 0.f, f == fw[2] ? vw[2] : 0.f,
+                      f == fw[3] ? vw[3] : 0.f);
+    }
+    if (winner_f)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) winner_f[b * HW + p + j] = int16_t(fw[j]);
+  }
+}
+
 int inhibit_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, uint8_t* lat_out, float* v_out,
                    int16_t* winner_f, cudaStream_t s) {
   const int64_t HW = int64_t(H) * W, total = int64_t(B) * HW;
   if (total == 0) return SNN_OK;
   if (total <= kWarpPerPosMax) {
     launch_k(inhibit_warp_kernel, dim3(int(ceil_div(total, 8))), dim3(256), 0, s, lat, v, B, F, HW, lat_out, v_out, winner_f);
+    note_launch();
+    return check_launch("snn_inhibit");
+  }
+  const bool aligned = (reinterpret_cast<uintptr_t>(lat) & 3) == 0 && (reinterpret_cast<uintptr_t>(lat_out) & 3) == 0 &&
+                       (reinterpret_cast<uintptr_t>(v) & 15) == 0 && (reinterpret_cast<uintptr_t>(v_out) & 15) == 0;
+  if (HW % 4 == 0 && aligned && !getenv("SNN_INHIBIT1")) {
+    int64_t b4 = ceil_div(total / 4, 256);
+    if (b4 > int64_t(num_sms()) * 8) b4 = int64_t(num_sms()) * 8;
+    launch_k(inhibit4_kernel, dim3(int(b4)), dim3(256), 0, s, lat, v, B, F, HW, lat_out, v_out, winner_f);
     note_launch();
     return check_launch("snn_inhibit");
   }

@@ -198,7 +198,8 @@ def test_pool_vs_oracle(G, orc, win, stride, pad, with_v):
 
 # ---------------------------------------------------------------------------------------- inhibit
 @pytest.mark.parametrize("F,levels,hw", [(1, 0, (13, 17)), (6, 3, (13, 17)), (30, 0, (13, 17)), (257, 2, (13, 17)),
-                                         (7, 2, (131, 129))])
+                                         (7, 2, (131, 129)),
+                                         (9, 3, (100, 100)), (1, 0, (128, 128)), (40, 2, (96, 96))])  # 4 positions/thread
 def test_inhibit_vs_oracle(G, orc, F, levels, hw):
     """Small maps take the warp-per-position kernel, large ones (> 16384 positions) the thread one."""
     import synth
