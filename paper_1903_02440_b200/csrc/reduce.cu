@@ -386,7 +386,8 @@ int inhibit_launch(const uint8_t* lat, const float* v, int B, int F, int H, int 
 // feature (a warp reads 128 contiguous bytes per feature plane), 8 features in flight -- the map is
 // far larger than L2 on the throughput configs, so bytes in flight set the speed.
 __global__ void __launch_bounds__(256) kwta_posbest4_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
-                                                            int B, int F, int HW, uint64_t* __restrict__ pos_best) {
+                                                            int B, int F, int HW, uint64_t* __restrict__ pos_best,
+                                                            uint8_t* __restrict__ multi) {
   pdl_begin();
   const int HW4 = HW >> 2;
   const int64_t total = int64_t(B) * HW4;
@@ -395,6 +396,7 @@ __global__ void __launch_bounds__(256) kwta_posbest4_kernel(const uint8_t* __res
     const uint32_t* lp = reinterpret_cast<const uint32_t*>(lat + int64_t(b) * F * HW + p);
     const float* vp = v + int64_t(b) * F * HW + p;
     uint64_t best[4] = {~uint64_t(0), ~uint64_t(0), ~uint64_t(0), ~uint64_t(0)};
+    int nspk[4] = {0, 0, 0, 0};
     for (int f = 0; f < F; f += 8) {
       uint32_t l[8];
 #pragma unroll
@@ -408,19 +410,24 @@ __global__ void __launch_bounds__(256) kwta_posbest4_kernel(const uint8_t* __res
           if (lj == kNoSpike) continue;
           const uint64_t k = wta_key(lj, vp[(f + u) * HW + j], uint32_t((f + u) * HW + p + j));
           best[j] = k < best[j] ? k : best[j];
+          ++nspk[j];
         }
       }
     }
     uint64_t* out = pos_best + int64_t(b) * HW + p;
 #pragma unroll
     for (int j = 0; j < 4; ++j) out[j] = best[j];
+    if (multi)
+      *reinterpret_cast<uint32_t*>(multi + int64_t(b) * HW + p) =
+          uint32_t(nspk[0] > 1) | uint32_t(nspk[1] > 1) << 8 | uint32_t(nspk[2] > 1) << 16 | uint32_t(nspk[3] > 1) << 24;
   }
 }
 
 // Stage 1 (all SMs): best key over features for every position -> pos_best[b][p].
 // 32-bit indexing (F*H*W <= 2^24 is checked at the ABI), 4 features in flight per thread.
 __global__ void __launch_bounds__(256) kwta_posbest_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
-                                                           int B, int F, int HW, uint64_t* __restrict__ pos_best) {
+                                                           int B, int F, int HW, uint64_t* __restrict__ pos_best,
+                                                           uint8_t* __restrict__ multi) {
   pdl_begin();
   const int64_t total = int64_t(B) * HW;
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < total; q += int64_t(gridDim.x) * blockDim.x) {
@@ -428,6 +435,7 @@ __global__ void __launch_bounds__(256) kwta_posbest_kernel(const uint8_t* __rest
     const uint8_t* lp = lat + int64_t(b) * F * HW + p;
     const float* vp = v + int64_t(b) * F * HW + p;
     uint64_t best = ~uint64_t(0);
+    int nspk = 0;
     int f = 0;
     for (; f + 4 <= F; f += 4) {
       uint8_t l[4];
@@ -438,6 +446,7 @@ __global__ void __launch_bounds__(256) kwta_posbest_kernel(const uint8_t* __rest
         if (l[u] == kNoSpike) continue;
         const uint64_t k = wta_key(l[u], vp[(f + u) * HW], uint32_t((f + u) * HW + p));
         best = k < best ? k : best;
+        ++nspk;
       }
     }
     for (; f < F; ++f) {
@@ -445,8 +454,10 @@ __global__ void __launch_bounds__(256) kwta_posbest_kernel(const uint8_t* __rest
       if (l == kNoSpike) continue;
       const uint64_t k = wta_key(l, vp[f * HW], uint32_t(f * HW + p));
       best = k < best ? k : best;
+      ++nspk;
     }
     pos_best[q] = best;
+    if (multi) multi[q] = uint8_t(nspk > 1);
   }
 }
 
@@ -533,7 +544,8 @@ __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t
                                                                    int k, int r, uint64_t* __restrict__ pos_best,
                                                                    const uint64_t* __restrict__ topk, int M,
                                                                    int32_t* __restrict__ winners,
-                                                                   int32_t* __restrict__ count, int use_smem) {
+                                                                   int32_t* __restrict__ count, int use_smem,
+                                                                   const uint8_t* __restrict__ multi) {
   pdl_begin();
   extern __shared__ uint64_t dyn[];  // [HW] current keys, then (topk) [HW] list cursors (u8)
   __shared__ uint32_t fexcl[256];  // bitmask of excluded features (F <= 8192)
@@ -647,6 +659,10 @@ __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t
         pb[p] = kk;
         continue;
       }
+      if (multi && !multi[int64_t(b) * HW + p]) {  // its only spiking feature won: nothing left
+        pb[p] = ~uint64_t(0);
+        continue;
+      }
       const int slot = atomicAdd(&s_qn, 1);
       if (slot < kKwtaQueue) {
         pb[p] = ~uint64_t(0);
@@ -677,7 +693,8 @@ size_t k_winners_workspace(int B, int F, int H, int W) {
   (void)F;
   // current key per position + (maps up to kKwtaSmemPos positions) candidate lists of up to kTopM keys
   const size_t per = (size_t(H) * W <= size_t(kKwtaSmemPos)) ? 1 + size_t(kTopM) : 1;
-  return size_t(B) * H * W * sizeof(uint64_t) * per + 256;
+  // + one byte per position: "more than one feature spikes here" (a lone candidate is not rescanned)
+  return size_t(B) * H * W * sizeof(uint64_t) * per + size_t(B) * H * W + 256;
 }
 
 // Stage 2 for small maps with candidate lists (H*W <= 1024: one position per thread): one barrier
@@ -869,19 +886,22 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
   const bool lists = k >= 2 && total <= kWarpPerPosMax && use_smem && M <= kTopM && F <= 512 &&
                      ws_bytes >= size_t(B) * HW * sizeof(uint64_t) * (1 + size_t(M));
   uint64_t* topk = lists ? pb + total : nullptr;
+  const size_t multi_off = size_t(total) * sizeof(uint64_t) * (1 + (lists ? size_t(M) : 0));
+  uint8_t* multi = !lists && ws_bytes >= multi_off + size_t(total) ? static_cast<uint8_t*>(ws) + multi_off : nullptr;
   if (lists) {
     int64_t wb = ceil_div(total, 8);
     if (wb > int64_t(num_sms()) * 32) wb = int64_t(num_sms()) * 32;
     launch_k(kwta_topk_kernel, dim3(int(wb)), dim3(256), 0, s, lat, v, B, F, int(HW), M, pb, topk);
   } else if (total <= kWarpPerPosMax) {
     launch_k(kwta_posbest_warp_kernel, dim3(int(ceil_div(total, 8))), dim3(256), 0, s, lat, v, B, F, int(HW), pb);
+    multi = nullptr;  // (the warp-per-position stage does not count candidates)
   } else {
     if (HW % 4 == 0 && (reinterpret_cast<uintptr_t>(lat) & 3) == 0 && !getenv("SNN_KWTA_POSBEST1")) {
       int64_t b4 = ceil_div(total / 4, 256);
       if (b4 > int64_t(num_sms()) * 8) b4 = int64_t(num_sms()) * 8;
-      launch_k(kwta_posbest4_kernel, dim3(int(b4)), dim3(256), 0, s, lat, v, B, F, int(HW), pb);
+      launch_k(kwta_posbest4_kernel, dim3(int(b4)), dim3(256), 0, s, lat, v, B, F, int(HW), pb, multi);
     } else {
-      launch_k(kwta_posbest_kernel, dim3(int(blocks)), dim3(256), 0, s, lat, v, B, F, int(HW), pb);
+      launch_k(kwta_posbest_kernel, dim3(int(blocks)), dim3(256), 0, s, lat, v, B, F, int(HW), pb, multi);
     }
   }
   note_launch();
@@ -896,7 +916,8 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_k_winners: %s", cudaGetErrorString(e));
   int nthr = kKwtaThreads;  // measured C1 (784 positions): 1024 threads 59 us step, 512 67, 256 70
   if (const char* e = getenv("SNN_KWTA_THREADS")) nthr = atoi(e);  // tuning experiments
-  launch_k(kwta_rounds_kernel, dim3(B), dim3(nthr), smem, s, lat, v, F, H, W, k, r, pb, topk, M, winners, count, use_smem);
+  launch_k(kwta_rounds_kernel, dim3(B), dim3(nthr), smem, s, lat, v, F, H, W, k, r, pb, topk, M, winners, count, use_smem,
+           const_cast<const uint8_t*>(multi));
   note_launch();
   return check_launch("snn_k_winners");
 }
