@@ -45,6 +45,8 @@ def test_version_and_workspaces(L):
     assert L.snn_conv_fire_workspace(1000, 250, 4, 4, 2, 200, 5, 5, 15, float('inf')) > 16000 * 6250
     assert L.snn_conv_fire_workspace(1, 1, 4, 4, 0, 1, 5, 5, 3, 1.0) == 0   # kernel larger than input
     assert L.snn_k_winners_workspace(64, 256, 128, 128) >= 64 * 128 * 128 * 8
+    # large maps: a key per position + the one-byte "several candidates" flag per position
+    assert L.snn_k_winners_workspace(1, 9, 140, 141) >= 140 * 141 * 9
 
 
 def test_host_side_errors_without_gpu(L):
