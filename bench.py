@@ -167,14 +167,12 @@ class C2Step:
                 ev[i].record()
         mark(0)
         snn.filter_bank(self.raw if src is None else src, self.bank, fr["pad"], mode=fr["mode"], out=self.x); mark(1)
-        snn.encode(self.x, T, out=n.lat0, ws=n.ws_enc); mark(2)
-        snn.conv_fire(n.lat0, n.w[0], s1.pad, T, s1.theta, lat_out=n.l1.lat, v_out=n.l1.v, ws=n.l1.ws); mark(3)
-        p = n.l1.pool_spec
-        snn.pool(n.l1.lat, None, (p.PH, p.PW), (p.SH, p.SW), (p.DH, p.DW), lat_out=n.l1.plat); mark(4)
-        snn.conv_fire(n.l1.plat, n.w[1], s2.pad, T, s2.theta, lat_out=n.l2.lat, v_out=n.l2.v, ws=n.l2.ws); mark(5)
-        p = n.l2.pool_spec
-        snn.pool(n.l2.lat, None, (p.PH, p.PW), (p.SH, p.SW), (p.DH, p.DW), lat_out=n.l2.plat); mark(6)
-        snn.conv_fire(n.l2.plat, n.w[2], s3.pad, T, s3.theta, lat_out=n.l3.lat, v_out=n.l3.v, ws=n.l3.ws); mark(7)
+        n.encode(self.x); mark(2)         # channels-last maps from here to layer 3's input
+        n.l1.conv(n.lat0_buf); mark(3)    # no potentials: pool1 needs none
+        n.l1.pool(); mark(4)
+        n.l2.conv(n.l1.out_lat); mark(5)
+        n.l2.pool(); mark(6)
+        n.l3.conv(n.l2.out_lat); mark(7)
         snn.k_winners(n.l3.lat, n.l3.v, 1, 0, winners=n.winners, count=n.count, ws=n.ws_kw); mark(8)
         snn.decide(n.winners, n.count, s3.F, self.wl.extra["n_classes"], None, decision=n.decision,
                    reward=n.reward); mark(9)
@@ -203,7 +201,7 @@ class C2Step:
         for name, lat_in, spec, lo in (("conv1", n.lat0, self.wl.convs[0], n.l1.lat),
                                        ("conv2", n.l1.plat, self.wl.convs[1], n.l2.lat),
                                        ("conv3", n.l2.plat, self.wl.convs[2], n.l3.lat)):
-            out[name] = snn.count_events(lat_in, spec.F, spec.KH, spec.KW, spec.pad, T, lo)
+            out[name] = snn.count_events(lat_in.contiguous(), spec.F, spec.KH, spec.KW, spec.pad, T, lo.contiguous())
             out["_shape_" + name] = (int(lat_in.shape[1]), int(lo.shape[0] * lo.shape[2] * lo.shape[3]))
         return out
 
@@ -246,11 +244,9 @@ class C5Step(C2Step):
             if ev is not None:
                 ev[i].record()
         mark(0)
-        snn.encode(self.x if src is None else src, T, out=n.lat0, ws=n.ws_enc); mark(1)
-        snn.conv_fire(n.lat0, n.w, s.pad, T, s.theta, lat_out=n.l1.lat, v_out=n.l1.v, ws=n.l1.ws); mark(2)
-        p = n.l1.pool_spec
-        snn.pool(n.l1.lat, n.l1.v, (p.PH, p.PW), (p.SH, p.SW), (p.DH, p.DW), lat_out=n.l1.plat, v_out=n.l1.pv)
-        mark(3)
+        n.encode(self.x if src is None else src); mark(1)
+        n.l1.conv(n.lat0_buf); mark(2)    # channels-last in and out (lat, v): coalesced walk loads and stores
+        n.l1.pool(); mark(3)
         snn.inhibit(n.l1.plat, n.l1.pv, lat_out=n.ilat, v_out=n.iv, winner_f=n.wf); mark(4)
         snn.k_winners(n.ilat, n.iv, self.wl.extra["k"], self.wl.extra["r"], winners=n.winners, count=n.count,
                       ws=n.ws_kw); mark(5)
@@ -272,7 +268,7 @@ class C5Step(C2Step):
         n, snn, T = self.net, self.snn, self.wl.T
         self.run()
         s = self.wl.convs[0]
-        return {"conv1": snn.count_events(n.lat0, s.F, s.KH, s.KW, s.pad, T, n.l1.lat)}
+        return {"conv1": snn.count_events(n.lat0.contiguous(), s.F, s.KH, s.KW, s.pad, T, n.l1.lat.contiguous())}
 
     def config(self):
         return {"workload": "c5: BASELINE.json configs[4], throughput stress, T=32", "global_batch": self.B,
@@ -291,8 +287,8 @@ class SeqBase(C2Step):
     plasticity steps (conv+fire -> [inhibit] -> kWTA -> [decide] -> STDP), no host sync per image."""
     def _prefix(self, src=None):
         snn, T = self.snn, self.wl.T
-        snn.encode(self.x if src is None else src, T, out=self.lat0, ws=self.ws_enc)
-        if self.l1 is not None:
+        snn.encode(self.x if src is None else src, T, out=self.lat0, ws=self.ws_enc, nhwc=self.l1 is not None)
+        if self.l1 is not None:  # layer 1 reads and writes channels-last maps, its pool writes planar ones
             self.l1(self.lat0)
         if getattr(self, "prep", None) is not None:  # C4: the theta = +inf layer's A operands, all images
             s2 = self.wl.convs[1]
@@ -339,9 +335,9 @@ class C3Step(SeqBase):
         self.x = torch.from_numpy(wl.X).to(dev)
         _, C, H, W = wl.X.shape
         self.ws_enc = torch.empty(snn.encode_workspace(batch, C, H, W, wl.T), dtype=torch.uint8, device=dev)
-        self.lat0 = torch.empty(wl.X.shape, dtype=torch.uint8, device=dev)
+        self.lat0 = torch.empty((batch, H, W, C), dtype=torch.uint8, device=dev)   # channels-last
         self.l1 = pipeline.Layer(wl.convs[0], torch.from_numpy(wl.weights[0]).to(dev), batch, C, H, W, wl.T,
-                                 wl.pools[0], pool_v=False, device=dev)
+                                 wl.pools[0], pool_v=False, device=dev, nhwc=True, want_v=False, in_nhwc=True)
         self._prefix()
         s2 = wl.convs[1]
         if pipeline.SeqPersistent.supported(s2, tuple(self.l1.plat.shape), wl.weights[1].shape, wl.T, wl.extra["k"]):
@@ -381,9 +377,9 @@ class C4Step(SeqBase):
         self.x = torch.from_numpy(wl.X).to(dev)
         _, C, H, W = wl.X.shape
         self.ws_enc = torch.empty(snn.encode_workspace(batch, C, H, W, wl.T), dtype=torch.uint8, device=dev)
-        self.lat0 = torch.empty(wl.X.shape, dtype=torch.uint8, device=dev)
+        self.lat0 = torch.empty((batch, H, W, C), dtype=torch.uint8, device=dev)   # channels-last
         self.l1 = pipeline.Layer(wl.convs[0], torch.from_numpy(wl.weights[0]).to(dev), batch, C, H, W, wl.T,
-                                 wl.pools[0], pool_v=False, device=dev)
+                                 wl.pools[0], pool_v=False, device=dev, nhwc=True, want_v=False, in_nhwc=True)
         self.seq = pipeline.SeqSTDP(wl.convs[1], wl.weights[1], wl.convs[0].F, self.l1.PHo, self.l1.PWo, wl.T,
                                     1, 0, False, wl.extra["stdp"], n_classes=wl.extra["n_classes"], device=dev)
         self.labels = torch.from_numpy(wl.extra["labels"].astype(np.int32)).to(dev)

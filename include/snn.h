@@ -97,6 +97,10 @@ SNN_API int snn_encode(const float* x, int B, int C, int H, int W, int T, uint8_
 #define SNN_BINS_R1 0
 #define SNN_BINS_PROPORTIONAL 1
 #define SNN_BINS_FLOOR 2
+/* or'ed into bins: lat is written channels-last [B, H, W, C] (the ranking still uses the planar flat
+ * index c*H*W + y*W + x; only the storage changes) -- the input layout of snn_conv_fire_ex
+ * SNN_CONV_IN_NHWC. */
+#define SNN_ENCODE_OUT_NHWC 0x100
 SNN_API int snn_encode_ex(const float* x, int B, int C, int H, int W, int T, int bins, uint8_t* lat,
                           void* ws, size_t ws_bytes, snn_stream_t s);
 
@@ -122,7 +126,7 @@ SNN_API int snn_validate_lat(const uint8_t* lat, size_t n, int T, int32_t* n_bad
  * every weight must satisfy w*2^31 integral and 0 <= w <= 1 (true for every w in {0} U [2^-8, 1]).
  * A weight outside that domain sets the device error word (SNN_EINEXACT at snn_sync_status()).
  *   lat_in  uint8 [B, C, H, W];   w float32 [F, C, KH, KW]
- *   lat_out uint8 [B, F, Ho, Wo]; v_out float32 [B, F, Ho, Wo]
+ *   lat_out uint8 [B, F, Ho, Wo]; v_out float32 [B, F, Ho, Wo] or NULL (not written)
  *   pot_out float32 [B, T, F, Ho, Wo] or NULL: if non-NULL every fp32(P[t]) is written (validation
  *           mode, no early exit).
  * Workspace: snn_conv_fire_workspace(..., theta) bytes.  theta = +inf without pot_out runs the
@@ -135,6 +139,22 @@ SNN_API int snn_conv_fire(const uint8_t* lat_in, int B, int C, int H, int W, int
                   const float* w, int F, int KH, int KW, int T, float theta,
                   uint8_t* lat_out, float* v_out, float* pot_out,
                   void* ws, size_t ws_bytes, snn_stream_t s);
+
+/* snn_conv_fire with options (same arguments, workspace and errors; flags = 0 is snn_conv_fire).
+ *   SNN_CONV_OUT_NHWC  lat_out and v_out are channels-last [B, Ho, Wo, F] (pot_out keeps its layout).
+ *                      The finite-threshold walk assigns features to lanes, so a position's outputs
+ *                      are contiguous in this layout and its stores coalesce (the planar layout puts
+ *                      every feature in a separate plane); snn_pool_ex(SNN_POOL_IN_NHWC) reads it.
+ *   SNN_CONV_IN_NHWC   lat_in is channels-last [B, H, W, C] (snn_encode_ex SNN_ENCODE_OUT_NHWC,
+ *                      snn_pool_ex SNN_POOL_OUT_NHWC): a receptive field is KH x KW runs of C contiguous
+ *                      bytes.  Not with pot_out or SNN_CONV_PATH=tct/ref (SNN_EINVAL).
+ * v_out may be NULL in both calls: the potentials are then not written (a layer whose consumer only
+ * needs spike times, e.g. latency-only pooling).  Unknown flag bits: SNN_EINVAL. */
+#define SNN_CONV_OUT_NHWC 1
+#define SNN_CONV_IN_NHWC 2
+SNN_API int snn_conv_fire_ex(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F,
+                             int KH, int KW, int T, float theta, int flags, uint8_t* lat_out, float* v_out,
+                             float* pot_out, void* ws, size_t ws_bytes, snn_stream_t s);
 
 /* Sequential theta = +inf layers (C4's R-STDP layer: one image at a time, new weights every image).
  * The A operand of Eq. 5 (the binary im2col of each image's S[T-1]) does not depend on the weights, so
@@ -170,9 +190,15 @@ SNN_API int snn_pool(const uint8_t* lat, const float* v, int B, int F, int H, in
  *                   Requires H + 2 DH >= SH and W + 2 DW >= SW instead of the window rule.
  *   SNN_POOL_VFINAL v_out = max of v over EVERY spiking entry of the window (the pooled potentials
  *                   tensor at t = T - 1, for v = final potentials: the A13 tie-break variant).
+ *   SNN_POOL_IN_NHWC / SNN_POOL_OUT_NHWC channels-last layouts (below); combine with the other two.
  * flags = 0 is snn_pool.  Unknown bits: SNN_EINVAL. */
 #define SNN_POOL_EQ3 1
 #define SNN_POOL_VFINAL 2
+#define SNN_POOL_IN_NHWC 4  /* lat, v are channels-last [B, H, W, F] (snn_conv_fire_ex SNN_CONV_OUT_NHWC);
+                               lat_out, v_out are [B, F, Ho, Wo] unless SNN_POOL_OUT_NHWC.  Requires
+                               H*W*F < 2^32; planar output also B, Ho <= 65535. */
+#define SNN_POOL_OUT_NHWC 8 /* with SNN_POOL_IN_NHWC only: lat_out, v_out channels-last [B, Ho, Wo, F]
+                               (the input layout of snn_conv_fire_ex SNN_CONV_IN_NHWC) */
 SNN_API int snn_pool_ex(const uint8_t* lat, const float* v, int B, int F, int H, int W, int PH, int PW, int SH,
                         int SW, int DH, int DW, int flags, uint8_t* lat_out, float* v_out, snn_stream_t s);
 

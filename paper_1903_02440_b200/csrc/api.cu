@@ -23,7 +23,7 @@ int conv_fire_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW, i
                    int* launches, int* chunks);
 int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
                      int KW, int T, float theta, uint8_t* lat_out, float* v_out, float* pot_out, void* ws,
-                     size_t ws_bytes, cudaStream_t s);
+                     size_t ws_bytes, cudaStream_t s, int nhwc, int in_nhwc);
 int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, int PH, int PW, int SH, int SW,
                 int DH, int DW, int flags, uint8_t* lat_out, float* v_out, cudaStream_t s);
 int inhibit_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, uint8_t* lat_out, float* v_out,
@@ -194,7 +194,8 @@ int snn_lateral_inhibition(const float* x, int B, int C, int H, int W, const flo
 int snn_encode_ex(const float* x, int B, int C, int H, int W, int T, int bins, uint8_t* lat, void* ws,
                   size_t ws_bytes, snn_stream_t s) {
   REQUIRE(T >= 1 && T <= 254, SNN_EINVAL, "snn_encode: T=%d outside [1, 254]", T);
-  REQUIRE(bins >= SNN_BINS_R1 && bins <= SNN_BINS_FLOOR, SNN_EINVAL, "snn_encode: bins=%d unknown", bins);
+  REQUIRE((bins & 0xFF) <= SNN_BINS_FLOOR && (bins & ~(0xFF | SNN_ENCODE_OUT_NHWC)) == 0, SNN_EINVAL,
+          "snn_encode: bins=0x%x unknown", bins);
   REQUIRE(B >= 0 && C >= 0 && H >= 0 && W >= 0, SNN_ESHAPE, "snn_encode: negative dimension");
   REQUIRE(int64_t(C) * H * W < (int64_t(1) << 24), SNN_ESHAPE, "snn_encode: C*H*W >= 2^24");
   if (int64_t(B) * C * H * W == 0) return SNN_OK;
@@ -287,23 +288,32 @@ int snn_conv_fire_plan(int B, int C, int H, int W, int pad, int F, int KH, int K
   return conv_fire_plan(B, C, H, W, pad, F, KH, KW, T, theta, path, launches, chunks);
 }
 
+int snn_conv_fire_ex(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
+                     int KW, int T, float theta, int flags, uint8_t* lat_out, float* v_out, float* pot_out, void* ws,
+                     size_t ws_bytes, snn_stream_t s) {
+  int rc = conv_checks(B, C, H, W, pad, F, KH, KW, T, theta);
+  if (rc) return rc;
+  REQUIRE((flags & ~(SNN_CONV_OUT_NHWC | SNN_CONV_IN_NHWC)) == 0, SNN_EINVAL, "snn_conv_fire: unknown flags 0x%x", flags);
+  if (B == 0 || F == 0) return SNN_OK;
+  REQUIRE(lat_in && w && lat_out, SNN_EINVAL, "snn_conv_fire: NULL tensor");
+  REQUIRE(ws, SNN_EWORKSPACE, "snn_conv_fire: NULL workspace");
+  return conv_fire_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, theta, lat_out, v_out, pot_out, ws, ws_bytes,
+                          S(s), (flags & SNN_CONV_OUT_NHWC) ? 1 : 0, (flags & SNN_CONV_IN_NHWC) ? 1 : 0);
+}
+
 int snn_conv_fire(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH, int KW,
                   int T, float theta, uint8_t* lat_out, float* v_out, float* pot_out, void* ws, size_t ws_bytes,
                   snn_stream_t s) {
-  int rc = conv_checks(B, C, H, W, pad, F, KH, KW, T, theta);
-  if (rc) return rc;
-  if (B == 0 || F == 0) return SNN_OK;
-  REQUIRE(lat_in && w && lat_out && v_out, SNN_EINVAL, "snn_conv_fire: NULL tensor");
-  REQUIRE(ws, SNN_EWORKSPACE, "snn_conv_fire: NULL workspace");
-  return conv_fire_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, theta, lat_out, v_out, pot_out, ws, ws_bytes,
-                          S(s));
+  return snn_conv_fire_ex(lat_in, B, C, H, W, pad, w, F, KH, KW, T, theta, 0, lat_out, v_out, pot_out, ws, ws_bytes,
+                          s);
 }
 
 int snn_pool_ex(const uint8_t* lat, const float* v, int B, int F, int H, int W, int PH, int PW, int SH, int SW,
                 int DH, int DW, int flags, uint8_t* lat_out, float* v_out, snn_stream_t s) {
   REQUIRE(B >= 0 && F >= 0 && H >= 1 && W >= 1, SNN_ESHAPE, "snn_pool: bad dimensions");
   REQUIRE(PH >= 1 && PW >= 1 && SH >= 1 && SW >= 1 && DH >= 0 && DW >= 0, SNN_EINVAL, "snn_pool: bad window");
-  REQUIRE((flags & ~(SNN_POOL_EQ3 | SNN_POOL_VFINAL)) == 0, SNN_EINVAL, "snn_pool: unknown flags 0x%x", flags);
+  REQUIRE((flags & ~(SNN_POOL_EQ3 | SNN_POOL_VFINAL | SNN_POOL_IN_NHWC | SNN_POOL_OUT_NHWC)) == 0, SNN_EINVAL, "snn_pool: unknown flags 0x%x",
+          flags);
   REQUIRE((flags & SNN_POOL_EQ3) ? (H + 2 * DH >= SH && W + 2 * DW >= SW) : (PH <= H + 2 * DH && PW <= W + 2 * DW),
           SNN_ESHAPE, "snn_pool: window larger than padded input");
   REQUIRE(DH < PH && DW < PW, SNN_EINVAL, "snn_pool: padding must be smaller than the window");

@@ -52,6 +52,7 @@ struct ConvArgs {
   uint8_t* lat_out;
   float* v_out;
   float* pot_out;      // nullable [B][T][F][Ho][Wo]
+  int nhwc;            // lat_out / v_out layout: 0 = [B, F, Ho, Wo], 1 = [B, Ho, Wo, F]
   int ws_off_eoff, ws_off_ekk, ws_off_warps, warp_bytes;
   int cnt_off, start_off, size_off, list_off;
 };
@@ -62,7 +63,7 @@ static inline int align16(int x) { return (x + 15) & ~15; }
 // w [F][R] fp32 -> wq [g][R+1][FGS] uint32 fixed point (w * 2^31).  Flags weights whose value is
 // not an integer multiple of 2^-31 in [0, 1] (outside the exact domain, N1).
 __global__ void weight_prep_kernel(const float* __restrict__ w, int F, int R, int FGS, int n_groups,
-                                   uint32_t* __restrict__ wq) {
+                                   uint32_t* __restrict__ wq, int nhwc_C, int KK) {
   pdl_begin();
   int64_t total = int64_t(n_groups) * (R + 1) * FGS;
   int bad = 0;
@@ -74,7 +75,9 @@ __global__ void weight_prep_kernel(const float* __restrict__ w, int F, int R, in
     int f = g * FGS + j;
     uint32_t u = 0;
     if (f < F && e < R) {
-      float x = w[int64_t(f) * R + e];
+      int se = e;  // nhwc_C > 0: rows ordered (ky, kx, c) for channels-last input (SNN_CONV_IN_NHWC)
+      if (nhwc_C) { const int kk = e / nhwc_C; se = (e - kk * nhwc_C) * KK + kk; }
+      float x = w[int64_t(f) * R + se];
       float s = x * 2147483648.0f;  // exact power-of-two scaling
       if (!(x >= 0.0f && x <= 1.0f) || s != truncf(s)) bad = 1;
       else u = uint32_t(s);
@@ -253,9 +256,9 @@ __global__ void __launch_bounds__(1024, 1) conv_fire_kernel(const ConvArgs a) {
 #pragma unroll
     for (int j = 0; j < FPL; ++j) {
       if (valid >> j & 1) {
-        const int64_t o = (int64_t(b) * a.F + fbase + j) * HoWo + rem;
+        const int64_t o = a.nhwc ? (int64_t(b) * HoWo + rem) * a.F + fbase + j : (int64_t(b) * a.F + fbase + j) * HoWo + rem;
         a.lat_out[o] = lo[j];
-        a.v_out[o] = vo[j];
+        if (a.v_out) a.v_out[o] = vo[j];
       }
     }
     __syncwarp();
@@ -300,9 +303,9 @@ __global__ void __launch_bounds__(256) conv_dense_kernel(const ConvArgs a) {
     }
     const int f = g * 32 + lane;
     if (f < a.F) {
-      const int64_t o = (int64_t(b) * a.F + f) * HoWo + rem;
+      const int64_t o = a.nhwc ? (int64_t(b) * HoWo + rem) * a.F + f : (int64_t(b) * a.F + f) * HoWo + rem;
       a.lat_out[o] = acc > 0 ? uint8_t(a.T - 1) : kNoSpike;
-      a.v_out[o] = fixed_to_float(int64_t(acc));
+      if (a.v_out) a.v_out[o] = fixed_to_float(int64_t(acc));
     }
     if (a.pot_out) {  // validation mode: P[t] for every t (one masked pass per time step)
       for (int t = 0; t < a.T; ++t) {
@@ -395,7 +398,7 @@ size_t conv_walk_workspace(int B, int C, int H, int W, int pad, int F, int KH, i
 size_t conv_tct_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T);
 int conv_tct_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
                     int KW, int T, float theta, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes,
-                    cudaStream_t s);
+                    cudaStream_t s, int nhwc);
 
 // Finite-threshold path selection.  Default: the SIMT delta walk (conv_walk.cu).  SNN_CONV_PATH=tct
 // selects the tensor-core time-stepped kernel (conv_tct.cu; exact, parity-tested, but slower than the
@@ -410,7 +413,7 @@ static int conv_path_override() {
 }
 int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
                      int KW, int T, float theta, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes,
-                     cudaStream_t s);
+                     cudaStream_t s, int nhwc, int in_nhwc);
 
 static int conv_path_override();
 int conv_walk_describe(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, int* pre, int* chunks,
@@ -438,18 +441,19 @@ int conv_fire_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW, i
   return SNN_OK;
 }
 
-int weight_prep_launch(const float* w, int F, int R, int FGS, int n_groups, uint32_t* wq, cudaStream_t s) {
+int weight_prep_launch(const float* w, int F, int R, int FGS, int n_groups, uint32_t* wq, cudaStream_t s,
+                       int nhwc_C, int KK) {
   const int64_t total = int64_t(n_groups) * (R + 1) * FGS;
   int blocks = int(ceil_div(total, 256));
   if (blocks > 2048) blocks = 2048;
   if (blocks < 1) blocks = 1;
-  launch_k(weight_prep_kernel, dim3(blocks), dim3(256), 0, s, w, F, R, FGS, n_groups, wq);
+  launch_k(weight_prep_kernel, dim3(blocks), dim3(256), 0, s, w, F, R, FGS, n_groups, wq, nhwc_C, KK);
   note_launch();
   return check_launch("snn_conv_fire(weight prep)");
 }
 int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH, int KW,
                    int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes, cudaStream_t s,
-                   const uint8_t* aq_pre = nullptr);
+                   const uint8_t* aq_pre = nullptr, int nhwc = 0, int in_nhwc = 0);
 
 size_t conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, float theta) {
   const bool inf = isinf(theta) && theta > 0;
@@ -470,7 +474,7 @@ size_t conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, i
 
 int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
                      int KW, int T, float theta, uint8_t* lat_out, float* v_out, float* pot_out, void* ws,
-                     size_t ws_bytes, cudaStream_t s) {
+                     size_t ws_bytes, cudaStream_t s, int nhwc, int in_nhwc) {
   const bool inf = isinf(theta) && theta > 0;
   ConvPlan pl;
   make_plan(B, C, H, W, pad, F, KH, KW, T, inf, &pl);
@@ -478,7 +482,7 @@ int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   if (pl.dense && !inf)
     return set_error(SNN_ESHAPE, "snn_conv_fire: receptive field R=%d too large for a finite threshold", a.R);
   if (ws_bytes < pl.wq_bytes) return set_error(SNN_EWORKSPACE, "snn_conv_fire: workspace %zu < %zu", ws_bytes, pl.wq_bytes);
-  a.lat_in = lat_in; a.lat_out = lat_out; a.v_out = v_out; a.pot_out = pot_out;
+  a.lat_in = lat_in; a.lat_out = lat_out; a.v_out = v_out; a.pot_out = pot_out; a.nhwc = nhwc;
   a.wq = reinterpret_cast<uint32_t*>(ws);
   if (!inf) {
     double t = floor(double(theta) * 2147483648.0);
@@ -487,21 +491,26 @@ int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   const int64_t npos = int64_t(B) * a.Ho * a.Wo;
   if (npos == 0 || F == 0) return SNN_OK;
   if (inf && !pot_out)  // Eq. 5: dense contraction of S[T-1] on the tensor cores
-    return conv_tc_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, lat_out, v_out, ws, ws_bytes, s);
+    return conv_tc_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, lat_out, v_out, ws, ws_bytes, s, nullptr, nhwc,
+                          in_nhwc);
   const int path = conv_path_override();
+  if (in_nhwc && (pot_out || path != 1))
+    return set_error(SNN_EINVAL, "snn_conv_fire: channels-last input needs the default path without pot_out");
   if (!inf && !pot_out && path == 0) {  // tensor cores, time step by time step (conv_tct.cu)
-    int rc = conv_tct_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, theta, lat_out, v_out, ws, ws_bytes, s);
+    int rc = conv_tct_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, theta, lat_out, v_out, ws, ws_bytes, s, nhwc);
     if (rc != 1) return rc;
   }
   if (!inf && !pot_out && path <= 1) {  // SIMT delta walk (conv_walk.cu); the kernel below validates
-    int rc = conv_walk_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, theta, lat_out, v_out, ws, ws_bytes, s);
+    int rc = conv_walk_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, theta, lat_out, v_out, ws, ws_bytes, s, nhwc,
+                              in_nhwc);
     if (rc != 1) return rc;
+    if (in_nhwc) return set_error(SNN_ESHAPE, "snn_conv_fire: channels-last input: receptive field too large for the walk");
   }
   {
     int64_t total = int64_t(pl.n_groups) * (a.R + 1) * pl.FGS;
     int blocks = int(ceil_div(total, 256));
     if (blocks > 2048) blocks = 2048;
-    weight_prep_kernel<<<blocks, 256, 0, s>>>(w, F, a.R, pl.FGS, pl.n_groups, a.wq);
+    weight_prep_kernel<<<blocks, 256, 0, s>>>(w, F, a.R, pl.FGS, pl.n_groups, a.wq, 0, 1);
     note_launch();
   }
   if (pl.dense) {

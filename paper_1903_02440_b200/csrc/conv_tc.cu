@@ -105,7 +105,8 @@ __device__ __forceinline__ size_t tc_off(int row, int k, int rows_per_tile, int 
 // grid.y > 1: blockIdx.y is an image of a batch prepared image by image (snn_conv_inf_prepare), each
 // with its own one-image plan p and an A block of img_bytes.
 __global__ void tc_prep_a_kernel(const uint8_t* __restrict__ lat_in, int C, int H, int W, int pad, int KH, int KW,
-                                 int Ho, int Wo, int T, TcPlan p, uint8_t* __restrict__ aq, size_t img_bytes) {
+                                 int Ho, int Wo, int T, TcPlan p, uint8_t* __restrict__ aq, size_t img_bytes,
+                                 int in_nhwc) {
   pdl_begin();
   lat_in += int64_t(blockIdx.y) * C * H * W;
   aq += size_t(blockIdx.y) * img_bytes;
@@ -129,7 +130,7 @@ __global__ void tc_prep_a_kernel(const uint8_t* __restrict__ lat_in, int C, int 
       for (int j = 0; j < 16; ++j) {  // addresses and predicates first, then all loads in flight
         const int yy = y + ky - pad, xx = x + kx - pad;
         const bool in = k0 + j < p.K && yy >= 0 && yy < H && xx >= 0 && xx < W;
-        lv[j] = in ? base[(int64_t(c) * H + yy) * W + xx] : 0xFFu;
+        lv[j] = in ? base[in_nhwc ? (int64_t(yy) * W + xx) * C + c : (int64_t(c) * H + yy) * W + xx] : 0xFFu;
         if (++kx == KW) { kx = 0; if (++ky == KH) { ky = 0; ++c; } }
       }
 #pragma unroll
@@ -193,7 +194,7 @@ __global__ void tc_prep_b16_kernel(const float* __restrict__ w, int F, int R, in
 __global__ void __launch_bounds__(256) tc_prep_a_band_kernel(const uint8_t* __restrict__ lat_in, int C, int H, int W,
                                                              int pad, int KH, int KW, int Ho, int Wo, int T,
                                                              TcPlan p, int RB, int nbands, int B, int KS,
-                                                             uint8_t* __restrict__ aq) {
+                                                             uint8_t* __restrict__ aq, int in_nhwc) {
   pdl_begin();
   extern __shared__ uint8_t band[];
   const int Wp = W + 2 * pad, TR = RB + KH - 1, KK = KH * KW, nk16 = p.Kp / 16;
@@ -218,7 +219,8 @@ __global__ void __launch_bounds__(256) tc_prep_a_band_kernel(const uint8_t* __re
     const int nr = iy1 - iy0 + 1, per_c = nr * W;
     for (int i = threadIdx.x; i < C * per_c; i += blockDim.x) {
       const int c = i / per_c, r = i - c * per_c, ry = r / W, ix = r - ry * W;
-      band[(c * TR + iy0 + ry - top) * Wp + ix + pad] = __ldg(lb + (int64_t(c) * H + iy0 + ry) * W + ix) < T ? 1 : 0;
+      const int64_t li = in_nhwc ? (int64_t(iy0 + ry) * W + ix) * C + c : (int64_t(c) * H + iy0 + ry) * W + ix;
+      band[(c * TR + iy0 + ry - top) * Wp + ix + pad] = __ldg(lb + li) < T ? 1 : 0;
     }
   }
   const int mcount = (yb - ya) * Wo, m0 = b * Ho * Wo + ya * Wo;
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(256) tc_prep_a_band_kernel(const uint8_t* __re
 // shared-memory load and one 16-byte global store.
 __global__ void __launch_bounds__(256) tc_prep_a_hwc_kernel(const uint8_t* __restrict__ lat_in, int C, int H, int W,
                                                             int pad, int KH, int KW, int Ho, int Wo, int T, TcPlan p,
-                                                            int B, uint8_t* __restrict__ aq) {
+                                                            int B, uint8_t* __restrict__ aq, int in_nhwc) {
   pdl_begin();
   extern __shared__ __align__(16) uint8_t hband[];
   const int Wp = W + 2 * pad, TR = p.RB + KH - 1, Cp = p.Cp, nk16 = p.Kp / 16;
@@ -266,8 +268,9 @@ __global__ void __launch_bounds__(256) tc_prep_a_hwc_kernel(const uint8_t* __res
     const int npx = (iy1 - iy0 + 1) * W;
     for (int i = threadIdx.x; i < C * npx; i += blockDim.x) {  // channel fastest: conflict-free byte stores
       const int px = i / C, c = i - px * C, ry = px / W, ix = px - ry * W;
-      hband[((iy0 + ry - top) * Wp + ix + pad) * Cp + c] =
-          __ldg(lb + (int64_t(c) * H + iy0 + ry) * W + ix) < T ? 1 : 0;
+      // channels-last input: i runs along memory (coalesced); planar input: a byte gather per channel
+      const int64_t li = in_nhwc ? int64_t(iy0) * W * C + i : (int64_t(c) * H + iy0 + ry) * W + ix;
+      hband[((iy0 + ry - top) * Wp + ix + pad) * Cp + c] = __ldg(lb + li) < T ? 1 : 0;
     }
   }
   __syncthreads();
@@ -291,7 +294,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
                                                                  int HoWo, int T, uint32_t tmem_cols,
                                                                  uint8_t* __restrict__ lat_out,
                                                                  float* __restrict__ v_out,
-                                                                 unsigned long long* __restrict__ part) {
+                                                                 unsigned long long* __restrict__ part, int nhwc) {
   pdl_begin();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -379,9 +382,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
               atomicAdd(part + int64_t(m) * F + f, (unsigned long long)acc);
               continue;
             }
-            const int64_t o = (int64_t(b) * F + f) * HoWo + rem;
+            const int64_t o = nhwc ? int64_t(m) * F + f : (int64_t(b) * F + f) * HoWo + rem;
             lat_out[o] = acc > 0 ? uint8_t(T - 1) : kNoSpike;
-            v_out[o] = fixed_to_float(acc);
+            if (v_out) v_out[o] = fixed_to_float(acc);
           }
         }
       }
@@ -397,22 +400,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
 
 // split-K finalize: the summed fixed-point potentials -> (lat, v) (Eq. 5).
 __global__ void conv_tc_finalize_kernel(const unsigned long long* __restrict__ part, int M, int F, int HoWo, int T,
-                                        uint8_t* __restrict__ lat_out, float* __restrict__ v_out) {
+                                        uint8_t* __restrict__ lat_out, float* __restrict__ v_out, int nhwc) {
   pdl_begin();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < int64_t(M) * F;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int m = int(i / F), f = int(i - int64_t(m) * F);
     const int b = m / HoWo, rem = m - b * HoWo;
     const int64_t acc = int64_t(part[i]);
-    const int64_t o = (int64_t(b) * F + f) * HoWo + rem;
+    const int64_t o = nhwc ? i : (int64_t(b) * F + f) * HoWo + rem;
     lat_out[o] = acc > 0 ? uint8_t(T - 1) : kNoSpike;
-    v_out[o] = fixed_to_float(acc);
+    if (v_out) v_out[o] = fixed_to_float(acc);
   }
 }
 
 int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH, int KW,
                    int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes, cudaStream_t s,
-                   const uint8_t* aq_pre = nullptr);
+                   const uint8_t* aq_pre = nullptr, int nhwc = 0, int in_nhwc = 0);
 
 // A operands of B images, one one-image block each (tc_plan(1, ...)), for later snn_conv_fire_prepared.
 size_t conv_inf_prepare_bytes(int B, int C, int H, int W, int pad, int F, int KH, int KW) {
@@ -429,7 +432,7 @@ int conv_inf_prepare_launch(const uint8_t* lat_in, int B, int C, int H, int W, i
   const int blocks = int(ceil_div(rows16, 256));
   if (B > 65535) return set_error(SNN_ESHAPE, "snn_conv_inf_prepare: B > 65535");
   launch_k(tc_prep_a_kernel, dim3(blocks, B), dim3(256), 0, s, lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p,
-           static_cast<uint8_t*>(prep), p.a_bytes);
+           static_cast<uint8_t*>(prep), p.a_bytes, 0);
   note_launch();
   return check_launch("snn_conv_inf_prepare");
 }
@@ -444,7 +447,7 @@ int conv_fire_prepared_launch(const void* prep, int b, int C, int H, int W, int 
 
 int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH, int KW,
                    int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes, cudaStream_t s,
-                   const uint8_t* aq_pre) {
+                   const uint8_t* aq_pre, int nhwc, int in_nhwc) {
   const int Ho = H + 2 * pad - KH + 1, Wo = W + 2 * pad - KW + 1, R = C * KH * KW;
   TcPlan p = tc_plan(B, C, H, W, pad, KH, KW, F, num_sms());
   const size_t a_off = 0, b_off = (p.a_bytes + 1023) & ~size_t(1023);
@@ -467,16 +470,16 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
   } else {
     if (p.hwc) {
       launch_k(tc_prep_a_hwc_kernel, dim3(unsigned(int64_t(B) * p.nbands + 1)), dim3(256), p.band_smem, s, lat_in, C, H, W, pad, KH, KW,
-                                                                                      Ho, Wo, T, p, B, aq);
+                                                                                      Ho, Wo, T, p, B, aq, in_nhwc);
     } else if (p.band) {
       launch_k(tc_prep_a_band_kernel, dim3(unsigned(int64_t(B) * p.nbands + 1)), dim3(256), p.band_smem, s, 
-          lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p, p.RB, p.nbands, B, 1, aq);
+          lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p, p.RB, p.nbands, B, 1, aq, in_nhwc);
     } else {
       const int64_t rows16 = int64_t(p.Mt) * kTcM * (p.Kp / 16);
       int64_t blocks = ceil_div(rows16, 256);
       if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
       launch_k(tc_prep_a_kernel, dim3(int(blocks)), dim3(256), 0, s, lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p, aq,
-               size_t(0));
+               size_t(0), in_nhwc);
     }
     note_launch();
   }
@@ -486,13 +489,13 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
   cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_conv_fire(tc): %s", cudaGetErrorString(e));
   launch_k(conv_tc_kernel, dim3(unsigned(int64_t(p.Mt) * p.nch * p.KS)), dim3(kTcThreads), smem, s, aq, bq, p, F, Ho * Wo, T, cols,
-                                                                               lat_out, v_out, part);
+                                                                               lat_out, v_out, part, nhwc);
   note_launch();
   if (part) {
     const int64_t n = int64_t(p.M) * F;
     int blocks = int(ceil_div(n, 256));
     if (blocks > num_sms() * 8) blocks = num_sms() * 8;
-    launch_k(conv_tc_finalize_kernel, dim3(blocks), dim3(256), 0, s, part, p.M, F, Ho * Wo, T, lat_out, v_out);
+    launch_k(conv_tc_finalize_kernel, dim3(blocks), dim3(256), 0, s, part, p.M, F, Ho * Wo, T, lat_out, v_out, nhwc);
     note_launch();
   }
   return check_launch("snn_conv_fire(tc)");

@@ -146,6 +146,7 @@ struct T2Args {
   T2Plan p;
   int units;  // tiles * chunks
   int dbg;    // timing experiments only (SNN_TCT_DBG): 1 = no epilogue work, 2 = no MMAs, 4 = no S writes
+  int nhwc;   // output layout [B, Ho, Wo, F] (else [B, F, Ho, Wo])
 };
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(kT2Threads, 1) conv_tct_kernel(const T2Args a)
       const int m = m0 + tid;
       if (m < p.M) {
         const int b = m / HoWo;
-        rowout[tid] = (int64_t(b) * a.F + fbase) * HoWo + (m - b * HoWo);
+        rowout[tid] = a.nhwc ? int64_t(m) * a.F + fbase : (int64_t(b) * a.F + fbase) * HoWo + (m - b * HoWo);
       } else {
         rowout[tid] = -1;
       }
@@ -400,8 +401,9 @@ __global__ void __launch_bounds__(kT2Threads, 1) conv_tct_kernel(const T2Args a)
         const int f = i >> 7, r = i & (kT2M - 1);
         const int64_t o = rowout[r];
         if (o >= 0) {
-          a.lat_out[o + int64_t(f) * HoWo] = sLat[i];
-          a.v_out[o + int64_t(f) * HoWo] = sV[i];
+          const int64_t fo = a.nhwc ? int64_t(f) : int64_t(f) * HoWo;
+          a.lat_out[o + fo] = sLat[i];
+          if (a.v_out) a.v_out[o + fo] = sV[i];
         }
       }
     }
@@ -416,7 +418,7 @@ __global__ void __launch_bounds__(kT2Threads, 1) conv_tct_kernel(const T2Args a)
 // Returns 1 if this path does not apply (caller falls back), else an SNN code.
 int conv_tct_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
                     int KW, int T, float theta, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes,
-                    cudaStream_t s) {
+                    cudaStream_t s, int nhwc) {
   T2Plan p;
   if (!(theta >= 0.0f) || !t2_plan(B, C, H, W, pad, F, KH, KW, T, &p)) return 1;
   if (ws_bytes < p.b_bytes) return 1;
@@ -425,7 +427,7 @@ int conv_tct_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, 
   a.C = C; a.H = H; a.W = W; a.pad = pad; a.KH = KH; a.KW = KW; a.T = T; a.F = F;
   const double tt = floor(double(theta) * 2147483648.0);
   a.thr = tt >= 9.0e18 ? INT64_MAX : int64_t(tt);
-  a.lat_out = lat_out; a.v_out = v_out; a.p = p;
+  a.lat_out = lat_out; a.v_out = v_out; a.p = p; a.nhwc = nhwc;
   a.dbg = getenv("SNN_TCT_DBG") ? atoi(getenv("SNN_TCT_DBG")) : 0;
   const int mtiles = int(ceil_div(p.M, kT2M));
   a.units = mtiles * p.nch;

@@ -36,7 +36,8 @@
 
 namespace snn {
 
-int weight_prep_launch(const float* w, int F, int R, int FGS, int n_groups, uint32_t* wq, cudaStream_t s);
+int weight_prep_launch(const float* w, int F, int R, int FGS, int n_groups, uint32_t* wq, cudaStream_t s,
+                       int nhwc_C = 0, int KK = 1);
 
 // ------------------------------------------------------------------------------------- sort only
 template <int PPW>
@@ -70,14 +71,12 @@ __global__ void __launch_bounds__(512) rf_sort_kernel(const WalkArgs a) {
   }
 }
 
-template <int FPL, int PPW, bool PRE, bool WCONV = false>
-__global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(const WalkArgs a) {
-  pdl_wait();
+// The per-position loop of conv_walk_kernel once the CTA's weight slice is staged (S28: the slice is
+// in units of 2^-28, see walk_block).
+template <int FPL, int PPW, bool PRE, bool S28>
+__device__ __forceinline__ void walk_positions(const WalkArgs& a, unsigned char* smem) {
   constexpr int LPP = 32 / PPW;
   constexpr int FGS = LPP * FPL;
-  static_assert(!PRE || PPW == 1, "presorted walk: one position per warp");
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int R = a.R;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int grp = lane / LPP, gl = lane - grp * LPP;
   unsigned char* wbase = smem + a.off_warps + warp * a.warp_bytes;
@@ -86,29 +85,6 @@ __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(
   uint16_t* start = reinterpret_cast<uint16_t*>(pb + a.start_off);
   uint32_t* list = reinterpret_cast<uint32_t*>(pb + a.list_off);  // fused: the sorted list; PRE: the ring
   const int g = blockIdx.y;
-  if constexpr (WCONV) {  // fixed point straight from the fp32 weights (exact domain checked, N1)
-    uint32_t* dst = reinterpret_cast<uint32_t*>(smem);
-    for (int i = tid; i < (R + 1) * FGS; i += blockDim.x) {
-      const int e = i / FGS, f = g * FGS + (i - (i / FGS) * FGS);
-      uint32_t u = 0;
-      if (f < a.F && e < R) {
-        const float x = __ldg(a.wf32 + int64_t(f) * R + e);
-        const float sx = x * 2147483648.0f;  // exact power-of-two scaling
-        if (!(x >= 0.0f && x <= 1.0f) || sx != truncf(sx)) flag_error(a.err, kErrInexact);
-        else u = uint32_t(sx);
-      }
-      dst[i] = u;
-    }
-    rf_tables(a, smem);
-  } else {
-    const uint4* src = reinterpret_cast<const uint4*>(a.wq + int64_t(g) * (R + 1) * FGS);
-    uint4* dst = reinterpret_cast<uint4*>(smem);
-    const int n4 = (R + 1) * FGS / 4;
-    for (int i = tid; i < n4; i += blockDim.x) dst[i] = src[i];
-    if (!PRE) rf_tables(a, smem);
-  }
-  __syncthreads();
-
   const int HoWo = a.Ho * a.Wo;
   const int fbase = g * FGS + gl * FPL;
   unsigned valid = 0;
@@ -162,18 +138,78 @@ __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(
 
     uint32_t lo;
     float vo[FPL];
-    walk_list<FPL, PPW, PRE>(a, wl, start, sent, ent, list, pv, valid, gmask, lo, vo);
+    walk_list<FPL, PPW, PRE, S28>(a, wl, start, sent, ent, list, pv, valid, gmask, lo, vo);
     if (pv) {
+      // NHWC: the warp's features of one position are contiguous (one or two lines per store);
+      // NCHW: every feature is a separate plane (a line per lane per store)
+      const int64_t o0 = a.nhwc ? int64_t(p) * a.F + fbase : (int64_t(b) * a.F + fbase) * HoWo + rem;
+      const int64_t fs = a.nhwc ? 1 : HoWo;
 #pragma unroll
       for (int j = 0; j < FPL; ++j) {
         if (valid >> j & 1) {
-          const int64_t o = (int64_t(b) * a.F + fbase + j) * HoWo + rem;
-          a.lat_out[o] = uint8_t(lo >> (8 * j));
-          a.v_out[o] = vo[j];
+          a.lat_out[o0 + j * fs] = uint8_t(lo >> (8 * j));
+          if (a.v_out) a.v_out[o0 + j * fs] = vo[j];
         }
       }
     }
     __syncwarp();
+  }
+}
+
+template <int FPL, int PPW, bool PRE, bool WCONV = false>
+__global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(const WalkArgs a) {
+  pdl_wait();
+  constexpr int LPP = 32 / PPW;
+  constexpr int FGS = LPP * FPL;
+  static_assert(!PRE || PPW == 1, "presorted walk: one position per warp");
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int R = a.R;
+  const int tid = threadIdx.x;
+  const int g = blockIdx.y;
+  // Stage the group's weight slice as fixed point (units of 2^-31) and test whether every weight is
+  // also a multiple of 2^-28 (bits 0-2 clear): then the whole slice is rescaled to 2^-28 and the
+  // walk sums blocks in 32 bits (S28).  Each CTA decides for its own slice (its features only).
+  bool ok28 = true;
+  if constexpr (WCONV) {  // fixed point straight from the fp32 weights (exact domain checked, N1)
+    uint32_t* dst = reinterpret_cast<uint32_t*>(smem);
+    for (int i = tid; i < (R + 1) * FGS; i += blockDim.x) {
+      const int e = i / FGS, f = g * FGS + (i - (i / FGS) * FGS);
+      uint32_t u = 0;
+      if (f < a.F && e < R) {
+        int se = e;  // the row's source element in w[f] = [C][KH][KW]
+        if (a.in_nhwc) { const int kk = e / a.C; se = (e - kk * a.C) * (a.KH * a.KW) + kk; }
+        const float x = __ldg(a.wf32 + int64_t(f) * R + se);
+        const float sx = x * 2147483648.0f;  // exact power-of-two scaling
+        if (!(x >= 0.0f && x <= 1.0f) || sx != truncf(sx)) flag_error(a.err, kErrInexact);
+        else u = uint32_t(sx);
+      }
+      ok28 &= (u & 7u) == 0;
+      dst[i] = u;
+    }
+    rf_tables(a, smem);
+  } else {
+    const uint4* src = reinterpret_cast<const uint4*>(a.wq + int64_t(g) * (R + 1) * FGS);
+    uint4* dst = reinterpret_cast<uint4*>(smem);
+    const int n4 = (R + 1) * FGS / 4;
+    for (int i = tid; i < n4; i += blockDim.x) {
+      const uint4 v = src[i];
+      ok28 &= ((v.x | v.y | v.z | v.w) & 7u) == 0;
+      dst[i] = v;
+    }
+    if (!PRE) rf_tables(a, smem);
+  }
+  const bool s28 = __syncthreads_and(ok28) != 0;
+  if (s28) {
+    uint4* w4 = reinterpret_cast<uint4*>(smem);
+    for (int i = tid; i < (R + 1) * FGS / 4; i += blockDim.x) {
+      uint4 v = w4[i];
+      v.x >>= 3; v.y >>= 3; v.z >>= 3; v.w >>= 3;
+      w4[i] = v;
+    }
+    __syncthreads();
+    walk_positions<FPL, PPW, PRE, true>(a, smem);
+  } else {
+    walk_positions<FPL, PPW, PRE, false>(a, smem);
   }
 }
 
@@ -421,19 +457,21 @@ int conv_walk_describe(int B, int C, int H, int W, int pad, int F, int KH, int K
 // Returns 1 if this path does not apply (caller falls back), else an SNN code.
 int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
                      int KW, int T, float theta, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes,
-                     cudaStream_t s) {
+                     cudaStream_t s, int nhwc, int in_nhwc) {
   WalkPlan pl;
   if (!walk_plan(B, C, H, W, pad, F, KH, KW, T, &pl)) return 1;
   WalkArgs a = pl.a;
   size_t wq_bytes = (size_t(pl.n_groups) * (a.R + 1) * pl.FGS * 4 + 255) & ~size_t(255);
   const size_t need = wq_bytes + (pl.pre ? size_t(pl.chunk) * a.rec + kListSlack : 0);
   if (ws_bytes < need) return set_error(SNN_EWORKSPACE, "snn_conv_fire: workspace %zu < %zu", ws_bytes, need);
-  a.lat_in = lat_in; a.lat_out = lat_out; a.v_out = v_out;
+  a.lat_in = lat_in; a.lat_out = lat_out; a.v_out = v_out; a.nhwc = nhwc; a.in_nhwc = in_nhwc;
   a.err = error_word_ptr();
   a.wq = reinterpret_cast<const uint32_t*>(ws);
   a.lists = reinterpret_cast<unsigned char*>(ws) + wq_bytes;
   const double tt = floor(double(theta) * 2147483648.0);
   a.thr = tt >= 9.0e18 ? INT64_MAX : (tt < -1.0 ? -1 : int64_t(tt));
+  const double t28 = floor(double(theta) * 268435456.0);
+  a.thr28 = t28 >= 9.0e18 ? INT64_MAX : (t28 < -1.0 ? -1 : int64_t(t28));
   const int64_t npos = int64_t(B) * a.Ho * a.Wo;
   if (getenv("SNN_DEBUG_PLAN"))
     fprintf(stderr, "walk plan: pre %d fpl %d ppw %d FGS %d groups %d warps %d smem %d | sort ppw %d "
@@ -449,7 +487,8 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
       default: return walk_go<1, 1, false, true>(pl, a, s);
     }
   }
-  int rc = weight_prep_launch(w, F, a.R, pl.FGS, pl.n_groups, reinterpret_cast<uint32_t*>(ws), s);
+  int rc = weight_prep_launch(w, F, a.R, pl.FGS, pl.n_groups, reinterpret_cast<uint32_t*>(ws), s, in_nhwc ? C : 0,
+                              KH * KW);
   if (rc) return rc;
   if (!pl.pre) {
     a.p0 = 0; a.np = npos;
@@ -464,6 +503,7 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
     }
   }
   WalkArgs sa = pl.sa;
+  sa.in_nhwc = in_nhwc;
   sa.lat_in = lat_in; sa.lists = a.lists; sa.hdr = a.hdr; sa.rec = a.rec;
   for (int64_t p0 = 0; p0 < npos; p0 += pl.chunk) {
     a.p0 = p0;

@@ -242,8 +242,19 @@ __global__ void __launch_bounds__(256) enc_select_kernel(int T, int bins, int le
   }
 }
 
+// Output index of flat input element i: planar (hw = 0) or channels-last [H, W, C] (SNN_ENCODE_OUT_NHWC).
+struct EncOut {
+  int hw, c;
+  __device__ __forceinline__ uint32_t idx(uint32_t i) const {
+    if (!hw) return i;
+    const uint32_t ch = i / uint32_t(hw);
+    return (i - ch * uint32_t(hw)) * uint32_t(c) + ch;
+  }
+};
+
 __global__ void __launch_bounds__(kEncThreads) enc_assign_kernel(const float* __restrict__ x, int64_t n, int T,
-                                                                  int bins, uint8_t* __restrict__ lat, EncodeWS ws) {
+                                                                  int bins, uint8_t* __restrict__ lat, EncodeWS ws,
+                                                                  EncOut eo) {
   pdl_begin();
   const int g = blockIdx.y;
   const int S = T;
@@ -273,7 +284,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_assign_kernel(const float* __
       }
       out = lo >= T ? kNoSpike : uint8_t(lo);
     }
-    lg[i] = out;
+    lg[eo.idx(uint32_t(i))] = out;
   }
 }
 
@@ -289,7 +300,7 @@ constexpr int kSmThreads = 512;
 __device__ __forceinline__ uint64_t sm_key(uint32_t vk, int i) { return (uint64_t(vk) << 24) | uint32_t(i); }
 
 __global__ void __launch_bounds__(kSmThreads) enc_small_kernel(const float* __restrict__ x, int n, int T, int bins,
-                                                                uint8_t* __restrict__ lat) {
+                                                                uint8_t* __restrict__ lat, EncOut eo) {
   pdl_begin();
   extern __shared__ uint32_t vk[];              // [n] 0x7FFFFFFF - bits(x), or ~0 for x <= 0; then [n] u16 candidates
   uint16_t* cand = reinterpret_cast<uint16_t*>(vk + n);
@@ -456,17 +467,17 @@ __global__ void __launch_bounds__(kSmThreads) enc_small_kernel(const float* __re
   // ---- assign: lat = number of cuts whose prefix the key reaches ----
   for (int i = tid; i < n; i += kSmThreads) {
     const uint32_t k32 = vk[i];
-    if (k32 == 0xFFFFFFFFu) { lb[i] = kNoSpike; continue; }
+    if (k32 == 0xFFFFFFFFu) { lb[eo.idx(i)] = kNoSpike; continue; }
     const uint64_t K = sm_key(k32, i);
     const int bl = bin_lat[uint32_t(K >> 43)];
-    if (bl != 0xFF) { lb[i] = bl >= T ? kNoSpike : uint8_t(bl); continue; }
+    if (bl != 0xFF) { lb[eo.idx(i)] = bl >= T ? kNoSpike : uint8_t(bl); continue; }
     int lo = 0, hi = NC;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       const bool pass = cut_shift[mid] >= 0 && (K >> cut_shift[mid]) >= cut_prefix[mid];
       if (pass) lo = mid + 1; else hi = mid;
     }
-    lb[i] = lo >= T ? kNoSpike : uint8_t(lo);
+    lb[eo.idx(i)] = lo >= T ? kNoSpike : uint8_t(lo);
   }
 }
 
@@ -486,7 +497,7 @@ __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
 // shuffle away (no barrier), farther ones go through shared memory (one barrier per stride).
 template <int EPT, int NT = kBtThreads>
 __global__ void __launch_bounds__(NT) enc_bitonic_kernel(const float* __restrict__ x, int n, int T, int bins,
-                                                         uint8_t* __restrict__ lat) {
+                                                         uint8_t* __restrict__ lat, EncOut eo) {
   pdl_begin();
   constexpr int np2 = NT * EPT, WCH = 32 * EPT;
   extern __shared__ uint64_t bk[];  // [np2] keys for the long strides
@@ -506,7 +517,7 @@ __global__ void __launch_bounds__(NT) enc_bitonic_kernel(const float* __restrict
     if (i < n) {
       const float xv = xb[i];
       if (xv > 0.0f) { v[k] = (uint64_t(0x7FFFFFFFu - __float_as_uint(xv)) << 24) | uint32_t(i); ++cnt; }
-      else lb[i] = kNoSpike;
+      else lb[eo.idx(i)] = kNoSpike;
     }
   }
   cnt = __reduce_add_sync(0xffffffffu, cnt);
@@ -562,13 +573,17 @@ __global__ void __launch_bounds__(NT) enc_bitonic_kernel(const float* __restrict
     if (bins == 1) bin = uint32_t((uint64_t(r) * T) / N);
     else if (bins == 2) bin = q ? (r < q * uint32_t(T) ? r / q : 255u) : 255u;
     else bin = r < m * (q + 1) ? r / (q + 1) : m + (r - m * (q + 1)) / q;  // R1
-    lb[uint32_t(v[k] & 0xFFFFFFu)] = bin >= uint32_t(T) ? kNoSpike : uint8_t(bin);
+    lb[eo.idx(uint32_t(v[k] & 0xFFFFFFu))] = bin >= uint32_t(T) ? kNoSpike : uint8_t(bin);
   }
 }
 
 int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, uint8_t* lat, void* wsp,
                   size_t ws_bytes, cudaStream_t s) {
   int64_t n = int64_t(C) * H * W;
+  EncOut eo;  // SNN_ENCODE_OUT_NHWC: latency of flat element i = c H W + p stored at p C + c
+  eo.hw = (bins & SNN_ENCODE_OUT_NHWC) ? H * W : 0;
+  eo.c = C;
+  bins &= 0xFF;
   if (B == 0 || n == 0) return SNN_OK;
   if (n <= 8192 && B * 2 <= num_sms()) {  // a few small images: latency path
     // keys per thread x threads = the padded key count (measured C1: 1024 threads 53 us per step, 512 56,
@@ -579,14 +594,14 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, u
     if (nt != 256 && nt != 512 && nt != 1024) nt = 1024;
     if (keys / nt > 16) nt = keys / 16;
     const int ept = keys / nt;
-    void (*k)(const float*, int, int, int, uint8_t*) = nullptr;
+    void (*k)(const float*, int, int, int, uint8_t*, EncOut) = nullptr;
     if (nt == 256) k = ept == 8 ? enc_bitonic_kernel<8, 256> : enc_bitonic_kernel<16, 256>;
     else if (nt == 512) k = ept == 4 ? enc_bitonic_kernel<4, 512> : ept == 8 ? enc_bitonic_kernel<8, 512> : enc_bitonic_kernel<16, 512>;
     else k = ept == 2 ? enc_bitonic_kernel<2, 1024> : ept == 4 ? enc_bitonic_kernel<4, 1024> : enc_bitonic_kernel<8, 1024>;
     const size_t smem = size_t(keys) * sizeof(uint64_t);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_encode: %s", cudaGetErrorString(e));
-    launch_k(k, dim3(B), dim3(nt), smem, s, x, int(n), T, bins, lat);
+    launch_k(k, dim3(B), dim3(nt), smem, s, x, int(n), T, bins, lat, eo);
     note_launch();
     return check_launch("snn_encode(bitonic)");
   }
@@ -594,7 +609,7 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, u
     const size_t smem = size_t(n) * (sizeof(uint32_t) + sizeof(uint16_t)) + 16;
     cudaError_t e = cudaFuncSetAttribute(enc_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_encode: %s", cudaGetErrorString(e));
-    launch_k(enc_small_kernel, dim3(B), dim3(kSmThreads), smem, s, x, int(n), T, bins, lat);
+    launch_k(enc_small_kernel, dim3(B), dim3(kSmThreads), smem, s, x, int(n), T, bins, lat, eo);
     note_launch();
     return check_launch("snn_encode(small)");
   }
@@ -621,7 +636,7 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, u
         note_launch();
       }
     }
-    launch_k(enc_assign_kernel, dim3(grid), dim3(kEncThreads), 0, s, xg, n, T, bins, lat + int64_t(g0) * n, ws);
+    launch_k(enc_assign_kernel, dim3(grid), dim3(kEncThreads), 0, s, xg, n, T, bins, lat + int64_t(g0) * n, ws, eo);
     note_launch();
     int rc = check_launch("snn_encode");
     if (rc) return rc;

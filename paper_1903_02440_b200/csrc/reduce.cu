@@ -145,6 +145,148 @@ __global__ void __launch_bounds__(256) pool_rows_kernel(const uint8_t* __restric
   }
 }
 
+// Channels-last input (lat, v [B, H, W, F], the SNN_CONV_OUT_NHWC output of snn_conv_fire_ex).
+// Window rule as pool_kernel (R10-R12; EQ3's truncated windows: entries past the input never spike),
+// evaluated branch-free so a thread's window loads are all in flight together.
+template <int VEC>
+__device__ __forceinline__ void pool_window_nhwc(const uint8_t* limg, const float* vimg, int F, int H, int W, int PH,
+                                                 int PW, int SH, int SW, int DH, int DW, int oy, int ox, int f,
+                                                 int vfinal, unsigned (&best)[VEC], float (&bv)[VEC]) {
+#pragma unroll
+  for (int u = 0; u < VEC; ++u) { best[u] = kNoSpike; bv[u] = 0.0f; }
+  const int y0 = oy * SH - DH, x0 = ox * SW - DW;
+  const int ya = y0 < 0 ? 0 : y0, yb = (y0 + PH < H ? y0 + PH : H);
+  const int xa = x0 < 0 ? 0 : x0, xb = (x0 + PW < W ? x0 + PW : W);
+  for (int yy = ya; yy < yb; ++yy) {
+    uint32_t i = (uint32_t(yy) * W + xa) * F + f;
+#pragma unroll 4
+    for (int xx = xa; xx < xb; ++xx, i += F) {
+      unsigned lv[VEC];
+      float vv[VEC];
+      if constexpr (VEC == 4) {
+        const uint32_t q = __ldg(reinterpret_cast<const uint32_t*>(limg + i));
+        lv[0] = q & 0xFF; lv[1] = (q >> 8) & 0xFF; lv[2] = (q >> 16) & 0xFF; lv[3] = q >> 24;
+        if (vimg) {
+          const float4 w4 = __ldg(reinterpret_cast<const float4*>(vimg + i));
+          vv[0] = w4.x; vv[1] = w4.y; vv[2] = w4.z; vv[3] = w4.w;
+        } else {
+          vv[0] = vv[1] = vv[2] = vv[3] = 0.0f;
+        }
+      } else {
+        lv[0] = __ldg(limg + i);
+        vv[0] = vimg ? __ldg(vimg + i) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < VEC; ++u) {
+        const unsigned li = lv[u];
+        const bool sp = li != kNoSpike;
+        if (vfinal) {  // SNN_POOL_VFINAL: max over every spiking entry
+          const bool tv = sp && (best[u] == kNoSpike || vv[u] > bv[u]);
+          bv[u] = tv ? vv[u] : bv[u];
+          best[u] = (sp && li < best[u]) ? li : best[u];
+        } else {       // earliest spike, then the max potential among the entries at that time
+          const bool tk = sp && (li < best[u] || (li == best[u] && vv[u] > bv[u]));
+          bv[u] = tk ? vv[u] : bv[u];
+          best[u] = tk ? li : best[u];
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < VEC; ++u) bv[u] = best[u] == kNoSpike ? 0.0f : bv[u];
+}
+
+// -> planar output [B, F, Ho, Wo].  CTA = (32 output columns, 32 * VEC features) of one output row
+// of one image: warps take the columns, lanes VEC features each (coalesced channels-last reads), the
+// tile transposes through shared memory, then warps take features and lanes columns (coalesced
+// planar rows).  blockIdx.x = column tile + ntx * feature chunk, y = output row, z = image.
+template <int VEC>
+__global__ void __launch_bounds__(256) pool_nhwc_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
+                                                        int F, int H, int W, int PH, int PW, int SH, int SW, int DH,
+                                                        int DW, int Ho, int Wo, int ntx, int vfinal,
+                                                        uint8_t* __restrict__ lat_out, float* __restrict__ v_out) {
+  pdl_begin();
+  constexpr int FT = 32 * VEC;                        // features per tile
+  constexpr int LS = FT + 4;                          // lat row stride (bytes), 4-aligned, odd word count
+  __shared__ __align__(16) uint8_t s_lat[32 * LS];    // [column][feature]
+  __shared__ float s_v[32 * (FT + 1)];                // [column][feature]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int xt = blockIdx.x % ntx, fc = blockIdx.x / ntx, oy = blockIdx.y, b = blockIdx.z;
+  const uint8_t* limg = lat + int64_t(b) * H * W * F;
+  const float* vimg = v ? v + int64_t(b) * H * W * F : nullptr;
+  const int f = fc * FT + lane * VEC;
+  for (int p = warp; p < 32; p += 8) {
+    const int ox = xt * 32 + p;
+    unsigned best[VEC];
+    float bv[VEC];
+    if (ox < Wo && f < F) {
+      pool_window_nhwc<VEC>(limg, vimg, F, H, W, PH, PW, SH, SW, DH, DW, oy, ox, f, vfinal, best, bv);
+    } else {
+#pragma unroll
+      for (int u = 0; u < VEC; ++u) { best[u] = kNoSpike; bv[u] = 0.0f; }
+    }
+    if constexpr (VEC == 4)
+      *reinterpret_cast<uint32_t*>(s_lat + p * LS + lane * 4) = best[0] | (best[1] << 8) | (best[2] << 16) | (best[3] << 24);
+    else
+      s_lat[p * LS + lane] = uint8_t(best[0]);
+#pragma unroll
+    for (int u = 0; u < VEC; ++u) s_v[p * (FT + 1) + lane * VEC + u] = bv[u];
+  }
+  __syncthreads();
+  const int ox = xt * 32 + lane;
+  if (ox >= Wo) return;
+  for (int fl = warp; fl < FT; fl += 8) {
+    const int ff = fc * FT + fl;
+    if (ff >= F) break;
+    const int64_t o = ((int64_t(b) * F + ff) * Ho + oy) * Wo + ox;
+    lat_out[o] = s_lat[lane * LS + fl];
+    if (v_out) v_out[o] = s_v[lane * (FT + 1) + fl];
+  }
+}
+
+// -> channels-last output [B, Ho, Wo, F]: one thread per (output pixel, VEC features), grid-stride;
+// lat-only VEC = 4 windows reduce with byte-wise SIMD minima.
+template <int VEC>
+__global__ void __launch_bounds__(256) pool_nhwc2nhwc_kernel(const uint8_t* __restrict__ lat,
+                                                             const float* __restrict__ v, int B, int F, int H, int W,
+                                                             int PH, int PW, int SH, int SW, int DH, int DW, int Ho,
+                                                             int Wo, int vfinal, uint8_t* __restrict__ lat_out,
+                                                             float* __restrict__ v_out) {
+  pdl_begin();
+  const uint32_t FV = uint32_t(F / VEC), HoWo = uint32_t(Ho) * Wo;
+  const uint64_t total = uint64_t(B) * HoWo * FV;
+  for (uint64_t o = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; o < total; o += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t pix = o / FV;
+    const int f = int(o - pix * FV) * VEC;
+    const uint32_t b = uint32_t(pix / HoWo), rem = uint32_t(pix - uint64_t(b) * HoWo);
+    const int oy = int(rem / uint32_t(Wo)), ox = int(rem - uint32_t(oy) * Wo);
+    const uint8_t* limg = lat + int64_t(b) * H * W * F;
+    const int64_t oi = int64_t(pix) * F + f;
+    if (VEC == 4 && !v) {  // latencies only: min of the window's 4-byte words
+      const int y0 = oy * SH - DH, x0 = ox * SW - DW;
+      const int ya = y0 < 0 ? 0 : y0, yb = (y0 + PH < H ? y0 + PH : H);
+      const int xa = x0 < 0 ? 0 : x0, xb = (x0 + PW < W ? x0 + PW : W);
+      uint32_t m = 0xFFFFFFFFu;
+      for (int yy = ya; yy < yb; ++yy) {
+        uint32_t i = (uint32_t(yy) * W + xa) * F + f;
+#pragma unroll 4
+        for (int xx = xa; xx < xb; ++xx, i += F) m = __vminu4(m, __ldg(reinterpret_cast<const uint32_t*>(limg + i)));
+      }
+      *reinterpret_cast<uint32_t*>(lat_out + oi) = m;
+      continue;
+    }
+    unsigned best[VEC];
+    float bv[VEC];
+    pool_window_nhwc<VEC>(limg, v ? v + int64_t(b) * H * W * F : nullptr, F, H, W, PH, PW, SH, SW, DH, DW, oy, ox, f,
+                          vfinal, best, bv);
+#pragma unroll
+    for (int u = 0; u < VEC; ++u) {
+      lat_out[oi + u] = uint8_t(best[u]);
+      if (v_out) v_out[oi + u] = bv[u];
+    }
+  }
+}
+
 int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, int PH, int PW, int SH, int SW,
                 int DH, int DW, int flags, uint8_t* lat_out, float* v_out, cudaStream_t s) {
   // R10 (windows inside the padded input), or Eq. 3 literally (last window truncated at the edge)
@@ -153,6 +295,36 @@ int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, 
   const int Wo = eq3 ? (W + 2 * DW) / SW : (W + 2 * DW - PW) / SW + 1;
   const int64_t total = int64_t(B) * F * Ho * Wo;
   if (total == 0) return SNN_OK;
+  if (flags & (SNN_POOL_IN_NHWC | SNN_POOL_OUT_NHWC)) {
+    if (!(flags & SNN_POOL_IN_NHWC)) return set_error(SNN_EINVAL, "snn_pool: SNN_POOL_OUT_NHWC needs SNN_POOL_IN_NHWC");
+    if (int64_t(H) * W * F >= (int64_t(1) << 32)) return set_error(SNN_ESHAPE, "snn_pool(NHWC input): H*W*F >= 2^32");
+    const bool al = (reinterpret_cast<uintptr_t>(lat) & 3) == 0 && (reinterpret_cast<uintptr_t>(lat_out) & 3) == 0 &&
+                    (!v_out || ((reinterpret_cast<uintptr_t>(v) & 15) == 0));
+    const int vec = (F % 4 == 0 && al) ? 4 : 1;
+    const float* vin = v_out ? v : nullptr;
+    const int vf = (flags & SNN_POOL_VFINAL) ? 1 : 0;
+    if (flags & SNN_POOL_OUT_NHWC) {
+      int64_t nb = ceil_div(total / vec, 256);
+      if (nb > int64_t(num_sms()) * 16) nb = int64_t(num_sms()) * 16;
+      if (vec == 4)
+        launch_k(pool_nhwc2nhwc_kernel<4>, dim3(unsigned(nb)), dim3(256), 0, s, lat, vin, B, F, H, W, PH, PW, SH, SW,
+                 DH, DW, Ho, Wo, vf, lat_out, v_out);
+      else
+        launch_k(pool_nhwc2nhwc_kernel<1>, dim3(unsigned(nb)), dim3(256), 0, s, lat, vin, B, F, H, W, PH, PW, SH, SW,
+                 DH, DW, Ho, Wo, vf, lat_out, v_out);
+    } else {
+      if (B > 65535 || Ho > 65535) return set_error(SNN_ESHAPE, "snn_pool(NHWC input): B or Ho > 65535");
+      const int ntx = int(ceil_div(Wo, 32)), nfc = int(ceil_div(F, 32 * vec));
+      if (vec == 4)
+        launch_k(pool_nhwc_kernel<4>, dim3(unsigned(ntx * nfc), unsigned(Ho), unsigned(B)), dim3(256), 0, s, lat, vin,
+                 F, H, W, PH, PW, SH, SW, DH, DW, Ho, Wo, ntx, vf, lat_out, v_out);
+      else
+        launch_k(pool_nhwc_kernel<1>, dim3(unsigned(ntx * nfc), unsigned(Ho), unsigned(B)), dim3(256), 0, s, lat, vin,
+                 F, H, W, PH, PW, SH, SW, DH, DW, Ho, Wo, ntx, vf, lat_out, v_out);
+    }
+    note_launch();
+    return check_launch("snn_pool(NHWC input)");
+  }
   int64_t blocks = ceil_div(total, 256);
   if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
   const bool small = total < (int64_t(1) << 32) && int64_t(B) * F * H * W < (int64_t(1) << 32);

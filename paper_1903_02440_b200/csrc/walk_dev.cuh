@@ -26,7 +26,8 @@ struct WalkArgs {
   int B, C, H, W, pad;
   int F, KH, KW, T, Ho, Wo, R;
   const uint32_t* wq;  // [n_groups][R+1][FGS]
-  int64_t thr;
+  int64_t thr;        // threshold in units of 2^-31: floor(theta * 2^31) (saturated)
+  int64_t thr28;      // the same in units of 2^-28 (walks of S28 weight slices)
   uint8_t* lat_out;
   float* v_out;
   int off_eoff, off_ekk, off_warps, warp_bytes, pos_bytes;
@@ -46,6 +47,9 @@ struct WalkArgs {
   // fused schedule: the fp32 weights [F][R], converted to fixed point while staged into shared memory
   // (no separate weight-prep launch); nullptr = copy the prepared wq
   const float* wf32;
+  int nhwc;           // output layout: 0 = [B, F, Ho, Wo], 1 = [B, Ho, Wo, F] (SNN_CONV_OUT_NHWC)
+  int in_nhwc;        // input layout [B, H, W, C] (SNN_CONV_IN_NHWC): receptive-field entries are then
+                      // ordered (ky, kx, c) -- e = (ky KW + kx) C + c -- and so are the weight rows
 };
 
 static inline int al16(int x) { return (x + 15) & ~15; }
@@ -164,7 +168,7 @@ __device__ __forceinline__ void rf_sort_warp(const WalkArgs& a, const unsigned c
     uint8_t* patch = wbase + a.patch_off;
     const int b = pf / HoWo, rem = pf - b * HoWo, y = rem / a.Wo, x = rem - (rem / a.Wo) * a.Wo;
     const int y0 = y - a.pad, x0 = x - a.pad;
-    const uint8_t* in0 = a.lat_in + int64_t(b) * CHW + int64_t(y0) * a.W + x0;
+    const uint8_t* in0 = a.lat_in + int64_t(b) * CHW + (int64_t(y0) * a.W + x0) * (a.in_nhwc ? a.C : 1);
     const bool interior = y0 >= 0 && x0 >= 0 && y0 + a.KH <= a.H && x0 + a.patch_w <= a.W;
     if (interior) {
       for (int i = lane; i < a.patch_n; i += 32) patch[i] = __ldg(in0 + ptab[i]);
@@ -175,7 +179,7 @@ __device__ __forceinline__ void rf_sort_warp(const WalkArgs& a, const unsigned c
       }
     }
     __syncwarp();
-    const uint8_t* pg = patch + grp;
+    const uint8_t* pg = patch + grp * (a.in_nhwc ? a.C : 1);  // the group's position is grp columns right
     rf_sort_group<LPP>(a, pv, gl, cnt, start, list, [&](int e) { return int(pg[eoffp[e]]); });
   } else {
     const int32_t* eoff = reinterpret_cast<const int32_t*>(tabs + a.off_eoff);
@@ -185,7 +189,7 @@ __device__ __forceinline__ void rf_sort_warp(const WalkArgs& a, const unsigned c
     const int rem = pv ? p - b * HoWo : 0;
     const int y = rem / a.Wo, x = rem - (rem / a.Wo) * a.Wo;
     const int y0 = y - a.pad, x0 = x - a.pad;
-    const uint8_t* in = a.lat_in + int64_t(b) * CHW + int64_t(y0) * a.W + x0;
+    const uint8_t* in = a.lat_in + int64_t(b) * CHW + (int64_t(y0) * a.W + x0) * (a.in_nhwc ? a.C : 1);
     const bool interior = y0 >= 0 && x0 >= 0 && y0 + a.KH <= a.H && x0 + a.KW <= a.W;
     rf_sort_group<LPP>(a, pv, gl, cnt, start, list,
                        [&](int e) { return int(rf_lat(a, eoff, ekk, in, interior, y0, x0, e)); });
@@ -197,16 +201,36 @@ __device__ __forceinline__ void rf_tables(const WalkArgs& a, unsigned char* tabs
   uint16_t* ekk = reinterpret_cast<uint16_t*>(tabs + a.off_ekk);
   const int KK = a.KH * a.KW;
   for (int e = threadIdx.x; e < a.R; e += blockDim.x) {
-    const int c = e / KK, r = e - c * KK, ky = r / a.KW, kx = r - ky * a.KW;
-    eoff[e] = c * a.H * a.W + ky * a.W + kx;
+    int c, ky, kx;
+    if (a.in_nhwc) {  // e = (ky KW + kx) C + c
+      const int kk = e / a.C;
+      c = e - kk * a.C; ky = kk / a.KW; kx = kk - ky * a.KW;
+      eoff[e] = (ky * a.W + kx) * a.C + c;
+      if (a.patch_n > 0)
+        reinterpret_cast<uint16_t*>(tabs + a.off_eoffp)[e] = uint16_t((ky * a.patch_w + kx) * a.C + c);
+    } else {          // e = (c KH + ky) KW + kx
+      c = e / KK;
+      const int r = e - c * KK;
+      ky = r / a.KW; kx = r - ky * a.KW;
+      eoff[e] = c * a.H * a.W + ky * a.W + kx;
+      if (a.patch_n > 0)
+        reinterpret_cast<uint16_t*>(tabs + a.off_eoffp)[e] = uint16_t((c * a.KH + ky) * a.patch_w + kx);
+    }
     ekk[e] = uint16_t((ky << 8) | kx);
-    if (a.patch_n > 0)
-      reinterpret_cast<uint16_t*>(tabs + a.off_eoffp)[e] = uint16_t((c * a.KH + ky) * a.patch_w + kx);
   }
   const int PK = a.KH * a.patch_w;
   for (int i = threadIdx.x; i < a.patch_n; i += blockDim.x) {
-    const int c = i / PK, r = i - c * PK, ky = r / a.patch_w, kx = r - ky * a.patch_w;
-    reinterpret_cast<int32_t*>(tabs + a.off_ptab)[i] = c * a.H * a.W + ky * a.W + kx;
+    int c, ky, kx;
+    if (a.in_nhwc) {
+      const int kk = i / a.C;
+      c = i - kk * a.C; ky = kk / a.patch_w; kx = kk - ky * a.patch_w;
+      reinterpret_cast<int32_t*>(tabs + a.off_ptab)[i] = (ky * a.W + kx) * a.C + c;
+    } else {
+      c = i / PK;
+      const int r = i - c * PK;
+      ky = r / a.patch_w; kx = r - ky * a.patch_w;
+      reinterpret_cast<int32_t*>(tabs + a.off_ptab)[i] = c * a.H * a.W + ky * a.W + kx;
+    }
     reinterpret_cast<uint16_t*>(tabs + a.off_pkk)[i] = uint16_t((ky << 8) | kx);
   }
 }
@@ -214,16 +238,28 @@ __device__ __forceinline__ void rf_tables(const WalkArgs& a, unsigned char* tabs
 // ------------------------------------------------------------------------------------- walk
 template <int FPL, bool PRE> struct WalkThreads { static constexpr int v = FPL == 4 ? 768 : 1024; };
 
+// Accumulator of a fired (or padding) feature: INT64_MIN, so no later sum along the list (at most
+// R * 2^31 < 2^44) can bring it back above a threshold, and "fired" needs no separate mask.
+constexpr uint64_t kFiredAcc = 0x8000000000000000ull;
+
+// Fixed-point scale of a walk: S28 = weights in units of 2^-28 (every weight of the slice is 0 or a
+// multiple of 2^-28 in [0, 1], i.e. w = 0 or w >= 2^-5 for fp32), else units of 2^-31 (N1).
+// At 2^-28 the sum of any 8 weights is < 2^31, so a block sums in 32 bits exactly (K3b).
+template <bool S28>
+__device__ __forceinline__ float fixed_to_float_s(int64_t acc) {
+  if constexpr (S28) return __ll2float_rn(acc) * 3.7252902984619140625e-09f;  // 2^-28, exact scaling
+  else return fixed_to_float(acc);
+}
+
 // Fire every unfired feature whose potential at the end of bucket t exceeds the threshold.
-template <int FPL>
-__device__ __forceinline__ void fire_at(const uint64_t (&acc)[FPL], int64_t thr, int t, unsigned& fired,
-                                        uint32_t& lo, float (&vo)[FPL]) {
+template <int FPL, bool S28>
+__device__ __forceinline__ void fire_at(uint64_t (&acc)[FPL], int64_t thr, int t, uint32_t& lo, float (&vo)[FPL]) {
 #pragma unroll
   for (int j = 0; j < FPL; ++j) {
-    if (!(fired >> j & 1) && int64_t(acc[j]) > thr) {
-      fired |= 1u << j;
+    if (int64_t(acc[j]) > thr) {
       lo = (lo & ~(0xFFu << (8 * j))) | (uint32_t(t) << (8 * j));
-      vo[j] = fixed_to_float(int64_t(acc[j]));
+      vo[j] = fixed_to_float_s<S28>(int64_t(acc[j]));
+      acc[j] = kFiredAcc;
     }
   }
 }
@@ -234,11 +270,12 @@ __device__ __forceinline__ void fire_at(const uint64_t (&acc)[FPL], int64_t thr,
 // unfired feature of the lane then exceeds the threshold, no test inside the block could fire
 // (potentials only grow along the list) and the block is taken whole; otherwise the lane re-adds it
 // pair by pair from the same registers and tests at every bucket end (K3).  Lanes decide
-// independently (no vote): the group's bookkeeping does not depend on the branch taken.
-template <int FPL>
+// independently (no vote): the group's bookkeeping does not depend on the branch taken.  S28: the
+// block's 8 weights are summed in 32 bits (exact, < 2^31) and added to the 64-bit accumulator once.
+template <int FPL, bool S28>
 __device__ __forceinline__ void walk_block(uint32_t wls, const uint4& e0, const uint4& e1, unsigned endm,
-                                           uint32_t tpk, int64_t thr, uint64_t (&acc)[FPL], unsigned& fired,
-                                           uint32_t& lo, float (&vo)[FPL]) {
+                                           uint32_t tpk, int64_t thr, uint64_t (&acc)[FPL], uint32_t& lo,
+                                           float (&vo)[FPL]) {
   const uint32_t off[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
   uint32_t wv[8][FPL];
 #pragma unroll
@@ -247,21 +284,33 @@ __device__ __forceinline__ void walk_block(uint32_t wls, const uint4& e0, const 
   bool hit = false;
 #pragma unroll
   for (int j = 0; j < FPL; ++j) {
-    s[j] = acc[j] + (uint64_t(wv[0][j]) + wv[1][j]) + (uint64_t(wv[2][j]) + wv[3][j]) +
-           (uint64_t(wv[4][j]) + wv[5][j]) + (uint64_t(wv[6][j]) + wv[7][j]);
-    hit |= !(fired >> j & 1) && int64_t(s[j]) > thr;
+    if constexpr (S28) {
+      const uint32_t b = ((wv[0][j] + wv[1][j]) + (wv[2][j] + wv[3][j])) + ((wv[4][j] + wv[5][j]) + (wv[6][j] + wv[7][j]));
+      s[j] = acc[j] + b;
+    } else {
+      s[j] = acc[j] + (uint64_t(wv[0][j]) + wv[1][j]) + (uint64_t(wv[2][j]) + wv[3][j]) +
+             (uint64_t(wv[4][j]) + wv[5][j]) + (uint64_t(wv[6][j]) + wv[7][j]);
+    }
+    hit |= int64_t(s[j]) > thr;
   }
   if (hit && endm) {
     if (endm & 7u) {  // a bucket ends strictly inside the block: pair by pair
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
 #pragma unroll
-        for (int j = 0; j < FPL; ++j) acc[j] += uint64_t(wv[2 * m][j]) + wv[2 * m + 1][j];
-        if (endm >> m & 1) fire_at<FPL>(acc, thr, int((tpk >> (8 * m)) & 0xFFu), fired, lo, vo);
+        for (int j = 0; j < FPL; ++j) {
+          if constexpr (S28) acc[j] += uint32_t(wv[2 * m][j] + wv[2 * m + 1][j]);
+          else acc[j] += uint64_t(wv[2 * m][j]) + wv[2 * m + 1][j];
+        }
+        if (endm >> m & 1) fire_at<FPL, S28>(acc, thr, int((tpk >> (8 * m)) & 0xFFu), lo, vo);
       }
-    } else {  // the only bucket end is the block end
-      fire_at<FPL>(s, thr, int(tpk >> 24), fired, lo, vo);
+      return;
     }
+    // the only bucket end is the block end
+#pragma unroll
+    for (int j = 0; j < FPL; ++j) acc[j] = s[j];
+    fire_at<FPL, S28>(acc, thr, int(tpk >> 24), lo, vo);
+    return;
   }
 #pragma unroll
   for (int j = 0; j < FPL; ++j) acc[j] = s[j];
@@ -269,31 +318,35 @@ __device__ __forceinline__ void walk_block(uint32_t wls, const uint4& e0, const 
 
 // Walk one position's sorted list (K2/K3) for the FPL features of this lane; group-uniform control,
 // full-warp votes only.  start: T+1 bucket starts; entries come from shared memory (sent for PRE,
-// list otherwise) or, for PRE past the prefetched npre entries, from global memory (ent).
-template <int FPL, int PPW, bool PRE>
+// list otherwise) or, for PRE past the prefetched npre entries, from global memory (ent).  thr is
+// the threshold in the walk's fixed-point units (S28: 2^-28, else 2^-31).
+template <int FPL, int PPW, bool PRE, bool S28 = false>
 __device__ __forceinline__ void walk_list(const WalkArgs& a, const unsigned char* wl, const uint16_t* start,
                                           const unsigned char* sent, const unsigned char* ent, const uint32_t* list,
                                           bool pv, unsigned valid, unsigned gmask, uint32_t& lo, float (&vo)[FPL]) {
-  constexpr unsigned kAll = (1u << FPL) - 1;
   const int T = a.T;
-  const int64_t thr = a.thr;
+  const int64_t thr = S28 ? a.thr28 : a.thr;
   uint32_t wls;  // the lane's weight base as a shared-window address, opaque so it stays in a register
   asm volatile("mov.u32 %0, %1;" : "=r"(wls) : "r"(smem_u32(wl)));
     uint64_t acc[FPL];
     lo = 0xFFFFFFFFu;  // byte j = lat of feature j (255 = no spike)
 #pragma unroll
-    for (int j = 0; j < FPL; ++j) { acc[j] = 0; vo[j] = 0.0f; }
-    unsigned fired = ~valid & kAll;
+    for (int j = 0; j < FPL; ++j) { acc[j] = (valid >> j & 1) ? 0ull : kFiredAcc; vo[j] = 0.0f; }
     const int total = pv ? int(start[T]) : 0;
     if (pv && int(start[1]) == 0 && int64_t(0) > thr) {  // empty bucket 0: P[0] = 0 > a negative threshold
 #pragma unroll
       for (int j = 0; j < FPL; ++j)
-        if (!(fired >> j & 1)) lo &= ~(0xFFu << (8 * j));
-      fired = kAll;
+        if (int64_t(acc[j]) >= 0) { lo &= ~(0xFFu << (8 * j)); acc[j] = kFiredAcc; }
     }
     bool done = !pv || total == 0;  // group-uniform, like every later update of done
+    auto alive = [&]() {  // an unfired valid feature remains in this lane
+      bool al = false;
+#pragma unroll
+      for (int j = 0; j < FPL; ++j) al |= int64_t(acc[j]) >= 0;
+      return al;
+    };
     {
-      const unsigned nd = __ballot_sync(0xffffffffu, fired != kAll);
+      const unsigned nd = __ballot_sync(0xffffffffu, alive());
       if ((nd & gmask) == 0) done = true;  // all features of the group fired (or are padding)
     }
     int i = 0, t = 0, it = 0;
@@ -332,9 +385,9 @@ __device__ __forceinline__ void walk_list(const WalkArgs& a, const unsigned char
             while (t < T && int(start[t + 1]) == bend) ++t;  // empty buckets add nothing
             bend = t < T ? int(start[t + 1]) : 0x7FFFFFFF;
           }
-          walk_block<FPL>(wls, cur[2 * h], cur[2 * h + 1], endm, tpk, thr, acc, fired, lo, vo);
+          walk_block<FPL, S28>(wls, cur[2 * h], cur[2 * h + 1], endm, tpk, thr, acc, lo, vo);
         }
-        const unsigned nf = __ballot_sync(0xffffffffu, !done && fired != kAll);
+        const unsigned nf = __ballot_sync(0xffffffffu, !done && alive());
         if (!done && ((nf & gmask) == 0 || i >= total)) done = true;
       }
       ++it;

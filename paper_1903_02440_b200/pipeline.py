@@ -22,59 +22,114 @@ def _dev(a, device, dtype=None):
 
 
 class Layer:
-    """conv+fire (+ optional pool) with preallocated outputs."""
+    """conv+fire (+ optional pool) with preallocated outputs.
+
+    Layouts: nhwc -- the conv writes channels-last [B, Ho, Wo, F] (snn_conv_fire_ex
+    SNN_CONV_OUT_NHWC: a walk warp's features of one position are contiguous, so its stores coalesce)
+    and the pool reads that layout (SNN_POOL_IN_NHWC); in_nhwc -- the layer's input is channels-last
+    [B, H, W, C] (SNN_CONV_IN_NHWC: a receptive field is KH x KW runs of C contiguous bytes);
+    pool_out_nhwc -- the pooled output is channels-last too (the next layer's in_nhwc input).
+    want_v False: the conv's potentials are not written (latency-only pooling needs none).
+    ``lat``, ``v``, ``plat``, ``pv`` are always planar [B, F, H, W] views; ``*_buf`` the buffers."""
 
     def __init__(self, spec, w: torch.Tensor, B: int, C: int, H: int, W: int, T: int, pool_spec=None,
-                 pool_v: bool = True, device="cuda"):
+                 pool_v: bool = True, device="cuda", nhwc: bool = False, want_v: bool = True,
+                 in_nhwc: bool = False, pool_out_nhwc: bool = False):
         self.spec, self.w, self.T = spec, w, T
         self.B, self.C, self.H, self.W = B, C, H, W
         self.Ho, self.Wo = snn.conv_out_hw(H, W, spec.KH, spec.KW, spec.pad)
         F = spec.F
-        self.lat = torch.empty((B, F, self.Ho, self.Wo), dtype=torch.uint8, device=device)
-        self.v = torch.empty((B, F, self.Ho, self.Wo), dtype=torch.float32, device=device)
+        if pool_spec is not None and pool_v and not want_v:
+            raise ValueError("pooled potentials need the conv's potentials (want_v)")
+        if pool_out_nhwc and not nhwc:
+            raise ValueError("a channels-last pooled output needs a channels-last conv output")
+        self.nhwc, self.in_nhwc, self.pool_out_nhwc = nhwc, in_nhwc, pool_out_nhwc
+        shape = (B, self.Ho, self.Wo, F) if nhwc else (B, F, self.Ho, self.Wo)
+        self.lat_buf = torch.empty(shape, dtype=torch.uint8, device=device)
+        self.v_buf = torch.empty(shape, dtype=torch.float32, device=device) if want_v else None
         self.ws = torch.empty(snn.conv_fire_workspace(B, C, H, W, spec.pad, F, spec.KH, spec.KW, T, spec.theta),
                               dtype=torch.uint8, device=device)
         self.pool_spec = pool_spec
         if pool_spec is not None:
             self.PHo, self.PWo = snn.pool_out_hw(self.Ho, self.Wo, pool_spec.PH, pool_spec.PW, pool_spec.SH,
                                                  pool_spec.SW, pool_spec.DH, pool_spec.DW)
-            self.plat = torch.empty((B, F, self.PHo, self.PWo), dtype=torch.uint8, device=device)
-            self.pv = torch.empty((B, F, self.PHo, self.PWo), dtype=torch.float32, device=device) if pool_v else None
+            pshape = (B, self.PHo, self.PWo, F) if pool_out_nhwc else (B, F, self.PHo, self.PWo)
+            self.plat_buf = torch.empty(pshape, dtype=torch.uint8, device=device)
+            self.pv_buf = torch.empty(pshape, dtype=torch.float32, device=device) if pool_v else None
+
+    @staticmethod
+    def _planar(t, nhwc):
+        if t is None:
+            return None
+        return t.permute(0, 3, 1, 2) if nhwc else t
+
+    @property
+    def lat(self):
+        return self._planar(self.lat_buf, self.nhwc)
+
+    @property
+    def v(self):
+        return self._planar(self.v_buf, self.nhwc)
+
+    @property
+    def plat(self):
+        return self._planar(self.plat_buf, self.pool_out_nhwc)
+
+    @property
+    def pv(self):
+        return self._planar(self.pv_buf, self.pool_out_nhwc)
 
     @property
     def out_lat(self):
-        return self.plat if self.pool_spec is not None else self.lat
+        """What the next layer reads (its in_nhwc = this layer's pool_out_nhwc when pooled)."""
+        if self.pool_spec is not None:
+            return self.plat_buf
+        return self.lat_buf
 
     @property
     def out_v(self):
-        return self.pv if self.pool_spec is not None else self.v
+        return self.pv_buf if self.pool_spec is not None else self.v_buf
+
+    def conv(self, lat_in: torch.Tensor, w: Optional[torch.Tensor] = None):
+        s = self.spec
+        snn.conv_fire(lat_in, self.w if w is None else w, s.pad, self.T, s.theta, lat_out=self.lat_buf,
+                      v_out=self.v_buf, ws=self.ws, nhwc=self.nhwc, want_v=self.v_buf is not None,
+                      in_nhwc=self.in_nhwc)
+
+    def pool(self):
+        p = self.pool_spec
+        flags = (snn.POOL_IN_NHWC if self.nhwc else 0) | (snn.POOL_OUT_NHWC if self.pool_out_nhwc else 0)
+        snn.pool(self.lat_buf, self.v_buf if self.pv_buf is not None else None, (p.PH, p.PW), (p.SH, p.SW),
+                 (p.DH, p.DW), lat_out=self.plat_buf, v_out=self.pv_buf, flags=flags)
 
     def __call__(self, lat_in: torch.Tensor, w: Optional[torch.Tensor] = None):
-        s = self.spec
-        snn.conv_fire(lat_in, self.w if w is None else w, s.pad, self.T, s.theta, lat_out=self.lat, v_out=self.v,
-                      ws=self.ws)
+        self.conv(lat_in, w)
         if self.pool_spec is not None:
-            p = self.pool_spec
-            snn.pool(self.lat, self.v if self.pv is not None else None, (p.PH, p.PW), (p.SH, p.SW), (p.DH, p.DW),
-                     lat_out=self.plat, v_out=self.pv)
+            self.pool()
         return self.out_lat
 
 
 class C2Net:
     """3-layer DCSNN inference (configs[1]): encode -> [conv+fire -> pool] x 2 -> conv (theta = inf)
-    -> 1 winner (global max potential, P:191) -> class = f // (F / 10)."""
+    -> 1 winner (global max potential, P:191) -> class = f // (F / 10).
 
-    def __init__(self, wl, B: int, device="cuda"):
+    nhwc (the bench configuration): every map between the encoder and layer 3 is channels-last
+    (encode -> conv1 -> pool1 -> conv2 -> pool2 -> conv3's input); conv_v False: layers 1 and 2 write
+    no potentials (their latency-only pools need none).  Layer 3's output stays planar."""
+
+    def __init__(self, wl, B: int, device="cuda", nhwc: bool = True, conv_v: bool = False):
         self.wl, self.B, self.T = wl, B, wl.T
         _, C, H, W = wl.X.shape
+        self.nhwc = nhwc
         self.ws_enc = torch.empty(snn.encode_workspace(B, C, H, W, wl.T), dtype=torch.uint8, device=device)
-        self.lat0 = torch.empty((B, C, H, W), dtype=torch.uint8, device=device)
+        self.lat0_buf = torch.empty((B, H, W, C) if nhwc else (B, C, H, W), dtype=torch.uint8, device=device)
         self.w = [_dev(w, device) for w in wl.weights]
         s1, s2, s3 = wl.convs
-        self.l1 = Layer(s1, self.w[0], B, C, H, W, wl.T, wl.pools[0], pool_v=False, device=device)
+        self.l1 = Layer(s1, self.w[0], B, C, H, W, wl.T, wl.pools[0], pool_v=False, device=device, nhwc=nhwc,
+                        want_v=conv_v, in_nhwc=nhwc, pool_out_nhwc=nhwc)
         self.l2 = Layer(s2, self.w[1], B, s1.F, self.l1.PHo, self.l1.PWo, wl.T, wl.pools[1], pool_v=False,
-                        device=device)
-        self.l3 = Layer(s3, self.w[2], B, s2.F, self.l2.PHo, self.l2.PWo, wl.T, None, device=device)
+                        device=device, nhwc=nhwc, want_v=conv_v, in_nhwc=nhwc, pool_out_nhwc=nhwc)
+        self.l3 = Layer(s3, self.w[2], B, s2.F, self.l2.PHo, self.l2.PWo, wl.T, None, device=device, in_nhwc=nhwc)
         self.winners = torch.empty((B, 1, 3), dtype=torch.int32, device=device)
         self.count = torch.empty((B,), dtype=torch.int32, device=device)
         n = int(snn.lib().snn_k_winners_workspace(B, s3.F, self.l3.Ho, self.l3.Wo))
@@ -82,9 +137,16 @@ class C2Net:
         self.decision = torch.empty((B,), dtype=torch.int32, device=device)
         self.reward = torch.empty((B,), dtype=torch.float32, device=device)
 
+    @property
+    def lat0(self):
+        return self.lat0_buf.permute(0, 3, 1, 2) if self.nhwc else self.lat0_buf
+
+    def encode(self, x: torch.Tensor):
+        snn.encode(x, self.T, out=self.lat0_buf, ws=self.ws_enc, nhwc=self.nhwc)
+
     def forward(self, x: torch.Tensor) -> torch.Tensor:
-        snn.encode(x, self.T, out=self.lat0, ws=self.ws_enc)
-        a = self.l1(self.lat0)
+        self.encode(x)
+        a = self.l1(self.lat0_buf)
         a = self.l2(a)
         self.l3(a)
         snn.k_winners(self.l3.lat, self.l3.v, 1, 0, winners=self.winners, count=self.count, ws=self.ws_kw)
@@ -94,15 +156,19 @@ class C2Net:
 
 
 class C5Net:
-    """Throughput stress (configs[4]): encode -> conv+fire -> pool 2/2 -> inhibit -> kWTA(k16, r4)."""
+    """Throughput stress (configs[4]): encode -> conv+fire -> pool 2/2 -> inhibit -> kWTA(k16, r4).
+    nhwc: encode and conv write channels-last maps (the conv reads that layout); the pool reads the
+    channels-last conv output and writes the planar map inhibition and k-WTA read."""
 
-    def __init__(self, wl, B: int, device="cuda"):
+    def __init__(self, wl, B: int, device="cuda", nhwc: bool = True):
         self.wl, self.B, self.T = wl, B, wl.T
         _, C, H, W = wl.X.shape
+        self.nhwc = nhwc
         self.ws_enc = torch.empty(snn.encode_workspace(B, C, H, W, wl.T), dtype=torch.uint8, device=device)
-        self.lat0 = torch.empty((B, C, H, W), dtype=torch.uint8, device=device)
+        self.lat0_buf = torch.empty((B, H, W, C) if nhwc else (B, C, H, W), dtype=torch.uint8, device=device)
         self.w = _dev(wl.weights[0], device)
-        self.l1 = Layer(wl.convs[0], self.w, B, C, H, W, wl.T, wl.pools[0], pool_v=True, device=device)
+        self.l1 = Layer(wl.convs[0], self.w, B, C, H, W, wl.T, wl.pools[0], pool_v=True, device=device, nhwc=nhwc,
+                        in_nhwc=nhwc)
         F, Hp, Wp = wl.convs[0].F, self.l1.PHo, self.l1.PWo
         self.ilat = torch.empty((B, F, Hp, Wp), dtype=torch.uint8, device=device)
         self.iv = torch.empty((B, F, Hp, Wp), dtype=torch.float32, device=device)
@@ -113,9 +179,16 @@ class C5Net:
         self.ws_kw = torch.empty(int(snn.lib().snn_k_winners_workspace(B, F, Hp, Wp)), dtype=torch.uint8,
                                  device=device)
 
+    @property
+    def lat0(self):
+        return self.lat0_buf.permute(0, 3, 1, 2) if self.nhwc else self.lat0_buf
+
+    def encode(self, x: torch.Tensor):
+        snn.encode(x, self.T, out=self.lat0_buf, ws=self.ws_enc, nhwc=self.nhwc)
+
     def forward(self, x: torch.Tensor):
-        snn.encode(x, self.T, out=self.lat0, ws=self.ws_enc)
-        self.l1(self.lat0)
+        self.encode(x)
+        self.l1(self.lat0_buf)
         snn.inhibit(self.l1.plat, self.l1.pv, lat_out=self.ilat, v_out=self.iv, winner_f=self.wf)
         snn.k_winners(self.ilat, self.iv, self.wl.extra["k"], self.wl.extra["r"], winners=self.winners,
                       count=self.count, ws=self.ws_kw)

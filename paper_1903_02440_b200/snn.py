@@ -50,6 +50,8 @@ def lib() -> C.CDLL:
                 "snn_validate_lat": (i32, [p, sz, i32, p, p]),
                 "snn_conv_fire_workspace": (sz, [i32] * 9 + [f32]),
                 "snn_conv_fire": (i32, [p, i32, i32, i32, i32, i32, p, i32, i32, i32, i32, f32, p, p, p, p, sz, p]),
+                "snn_conv_fire_ex": (i32, [p, i32, i32, i32, i32, i32, p, i32, i32, i32, i32, f32, i32, p, p, p, p, sz,
+                                           p]),
                 "snn_pool": (i32, [p, p, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, p, p, p]),
                 "snn_pool_ex": (i32, [p, p] + [i32] * 11 + [p, p, p]),
                 "snn_encode_ex": (i32, [p, i32, i32, i32, i32, i32, i32, p, p, sz, p]),
@@ -93,7 +95,7 @@ def exported_symbols():
             "snn_stdp_sequence", "snn_filter_bank", "snn_local_norm", "snn_lateral_inhibition",
             "snn_encode_ex", "snn_pool_ex", "snn_position_keys", "snn_k_winners_keys_workspace",
             "snn_k_winners_keys", "snn_stdp_update_shard", "snn_conv_inf_prepare_bytes", "snn_conv_inf_prepare",
-            "snn_conv_fire_prepared"]
+            "snn_conv_fire_prepared", "snn_conv_fire_ex"]
 
 
 def _check(rc: int):
@@ -120,16 +122,21 @@ def _req(t: torch.Tensor, dtype, name: str):
 
 
 class _Workspace:
-    """Grow-only device scratch buffers, one per (device, tag)."""
+    """Grow-only device scratch buffers, one per (device, tag, stream): calls on different streams never
+    share scratch.  A buffer replaced by a larger one is released to torch's caching allocator; when it
+    was used on a side stream, record_stream keeps it from being reused before that stream's work ends."""
 
     def __init__(self):
         self._bufs = {}
 
-    def get(self, nbytes: int, device, tag: str = "") -> torch.Tensor:
-        key = (str(device), tag)
+    def get(self, nbytes: int, device, tag: str = "", stream=None) -> torch.Tensor:
+        s = stream if stream is not None else torch.cuda.current_stream(device)
+        key = (str(device), tag, s.cuda_stream)
         b = self._bufs.get(key)
         if b is None or b.numel() < nbytes:
             b = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+            if stream is not None:
+                b.record_stream(stream)
             self._bufs[key] = b
         return b
 
@@ -142,15 +149,22 @@ def encode_workspace(B, C_, H, W, T) -> int:
     return int(lib().snn_encode_workspace(B, C_, H, W, T))
 
 
+ENCODE_OUT_NHWC = 0x100  # or'ed into snn_encode_ex's bins
+
+
 def encode(x: torch.Tensor, T: int, out: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None,
-           stream=None, bins: int = 0) -> torch.Tensor:
-    """x float32 [B, C, H, W] -> lat uint8 [B, C, H, W] (snn_encode; bins != 0: snn_encode_ex variant)."""
+           stream=None, bins: int = 0, nhwc: bool = False) -> torch.Tensor:
+    """x float32 [B, C, H, W] -> lat uint8 [B, C, H, W] (snn_encode; bins != 0: snn_encode_ex variant);
+    nhwc: lat channels-last [B, H, W, C] (SNN_ENCODE_OUT_NHWC)."""
     _req(x, torch.float32, "x")
     B, C_, H, W = x.shape
-    lat = out if out is not None else torch.empty(x.shape, dtype=torch.uint8, device=x.device)
+    shape = (B, H, W, C_) if nhwc else tuple(x.shape)
+    lat = out if out is not None else torch.empty(shape, dtype=torch.uint8, device=x.device)
     _req(lat, torch.uint8, "lat")
     n = encode_workspace(B, C_, H, W, T)
-    buf = ws if ws is not None else _ws.get(n, x.device, "encode")
+    buf = ws if ws is not None else _ws.get(n, x.device, "encode", stream)
+    if nhwc:
+        bins |= ENCODE_OUT_NHWC
     if bins:
         _check(lib().snn_encode_ex(_ptr(x), B, C_, H, W, T, bins, _ptr(lat), _ptr(buf), buf.numel(),
                                    _stream(stream)))
@@ -224,26 +238,40 @@ def conv_fire_workspace(B, C_, H, W, pad, F, KH, KW, T, theta) -> int:
     return int(lib().snn_conv_fire_workspace(B, C_, H, W, pad, F, KH, KW, T, float(theta)))
 
 
+CONV_OUT_NHWC, CONV_IN_NHWC = 1, 2  # snn_conv_fire_ex flags
+
+
 def conv_fire(lat_in: torch.Tensor, w: torch.Tensor, pad: int, T: int, theta: float, want_pot: bool = False,
-              lat_out=None, v_out=None, ws=None, stream=None):
+              lat_out=None, v_out=None, ws=None, stream=None, nhwc: bool = False, want_v: bool = True,
+              in_nhwc: bool = False):
     """lat_in uint8 [B, C, H, W], w float32 [F, C, KH, KW] -> (lat uint8, v float32) [B, F, Ho, Wo]
-    (+ pot float32 [B, T, F, Ho, Wo] when want_pot)."""
+    (+ pot float32 [B, T, F, Ho, Wo] when want_pot).  nhwc: outputs channels-last [B, Ho, Wo, F]
+    (snn_conv_fire_ex SNN_CONV_OUT_NHWC); in_nhwc: lat_in is [B, H, W, C] (SNN_CONV_IN_NHWC);
+    want_v False: v is not written (None returned)."""
     _req(lat_in, torch.uint8, "lat_in")
     _req(w, torch.float32, "w")
-    B, C_, H, W = lat_in.shape
+    if in_nhwc:
+        B, H, W, C_ = lat_in.shape
+    else:
+        B, C_, H, W = lat_in.shape
     F, Cw, KH, KW = w.shape
     if Cw != C_:
         raise ValueError("channel mismatch between lat_in and w")
     Ho, Wo = conv_out_hw(H, W, KH, KW, pad)
     Ho, Wo = max(Ho, 0), max(Wo, 0)          # invalid shapes are rejected by the library (SNN_ESHAPE)
     dev = lat_in.device
-    lat = lat_out if lat_out is not None else torch.empty((B, F, Ho, Wo), dtype=torch.uint8, device=dev)
-    v = v_out if v_out is not None else torch.empty((B, F, Ho, Wo), dtype=torch.float32, device=dev)
+    shape = (B, Ho, Wo, F) if nhwc else (B, F, Ho, Wo)
+    lat = lat_out if lat_out is not None else torch.empty(shape, dtype=torch.uint8, device=dev)
+    v = None
+    if want_v:
+        v = v_out if v_out is not None else torch.empty(shape, dtype=torch.float32, device=dev)
     pot = torch.empty((B, T, F, Ho, Wo), dtype=torch.float32, device=dev) if want_pot else None
     n = conv_fire_workspace(B, C_, H, W, pad, F, KH, KW, T, theta)
-    buf = ws if ws is not None else _ws.get(n, dev, "conv")
-    _check(lib().snn_conv_fire(_ptr(lat_in), B, C_, H, W, pad, _ptr(w), F, KH, KW, T, float(theta),
-                               _ptr(lat), _ptr(v), _ptr(pot), _ptr(buf), buf.numel(), _stream(stream)))
+    buf = ws if ws is not None else _ws.get(n, dev, "conv", stream)
+    _check(lib().snn_conv_fire_ex(_ptr(lat_in), B, C_, H, W, pad, _ptr(w), F, KH, KW, T, float(theta),
+                                  (CONV_OUT_NHWC if nhwc else 0) | (CONV_IN_NHWC if in_nhwc else 0), _ptr(lat),
+                                  _ptr(v), _ptr(pot), _ptr(buf), buf.numel(),
+                                  _stream(stream)))
     return (lat, v, pot) if want_pot else (lat, v)
 
 
@@ -268,7 +296,7 @@ def conv_fire_prepared(prep: torch.Tensor, b: int, C_: int, H: int, W: int, w: t
     lat = lat_out if lat_out is not None else torch.empty((1, F, Ho, Wo), dtype=torch.uint8, device=dev)
     v = v_out if v_out is not None else torch.empty((1, F, Ho, Wo), dtype=torch.float32, device=dev)
     n = conv_fire_workspace(1, C_, H, W, pad, F, KH, KW, T, float("inf"))
-    buf = ws if ws is not None else _ws.get(n, dev, "conv")
+    buf = ws if ws is not None else _ws.get(n, dev, "conv", stream)
     _check(lib().snn_conv_fire_prepared(_ptr(prep), int(b), C_, H, W, pad, _ptr(w), F, KH, KW, T, _ptr(lat), _ptr(v),
                                         _ptr(buf), buf.numel(), _stream(stream)))
     return lat, v
@@ -281,7 +309,7 @@ def pool_out_hw(H, W, PH, PW, SH, SW, DH=0, DW=0, eq3=False):
     return (H + 2 * DH - PH) // SH + 1, (W + 2 * DW - PW) // SW + 1
 
 
-POOL_EQ3, POOL_VFINAL = 1, 2  # snn_pool_ex flags (f3 variants)
+POOL_EQ3, POOL_VFINAL, POOL_IN_NHWC, POOL_OUT_NHWC = 1, 2, 4, 8  # snn_pool_ex flags (f3 variants; layouts)
 
 
 def pool(lat: torch.Tensor, v: Optional[torch.Tensor], window, stride=None, padding=(0, 0),
@@ -292,12 +320,16 @@ def pool(lat: torch.Tensor, v: Optional[torch.Tensor], window, stride=None, padd
     PH, PW = (window, window) if isinstance(window, int) else window
     SH, SW = (PH, PW) if stride is None else ((stride, stride) if isinstance(stride, int) else stride)
     DH, DW = (padding, padding) if isinstance(padding, int) else padding
-    B, F, H, W = lat.shape
+    if flags & POOL_IN_NHWC:
+        B, H, W, F = lat.shape
+    else:
+        B, F, H, W = lat.shape
     Ho, Wo = (max(d, 0) for d in pool_out_hw(H, W, PH, PW, SH, SW, DH, DW, bool(flags & POOL_EQ3)))
-    lo = lat_out if lat_out is not None else torch.empty((B, F, Ho, Wo), dtype=torch.uint8, device=lat.device)
+    oshape = (B, Ho, Wo, F) if flags & POOL_OUT_NHWC else (B, F, Ho, Wo)
+    lo = lat_out if lat_out is not None else torch.empty(oshape, dtype=torch.uint8, device=lat.device)
     vo = None
     if v is not None:
-        vo = v_out if v_out is not None else torch.empty((B, F, Ho, Wo), dtype=torch.float32, device=lat.device)
+        vo = v_out if v_out is not None else torch.empty(oshape, dtype=torch.float32, device=lat.device)
     if flags:
         _check(lib().snn_pool_ex(_ptr(lat), _ptr(v), B, F, H, W, PH, PW, SH, SW, DH, DW, flags, _ptr(lo), _ptr(vo),
                                  _stream(stream)))
@@ -327,7 +359,7 @@ def k_winners(lat: torch.Tensor, v: torch.Tensor, k: int, r: int, winners=None, 
     win = winners if winners is not None else torch.empty((B, k, 3), dtype=torch.int32, device=lat.device)
     cnt = count if count is not None else torch.empty((B,), dtype=torch.int32, device=lat.device)
     n = int(lib().snn_k_winners_workspace(B, F, H, W))
-    buf = ws if ws is not None else _ws.get(n, lat.device, "kwta")
+    buf = ws if ws is not None else _ws.get(n, lat.device, "kwta", stream)
     _check(lib().snn_k_winners(_ptr(lat), _ptr(v), B, F, H, W, k, r, _ptr(win), _ptr(cnt), _ptr(buf), buf.numel(),
                                _stream(stream)))
     return win, cnt
@@ -385,7 +417,7 @@ def k_winners_keys(keys: torch.Tensor, F: int, k: int, r: int, winners=None, cou
     win = winners if winners is not None else torch.empty((B, k, 3), dtype=torch.int32, device=keys.device)
     cnt = count if count is not None else torch.empty((B,), dtype=torch.int32, device=keys.device)
     n = int(lib().snn_k_winners_keys_workspace(B, H, W))
-    buf = ws if ws is not None else _ws.get(n, keys.device, "kwta_keys")
+    buf = ws if ws is not None else _ws.get(n, keys.device, "kwta_keys", stream)
     _check(lib().snn_k_winners_keys(_ptr(keys), B, int(F), H, W, k, r, _ptr(win), _ptr(cnt), _ptr(buf), buf.numel(),
                                     _stream(stream)))
     return win, cnt

@@ -54,20 +54,31 @@ def test_c1_full(G, orc):
     assert np.array_equal(host(seq.w), ref["w_new"])
 
 
-def test_c2_parity(G, orc):
+@pytest.fixture(scope="module")
+def c2_ref(orc):
     from oracle import flows
+    wl = synth.C2(n=1000)
+    return wl, flows.c2(wl)
+
+
+@pytest.mark.parametrize("nhwc,conv_v", [(True, False), (True, True), (False, True)])
+def test_c2_parity(G, c2_ref, nhwc, conv_v):
+    """(True, False) is the bench's configuration (channels-last layers 1-2, no unused potentials)."""
     from paper_1903_02440_b200 import pipeline
-    n = 1000
-    wl = synth.C2(n=n)
-    ref = flows.c2(wl)
-    net = pipeline.C2Net(wl, n)
+    wl, ref = c2_ref
+    n = wl.X.shape[0]
+    net = pipeline.C2Net(wl, n, nhwc=nhwc, conv_v=conv_v)
     net.forward(cu(wl.X))
     G.sync_status()
     assert np.array_equal(host(net.lat0), ref["lat0"])
     assert np.array_equal(host(net.l1.lat), ref["l1"]["lat"])
     assert np.array_equal(host(net.l1.plat), ref["l1"]["pool_lat"])
     assert np.array_equal(host(net.l2.lat), ref["l2"]["lat"])
-    assert np.array_equal(host(net.l2.v), ref["l2"]["v"])
+    if conv_v:
+        assert np.array_equal(host(net.l1.v), ref["l1"]["v"])
+        assert np.array_equal(host(net.l2.v), ref["l2"]["v"])
+    else:
+        assert net.l1.v is None and net.l2.v is None
     assert np.array_equal(host(net.l2.plat), ref["l2"]["pool_lat"])
     assert np.array_equal(host(net.l3.lat), ref["l3"]["lat"])
     assert np.array_equal(host(net.l3.v), ref["l3"]["v"])

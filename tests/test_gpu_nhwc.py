@@ -1,0 +1,170 @@
+"""GPU parity of the channels-last options: snn_conv_fire_ex(SNN_CONV_OUT_NHWC) and
+snn_pool_ex(SNN_POOL_IN_NHWC), and of v_out = NULL.
+
+The conv's channels-last output is the planar oracle result transposed (same neurons, other layout);
+the pool reading it must equal the oracle pool of the planar map.  Bit-exact (N1).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from test_gpu_kernels import CONV_CASES, cu, exact_weights, host
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_1903_02440_b200 import build, snn
+    build.build()
+    snn.lib()
+    return snn
+
+
+@pytest.mark.parametrize("path", ["walk", "tct", "ref"])
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_fire_nhwc_vs_oracle(G, orc, case, path, monkeypatch):
+    monkeypatch.setenv("SNN_CONV_PATH", path)
+    B, C, H, W, pad, F, K, T, theta, p = case
+    rng = np.random.default_rng((abs(hash(case)) + 7) % 2 ** 31)
+    import synth
+    lat_in = synth.random_latencies(rng, (B, C, H, W), T, p)
+    w = exact_weights(rng, (F, C, K, K))
+    lat, v = G.conv_fire(cu(lat_in), cu(w), pad, T, theta, nhwc=True)
+    lat_only, none_v = G.conv_fire(cu(lat_in), cu(w), pad, T, theta, nhwc=True, want_v=False)
+    G.sync_status()
+    assert none_v is None
+    ol, ov = orc.conv_fire(lat_in, w, pad, T, theta)
+    assert np.array_equal(host(lat), ol.transpose(0, 2, 3, 1))
+    assert np.array_equal(host(v), ov.transpose(0, 2, 3, 1))
+    assert np.array_equal(host(lat_only), ol.transpose(0, 2, 3, 1))
+
+
+@pytest.mark.parametrize("case", CONV_CASES[:6])
+def test_conv_fire_planar_without_v(G, orc, case):
+    B, C, H, W, pad, F, K, T, theta, p = case
+    rng = np.random.default_rng(abs(hash(case)) % 2 ** 31)
+    import synth
+    lat_in = synth.random_latencies(rng, (B, C, H, W), T, p)
+    w = exact_weights(rng, (F, C, K, K))
+    lat, v = G.conv_fire(cu(lat_in), cu(w), pad, T, theta, want_v=False)
+    G.sync_status()
+    assert v is None
+    ol, _ = orc.conv_fire(lat_in, w, pad, T, theta)
+    assert np.array_equal(host(lat), ol)
+
+
+@pytest.mark.parametrize("win,stride,pad,with_v,F,flags", [
+    ((2, 2), (2, 2), (0, 0), True, 256, 0), ((2, 2), (2, 2), (0, 0), False, 30, 0),
+    ((3, 3), (3, 3), (0, 0), False, 250, 0), ((7, 7), (6, 6), (0, 0), False, 20, 0),
+    ((7, 7), (6, 6), (0, 0), True, 33, 0), ((3, 2), (2, 1), (1, 1), True, 5, 0),
+    ((2, 3), (3, 2), (1, 0), True, 70, 0), ((1, 1), (1, 1), (0, 0), True, 1, 0),
+    ((3, 3), (2, 2), (1, 1), True, 40, 1), ((2, 2), (2, 2), (0, 0), True, 64, 2),
+    ((3, 3), (3, 3), (0, 0), True, 31, 3)])
+def test_pool_nhwc_vs_oracle(G, orc, win, stride, pad, with_v, F, flags):
+    """flags: 1 = SNN_POOL_EQ3, 2 = SNN_POOL_VFINAL (combined with SNN_POOL_IN_NHWC)."""
+    import synth
+    rng = np.random.default_rng(F * 7 + flags)
+    T = 9
+    lat = synth.random_latencies(rng, (3, F, 37, 70), T, 0.5)
+    v = synth.random_potentials_at_spike(rng, lat, 4)
+    lat_h = np.ascontiguousarray(lat.transpose(0, 2, 3, 1))
+    v_h = np.ascontiguousarray(v.transpose(0, 2, 3, 1))
+    gl, gv = G.pool(cu(lat_h), cu(v_h) if with_v else None, win, stride, pad, flags=flags | G.POOL_IN_NHWC)
+    gl2, gv2 = G.pool(cu(lat), cu(v) if with_v else None, win, stride, pad, flags=flags)
+    ol, ov = orc.pool(lat, v if with_v else None, *win, *stride, *pad, T, eq3=bool(flags & 1), vfinal=bool(flags & 2))
+    assert np.array_equal(host(gl), ol) and np.array_equal(host(gl2), ol)
+    if with_v:
+        assert np.array_equal(host(gv), ov) and np.array_equal(host(gv2), ov)
+
+
+def test_nhwc_conv_then_pool_chain(G, orc):
+    """C5-shaped chain (smaller): conv (channels-last, lat + v) -> pool 2/2 reading it == oracle."""
+    import synth
+    rng = np.random.default_rng(21)
+    B, C, H, W, pad, F, K, T, theta = 2, 32, 24, 24, 2, 256, 5, 32, 40.0
+    lat_in = synth.random_latencies(rng, (B, C, H, W), T, 0.5)
+    w = exact_weights(rng, (F, C, K, K), lo=2 ** -5)
+    lat, v = G.conv_fire(cu(lat_in), cu(w), pad, T, theta, nhwc=True)
+    pl, pv = G.pool(lat, v, 2, 2, 0, flags=G.POOL_IN_NHWC)
+    G.sync_status()
+    ol, ov = orc.conv_fire(lat_in, w, pad, T, theta)
+    opl, opv = orc.pool(ol, ov, 2, 2, 2, 2, 0, 0, T)
+    assert np.array_equal(host(pl), opl) and np.array_equal(host(pv), opv)
+
+
+def test_conv_fire_ex_bad_flags(G):
+    lat_in = torch.zeros((1, 1, 4, 4), dtype=torch.uint8, device="cuda")
+    w = torch.full((2, 1, 3, 3), 0.5, dtype=torch.float32, device="cuda")
+    out = torch.empty((1, 2, 2, 2), dtype=torch.uint8, device="cuda")
+    ws = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    L = G.lib()
+    rc = L.snn_conv_fire_ex(G._ptr(lat_in), 1, 1, 4, 4, 0, G._ptr(w), 2, 3, 3, 4, 1.0, 8, G._ptr(out), None, None,
+                            G._ptr(ws), ws.numel(), G._stream(None))
+    assert rc == G.SNN_EINVAL
+
+
+# ----------------------------------------------------------------- channels-last inputs (encode -> conv -> pool)
+@pytest.mark.parametrize("shape,T", [((1, 2, 28, 28), 15), ((7, 6, 28, 28), 15), ((3, 4, 60, 70), 30),
+                                     ((2, 32, 40, 40), 32), ((2, 1, 1, 5), 10)])
+def test_encode_nhwc_vs_oracle(G, orc, shape, T):
+    """all three encode paths (bitonic: few small images; one-CTA select; multi-kernel radix select)."""
+    rng = np.random.default_rng(sum(shape) + T)
+    x = rng.random(shape).astype(np.float32)
+    x[rng.random(shape) < 0.4] = 0
+    x.reshape(-1)[::13] = 0.5
+    got = host(G.encode(cu(x), T, nhwc=True))
+    assert np.array_equal(got, orc.encode(x, T).transpose(0, 2, 3, 1))
+
+
+@pytest.mark.parametrize("out_nhwc", [True, False])
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_fire_in_nhwc_vs_oracle(G, orc, case, out_nhwc):
+    """channels-last input on the default path: fused / presorted walk (finite theta), tcgen05 (theta = inf)."""
+    B, C, H, W, pad, F, K, T, theta, p = case
+    rng = np.random.default_rng((abs(hash(case)) + 11) % 2 ** 31)
+    import synth
+    lat_in = synth.random_latencies(rng, (B, C, H, W), T, p)
+    w = exact_weights(rng, (F, C, K, K))
+    lat, v = G.conv_fire(cu(np.ascontiguousarray(lat_in.transpose(0, 2, 3, 1))), cu(w), pad, T, theta,
+                         nhwc=out_nhwc, in_nhwc=True)
+    G.sync_status()
+    ol, ov = orc.conv_fire(lat_in, w, pad, T, theta)
+    if out_nhwc:
+        ol, ov = ol.transpose(0, 2, 3, 1), ov.transpose(0, 2, 3, 1)
+    assert np.array_equal(host(lat), ol)
+    assert np.array_equal(host(v), ov)
+
+
+def test_conv_in_nhwc_rejects_validation_paths(G, monkeypatch):
+    lat_in = torch.zeros((1, 4, 4, 1), dtype=torch.uint8, device="cuda")
+    w = torch.full((2, 1, 3, 3), 0.5, dtype=torch.float32, device="cuda")
+    with pytest.raises(G.SNNError):
+        G.conv_fire(lat_in, w, 0, 4, 1.0, want_pot=True, in_nhwc=True)
+    monkeypatch.setenv("SNN_CONV_PATH", "ref")
+    with pytest.raises(G.SNNError):
+        G.conv_fire(lat_in, w, 0, 4, 1.0, in_nhwc=True)
+
+
+@pytest.mark.parametrize("win,stride,pad,with_v,F,flags", [
+    ((2, 2), (2, 2), (0, 0), False, 30, 0), ((3, 3), (3, 3), (0, 0), False, 250, 0),
+    ((2, 2), (2, 2), (0, 0), True, 256, 0), ((2, 2), (2, 2), (0, 0), False, 64, 0),
+    ((7, 7), (6, 6), (0, 0), False, 20, 0), ((3, 2), (2, 1), (1, 1), True, 5, 0),
+    ((3, 3), (2, 2), (1, 1), True, 40, 1), ((2, 2), (2, 2), (0, 0), True, 64, 2)])
+def test_pool_nhwc_to_nhwc_vs_oracle(G, orc, win, stride, pad, with_v, F, flags):
+    import synth
+    rng = np.random.default_rng(F * 3 + flags + 1)
+    T = 9
+    lat = synth.random_latencies(rng, (3, F, 37, 70), T, 0.5)
+    v = synth.random_potentials_at_spike(rng, lat, 4)
+    lat_h = np.ascontiguousarray(lat.transpose(0, 2, 3, 1))
+    v_h = np.ascontiguousarray(v.transpose(0, 2, 3, 1))
+    gl, gv = G.pool(cu(lat_h), cu(v_h) if with_v else None, win, stride, pad,
+                    flags=flags | G.POOL_IN_NHWC | G.POOL_OUT_NHWC)
+    ol, ov = orc.pool(lat, v if with_v else None, *win, *stride, *pad, T, eq3=bool(flags & 1), vfinal=bool(flags & 2))
+    assert np.array_equal(host(gl), ol.transpose(0, 2, 3, 1))
+    if with_v:
+        assert np.array_equal(host(gv), ov.transpose(0, 2, 3, 1))
