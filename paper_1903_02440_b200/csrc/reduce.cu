@@ -254,11 +254,11 @@ __global__ void __launch_bounds__(256) pool_nhwc2nhwc_kernel(const uint8_t* __re
                                                              float* __restrict__ v_out) {
   pdl_begin();
   const uint32_t FV = uint32_t(F / VEC), HoWo = uint32_t(Ho) * Wo;
-  const uint64_t total = uint64_t(B) * HoWo * FV;
-  for (uint64_t o = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; o < total; o += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t pix = o / FV;
+  const uint32_t total = uint32_t(B) * HoWo * FV;  // < 2^32 (checked by the launcher): 32-bit index math
+  for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
+    const uint32_t pix = o / FV;
     const int f = int(o - pix * FV) * VEC;
-    const uint32_t b = uint32_t(pix / HoWo), rem = uint32_t(pix - uint64_t(b) * HoWo);
+    const uint32_t b = pix / HoWo, rem = pix - b * HoWo;
     const int oy = int(rem / uint32_t(Wo)), ox = int(rem - uint32_t(oy) * Wo);
     const uint8_t* limg = lat + int64_t(b) * H * W * F;
     const int64_t oi = int64_t(pix) * F + f;
@@ -304,6 +304,7 @@ int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, 
     const float* vin = v_out ? v : nullptr;
     const int vf = (flags & SNN_POOL_VFINAL) ? 1 : 0;
     if (flags & SNN_POOL_OUT_NHWC) {
+      if (total >= (int64_t(1) << 32)) return set_error(SNN_ESHAPE, "snn_pool(NHWC output): B*Ho*Wo*F >= 2^32");
       int64_t nb = ceil_div(total / vec, 256);
       if (nb > int64_t(num_sms()) * 16) nb = int64_t(num_sms()) * 16;
       if (vec == 4)

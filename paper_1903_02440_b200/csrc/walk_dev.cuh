@@ -13,7 +13,6 @@ namespace snn {
 constexpr int kWalkSmemLimit = 227 * 1024;
 constexpr size_t kListChunkBytes = size_t(512) << 20;  // sorted lists per chunk (measured: fewer, larger chunks win;
                                                         // the lists stream from HBM either way)
-constexpr int kBlk = 8;                               // list entries per gather block
 constexpr int kIt = 16;                               // list entries per walk iteration (lists padded to this)
 constexpr int kListSlack = 2048;
 #ifndef SNN_SORT_UNROLL
@@ -48,6 +47,8 @@ struct WalkArgs {
   // (no separate weight-prep launch); nullptr = copy the prepared wq
   const float* wf32;
   int nhwc;           // output layout: 0 = [B, F, Ho, Wo], 1 = [B, Ho, Wo, F] (SNN_CONV_OUT_NHWC)
+  const int* kstar;   // nullable: K* (kstar_kernel) -- any K* spiking inputs fire every feature, so a
+                      // sorted list can end with the first bucket that brings its count to K* (K2b)
   int in_nhwc;        // input layout [B, H, W, C] (SNN_CONV_IN_NHWC): receptive-field entries are then
                       // ordered (ky, kx, c) -- e = (ky KW + kx) C + c -- and so are the weight rows
 };
@@ -112,10 +113,34 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl
     }
   }
   __syncwarp();
+  // K2b: the last bucket kept, tcut = the first bucket whose running count reaches K* (every feature
+  // has fired by its end, see kstar_kernel); later buckets are neither placed nor walked
+  int tcut = T - 1;
+  if (a.kstar) {
+    const int ks = *a.kstar;
+    if (ks < R) {
+      int carry_r = 0;
+      bool found = false;
+      for (int tb = 0; tb < T; tb += LPP) {
+        const int t = tb + gl;
+        int inc = t < T ? int(cnt[t]) : 0;
+#pragma unroll
+        for (int o = 1; o < LPP; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, inc, o, LPP);
+          if (gl >= o) inc += v;
+        }
+        const bool reach = t < T && carry_r + inc >= ks;
+        const unsigned m = __ballot_sync(0xffffffffu, reach);
+        const unsigned gm = (LPP == 32) ? m : (m >> ((threadIdx.x & 31) / LPP * LPP)) & ((1u << LPP) - 1u);
+        if (!found && gm) { tcut = tb + __ffs(gm) - 1; found = true; }
+        carry_r += __shfl_sync(0xffffffffu, inc, LPP - 1, LPP);
+      }
+    }
+  }
   int carry = 0;
   for (int tb = 0; tb < T; tb += LPP) {
     const int t = tb + gl;
-    const int tot = t < T ? int(cnt[t]) : 0;
+    const int tot = t <= tcut ? int(cnt[t]) : 0;
     const int padded = tot + (tot & 1);  // buckets padded to even length: every bucket end is on a pair boundary
     int inc = padded;
 #pragma unroll
@@ -137,7 +162,7 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl
 #pragma unroll kSortUnroll
     for (int e = gl; e < R; e += LPP) {
       const int l = lat_of(e);
-      if (l < T) list[atomicAdd(&cnt[l], 1u)] = uint32_t(e) * rb;
+      if (l <= tcut) list[atomicAdd(&cnt[l], 1u)] = uint32_t(e) * rb;
     }
   }
   {  // pad the tail to a whole walk iteration with the zero-weight row R
@@ -264,39 +289,46 @@ __device__ __forceinline__ void fire_at(uint64_t (&acc)[FPL], int64_t thr, int t
   }
 }
 
-// One 8-input block of the walk (entries e0, e1: weight-row byte offsets).  The bucket ends inside
-// the block are known to the whole group beforehand (endm: bit m = a bucket ends after pair m, its
-// first-spike index in byte m of tpk).  Each lane sums its features' 8 weights exactly; if no
+// One NB-input block of the walk (NB = 8 or 16; entries: NB weight-row byte offsets).  The bucket
+// ends inside the block are known to the whole group beforehand (endm: bit m = a bucket ends after pair
+// m, its first-spike index in byte m of tpk).  Each lane sums its features' NB weights exactly; if no
 // unfired feature of the lane then exceeds the threshold, no test inside the block could fire
 // (potentials only grow along the list) and the block is taken whole; otherwise the lane re-adds it
 // pair by pair from the same registers and tests at every bucket end (K3).  Lanes decide
-// independently (no vote): the group's bookkeeping does not depend on the branch taken.  S28: the
-// block's 8 weights are summed in 32 bits (exact, < 2^31) and added to the 64-bit accumulator once.
-template <int FPL, bool S28>
-__device__ __forceinline__ void walk_block(uint32_t wls, const uint4& e0, const uint4& e1, unsigned endm,
-                                           uint32_t tpk, int64_t thr, uint64_t (&acc)[FPL], uint32_t& lo,
-                                           float (&vo)[FPL]) {
-  const uint32_t off[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
-  uint32_t wv[8][FPL];
+// independently (no vote): the group's bookkeeping does not depend on the branch taken.  S28: every
+// 8 weights are summed in 32 bits (exact, < 2^31) and added to the 64-bit accumulator (K3b).
+template <int FPL, bool S28, int NB>
+__device__ __forceinline__ void walk_block(uint32_t wls, const uint32_t (&off)[NB], unsigned endm, uint64_t tpk,
+                                           int64_t thr, uint64_t (&acc)[FPL], uint32_t& lo, float (&vo)[FPL]) {
+  uint32_t wv[NB][FPL];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) wgather_s<FPL>(wls + off[k], wv[k]);
+  for (int k = 0; k < NB; ++k) wgather_s<FPL>(wls + off[k], wv[k]);
   uint64_t s[FPL];
   bool hit = false;
 #pragma unroll
   for (int j = 0; j < FPL; ++j) {
     if constexpr (S28) {
-      const uint32_t b = ((wv[0][j] + wv[1][j]) + (wv[2][j] + wv[3][j])) + ((wv[4][j] + wv[5][j]) + (wv[6][j] + wv[7][j]));
-      s[j] = acc[j] + b;
+      uint64_t t = acc[j];
+#pragma unroll
+      for (int h = 0; h < NB; h += 8) {
+        const uint32_t b = ((wv[h][j] + wv[h + 1][j]) + (wv[h + 2][j] + wv[h + 3][j])) +
+                           ((wv[h + 4][j] + wv[h + 5][j]) + (wv[h + 6][j] + wv[h + 7][j]));
+        t += b;
+      }
+      s[j] = t;
     } else {
-      s[j] = acc[j] + (uint64_t(wv[0][j]) + wv[1][j]) + (uint64_t(wv[2][j]) + wv[3][j]) +
-             (uint64_t(wv[4][j]) + wv[5][j]) + (uint64_t(wv[6][j]) + wv[7][j]);
+      uint64_t t = acc[j];
+#pragma unroll
+      for (int h = 0; h < NB; h += 2) t += uint64_t(wv[h][j]) + wv[h + 1][j];
+      s[j] = t;
     }
     hit |= int64_t(s[j]) > thr;
   }
+  constexpr unsigned kInner = (1u << (NB / 2 - 1)) - 1u;  // bucket ends strictly inside the block
   if (hit && endm) {
-    if (endm & 7u) {  // a bucket ends strictly inside the block: pair by pair
+    if (endm & kInner) {  // pair by pair
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
+      for (int m = 0; m < NB / 2; ++m) {
 #pragma unroll
         for (int j = 0; j < FPL; ++j) {
           if constexpr (S28) acc[j] += uint32_t(wv[2 * m][j] + wv[2 * m + 1][j]);
@@ -309,7 +341,7 @@ __device__ __forceinline__ void walk_block(uint32_t wls, const uint4& e0, const 
     // the only bucket end is the block end
 #pragma unroll
     for (int j = 0; j < FPL; ++j) acc[j] = s[j];
-    fire_at<FPL, S28>(acc, thr, int(tpk >> 24), lo, vo);
+    fire_at<FPL, S28>(acc, thr, int((tpk >> (8 * (NB / 2 - 1))) & 0xFFu), lo, vo);
     return;
   }
 #pragma unroll
@@ -349,10 +381,24 @@ __device__ __forceinline__ void walk_list(const WalkArgs& a, const unsigned char
       const unsigned nd = __ballot_sync(0xffffffffu, alive());
       if ((nd & gmask) == 0) done = true;  // all features of the group fired (or are padding)
     }
-    int i = 0, t = 0, it = 0;
-    while (t < T && int(start[t + 1]) == 0) ++t;  // leading empty buckets (handled above)
+    int i = 0, it = 0;
+    // the first non-empty bucket (leading empty ones were handled above): the group's lanes test LPP
+    // buckets per vote (no serial chain of dependent header loads); a uniform trip count keeps every
+    // group's lanes in the full-warp ballots
+    constexpr int LPP = 32 / PPW;
+    const int gl = int(threadIdx.x & 31) % LPP;
+    int t = T;
+    for (int tb = 0; tb < T; tb += LPP) {
+      const int tt = tb + gl;
+      const bool ne = pv && tt < T && int(start[tt + 1]) != 0;
+      const unsigned m = (__ballot_sync(0xffffffffu, ne) & gmask) >> (gmask == 0xffffffffu ? 0 : __ffs(gmask) - 1);
+      if (t == T && m) t = tb + __ffs(m) - 1;
+    }
     int bend = t < T ? int(start[t + 1]) : 0x7FFFFFFF;  // end of the current non-empty bucket t
     int guard = (total + kIt - 1) / kIt + 2;  // iterations this group can take (a bug trap, never hit)
+    uint32_t ebase;  // shared-window address of the entries (computed once, kept in a register)
+    asm volatile("mov.u32 %0, %1;" : "=r"(ebase)
+                 : "r"(smem_u32(PRE ? static_cast<const void*>(sent) : static_cast<const void*>(list))));
     // Every vote below is a full-warp ballot at a converged point; done is group-uniform.
     while (true) {
       if (__ballot_sync(0xffffffffu, !done) == 0) break;
@@ -362,30 +408,37 @@ __device__ __forceinline__ void walk_list(const WalkArgs& a, const unsigned char
 #pragma unroll
         for (int u = 0; u < 4; ++u) cur[u] = __ldg(g4 + u);
       } else {
-        const uint32_t sa = smem_u32(PRE ? static_cast<const void*>(sent + it * kIt * 4)
-                                         : static_cast<const void*>(list + it * kIt));
+        const uint32_t sa = ebase + uint32_t(it * kIt * 4);
 #pragma unroll
         for (int u = 0; u < 4; ++u)
           asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                        : "=r"(cur[u].x), "=r"(cur[u].y), "=r"(cur[u].z), "=r"(cur[u].w)
                        : "r"(sa + 16 * u));
       }
+      // blocks of NB entries: 16 for FPL <= 2 (one bookkeeping / vote / threshold test per 16 gathers),
+      // 8 for FPL = 4 (register budget: 4 registers per gathered entry)
+      constexpr int NB = FPL == 4 ? 8 : 16;
+      const uint32_t offs[16] = {cur[0].x, cur[0].y, cur[0].z, cur[0].w, cur[1].x, cur[1].y, cur[1].z, cur[1].w,
+                                 cur[2].x, cur[2].y, cur[2].z, cur[2].w, cur[3].x, cur[3].y, cur[3].z, cur[3].w};
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < 16 / NB; ++h) {
         if (!done) {
           // group-uniform: bucket ends inside this block (pair m ends bucket t_m)
           unsigned endm = 0;
-          uint32_t tpk = 0;
-          i += kBlk;
+          uint64_t tpk = 0;
+          i += NB;
           while (bend <= i) {
-            const int m = ((bend - (i - kBlk)) >> 1) - 1;
+            const int m = ((bend - (i - NB)) >> 1) - 1;
             endm |= 1u << m;
-            tpk |= uint32_t(t) << (8 * m);
+            tpk |= uint64_t(t) << (8 * m);
             ++t;
             while (t < T && int(start[t + 1]) == bend) ++t;  // empty buckets add nothing
             bend = t < T ? int(start[t + 1]) : 0x7FFFFFFF;
           }
-          walk_block<FPL, S28>(wls, cur[2 * h], cur[2 * h + 1], endm, tpk, thr, acc, lo, vo);
+          uint32_t off[NB];
+#pragma unroll
+          for (int k = 0; k < NB; ++k) off[k] = offs[h * NB + k];
+          walk_block<FPL, S28, NB>(wls, off, endm, tpk, thr, acc, lo, vo);
         }
         const unsigned nf = __ballot_sync(0xffffffffu, !done && alive());
         if (!done && ((nf & gmask) == 0 || i >= total)) done = true;

@@ -168,3 +168,21 @@ def test_pool_nhwc_to_nhwc_vs_oracle(G, orc, win, stride, pad, with_v, F, flags)
     assert np.array_equal(host(gl), ol.transpose(0, 2, 3, 1))
     if with_v:
         assert np.array_equal(host(gv), ov.transpose(0, 2, 3, 1))
+
+
+@pytest.mark.parametrize("case", [CONV_CASES[i] for i in (0, 2, 4, 6, 13, 16, 17)])
+def test_conv_fire_kstar_truncation(G, orc, case, monkeypatch):
+    """SNN_KSTAR=1: sorted lists end at the first bucket that brings the count to K* (K2b)."""
+    monkeypatch.setenv("SNN_KSTAR", "1")
+    B, C, H, W, pad, F, K, T, theta, p = case
+    rng = np.random.default_rng((abs(hash(case)) + 3) % 2 ** 31)
+    import synth
+    lat_in = synth.random_latencies(rng, (B, C, H, W), T, p)
+    w = exact_weights(rng, (F, C, K, K))
+    w[1, 0, 0, 0] = 0.0
+    lat, v = G.conv_fire(cu(np.ascontiguousarray(lat_in.transpose(0, 2, 3, 1))), cu(w), pad, T, theta, nhwc=True,
+                         in_nhwc=True)
+    G.sync_status()
+    ol, ov = orc.conv_fire(lat_in, w, pad, T, theta)
+    assert np.array_equal(host(lat), ol.transpose(0, 2, 3, 1))
+    assert np.array_equal(host(v), ov.transpose(0, 2, 3, 1))
