@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(512) rf_sort_kernel(const WalkArgs a) {
       unsigned char* rec = a.lists + q * a.rec;
       uint16_t* hdr = reinterpret_cast<uint16_t*>(rec);
       for (int t = gl; t <= a.T; t += LPP) hdr[t] = start[t];
-      const int n4 = ((int(start[a.T]) + kIt - 1) / kIt) * (kIt / 4);  // uint4 per walk iteration
+      const int n4 = (((int(start[a.T]) & ~3) + kIt - 1) / kIt) * (kIt / 4);  // uint4 per walk iteration
       const uint4* src = reinterpret_cast<const uint4*>(list);
       uint4* dst = reinterpret_cast<uint4*>(rec + a.hdr);
       for (int k = gl; k < n4; k += LPP) dst[k] = src[k];
@@ -286,7 +286,7 @@ static int pos_scratch_bytes(int T, int R, WalkArgs* a) {
   int o = 0, c0, c1, c3;
   c0 = o; o += al16(T * 4);                // bucket counters (u32, shared-memory atomics)
   c1 = o; o += al16((T + 1) * 2);          // bucket starts
-  c3 = o; o += al16((R + T + kIt) * 4);    // entries + one pad per bucket + tail
+  c3 = o; o += al16(list_cap(R, T) * 4);  // entries + up to 3 pads per bucket + tail + over-read
   if (a) { a->cnt_off = c0; a->start_off = c1; a->list_off = c3; a->pos_bytes = o; }
   return o;
 }
@@ -328,7 +328,7 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
   a.B = B; a.C = C; a.H = H; a.W = W; a.pad = pad; a.F = F; a.KH = KH; a.KW = KW; a.T = T;
   a.Ho = H + 2 * pad - KH + 1; a.Wo = W + 2 * pad - KW + 1; a.R = C * KH * KW;
   const int R = a.R;
-  if (R + T + kIt >= 65536) return false;  // u16 bucket starts
+  if (list_cap(R, T) >= 65536) return false;  // u16 bucket starts
   struct Cand { int ppw, fpl; };
   auto sort_cost = [&](int ppw, long* tables) {  // (tables bytes, per-warp bytes) of a fused candidate
     WalkArgs t = a;
@@ -419,7 +419,7 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
     a.off_eoff = al16(int(wsb)); a.off_ekk = a.off_eoff; a.off_warps = a.off_eoff;
     pl->smem = a.off_warps + pl->nwarps * a.warp_bytes;
     a.hdr = hdr_bytes;
-    a.rec = hdr_bytes + int(ceil_div(R + T, kIt)) * kIt * 4;
+    a.rec = hdr_bytes + int(ceil_div(list_cap(R, T), kIt)) * kIt * 4;
     pl->sort_nwarps = 16;
     WalkArgs& sa = pl->sa;
     sa = a;

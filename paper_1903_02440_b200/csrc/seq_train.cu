@@ -333,7 +333,7 @@ static bool seq_plan(int C, int H, int W, int pad, int F, int KH, int KW, int T,
   a.B = 1; a.C = C; a.H = H; a.W = W; a.pad = pad; a.F = F; a.KH = KH; a.KW = KW; a.T = T;
   a.Ho = H + 2 * pad - KH + 1; a.Wo = W + 2 * pad - KW + 1; a.R = C * KH * KW;
   const int R = a.R;
-  if (a.Ho < 1 || a.Wo < 1 || R + T + kIt >= 65536 || F > 8192) return false;
+  if (a.Ho < 1 || a.Wo < 1 || list_cap(R, T) >= 65536 || F > 8192) return false;
   const int HoWo = a.Ho * a.Wo;
   if (int64_t(F) * HoWo >= (int64_t(1) << 24)) return false;
   // Latency-bound (one image at a time): when one walk per (position, 32-feature group) fits in a wave
@@ -350,7 +350,7 @@ static bool seq_plan(int C, int H, int W, int pad, int F, int KH, int KW, int T,
     a.row_bytes = fgs * 4;
     const int wsb = al16h((R + 1) * fgs * 4);
     pl->hdr = al16h((T + 1) * 2);
-    pl->rec = pl->hdr + int((R + T + kIt - 1) / kIt) * kIt * 4;
+    pl->rec = pl->hdr + int((list_cap(R, T) + kIt - 1) / kIt) * kIt * 4;
     // per warp: 2 mbarriers + 2 record buffers [header | up to 256 prefetched entries]
     const long left = (220L * 1024 - wsb - al16h(HoWo * 8) - al16h(HoWo * 6)) / nwarps - 16;
     int npre = int(((left / 2 - pl->hdr) / 4) / kIt) * kIt;

@@ -15,6 +15,9 @@ constexpr size_t kListChunkBytes = size_t(512) << 20;  // sorted lists per chunk
                                                         // the lists stream from HBM either way)
 constexpr int kIt = 16;                               // list entries per walk iteration (lists padded to this)
 constexpr int kListSlack = 2048;
+// entries a sorted list can take: R spiking inputs, up to 3 pads per bucket, the tail padding and a
+// partial last block's entry over-read (never gathered)
+__host__ __device__ constexpr int list_cap(int R, int T) { return R + 3 * T + 2 * kIt; }
 #ifndef SNN_SORT_UNROLL
 #define SNN_SORT_UNROLL 4  // receptive-field entries per lane whose latency loads are in flight together
 #endif
@@ -92,11 +95,12 @@ __device__ __forceinline__ uint8_t rf_lat(const WalkArgs& a, const int32_t* eoff
 
 // Counting sort of one position's receptive field by a group of LPP lanes into (start, list).
 // Pass 1 counts the spiking inputs of each bucket with shared-memory atomics (independent, no
-// read-modify-write chains in the lane); the counts are scanned (each bucket padded to an even
-// length with the zero-weight row R, so every bucket end is on a pair boundary) into the bucket
-// starts; pass 2 re-reads the latencies (L1-resident) and takes each entry's slot with an atomic on
-// the bucket's running position.  Entries are weight-row byte offsets e * row_bytes; the tail is
-// padded to a whole walk iteration.  The order inside a bucket is whatever the atomics gave: it does
+// read-modify-write chains in the lane); the counts are scanned (each bucket padded to a multiple of
+// 4 entries with the zero-weight row R, so every bucket starts on a 16-byte boundary) into the header:
+// start[0] = 0 and start[t + 1] = (padded end of bucket t) | (its pad count, 0..3, in the low 2 bits);
+// pass 2 re-reads the latencies (L1-resident) and takes each entry's slot with an atomic on the
+// bucket's running position.  Entries are weight-row byte offsets e * row_bytes; the tail is padded
+// to a whole walk iteration.  The order inside a bucket is whatever the atomics gave: it does
 // not change any result (the sum at a bucket end is exact and order-free).
 template <int LPP, class Lat>
 __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl, uint32_t* cnt, uint16_t* start,
@@ -138,10 +142,11 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl
     }
   }
   int carry = 0;
+  if (gl == 0) start[0] = 0;
   for (int tb = 0; tb < T; tb += LPP) {
     const int t = tb + gl;
     const int tot = t <= tcut ? int(cnt[t]) : 0;
-    const int padded = tot + (tot & 1);  // buckets padded to even length: every bucket end is on a pair boundary
+    const int padded = (tot + 3) & ~3;  // buckets start 16-byte aligned (4 entries): vector entry loads
     int inc = padded;
 #pragma unroll
     for (int o = 1; o < LPP; o <<= 1) {
@@ -150,13 +155,12 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl
     }
     const int st = carry + inc - padded;
     if (t < T) {
-      start[t] = uint16_t(st);
-      cnt[t] = uint32_t(st);                           // pass 2: running slot of the bucket
-      if (tot & 1) list[st + tot] = uint32_t(R) * rb;  // the pad entry: zero-weight row
+      start[t + 1] = uint16_t((st + padded) | (padded - tot));  // padded end | this bucket's pad count
+      cnt[t] = uint32_t(st);                                    // pass 2: running slot of the bucket
+      for (int k = tot; k < padded; ++k) list[st + k] = uint32_t(R) * rb;  // pads: the zero-weight row
     }
     carry += __shfl_sync(0xffffffffu, inc, LPP - 1, LPP);
   }
-  if (gl == 0) start[T] = uint16_t(carry);
   __syncwarp();
   if (pv) {
 #pragma unroll kSortUnroll
@@ -289,166 +293,129 @@ __device__ __forceinline__ void fire_at(uint64_t (&acc)[FPL], int64_t thr, int t
   }
 }
 
-// One NB-input block of the walk (NB = 8 or 16; entries: NB weight-row byte offsets).  The bucket
-// ends inside the block are known to the whole group beforehand (endm: bit m = a bucket ends after pair
-// m, its first-spike index in byte m of tpk).  Each lane sums its features' NB weights exactly; if no
-// unfired feature of the lane then exceeds the threshold, no test inside the block could fire
-// (potentials only grow along the list) and the block is taken whole; otherwise the lane re-adds it
-// pair by pair from the same registers and tests at every bucket end (K3).  Lanes decide
-// independently (no vote): the group's bookkeeping does not depend on the branch taken.  S28: every
-// 8 weights are summed in 32 bits (exact, < 2^31) and added to the 64-bit accumulator (K3b).
+// NB consecutive entries of one bucket: gather each lane's FPL weights per entry (one conflict-free
+// LDS.32/64/128) and add them to the exact accumulators.  S28: every (up to) 8 weights are summed in
+// 32 bits (exact, < 2^31) before the 64-bit add (K3b).  Pad entries (the zero-weight row) add 0.
 template <int FPL, bool S28, int NB>
-__device__ __forceinline__ void walk_block(uint32_t wls, const uint32_t (&off)[NB], unsigned endm, uint64_t tpk,
-                                           int64_t thr, uint64_t (&acc)[FPL], uint32_t& lo, float (&vo)[FPL]) {
+__device__ __forceinline__ void walk_gather_add(uint32_t wls, const uint32_t (&off)[NB], uint64_t (&acc)[FPL]) {
   uint32_t wv[NB][FPL];
 #pragma unroll
   for (int k = 0; k < NB; ++k) wgather_s<FPL>(wls + off[k], wv[k]);
-  uint64_t s[FPL];
-  bool hit = false;
 #pragma unroll
   for (int j = 0; j < FPL; ++j) {
+    uint64_t t = acc[j];
     if constexpr (S28) {
-      uint64_t t = acc[j];
 #pragma unroll
       for (int h = 0; h < NB; h += 8) {
-        const uint32_t b = ((wv[h][j] + wv[h + 1][j]) + (wv[h + 2][j] + wv[h + 3][j])) +
-                           ((wv[h + 4][j] + wv[h + 5][j]) + (wv[h + 6][j] + wv[h + 7][j]));
-        t += b;
+        if constexpr (NB >= 8)
+          t += ((wv[h][j] + wv[h + 1][j]) + (wv[h + 2][j] + wv[h + 3][j])) +
+               ((wv[h + 4][j] + wv[h + 5][j]) + (wv[h + 6][j] + wv[h + 7][j]));
+        else
+          t += (wv[h][j] + wv[h + 1][j]) + (wv[h + 2][j] + wv[h + 3][j]);
       }
-      s[j] = t;
     } else {
-      uint64_t t = acc[j];
 #pragma unroll
       for (int h = 0; h < NB; h += 2) t += uint64_t(wv[h][j]) + wv[h + 1][j];
-      s[j] = t;
     }
-    hit |= int64_t(s[j]) > thr;
+    acc[j] = t;
   }
-  constexpr unsigned kInner = (1u << (NB / 2 - 1)) - 1u;  // bucket ends strictly inside the block
-  if (hit && endm) {
-    if (endm & kInner) {  // pair by pair
-#pragma unroll
-      for (int m = 0; m < NB / 2; ++m) {
-#pragma unroll
-        for (int j = 0; j < FPL; ++j) {
-          if constexpr (S28) acc[j] += uint32_t(wv[2 * m][j] + wv[2 * m + 1][j]);
-          else acc[j] += uint64_t(wv[2 * m][j]) + wv[2 * m + 1][j];
-        }
-        if (endm >> m & 1) fire_at<FPL, S28>(acc, thr, int((tpk >> (8 * m)) & 0xFFu), lo, vo);
-      }
-      return;
-    }
-    // the only bucket end is the block end
-#pragma unroll
-    for (int j = 0; j < FPL; ++j) acc[j] = s[j];
-    fire_at<FPL, S28>(acc, thr, int((tpk >> (8 * (NB / 2 - 1))) & 0xFFu), lo, vo);
-    return;
-  }
-#pragma unroll
-  for (int j = 0; j < FPL; ++j) acc[j] = s[j];
 }
 
-// Walk one position's sorted list (K2/K3) for the FPL features of this lane; group-uniform control,
-// full-warp votes only.  start: T+1 bucket starts; entries come from shared memory (sent for PRE,
-// list otherwise) or, for PRE past the prefetched npre entries, from global memory (ent).  thr is
-// the threshold in the walk's fixed-point units (S28: 2^-28, else 2^-31).
+// Walk one position's sorted list (K2/K3) for the FPL features of this lane, bucket by bucket: a
+// bucket's entries are added in blocks of NB (no test inside a bucket -- the potential is only
+// defined per time step), then every unfired feature is tested once at the bucket end (exact:
+// lat = t, v = P[t]); the group stops when all its features fired.  Control is group-uniform and every
+// vote / shuffle is group-masked, so groups of a warp (PPW > 1) may diverge.  start: the header
+// (start[t + 1] = padded end of bucket t | its pad count); entries come from shared memory (sent for
+// PRE, list otherwise) or, for PRE past the prefetched npre entries, from global memory (ent).  thr
+// is the threshold in the walk's fixed-point units (S28: 2^-28, else 2^-31).
 template <int FPL, int PPW, bool PRE, bool S28 = false>
 __device__ __forceinline__ void walk_list(const WalkArgs& a, const unsigned char* wl, const uint16_t* start,
                                           const unsigned char* sent, const unsigned char* ent, const uint32_t* list,
                                           bool pv, unsigned valid, unsigned gmask, uint32_t& lo, float (&vo)[FPL]) {
+  constexpr int NB = FPL == 4 ? 8 : 16;  // register budget: FPL registers per gathered entry
+  constexpr int LPP = 32 / PPW;
   const int T = a.T;
   const int64_t thr = S28 ? a.thr28 : a.thr;
   uint32_t wls;  // the lane's weight base as a shared-window address, opaque so it stays in a register
   asm volatile("mov.u32 %0, %1;" : "=r"(wls) : "r"(smem_u32(wl)));
-    uint64_t acc[FPL];
-    lo = 0xFFFFFFFFu;  // byte j = lat of feature j (255 = no spike)
+  uint32_t ebase;  // shared-window address of the entries
+  asm volatile("mov.u32 %0, %1;" : "=r"(ebase)
+               : "r"(smem_u32(PRE ? static_cast<const void*>(sent) : static_cast<const void*>(list))));
+  uint64_t acc[FPL];
+  lo = 0xFFFFFFFFu;  // byte j = lat of feature j (255 = no spike)
 #pragma unroll
-    for (int j = 0; j < FPL; ++j) { acc[j] = (valid >> j & 1) ? 0ull : kFiredAcc; vo[j] = 0.0f; }
-    const int total = pv ? int(start[T]) : 0;
-    if (pv && int(start[1]) == 0 && int64_t(0) > thr) {  // empty bucket 0: P[0] = 0 > a negative threshold
+  for (int j = 0; j < FPL; ++j) { acc[j] = (valid >> j & 1) ? 0ull : kFiredAcc; vo[j] = 0.0f; }
+  if (!pv) return;                       // group-uniform
+  auto alive = [&]() {
+    bool al = false;
 #pragma unroll
-      for (int j = 0; j < FPL; ++j)
-        if (int64_t(acc[j]) >= 0) { lo &= ~(0xFFu << (8 * j)); acc[j] = kFiredAcc; }
-    }
-    bool done = !pv || total == 0;  // group-uniform, like every later update of done
-    auto alive = [&]() {  // an unfired valid feature remains in this lane
-      bool al = false;
+    for (int j = 0; j < FPL; ++j) al |= int64_t(acc[j]) >= 0;
+    return al;
+  };
+  if (int(start[1]) == 0 && int64_t(0) > thr) {  // empty bucket 0: P[0] = 0 > a negative threshold
 #pragma unroll
-      for (int j = 0; j < FPL; ++j) al |= int64_t(acc[j]) >= 0;
-      return al;
-    };
-    {
-      const unsigned nd = __ballot_sync(0xffffffffu, alive());
-      if ((nd & gmask) == 0) done = true;  // all features of the group fired (or are padding)
-    }
-    int i = 0, it = 0;
-    // the first non-empty bucket (leading empty ones were handled above): the group's lanes test LPP
-    // buckets per vote (no serial chain of dependent header loads); a uniform trip count keeps every
-    // group's lanes in the full-warp ballots
-    constexpr int LPP = 32 / PPW;
-    const int gl = int(threadIdx.x & 31) % LPP;
-    int t = T;
-    for (int tb = 0; tb < T; tb += LPP) {
-      const int tt = tb + gl;
-      const bool ne = pv && tt < T && int(start[tt + 1]) != 0;
-      const unsigned m = (__ballot_sync(0xffffffffu, ne) & gmask) >> (gmask == 0xffffffffu ? 0 : __ffs(gmask) - 1);
-      if (t == T && m) t = tb + __ffs(m) - 1;
-    }
-    int bend = t < T ? int(start[t + 1]) : 0x7FFFFFFF;  // end of the current non-empty bucket t
-    int guard = (total + kIt - 1) / kIt + 2;  // iterations this group can take (a bug trap, never hit)
-    uint32_t ebase;  // shared-window address of the entries (computed once, kept in a register)
-    asm volatile("mov.u32 %0, %1;" : "=r"(ebase)
-                 : "r"(smem_u32(PRE ? static_cast<const void*>(sent) : static_cast<const void*>(list))));
-    // Every vote below is a full-warp ballot at a converged point; done is group-uniform.
-    while (true) {
-      if (__ballot_sync(0xffffffffu, !done) == 0) break;
-      uint4 cur[4];  // this iteration's 16 entries: shared memory (PRE past npre: global memory)
-      if (PRE && it * kIt >= a.npre) {
-        const uint4* g4 = reinterpret_cast<const uint4*>(ent + it * kIt * 4);
+    for (int j = 0; j < FPL; ++j)
+      if (int64_t(acc[j]) >= 0) { lo &= ~(0xFFu << (8 * j)); acc[j] = kFiredAcc; }
+  }
+  if (__ballot_sync(gmask, alive()) == 0) return;
+  // the first non-empty bucket: the group's lanes test LPP buckets per vote
+  const int gl = int(threadIdx.x & 31) % LPP;
+  int t = T;
+  for (int tb = 0; tb < T && t == T; tb += LPP) {
+    const int tt = tb + gl;
+    const unsigned m = __ballot_sync(gmask, tt < T && int(start[tt + 1]) != 0) & gmask;
+    if (m) t = tb + __ffs(m >> (__ffs(gmask) - 1)) - 1;
+  }
+  int b0 = 0;                            // padded start of bucket t (all earlier buckets are empty)
+  uint32_t wnext = t < T ? start[t + 1] : 0;
+  for (; t < T; ++t) {
+    const uint32_t w1 = wnext;
+    if (t + 1 < T) wnext = start[t + 2];  // the next header word in flight while this bucket is walked
+    const int b1 = int(w1 & ~3u), n = b1 - b0 - int(w1 & 3u);
+    if (n > 0) {
+      // entries [b0, b0 + n): NB per block, the 16-byte entry groups from shared memory below npre,
+      // else from global memory (PRE)
+      auto load_off = [&](int k, auto& off) {
+        constexpr int M = sizeof(off) / sizeof(off[0]);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) cur[u] = __ldg(g4 + u);
-      } else {
-        const uint32_t sa = ebase + uint32_t(it * kIt * 4);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(cur[u].x), "=r"(cur[u].y), "=r"(cur[u].z), "=r"(cur[u].w)
-                       : "r"(sa + 16 * u));
-      }
-      // blocks of NB entries: 16 for FPL <= 2 (one bookkeeping / vote / threshold test per 16 gathers),
-      // 8 for FPL = 4 (register budget: 4 registers per gathered entry)
-      constexpr int NB = FPL == 4 ? 8 : 16;
-      const uint32_t offs[16] = {cur[0].x, cur[0].y, cur[0].z, cur[0].w, cur[1].x, cur[1].y, cur[1].z, cur[1].w,
-                                 cur[2].x, cur[2].y, cur[2].z, cur[2].w, cur[3].x, cur[3].y, cur[3].z, cur[3].w};
-#pragma unroll
-      for (int h = 0; h < 16 / NB; ++h) {
-        if (!done) {
-          // group-uniform: bucket ends inside this block (pair m ends bucket t_m)
-          unsigned endm = 0;
-          uint64_t tpk = 0;
-          i += NB;
-          while (bend <= i) {
-            const int m = ((bend - (i - NB)) >> 1) - 1;
-            endm |= 1u << m;
-            tpk |= uint64_t(t) << (8 * m);
-            ++t;
-            while (t < T && int(start[t + 1]) == bend) ++t;  // empty buckets add nothing
-            bend = t < T ? int(start[t + 1]) : 0x7FFFFFFF;
+        for (int q = 0; q < M / 4; ++q) {
+          const int e4 = k + 4 * q;
+          uint4 c;
+          if (PRE && e4 >= a.npre) {
+            c = __ldg(reinterpret_cast<const uint4*>(ent + e4 * 4));
+          } else {
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "r"(ebase + uint32_t(e4 * 4)));
           }
-          uint32_t off[NB];
-#pragma unroll
-          for (int k = 0; k < NB; ++k) off[k] = offs[h * NB + k];
-          walk_block<FPL, S28, NB>(wls, off, endm, tpk, thr, acc, lo, vo);
+          off[4 * q] = c.x; off[4 * q + 1] = c.y; off[4 * q + 2] = c.z; off[4 * q + 3] = c.w;
         }
-        const unsigned nf = __ballot_sync(0xffffffffu, !done && alive());
-        if (!done && ((nf & gmask) == 0 || i >= total)) done = true;
+      };
+      // the padded bucket [b0, b1) (a multiple of 4 entries; its 0-3 pads gather the zero row) in
+      // blocks of NB, then at most one block of 8 (NB = 16) and one of 4: no per-entry predicates
+      int k = b0;
+      if constexpr (NB == 16) {
+        for (; k + 16 <= b1; k += 16) {
+          uint32_t off[16];
+          load_off(k, off);
+          walk_gather_add<FPL, S28, 16>(wls, off, acc);
+        }
       }
-      ++it;
-      if (!done && --guard < 0) {
-        flag_error(a.err, kErrInternal);
-        done = true;
+      for (; k + 8 <= b1; k += 8) {
+        uint32_t off[8];
+        load_off(k, off);
+        walk_gather_add<FPL, S28, 8>(wls, off, acc);
       }
+      if (k < b1) {
+        uint32_t off[4];
+        load_off(k, off);
+        walk_gather_add<FPL, S28, 4>(wls, off, acc);
+      }
+      fire_at<FPL, S28>(acc, thr, t, lo, vo);  // the exact test at the bucket end
+      if (__ballot_sync(gmask, alive()) == 0) break;
     }
+    b0 = b1;
+  }
 }
 
 }  // namespace snn
