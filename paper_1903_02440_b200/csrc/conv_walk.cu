@@ -176,8 +176,6 @@ __device__ __forceinline__ void walk_positions(const WalkArgs& a, unsigned char*
     const int64_t q = wi * PPW + grp;
     const bool pv = q < a.np;
     const int p = int(a.p0 + q);  // npos < 2^31 (checked by the planner)
-    const int b = pv ? p / HoWo : 0;
-    const int rem = pv ? p - b * HoWo : 0;
     const unsigned char* ent = nullptr;   // PRE: this position's entries in global memory
     const unsigned char* sent = nullptr;  // PRE: its first npre entries in shared memory
     if constexpr (PRE) {
@@ -201,7 +199,11 @@ __device__ __forceinline__ void walk_positions(const WalkArgs& a, unsigned char*
     if (pv) {
       // NHWC: the warp's features of one position are contiguous (one or two lines per store);
       // NCHW: every feature is a separate plane (a line per lane per store)
-      const int64_t o0 = a.nhwc ? int64_t(p) * a.F + fbase : (int64_t(b) * a.F + fbase) * HoWo + rem;
+      int64_t o0 = int64_t(p) * a.F + fbase;
+      if (!a.nhwc) {  // planar: (image, position in the image) -- a division only for this layout
+        const int b = p / HoWo, rem = p - b * HoWo;
+        o0 = (int64_t(b) * a.F + fbase) * HoWo + rem;
+      }
       const int64_t fs = a.nhwc ? 1 : HoWo;
 #pragma unroll
       for (int j = 0; j < FPL; ++j) {

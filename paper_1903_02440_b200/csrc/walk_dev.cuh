@@ -378,17 +378,27 @@ __device__ __forceinline__ void walk_list(const WalkArgs& a, const unsigned char
       // else from global memory (PRE)
       auto load_off = [&](int k, auto& off) {
         constexpr int M = sizeof(off) / sizeof(off[0]);
+        if (!PRE || k + M <= a.npre) {  // the common case: every entry prefetched (no global code)
 #pragma unroll
-        for (int q = 0; q < M / 4; ++q) {
-          const int e4 = k + 4 * q;
-          uint4 c;
-          if (PRE && e4 >= a.npre) {
-            c = __ldg(reinterpret_cast<const uint4*>(ent + e4 * 4));
-          } else {
+          for (int q = 0; q < M / 4; ++q) {
+            uint4 c;
             asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "r"(ebase + uint32_t(e4 * 4)));
+                         : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "r"(ebase + uint32_t((k + 4 * q) * 4)));
+            off[4 * q] = c.x; off[4 * q + 1] = c.y; off[4 * q + 2] = c.z; off[4 * q + 3] = c.w;
           }
-          off[4 * q] = c.x; off[4 * q + 1] = c.y; off[4 * q + 2] = c.z; off[4 * q + 3] = c.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < M / 4; ++q) {
+            const int e4 = k + 4 * q;
+            uint4 c;
+            if (e4 >= a.npre) {
+              c = __ldg(reinterpret_cast<const uint4*>(ent + e4 * 4));
+            } else {
+              asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "r"(ebase + uint32_t(e4 * 4)));
+            }
+            off[4 * q] = c.x; off[4 * q + 1] = c.y; off[4 * q + 2] = c.z; off[4 * q + 3] = c.w;
+          }
         }
       };
       // the padded bucket [b0, b1) (a multiple of 4 entries; its 0-3 pads gather the zero row) in
