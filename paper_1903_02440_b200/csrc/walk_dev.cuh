@@ -220,8 +220,11 @@ __device__ __forceinline__ void rf_sort_warp(const WalkArgs& a, const unsigned c
     const int y0 = y - a.pad, x0 = x - a.pad;
     const uint8_t* in = a.lat_in + int64_t(b) * CHW + (int64_t(y0) * a.W + x0) * (a.in_nhwc ? a.C : 1);
     const bool interior = y0 >= 0 && x0 >= 0 && y0 + a.KH <= a.H && x0 + a.KW <= a.W;
-    rf_sort_group<LPP>(a, pv, gl, cnt, start, list,
-                       [&](int e) { return int(rf_lat(a, eoff, ekk, in, interior, y0, x0, e)); });
+    if (PPW == 1 && interior)  // no bounds tests: the loads of an unrolled group issue back to back
+      rf_sort_group<LPP>(a, pv, gl, cnt, start, list, [&](int e) { return int(__ldg(in + eoff[e])); });
+    else  // (PPW > 1 only reaches here for a warp straddling a row end: one lambda keeps its code small)
+      rf_sort_group<LPP>(a, pv, gl, cnt, start, list,
+                         [&](int e) { return int(rf_lat(a, eoff, ekk, in, interior, y0, x0, e)); });
   }
 }
 

@@ -18,7 +18,7 @@ from typing import Optional, Tuple
 import torch
 
 NO_SPIKE = 255
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsnn.so")
+_LIB_PATH = os.environ.get("SNN_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsnn.so")  # SNN_LIB: A/B experiments with another build
 _lib = None
 _lock = threading.Lock()
 
