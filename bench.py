@@ -643,11 +643,35 @@ def run_ours(args, rank, world, local):
     print(json.dumps(line), flush=True)
 
 
+def spawn_cmd(argv, gpus: int, port: int):
+    """The torchrun command that runs this bench with one process per GPU (used when ``--gpus N`` > 1 is
+    given without a torchrun environment)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # --gpus N without torchrun: start the N ranks ourselves (one process per GPU), same arguments
+        if args.impl == "ours":
+            import torch
+            have = torch.cuda.device_count()
+            if have < args.gpus:
+                raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible")
+        sys.exit(subprocess.call(spawn_cmd(sys.argv[1:], args.gpus, _free_port())))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank)
         return

@@ -39,7 +39,7 @@ int k_winners_launch(const uint8_t* lat, const float* v, int B, int F, int H, in
 int stdp_launch(float* w, int F, int C, int KH, int KW, const uint8_t* lat_in, int H, int W, int pad,
                 const uint8_t* lat_out, int Ho, int Wo, const int32_t* winners, const int32_t* count, int k,
                 float a_plus, float a_minus, float lb, float ub, int stabilizer, const float* reward, int f0,
-                cudaStream_t s);
+                int sharded, cudaStream_t s);
 int position_keys_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, int f0, int64_t* keys,
                          cudaStream_t s);
 size_t k_winners_keys_workspace(int B, int H, int W);
@@ -92,11 +92,14 @@ bool pdl_enabled() {
 }
 
 int num_sms() {
-  static int n = 0;
+  static std::atomic<int> cache[64];  // per device ordinal (0 = not looked up yet)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  int n = cache[dev].load(std::memory_order_relaxed);
   if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
   return n;
 }
@@ -144,9 +147,11 @@ int snn_sync_status(snn_stream_t s) {
   cudaError_t e = cudaStreamSynchronize(S(s));
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_sync_status: %s", cudaGetErrorString(e));
   int word = 0;
-  int rc = read_clear_error_word(&word);
+  int rc = read_clear_error_word(S(s), &word);
   if (rc) return rc;
   if (word & kErrInternal) return set_error(SNN_ECUDA, "internal error: a kernel consistency trap fired");
+  if (word & kErrWinner)
+    return set_error(SNN_EINVAL, "snn_stdp_update: a winner lies outside the map or the layer's features (skipped)");
   if (word & kErrInexact)
     return set_error(SNN_EINEXACT, "a weight is outside the exact domain {w : w*2^31 integral, 0 <= w <= 1}");
   return SNN_OK;
@@ -355,10 +360,10 @@ int snn_k_winners(const uint8_t* lat, const float* v, int B, int F, int H, int W
   return k_winners_launch(lat, v, B, F, H, W, k, r, winners, count, ws, ws_bytes, S(s));
 }
 
-int snn_stdp_update_shard(float* w, int F_local, int f_offset, int C, int KH, int KW, const uint8_t* lat_in, int H,
-                          int W, int pad, const uint8_t* lat_out, int Ho, int Wo, const int32_t* winners,
-                          const int32_t* count, int k, float a_plus, float a_minus, float lb, float ub, int stabilizer,
-                          const float* reward, snn_stream_t s) {
+static int stdp_update_impl(float* w, int F_local, int f_offset, int C, int KH, int KW, const uint8_t* lat_in, int H,
+                            int W, int pad, const uint8_t* lat_out, int Ho, int Wo, const int32_t* winners,
+                            const int32_t* count, int k, float a_plus, float a_minus, float lb, float ub,
+                            int stabilizer, const float* reward, int sharded, snn_stream_t s) {
   const int F = F_local;
   REQUIRE(stabilizer >= 0 && stabilizer <= 2, SNN_EINVAL, "snn_stdp_update: stabilizer=%d not in {0, 1, 2}", stabilizer);
   REQUIRE(lb < ub, SNN_EINVAL, "snn_stdp_update: LB >= UB");
@@ -372,15 +377,23 @@ int snn_stdp_update_shard(float* w, int F_local, int f_offset, int C, int KH, in
   if (k == 0) return SNN_OK;
   REQUIRE(w && lat_in && lat_out && winners && count, SNN_EINVAL, "snn_stdp_update: NULL tensor");
   return stdp_launch(w, F, C, KH, KW, lat_in, H, W, pad, lat_out, Ho, Wo, winners, count, k, a_plus, a_minus, lb, ub,
-                     stabilizer, reward, f_offset, S(s));
+                     stabilizer, reward, f_offset, sharded, S(s));
+}
+
+int snn_stdp_update_shard(float* w, int F_local, int f_offset, int C, int KH, int KW, const uint8_t* lat_in, int H,
+                          int W, int pad, const uint8_t* lat_out, int Ho, int Wo, const int32_t* winners,
+                          const int32_t* count, int k, float a_plus, float a_minus, float lb, float ub, int stabilizer,
+                          const float* reward, snn_stream_t s) {
+  return stdp_update_impl(w, F_local, f_offset, C, KH, KW, lat_in, H, W, pad, lat_out, Ho, Wo, winners, count, k,
+                          a_plus, a_minus, lb, ub, stabilizer, reward, 1, s);
 }
 
 int snn_stdp_update(float* w, int F, int C, int KH, int KW, const uint8_t* lat_in, int H, int W, int pad,
                     const uint8_t* lat_out, int Ho, int Wo, const int32_t* winners, const int32_t* count, int k,
                     float a_plus, float a_minus, float lb, float ub, int stabilizer, const float* reward,
                     snn_stream_t s) {
-  return snn_stdp_update_shard(w, F, 0, C, KH, KW, lat_in, H, W, pad, lat_out, Ho, Wo, winners, count, k, a_plus,
-                               a_minus, lb, ub, stabilizer, reward, s);
+  return stdp_update_impl(w, F, 0, C, KH, KW, lat_in, H, W, pad, lat_out, Ho, Wo, winners, count, k, a_plus,
+                          a_minus, lb, ub, stabilizer, reward, 0, s);
 }
 
 int snn_position_keys(const uint8_t* lat, const float* v, int B, int F, int H, int W, int f_offset, int64_t* keys,

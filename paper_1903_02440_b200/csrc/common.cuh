@@ -13,14 +13,15 @@ constexpr uint8_t kNoSpike = SNN_NO_SPIKE;
 // read and cleared by snn_sync_status() through read_clear_error_word().
 constexpr int kErrInexact = 1;
 constexpr int kErrInternal = 2;  // a kernel's internal consistency trap fired (a library bug)
-int read_clear_error_word(int* word);
-int* error_word_ptr();  // device address of the error word, for kernels of other translation units
+constexpr int kErrWinner = 4;    // snn_stdp_update: a winner outside the map / the layer (skipped)
+int read_clear_error_word(cudaStream_t s, int* word);
+int* error_word_ptr(cudaStream_t s);  // device address of the stream's error word (current device)
 __device__ __forceinline__ void flag_error(int* err, int bit) { atomicOr(err, bit); }
 
 // Host-side error reporting (thread-local message), defined in api.cu.
 int set_error(int code, const char* fmt, ...);
 int check_launch(const char* what);
-int num_sms();  // multiprocessor count of the current device (cached)
+int num_sms();  // multiprocessor count of the current device (cached per device)
 void note_launch(int n = 1);  // diagnostic kernel-launch counter (snn_launch_count)
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -20,22 +20,51 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
 
 namespace snn {
 
-__device__ int g_error_word = 0;
+// Device error words, one per stream (snn_sync_status(stream) reads and clears its stream's word):
+// streams are given slots of this per-device array in order of first use; past kErrSlots streams of
+// one device, slots are shared (documented in snn.h).  The array is a module global, so every device
+// has its own copy; its address is looked up per device.
+constexpr int kErrSlots = 64;
+constexpr int kMaxDevices = 64;
+__device__ int g_error_words[kErrSlots];
 
-int* error_word_ptr() {
-  static int* p = nullptr;
-  if (!p) cudaGetSymbolAddress(reinterpret_cast<void**>(&p), g_error_word);
-  return p;
+namespace {
+std::mutex g_err_mu;
+std::unordered_map<uint64_t, int> g_err_slot;  // (device << 48) ^ stream -> slot
+int g_err_next[kMaxDevices];
+int* g_err_base[kMaxDevices];
+}  // namespace
+
+int* error_word_ptr(cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  if (!g_err_base[dev]) cudaGetSymbolAddress(reinterpret_cast<void**>(&g_err_base[dev]), g_error_words);
+  const uint64_t key = (uint64_t(dev) << 48) ^ uint64_t(reinterpret_cast<uintptr_t>(s));
+  auto it = g_err_slot.find(key);
+  int slot;
+  if (it != g_err_slot.end()) {
+    slot = it->second;
+  } else {
+    slot = g_err_next[dev]++ % kErrSlots;
+    g_err_slot.emplace(key, slot);
+  }
+  return g_err_base[dev] + slot;
 }
 
-int read_clear_error_word(int* word) {
-  int zero = 0;
-  cudaError_t e = cudaMemcpyFromSymbol(word, g_error_word, sizeof(int));
-  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_error_word, &zero, sizeof(int));
+int read_clear_error_word(cudaStream_t s, int* word) {
+  int* p = error_word_ptr(s);
+  cudaError_t e = cudaMemcpyAsync(word, p, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p, 0, sizeof(int), s);
   return e == cudaSuccess ? SNN_OK : set_error(SNN_ECUDA, "snn_sync_status: %s", cudaGetErrorString(e));
 }
 
@@ -63,7 +92,7 @@ static inline int align16(int x) { return (x + 15) & ~15; }
 // w [F][R] fp32 -> wq [g][R+1][FGS] uint32 fixed point (w * 2^31).  Flags weights whose value is
 // not an integer multiple of 2^-31 in [0, 1] (outside the exact domain, N1).
 __global__ void weight_prep_kernel(const float* __restrict__ w, int F, int R, int FGS, int n_groups,
-                                   uint32_t* __restrict__ wq, int nhwc_C, int KK) {
+                                   uint32_t* __restrict__ wq, int nhwc_C, int KK, int* err) {
   pdl_begin();
   int64_t total = int64_t(n_groups) * (R + 1) * FGS;
   int bad = 0;
@@ -84,7 +113,7 @@ __global__ void weight_prep_kernel(const float* __restrict__ w, int F, int R, in
     }
     wq[i] = u;
   }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&g_error_word, kErrInexact);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, kErrInexact);
 }
 
 // ------------------------------------------------------------------------- fused sort + walk
@@ -447,7 +476,7 @@ int weight_prep_launch(const float* w, int F, int R, int FGS, int n_groups, uint
   int blocks = int(ceil_div(total, 256));
   if (blocks > 2048) blocks = 2048;
   if (blocks < 1) blocks = 1;
-  launch_k(weight_prep_kernel, dim3(blocks), dim3(256), 0, s, w, F, R, FGS, n_groups, wq, nhwc_C, KK);
+  launch_k(weight_prep_kernel, dim3(blocks), dim3(256), 0, s, w, F, R, FGS, n_groups, wq, nhwc_C, KK, error_word_ptr(s));
   note_launch();
   return check_launch("snn_conv_fire(weight prep)");
 }
@@ -510,7 +539,7 @@ int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
     int64_t total = int64_t(pl.n_groups) * (a.R + 1) * pl.FGS;
     int blocks = int(ceil_div(total, 256));
     if (blocks > 2048) blocks = 2048;
-    weight_prep_kernel<<<blocks, 256, 0, s>>>(w, F, a.R, pl.FGS, pl.n_groups, a.wq, 0, 1);
+    weight_prep_kernel<<<blocks, 256, 0, s>>>(w, F, a.R, pl.FGS, pl.n_groups, a.wq, 0, 1, error_word_ptr(s));
     note_launch();
   }
   if (pl.dense) {

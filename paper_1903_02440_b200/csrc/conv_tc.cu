@@ -462,7 +462,7 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
     const int64_t total = int64_t(p.nch) * p.Fc * (p.Kp / 16);
     int64_t blocks = ceil_div(total, 256);
     if (blocks > int64_t(num_sms()) * 8) blocks = int64_t(num_sms()) * 8;
-    launch_k(tc_prep_b16_kernel, dim3(int(blocks)), dim3(256), 0, s, w, F, R, KH * KW, p, bq, error_word_ptr());
+    launch_k(tc_prep_b16_kernel, dim3(int(blocks)), dim3(256), 0, s, w, F, R, KH * KW, p, bq, error_word_ptr(s));
     note_launch();
   }
   if (aq_pre) {  // prepared by snn_conv_inf_prepare

@@ -436,7 +436,7 @@ int conv_tct_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, 
     int64_t blocks = ceil_div(total, 256);
     if (blocks > int64_t(num_sms()) * 8) blocks = int64_t(num_sms()) * 8;
     t2_prep_b_kernel<<<int(blocks), 256, 0, s>>>(w, F, p.R, p.Kp, p.N, p.Fc, p.nch, const_cast<uint8_t*>(a.bq),
-                                                 error_word_ptr());
+                                                 error_word_ptr(s));
     note_launch();
   }
   // TMEM (512 columns per SM) and shared memory both cap the resident CTAs: request enough shared

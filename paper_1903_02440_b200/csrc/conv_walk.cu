@@ -527,7 +527,7 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   const size_t need = wq_bytes + 256 + (pl.pre ? size_t(pl.chunk) * a.rec + kListSlack : 0);
   if (ws_bytes < need) return set_error(SNN_EWORKSPACE, "snn_conv_fire: workspace %zu < %zu", ws_bytes, need);
   a.lat_in = lat_in; a.lat_out = lat_out; a.v_out = v_out; a.nhwc = nhwc; a.in_nhwc = in_nhwc;
-  a.err = error_word_ptr();
+  a.err = error_word_ptr(s);
   a.wq = reinterpret_cast<const uint32_t*>(ws);
   int* kstar = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(ws) + wq_bytes);
   a.lists = reinterpret_cast<unsigned char*>(ws) + wq_bytes + 256;

@@ -329,14 +329,18 @@ int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, 
   int64_t blocks = ceil_div(total, 256);
   if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
   const bool small = total < (int64_t(1) << 32) && int64_t(B) * F * H * W < (int64_t(1) << 32);
-  if (small && v_out && PH == 2 && PW == 2 && SH == 2 && SW == 2 && DH == 0 && DW == 0 && W % 4 == 0 &&
+  // the vector paths load 4-byte latency words / 16-byte potential vectors and store 2-byte / 8-byte
+  // pairs: only for pointers with that alignment (a tensor view with an offset takes the scalar path)
+  const auto al = [](const void* p, uintptr_t m) { return (reinterpret_cast<uintptr_t>(p) & (m - 1)) == 0; };
+  const bool vec_ok = al(lat, 4) && al(lat_out, 2) && (!v_out || (al(v, 16) && al(v_out, 8)));
+  if (small && vec_ok && v_out && PH == 2 && PW == 2 && SH == 2 && SW == 2 && DH == 0 && DW == 0 && W % 4 == 0 &&
       H % 2 == 0 && Wo % 2 == 0) {
     const uint32_t pairs = uint32_t(total / 2);
     int64_t pb = ceil_div(pairs, 256);
     if (pb > int64_t(num_sms()) * 16) pb = int64_t(num_sms()) * 16;
     launch_k(pool2x2_v_kernel, dim3(int(pb)), dim3(256), 0, s, lat, v, pairs, H, W, Ho, Wo, (flags & SNN_POOL_VFINAL) ? 1 : 0, lat_out,
                                               v_out);
-  } else if (small && !v_out && PH == 2 && PW == 2 && SH == 2 && SW == 2 && DH == 0 && DW == 0 && W % 4 == 0 &&
+  } else if (small && vec_ok && !v_out && PH == 2 && PW == 2 && SH == 2 && SW == 2 && DH == 0 && DW == 0 && W % 4 == 0 &&
              Wo * 2 == W) {
     const uint32_t words = uint32_t(int64_t(B) * F * Ho * (W / 4));
     int64_t wb = ceil_div(words, 256);

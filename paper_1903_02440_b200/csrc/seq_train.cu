@@ -418,7 +418,7 @@ int seq_train_launch(const uint8_t* lat_all, int N, int C, int H, int W, int pad
   SeqArgs s;
   s.wa = pl.a;
   s.wa.lat_in = lat_all;
-  s.wa.err = error_word_ptr();
+  s.wa.err = error_word_ptr(st);
   const double tt = floor(double(theta) * 2147483648.0);
   s.wa.thr = tt >= 9.0e18 ? INT64_MAX : (tt < -1.0 ? -1 : int64_t(tt));
   s.lat_all = lat_all; s.N = N; s.w = w; s.k = k; s.r = r;

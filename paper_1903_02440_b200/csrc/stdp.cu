@@ -18,10 +18,19 @@ __global__ void __launch_bounds__(256) stdp_kernel(float* __restrict__ w, int C,
                                                    const int32_t* __restrict__ winners,
                                                    const int32_t* __restrict__ count, float a_plus, float a_minus,
                                                    float lb, float ub, int stabilizer,
-                                                   const float* __restrict__ reward, int f0, int Floc) {
+                                                   const float* __restrict__ reward, int f0, int Floc, int sharded,
+                                                   int* err) {
   pdl_begin();
   const int i = blockIdx.x;  // winner slot; blockIdx.y = slice of its synapses (gridDim.y slices)
   if (i >= count[0]) return;
+  {  // a winner outside the map (or, unsharded, outside the layer's features) is skipped and reported
+    const int wf = winners[i * 3], wy = winners[i * 3 + 1], wx = winners[i * 3 + 2];
+    const bool bad = wf < 0 || wy < 0 || wy >= Ho || wx < 0 || wx >= Wo || (!sharded && wf >= Floc);
+    if (bad) {
+      if (blockIdx.y == 0 && threadIdx.x == 0) flag_error(err, kErrWinner);
+      return;
+    }
+  }
   if (winners[i * 3] < f0 || winners[i * 3] >= f0 + Floc) return;  // another rank's feature (f4 sharding)
   float rw = reward ? reward[0] : 1.0f;
   if (rw == 0.0f) return;  // silent sample: no plasticity
@@ -51,7 +60,7 @@ __global__ void __launch_bounds__(256) stdp_kernel(float* __restrict__ w, int C,
 int stdp_launch(float* w, int F, int C, int KH, int KW, const uint8_t* lat_in, int H, int W, int pad,
                 const uint8_t* lat_out, int Ho, int Wo, const int32_t* winners, const int32_t* count, int k,
                 float a_plus, float a_minus, float lb, float ub, int stabilizer, const float* reward,
-                int f0, cudaStream_t s) {
+                int f0, int sharded, cudaStream_t s) {
   if (k == 0) return SNN_OK;
   // one CTA per (winner, slice of 256 synapses): a large kernel (C4: 5,780 synapses) is updated by many
   // SMs at once instead of one CTA looping over it
@@ -59,7 +68,7 @@ int stdp_launch(float* w, int F, int C, int KH, int KW, const uint8_t* lat_in, i
   int slices = int(ceil_div(R, 256));
   if (slices > 64) slices = 64;
   launch_k(stdp_kernel, dim3(dim3(k, slices)), dim3(256), 0, s, w, C, KH, KW, lat_in, H, W, pad, lat_out, Ho, Wo, winners, count, a_plus, a_minus,
-                                lb, ub, stabilizer, reward, f0, F);
+                                lb, ub, stabilizer, reward, f0, F, sharded, error_word_ptr(s));
   note_launch();
   return check_launch("snn_stdp_update");
 }

@@ -74,9 +74,12 @@ def gather_decisions(decision: torch.Tensor) -> torch.Tensor:
     """All-gather of the per-image results of every rank (equal batch per rank), rank order."""
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return decision
-    out = torch.empty((dist.get_world_size(),) + tuple(decision.shape), dtype=decision.dtype,
-                      device=decision.device)
-    dist.all_gather_into_tensor(out, decision.contiguous())
+    world = dist.get_world_size()
+    out = torch.empty((world,) + tuple(decision.shape), dtype=decision.dtype, device=decision.device)
+    if dist.get_backend() == "nccl":
+        dist.all_gather_into_tensor(out, decision.contiguous())
+    else:  # gloo has no all_gather_into_tensor
+        dist.all_gather(list(out.unbind(0)), decision.contiguous())
     return out.reshape((-1,) + tuple(decision.shape[1:]))
 
 
