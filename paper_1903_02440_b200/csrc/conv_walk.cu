@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(512) rf_sort_kernel(const WalkArgs a) {
       unsigned char* rec = a.lists + q * a.rec;
       uint16_t* hdr = reinterpret_cast<uint16_t*>(rec);
       for (int t = gl; t <= a.T; t += LPP) hdr[t] = start[t];
-      const int n4 = (((int(start[a.T]) & ~3) + kIt - 1) / kIt) * (kIt / 4);  // uint4 per walk iteration
+      const int n4 = (((int(start[a.T]) & -a.pad_unit) + kIt - 1) / kIt) * (kIt / 4);  // uint4 per walk iteration
       const uint4* src = reinterpret_cast<const uint4*>(list);
       uint4* dst = reinterpret_cast<uint4*>(rec + a.hdr);
       for (int k = gl; k < n4; k += LPP) dst[k] = src[k];
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(512) rf_sort_kernel(const WalkArgs a) {
 
 // The per-position loop of conv_walk_kernel once the CTA's weight slice is staged (S28: the slice is
 // in units of 2^-28, see walk_block).
-template <int FPL, int PPW, bool PRE, bool S28>
+template <int FPL, int PPW, bool PRE, bool S28, bool BW>
 __device__ __forceinline__ void walk_positions(const WalkArgs& a, unsigned char* smem) {
   constexpr int LPP = 32 / PPW;
   constexpr int FGS = LPP * FPL;
@@ -195,7 +195,7 @@ __device__ __forceinline__ void walk_positions(const WalkArgs& a, unsigned char*
 
     uint32_t lo;
     float vo[FPL];
-    walk_list<FPL, PPW, PRE, S28>(a, wl, start, sent, ent, list, pv, valid, gmask, lo, vo);
+    walk_list<FPL, PPW, PRE, S28, BW>(a, wl, start, sent, ent, list, pv, valid, gmask, lo, vo);
     if (pv) {
       // NHWC: the warp's features of one position are contiguous (one or two lines per store);
       // NCHW: every feature is a separate plane (a line per lane per store)
@@ -217,7 +217,7 @@ __device__ __forceinline__ void walk_positions(const WalkArgs& a, unsigned char*
   }
 }
 
-template <int FPL, int PPW, bool PRE, bool WCONV = false>
+template <int FPL, int PPW, bool PRE, bool WCONV = false, bool BW = true>
 __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(const WalkArgs a) {
   pdl_wait();
   constexpr int LPP = 32 / PPW;
@@ -268,9 +268,9 @@ __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(
       w4[i] = v;
     }
     __syncthreads();
-    walk_positions<FPL, PPW, PRE, true>(a, smem);
+    walk_positions<FPL, PPW, PRE, true, BW>(a, smem);
   } else {
-    walk_positions<FPL, PPW, PRE, false>(a, smem);
+    walk_positions<FPL, PPW, PRE, false, BW>(a, smem);
   }
 }
 
@@ -323,6 +323,14 @@ static int sort_ppw_for(int R) {
   return R <= 512 ? 4 : 1;
 }
 
+// Bucket-by-bucket walk (pad unit 4) when the buckets hold enough entries to amortise a test and a
+// vote per bucket (R >= 8 T: C2's second layer, C3, C5), else K3 blocks across buckets (pad unit 2:
+// C1, C2's first layer, C4's first layer).  SNN_WALK_BW=0/1 forces one (experiments).
+static bool walk_bucketwise(int R, int T) {
+  if (const char* e = getenv("SNN_WALK_BW")) return e[0] == '1';
+  return R >= 8 * T;
+}
+
 static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, WalkPlan* pl) {
   WalkArgs& a = pl->a;
   a = WalkArgs{};
@@ -331,6 +339,7 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
   a.Ho = H + 2 * pad - KH + 1; a.Wo = W + 2 * pad - KW + 1; a.R = C * KH * KW;
   const int R = a.R;
   if (list_cap(R, T) >= 65536) return false;  // u16 bucket starts
+  a.pad_unit = walk_bucketwise(R, T) ? 4 : 2;
   struct Cand { int ppw, fpl; };
   auto sort_cost = [&](int ppw, long* tables) {  // (tables bytes, per-warp bytes) of a fused candidate
     WalkArgs t = a;
@@ -452,7 +461,7 @@ size_t conv_walk_workspace(int B, int C, int H, int W, int pad, int F, int KH, i
 
 template <int FPL, int PPW, bool PRE, bool WCONV = false>
 static int walk_go(const WalkPlan& pl, const WalkArgs& a, cudaStream_t s) {
-  auto k = conv_walk_kernel<FPL, PPW, PRE, WCONV>;
+  auto k = a.pad_unit == 4 ? conv_walk_kernel<FPL, PPW, PRE, WCONV, true> : conv_walk_kernel<FPL, PPW, PRE, WCONV, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_conv_fire(walk): %s", cudaGetErrorString(e));
   int occ = 1;
@@ -494,6 +503,7 @@ int rf_sort_lists_launch(const uint8_t* lat_in, int B, int C, int H, int W, int 
   sa.B = B; sa.C = C; sa.H = H; sa.W = W; sa.pad = pad; sa.KH = KH; sa.KW = KW; sa.T = T;
   sa.Ho = H + 2 * pad - KH + 1; sa.Wo = W + 2 * pad - KW + 1; sa.R = C * KH * KW;
   sa.row_bytes = row_bytes; sa.lists = lists; sa.rec = rec; sa.hdr = hdr;
+  sa.pad_unit = 4;  // seq_train walks bucket by bucket
   sa.lat_in = lat_in; sa.p0 = 0; sa.np = int64_t(B) * sa.Ho * sa.Wo;
   const int R = sa.R;
   pl.sort_ppw = sort_ppw_for(R);

@@ -334,6 +334,7 @@ static bool seq_plan(int C, int H, int W, int pad, int F, int KH, int KW, int T,
   a.Ho = H + 2 * pad - KH + 1; a.Wo = W + 2 * pad - KW + 1; a.R = C * KH * KW;
   const int R = a.R;
   if (a.Ho < 1 || a.Wo < 1 || list_cap(R, T) >= 65536 || F > 8192) return false;
+  a.pad_unit = 4;  // bucket-by-bucket walk (walk_list default)
   const int HoWo = a.Ho * a.Wo;
   if (int64_t(F) * HoWo >= (int64_t(1) << 24)) return false;
   // Latency-bound (one image at a time): when one walk per (position, 32-feature group) fits in a wave

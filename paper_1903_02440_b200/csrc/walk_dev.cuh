@@ -52,6 +52,7 @@ struct WalkArgs {
   int nhwc;           // output layout: 0 = [B, F, Ho, Wo], 1 = [B, Ho, Wo, F] (SNN_CONV_OUT_NHWC)
   const int* kstar;   // nullable: K* (kstar_kernel) -- any K* spiking inputs fire every feature, so a
                       // sorted list can end with the first bucket that brings its count to K* (K2b)
+  int pad_unit;       // sorted buckets padded to a multiple of this many entries: 4 (bucket walk) or 2 (K3 blocks)
   int in_nhwc;        // input layout [B, H, W, C] (SNN_CONV_IN_NHWC): receptive-field entries are then
                       // ordered (ky, kx, c) -- e = (ky KW + kx) C + c -- and so are the weight rows
 };
@@ -146,7 +147,7 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl
   for (int tb = 0; tb < T; tb += LPP) {
     const int t = tb + gl;
     const int tot = t <= tcut ? int(cnt[t]) : 0;
-    const int padded = (tot + 3) & ~3;  // buckets start 16-byte aligned (4 entries): vector entry loads
+    const int padded = (tot + a.pad_unit - 1) & -a.pad_unit;  // 4: buckets 16-byte aligned (bucket walk); 2: pairs
     int inc = padded;
 #pragma unroll
     for (int o = 1; o < LPP; o <<= 1) {
@@ -324,6 +325,170 @@ __device__ __forceinline__ void walk_gather_add(uint32_t wls, const uint32_t (&o
   }
 }
 
+// ---------------------------------------------------------------- walk in blocks across buckets (K3)
+// For layers whose buckets are small (a few entries: R / T below ~8, e.g. C1, C4's first layer) the
+// bucket-by-bucket walk below would pay its per-bucket test, vote and padding for 2-3 entries; this
+// walk streams the list in fixed blocks instead.  The bucket ends inside a block are known to the
+// whole group beforehand (endm: bit m = a bucket ends after pair m, its index in byte m of tpk); each
+// lane sums its features' weights for the block exactly; if no unfired feature then exceeds the
+// threshold no test inside the block could fire (potentials only grow along the list) and the block is
+// taken whole; otherwise the lane re-adds it pair by pair and tests at every bucket end (K3).
+// Sorted with pad unit 2: header word = padded end | pad count (bit 0).
+template <int FPL, bool S28, int NB>
+__device__ __forceinline__ void walk_block_k3(uint32_t wls, const uint32_t (&off)[NB], unsigned endm, uint64_t tpk,
+                                           int64_t thr, uint64_t (&acc)[FPL], uint32_t& lo, float (&vo)[FPL]) {
+  uint32_t wv[NB][FPL];
+#pragma unroll
+  for (int k = 0; k < NB; ++k) wgather_s<FPL>(wls + off[k], wv[k]);
+  uint64_t s[FPL];
+  bool hit = false;
+#pragma unroll
+  for (int j = 0; j < FPL; ++j) {
+    if constexpr (S28) {
+      uint64_t t = acc[j];
+#pragma unroll
+      for (int h = 0; h < NB; h += 8) {
+        const uint32_t b = ((wv[h][j] + wv[h + 1][j]) + (wv[h + 2][j] + wv[h + 3][j])) +
+                           ((wv[h + 4][j] + wv[h + 5][j]) + (wv[h + 6][j] + wv[h + 7][j]));
+        t += b;
+      }
+      s[j] = t;
+    } else {
+      uint64_t t = acc[j];
+#pragma unroll
+      for (int h = 0; h < NB; h += 2) t += uint64_t(wv[h][j]) + wv[h + 1][j];
+      s[j] = t;
+    }
+    hit |= int64_t(s[j]) > thr;
+  }
+  constexpr unsigned kInner = (1u << (NB / 2 - 1)) - 1u;  // bucket ends strictly inside the block
+  if (hit && endm) {
+    if (endm & kInner) {  // pair by pair
+#pragma unroll
+      for (int m = 0; m < NB / 2; ++m) {
+#pragma unroll
+        for (int j = 0; j < FPL; ++j) {
+          if constexpr (S28) acc[j] += uint32_t(wv[2 * m][j] + wv[2 * m + 1][j]);
+          else acc[j] += uint64_t(wv[2 * m][j]) + wv[2 * m + 1][j];
+        }
+        if (endm >> m & 1) fire_at<FPL, S28>(acc, thr, int((tpk >> (8 * m)) & 0xFFu), lo, vo);
+      }
+      return;
+    }
+    // the only bucket end is the block end
+#pragma unroll
+    for (int j = 0; j < FPL; ++j) acc[j] = s[j];
+    fire_at<FPL, S28>(acc, thr, int((tpk >> (8 * (NB / 2 - 1))) & 0xFFu), lo, vo);
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < FPL; ++j) acc[j] = s[j];
+}
+
+// Walk one position's sorted list (K2/K3) for the FPL features of this lane; group-uniform control,
+// full-warp votes only.  start: T+1 bucket starts; entries come from shared memory (sent for PRE,
+// list otherwise) or, for PRE past the prefetched npre entries, from global memory (ent).  thr is
+// the threshold in the walk's fixed-point units (S28: 2^-28, else 2^-31).
+template <int FPL, int PPW, bool PRE, bool S28>
+__device__ __forceinline__ void walk_list_blocks(const WalkArgs& a, const unsigned char* wl, const uint16_t* start,
+                                          const unsigned char* sent, const unsigned char* ent, const uint32_t* list,
+                                          bool pv, unsigned valid, unsigned gmask, uint32_t& lo, float (&vo)[FPL]) {
+  const int T = a.T;
+  const int64_t thr = S28 ? a.thr28 : a.thr;
+  uint32_t wls;  // the lane's weight base as a shared-window address, opaque so it stays in a register
+  asm volatile("mov.u32 %0, %1;" : "=r"(wls) : "r"(smem_u32(wl)));
+    uint64_t acc[FPL];
+    lo = 0xFFFFFFFFu;  // byte j = lat of feature j (255 = no spike)
+#pragma unroll
+    for (int j = 0; j < FPL; ++j) { acc[j] = (valid >> j & 1) ? 0ull : kFiredAcc; vo[j] = 0.0f; }
+    const int total = pv ? int(start[T] & ~1u) : 0;  // padded end of the list
+    if (pv && int(start[1]) == 0 && int64_t(0) > thr) {  // empty bucket 0: P[0] = 0 > a negative threshold
+#pragma unroll
+      for (int j = 0; j < FPL; ++j)
+        if (int64_t(acc[j]) >= 0) { lo &= ~(0xFFu << (8 * j)); acc[j] = kFiredAcc; }
+    }
+    bool done = !pv || total == 0;  // group-uniform, like every later update of done
+    auto alive = [&]() {  // an unfired valid feature remains in this lane
+      bool al = false;
+#pragma unroll
+      for (int j = 0; j < FPL; ++j) al |= int64_t(acc[j]) >= 0;
+      return al;
+    };
+    {
+      const unsigned nd = __ballot_sync(0xffffffffu, alive());
+      if ((nd & gmask) == 0) done = true;  // all features of the group fired (or are padding)
+    }
+    int i = 0, it = 0;
+    // the first non-empty bucket (leading empty ones were handled above): the group's lanes test LPP
+    // buckets per vote (no serial chain of dependent header loads); a uniform trip count keeps every
+    // group's lanes in the full-warp ballots
+    constexpr int LPP = 32 / PPW;
+    const int gl = int(threadIdx.x & 31) % LPP;
+    int t = T;
+    for (int tb = 0; tb < T; tb += LPP) {
+      const int tt = tb + gl;
+      const bool ne = pv && tt < T && int(start[tt + 1]) != 0;
+      const unsigned m = (__ballot_sync(0xffffffffu, ne) & gmask) >> (gmask == 0xffffffffu ? 0 : __ffs(gmask) - 1);
+      if (t == T && m) t = tb + __ffs(m) - 1;
+    }
+    int bend = t < T ? int(start[t + 1] & ~1u) : 0x7FFFFFFF;  // (padded) end of the current non-empty bucket t
+    int guard = (total + kIt - 1) / kIt + 2;  // iterations this group can take (a bug trap, never hit)
+    uint32_t ebase;  // shared-window address of the entries (computed once, kept in a register)
+    asm volatile("mov.u32 %0, %1;" : "=r"(ebase)
+                 : "r"(smem_u32(PRE ? static_cast<const void*>(sent) : static_cast<const void*>(list))));
+    // Every vote below is a full-warp ballot at a converged point; done is group-uniform.
+    while (true) {
+      if (__ballot_sync(0xffffffffu, !done) == 0) break;
+      uint4 cur[4];  // this iteration's 16 entries: shared memory (PRE past npre: global memory)
+      if (PRE && it * kIt >= a.npre) {
+        const uint4* g4 = reinterpret_cast<const uint4*>(ent + it * kIt * 4);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cur[u] = __ldg(g4 + u);
+      } else {
+        const uint32_t sa = ebase + uint32_t(it * kIt * 4);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(cur[u].x), "=r"(cur[u].y), "=r"(cur[u].z), "=r"(cur[u].w)
+                       : "r"(sa + 16 * u));
+      }
+      // blocks of NB entries: 16 for FPL <= 2 (one bookkeeping / vote / threshold test per 16 gathers),
+      // 8 for FPL = 4 (register budget: 4 registers per gathered entry)
+      constexpr int NB = FPL == 4 ? 8 : 16;
+      const uint32_t offs[16] = {cur[0].x, cur[0].y, cur[0].z, cur[0].w, cur[1].x, cur[1].y, cur[1].z, cur[1].w,
+                                 cur[2].x, cur[2].y, cur[2].z, cur[2].w, cur[3].x, cur[3].y, cur[3].z, cur[3].w};
+#pragma unroll
+      for (int h = 0; h < 16 / NB; ++h) {
+        if (!done) {
+          // group-uniform: bucket ends inside this block (pair m ends bucket t_m)
+          unsigned endm = 0;
+          uint64_t tpk = 0;
+          i += NB;
+          while (bend <= i) {
+            const int m = ((bend - (i - NB)) >> 1) - 1;
+            endm |= 1u << m;
+            tpk |= uint64_t(t) << (8 * m);
+            ++t;
+            while (t < T && int(start[t + 1] & ~1u) == bend) ++t;  // empty buckets add nothing
+            bend = t < T ? int(start[t + 1] & ~1u) : 0x7FFFFFFF;
+          }
+          uint32_t off[NB];
+#pragma unroll
+          for (int k = 0; k < NB; ++k) off[k] = offs[h * NB + k];
+          walk_block_k3<FPL, S28, NB>(wls, off, endm, tpk, thr, acc, lo, vo);
+        }
+        const unsigned nf = __ballot_sync(0xffffffffu, !done && alive());
+        if (!done && ((nf & gmask) == 0 || i >= total)) done = true;
+      }
+      ++it;
+      if (!done && --guard < 0) {
+        flag_error(a.err, kErrInternal);
+        done = true;
+      }
+    }
+}
+
+
 // Walk one position's sorted list (K2/K3) for the FPL features of this lane, bucket by bucket: a
 // bucket's entries are added in blocks of NB (no test inside a bucket -- the potential is only
 // defined per time step), then every unfired feature is tested once at the bucket end (exact:
@@ -332,10 +497,14 @@ __device__ __forceinline__ void walk_gather_add(uint32_t wls, const uint32_t (&o
 // (start[t + 1] = padded end of bucket t | its pad count); entries come from shared memory (sent for
 // PRE, list otherwise) or, for PRE past the prefetched npre entries, from global memory (ent).  thr
 // is the threshold in the walk's fixed-point units (S28: 2^-28, else 2^-31).
-template <int FPL, int PPW, bool PRE, bool S28 = false>
+template <int FPL, int PPW, bool PRE, bool S28 = false, bool BW = true>
 __device__ __forceinline__ void walk_list(const WalkArgs& a, const unsigned char* wl, const uint16_t* start,
                                           const unsigned char* sent, const unsigned char* ent, const uint32_t* list,
                                           bool pv, unsigned valid, unsigned gmask, uint32_t& lo, float (&vo)[FPL]) {
+  if constexpr (!BW) {
+    walk_list_blocks<FPL, PPW, PRE, S28>(a, wl, start, sent, ent, list, pv, valid, gmask, lo, vo);
+    return;
+  }
   constexpr int NB = FPL == 4 ? 8 : 16;  // register budget: FPL registers per gathered entry
   constexpr int LPP = 32 / PPW;
   const int T = a.T;
