@@ -196,27 +196,27 @@ __device__ __forceinline__ void pool_window_nhwc(const uint8_t* limg, const floa
   for (int u = 0; u < VEC; ++u) bv[u] = best[u] == kNoSpike ? 0.0f : bv[u];
 }
 
-// -> planar output [B, F, Ho, Wo].  CTA = (32 output columns, 32 * VEC features) of one output row
-// of one image: warps take the columns, lanes VEC features each (coalesced channels-last reads), the
-// tile transposes through shared memory, then warps take features and lanes columns (coalesced
-// planar rows).  blockIdx.x = column tile + ntx * feature chunk, y = output row, z = image.
+// -> planar output [B, F, Ho, Wo].  CTA = (32 output columns, FT <= 32 * VEC features) of one output
+// row of one image.  Pass 1: the tile's (column, VEC-feature slot) items over the CTA's threads,
+// slots fastest (coalesced channels-last reads; a narrow layer -- C4's F = 20 -- still fills the
+// warps); the results transpose through shared memory; pass 2: warps take features, lanes columns
+// (coalesced planar rows).  blockIdx.x = column tile + ntx * feature chunk, y = output row, z = image.
 template <int VEC>
 __global__ void __launch_bounds__(256) pool_nhwc_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ v,
                                                         int F, int H, int W, int PH, int PW, int SH, int SW, int DH,
-                                                        int DW, int Ho, int Wo, int ntx, int vfinal,
+                                                        int DW, int Ho, int Wo, int ntx, int FT, int vfinal,
                                                         uint8_t* __restrict__ lat_out, float* __restrict__ v_out) {
   pdl_begin();
-  constexpr int FT = 32 * VEC;                        // features per tile
-  constexpr int LS = FT + 4;                          // lat row stride (bytes), 4-aligned, odd word count
-  __shared__ __align__(16) uint8_t s_lat[32 * LS];    // [column][feature]
-  __shared__ float s_v[32 * (FT + 1)];                // [column][feature]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int FTM = 32 * VEC;                       // the largest feature tile
+  __shared__ __align__(16) uint8_t s_lat[32 * (FTM + 4)];   // [column][feature], row stride FT + 4
+  __shared__ float s_v[32 * (FTM + 1)];                     // [column][feature], row stride FT + 1
+  const int LS = FT + 4, VS = FT + 1, FV = FT / VEC;
   const int xt = blockIdx.x % ntx, fc = blockIdx.x / ntx, oy = blockIdx.y, b = blockIdx.z;
   const uint8_t* limg = lat + int64_t(b) * H * W * F;
   const float* vimg = v ? v + int64_t(b) * H * W * F : nullptr;
-  const int f = fc * FT + lane * VEC;
-  for (int p = warp; p < 32; p += 8) {
-    const int ox = xt * 32 + p;
+  for (int it = threadIdx.x; it < 32 * FV; it += blockDim.x) {
+    const int p = FV == 32 ? (it >> 5) : it / FV, sl = it - p * FV;  // (a full tile: shifts)
+    const int ox = xt * 32 + p, f = fc * FT + sl * VEC;
     unsigned best[VEC];
     float bv[VEC];
     if (ox < Wo && f < F) {
@@ -226,13 +226,14 @@ __global__ void __launch_bounds__(256) pool_nhwc_kernel(const uint8_t* __restric
       for (int u = 0; u < VEC; ++u) { best[u] = kNoSpike; bv[u] = 0.0f; }
     }
     if constexpr (VEC == 4)
-      *reinterpret_cast<uint32_t*>(s_lat + p * LS + lane * 4) = best[0] | (best[1] << 8) | (best[2] << 16) | (best[3] << 24);
+      *reinterpret_cast<uint32_t*>(s_lat + p * LS + sl * 4) = best[0] | (best[1] << 8) | (best[2] << 16) | (best[3] << 24);
     else
-      s_lat[p * LS + lane] = uint8_t(best[0]);
+      s_lat[p * LS + sl] = uint8_t(best[0]);
 #pragma unroll
-    for (int u = 0; u < VEC; ++u) s_v[p * (FT + 1) + lane * VEC + u] = bv[u];
+    for (int u = 0; u < VEC; ++u) s_v[p * VS + sl * VEC + u] = bv[u];
   }
   __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ox = xt * 32 + lane;
   if (ox >= Wo) return;
   for (int fl = warp; fl < FT; fl += 8) {
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(256) pool_nhwc_kernel(const uint8_t* __restric
     if (ff >= F) break;
     const int64_t o = ((int64_t(b) * F + ff) * Ho + oy) * Wo + ox;
     lat_out[o] = s_lat[lane * LS + fl];
-    if (v_out) v_out[o] = s_v[lane * (FT + 1) + fl];
+    if (v_out) v_out[o] = s_v[lane * VS + fl];
   }
 }
 
@@ -315,13 +316,15 @@ int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, 
                  DH, DW, Ho, Wo, vf, lat_out, v_out);
     } else {
       if (B > 65535 || Ho > 65535) return set_error(SNN_ESHAPE, "snn_pool(NHWC input): B or Ho > 65535");
-      const int ntx = int(ceil_div(Wo, 32)), nfc = int(ceil_div(F, 32 * vec));
+      const int ntx = int(ceil_div(Wo, 32));
+      const int FT = F < 32 * vec ? int(ceil_div(F, vec)) * vec : 32 * vec;  // features per tile
+      const int nfc = int(ceil_div(F, FT));
       if (vec == 4)
         launch_k(pool_nhwc_kernel<4>, dim3(unsigned(ntx * nfc), unsigned(Ho), unsigned(B)), dim3(256), 0, s, lat, vin,
-                 F, H, W, PH, PW, SH, SW, DH, DW, Ho, Wo, ntx, vf, lat_out, v_out);
+                 F, H, W, PH, PW, SH, SW, DH, DW, Ho, Wo, ntx, FT, vf, lat_out, v_out);
       else
         launch_k(pool_nhwc_kernel<1>, dim3(unsigned(ntx * nfc), unsigned(Ho), unsigned(B)), dim3(256), 0, s, lat, vin,
-                 F, H, W, PH, PW, SH, SW, DH, DW, Ho, Wo, ntx, vf, lat_out, v_out);
+                 F, H, W, PH, PW, SH, SW, DH, DW, Ho, Wo, ntx, FT, vf, lat_out, v_out);
     }
     note_launch();
     return check_launch("snn_pool(NHWC input)");
