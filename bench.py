@@ -285,22 +285,25 @@ class C5Step(C2Step):
 class SeqBase(C2Step):
     """Sequential plasticity configs: a batched fixed-weight prefix, then a CUDA graph of per-image
     plasticity steps (conv+fire -> [inhibit] -> kWTA -> [decide] -> STDP), no host sync per image."""
-    def _prefix(self, src=None):
+    def _prefix(self, src=None, mark=lambda i: None):
         snn, T = self.snn, self.wl.T
         snn.encode(self.x if src is None else src, T, out=self.lat0, ws=self.ws_enc, nhwc=self.l1 is not None)
+        mark(1)
         if self.l1 is not None:  # layer 1 reads and writes channels-last maps, its pool writes planar ones
-            self.l1(self.lat0)
+            self.l1.conv(self.lat0); mark(2)
+            self.l1.pool(); mark(3)
         if getattr(self, "prep", None) is not None:  # C4: the theta = +inf layer's A operands, all images
             s2 = self.wl.convs[1]
             snn.conv_inf_prepare(self.l1.plat, s2.F, s2.KH, s2.KW, s2.pad, T, out=self.prep)
+        mark(4)
 
     def run(self, ev=None, src=None):
         def mark(i):
             if ev is not None:
                 ev[i].record()
         mark(0)
-        self._prefix(src); mark(1)
-        self.graph.replay(); mark(2)
+        self._prefix(src, mark)
+        self.graph.replay(); mark(5)
 
     def e2e(self, x_host, out_host):
         self.x.copy_(x_host, non_blocking=True)
@@ -320,7 +323,12 @@ class SeqBase(C2Step):
         self.run()
         s = self.wl.convs[-1]
         lat_in = self.l1.plat if self.l1 is not None else self.lat0
-        return {"seq": self.snn.count_events(lat_in, s.F, s.KH, s.KW, s.pad, self.wl.T, None)}
+        out = {"seq": self.snn.count_events(lat_in, s.F, s.KH, s.KW, s.pad, self.wl.T, None)}
+        if self.l1 is not None:  # layer 1 (batched, fixed weights): paper and necessary events
+            s1 = self.wl.convs[0]
+            lat0 = self.lat0.permute(0, 3, 1, 2).contiguous()
+            out["conv1"] = self.snn.count_events(lat0, s1.F, s1.KH, s1.KW, s1.pad, self.wl.T, self.l1.lat.contiguous())
+        return out
 
 
 class C3Step(SeqBase):
@@ -351,7 +359,7 @@ class C3Step(SeqBase):
                                         wl.extra["k"], wl.extra["r"], True, wl.extra["stdp"], device=dev)
             self.graph = pipeline.SeqGraph(self.seq, self.l1.plat, batch, snapshot_every=wl.extra["snapshot_every"])
             self.mode = "per-image CUDA graph, no host sync"
-        self.stages = ["l1_prefix", "seq_stdp"]
+        self.stages = ["encode", "conv1", "pool1", "prep", "seq_stdp"]
 
     def config(self):
         return {"workload": "c3: BASELINE.json configs[2], sequential STDP on layer 2, 2000 images",
@@ -390,7 +398,7 @@ class C4Step(SeqBase):
                                 dtype=torch.uint8, device=dev)
         self._prefix()
         self.graph = pipeline.SeqGraph(self.seq, self.l1.plat, batch, labels=self.labels, prep=self.prep)
-        self.stages = ["l1_prefix", "seq_rstdp"]
+        self.stages = ["encode", "conv1", "pool1", "prep", "seq_rstdp"]
 
     def config(self):
         return {"workload": "c4: BASELINE.json configs[3], Caltech-shaped R-STDP, 1000 sequential images, T=30",

@@ -593,7 +593,12 @@ __device__ __forceinline__ void walk_list(const WalkArgs& a, const unsigned char
         load_off(k, off);
         walk_gather_add<FPL, S28, 4>(wls, off, acc);
       }
-      fire_at<FPL, S28>(acc, thr, t, lo, vo);  // the exact test at the bucket end
+      {  // the exact test at the bucket end; the conversions only in the (rare) bucket where one fires
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < FPL; ++j) any |= int64_t(acc[j]) > thr;
+        if (any) fire_at<FPL, S28>(acc, thr, t, lo, vo);
+      }
       if (__ballot_sync(gmask, alive()) == 0) break;
     }
     b0 = b1;
