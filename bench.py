@@ -388,8 +388,6 @@ class C4Step(SeqBase):
         self.lat0 = torch.empty((batch, H, W, C), dtype=torch.uint8, device=dev)   # channels-last
         self.l1 = pipeline.Layer(wl.convs[0], torch.from_numpy(wl.weights[0]).to(dev), batch, C, H, W, wl.T,
                                  wl.pools[0], pool_v=False, device=dev, nhwc=True, want_v=False, in_nhwc=True)
-        self.seq = pipeline.SeqSTDP(wl.convs[1], wl.weights[1], wl.convs[0].F, self.l1.PHo, self.l1.PWo, wl.T,
-                                    1, 0, False, wl.extra["stdp"], n_classes=wl.extra["n_classes"], device=dev)
         self.labels = torch.from_numpy(wl.extra["labels"].astype(np.int32)).to(dev)
         s2 = wl.convs[1]
         _, C2, H2, W2 = self.l1.plat.shape
@@ -397,14 +395,19 @@ class C4Step(SeqBase):
         self.prep = torch.empty(max(snn.lib().snn_conv_inf_prepare_bytes(batch, C2, H2, W2, s2.pad, s2.F, s2.KH, s2.KW), 1),
                                 dtype=torch.uint8, device=dev)
         self._prefix()
-        self.graph = pipeline.SeqGraph(self.seq, self.l1.plat, batch, labels=self.labels, prep=self.prep)
+        # f1: every image's chain (GEMM + tail CTA) from snn_rstdp_inf_sequence, captured as one CUDA graph
+        self.seq = pipeline.SeqInfRSTDP(s2, wl.weights[1], self.l1.plat, self.prep, self.labels, wl.T,
+                                        wl.extra["n_classes"], wl.extra["stdp"], device=dev)
+        self.graph = pipeline.StepGraph(self.seq.replay)
         self.stages = ["encode", "conv1", "pool1", "prep", "seq_rstdp"]
 
     def config(self):
         return {"workload": "c4: BASELINE.json configs[3], Caltech-shaped R-STDP, 1000 sequential images, T=30",
                 "global_batch": self.B,
                 "layers": "F20 5x5 th15 (4x160x250) -> pool7/6 -> F100 17x17 th=inf (tcgen05) -> 1 winner -> decide -> R-STDP",
-                "plasticity": "per-image CUDA graph, reward decided on device", "l2": "flushed between timed steps"}
+                "plasticity": "snn_rstdp_inf_sequence (per image: tcgen05 GEMM + one tail CTA for winner, decision, "
+                              "R-STDP and the winner's limbs), one CUDA graph, no host sync",
+                "l2": "flushed between timed steps"}
 
     def oracle_step(self, n):
         from oracle import flows

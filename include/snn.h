@@ -172,6 +172,27 @@ SNN_API int snn_conv_fire_prepared(const void* prep, int b, int C, int H, int W,
                                    snn_stream_t s);
 
 /* ---------------------------------------------------------------------------------------------
+ * snn_rstdp_inf_sequence -- SURVEY.md §8(f) f1 for a theta = +inf plastic layer (C4's R-STDP layer):
+ * N sequential images, each: conv Eq. 5 of image b0 + i of a snn_conv_inf_prepare batch `prep` with
+ * the current w -> the single winner = snn_k_winners(k = 1, r = 0) of that map (R13/R14)
+ * -> decision[i] / reward[i] as snn_decide with labels[i] (R24/R25; labels NULL: reward
+ * 0) -> snn_stdp_update of the winner (Eq. 4 with post = T - 1, rates negated for reward -1, skipped
+ * for 0 or no winner, R17-R23), w updated in place.  Bit-identical to those calls made image
+ * by image.  lat_in uint8 [N, C, H, W] (the layer input of the N images, planar, for the pre-synaptic
+ * times); w fp32 [F, C, KH, KW]; winners int32 [N, 3] (f, y, x; -1 when silent); count int32 [N];
+ * decision int32 [N] and reward fp32 [N] nullable.  Per image two kernels (a split-K tcgen05 GEMM
+ * and one tail CTA: winner, decision, Eq. 4 and the re-quantisation of the winner's weights only);
+ * no host synchronisation.  Workspace: snn_rstdp_inf_workspace (0 = unsupported shape).
+ * Errors: as snn_conv_fire (theta = +inf) and snn_stdp_update; F*Ho*Wo > 2^24: SNN_ESHAPE.
+ * ------------------------------------------------------------------------------------------- */
+SNN_API size_t snn_rstdp_inf_workspace(int C, int H, int W, int pad, int F, int KH, int KW);
+SNN_API int snn_rstdp_inf_sequence(const void* prep, int b0, int N, int C, int H, int W, int pad,
+                                   const uint8_t* lat_in, float* w, int F, int KH, int KW, int T,
+                                   const int32_t* labels, int n_classes, float a_plus, float a_minus, float lb,
+                                   float ub, int stabilizer, int32_t* winners, int32_t* count, int32_t* decision,
+                                   float* reward, void* ws, size_t ws_bytes, snn_stream_t s);
+
+/* ---------------------------------------------------------------------------------------------
  * a4. Spike-wave max-pooling (Eq. 3; readings R10-R12).
  * Window PH x PW, stride SH x SW, zero padding DH x DW (padding never spikes).
  * Ho = (H + 2*DH - PH) / SH + 1, Wo = (W + 2*DW - PW) / SW + 1 (windows inside the padded input).

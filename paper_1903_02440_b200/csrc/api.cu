@@ -57,6 +57,12 @@ int lateral_inhibition_launch(const float* x, int B, int C, int H, int W, const 
 size_t conv_inf_prepare_bytes(int B, int C, int H, int W, int pad, int F, int KH, int KW);
 int conv_inf_prepare_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, int F, int KH, int KW, int T,
                             void* prep, size_t prep_bytes, cudaStream_t s);
+size_t rstdp_inf_workspace(int C, int H, int W, int pad, int F, int KH, int KW);
+int rstdp_inf_sequence_launch(const void* prep, int b0, int N, int C, int H, int W, int pad, const uint8_t* lat_in,
+                              float* w, int F, int KH, int KW, int T, const int32_t* labels, int n_classes,
+                              float a_plus, float a_minus, float lb, float ub, int stabilizer, int32_t* winners,
+                              int32_t* count, int32_t* decision, float* reward, void* ws, size_t ws_bytes,
+                              cudaStream_t s);
 int conv_fire_prepared_launch(const void* prep, int b, int C, int H, int W, int pad, const float* w, int F, int KH,
                               int KW, int T, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes,
                               cudaStream_t s);
@@ -246,6 +252,31 @@ int snn_conv_inf_prepare(const uint8_t* lat_in, int B, int C, int H, int W, int 
   if (B == 0 || F == 0) return SNN_OK;
   REQUIRE(lat_in && prep, SNN_EINVAL, "snn_conv_inf_prepare: NULL tensor");
   return conv_inf_prepare_launch(lat_in, B, C, H, W, pad, F, KH, KW, T, prep, prep_bytes, S(s));
+}
+
+size_t snn_rstdp_inf_workspace(int C, int H, int W, int pad, int F, int KH, int KW) {
+  if (C < 1 || H < 1 || W < 1 || pad < 0 || F < 1 || KH < 1 || KW < 1 || KH > H + 2 * pad || KW > W + 2 * pad) return 0;
+  return rstdp_inf_workspace(C, H, W, pad, F, KH, KW);
+}
+
+int snn_rstdp_inf_sequence(const void* prep, int b0, int N, int C, int H, int W, int pad, const uint8_t* lat_in,
+                           float* w, int F, int KH, int KW, int T, const int32_t* labels, int n_classes, float a_plus,
+                           float a_minus, float lb, float ub, int stabilizer, int32_t* winners, int32_t* count,
+                           int32_t* decision, float* reward, void* ws, size_t ws_bytes, snn_stream_t s) {
+  int rc = conv_checks(1, C, H, W, pad, F, KH, KW, T, INFINITY);
+  if (rc) return rc;
+  REQUIRE(b0 >= 0 && N >= 0, SNN_EINVAL, "snn_rstdp_inf_sequence: b0 or N negative");
+  REQUIRE(n_classes >= 1 && F / n_classes >= 1, SNN_EINVAL, "snn_rstdp_inf_sequence: n_classes=%d", n_classes);
+  REQUIRE(stabilizer >= 0 && stabilizer <= 2, SNN_EINVAL, "snn_rstdp_inf_sequence: stabilizer=%d", stabilizer);
+  REQUIRE(lb < ub, SNN_EINVAL, "snn_rstdp_inf_sequence: LB >= UB");
+  REQUIRE(!isnan(a_plus) && !isnan(a_minus), SNN_EINVAL, "snn_rstdp_inf_sequence: NaN rate");
+  REQUIRE(int64_t(F) * (H + 2 * pad - KH + 1) * (W + 2 * pad - KW + 1) <= (int64_t(1) << 24), SNN_ESHAPE,
+          "snn_rstdp_inf_sequence: F*Ho*Wo > 2^24");
+  if (N == 0) return SNN_OK;
+  REQUIRE(prep && lat_in && w && winners && count, SNN_EINVAL, "snn_rstdp_inf_sequence: NULL tensor");
+  REQUIRE(ws, SNN_EWORKSPACE, "snn_rstdp_inf_sequence: NULL workspace");
+  return rstdp_inf_sequence_launch(prep, b0, N, C, H, W, pad, lat_in, w, F, KH, KW, T, labels, n_classes, a_plus,
+                                   a_minus, lb, ub, stabilizer, winners, count, decision, reward, ws, ws_bytes, S(s));
 }
 
 int snn_conv_fire_prepared(const void* prep, int b, int C, int H, int W, int pad, const float* w, int F, int KH,

@@ -502,3 +502,225 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
 }
 
 }  // namespace snn
+
+namespace snn {
+
+__device__ unsigned long long g_rstdp_stamps[4 * 4096];  // timing experiments (SNN_RSTDP_DBG & 8)
+extern "C" __attribute__((visibility("default"))) int snn_debug_rstdp_stamps(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, g_rstdp_stamps, sizeof(unsigned long long) * 4 * (n < 4096 ? n : 4096)) ==
+                 cudaSuccess ? 0 : -3;
+}
+
+// ------------------------------------------------------------------ f1: theta = +inf R-STDP chain
+// The per-image chain of a theta = +inf plastic layer (C4's second layer, Eq. 5, P:191,
+// P:258, Eq. 4 / P:161): conv (Eq. 5) -> one winner (k-WTA, k = 1) -> decision vs label -> reward ->
+// R-STDP of the winner's feature.  Per image two kernels: the split-K tcgen05 GEMM of the image's
+// prepared A operand (snn_conv_inf_prepare) with the resident B limbs, whose epilogue adds exact
+// int64 partial sums into part[M][F]; and one tail CTA that reads and clears part, takes the minimum
+// key (lat = T - 1 iff P > 0, v = fp32(P), flat index f H W + y W + x: the snn_k_winners order, R13/
+// R14), decides (the block decision_map of snn_decide, R24/R25), applies Eq. 4 to the winner's
+// weights (the snn_stdp_update arithmetic, R17-R22) and re-quantises only that feature's B limbs.
+// No host round trip and no full re-quantisation of the weights per image.
+// State shared by the two tail kernels of one image (zeroed by the launcher once; each image leaves it
+// clean for the next): the running minimum key, the CTA ticket, and the decided winner and reward.
+struct RstdpState {
+  unsigned long long best;  // minimum key over the CTAs (~0 = none)
+  unsigned int ticket;      // CTAs done with their slice
+  int f, y, x;              // winner of the image (f = -1: silent)
+  float rw;                 // its reward (+1, -1, 0 = no plasticity)
+};
+
+// Tail 1: CTAs share the M x F partial sums (each reads and clears its slice and offers its minimum key,
+// lat = T - 1 and v = fp32(P) descending, then flat index f H W + y W + x ascending: the snn_k_winners
+// order, R13/R14); the last CTA to finish decides (snn_decide's block decision_map, R24/R25) and
+// writes the image's outputs and the winner for tail 2.
+__global__ void __launch_bounds__(256) rstdp_inf_tail1_kernel(
+    unsigned long long* __restrict__ part, int M, int Wo, int F, int T, const int32_t* __restrict__ labels, int b,
+    int n_classes, RstdpState* st, int32_t* __restrict__ winners, int32_t* __restrict__ count,
+    int32_t* __restrict__ decision, float* __restrict__ reward, int dbg) {
+  pdl_begin();
+  if ((dbg & 8) && blockIdx.x == 0 && threadIdx.x == 0 && b < 4096) g_rstdp_stamps[4 * b + 0] = globaltimer_ns();
+  __shared__ uint64_t wmin[8];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int MF = M * F;
+  const int per = int(ceil_div(MF, gridDim.x));
+  const int i0 = blockIdx.x * per, i1 = min(MF, i0 + per);
+  uint64_t best = ~uint64_t(0);
+  for (int i = i0 + tid; i < i1; i += blockDim.x) {
+    const int64_t acc = int64_t(part[i]);
+    part[i] = 0ull;
+    if (acc > 0) {
+      const int m = i / F, f = i - m * F;
+      const uint64_t key = wta_key(uint8_t(T - 1), fixed_to_float(acc), uint32_t(f * M + m));
+      best = key < best ? key : best;
+    }
+  }
+  best = warp_min_u64(best);
+  if (lane == 0) wmin[warp] = best;
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t x = ~uint64_t(0);
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) x = wmin[w] < x ? wmin[w] : x;
+    if (x != ~uint64_t(0)) atomicMin(&st->best, (unsigned long long)x);
+    __threadfence();
+    s_last = atomicAdd(&st->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last || tid != 0) return;
+  __threadfence();
+  const uint64_t k = atomicExch(&st->best, ~0ull);  // read and reset for the next image
+  st->ticket = 0;
+  int f = -1, y = -1, x = -1, d = -1;
+  float rw = 0.0f;
+  if (k != ~0ull) {
+    const int idx = int(k & 0xFFFFFFu);
+    f = idx / M;
+    const int pos = idx - f * M;
+    y = pos / Wo;
+    x = pos - y * Wo;
+    d = f / (F / n_classes);
+    if (labels) rw = (d == labels[b]) ? 1.0f : -1.0f;
+  }
+  winners[0] = f; winners[1] = y; winners[2] = x;
+  count[0] = f >= 0 ? 1 : 0;
+  if (decision) decision[0] = d;
+  if (reward) reward[0] = rw;
+  st->f = f; st->y = y; st->x = x; st->rw = rw;
+  if ((dbg & 8) && b < 4096) g_rstdp_stamps[4 * b + 1] = globaltimer_ns();
+}
+
+// Tail 2: Eq. 4 on the winner's weights (post = T - 1, Eq. 5; the snn_stdp_update arithmetic, R17-R22)
+// and the re-quantisation of only that feature's B limbs: one thread per 16 consecutive GEMM columns k
+// -- the 16 weights' updates, then the four 16-byte limb rows of that core-matrix column (the
+// tc_prep_b16 layout); every load is issued before any use.
+__global__ void __launch_bounds__(128) rstdp_inf_tail2_kernel(
+    const RstdpState* __restrict__ st, int T, const uint8_t* __restrict__ lat_img, int C, int H, int W, int KH,
+    int KW, int pad, float* __restrict__ w, uint8_t* __restrict__ bq, TcPlan p, float a_plus, float a_minus,
+    float lb, float ub, int stabilizer, int* err, int b, int dbg) {
+  pdl_begin();
+  const int f = st->f, y = st->y, x = st->x;
+  const float rw = st->rw;
+  if (f < 0 || rw == 0.0f) return;
+  const float ap = rw > 0.0f ? a_plus : -a_plus, am = rw > 0.0f ? a_minus : -a_minus;
+  const int KK = KH * KW, R = C * KK, post = T - 1;
+  float* wf = w + int64_t(f) * R;
+  const int ch = f / p.Fc, fl = f - ch * p.Fc;
+  uint8_t* base = bq + size_t(ch) * p.Kt * p.N * kTcKT;
+  bool bad = false;
+  const int nk16 = p.K / 16 + (p.K % 16 ? 1 : 0);
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < nk16) {
+    const int k0 = g * 16;
+    uint32_t limb[4][4] = {};
+    const int kyx = p.hwc ? k0 / p.Cp : 0, c0 = p.hwc ? k0 - kyx * p.Cp : 0;
+    int ev[16], pre[16];
+    float w0v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      int e = -1, c = 0, ky = 0, kx = 0;
+      if (p.hwc) {  // column k = kyx Cp + c (channels padded to Cp)
+        c = c0 + j;
+        ky = kyx / KW; kx = kyx - ky * KW;
+        if (c < C) e = c * KK + kyx;
+      } else {      // column k = e = (c KH + ky) KW + kx
+        if (k0 + j < R) {
+          e = k0 + j;
+          c = e / KK;
+          const int rr = e - c * KK;
+          ky = rr / KW; kx = rr - ky * KW;
+        }
+      }
+      ev[j] = e;
+      const int yy = y + ky - pad, xx = x + kx - pad;
+      const bool inb = e >= 0 && yy >= 0 && yy < H && xx >= 0 && xx < W;
+      pre[j] = inb ? int(__ldg(lat_img + (int64_t(c) * H + yy) * W + xx)) : int(kNoSpike);
+      w0v[j] = e >= 0 ? wf[e] : 0.0f;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int e = ev[j];
+      if (e < 0) continue;
+      const float a = (pre[j] != kNoSpike && pre[j] <= post) ? ap : am;
+      const float w0 = w0v[j];
+      const float dw = stabilizer ? __fmul_rn(__fmul_rn(a, __fsub_rn(w0, lb)), __fsub_rn(ub, w0)) : a;
+      float w1 = __fadd_rn(w0, dw);
+      if (stabilizer != 2) {
+        w1 = w1 < lb ? lb : w1;
+        w1 = w1 > ub ? ub : w1;
+      }
+      wf[e] = w1;
+      const float sx = w1 * 2147483648.0f;
+      uint32_t q = 0;
+      if (!(w1 >= 0.0f && w1 <= 1.0f) || sx != truncf(sx)) bad = true;
+      else q = uint32_t(sx);
+#pragma unroll
+      for (int l = 0; l < 4; ++l) limb[l][j >> 2] |= ((q >> (8 * l)) & 0xFFu) << (8 * (j & 3));
+    }
+#pragma unroll
+    for (int l = 0; l < 4; ++l)
+      *reinterpret_cast<uint4*>(base + tc_off(4 * fl + l, k0, p.N, p.Kt)) =
+          make_uint4(limb[l][0], limb[l][1], limb[l][2], limb[l][3]);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flag_error(err, kErrInexact);
+  if ((dbg & 8) && blockIdx.x == 0 && threadIdx.x == 0 && b < 4096) g_rstdp_stamps[4 * b + 2] = globaltimer_ns();
+}
+
+size_t rstdp_inf_workspace(int C, int H, int W, int pad, int F, int KH, int KW) {
+  const TcPlan p = tc_plan(1, C, H, W, pad, KH, KW, F, num_sms());
+  return ((p.b_bytes + 1023) & ~size_t(1023)) + ((size_t(p.M) * F * sizeof(unsigned long long) + 255) & ~size_t(255)) +
+         256 + 1024;
+}
+
+int rstdp_inf_sequence_launch(const void* prep, int b0, int N, int C, int H, int W, int pad, const uint8_t* lat_in,
+                              float* w, int F, int KH, int KW, int T, const int32_t* labels, int n_classes,
+                              float a_plus, float a_minus, float lb, float ub, int stabilizer, int32_t* winners,
+                              int32_t* count, int32_t* decision, float* reward, void* ws, size_t ws_bytes,
+                              cudaStream_t s) {
+  TcPlan p = tc_plan(1, C, H, W, pad, KH, KW, F, num_sms());
+  if (ws_bytes < rstdp_inf_workspace(C, H, W, pad, F, KH, KW))
+    return set_error(SNN_EWORKSPACE, "snn_rstdp_inf_sequence: workspace too small");
+  const int Ho = H + 2 * pad - KH + 1, Wo = W + 2 * pad - KW + 1, R = C * KH * KW;
+  uint8_t* bq = reinterpret_cast<uint8_t*>(ws);
+  unsigned long long* part =
+      reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(ws) + ((p.b_bytes + 1023) & ~size_t(1023)));
+  int* err = error_word_ptr(s);
+  {  // the B limbs of the initial weights (afterwards only the winner's feature is re-quantised)
+    const int64_t total = int64_t(p.nch) * p.Fc * (p.Kp / 16);
+    int64_t blocks = ceil_div(total, 256);
+    if (blocks > int64_t(num_sms()) * 8) blocks = int64_t(num_sms()) * 8;
+    launch_k(tc_prep_b16_kernel, dim3(int(blocks)), dim3(256), 0, s, w, F, R, KH * KW, p, bq, err);
+    note_launch();
+  }
+  RstdpState* stp = reinterpret_cast<RstdpState*>(reinterpret_cast<uint8_t*>(part) +
+                                                   ((size_t(p.M) * F * sizeof(unsigned long long) + 255) & ~size_t(255)));
+  if (cudaMemsetAsync(part, 0, size_t(p.M) * F * sizeof(unsigned long long), s) != cudaSuccess ||
+      cudaMemsetAsync(stp, 0xFF, sizeof(unsigned long long), s) != cudaSuccess ||
+      cudaMemsetAsync(&stp->ticket, 0, sizeof(unsigned int), s) != cudaSuccess)
+    return check_launch("snn_rstdp_inf_sequence memset");
+  uint32_t cols = 32;
+  while (cols < uint32_t(p.N)) cols <<= 1;
+  const int smem = kTcStages * (kTcM * kTcKT + p.N * kTcKT) + 1024;
+  cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_rstdp_inf_sequence: %s", cudaGetErrorString(e));
+  const int64_t CHW = int64_t(C) * H * W;
+  const int dbg = getenv("SNN_RSTDP_DBG") ? atoi(getenv("SNN_RSTDP_DBG")) : 0;  // timing experiments only
+  const int MF = p.M * F;
+  const int t1 = int(ceil_div(MF, 1024)) < num_sms() ? int(ceil_div(MF, 1024)) : num_sms();  // ~1K neurons per CTA
+  const int nk16 = p.K / 16 + (p.K % 16 ? 1 : 0);
+  for (int i = 0; i < N; ++i) {
+    const uint8_t* aq = static_cast<const uint8_t*>(prep) + size_t(b0 + i) * p.a_bytes;
+    if (!(dbg & 2)) launch_k(conv_tc_kernel, dim3(unsigned(int64_t(p.Mt) * p.nch * p.KS)), dim3(kTcThreads), smem, s, aq,
+             (const uint8_t*)bq, p, F, Ho * Wo, T, cols, (uint8_t*)nullptr, (float*)nullptr, part, 0);
+    launch_k(rstdp_inf_tail1_kernel, dim3(t1 > 0 ? t1 : 1), dim3(256), 0, s, part, Ho * Wo, Wo, F, T, labels, i,
+             n_classes, stp, winners + 3 * i, count + i, decision ? decision + i : nullptr,
+             reward ? reward + i : nullptr, dbg);
+    launch_k(rstdp_inf_tail2_kernel, dim3(int(ceil_div(nk16, 128))), dim3(128), 0, s, (const RstdpState*)stp, T,
+             lat_in + int64_t(i) * CHW, C, H, W, KH, KW, pad, w, bq, p, a_plus, a_minus, lb, ub, stabilizer, err, i,
+             dbg);
+    note_launch(3);
+  }
+  return check_launch("snn_rstdp_inf_sequence");
+}
+
+}  // namespace snn

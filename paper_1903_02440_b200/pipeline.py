@@ -329,6 +329,37 @@ class SeqPersistent:
         self.run()
 
 
+class SeqInfRSTDP:
+    """f1 for a theta = +inf plastic layer (C4's R-STDP layer): all n images' chains -- conv (Eq. 5,
+    tcgen05) -> 1 winner -> decision -> R-STDP -- through snn_rstdp_inf_sequence, two kernels per image
+    (GEMM, tail CTA) and no host synchronisation.  ``replay()`` restores the initial weights first."""
+
+    def __init__(self, spec, w0, lat_in_all: torch.Tensor, prep: torch.Tensor, labels: torch.Tensor, T: int,
+                 n_classes: int, rates: Dict, device="cuda"):
+        self.spec, self.T, self.n_classes, self.rates = spec, T, n_classes, rates
+        self.w = _dev(w0, device).clone()
+        self.w0 = self.w.clone()
+        self.lat, self.prep, self.labels = lat_in_all, prep, labels
+        n, C, H, W = lat_in_all.shape
+        F, _, KH, KW = self.w.shape
+        self.winners = torch.empty((n, 3), dtype=torch.int32, device=device)
+        self.count = torch.empty((n,), dtype=torch.int32, device=device)
+        self.decision = torch.empty((n,), dtype=torch.int32, device=device)
+        self.reward = torch.empty((n,), dtype=torch.float32, device=device)
+        nb = int(snn.lib().snn_rstdp_inf_workspace(C, H, W, spec.pad, F, KH, KW))
+        self.ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=device)
+
+    def run(self):
+        R = self.rates
+        snn.rstdp_inf_sequence(self.prep, 0, self.lat, self.w, self.spec.pad, self.T, self.labels, self.n_classes,
+                               R["a_plus"], R["a_minus"], R["lb"], R["ub"], R["stabilizer"], winners=self.winners,
+                               count=self.count, decision=self.decision, reward=self.reward, ws=self.ws)
+
+    def replay(self):
+        self.w.copy_(self.w0)
+        self.run()
+
+
 class StepGraph:
     """CUDA graph of one fixed sequence of libsnn calls (``fn``) on preallocated buffers."""
 

@@ -50,6 +50,9 @@ def lib() -> C.CDLL:
                 "snn_validate_lat": (i32, [p, sz, i32, p, p]),
                 "snn_conv_fire_workspace": (sz, [i32] * 9 + [f32]),
                 "snn_conv_fire": (i32, [p, i32, i32, i32, i32, i32, p, i32, i32, i32, i32, f32, p, p, p, p, sz, p]),
+                "snn_rstdp_inf_workspace": (sz, [i32] * 7),
+                "snn_rstdp_inf_sequence": (i32, [p, i32, i32, i32, i32, i32, i32, p, p, i32, i32, i32, i32, p, i32,
+                                                 f32, f32, f32, f32, i32, p, p, p, p, p, sz, p]),
                 "snn_conv_fire_ex": (i32, [p, i32, i32, i32, i32, i32, p, i32, i32, i32, i32, f32, i32, p, p, p, p, sz,
                                            p]),
                 "snn_pool": (i32, [p, p, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, p, p, p]),
@@ -95,7 +98,7 @@ def exported_symbols():
             "snn_stdp_sequence", "snn_filter_bank", "snn_local_norm", "snn_lateral_inhibition",
             "snn_encode_ex", "snn_pool_ex", "snn_position_keys", "snn_k_winners_keys_workspace",
             "snn_k_winners_keys", "snn_stdp_update_shard", "snn_conv_inf_prepare_bytes", "snn_conv_inf_prepare",
-            "snn_conv_fire_prepared", "snn_conv_fire_ex"]
+            "snn_conv_fire_prepared", "snn_conv_fire_ex", "snn_rstdp_inf_workspace", "snn_rstdp_inf_sequence"]
 
 
 def _check(rc: int):
@@ -300,6 +303,31 @@ def conv_fire_prepared(prep: torch.Tensor, b: int, C_: int, H: int, W: int, w: t
     _check(lib().snn_conv_fire_prepared(_ptr(prep), int(b), C_, H, W, pad, _ptr(w), F, KH, KW, T, _ptr(lat), _ptr(v),
                                         _ptr(buf), buf.numel(), _stream(stream)))
     return lat, v
+
+
+def rstdp_inf_sequence(prep: torch.Tensor, b0: int, lat_in: torch.Tensor, w: torch.Tensor, pad: int, T: int,
+                       labels: Optional[torch.Tensor], n_classes: int, a_plus: float, a_minus: float, lb: float = 0.0,
+                       ub: float = 1.0, stabilizer: int = 1, winners=None, count=None, decision=None, reward=None,
+                       ws=None, stream=None):
+    """f1 theta = +inf R-STDP chain (snn_rstdp_inf_sequence): images b0 .. b0 + N - 1 of the prepared batch
+    ``prep``; lat_in uint8 [N, C, H, W] their (planar) layer input; w fp32 [F, C, KH, KW] updated in place.
+    Returns (winners [N, 3], count [N], decision [N], reward [N])."""
+    _req(lat_in, torch.uint8, "lat_in")
+    _req(w, torch.float32, "w")
+    N, C_, H, W = lat_in.shape
+    F, _, KH, KW = w.shape
+    dev = w.device
+    win = winners if winners is not None else torch.empty((N, 3), dtype=torch.int32, device=dev)
+    cnt = count if count is not None else torch.empty((N,), dtype=torch.int32, device=dev)
+    dec = decision if decision is not None else torch.empty((N,), dtype=torch.int32, device=dev)
+    rw = reward if reward is not None else torch.empty((N,), dtype=torch.float32, device=dev)
+    n = int(lib().snn_rstdp_inf_workspace(C_, H, W, pad, F, KH, KW))
+    buf = ws if ws is not None else _ws.get(n, dev, "rstdp_inf", stream)
+    _check(lib().snn_rstdp_inf_sequence(_ptr(prep), int(b0), N, C_, H, W, pad, _ptr(lat_in), _ptr(w), F, KH, KW, T,
+                                        _ptr(labels), int(n_classes), float(a_plus), float(a_minus), float(lb),
+                                        float(ub), int(stabilizer), _ptr(win), _ptr(cnt), _ptr(dec), _ptr(rw),
+                                        _ptr(buf), buf.numel(), _stream(stream)))
+    return win, cnt, dec, rw
 
 
 # ------------------------------------------------------------------------------------------ a4

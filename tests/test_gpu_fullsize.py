@@ -37,6 +37,8 @@ def test_c4_full_chain_bench_config(B, orc):
     step.snn.sync_status()
     ref = flows.c4(step.wl)
     assert np.array_equal(step.l1.plat.cpu().numpy(), ref["l1_pool_lat"])
+    assert np.array_equal(step.seq.decision.cpu().numpy(), ref["decision"])      # every image's decision
+    assert np.array_equal(step.seq.winners.cpu().numpy(), np.asarray(ref["winners"]).reshape(-1, 3))
     assert np.array_equal(step.seq.w.cpu().numpy(), ref["w2"])
 
 
