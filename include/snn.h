@@ -132,6 +132,10 @@ SNN_API int snn_validate_lat(const uint8_t* lat, size_t n, int T, int32_t* n_bad
  * Workspace: snn_conv_fire_workspace(..., theta) bytes.  theta = +inf without pot_out runs the
  * tensor-core path (tcgen05 kind::i8, exact 4-limb split of the fixed-point weights); its workspace
  * holds the binary im2col of S[T-1] (positions x C*KH*KW bytes) and the weight limbs.
+ * Finite theta: any receptive field R = C*KH*KW up to ~65,000 entries (a sorted list's u16 bucket
+ * starts); a layer whose weight slice does not fit shared memory (R above ~1,700 for 32 features)
+ * walks from the prepared slice in global memory (L2).  With pot_out (validation mode) the weight
+ * slice must fit shared memory: SNN_ESHAPE otherwise.
  * ------------------------------------------------------------------------------------------- */
 SNN_API size_t snn_conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T,
                                        float theta);
@@ -342,7 +346,8 @@ SNN_API int snn_stdp_update_shard(float* w, int F_local, int f_offset, int C, in
  * snn_conv_fire_plan (host only, no GPU needed) describes what one snn_conv_fire call with the same
  *   scalars (pot_out NULL) launches: *path = 0 fused sort+walk, 1 presorted walk (a sort and a walk
  *   kernel per list chunk, *chunks of them), 2 tensor-core Eq. 5 (theta = +inf), 3 tensor-core
- *   time-stepped (SNN_CONV_PATH=tct), 4 validation kernel; *launches = kernels per call.  Same
+ *   time-stepped (SNN_CONV_PATH=tct), 4 validation kernel, 5 presorted walk gathering its weights
+ *   from global memory (receptive fields too large for shared memory); *launches = kernels per call.  Same
  *   argument errors as snn_conv_fire.
  * ------------------------------------------------------------------------------------------- */
 SNN_API int snn_count_events(const uint8_t* lat_in, int B, int C, int H, int W, int pad, int F, int KH, int KW,

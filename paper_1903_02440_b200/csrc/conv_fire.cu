@@ -461,7 +461,7 @@ int conv_fire_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW, i
   if (ov == 0 && conv_tct_applies(B, C, H, W, pad, F, KH, KW, T, theta)) { *path = 3; *launches = 2; return SNN_OK; }
   int pre = 0, ch = 1, nl = 0;
   if (ov <= 1 && conv_walk_describe(B, C, H, W, pad, F, KH, KW, T, &pre, &ch, &nl)) {
-    *path = pre ? 1 : 0;
+    *path = pre == 2 ? 5 : pre ? 1 : 0;
     *chunks = ch;
     *launches = nl;  // weight prep + walk (latency mode: the walk converts the weights itself), or per chunk
     return SNN_OK;
@@ -508,8 +508,6 @@ int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   ConvPlan pl;
   make_plan(B, C, H, W, pad, F, KH, KW, T, inf, &pl);
   ConvArgs a = pl.a;
-  if (pl.dense && !inf)
-    return set_error(SNN_ESHAPE, "snn_conv_fire: receptive field R=%d too large for a finite threshold", a.R);
   if (ws_bytes < pl.wq_bytes) return set_error(SNN_EWORKSPACE, "snn_conv_fire: workspace %zu < %zu", ws_bytes, pl.wq_bytes);
   a.lat_in = lat_in; a.lat_out = lat_out; a.v_out = v_out; a.pot_out = pot_out; a.nhwc = nhwc;
   a.wq = reinterpret_cast<uint32_t*>(ws);
@@ -535,6 +533,9 @@ int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
     if (rc != 1) return rc;
     if (in_nhwc) return set_error(SNN_ESHAPE, "snn_conv_fire: channels-last input: receptive field too large for the walk");
   }
+  if (pl.dense && !inf)  // the walk did not apply and the validation kernel's weight slice does not fit
+    return set_error(SNN_ESHAPE, "snn_conv_fire: receptive field R=%d too large for a finite threshold%s", a.R,
+                     pot_out ? " with pot_out" : "");
   {
     int64_t total = int64_t(pl.n_groups) * (a.R + 1) * pl.FGS;
     int blocks = int(ceil_div(total, 256));

@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(512) rf_sort_kernel(const WalkArgs a) {
 
 // The per-position loop of conv_walk_kernel once the CTA's weight slice is staged (S28: the slice is
 // in units of 2^-28, see walk_block).
-template <int FPL, int PPW, bool PRE, bool S28, bool BW>
+template <int FPL, int PPW, bool PRE, bool S28, bool BW, bool GW = false, bool LS = false>
 __device__ __forceinline__ void walk_positions(const WalkArgs& a, unsigned char* smem) {
   constexpr int LPP = 32 / PPW;
   constexpr int FGS = LPP * FPL;
@@ -151,7 +151,9 @@ __device__ __forceinline__ void walk_positions(const WalkArgs& a, unsigned char*
   for (int j = 0; j < FPL; ++j) valid |= (fbase + j < a.F) ? (1u << j) : 0u;
   const unsigned gmask = (LPP == 32) ? 0xffffffffu : (((1u << LPP) - 1u) << (grp * LPP));
   const int64_t stride_w = int64_t(gridDim.x) * nwarps;
-  const unsigned char* wl = smem + gl * FPL * 4;  // this lane's features in weight row 0
+  // this lane's features in weight row 0: the shared-memory slice, or (GW) the group's prepared slice
+  const unsigned char* wl = GW ? reinterpret_cast<const unsigned char*>(a.wq + int64_t(g) * (a.R + 1) * FGS) + gl * FPL * 4
+                               : smem + gl * FPL * 4;
 
   // PRE: two per-warp position buffers [header | first npre entries], each filled by one bulk copy
   // (TMA, mbarrier completion) issued one position ahead, so the list of the next position streams in
@@ -171,6 +173,9 @@ __device__ __forceinline__ void walk_positions(const WalkArgs& a, unsigned char*
     }
     __syncwarp();
   }
+  // channels-last outputs with F % FPL == 0 and aligned pointers: a lane's FPL outputs are contiguous
+  const bool vec_out = a.nhwc && (a.F % FPL) == 0 && (reinterpret_cast<uintptr_t>(a.lat_out) % FPL) == 0 &&
+                       (reinterpret_cast<uintptr_t>(a.v_out) % (4 * FPL)) == 0;
   int npos_done = 0;
   for (int64_t wi = int64_t(blockIdx.x) * nwarps + warp; wi * PPW < a.np; wi += stride_w, ++npos_done) {
     const int64_t q = wi * PPW + grp;
@@ -195,7 +200,8 @@ __device__ __forceinline__ void walk_positions(const WalkArgs& a, unsigned char*
 
     uint32_t lo;
     float vo[FPL];
-    walk_list<FPL, PPW, PRE, S28, BW>(a, wl, start, sent, ent, list, pv, valid, gmask, lo, vo);
+    if constexpr (LS) walk_list_lockstep<FPL, PPW, S28>(a, wl, start, list, pv, valid, lo, vo);
+    else walk_list<FPL, PPW, PRE, S28, BW, GW>(a, wl, start, sent, ent, list, pv, valid, gmask, lo, vo);
     if (pv) {
       // NHWC: the warp's features of one position are contiguous (one or two lines per store);
       // NCHW: every feature is a separate plane (a line per lane per store)
@@ -204,12 +210,23 @@ __device__ __forceinline__ void walk_positions(const WalkArgs& a, unsigned char*
         const int b = p / HoWo, rem = p - b * HoWo;
         o0 = (int64_t(b) * a.F + fbase) * HoWo + rem;
       }
-      const int64_t fs = a.nhwc ? 1 : HoWo;
+      if (FPL > 1 && vec_out) {  // the lane's FPL outputs as one vector store each (a lane past F: none)
+        if (valid == 0) {
+        } else if constexpr (FPL == 2) {
+          *reinterpret_cast<uint16_t*>(a.lat_out + o0) = uint16_t(lo);
+          if (a.v_out) __stcs(reinterpret_cast<float2*>(a.v_out + o0), make_float2(vo[0], vo[1]));
+        } else if constexpr (FPL == 4) {
+          *reinterpret_cast<uint32_t*>(a.lat_out + o0) = lo;
+          if (a.v_out) __stcs(reinterpret_cast<float4*>(a.v_out + o0), make_float4(vo[0], vo[1], vo[2], vo[3]));
+        }
+      } else {
+        const int64_t fs = a.nhwc ? 1 : HoWo;
 #pragma unroll
-      for (int j = 0; j < FPL; ++j) {
-        if (valid >> j & 1) {
-          a.lat_out[o0 + j * fs] = uint8_t(lo >> (8 * j));
-          if (a.v_out) a.v_out[o0 + j * fs] = vo[j];
+        for (int j = 0; j < FPL; ++j) {
+          if (valid >> j & 1) {
+            a.lat_out[o0 + j * fs] = uint8_t(lo >> (8 * j));
+            if (a.v_out) a.v_out[o0 + j * fs] = vo[j];
+          }
         }
       }
     }
@@ -217,13 +234,18 @@ __device__ __forceinline__ void walk_positions(const WalkArgs& a, unsigned char*
   }
 }
 
-template <int FPL, int PPW, bool PRE, bool WCONV = false, bool BW = true>
+template <int FPL, int PPW, bool PRE, bool WCONV = false, bool BW = true, bool GW = false, bool LS = false>
 __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(const WalkArgs a) {
   pdl_wait();
   constexpr int LPP = 32 / PPW;
   constexpr int FGS = LPP * FPL;
   static_assert(!PRE || PPW == 1, "presorted walk: one position per warp");
+  static_assert(!GW || PRE, "global-weight walk: presorted lists");
   extern __shared__ __align__(16) unsigned char smem[];
+  if constexpr (GW) {  // the slice stays in global memory (units of 2^-31, from weight_prep)
+    walk_positions<FPL, PPW, PRE, false, BW, true>(a, smem);
+    return;
+  }
   const int R = a.R;
   const int tid = threadIdx.x;
   const int g = blockIdx.y;
@@ -268,15 +290,16 @@ __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(
       w4[i] = v;
     }
     __syncthreads();
-    walk_positions<FPL, PPW, PRE, true, BW>(a, smem);
+    walk_positions<FPL, PPW, PRE, true, BW, false, LS>(a, smem);
   } else {
-    walk_positions<FPL, PPW, PRE, false, BW>(a, smem);
+    walk_positions<FPL, PPW, PRE, false, BW, false, LS>(a, smem);
   }
 }
 
 // ------------------------------------------------------------------------------------- host
 struct WalkPlan {
   int fpl, ppw, FGS, n_groups, nwarps, smem;  // walk kernel
+  bool gw;                                     // presorted walk gathering from global memory (large R)
   int sort_ppw, sort_nwarps, sort_smem;        // sort kernel (presorted mode)
   bool pre;
   int64_t chunk;                                   // positions per list chunk
@@ -334,6 +357,7 @@ static bool walk_bucketwise(int R, int T) {
 static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, WalkPlan* pl) {
   WalkArgs& a = pl->a;
   a = WalkArgs{};
+  pl->gw = false;
   if (int64_t(B) * (H + 2 * pad - KH + 1) * (W + 2 * pad - KW + 1) >= (int64_t(1) << 31)) return false;
   a.B = B; a.C = C; a.H = H; a.W = W; a.pad = pad; a.F = F; a.KH = KH; a.KW = KW; a.T = T;
   a.Ho = H + 2 * pad - KH + 1; a.Wo = W + 2 * pad - KW + 1; a.R = C * KH * KW;
@@ -385,6 +409,9 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
   if (best >= 0) {
     pl->pre = false;
     pl->ppw = cands[best].ppw; pl->fpl = cands[best].fpl;
+    // several positions per warp: their lists are walked in lockstep (K3c, no pads); SNN_WALK_LOCKSTEP=0
+    // keeps the per-group walks (experiments)
+    if (pl->ppw > 1 && !(getenv("SNN_WALK_LOCKSTEP") && getenv("SNN_WALK_LOCKSTEP")[0] == '0')) a.pad_unit = 1;
     const int lpp = 32 / pl->ppw;
     pl->FGS = lpp * pl->fpl; pl->n_groups = 1; pl->nwarps = best_warps;
     a.row_bytes = pl->FGS * 4;
@@ -399,13 +426,19 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
   const int fpls[3] = {4, 2, 1};
   const char* fe = getenv("SNN_WALK_PRE_FPL");  // tuning experiments: force the presorted FPL
   const int force_fpl = fe ? atoi(fe) : 0;
-  for (int k = 0; k < 3; ++k) {
-    const int fpl = fpls[k], fgs = 32 * fpl;
+  // 3) receptive fields too large for any shared-memory slice (e.g. C2's layer 3 at a finite
+  //    threshold, R = 6,250): the same presorted walk gathering from the prepared slice in global
+  //    memory (L2-resident, (R + 1) x FGS x 4 bytes per group) -- Eq. 2 holds for any kernel size
+  for (int k = 0; k < 6; ++k) {
+    const bool gw = k >= 3;
+    const int fpl = fpls[k % 3], fgs = 32 * fpl;
     if (force_fpl && fpl != force_fpl) continue;
     if (!force_fpl && fgs > 32 && F <= fgs / 2) continue;
-    const long wsb = long(R + 1) * fgs * 4;
+    if (gw && getenv("SNN_WALK_NOGW")) continue;
+    const long wsb = gw ? 0 : long(R + 1) * fgs * 4;
     const int hdr_bytes = al16((T + 1) * 2);
     if (al16(int(wsb)) + 20L * (16 + 2 * (hdr_bytes + kIt * 4)) > kWalkSmemLimit) continue;
+    pl->gw = gw;
     pl->sort_ppw = sort_ppw_for(R);
     pl->pre = true;
     pl->ppw = 1; pl->fpl = fpl; pl->FGS = fgs;
@@ -438,6 +471,7 @@ static bool walk_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW
     sort_layout(sa, pl->sort_ppw, 0);
     while (pl->sort_nwarps > 1 && sa.off_warps + pl->sort_nwarps * sa.warp_bytes > kWalkSmemLimit) pl->sort_nwarps /= 2;
     pl->sort_smem = sa.off_warps + pl->sort_nwarps * sa.warp_bytes;
+    if (pl->sort_smem > kWalkSmemLimit) return false;  // not even one warp's sort scratch fits
     const int64_t npos = int64_t(B) * a.Ho * a.Wo;
     size_t chunk_bytes = kListChunkBytes;
     if (const char* e = getenv("SNN_LIST_CHUNK_MB")) chunk_bytes = size_t(atoi(e)) << 20;  // tuning experiments
@@ -459,9 +493,11 @@ size_t conv_walk_workspace(int B, int C, int H, int W, int pad, int F, int KH, i
   return n + 256;
 }
 
-template <int FPL, int PPW, bool PRE, bool WCONV = false>
+template <int FPL, int PPW, bool PRE, bool WCONV = false, bool GW = false>
 static int walk_go(const WalkPlan& pl, const WalkArgs& a, cudaStream_t s) {
-  auto k = a.pad_unit == 4 ? conv_walk_kernel<FPL, PPW, PRE, WCONV, true> : conv_walk_kernel<FPL, PPW, PRE, WCONV, false>;
+  auto k = a.pad_unit == 4 ? conv_walk_kernel<FPL, PPW, PRE, WCONV, true, GW>
+           : (PPW > 1 && !PRE && a.pad_unit == 1) ? conv_walk_kernel<FPL, PPW, PRE, WCONV, false, GW, PPW != 1>
+                                                  : conv_walk_kernel<FPL, PPW, PRE, WCONV, false, GW>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_conv_fire(walk): %s", cudaGetErrorString(e));
   int occ = 1;
@@ -520,7 +556,7 @@ int conv_walk_describe(int B, int C, int H, int W, int pad, int F, int KH, int K
                        int* launches) {
   WalkPlan pl;
   if (!walk_plan(B, C, H, W, pad, F, KH, KW, T, &pl)) return 0;
-  *pre = pl.pre ? 1 : 0;
+  *pre = pl.pre ? (pl.gw ? 2 : 1) : 0;
   *launches = pl.pre ? 1 + 2 * int(ceil_div(int64_t(B) * pl.a.Ho * pl.a.Wo, pl.chunk)) : (pl.ppw == 1 ? 1 : 2);
   *chunks = int(ceil_div(int64_t(B) * pl.a.Ho * pl.a.Wo, pl.chunk));
   return 1;
@@ -548,9 +584,9 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   const int64_t npos = int64_t(B) * a.Ho * a.Wo;
   if (getenv("SNN_DEBUG_PLAN"))
     fprintf(stderr, "walk plan: pre %d fpl %d ppw %d FGS %d groups %d warps %d smem %d | sort ppw %d "
-            "warps %d smem %d | rec %d hdr %d chunk %lld npos %lld\n", int(pl.pre), pl.fpl, pl.ppw, pl.FGS,
+            "warps %d smem %d | rec %d hdr %d chunk %lld npos %lld gw %d\n", int(pl.pre), pl.fpl, pl.ppw, pl.FGS,
             pl.n_groups, pl.nwarps, pl.smem, pl.sort_ppw, pl.sort_nwarps, pl.sort_smem, a.rec,
-            a.hdr, (long long)pl.chunk, (long long)npos);
+            a.hdr, (long long)pl.chunk, (long long)npos, int(pl.gw));
   if (!pl.pre && pl.ppw == 1) {  // latency mode (few positions): the walk converts the weights itself
     a.wf32 = w;
     a.p0 = 0; a.np = npos;
@@ -592,10 +628,18 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
     sa.p0 = a.p0; sa.np = a.np;
     rc = pl.sort_ppw == 4 ? sort_go<4>(pl, sa, s) : pl.sort_ppw == 2 ? sort_go<2>(pl, sa, s) : sort_go<1>(pl, sa, s);
     if (rc) return rc;
-    switch (pl.fpl) {
-      case 4: rc = walk_go<4, 1, true>(pl, a, s); break;
-      case 2: rc = walk_go<2, 1, true>(pl, a, s); break;
-      default: rc = walk_go<1, 1, true>(pl, a, s); break;
+    if (pl.gw) {
+      switch (pl.fpl) {
+        case 4: rc = walk_go<4, 1, true, false, true>(pl, a, s); break;
+        case 2: rc = walk_go<2, 1, true, false, true>(pl, a, s); break;
+        default: rc = walk_go<1, 1, true, false, true>(pl, a, s); break;
+      }
+    } else {
+      switch (pl.fpl) {
+        case 4: rc = walk_go<4, 1, true>(pl, a, s); break;
+        case 2: rc = walk_go<2, 1, true>(pl, a, s); break;
+        default: rc = walk_go<1, 1, true>(pl, a, s); break;
+      }
     }
     if (rc) return rc;
   }

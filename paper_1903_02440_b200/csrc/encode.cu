@@ -3,11 +3,14 @@
 // Per image, the N positive intensities are ranked by the unique 55-bit key
 //     K = ((0x7FFFFFFF - bits(x)) << 24) | flat_index          (x > 0, flat_index < 2^24)
 // whose ascending order is (value descending, index ascending).  Bin b (b = 1..T-1) starts at rank
-// start_b = b*q + min(b, m).  Instead of sorting, a multi-level MSB radix SELECT finds, for every
-// cut b, the key prefix of the element of rank start_b (levels of 12/12/12/12/7 bits; a cut stops
-// as soon as its digit bucket holds a single element).  Then every element's latency is the number
-// of cuts whose prefix it reaches: lat = #{b : (K >> shift_b) >= prefix_b}.  HBM traffic is one read
-// of x per level (L2-resident for a group of images) plus one write of lat.
+// start_b = b*q + min(b, m).  Instead of sorting, an MSB radix SELECT finds, for every cut b, the key
+// prefix of the element of rank start_b; every element's latency is then the number of cuts whose
+// prefix it reaches: lat = #{b : (K >> shift_b) >= prefix_b}.  Large images: two levels (12 + 8 bits,
+// per-image histograms; level 1 in shared memory), then pass 3 writes every element's latency except
+// those sharing a still unresolved cut's 20-bit prefix (the candidates, a few thousand per image),
+// which one CTA per image sorts by key to place the cuts exactly (enc_finish_kernel).  Three reads of
+// x in all.  An image with more than kEncCandCap candidates (heavy ties) takes levels 2-4 (12/12/11
+// bits) and the full assign instead, gated on the device.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -17,11 +20,18 @@ namespace snn {
 
 constexpr int kEncLevels = 5;
 constexpr int kEncBins = 4096;
-__constant__ int c_enc_bits[kEncLevels] = {12, 12, 12, 12, 7};
-__constant__ int c_enc_shift[kEncLevels] = {43, 31, 19, 7, 0};  // prefix after level L = K >> shift[L]
+// level 1 takes 8 bits so that its histograms (one per unresolved prefix) fit shared memory
+__constant__ int c_enc_bits[kEncLevels] = {12, 8, 12, 12, 11};
+__constant__ int c_enc_shift[kEncLevels] = {43, 35, 23, 11, 0};  // prefix after level L = K >> shift[L]
+constexpr int kEncL1Bins = 256, kEncL1MaxSlots = 32;
+// pass-3 tables per image: lat0[4096] (cuts passed by every key of a level-0 digit, 0xFF = depends on
+// the level-1 digit), slot0[4096] (that digit's row in lat1, 0xFF = none), lat1[32][256] (cuts passed by
+// every key of a 20-bit prefix, 0xFF = a still unresolved cut's prefix: a candidate)
+constexpr int kEncTabBytes = 4096 + 4096 + kEncL1MaxSlots * kEncL1Bins;
 constexpr int kEncThreads = 256;
 constexpr int kEncPerThread = 16;
 constexpr int kEncChunk = kEncThreads * kEncPerThread;
+constexpr int kEncCandCap = 8192;  // candidates per image after level 1 (20-bit prefixes; U(0,1) data: ~4K)
 
 struct EncodeWS {
   uint32_t* hist0;      // [G][4096]
@@ -32,6 +42,11 @@ struct EncodeWS {
   int32_t* cut_slot;    // [G][S]  slot of an unresolved cut, -1 when resolved / empty
   uint64_t* slot_prefix;// [G][S]
   int32_t* n_slots;     // [G]
+  uint64_t* cand;       // [G][kEncCandCap] keys of the elements whose 20-bit prefix is an unresolved cut's
+  int32_t* ncand;       // [G] candidate count (may exceed the capacity: overflow -> the full-level fallback)
+  int32_t* ovf;         // [G] 1 = the image takes the level 2-4 fallback
+  uint8_t* tab;         // [G][kEncTabBytes] pass-3 tables (enc_build_tables): lat0, slot0, lat1
+  int32_t* tabok;       // [G] the tables are valid (at most kEncL1MaxSlots level-0 cut digits)
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -49,6 +64,11 @@ static size_t encode_ws_layout(int G, int T, EncodeWS* ws, char* base) {
   w.cut_slot = (int32_t*)take(sizeof(int32_t) * size_t(G) * NC);
   w.slot_prefix = (uint64_t*)take(sizeof(uint64_t) * size_t(G) * S);
   w.n_slots = (int32_t*)take(sizeof(int32_t) * size_t(G));
+  w.cand = (uint64_t*)take(sizeof(uint64_t) * size_t(G) * kEncCandCap);
+  w.ncand = (int32_t*)take(sizeof(int32_t) * size_t(G));
+  w.ovf = (int32_t*)take(sizeof(int32_t) * size_t(G));
+  w.tab = (uint8_t*)take(size_t(G) * kEncTabBytes);
+  w.tabok = (int32_t*)take(sizeof(int32_t) * size_t(G));
   if (ws) *ws = w;
   return off;
 }
@@ -82,8 +102,32 @@ __device__ __forceinline__ uint32_t enc_cut_start(uint32_t b, uint32_t N, uint32
   return b * q + (b < m ? b : m);
 }
 
-// Level 0: histogram of the top 12 bits of every positive key (all images of the group).
-__global__ void __launch_bounds__(kEncThreads) enc_hist0_kernel(const float* __restrict__ x, int64_t n,
+// The 16 elements of a thread's share of a 4096-element chunk: element 4 (j kEncThreads + tid) + u of the
+// chunk in v[4 j + u] (j, u < 4), loaded as four float4 (vec: every image 16-byte aligned, n % 4 == 0)
+// or element by element; all loads issued before any use.  Out of range: 0 (never positive).
+__device__ __forceinline__ void enc_load16(const float* __restrict__ xg, int64_t n, int64_t base, bool vec,
+                                           float (&v)[16]) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t i = base + 4 * (int64_t(j) * kEncThreads + tid);
+    if (vec && i + 3 < n) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(xg + i));
+      v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[4 * j + u] = (i + u < n) ? __ldg(xg + i + u) : 0.0f;
+    }
+  }
+}
+__device__ __forceinline__ int64_t enc_elem(int64_t base, int k) {
+  return base + 4 * (int64_t(k >> 2) * kEncThreads + threadIdx.x) + (k & 3);
+}
+
+// Level 0: histogram of the top 12 bits of every positive key (all images of the group).  A CTA walks
+// several 4096-element chunks of its image (grid-stride), counting in one shared histogram with plain
+// shared atomics, then adds its non-zero bins to the image's histogram once.
+__global__ void __launch_bounds__(kEncThreads) enc_hist0_kernel(const float* __restrict__ x, int64_t n, bool vec,
                                                                  EncodeWS ws) {
   pdl_begin();
   __shared__ uint32_t sh[kEncBins];
@@ -91,23 +135,13 @@ __global__ void __launch_bounds__(kEncThreads) enc_hist0_kernel(const float* __r
   __syncthreads();
   const int g = blockIdx.y;
   const float* xg = x + int64_t(g) * n;
-  int64_t base = int64_t(blockIdx.x) * kEncChunk;
-  for (int j = 0; j < kEncPerThread; ++j) {
-    int64_t i = base + int64_t(j) * kEncThreads + threadIdx.x;
-    bool pos = false;
-    uint32_t d = 0;
-    if (i < n) {
-      float v = xg[i];
-      pos = v > 0.0f;
-      if (pos) d = uint32_t(enc_key(v, uint32_t(i)) >> 43);
-    }
-    // warp-aggregated shared atomics: intensities cluster in few bins (e.g. one exponent)
-    unsigned act = __ballot_sync(0xffffffffu, pos);
-    if (pos) {
-      unsigned peers = __match_any_sync(act, d);
-      int leader = __ffs(peers) - 1;
-      if ((threadIdx.x & 31) == leader) atomicAdd(&sh[d], __popc(peers));
-    }
+  const int64_t nch = (n + kEncChunk - 1) / kEncChunk;
+  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+    float v[16];
+    enc_load16(xg, n, ch * kEncChunk, vec, v);
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (v[k] > 0.0f) atomicAdd(&sh[(0x7FFFFFFFu - __float_as_uint(v[k])) >> 19], 1u);  // key bits 54..43
   }
   __syncthreads();
   uint32_t* hg = ws.hist0 + int64_t(g) * kEncBins;
@@ -115,16 +149,9 @@ __global__ void __launch_bounds__(kEncThreads) enc_hist0_kernel(const float* __r
     if (sh[i]) atomicAdd(&hg[i], sh[i]);
 }
 
-// Levels 1..4: histogram of the next digit for elements whose prefix matches an unresolved cut.
-__global__ void __launch_bounds__(kEncThreads) enc_hist_kernel(const float* __restrict__ x, int64_t n, int T,
-                                                                int level, EncodeWS ws) {
-  pdl_begin();
-  const int g = blockIdx.y;
-  const int S = T;
+// Sorted unresolved prefixes of image g in shared memory (sp) and a 4096-bit mask of their low 12 bits.
+__device__ __forceinline__ int enc_slots_smem(const EncodeWS& ws, int g, int S, uint64_t* sp, uint32_t* dmask) {
   const int ns = ws.n_slots[g];
-  if (ns == 0) return;
-  __shared__ uint64_t sp[256];
-  __shared__ uint32_t dmask[kEncBins / 32];  // previous-level digits of the unresolved prefixes
   for (int i = threadIdx.x; i < kEncBins / 32; i += blockDim.x) dmask[i] = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < ns; i += blockDim.x) {
@@ -133,96 +160,151 @@ __global__ void __launch_bounds__(kEncThreads) enc_hist_kernel(const float* __re
     atomicOr(&dmask[uint32_t(q >> 5) & (kEncBins / 32 - 1)], 1u << (uint32_t(q) & 31));
   }
   __syncthreads();
+  return ns;
+}
+// Slot of prefix p (lower bound in the sorted sp), or -1.
+__device__ __forceinline__ int enc_slot_of(uint64_t p, const uint64_t* sp, const uint32_t* dmask, int ns) {
+  const uint32_t dg = uint32_t(p) & (kEncBins - 1);  // a 12-bit digit: most elements leave here
+  if (!(dmask[dg >> 5] >> (dg & 31) & 1)) return -1;
+  int lo = 0, hi = ns;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (sp[mid] < p) lo = mid + 1; else hi = mid;
+  }
+  return (lo < ns && sp[lo] == p) ? lo : -1;
+}
+
+// Levels 1..4: histogram of the next digit for elements whose prefix matches an unresolved cut.
+// gate != NULL: only images with gate[g] != 0 (the fallback levels of overflowed images).
+__global__ void __launch_bounds__(kEncThreads) enc_hist_kernel(const float* __restrict__ x, int64_t n, bool vec, int T,
+                                                                int level, EncodeWS ws, const int32_t* gate) {
+  pdl_begin();
+  const int g = blockIdx.y;
+  if (gate && !gate[g]) return;
+  const int S = T;
+  if (ws.n_slots[g] == 0) return;
+  __shared__ uint64_t sp[256];
+  __shared__ uint32_t dmask[kEncBins / 32];  // previous-level digits of the unresolved prefixes
+  const int ns = enc_slots_smem(ws, g, S, sp, dmask);
   const int shp = c_enc_shift[level - 1], sh = c_enc_shift[level];
   const uint64_t mask = (uint64_t(1) << c_enc_bits[level]) - 1;
   const float* xg = x + int64_t(g) * n;
   uint32_t* hg = ws.hist + int64_t(g) * S * kEncBins;
-  int64_t base = int64_t(blockIdx.x) * kEncChunk;
-  for (int j = 0; j < kEncPerThread; ++j) {
-    int64_t i = base + int64_t(j) * kEncThreads + threadIdx.x;
-    if (i >= n) break;
-    float v = xg[i];
-    if (!(v > 0.0f)) continue;
-    uint64_t K = enc_key(v, uint32_t(i));
-    uint64_t p = K >> shp;
-    const uint32_t dg = uint32_t(p) & (kEncBins - 1);  // a 12-bit digit: most elements leave here
-    if (!(dmask[dg >> 5] >> (dg & 31) & 1)) continue;
-    int lo = 0, hi = ns;  // lower_bound
-    while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (sp[mid] < p) lo = mid + 1; else hi = mid;
+  // level 1 (8-bit digits, at most kEncL1MaxSlots prefixes): the CTA counts in shared memory and adds
+  // its non-zero bins to the image's histograms once; otherwise one global atomic per element
+  extern __shared__ uint32_t hs[];  // [ns][kEncL1Bins] (dynamic, level 1 only)
+  const bool sm = level == 1 && ns <= kEncL1MaxSlots;
+  __shared__ uint8_t slot_of[kEncBins];  // level 1: a level-0 digit's slot (the prefixes are the digits)
+  if (sm) {
+    for (int i = threadIdx.x; i < ns * kEncL1Bins; i += blockDim.x) hs[i] = 0;
+    for (int i = threadIdx.x; i < kEncBins; i += blockDim.x) slot_of[i] = 0xFF;
+    __syncthreads();
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) slot_of[uint32_t(sp[i]) & (kEncBins - 1)] = uint8_t(i);
+    __syncthreads();
+  }
+  const int64_t nch = (n + kEncChunk - 1) / kEncChunk;
+  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {  // grid-stride over the image's chunks
+    const int64_t base = ch * kEncChunk;
+    float v[16];
+    enc_load16(xg, n, base, vec, v);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      if (!(v[k] > 0.0f)) continue;
+      const uint64_t K = enc_key(v[k], uint32_t(enc_elem(base, k)));
+      int sl;
+      if (sm) {
+        const uint32_t s8 = slot_of[uint32_t(K >> shp)];  // K >> 43: exactly the 12-bit level-0 digit
+        sl = s8 == 0xFF ? -1 : int(s8);
+      } else {
+        sl = enc_slot_of(K >> shp, sp, dmask, ns);
+      }
+      if (sl < 0) continue;
+      const uint32_t dg = uint32_t((K >> sh) & mask);
+      if (sm) atomicAdd(&hs[sl * kEncL1Bins + dg], 1u);
+      else atomicAdd(&hg[int64_t(sl) * kEncBins + dg], 1u);
     }
-    if (lo < ns && sp[lo] == p) atomicAdd(&hg[int64_t(lo) * kEncBins + ((K >> sh) & mask)], 1u);
+  }
+  if (sm) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < ns * kEncL1Bins; i += blockDim.x)
+      if (hs[i]) atomicAdd(&hg[int64_t(i / kEncL1Bins) * kEncBins + (i % kEncL1Bins)], hs[i]);
   }
 }
 
-// Per-image selection after level L: locate every unresolved cut's digit, resolve or descend,
-// rebuild the sorted list of distinct prefixes for level L+1 and zero their histograms.
-__global__ void __launch_bounds__(256) enc_select_kernel(int T, int bins, int level, EncodeWS ws) {
+// Per-image selection after level L: locate every unresolved cut's digit (one warp per cut: the slot's
+// 4096-bin histogram scanned as 32 runs of 128 bins), resolve or descend, rebuild the sorted list of
+// distinct prefixes for level L+1 and zero their histograms.  gate: as enc_hist_kernel.
+__global__ void __launch_bounds__(1024) enc_select_kernel(int T, int bins, int level, EncodeWS ws,
+                                                          const int32_t* gate) {
   pdl_begin();
   const int g = blockIdx.x;
+  if (gate && !gate[g]) return;
   const int S = T;
   const int NC = enc_ncuts(T, bins);
-  __shared__ uint32_t cum[kEncBins + 1];
-  __shared__ uint32_t wsum[8];
   __shared__ int s_nslots;
   uint64_t* cp = ws.cut_prefix + int64_t(g) * S;
   int32_t* csh = ws.cut_shift + int64_t(g) * S;
   uint32_t* cr = ws.cut_resid + int64_t(g) * S;
   int32_t* cs = ws.cut_slot + int64_t(g) * S;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-
-  int nslots = (level == 0) ? 1 : ws.n_slots[g];
-  for (int s = 0; s < nslots; ++s) {
-    const uint32_t* h = (level == 0) ? ws.hist0 + int64_t(g) * kEncBins
-                                     : ws.hist + (int64_t(g) * S + s) * kEncBins;
-    // block exclusive scan of 4096 bins: 16 consecutive bins per thread
-    uint32_t loc[16], run = 0;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  if (level == 0) {  // initialise the cuts from N = total positives
+    __shared__ uint32_t s_n;
+    if (wid == 0) {
+      const uint4* h4 = reinterpret_cast<const uint4*>(ws.hist0 + int64_t(g) * kEncBins);
+      uint32_t sum = 0;
+      for (int i = lane; i < kEncBins / 4; i += 32) { const uint4 q = h4[i]; sum += q.x + q.y + q.z + q.w; }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) { loc[j] = h[tid * 16 + j]; run += loc[j]; }
-    uint32_t inc = run;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0) s_n = sum;
     }
-    if (lane == 31) wsum[wid] = inc;
     __syncthreads();
-    uint32_t wbase = 0;
-    for (int w = 0; w < wid; ++w) wbase += wsum[w];
-    uint32_t e = wbase + inc - run;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) { cum[tid * 16 + j] = e; e += loc[j]; }
-    if (tid == 255) cum[kEncBins] = e;
-    __syncthreads();
-    if (level == 0) {
-      // initialise the cuts from N = total positives
-      uint32_t N = cum[kEncBins];
-      for (int b = tid; b < NC; b += blockDim.x) {
-        uint32_t start = enc_cut_start(uint32_t(b + 1), N, uint32_t(T), bins);
-        cp[b] = 0;
-        if (start >= N) { csh[b] = -1; cs[b] = -1; cr[b] = 0; }
-        else { csh[b] = -2; cs[b] = 0; cr[b] = start; }
-      }
-      __syncthreads();
-    }
+    const uint32_t N = s_n;
     for (int b = tid; b < NC; b += blockDim.x) {
-      if (cs[b] != s || csh[b] == -1) continue;
-      uint32_t r = cr[b];
-      int lo = 0, hi = kEncBins - 1;  // largest d with cum[d] <= r
-      while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (cum[mid] <= r) lo = mid; else hi = mid - 1;
-      }
-      uint32_t cnt = cum[lo + 1] - cum[lo];
-      uint64_t np = (cp[b] << c_enc_bits[level]) | uint64_t(lo);
-      cp[b] = np;
-      cr[b] = r - cum[lo];
-      if (cnt == 1 || level == kEncLevels - 1) { csh[b] = c_enc_shift[level]; cs[b] = -1; }
-      else cs[b] = -3;  // unresolved, slot assigned below
+      const uint32_t start = enc_cut_start(uint32_t(b + 1), N, uint32_t(T), bins);
+      cp[b] = 0;
+      if (start >= N) { csh[b] = -1; cs[b] = -1; cr[b] = 0; }
+      else { csh[b] = -2; cs[b] = 0; cr[b] = start; }
     }
     __syncthreads();
   }
+  for (int b = wid; b < NC; b += nw) {
+    const int sl = cs[b];
+    if (sl < 0 || csh[b] == -1) continue;  // resolved or empty (warp-uniform)
+    const uint32_t* h = (level == 0) ? ws.hist0 + int64_t(g) * kEncBins : ws.hist + (int64_t(g) * S + sl) * kEncBins;
+    const uint32_t r = cr[b];
+    const uint4* h4 = reinterpret_cast<const uint4*>(h + lane * 128);
+    uint32_t run = 0;
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) {
+      const uint4 x4 = h4[q];
+      run += x4.x + x4.y + x4.z + x4.w;
+    }
+    uint32_t inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    // the digit holding rank r: the run whose inclusive sum first exceeds r, then a scan inside it
+    const unsigned over = __ballot_sync(0xffffffffu, inc > r);
+    const int L = __ffs(over) - 1;  // exists: r < the slot's total
+    if (lane == L) {
+      uint32_t c = inc - run;  // exclusive base of this run
+      int d = 0;
+      uint32_t cnt = 0;
+      for (int k = 0; k < 128; ++k) {
+        const uint32_t hk = h[lane * 128 + k];
+        if (c + hk > r) { d = k; cnt = hk; break; }
+        c += hk;
+      }
+      const int dig = L * 128 + d;
+      cp[b] = (cp[b] << c_enc_bits[level]) | uint64_t(dig);
+      cr[b] = r - c;
+      if (cnt == 1 || level == kEncLevels - 1) { csh[b] = c_enc_shift[level]; cs[b] = -1; }
+      else cs[b] = -3;  // unresolved, slot assigned below
+    }
+  }
+  __syncthreads();
   // rebuild slots for the next level: cuts are in rank order, so their prefixes are sorted
   if (tid == 0) {
     int n = 0;
@@ -237,8 +319,8 @@ __global__ void __launch_bounds__(256) enc_select_kernel(int T, int bins, int le
   }
   __syncthreads();
   if (level + 1 < kEncLevels) {
-    uint32_t* hg = ws.hist + int64_t(g) * S * kEncBins;
-    for (int64_t i = tid; i < int64_t(s_nslots) * kEncBins; i += blockDim.x) hg[i] = 0;
+    uint4* hg = reinterpret_cast<uint4*>(ws.hist + int64_t(g) * S * kEncBins);
+    for (int64_t i = tid; i < int64_t(s_nslots) * kEncBins / 4; i += blockDim.x) hg[i] = make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -252,39 +334,324 @@ struct EncOut {
   }
 };
 
+// The cuts of image g in shared memory for the latency count: sp = prefix, ssh = its shift (-1 = never
+// passed).  unres_shift >= 0: cuts still unresolved (after level 1) compare at that shift -- exact for
+// every element whose prefix is not theirs (those are the candidates).
+__device__ __forceinline__ void enc_cuts_smem(const EncodeWS& ws, int g, int S, int NC, int unres_shift,
+                                              uint64_t* sp, int* ssh) {
+  for (int b = threadIdx.x; b < NC; b += blockDim.x) {
+    sp[b] = ws.cut_prefix[int64_t(g) * S + b];
+    const int sh = ws.cut_shift[int64_t(g) * S + b];
+    ssh[b] = (sh == -2 && unres_shift >= 0) ? unres_shift : sh;
+  }
+}
+// Number of cuts passed by key K (pass(b) is monotone non-increasing in b).
+__device__ __forceinline__ int enc_passed(uint64_t K, const uint64_t* sp, const int* ssh, int NC) {
+  int lo = 0, hi = NC;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const bool pass = ssh[mid] >= 0 && (K >> ssh[mid]) >= sp[mid];
+    if (pass) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Fallback assign (all levels resolved): lat = number of cuts whose prefix the key reaches.
 __global__ void __launch_bounds__(kEncThreads) enc_assign_kernel(const float* __restrict__ x, int64_t n, int T,
                                                                   int bins, uint8_t* __restrict__ lat, EncodeWS ws,
-                                                                  EncOut eo) {
+                                                                  EncOut eo, const int32_t* gate) {
   pdl_begin();
   const int g = blockIdx.y;
+  if (gate && !gate[g]) return;
   const int S = T;
   const int NC = enc_ncuts(T, bins);
   __shared__ uint64_t sp[256];
   __shared__ int ssh[256];
-  for (int b = threadIdx.x; b < NC; b += blockDim.x) {
-    sp[b] = ws.cut_prefix[int64_t(g) * S + b];
-    ssh[b] = ws.cut_shift[int64_t(g) * S + b];
-  }
+  enc_cuts_smem(ws, g, S, NC, -1, sp, ssh);
   __syncthreads();
   const float* xg = x + int64_t(g) * n;
   uint8_t* lg = lat + int64_t(g) * n;
-  int64_t base = int64_t(blockIdx.x) * kEncChunk;
-  for (int j = 0; j < kEncPerThread; ++j) {
-    int64_t i = base + int64_t(j) * kEncThreads + threadIdx.x;
-    if (i >= n) break;
-    float v = xg[i];
-    uint8_t out = kNoSpike;
-    if (v > 0.0f) {
-      uint64_t K = enc_key(v, uint32_t(i));
-      int lo = 0, hi = NC;  // number of cuts passed (pass(b) is monotone non-increasing in b)
-      while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        bool pass = ssh[mid] >= 0 && (K >> ssh[mid]) >= sp[mid];
-        if (pass) lo = mid + 1; else hi = mid;
+  const int64_t nch = (n + kEncChunk - 1) / kEncChunk;
+  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {  // grid-stride over the image's chunks
+    const int64_t base = ch * kEncChunk;
+    for (int j = 0; j < kEncPerThread; ++j) {
+      int64_t i = base + int64_t(j) * kEncThreads + threadIdx.x;
+      if (i >= n) break;
+      float v = xg[i];
+      uint8_t out = kNoSpike;
+      if (v > 0.0f) {
+        const int lo = enc_passed(enc_key(v, uint32_t(i)), sp, ssh, NC);
+        out = lo >= T ? kNoSpike : uint8_t(lo);
       }
-      out = lo >= T ? kNoSpike : uint8_t(lo);
+      lg[eo.idx(uint32_t(i))] = out;
     }
-    lg[eo.idx(uint32_t(i))] = out;
+  }
+}
+
+// Per image after level 1: the pass-3 lookup tables (kEncTabBytes).  A key range (a level-0 digit, or a
+// 20-bit prefix) passes cut b entirely, not at all, or either way (ambiguous); a table entry is the number
+// of cuts the whole range passes, 0xFF if any cut is ambiguous there.  Cut b compares at its resolved
+// shift, a cut still unresolved after level 1 at shift 35 (its 20-bit prefix: ambiguous on that prefix,
+// whose elements become candidates).  More than kEncL1MaxSlots ambiguous level-0 digits: tabok = 0 and
+// pass 3 searches the cuts per element instead.
+// Cuts passed by every key of [kmin, kmax] (cuts are in rank order, so "passed" is monotone in b): all =
+// the cuts passed already at kmin (an unresolved cut only strictly above its prefix), any = the cuts
+// passed at kmax; all < any: some cut is ambiguous on the range -> 0xFF.
+__device__ __forceinline__ int enc_range_lat(uint64_t kmin, uint64_t kmax, const uint64_t* cp, const int* csh, int NC) {
+  const int shu = c_enc_shift[1];
+  auto count = [&](uint64_t K, bool strict_unres) {
+    int lo = 0, hi = NC;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const int c = csh[mid];
+      bool pass;
+      if (c == -1) pass = false;  // empty cut: never passed
+      else if (c >= 0) pass = (K >> c) >= cp[mid];
+      else pass = strict_unres ? (K >> shu) > cp[mid] : (K >> shu) >= cp[mid];
+      if (pass) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  const int all = count(kmin, true), any = count(kmax, false);
+  return any > all ? 0xFF : all;
+}
+__global__ void __launch_bounds__(1024) enc_tables_kernel(int T, int bins, EncodeWS ws) {
+  pdl_begin();
+  const int g = blockIdx.x, tid = threadIdx.x;
+  const int S = T, NC = enc_ncuts(T, bins);
+  __shared__ uint64_t cp[256];
+  __shared__ int csh[256];
+  __shared__ uint8_t lat0[kEncBins], slot0[kEncBins];
+  __shared__ uint16_t dig[kEncL1MaxSlots];
+  __shared__ int s_nk;
+  for (int b = tid; b < NC; b += blockDim.x) {
+    cp[b] = ws.cut_prefix[int64_t(g) * S + b];
+    csh[b] = ws.cut_shift[int64_t(g) * S + b];
+  }
+  __syncthreads();
+  const int sh0 = c_enc_shift[0], sh1 = c_enc_shift[1];
+  for (int d = tid; d < kEncBins; d += blockDim.x) {
+    const uint64_t kmin = uint64_t(d) << sh0, kmax = kmin + ((uint64_t(1) << sh0) - 1);
+    lat0[d] = uint8_t(enc_range_lat(kmin, kmax, cp, csh, NC));
+  }
+  __syncthreads();
+  if (tid < 32) {  // the ambiguous level-0 digits in ascending order -> rows of lat1
+    int nk = 0;
+    for (int d0 = 0; d0 < kEncBins; d0 += 32) {
+      const bool a = lat0[d0 + tid] == 0xFF;
+      const unsigned m = __ballot_sync(0xffffffffu, a);
+      const int k = nk + __popc(m & ((1u << tid) - 1u));
+      slot0[d0 + tid] = (a && k < kEncL1MaxSlots) ? uint8_t(k) : 0xFF;
+      if (a && k < kEncL1MaxSlots) dig[k] = uint16_t(d0 + tid);
+      nk += __popc(m);
+    }
+    if (tid == 0) s_nk = nk;
+  }
+  __syncthreads();
+  const int nk = s_nk;
+  uint8_t* tg = ws.tab + int64_t(g) * kEncTabBytes;
+  if (nk > kEncL1MaxSlots) {
+    if (tid == 0) ws.tabok[g] = 0;
+    return;
+  }
+  for (int i = tid; i < nk * kEncL1Bins; i += blockDim.x) {
+    const int k = i / kEncL1Bins, d1 = i - k * kEncL1Bins;
+    const uint64_t kmin = ((uint64_t(dig[k]) << c_enc_bits[1]) | uint64_t(d1)) << sh1;
+    const uint64_t kmax = kmin + ((uint64_t(1) << sh1) - 1);
+    tg[2 * kEncBins + i] = uint8_t(enc_range_lat(kmin, kmax, cp, csh, NC));
+  }
+  for (int i = tid; i < kEncBins; i += blockDim.x) { tg[i] = lat0[i]; tg[kEncBins + i] = slot0[i]; }
+  if (tid == 0) ws.tabok[g] = 1;
+}
+
+// Pass 3 (after level 1): the latency of every element whose 20-bit prefix no unresolved cut shares,
+// written in the output layout; the others (candidates, ~200 per U(0,1) image) are appended to the
+// image's candidate list for enc_finish_kernel.  Planar output: a 4096-element chunk per CTA, 4
+// consecutive latencies per 32-bit store.  Channels-last output (C <= 256): a tile of 128 positions x
+// all C channels per CTA (coalesced float4 reads of each channel's 128 positions), transposed in shared
+// memory and written as one contiguous 128 C-byte run.
+constexpr int kEncTileP = 128;
+__device__ __forceinline__ void enc_candidate(const EncodeWS& ws, int g, uint64_t K) {
+  const int slot = atomicAdd(&ws.ncand[g], 1);
+  if (slot < kEncCandCap) ws.cand[int64_t(g) * kEncCandCap + slot] = K;
+}
+__global__ void __launch_bounds__(kEncThreads) enc_assign2_kernel(const float* __restrict__ x, int64_t n, bool vec,
+                                                                   int T, int bins, uint8_t* __restrict__ lat,
+                                                                   EncodeWS ws, EncOut eo) {
+  pdl_begin();
+  const int g = blockIdx.y;
+  const int S = T;
+  const int NC = enc_ncuts(T, bins);
+  __shared__ uint64_t sp[256], slp[256];
+  __shared__ int ssh[256];
+  __shared__ uint32_t dmask[kEncBins / 32];
+  __shared__ __align__(16) uint8_t tab[kEncTabBytes];
+  extern __shared__ __align__(16) uint8_t tile[];  // [kEncTileP * C] (channels-last output only)
+  const bool tabok = ws.tabok[g] != 0;
+  if (tabok) {
+    const uint4* src = reinterpret_cast<const uint4*>(ws.tab + int64_t(g) * kEncTabBytes);
+    for (int i = threadIdx.x; i < kEncTabBytes / 16; i += blockDim.x) reinterpret_cast<uint4*>(tab)[i] = src[i];
+  }
+  enc_cuts_smem(ws, g, S, NC, c_enc_shift[1], sp, ssh);
+  const int ns = enc_slots_smem(ws, g, S, slp, dmask);  // (syncs)
+  const float* xg = x + int64_t(g) * n;
+  uint8_t* lg = lat + int64_t(g) * n;
+  const int shp = c_enc_shift[1];
+  auto lat_of = [&](float v, uint32_t i) -> uint8_t {
+    if (!(v > 0.0f)) return kNoSpike;
+    const uint64_t K = enc_key(v, i);
+    int c;
+    if (tabok) {  // two table lookups (level-0 digit, then its 20-bit prefix)
+      const uint32_t d0 = uint32_t(K >> c_enc_shift[0]);
+      c = tab[d0];
+      if (c == 0xFF) c = tab[2 * kEncBins + int(tab[kEncBins + d0]) * kEncL1Bins + int((K >> shp) & 0xFFu)];
+      if (c == 0xFF) {
+        enc_candidate(ws, g, K);
+        return kNoSpike;  // placeholder, rewritten by enc_finish_kernel
+      }
+    } else {
+      if (ns > 0 && enc_slot_of(K >> shp, slp, dmask, ns) >= 0) {
+        enc_candidate(ws, g, K);
+        return kNoSpike;
+      }
+      c = enc_passed(K, sp, ssh, NC);
+    }
+    return c >= T ? kNoSpike : uint8_t(c);
+  };
+  if (!eo.hw) {
+    const int64_t nch = (n + kEncChunk - 1) / kEncChunk;
+    for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {  // grid-stride over the image's chunks
+      const int64_t base = ch * kEncChunk;
+      float v[16];
+      enc_load16(xg, n, base, vec, v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t i = base + 4 * (int64_t(j) * kEncThreads + threadIdx.x);
+        uint32_t w = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) w |= uint32_t(lat_of(v[4 * j + u], uint32_t(i + u))) << (8 * u);
+        if (vec && i + 3 < n) {
+          *reinterpret_cast<uint32_t*>(lg + i) = w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (i + u < n) lg[i + u] = uint8_t(w >> (8 * u));
+        }
+      }
+    }
+    return;
+  }
+  // channels-last: tiles of positions [p0, p0 + 128) x channels [0, C), grid-stride.  C % 4 == 0 (and a
+  // 4-byte aligned output): a lane reads 4 channels at one position (each load coalesced across the
+  // warp's 32 positions), packs their latencies in one word and stores it to a tile row padded to an odd
+  // word count (conflict-free); the tile then leaves as whole words.  Otherwise byte-wise, rows of C + 1.
+  const int HW = eo.hw, C = eo.c;
+  const int ntiles = (HW + kEncTileP - 1) / kEncTileP;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool w4 = (C % 4 == 0) && (reinterpret_cast<uintptr_t>(lg) & 3) == 0;
+  const int rw = w4 ? C / 4 + 1 : 0;                 // tile row stride in words (w4)
+  uint32_t* tile32 = reinterpret_cast<uint32_t*>(tile);
+  for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+    const int p0 = tl * kEncTileP;
+    const int np = min(kEncTileP, HW - p0);
+    if (w4) {
+      const int ncg = C / 4;
+      for (int it = wid; it < ncg * (kEncTileP / 32); it += blockDim.x >> 5) {
+        const int cg = it / (kEncTileP / 32), q = (it - cg * (kEncTileP / 32)) * 32 + lane;
+        if (q < np) {
+          const int64_t i = int64_t(4 * cg) * HW + p0 + q;
+          float v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = __ldg(xg + i + int64_t(u) * HW);
+          uint32_t w = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) w |= uint32_t(lat_of(v[u], uint32_t(i + int64_t(u) * HW))) << (8 * u);
+          tile32[q * rw + cg] = w;
+        }
+      }
+      __syncthreads();
+      uint32_t* dst = reinterpret_cast<uint32_t*>(lg + int64_t(p0) * C);
+      for (int k = threadIdx.x; k < np * ncg; k += blockDim.x) {
+        const int p = k / ncg, wdx = k - p * ncg;
+        dst[k] = tile32[p * rw + wdx];
+      }
+    } else {
+      for (int it = threadIdx.x; it < C * kEncTileP; it += blockDim.x) {
+        const int c = it / kEncTileP, q = it - c * kEncTileP;
+        if (q < np) {
+          const int64_t i = int64_t(c) * HW + p0 + q;
+          tile[q * (C + 1) + c] = lat_of(__ldg(xg + i), uint32_t(i));
+        }
+      }
+      __syncthreads();
+      uint8_t* dst = lg + int64_t(p0) * C;
+      for (int k = threadIdx.x; k < np * C; k += blockDim.x) {
+        const int p = k / C, c = k - p * C;
+        dst[k] = tile[p * (C + 1) + c];
+      }
+    }
+    __syncthreads();  // the tile is rewritten by the next iteration
+  }
+}
+
+// Per image: the candidates of pass 3 sorted by key in shared memory (bitonic), each one's rank j among
+// the elements of its 20-bit prefix (all of them are candidates), and its latency: a cut still
+// unresolved with that prefix is passed iff j >= the cut's residual rank in the prefix (cut_resid);
+// every other cut compares as in pass 3.  More than kEncCandCap candidates: the image is flagged for
+// the level 2-4 fallback (ovf) and nothing is written here.
+constexpr int kEncFinThreads = 1024;
+__global__ void __launch_bounds__(kEncFinThreads) enc_finish_kernel(int T, int bins, uint8_t* __restrict__ lat,
+                                                                     int64_t n, EncodeWS ws, EncOut eo) {
+  pdl_begin();
+  extern __shared__ uint64_t ck[];  // [np2]
+  __shared__ uint64_t sp[256];
+  __shared__ int ssh[256];
+  __shared__ uint32_t cres[256];
+  const int g = blockIdx.x, tid = threadIdx.x;
+  const int S = T, NC = enc_ncuts(T, bins);
+  const int nc = ws.ncand[g];  // (zeroed by the launcher before pass 3)
+  if (tid == 0) ws.ovf[g] = nc > kEncCandCap ? 1 : 0;
+  if (nc > kEncCandCap || nc == 0) return;
+  const int shp = c_enc_shift[1];
+  for (int b = tid; b < NC; b += blockDim.x) {
+    sp[b] = ws.cut_prefix[int64_t(g) * S + b];
+    ssh[b] = ws.cut_shift[int64_t(g) * S + b];  // -2: unresolved at level 1 (prefix at shift shp)
+    cres[b] = ws.cut_resid[int64_t(g) * S + b];
+  }
+  int np2 = 1;
+  while (np2 < nc) np2 <<= 1;
+  for (int i = tid; i < np2; i += blockDim.x) ck[i] = i < nc ? ws.cand[int64_t(g) * kEncCandCap + i] : ~uint64_t(0);
+  __syncthreads();
+  for (int k = 2; k <= np2; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < np2; i += blockDim.x) {
+        const int p = i ^ j;
+        if (p > i) {
+          const uint64_t a = ck[i], b = ck[p];
+          if (((i & k) == 0) == (a > b)) { ck[i] = b; ck[p] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  uint8_t* lg = lat + int64_t(g) * n;
+  for (int q = tid; q < nc; q += blockDim.x) {
+    const uint64_t K = ck[q];
+    const uint64_t pfx = K >> shp;
+    int lo = 0, hi = q;  // first candidate of this prefix
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((ck[mid] >> shp) < pfx) lo = mid + 1; else hi = mid;
+    }
+    const uint32_t j = uint32_t(q - lo);
+    int a = 0, z = NC;  // cuts passed (monotone)
+    while (a < z) {
+      const int mid = (a + z) >> 1;
+      bool pass;
+      if (ssh[mid] == -2) pass = pfx > sp[mid] || (pfx == sp[mid] && j >= cres[mid]);
+      else pass = ssh[mid] >= 0 && (K >> ssh[mid]) >= sp[mid];
+      if (pass) a = mid + 1; else z = mid;
+    }
+    lg[eo.idx(uint32_t(K & 0xFFFFFFu))] = a >= T ? kNoSpike : uint8_t(a);
   }
 }
 
@@ -617,26 +984,55 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, u
   EncodeWS ws;
   size_t need = encode_ws_layout(G, T, &ws, (char*)wsp);
   if (ws_bytes < need) return set_error(SNN_EWORKSPACE, "snn_encode: workspace %zu < %zu bytes", ws_bytes, need);
-  int nchunks = int(ceil_div(n, kEncChunk));
+  const int nchunks = int(ceil_div(n, kEncChunk));
+  const bool vec = (n % 4 == 0) && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  // two radix levels over the image, then pass 3 (latencies + the few candidates) and a per-image
+  // finish; the level 2-4 passes run only for images with more than kEncCandCap candidates (gated
+  // on the device: no host round trip).  SNN_ENCODE_LEVELS=5 forces the all-level path (experiments).
+  const bool all_levels = (eo.hw && eo.c > 256) || (getenv("SNN_ENCODE_LEVELS") && atoi(getenv("SNN_ENCODE_LEVELS")) == 5);
+  int fin_smem = int(sizeof(uint64_t)) * kEncCandCap;
+  if (cudaFuncSetAttribute(enc_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_smem) != cudaSuccess)
+    return check_launch("snn_encode(finish attr)");
   for (int g0 = 0; g0 < B; g0 += G) {
     int gn = B - g0 < G ? B - g0 : G;
     const float* xg = x + int64_t(g0) * n;
-    if (cudaMemsetAsync(ws.hist0, 0, sizeof(uint32_t) * size_t(gn) * kEncBins, s) != cudaSuccess)
+    uint8_t* lg = lat + int64_t(g0) * n;
+    if (cudaMemsetAsync(ws.hist0, 0, sizeof(uint32_t) * size_t(gn) * kEncBins, s) != cudaSuccess ||
+        cudaMemsetAsync(ws.ncand, 0, sizeof(int32_t) * size_t(gn), s) != cudaSuccess)
       return check_launch("snn_encode memset");
     dim3 grid(nchunks, gn);
-    launch_k(enc_hist0_kernel, dim3(grid), dim3(kEncThreads), 0, s, xg, n, ws);
-    note_launch();
-    if (enc_ncuts(T, bins) > 0) {
-      launch_k(enc_select_kernel, dim3(gn), dim3(256), 0, s, T, bins, 0, ws);
+    // grid-stride kernels: about 16 chunks per CTA for level 0 (fewer flushes of the CTA histograms);
+    // the gated fallback kernels at most 16 CTAs per image (an image not taking them exits at once)
+    const dim3 grid0(unsigned(nchunks < 16 ? 1 : nchunks / 16), gn), gridg(unsigned(nchunks < 16 ? nchunks : 16), gn);
+    launch_k(enc_hist0_kernel, dim3(grid0), dim3(kEncThreads), 0, s, xg, n, vec, ws);
+    launch_k(enc_select_kernel, dim3(gn), dim3(1024), 0, s, T, bins, 0, ws, (const int32_t*)nullptr);
+    launch_k(enc_hist_kernel, dim3(grid0), dim3(kEncThreads), kEncL1MaxSlots * kEncL1Bins * 4, s, xg, n, vec, T, 1, ws,
+             (const int32_t*)nullptr);
+    launch_k(enc_select_kernel, dim3(gn), dim3(1024), 0, s, T, bins, 1, ws, (const int32_t*)nullptr);
+    note_launch(4);
+    if (!all_levels) {
+      launch_k(enc_tables_kernel, dim3(gn), dim3(1024), 0, s, T, bins, ws);
       note_launch();
-      for (int L = 1; L < kEncLevels; ++L) {
-        launch_k(enc_hist_kernel, dim3(grid), dim3(kEncThreads), 0, s, xg, n, T, L, ws);
-        note_launch();
-        launch_k(enc_select_kernel, dim3(gn), dim3(256), 0, s, T, bins, L, ws);
-        note_launch();
-      }
     }
-    launch_k(enc_assign_kernel, dim3(grid), dim3(kEncThreads), 0, s, xg, n, T, bins, lat + int64_t(g0) * n, ws, eo);
+    const int32_t* gate = nullptr;
+    if (!all_levels) {
+      // grid-stride pass 3: about 8 chunks (or tiles) per CTA, so the per-CTA table loads stay small
+      const int64_t units = eo.hw ? ceil_div(eo.hw, kEncTileP) : nchunks;
+      dim3 g3(unsigned(units < 8 ? 1 : units / 8), gn);
+      const int tile_bytes = eo.hw ? kEncTileP * (eo.c + 4) : 0;  // rows padded (see enc_assign2_kernel)
+      if (cudaFuncSetAttribute(enc_assign2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_bytes) != cudaSuccess)
+        return check_launch("snn_encode(assign attr)");
+      launch_k(enc_assign2_kernel, dim3(g3), dim3(kEncThreads), tile_bytes, s, xg, n, vec, T, bins, lg, ws, eo);
+      launch_k(enc_finish_kernel, dim3(gn), dim3(kEncFinThreads), fin_smem, s, T, bins, lg, n, ws, eo);
+      note_launch(2);
+      gate = ws.ovf;
+    }
+    for (int L = 2; L < kEncLevels; ++L) {
+      launch_k(enc_hist_kernel, dim3(gate ? gridg : grid), dim3(kEncThreads), 0, s, xg, n, vec, T, L, ws, gate);
+      launch_k(enc_select_kernel, dim3(gn), dim3(1024), 0, s, T, bins, L, ws, gate);
+      note_launch(2);
+    }
+    launch_k(enc_assign_kernel, dim3(gate ? gridg : grid), dim3(kEncThreads), 0, s, xg, n, T, bins, lg, ws, eo, gate);
     note_launch();
     int rc = check_launch("snn_encode");
     if (rc) return rc;

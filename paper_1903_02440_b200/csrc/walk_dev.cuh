@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
@@ -20,6 +22,9 @@ constexpr int kListSlack = 2048;
 __host__ __device__ constexpr int list_cap(int R, int T) { return R + 3 * T + 2 * kIt; }
 #ifndef SNN_SORT_UNROLL
 #define SNN_SORT_UNROLL 4  // receptive-field entries per lane whose latency loads are in flight together
+#endif
+#ifndef SNN_SORT_BATCH
+#define SNN_SORT_BATCH 0   // 1: each lane's latencies loaded in batches of kSortUnroll before their updates
 #endif
 constexpr int kSortUnroll = SNN_SORT_UNROLL;                      // bytes read past the last record (prefetch)
 
@@ -86,6 +91,24 @@ __device__ __forceinline__ void wgather_s(uint32_t a, uint32_t (&o)[FPL]) {
   }
 }
 
+// Where a walk gathers its weight rows from: the CTA's shared-memory slice (a 32-bit shared-window
+// base, the default) or, for receptive fields too large for any shared-memory slice, the prepared
+// fixed-point slice in global memory (L2-resident; GW walks, see conv_walk.cu).
+struct WSrcS {
+  uint32_t b;
+  template <int FPL> __device__ __forceinline__ void g(uint32_t off, uint32_t (&o)[FPL]) const { wgather_s<FPL>(b + off, o); }
+};
+struct WSrcG {
+  const unsigned char* b;
+  template <int FPL> __device__ __forceinline__ void g(uint32_t off, uint32_t (&o)[FPL]) const {
+    typedef typename WalkVec<FPL>::T V;
+    const V v = __ldg(reinterpret_cast<const V*>(b + off));
+    if constexpr (FPL == 1) { o[0] = v; }
+    else if constexpr (FPL == 2) { o[0] = v.x; o[1] = v.y; }
+    else { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+  }
+};
+
 __device__ __forceinline__ uint8_t rf_lat(const WalkArgs& a, const int32_t* eoff, const uint16_t* ekk,
                                           const uint8_t* in, bool interior, int y0, int x0, int e) {
   if (interior) return in[eoff[e]];
@@ -111,11 +134,24 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl
   for (int t = gl; t < T; t += LPP) cnt[t] = 0;
   __syncwarp();
   if (pv) {
+#if SNN_SORT_BATCH
+    // latencies loaded in batches before their updates (the shared-memory atomics would otherwise order
+    // each entry's table lookup and dependent load behind the previous entry's atomic)
+    for (int e0 = gl; e0 < R; e0 += LPP * kSortUnroll) {
+      int lb[kSortUnroll];
+#pragma unroll
+      for (int k = 0; k < kSortUnroll; ++k) lb[k] = e0 + k * LPP < R ? lat_of(e0 + k * LPP) : int(kNoSpike);
+#pragma unroll
+      for (int k = 0; k < kSortUnroll; ++k)
+        if (lb[k] < T) atomicAdd(&cnt[lb[k]], 1u);
+    }
+#else
 #pragma unroll kSortUnroll
     for (int e = gl; e < R; e += LPP) {
       const int l = lat_of(e);
       if (l < T) atomicAdd(&cnt[l], 1u);
     }
+#endif
   }
   __syncwarp();
   // K2b: the last bucket kept, tcut = the first bucket whose running count reaches K* (every feature
@@ -164,11 +200,22 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl
   }
   __syncwarp();
   if (pv) {
+#if SNN_SORT_BATCH
+    for (int e0 = gl; e0 < R; e0 += LPP * kSortUnroll) {
+      int lb[kSortUnroll];
+#pragma unroll
+      for (int k = 0; k < kSortUnroll; ++k) lb[k] = e0 + k * LPP < R ? lat_of(e0 + k * LPP) : int(kNoSpike);
+#pragma unroll
+      for (int k = 0; k < kSortUnroll; ++k)
+        if (lb[k] <= tcut) list[atomicAdd(&cnt[lb[k]], 1u)] = uint32_t(e0 + k * LPP) * rb;
+    }
+#else
 #pragma unroll kSortUnroll
     for (int e = gl; e < R; e += LPP) {
       const int l = lat_of(e);
       if (l <= tcut) list[atomicAdd(&cnt[l], 1u)] = uint32_t(e) * rb;
     }
+#endif
   }
   {  // pad the tail to a whole walk iteration with the zero-weight row R
     const int n = carry;
@@ -300,11 +347,11 @@ __device__ __forceinline__ void fire_at(uint64_t (&acc)[FPL], int64_t thr, int t
 // NB consecutive entries of one bucket: gather each lane's FPL weights per entry (one conflict-free
 // LDS.32/64/128) and add them to the exact accumulators.  S28: every (up to) 8 weights are summed in
 // 32 bits (exact, < 2^31) before the 64-bit add (K3b).  Pad entries (the zero-weight row) add 0.
-template <int FPL, bool S28, int NB>
-__device__ __forceinline__ void walk_gather_add(uint32_t wls, const uint32_t (&off)[NB], uint64_t (&acc)[FPL]) {
+template <int FPL, bool S28, int NB, class WS>
+__device__ __forceinline__ void walk_gather_add(const WS& wls, const uint32_t (&off)[NB], uint64_t (&acc)[FPL]) {
   uint32_t wv[NB][FPL];
 #pragma unroll
-  for (int k = 0; k < NB; ++k) wgather_s<FPL>(wls + off[k], wv[k]);
+  for (int k = 0; k < NB; ++k) wls.template g<FPL>(off[k], wv[k]);
 #pragma unroll
   for (int j = 0; j < FPL; ++j) {
     uint64_t t = acc[j];
@@ -334,12 +381,12 @@ __device__ __forceinline__ void walk_gather_add(uint32_t wls, const uint32_t (&o
 // threshold no test inside the block could fire (potentials only grow along the list) and the block is
 // taken whole; otherwise the lane re-adds it pair by pair and tests at every bucket end (K3).
 // Sorted with pad unit 2: header word = padded end | pad count (bit 0).
-template <int FPL, bool S28, int NB>
-__device__ __forceinline__ void walk_block_k3(uint32_t wls, const uint32_t (&off)[NB], unsigned endm, uint64_t tpk,
+template <int FPL, bool S28, int NB, class WS>
+__device__ __forceinline__ void walk_block_k3(const WS& wls, const uint32_t (&off)[NB], unsigned endm, uint64_t tpk,
                                            int64_t thr, uint64_t (&acc)[FPL], uint32_t& lo, float (&vo)[FPL]) {
   uint32_t wv[NB][FPL];
 #pragma unroll
-  for (int k = 0; k < NB; ++k) wgather_s<FPL>(wls + off[k], wv[k]);
+  for (int k = 0; k < NB; ++k) wls.template g<FPL>(off[k], wv[k]);
   uint64_t s[FPL];
   bool hit = false;
 #pragma unroll
@@ -389,14 +436,16 @@ __device__ __forceinline__ void walk_block_k3(uint32_t wls, const uint32_t (&off
 // full-warp votes only.  start: T+1 bucket starts; entries come from shared memory (sent for PRE,
 // list otherwise) or, for PRE past the prefetched npre entries, from global memory (ent).  thr is
 // the threshold in the walk's fixed-point units (S28: 2^-28, else 2^-31).
-template <int FPL, int PPW, bool PRE, bool S28>
+template <int FPL, int PPW, bool PRE, bool S28, bool GW>
 __device__ __forceinline__ void walk_list_blocks(const WalkArgs& a, const unsigned char* wl, const uint16_t* start,
                                           const unsigned char* sent, const unsigned char* ent, const uint32_t* list,
                                           bool pv, unsigned valid, unsigned gmask, uint32_t& lo, float (&vo)[FPL]) {
   const int T = a.T;
   const int64_t thr = S28 ? a.thr28 : a.thr;
-  uint32_t wls;  // the lane's weight base as a shared-window address, opaque so it stays in a register
-  asm volatile("mov.u32 %0, %1;" : "=r"(wls) : "r"(smem_u32(wl)));
+  // the lane's weight base: a shared-window address, opaque so it stays in a register (GW: global)
+  typename std::conditional<GW, WSrcG, WSrcS>::type wls;
+  if constexpr (GW) wls.b = wl;
+  else asm volatile("mov.u32 %0, %1;" : "=r"(wls.b) : "r"(smem_u32(wl)));
     uint64_t acc[FPL];
     lo = 0xFFFFFFFFu;  // byte j = lat of feature j (255 = no spike)
 #pragma unroll
@@ -497,20 +546,22 @@ __device__ __forceinline__ void walk_list_blocks(const WalkArgs& a, const unsign
 // (start[t + 1] = padded end of bucket t | its pad count); entries come from shared memory (sent for
 // PRE, list otherwise) or, for PRE past the prefetched npre entries, from global memory (ent).  thr
 // is the threshold in the walk's fixed-point units (S28: 2^-28, else 2^-31).
-template <int FPL, int PPW, bool PRE, bool S28 = false, bool BW = true>
+template <int FPL, int PPW, bool PRE, bool S28 = false, bool BW = true, bool GW = false>
 __device__ __forceinline__ void walk_list(const WalkArgs& a, const unsigned char* wl, const uint16_t* start,
                                           const unsigned char* sent, const unsigned char* ent, const uint32_t* list,
                                           bool pv, unsigned valid, unsigned gmask, uint32_t& lo, float (&vo)[FPL]) {
   if constexpr (!BW) {
-    walk_list_blocks<FPL, PPW, PRE, S28>(a, wl, start, sent, ent, list, pv, valid, gmask, lo, vo);
+    walk_list_blocks<FPL, PPW, PRE, S28, GW>(a, wl, start, sent, ent, list, pv, valid, gmask, lo, vo);
     return;
   }
   constexpr int NB = FPL == 4 ? 8 : 16;  // register budget: FPL registers per gathered entry
   constexpr int LPP = 32 / PPW;
   const int T = a.T;
   const int64_t thr = S28 ? a.thr28 : a.thr;
-  uint32_t wls;  // the lane's weight base as a shared-window address, opaque so it stays in a register
-  asm volatile("mov.u32 %0, %1;" : "=r"(wls) : "r"(smem_u32(wl)));
+  // the lane's weight base: a shared-window address, opaque so it stays in a register (GW: global)
+  typename std::conditional<GW, WSrcG, WSrcS>::type wls;
+  if constexpr (GW) wls.b = wl;
+  else asm volatile("mov.u32 %0, %1;" : "=r"(wls.b) : "r"(smem_u32(wl)));
   uint32_t ebase;  // shared-window address of the entries
   asm volatile("mov.u32 %0, %1;" : "=r"(ebase)
                : "r"(smem_u32(PRE ? static_cast<const void*>(sent) : static_cast<const void*>(list))));
@@ -540,66 +591,172 @@ __device__ __forceinline__ void walk_list(const WalkArgs& a, const unsigned char
     if (m) t = tb + __ffs(m >> (__ffs(gmask) - 1)) - 1;
   }
   int b0 = 0;                            // padded start of bucket t (all earlier buckets are empty)
-  uint32_t wnext = t < T ? start[t + 1] : 0;
+  // header words through a 32-bit shared-window address kept in a register (start[t + 2] = hdr + 2 t + 4)
+  uint32_t hdr_a;
+  asm volatile("mov.u32 %0, %1;" : "=r"(hdr_a) : "r"(smem_u32(start)));
+  auto hdr_word = [&](int i) {
+    uint16_t h;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(hdr_a + uint32_t(2 * i)));
+    return uint32_t(h);
+  };
+  // entries k.. of the list from shared memory (every entry of a bucket below npre), 4 per LDS.128
+  auto load_sm = [&](int k, auto& off) {
+    constexpr int M = sizeof(off) / sizeof(off[0]);
+#pragma unroll
+    for (int q = 0; q < M / 4; ++q) {
+      uint4 c;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "r"(ebase + uint32_t((k + 4 * q) * 4)));
+      off[4 * q] = c.x; off[4 * q + 1] = c.y; off[4 * q + 2] = c.z; off[4 * q + 3] = c.w;
+    }
+  };
+  // PRE, past the prefetched npre entries (a long walk): 16-byte groups from global memory
+  auto load_gl = [&](int k, auto& off) {
+    constexpr int M = sizeof(off) / sizeof(off[0]);
+#pragma unroll
+    for (int q = 0; q < M / 4; ++q) {
+      const int e4 = k + 4 * q;
+      uint4 c;
+      if (e4 >= a.npre) {
+        c = __ldg(reinterpret_cast<const uint4*>(ent + e4 * 4));
+      } else {
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "r"(ebase + uint32_t(e4 * 4)));
+      }
+      off[4 * q] = c.x; off[4 * q + 1] = c.y; off[4 * q + 2] = c.z; off[4 * q + 3] = c.w;
+    }
+  };
+  // the padded bucket [b0, b1) (a multiple of 4 entries; its 0-3 pads gather the zero row) in blocks of
+  // NB, then at most one block of 8 (NB = 16) and one of 4: no per-entry predicates
+  auto add_bucket = [&](int b0_, int b1_, auto load_off) {
+    int k = b0_;
+    if constexpr (NB == 16) {
+      for (; k + 16 <= b1_; k += 16) {
+        uint32_t off[16];
+        load_off(k, off);
+        walk_gather_add<FPL, S28, 16>(wls, off, acc);
+      }
+    }
+    if (k + 8 <= b1_) {
+      uint32_t off[8];
+      load_off(k, off);
+      walk_gather_add<FPL, S28, 8>(wls, off, acc);
+      k += 8;
+      if constexpr (NB == 8) {
+        for (; k + 8 <= b1_; k += 8) {
+          uint32_t off2[8];
+          load_off(k, off2);
+          walk_gather_add<FPL, S28, 8>(wls, off2, acc);
+        }
+      }
+    }
+    if (k < b1_) {
+      uint32_t off[4];
+      load_off(k, off);
+      walk_gather_add<FPL, S28, 4>(wls, off, acc);
+    }
+  };
+  const int nsm = PRE ? a.npre : 0x7FFFFFFF;  // entries below nsm are in shared memory
+  uint32_t wnext = t < T ? hdr_word(t + 1) : 0;
+#pragma unroll 1
   for (; t < T; ++t) {
     const uint32_t w1 = wnext;
-    if (t + 1 < T) wnext = start[t + 2];  // the next header word in flight while this bucket is walked
+    if (t + 1 < T) wnext = hdr_word(t + 2);  // the next header word in flight while this bucket is walked
     const int b1 = int(w1 & ~3u), n = b1 - b0 - int(w1 & 3u);
     if (n > 0) {
-      // entries [b0, b0 + n): NB per block, the 16-byte entry groups from shared memory below npre,
-      // else from global memory (PRE)
-      auto load_off = [&](int k, auto& off) {
-        constexpr int M = sizeof(off) / sizeof(off[0]);
-        if (!PRE || k + M <= a.npre) {  // the common case: every entry prefetched (no global code)
+      if (!PRE || b1 <= nsm) add_bucket(b0, b1, load_sm);  // the common case: no global-memory code
+      else add_bucket(b0, b1, load_gl);
+      // the exact test at the bucket end; the conversions only in the (rare) bucket where one fires
+      bool any = false;
 #pragma unroll
-          for (int q = 0; q < M / 4; ++q) {
-            uint4 c;
-            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "r"(ebase + uint32_t((k + 4 * q) * 4)));
-            off[4 * q] = c.x; off[4 * q + 1] = c.y; off[4 * q + 2] = c.z; off[4 * q + 3] = c.w;
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < M / 4; ++q) {
-            const int e4 = k + 4 * q;
-            uint4 c;
-            if (e4 >= a.npre) {
-              c = __ldg(reinterpret_cast<const uint4*>(ent + e4 * 4));
-            } else {
-              asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                           : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "r"(ebase + uint32_t(e4 * 4)));
-            }
-            off[4 * q] = c.x; off[4 * q + 1] = c.y; off[4 * q + 2] = c.z; off[4 * q + 3] = c.w;
-          }
-        }
-      };
-      // the padded bucket [b0, b1) (a multiple of 4 entries; its 0-3 pads gather the zero row) in
-      // blocks of NB, then at most one block of 8 (NB = 16) and one of 4: no per-entry predicates
-      int k = b0;
-      if constexpr (NB == 16) {
-        for (; k + 16 <= b1; k += 16) {
-          uint32_t off[16];
-          load_off(k, off);
-          walk_gather_add<FPL, S28, 16>(wls, off, acc);
-        }
-      }
-      for (; k + 8 <= b1; k += 8) {
-        uint32_t off[8];
-        load_off(k, off);
-        walk_gather_add<FPL, S28, 8>(wls, off, acc);
-      }
-      if (k < b1) {
-        uint32_t off[4];
-        load_off(k, off);
-        walk_gather_add<FPL, S28, 4>(wls, off, acc);
-      }
-      {  // the exact test at the bucket end; the conversions only in the (rare) bucket where one fires
-        bool any = false;
-#pragma unroll
-        for (int j = 0; j < FPL; ++j) any |= int64_t(acc[j]) > thr;
+      for (int j = 0; j < FPL; ++j) any |= int64_t(acc[j]) > thr;
+      // only a bucket in which some lane fired can end the group's walk: vote on liveness only then
+      if (__any_sync(gmask, any)) {
         if (any) fire_at<FPL, S28>(acc, thr, t, lo, vo);
+        if (__ballot_sync(gmask, alive()) == 0) break;
       }
-      if (__ballot_sync(gmask, alive()) == 0) break;
+    }
+    b0 = b1;
+  }
+}
+
+// Walk PPW > 1 positions' sorted lists in lockstep (K3c; the fused schedule of small-receptive-field
+// layers, e.g. C2's first layer and C4's first layer, whose buckets hold a few entries each).  Every
+// lane runs the same bucket loop t = 0..T-1: a group gathers its own bucket's entries, the warp iterates
+// to the largest bucket of its groups (a shorter bucket's lanes gather the zero-weight row R), so control
+// never diverges between the groups of a warp; the exact test at each bucket end as in walk_list
+// (lat = t, v = P[t]).  Lists sorted with pad unit 1 (start[t + 1] = the end of bucket t, no pads).  S28:
+// up to 14 weights are summed in 32 bits (< 2^32) before the 64-bit add.  A group whose features have
+// all fired stops gathering; the warp stops when every group has.
+template <int FPL, int PPW, bool S28>
+__device__ __forceinline__ void walk_list_lockstep(const WalkArgs& a, const unsigned char* wl, const uint16_t* start,
+                                                   const uint32_t* list, bool pv, unsigned valid, uint32_t& lo,
+                                                   float (&vo)[FPL]) {
+  const int T = a.T;
+  const int64_t thr = S28 ? a.thr28 : a.thr;
+  WSrcS wls;
+  asm volatile("mov.u32 %0, %1;" : "=r"(wls.b) : "r"(smem_u32(wl)));
+  const uint32_t zrow = uint32_t(a.R) * uint32_t(a.row_bytes);  // the zero-weight row
+  uint64_t acc[FPL];
+  lo = 0xFFFFFFFFu;
+#pragma unroll
+  for (int j = 0; j < FPL; ++j) { acc[j] = (pv && (valid >> j & 1)) ? 0ull : kFiredAcc; vo[j] = 0.0f; }
+  auto alive = [&]() {
+    bool al = false;
+#pragma unroll
+    for (int j = 0; j < FPL; ++j) al |= int64_t(acc[j]) >= 0;
+    return al;
+  };
+  // a group is alive while one of its lanes has an unfired feature (group-uniform via the group's ballot)
+  constexpr int LPP = 32 / PPW;
+  const int grp = int(threadIdx.x & 31) / LPP;
+  const unsigned gmask = (LPP == 32) ? 0xffffffffu : (((1u << LPP) - 1u) << (grp * LPP));
+  bool galive = (__ballot_sync(0xffffffffu, alive()) & gmask) != 0;
+  if (!__any_sync(0xffffffffu, galive)) return;
+  uint32_t lbase;  // the group's list as a shared-window address
+  asm volatile("mov.u32 %0, %1;" : "=r"(lbase) : "r"(smem_u32(list)));
+  int b0 = 0;
+#pragma unroll 1
+  for (int t = 0; t < T; ++t) {
+    const int b1 = pv ? int(start[t + 1]) : 0;
+    const int n = galive ? b1 - b0 : 0;
+    const int nmax = __reduce_max_sync(0xffffffffu, n);
+    for (int c0 = 0; c0 < nmax; c0 += 14) {  // chunks of <= 14 entries (32-bit partial sums, S28)
+      const int c1 = min(nmax, c0 + 14);
+      uint32_t part[FPL];
+#pragma unroll
+      for (int j = 0; j < FPL; ++j) part[j] = 0;
+      for (int k = c0; k < c1; k += 2) {
+        uint32_t off[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          uint32_t e = zrow;
+          if (k + u < n) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(lbase + uint32_t((b0 + k + u) * 4)));
+          off[u] = e;
+        }
+        uint32_t w0[FPL], w1[FPL];
+        wls.template g<FPL>(off[0], w0);
+        wls.template g<FPL>(off[1], w1);
+#pragma unroll
+        for (int j = 0; j < FPL; ++j) {
+          if constexpr (S28) part[j] += w0[j] + w1[j];
+          else acc[j] += uint64_t(w0[j]) + w1[j];
+        }
+      }
+      if constexpr (S28) {
+#pragma unroll
+        for (int j = 0; j < FPL; ++j) acc[j] += part[j];
+      }
+    }
+    if (n > 0 || t == 0) {  // the exact test at the end of bucket t (t = 0: a negative threshold)
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < FPL; ++j) any |= int64_t(acc[j]) > thr;
+      if (any) fire_at<FPL, S28>(acc, thr, t, lo, vo);
+    }
+    if (__any_sync(0xffffffffu, n > 0 || t == 0)) {
+      galive = (__ballot_sync(0xffffffffu, alive()) & gmask) != 0;
+      if (!__any_sync(0xffffffffu, galive)) break;
     }
     b0 = b1;
   }

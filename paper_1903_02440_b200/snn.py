@@ -481,7 +481,7 @@ def conv_fire_plan(B: int, Cin: int, H: int, W: int, pad: int, F: int, KH: int, 
     path, launches, chunks = C.c_int(), C.c_int(), C.c_int()
     _check(lib().snn_conv_fire_plan(B, Cin, H, W, pad, F, KH, KW, T, theta, C.byref(path), C.byref(launches),
                                     C.byref(chunks)))
-    names = {0: "walk_fused", 1: "walk_presorted", 2: "tc_inf", 3: "tct", 4: "ref"}
+    names = {0: "walk_fused", 1: "walk_presorted", 2: "tc_inf", 3: "tct", 4: "ref", 5: "walk_presorted_global"}
     return {"path": names[path.value], "launches": launches.value, "chunks": chunks.value}
 
 

@@ -72,3 +72,14 @@ def test_host_side_errors_without_gpu(L):
     assert rc == snn.SNN_EINVAL
     # empty inputs are legal no-ops
     assert L.snn_encode(None, 0, 1, 4, 4, 5, None, None, 0, None) == 0
+
+
+def test_conv_plan_large_receptive_fields(L):
+    """Finite theta at any receptive-field size (Eq. 2): the planner picks the global-weight
+    presorted walk when no shared-memory slice fits (host only, no GPU)."""
+    from paper_1903_02440_b200 import snn
+    assert snn.conv_fire_plan(1000, 250, 4, 4, 2, 200, 5, 5, 15, 5.0)["path"] == "walk_presorted_global"
+    assert snn.conv_fire_plan(1, 20, 25, 40, 0, 100, 17, 17, 30, 5.0)["path"] == "walk_presorted_global"
+    assert snn.conv_fire_plan(1000, 250, 4, 4, 2, 200, 5, 5, 15, float("inf"))["path"] == "tc_inf"
+    assert snn.conv_fire_plan(1000, 30, 14, 14, 1, 250, 3, 3, 15, 10.0)["path"] == "walk_presorted"
+    assert L.snn_conv_fire_workspace(1000, 250, 4, 4, 2, 200, 5, 5, 15, 5.0) > 0
