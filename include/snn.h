@@ -184,9 +184,10 @@ SNN_API int snn_conv_fire_prepared(const void* prep, int b, int C, int H, int W,
  * for 0 or no winner, R17-R23), w updated in place.  Bit-identical to those calls made image
  * by image.  lat_in uint8 [N, C, H, W] (the layer input of the N images, planar, for the pre-synaptic
  * times); w fp32 [F, C, KH, KW]; winners int32 [N, 3] (f, y, x; -1 when silent); count int32 [N];
- * decision int32 [N] and reward fp32 [N] nullable.  Per image two kernels (a split-K tcgen05 GEMM
- * and one tail CTA: winner, decision, Eq. 4 and the re-quantisation of the winner's weights only);
- * no host synchronisation.  Workspace: snn_rstdp_inf_workspace (0 = unsupported shape).
+ * decision int32 [N] and reward fp32 [N] nullable.  Per image three kernels (a split-K tcgen05 GEMM,
+ * the winner/decision kernel and Eq. 4 with the re-quantisation of the winner's weights only); no host
+ * synchronisation.  SNN_RSTDP_PERSIST=1 runs the whole chain as one cooperative kernel instead (same
+ * results; measured slower on C4's shape).  Workspace: snn_rstdp_inf_workspace (0 = unsupported shape).
  * Errors: as snn_conv_fire (theta = +inf) and snn_stdp_update; F*Ho*Wo > 2^24: SNN_ESHAPE.
  * ------------------------------------------------------------------------------------------- */
 SNN_API size_t snn_rstdp_inf_workspace(int C, int H, int W, int pad, int F, int KH, int KW);

@@ -666,10 +666,279 @@ __global__ void __launch_bounds__(128) rstdp_inf_tail2_kernel(
   if ((dbg & 8) && blockIdx.x == 0 && threadIdx.x == 0 && b < 4096) g_rstdp_stamps[4 * b + 2] = globaltimer_ns();
 }
 
+// ------------------------------------------------------------- f1, one launch: the persistent chain
+// The whole N-image chain as ONE cooperative kernel (one CTA per (M tile, feature chunk, K slice) of the
+// split-K GEMM, all co-resident; TMEM allocated once).  Per image three phases separated by grid
+// barriers: A) the CTA's K slice of the image's GEMM (bulk-copy + mbarrier pipeline whose stage/phase
+// counters run on across images), exact int64 partial sums added into part[M][F]; B) every CTA reads and
+// clears a slice of part, takes its minimum key (the snn_k_winners order) and folds it into the image's
+// best key (double-buffered: best[i & 1]); C) every CTA decodes the winner and decision, and applies
+// Eq. 4 to its share of the winner's 16-column groups (w and the B limbs, as rstdp_inf_tail2_kernel).
+// Bit-identical to the per-image kernels; no launch or host round trip per image.
+struct PersistArgs {
+  const uint8_t* prep;            // snn_conv_inf_prepare A blocks
+  int b0, N;
+  const uint8_t* lat_in;          // [N][C][H][W]
+  int C, H, W, pad, KH, KW, F, T, Ho, Wo;
+  float* w;
+  uint8_t* bq;
+  unsigned long long* part;       // [M][F] (zero on entry, left zero)
+  unsigned long long* best;       // [2] (~0 on entry)
+  unsigned* bar;                  // [2] grid barrier (zero on entry)
+  const int32_t* labels;
+  int n_classes;
+  float a_plus, a_minus, lb, ub;
+  int stabilizer;
+  int32_t *winners, *count, *decision;
+  float* reward;
+  int* err;
+  TcPlan p;
+  uint32_t tmem_cols;
+};
+
+__device__ __forceinline__ void tc_grid_barrier(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned g = gen;
+    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicExch(&bar[1], g + 1);
+    } else {
+      const uint64_t t0 = globaltimer_ns();
+      for (;;) {
+        unsigned cur;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+        if (cur != g) break;
+        watchdog(t0);
+      }
+    }
+    __threadfence();
+  }
+  ++gen;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) rstdp_inf_persist_kernel(const PersistArgs q) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const TcPlan& p = q.p;
+  const uint32_t a_bytes = kTcM * kTcKT, b_bytes = uint32_t(p.N) * kTcKT, stage_bytes = a_bytes + b_bytes;
+  __shared__ __align__(8) uint64_t full_bar[kTcStages], empty_bar[kTcStages], done_bar;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ uint64_t wmin[kTcThreads / 32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ksi = int(blockIdx.x % unsigned(p.KS)), tile = int(blockIdx.x / unsigned(p.KS));
+  const int ch = tile % p.nch, mt = tile / p.nch;
+  const int kt0 = int(int64_t(ksi) * p.Kt / p.KS), kt1 = int(int64_t(ksi + 1) * p.Kt / p.KS);
+  const int F = q.F, HoWo = q.Ho * q.Wo, M = p.M, MF = M * F;
+  if (tid == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(smem_u32(&full_bar[s]), 1);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
+    }
+    mbar_init(smem_u32(&done_bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(q.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sh;
+  unsigned gen = 0;
+  int it0 = 0;  // pipeline stages consumed before this image (counters run on across images)
+  const int nk = kt1 - kt0;
+  const int KK = q.KH * q.KW, R = q.C * KK, post = q.T - 1;
+  const int nk16 = p.K / 16 + (p.K % 16 ? 1 : 0);
+  const int64_t CHW = int64_t(q.C) * q.H * q.W;
+  for (int i = 0; i < q.N; ++i) {
+    // ---------------- A: this CTA's K slice of image i's GEMM ----------------
+    const uint8_t* aq = q.prep + size_t(q.b0 + i) * p.a_bytes;
+    if (warp == 0 && lane == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // B limbs written by phase C (generic proxy)
+      const uint8_t* a_src = aq + size_t(mt) * p.Kt * a_bytes;
+      const uint8_t* b_src = q.bq + size_t(ch) * p.Kt * b_bytes;
+      for (int kt = kt0; kt < kt1; ++kt) {
+        const int c = it0 + (kt - kt0), s = c % kTcStages, u = c / kTcStages;
+        if (c >= kTcStages) mbar_wait(smem_u32(&empty_bar[s]), (u - 1) & 1);
+        const uint32_t fb = smem_u32(&full_bar[s]);
+        mbar_expect_tx(fb, stage_bytes);
+        const uint32_t dst = smem_u32(smem + size_t(s) * stage_bytes);
+        bulk_g2s(dst, a_src + size_t(kt) * a_bytes, a_bytes, fb);
+        bulk_g2s(dst + a_bytes, b_src + size_t(kt) * b_bytes, b_bytes, fb);
+      }
+    } else if (warp == 1 && lane == 0) {
+      const uint32_t idesc = (2u << 4) | (0u << 7) | (0u << 10) | (uint32_t(p.N >> 3) << 17) | (uint32_t(kTcM >> 4) << 24);
+      tc_fence_after();
+      for (int kt = kt0; kt < kt1; ++kt) {
+        const int c = it0 + (kt - kt0), s = c % kTcStages, u = c / kTcStages;
+        mbar_wait(smem_u32(&full_bar[s]), u & 1);
+        tc_fence_after();
+        const uint32_t a_base = smem_u32(smem + size_t(s) * stage_bytes);
+        const uint32_t b_base = a_base + a_bytes;
+#pragma unroll
+        for (int ks = 0; ks < kTcKT / 32; ++ks) {
+          const uint64_t da = umma_desc(a_base + ks * 256, 128, 1024);
+          const uint64_t db = umma_desc(b_base + ks * 256, 128, 1024);
+          umma_i8(tmem_base, da, db, idesc, ((kt - kt0) | ks) != 0);
+        }
+        umma_commit(smem_u32(&empty_bar[s]));
+      }
+      umma_commit(smem_u32(&done_bar));
+    } else if (warp >= 4) {
+      mbar_wait(smem_u32(&done_bar), uint32_t(i & 1));
+      tc_fence_after();
+      const int qd = warp & 3;
+      const int row = qd * 32 + lane;
+      const int m = mt * kTcM + row;
+      const uint32_t trow = tmem_base + (uint32_t(qd * 32) << 16);
+      for (int gq = 0; gq < p.Fc / 4; ++gq) {
+        uint32_t v[16];
+        tmem_ld16(trow + uint32_t(gq * 16), v);
+        if (m < M) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int f = ch * p.Fc + gq * 4 + j;
+            if (f < F) {
+              const int64_t acc = int64_t(v[4 * j]) + (int64_t(v[4 * j + 1]) << 8) + (int64_t(v[4 * j + 2]) << 16) +
+                                  (int64_t(v[4 * j + 3]) << 24);
+              atomicAdd(q.part + int64_t(m) * F + f, (unsigned long long)acc);
+            }
+          }
+        }
+      }
+    }
+    it0 += nk;
+    tc_fence_before();
+    tc_grid_barrier(q.bar, gen);
+    tc_fence_after();
+    // ---------------- B: winner key (lat = T - 1 iff P > 0, v = fp32(P) desc, flat index asc) ----------------
+    {
+      const int per = int(ceil_div(MF, int(gridDim.x)));
+      const int i0 = int(blockIdx.x) * per, i1 = min(MF, i0 + per);
+      uint64_t bk = ~uint64_t(0);
+      for (int e = i0 + tid; e < i1; e += blockDim.x) {
+        const int64_t acc = int64_t(q.part[e]);
+        q.part[e] = 0ull;
+        if (acc > 0) {
+          const int m = e / F, f = e - m * F;
+          const uint64_t key = wta_key(uint8_t(q.T - 1), fixed_to_float(acc), uint32_t(f * M + m));
+          bk = key < bk ? key : bk;
+        }
+      }
+      bk = warp_min_u64(bk);
+      if (lane == 0) wmin[warp] = bk;
+      __syncthreads();
+      if (tid == 0) {
+        uint64_t x = ~uint64_t(0);
+        for (int w = 0; w < kTcThreads / 32; ++w) x = wmin[w] < x ? wmin[w] : x;
+        if (x != ~uint64_t(0)) atomicMin(&q.best[i & 1], (unsigned long long)x);
+      }
+    }
+    tc_grid_barrier(q.bar, gen);
+    // ---------------- C: decision and Eq. 4 on the winner (post = T - 1) ----------------
+    {
+      unsigned long long kb;
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(kb) : "l"(q.best + (i & 1)) : "memory");
+      int f = -1, y = -1, x = -1, d = -1;
+      float rw = 0.0f;
+      if (kb != ~0ull) {
+        const int idx = int(kb & 0xFFFFFFu);
+        f = idx / M;
+        const int pos = idx - f * M;
+        y = pos / q.Wo;
+        x = pos - y * q.Wo;
+        d = f / (F / q.n_classes);
+        if (q.labels) rw = (d == q.labels[i]) ? 1.0f : -1.0f;
+      }
+      if (blockIdx.x == 0 && tid == 0) {
+        q.winners[3 * i] = f; q.winners[3 * i + 1] = y; q.winners[3 * i + 2] = x;
+        q.count[i] = f >= 0 ? 1 : 0;
+        if (q.decision) q.decision[i] = d;
+        if (q.reward) q.reward[i] = rw;
+        q.best[(i + 1) & 1] = ~0ull;  // the next image's slot (last read before the previous barrier)
+      }
+      if (f >= 0 && rw != 0.0f) {
+        const float ap = rw > 0.0f ? q.a_plus : -q.a_plus, am = rw > 0.0f ? q.a_minus : -q.a_minus;
+        float* wf = q.w + int64_t(f) * R;
+        const int chw = f / p.Fc, fl = f - chw * p.Fc;
+        uint8_t* base = q.bq + size_t(chw) * p.Kt * p.N * kTcKT;
+        const uint8_t* lat_img = q.lat_in + int64_t(i) * CHW;
+        bool bad = false;
+        for (int g16 = int(blockIdx.x) * blockDim.x + tid; g16 < nk16; g16 += gridDim.x * blockDim.x) {
+          const int k0 = g16 * 16;
+          uint32_t limb[4][4] = {};
+          const int kyx = p.hwc ? k0 / p.Cp : 0, c0 = p.hwc ? k0 - kyx * p.Cp : 0;
+          int ev[16], pre[16];
+          float w0v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            int e = -1, c = 0, ky = 0, kx = 0;
+            if (p.hwc) {
+              c = c0 + j;
+              ky = kyx / q.KW; kx = kyx - ky * q.KW;
+              if (c < q.C) e = c * KK + kyx;
+            } else if (k0 + j < R) {
+              e = k0 + j;
+              c = e / KK;
+              const int rr = e - c * KK;
+              ky = rr / q.KW; kx = rr - ky * q.KW;
+            }
+            ev[j] = e;
+            const int yy = y + ky - q.pad, xx = x + kx - q.pad;
+            const bool inb = e >= 0 && yy >= 0 && yy < q.H && xx >= 0 && xx < q.W;
+            pre[j] = inb ? int(__ldg(lat_img + (int64_t(c) * q.H + yy) * q.W + xx)) : int(kNoSpike);
+            w0v[j] = e >= 0 ? wf[e] : 0.0f;
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int e = ev[j];
+            if (e < 0) continue;
+            const float a = (pre[j] != kNoSpike && pre[j] <= post) ? ap : am;
+            const float w0 = w0v[j];
+            const float dw = q.stabilizer ? __fmul_rn(__fmul_rn(a, __fsub_rn(w0, q.lb)), __fsub_rn(q.ub, w0)) : a;
+            float w1 = __fadd_rn(w0, dw);
+            if (q.stabilizer != 2) {
+              w1 = w1 < q.lb ? q.lb : w1;
+              w1 = w1 > q.ub ? q.ub : w1;
+            }
+            wf[e] = w1;
+            const float sx = w1 * 2147483648.0f;
+            uint32_t qq = 0;
+            if (!(w1 >= 0.0f && w1 <= 1.0f) || sx != truncf(sx)) bad = true;
+            else qq = uint32_t(sx);
+#pragma unroll
+            for (int l = 0; l < 4; ++l) limb[l][j >> 2] |= ((qq >> (8 * l)) & 0xFFu) << (8 * (j & 3));
+          }
+#pragma unroll
+          for (int l = 0; l < 4; ++l)
+            *reinterpret_cast<uint4*>(base + tc_off(4 * fl + l, k0, p.N, p.Kt)) =
+                make_uint4(limb[l][0], limb[l][1], limb[l][2], limb[l][3]);
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0) flag_error(q.err, kErrInexact);
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // the limbs are read by the next bulk copies
+      }
+    }
+    tc_grid_barrier(q.bar, gen);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(q.tmem_cols) : "memory");
+  }
+}
+
 size_t rstdp_inf_workspace(int C, int H, int W, int pad, int F, int KH, int KW) {
   const TcPlan p = tc_plan(1, C, H, W, pad, KH, KW, F, num_sms());
   return ((p.b_bytes + 1023) & ~size_t(1023)) + ((size_t(p.M) * F * sizeof(unsigned long long) + 255) & ~size_t(255)) +
-         256 + 1024;
+         256 + 256 + 1024;  // + the persistent kernel's best keys and grid barrier
 }
 
 int rstdp_inf_sequence_launch(const void* prep, int b0, int N, int C, int H, int W, int pad, const uint8_t* lat_in,
@@ -705,6 +974,35 @@ int rstdp_inf_sequence_launch(const void* prep, int b0, int N, int C, int H, int
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_rstdp_inf_sequence: %s", cudaGetErrorString(e));
   const int64_t CHW = int64_t(C) * H * W;
   const int dbg = getenv("SNN_RSTDP_DBG") ? atoi(getenv("SNN_RSTDP_DBG")) : 0;  // timing experiments only
+  {  // one persistent cooperative kernel for all N images when its CTAs fit the GPU -- opt-in
+     // (SNN_RSTDP_PERSIST=1): measured on C4 at 26.6 us per image against 20.0 us for the per-image kernels
+     // below (three software grid barriers per image cost more than two PDL-chained kernel boundaries)
+    const int grid = p.Mt * p.nch * p.KS;
+    int occ = 0;
+    cudaFuncSetAttribute(rstdp_inf_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rstdp_inf_persist_kernel, kTcThreads, smem);
+    const char* pe = getenv("SNN_RSTDP_PERSIST");
+    if (N > 0 && pe && pe[0] == '1' && occ >= 1 && grid <= occ * num_sms()) {
+      unsigned long long* best = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(stp) + 256);
+      unsigned* bar = reinterpret_cast<unsigned*>(best + 2);
+      if (cudaMemsetAsync(best, 0xFF, 2 * sizeof(unsigned long long), s) != cudaSuccess ||
+          cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess)
+        return check_launch("snn_rstdp_inf_sequence memset");
+      PersistArgs q;
+      q.prep = static_cast<const uint8_t*>(prep); q.b0 = b0; q.N = N; q.lat_in = lat_in;
+      q.C = C; q.H = H; q.W = W; q.pad = pad; q.KH = KH; q.KW = KW; q.F = F; q.T = T; q.Ho = Ho; q.Wo = Wo;
+      q.w = w; q.bq = bq; q.part = part; q.best = best; q.bar = bar; q.labels = labels; q.n_classes = n_classes;
+      q.a_plus = a_plus; q.a_minus = a_minus; q.lb = lb; q.ub = ub; q.stabilizer = stabilizer;
+      q.winners = winners; q.count = count; q.decision = decision; q.reward = reward; q.err = err; q.p = p;
+      q.tmem_cols = cols;
+      void* args[] = {&q};
+      e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(rstdp_inf_persist_kernel), dim3(grid),
+                                      dim3(kTcThreads), args, size_t(smem), s);
+      if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_rstdp_inf_sequence: %s", cudaGetErrorString(e));
+      note_launch();
+      return check_launch("snn_rstdp_inf_sequence");
+    }
+  }
   const int MF = p.M * F;
   const int t1 = int(ceil_div(MF, 1024)) < num_sms() ? int(ceil_div(MF, 1024)) : num_sms();  // ~1K neurons per CTA
   const int nk16 = p.K / 16 + (p.K % 16 ? 1 : 0);

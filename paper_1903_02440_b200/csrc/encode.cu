@@ -15,6 +15,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "tc_ptx.cuh"
 
 namespace snn {
 
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(kEncThreads) enc_hist_kernel(const float* __re
 // 4096-bin histogram scanned as 32 runs of 128 bins), resolve or descend, rebuild the sorted list of
 // distinct prefixes for level L+1 and zero their histograms.  gate: as enc_hist_kernel.
 __global__ void __launch_bounds__(1024) enc_select_kernel(int T, int bins, int level, EncodeWS ws,
-                                                          const int32_t* gate) {
+                                                          const int32_t* gate, int zero_next) {
   pdl_begin();
   const int g = blockIdx.x;
   if (gate && !gate[g]) return;
@@ -272,10 +273,11 @@ __global__ void __launch_bounds__(1024) enc_select_kernel(int T, int bins, int l
     if (sl < 0 || csh[b] == -1) continue;  // resolved or empty (warp-uniform)
     const uint32_t* h = (level == 0) ? ws.hist0 + int64_t(g) * kEncBins : ws.hist + (int64_t(g) * S + sl) * kEncBins;
     const uint32_t r = cr[b];
-    const uint4* h4 = reinterpret_cast<const uint4*>(h + lane * 128);
+    const int rl = level == 1 ? kEncL1Bins / 32 : 128;  // bins per lane run (level 1: 256 bins in use)
+    const uint4* h4 = reinterpret_cast<const uint4*>(h + lane * rl);
     uint32_t run = 0;
-#pragma unroll 8
-    for (int q = 0; q < 32; ++q) {
+#pragma unroll 2
+    for (int q = 0; q < rl / 4; ++q) {
       const uint4 x4 = h4[q];
       run += x4.x + x4.y + x4.z + x4.w;
     }
@@ -285,19 +287,32 @@ __global__ void __launch_bounds__(1024) enc_select_kernel(int T, int bins, int l
       const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
       if (lane >= o) inc += y;
     }
-    // the digit holding rank r: the run whose inclusive sum first exceeds r, then a scan inside it
+    // the digit holding rank r: the run whose inclusive sum first exceeds r; then the warp loads that
+    // run's 128 bins (4 per lane, one 16-byte load each) and finds the digit by a second scan
     const unsigned over = __ballot_sync(0xffffffffu, inc > r);
     const int L = __ffs(over) - 1;  // exists: r < the slot's total
-    if (lane == L) {
-      uint32_t c = inc - run;  // exclusive base of this run
+    const uint32_t rbase = __shfl_sync(0xffffffffu, inc - run, L);  // exclusive base of run L
+    const uint4 q4 = lane * 4 < rl ? reinterpret_cast<const uint4*>(h + L * rl)[lane] : make_uint4(0, 0, 0, 0);
+    const uint32_t s4 = q4.x + q4.y + q4.z + q4.w;
+    uint32_t inc2 = s4;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc2, o);
+      if (lane >= o) inc2 += y;
+    }
+    const unsigned over2 = __ballot_sync(0xffffffffu, rbase + inc2 > r);
+    const int L2 = __ffs(over2) - 1;
+    if (lane == L2) {
+      uint32_t c = rbase + inc2 - s4;  // exclusive base of these 4 bins
+      const uint32_t hb[4] = {q4.x, q4.y, q4.z, q4.w};
       int d = 0;
       uint32_t cnt = 0;
-      for (int k = 0; k < 128; ++k) {
-        const uint32_t hk = h[lane * 128 + k];
-        if (c + hk > r) { d = k; cnt = hk; break; }
-        c += hk;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (cnt == 0 && c + hb[k] > r) { d = L2 * 4 + k; cnt = hb[k]; }
+        else if (cnt == 0) c += hb[k];
       }
-      const int dig = L * 128 + d;
+      const int dig = L * rl + d;
       cp[b] = (cp[b] << c_enc_bits[level]) | uint64_t(dig);
       cr[b] = r - c;
       if (cnt == 1 || level == kEncLevels - 1) { csh[b] = c_enc_shift[level]; cs[b] = -1; }
@@ -318,9 +333,14 @@ __global__ void __launch_bounds__(1024) enc_select_kernel(int T, int bins, int l
     s_nslots = n;
   }
   __syncthreads();
-  if (level + 1 < kEncLevels) {
-    uint4* hg = reinterpret_cast<uint4*>(ws.hist + int64_t(g) * S * kEncBins);
-    for (int64_t i = tid; i < int64_t(s_nslots) * kEncBins / 4; i += blockDim.x) hg[i] = make_uint4(0, 0, 0, 0);
+  // zero the next level's histograms: level 1 uses 256 bins per slot; the level-2 histograms are needed
+  // only by the gated fallback, whose images enc_finish_kernel zeroes (zero_next = 0 here)
+  if (level + 1 < kEncLevels && zero_next) {
+    const int nb = level + 1 == 1 ? kEncL1Bins : kEncBins;
+    for (int64_t i = tid; i < int64_t(s_nslots) * nb; i += blockDim.x) {
+      const int64_t sl = i / nb;
+      ws.hist[(int64_t(g) * S + sl) * kEncBins + (i - sl * nb)] = 0;
+    }
   }
 }
 
@@ -497,19 +517,29 @@ __global__ void __launch_bounds__(kEncThreads) enc_assign2_kernel(const float* _
   const float* xg = x + int64_t(g) * n;
   uint8_t* lg = lat + int64_t(g) * n;
   const int shp = c_enc_shift[1];
+  uint32_t tab_a;  // the tables' shared-window address, kept in a register
+  asm volatile("mov.u32 %0, %1;" : "=r"(tab_a) : "r"(smem_u32(tab)));
+  auto ld8 = [&](uint32_t off) {
+    uint16_t r;
+    asm("ld.shared.u8 %0, [%1];" : "=h"(r) : "r"(tab_a + off));
+    return uint32_t(r);
+  };
   auto lat_of = [&](float v, uint32_t i) -> uint8_t {
     if (!(v > 0.0f)) return kNoSpike;
-    const uint64_t K = enc_key(v, i);
     int c;
-    if (tabok) {  // two table lookups (level-0 digit, then its 20-bit prefix)
-      const uint32_t d0 = uint32_t(K >> c_enc_shift[0]);
-      c = tab[d0];
-      if (c == 0xFF) c = tab[2 * kEncBins + int(tab[kEncBins + d0]) * kEncL1Bins + int((K >> shp) & 0xFFu)];
+    if (tabok) {  // two table lookups (level-0 digit, then its 20-bit prefix): value bits only (32-bit)
+      const uint32_t v31 = 0x7FFFFFFFu - __float_as_uint(v);  // key bits 54..24
+      const uint32_t d0 = v31 >> 19;                           // key bits 54..43
+      c = int(ld8(d0));
+      if (c == 0xFF) c = int(ld8(2 * kEncBins + ld8(kEncBins + d0) * kEncL1Bins + ((v31 >> 11) & 0xFFu)));
       if (c == 0xFF) {
-        enc_candidate(ws, g, K);
+        enc_candidate(ws, g, enc_key(v, i));
         return kNoSpike;  // placeholder, rewritten by enc_finish_kernel
       }
-    } else {
+      return c >= T ? kNoSpike : uint8_t(c);
+    }
+    const uint64_t K = enc_key(v, i);
+    {
       if (ns > 0 && enc_slot_of(K >> shp, slp, dmask, ns) >= 0) {
         enc_candidate(ws, g, K);
         return kNoSpike;
@@ -555,25 +585,41 @@ __global__ void __launch_bounds__(kEncThreads) enc_assign2_kernel(const float* _
     const int p0 = tl * kEncTileP;
     const int np = min(kEncTileP, HW - p0);
     if (w4) {
-      const int ncg = C / 4;
-      for (int it = wid; it < ncg * (kEncTileP / 32); it += blockDim.x >> 5) {
-        const int cg = it / (kEncTileP / 32), q = (it - cg * (kEncTileP / 32)) * 32 + lane;
-        if (q < np) {
+      const int ncg = C / 4, nit = ncg * (kEncTileP / 32), nwarp = blockDim.x >> 5;
+      for (int it0 = wid; it0 < nit; it0 += 4 * nwarp) {  // 4 items (16 loads) in flight per lane
+        float v[4][4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int it = it0 + m * nwarp;
+          const int cg = it / (kEncTileP / 32), q = (it - cg * (kEncTileP / 32)) * 32 + lane;
+          const bool ok = it < nit && q < np;
           const int64_t i = int64_t(4 * cg) * HW + p0 + q;
-          float v[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) v[u] = __ldg(xg + i + int64_t(u) * HW);
-          uint32_t w = 0;
+          for (int u = 0; u < 4; ++u) v[m][u] = ok ? __ldg(xg + i + int64_t(u) * HW) : 0.0f;
+        }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) w |= uint32_t(lat_of(v[u], uint32_t(i + int64_t(u) * HW))) << (8 * u);
-          tile32[q * rw + cg] = w;
+        for (int m = 0; m < 4; ++m) {
+          const int it = it0 + m * nwarp;
+          const int cg = it / (kEncTileP / 32), q = (it - cg * (kEncTileP / 32)) * 32 + lane;
+          if (it < nit && q < np) {
+            const int64_t i = int64_t(4 * cg) * HW + p0 + q;
+            uint32_t w = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) w |= uint32_t(lat_of(v[m][u], uint32_t(i + int64_t(u) * HW))) << (8 * u);
+            tile32[q * rw + cg] = w;
+          }
         }
       }
       __syncthreads();
       uint32_t* dst = reinterpret_cast<uint32_t*>(lg + int64_t(p0) * C);
-      for (int k = threadIdx.x; k < np * ncg; k += blockDim.x) {
-        const int p = k / ncg, wdx = k - p * ncg;
-        dst[k] = tile32[p * rw + wdx];
+      if (int(blockDim.x) % ncg == 0) {  // (position, word) advanced by a constant step: no division per word
+        const int wdx = threadIdx.x % ncg, pstep = blockDim.x / ncg;
+        for (int p = threadIdx.x / ncg; p < np; p += pstep) dst[p * ncg + wdx] = tile32[p * rw + wdx];
+      } else {
+        for (int k = threadIdx.x; k < np * ncg; k += blockDim.x) {
+          const int p = k / ncg, wdx = k - p * ncg;
+          dst[k] = tile32[p * rw + wdx];
+        }
       }
     } else {
       for (int it = threadIdx.x; it < C * kEncTileP; it += blockDim.x) {
@@ -611,7 +657,13 @@ __global__ void __launch_bounds__(kEncFinThreads) enc_finish_kernel(int T, int b
   const int S = T, NC = enc_ncuts(T, bins);
   const int nc = ws.ncand[g];  // (zeroed by the launcher before pass 3)
   if (tid == 0) ws.ovf[g] = nc > kEncCandCap ? 1 : 0;
-  if (nc > kEncCandCap || nc == 0) return;
+  if (nc > kEncCandCap) {  // the fallback's level-2 histograms (one per slot of enc_select level 1)
+    const int ns = ws.n_slots[g];
+    uint4* hg = reinterpret_cast<uint4*>(ws.hist + int64_t(g) * S * kEncBins);
+    for (int64_t i = tid; i < int64_t(ns) * kEncBins / 4; i += blockDim.x) hg[i] = make_uint4(0, 0, 0, 0);
+    return;
+  }
+  if (nc == 0) return;
   const int shp = c_enc_shift[1];
   for (int b = tid; b < NC; b += blockDim.x) {
     sp[b] = ws.cut_prefix[int64_t(g) * S + b];
@@ -1005,10 +1057,10 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, u
     // the gated fallback kernels at most 16 CTAs per image (an image not taking them exits at once)
     const dim3 grid0(unsigned(nchunks < 16 ? 1 : nchunks / 16), gn), gridg(unsigned(nchunks < 16 ? nchunks : 16), gn);
     launch_k(enc_hist0_kernel, dim3(grid0), dim3(kEncThreads), 0, s, xg, n, vec, ws);
-    launch_k(enc_select_kernel, dim3(gn), dim3(1024), 0, s, T, bins, 0, ws, (const int32_t*)nullptr);
+    launch_k(enc_select_kernel, dim3(gn), dim3(1024), 0, s, T, bins, 0, ws, (const int32_t*)nullptr, 1);
     launch_k(enc_hist_kernel, dim3(grid0), dim3(kEncThreads), kEncL1MaxSlots * kEncL1Bins * 4, s, xg, n, vec, T, 1, ws,
              (const int32_t*)nullptr);
-    launch_k(enc_select_kernel, dim3(gn), dim3(1024), 0, s, T, bins, 1, ws, (const int32_t*)nullptr);
+    launch_k(enc_select_kernel, dim3(gn), dim3(1024), 0, s, T, bins, 1, ws, (const int32_t*)nullptr, all_levels ? 1 : 0);
     note_launch(4);
     if (!all_levels) {
       launch_k(enc_tables_kernel, dim3(gn), dim3(1024), 0, s, T, bins, ws);
@@ -1029,7 +1081,7 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, u
     }
     for (int L = 2; L < kEncLevels; ++L) {
       launch_k(enc_hist_kernel, dim3(gate ? gridg : grid), dim3(kEncThreads), 0, s, xg, n, vec, T, L, ws, gate);
-      launch_k(enc_select_kernel, dim3(gn), dim3(1024), 0, s, T, bins, L, ws, gate);
+      launch_k(enc_select_kernel, dim3(gn), dim3(1024), 0, s, T, bins, L, ws, gate, 1);
       note_launch(2);
     }
     launch_k(enc_assign_kernel, dim3(gate ? gridg : grid), dim3(kEncThreads), 0, s, xg, n, T, bins, lg, ws, eo, gate);

@@ -1,7 +1,8 @@
 """f1 for theta = +inf: snn_rstdp_inf_sequence vs the oracle chain image by image
 (conv Eq. 5 -> k-WTA k = 1 -> decide -> R-STDP, Eq. 4): every winner,
 decision, reward and the final weights bit-exact, with silent images, labels = NULL (no plasticity),
-both clamp variants and a split-K GEMM (one-image plan)."""
+both clamp variants and a split-K GEMM (one-image plan); the persistent one-launch kernel and the
+per-image kernels."""
 import numpy as np
 import pytest
 import torch
@@ -43,7 +44,12 @@ def oracle_chain(orc, lat_in, w, pad, T, labels, n_classes, ap, am, lb, ub, stab
     ((4, 3, 8, 8, 1, 12, 3, 3, 7), 4, 2, 0.0, 1.0, True),         # stabilized, no clamp (A20 variant)
     ((3, 4, 10, 10, 0, 16, 5, 5, 9), 2, 1, 0.0, 1.0, False),      # labels NULL: decisions, no plasticity
 ])
-def test_rstdp_inf_sequence_vs_oracle(G, orc, shape, n_cls, stab, lb, ub, use_labels):
+@pytest.mark.parametrize("path", ["persistent", "percall"])
+def test_rstdp_inf_sequence_vs_oracle(G, orc, shape, n_cls, stab, lb, ub, use_labels, path, monkeypatch):
+    """persistent = one cooperative kernel for the whole chain (SNN_RSTDP_PERSIST=1); percall = the default
+    per-image GEMM + two tail kernels"""
+    if path == "persistent":
+        monkeypatch.setenv("SNN_RSTDP_PERSIST", "1")
     N, C, H, W, pad, F, KH, KW, T = shape
     rng = np.random.default_rng(sum(shape) + stab)
     import synth
