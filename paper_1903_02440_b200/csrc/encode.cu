@@ -585,28 +585,34 @@ __global__ void __launch_bounds__(kEncThreads) enc_assign2_kernel(const float* _
     const int p0 = tl * kEncTileP;
     const int np = min(kEncTileP, HW - p0);
     if (w4) {
-      const int ncg = C / 4, nit = ncg * (kEncTileP / 32), nwarp = blockDim.x >> 5;
-      for (int it0 = wid; it0 < nit; it0 += 4 * nwarp) {  // 4 items (16 loads) in flight per lane
-        float v[4][4];
+      const int ncg = C / 4, nwarp = blockDim.x >> 5;
+      // one warp per 4-channel group: lane l takes positions 4l .. 4l + 3 of the tile, one float4 per
+      // channel (vec) -- 16 elements from 4 loads, 4 packed words to the tile
+      const bool v4 = vec && (HW % 4 == 0);
+      for (int cg = wid; cg < ncg; cg += nwarp) {
+        const int q = lane * 4;
+        if (q < np) {
+          float v[4][4];  // [channel][position]
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const int it = it0 + m * nwarp;
-          const int cg = it / (kEncTileP / 32), q = (it - cg * (kEncTileP / 32)) * 32 + lane;
-          const bool ok = it < nit && q < np;
-          const int64_t i = int64_t(4 * cg) * HW + p0 + q;
+          for (int u = 0; u < 4; ++u) {
+            const float* src = xg + int64_t(4 * cg + u) * HW + p0 + q;
+            if (v4 && q + 3 < np) {
+              const float4 f = __ldg(reinterpret_cast<const float4*>(src));
+              v[u][0] = f.x; v[u][1] = f.y; v[u][2] = f.z; v[u][3] = f.w;
+            } else {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) v[m][u] = ok ? __ldg(xg + i + int64_t(u) * HW) : 0.0f;
-        }
+              for (int j = 0; j < 4; ++j) v[u][j] = (q + j < np) ? __ldg(src + j) : 0.0f;
+            }
+          }
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const int it = it0 + m * nwarp;
-          const int cg = it / (kEncTileP / 32), q = (it - cg * (kEncTileP / 32)) * 32 + lane;
-          if (it < nit && q < np) {
-            const int64_t i = int64_t(4 * cg) * HW + p0 + q;
-            uint32_t w = 0;
+          for (int j = 0; j < 4; ++j) {
+            if (q + j < np) {
+              uint32_t w = 0;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) w |= uint32_t(lat_of(v[m][u], uint32_t(i + int64_t(u) * HW))) << (8 * u);
-            tile32[q * rw + cg] = w;
+              for (int u = 0; u < 4; ++u)
+                w |= uint32_t(lat_of(v[u][j], uint32_t(int64_t(4 * cg + u) * HW + p0 + q + j))) << (8 * u);
+              tile32[(q + j) * rw + cg] = w;
+            }
           }
         }
       }
