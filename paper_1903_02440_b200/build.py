@@ -36,13 +36,16 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False, extra=()) -> str:
+def build(force: bool = False, verbose: bool = False, extra=(), out: str = None) -> str:
+    """out: another library path (e.g. the checked build, tools/build_checked.sh) -- objects go to their own
+    directory, the in-tree libsnn.so is not touched."""
     env_extra = os.environ.get("SNN_NVCC_EXTRA", "").split()  # tuning experiments, e.g. -DSNN_SORT_UNROLL=8
     if env_extra:
         extra, force = list(extra) + env_extra, True
-    if not force and not needs_build():
+    lib = out or LIB
+    if out is None and not force and not needs_build():
         return LIB
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build" if out is None else "build_" + os.path.splitext(os.path.basename(out))[0])
     os.makedirs(objdir, exist_ok=True)
 
     def compile_one(src):
@@ -57,15 +60,18 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=8) as ex:
         objs = list(ex.map(compile_one, _sources()))
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True,
-                extra=["-Xptxas", "-v"] if "--ptxas" in sys.argv else []))
+    if "--checked" in sys.argv:  # device bounds checks (SNN_DCHECK) in a separate library, libsnn_checked.so
+        print(build(force=True, verbose=True, extra=["-DSNN_CHECKED"], out=os.path.join(PKG, "libsnn_checked.so")))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True,
+                    extra=["-Xptxas", "-v"] if "--ptxas" in sys.argv else []))

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "../../include/snn.h"
 
@@ -25,6 +26,25 @@ int num_sms();  // multiprocessor count of the current device (cached per device
 void note_launch(int n = 1);  // diagnostic kernel-launch counter (snn_launch_count)
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Device bounds checks of the checked build (python -m paper_1903_02440_b200.build --checked ->
+// libsnn_checked.so, run by tools/gpu_checked.sh): an index outside its buffer prints the condition
+// and traps the launch.  Compiled out of the product library.  (Stands in for compute-sanitizer,
+// which is closed on this GPU pool.)
+#ifdef SNN_CHECKED
+#define SNN_DCHECK(cond)                                                                         \
+  do {                                                                                           \
+    if (!(cond)) {                                                                               \
+      printf("SNN_CHECKED %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond,         \
+             int(blockIdx.x), int(threadIdx.x));                                                 \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+#else
+#define SNN_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 // Total-order key of a float (ascending order of value), then complemented by callers that want
 // descending order.  v >= 0 for every potential this library produces.

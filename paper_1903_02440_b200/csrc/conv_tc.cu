@@ -379,6 +379,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
             const int64_t acc = int64_t(v[4 * j]) + (int64_t(v[4 * j + 1]) << 8) + (int64_t(v[4 * j + 2]) << 16) +
                                 (int64_t(v[4 * j + 3]) << 24);
             if (part) {  // split-K: exact partial sum of this K slice
+              SNN_DCHECK(m < p.M && f < F);
               atomicAdd(part + int64_t(m) * F + f, (unsigned long long)acc);
               continue;
             }
@@ -530,6 +531,72 @@ struct RstdpState {
   float rw;                 // its reward (+1, -1, 0 = no plasticity)
 };
 
+// Eq. 4 on one 16-column group k0 = 16 g16 of the winner f's GEMM columns (post = T - 1, Eq. 5; the
+// snn_stdp_update arithmetic, R17-R22): the 16 weights' updates, then the four 16-byte limb rows of that
+// core-matrix column (the tc_prep_b16 layout) -- every load issued before any use.  Returns true if a
+// new weight left the exact domain.
+__device__ __forceinline__ bool rstdp_eq4_group(int g16, int f, int y, int x, float ap, float am, int post,
+                                                const uint8_t* __restrict__ lat_img, int C, int H, int W, int KH,
+                                                int KW, int pad, float* __restrict__ w, uint8_t* __restrict__ bq,
+                                                const TcPlan& p, float lb, float ub, int stabilizer) {
+  const int KK = KH * KW, R = C * KK;
+  float* wf = w + int64_t(f) * R;
+  const int ch = f / p.Fc, fl = f - ch * p.Fc;
+  uint8_t* base = bq + size_t(ch) * p.Kt * p.N * kTcKT;
+  bool bad = false;
+  const int k0 = g16 * 16;
+  uint32_t limb[4][4] = {};
+  const int kyx = p.hwc ? k0 / p.Cp : 0, c0 = p.hwc ? k0 - kyx * p.Cp : 0;
+  int ev[16], pre[16];
+  float w0v[16];
+  // (c, ky, kx) of column k0 by divisions once, then stepped column by column
+  int cc, kyy, kxx;
+  if (p.hwc) { cc = c0; kyy = kyx / KW; kxx = kyx - kyy * KW; }
+  else { cc = k0 / KK; const int rr = k0 - cc * KK; kyy = rr / KW; kxx = rr - kyy * KW; }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    int e = -1;
+    const int c = cc, ky = kyy, kx = kxx;
+    if (p.hwc) {  // column k = kyx Cp + c (channels padded to Cp)
+      if (c < C) e = c * KK + kyx;
+      ++cc;
+    } else {      // column k = e = (c KH + ky) KW + kx
+      if (k0 + j < R) e = k0 + j;
+      if (++kxx == KW) { kxx = 0; if (++kyy == KH) { kyy = 0; ++cc; } }
+    }
+    ev[j] = e;
+    const int yy = y + ky - pad, xx = x + kx - pad;
+    const bool inb = e >= 0 && yy >= 0 && yy < H && xx >= 0 && xx < W;
+    pre[j] = inb ? int(__ldg(lat_img + (int64_t(c) * H + yy) * W + xx)) : int(kNoSpike);
+    w0v[j] = e >= 0 ? wf[e] : 0.0f;
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int e = ev[j];
+    if (e < 0) continue;
+    const float a = (pre[j] != kNoSpike && pre[j] <= post) ? ap : am;
+    const float w0 = w0v[j];
+    const float dw = stabilizer ? __fmul_rn(__fmul_rn(a, __fsub_rn(w0, lb)), __fsub_rn(ub, w0)) : a;
+    float w1 = __fadd_rn(w0, dw);
+    if (stabilizer != 2) {
+      w1 = w1 < lb ? lb : w1;
+      w1 = w1 > ub ? ub : w1;
+    }
+    wf[e] = w1;
+    const float sx = w1 * 2147483648.0f;
+    uint32_t q = 0;
+    if (!(w1 >= 0.0f && w1 <= 1.0f) || sx != truncf(sx)) bad = true;
+    else q = uint32_t(sx);
+#pragma unroll
+    for (int l = 0; l < 4; ++l) limb[l][j >> 2] |= ((q >> (8 * l)) & 0xFFu) << (8 * (j & 3));
+  }
+#pragma unroll
+  for (int l = 0; l < 4; ++l)
+    *reinterpret_cast<uint4*>(base + tc_off(4 * fl + l, k0, p.N, p.Kt)) =
+        make_uint4(limb[l][0], limb[l][1], limb[l][2], limb[l][3]);
+  return bad;
+}
+
 // Tail 1: CTAs share the M x F partial sums (each reads and clears its slice and offers its minimum key,
 // lat = T - 1 and v = fp32(P) descending, then flat index f H W + y W + x ascending: the snn_k_winners
 // order, R13/R14); the last CTA to finish decides (snn_decide's block decision_map, R24/R25) and
@@ -568,100 +635,47 @@ __global__ void __launch_bounds__(256) rstdp_inf_tail1_kernel(
   }
   __syncthreads();
   if (!s_last || tid != 0) return;
-  __threadfence();
-  const uint64_t k = atomicExch(&st->best, ~0ull);  // read and reset for the next image
-  st->ticket = 0;
-  int f = -1, y = -1, x = -1, d = -1;
-  float rw = 0.0f;
-  if (k != ~0ull) {
-    const int idx = int(k & 0xFFFFFFu);
-    f = idx / M;
-    const int pos = idx - f * M;
-    y = pos / Wo;
-    x = pos - y * Wo;
-    d = f / (F / n_classes);
-    if (labels) rw = (d == labels[b]) ? 1.0f : -1.0f;
+  {
+    __threadfence();
+    const uint64_t k = atomicExch(&st->best, ~0ull);  // read and reset for the next image
+    st->ticket = 0;
+    int f = -1, y = -1, x = -1, d = -1;
+    float rw = 0.0f;
+    if (k != ~0ull) {
+      const int idx = int(k & 0xFFFFFFu);
+      f = idx / M;
+      const int pos = idx - f * M;
+      y = pos / Wo;
+      x = pos - y * Wo;
+      d = f / (F / n_classes);
+      if (labels) rw = (d == labels[b]) ? 1.0f : -1.0f;
+    }
+    winners[0] = f; winners[1] = y; winners[2] = x;
+    count[0] = f >= 0 ? 1 : 0;
+    if (decision) decision[0] = d;
+    if (reward) reward[0] = rw;
+    st->f = f; st->y = y; st->x = x; st->rw = rw;
+    if ((dbg & 8) && b < 4096) g_rstdp_stamps[4 * b + 1] = globaltimer_ns();
   }
-  winners[0] = f; winners[1] = y; winners[2] = x;
-  count[0] = f >= 0 ? 1 : 0;
-  if (decision) decision[0] = d;
-  if (reward) reward[0] = rw;
-  st->f = f; st->y = y; st->x = x; st->rw = rw;
-  if ((dbg & 8) && b < 4096) g_rstdp_stamps[4 * b + 1] = globaltimer_ns();
 }
 
-// Tail 2: Eq. 4 on the winner's weights (post = T - 1, Eq. 5; the snn_stdp_update arithmetic, R17-R22)
-// and the re-quantisation of only that feature's B limbs: one thread per 16 consecutive GEMM columns k
-// -- the 16 weights' updates, then the four 16-byte limb rows of that core-matrix column (the
-// tc_prep_b16 layout); every load is issued before any use.
+// Tail 2: Eq. 4 on the winner's weights and the re-quantisation of only that feature's B limbs, one
+// thread per 16 consecutive GEMM columns (rstdp_eq4_group).  Spread over several CTAs: measured on C4,
+// 8.5 us as its own kernel against 11.8 us inside tail 1's last CTA.
 __global__ void __launch_bounds__(128) rstdp_inf_tail2_kernel(
     const RstdpState* __restrict__ st, int T, const uint8_t* __restrict__ lat_img, int C, int H, int W, int KH,
     int KW, int pad, float* __restrict__ w, uint8_t* __restrict__ bq, TcPlan p, float a_plus, float a_minus,
     float lb, float ub, int stabilizer, int* err, int b, int dbg) {
   pdl_begin();
-  const int f = st->f, y = st->y, x = st->x;
+  const int f = st->f;
   const float rw = st->rw;
   if (f < 0 || rw == 0.0f) return;
   const float ap = rw > 0.0f ? a_plus : -a_plus, am = rw > 0.0f ? a_minus : -a_minus;
-  const int KK = KH * KW, R = C * KK, post = T - 1;
-  float* wf = w + int64_t(f) * R;
-  const int ch = f / p.Fc, fl = f - ch * p.Fc;
-  uint8_t* base = bq + size_t(ch) * p.Kt * p.N * kTcKT;
-  bool bad = false;
   const int nk16 = p.K / 16 + (p.K % 16 ? 1 : 0);
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < nk16) {
-    const int k0 = g * 16;
-    uint32_t limb[4][4] = {};
-    const int kyx = p.hwc ? k0 / p.Cp : 0, c0 = p.hwc ? k0 - kyx * p.Cp : 0;
-    int ev[16], pre[16];
-    float w0v[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      int e = -1, c = 0, ky = 0, kx = 0;
-      if (p.hwc) {  // column k = kyx Cp + c (channels padded to Cp)
-        c = c0 + j;
-        ky = kyx / KW; kx = kyx - ky * KW;
-        if (c < C) e = c * KK + kyx;
-      } else {      // column k = e = (c KH + ky) KW + kx
-        if (k0 + j < R) {
-          e = k0 + j;
-          c = e / KK;
-          const int rr = e - c * KK;
-          ky = rr / KW; kx = rr - ky * KW;
-        }
-      }
-      ev[j] = e;
-      const int yy = y + ky - pad, xx = x + kx - pad;
-      const bool inb = e >= 0 && yy >= 0 && yy < H && xx >= 0 && xx < W;
-      pre[j] = inb ? int(__ldg(lat_img + (int64_t(c) * H + yy) * W + xx)) : int(kNoSpike);
-      w0v[j] = e >= 0 ? wf[e] : 0.0f;
-    }
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int e = ev[j];
-      if (e < 0) continue;
-      const float a = (pre[j] != kNoSpike && pre[j] <= post) ? ap : am;
-      const float w0 = w0v[j];
-      const float dw = stabilizer ? __fmul_rn(__fmul_rn(a, __fsub_rn(w0, lb)), __fsub_rn(ub, w0)) : a;
-      float w1 = __fadd_rn(w0, dw);
-      if (stabilizer != 2) {
-        w1 = w1 < lb ? lb : w1;
-        w1 = w1 > ub ? ub : w1;
-      }
-      wf[e] = w1;
-      const float sx = w1 * 2147483648.0f;
-      uint32_t q = 0;
-      if (!(w1 >= 0.0f && w1 <= 1.0f) || sx != truncf(sx)) bad = true;
-      else q = uint32_t(sx);
-#pragma unroll
-      for (int l = 0; l < 4; ++l) limb[l][j >> 2] |= ((q >> (8 * l)) & 0xFFu) << (8 * (j & 3));
-    }
-#pragma unroll
-    for (int l = 0; l < 4; ++l)
-      *reinterpret_cast<uint4*>(base + tc_off(4 * fl + l, k0, p.N, p.Kt)) =
-          make_uint4(limb[l][0], limb[l][1], limb[l][2], limb[l][3]);
-  }
+  bool bad = false;
+  if (g < nk16) bad = rstdp_eq4_group(g, f, st->y, st->x, ap, am, T - 1, lat_img, C, H, W, KH, KW, pad, w, bq, p, lb,
+                                      ub, stabilizer);
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flag_error(err, kErrInexact);
   if ((dbg & 8) && blockIdx.x == 0 && threadIdx.x == 0 && b < 4096) g_rstdp_stamps[4 * b + 2] = globaltimer_ns();
 }
@@ -673,7 +687,7 @@ __global__ void __launch_bounds__(128) rstdp_inf_tail2_kernel(
 // counters run on across images), exact int64 partial sums added into part[M][F]; B) every CTA reads and
 // clears a slice of part, takes its minimum key (the snn_k_winners order) and folds it into the image's
 // best key (double-buffered: best[i & 1]); C) every CTA decodes the winner and decision, and applies
-// Eq. 4 to its share of the winner's 16-column groups (w and the B limbs, as rstdp_inf_tail2_kernel).
+// Eq. 4 to its share of the winner's 16-column groups (w and the B limbs, rstdp_eq4_group).
 // Bit-identical to the per-image kernels; no launch or host round trip per image.
 struct PersistArgs {
   const uint8_t* prep;            // snn_conv_inf_prepare A blocks
@@ -732,7 +746,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rstdp_inf_persist_kernel(const 
   const int ksi = int(blockIdx.x % unsigned(p.KS)), tile = int(blockIdx.x / unsigned(p.KS));
   const int ch = tile % p.nch, mt = tile / p.nch;
   const int kt0 = int(int64_t(ksi) * p.Kt / p.KS), kt1 = int(int64_t(ksi + 1) * p.Kt / p.KS);
-  const int F = q.F, HoWo = q.Ho * q.Wo, M = p.M, MF = M * F;
+  const int F = q.F, M = p.M, MF = M * F;
   if (tid == 0) {
     for (int s = 0; s < kTcStages; ++s) {
       mbar_init(smem_u32(&full_bar[s]), 1);
@@ -754,7 +768,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) rstdp_inf_persist_kernel(const 
   unsigned gen = 0;
   int it0 = 0;  // pipeline stages consumed before this image (counters run on across images)
   const int nk = kt1 - kt0;
-  const int KK = q.KH * q.KW, R = q.C * KK, post = q.T - 1;
+  const int post = q.T - 1;
   const int nk16 = p.K / 16 + (p.K % 16 ? 1 : 0);
   const int64_t CHW = int64_t(q.C) * q.H * q.W;
   for (int i = 0; i < q.N; ++i) {
@@ -866,61 +880,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) rstdp_inf_persist_kernel(const 
       }
       if (f >= 0 && rw != 0.0f) {
         const float ap = rw > 0.0f ? q.a_plus : -q.a_plus, am = rw > 0.0f ? q.a_minus : -q.a_minus;
-        float* wf = q.w + int64_t(f) * R;
-        const int chw = f / p.Fc, fl = f - chw * p.Fc;
-        uint8_t* base = q.bq + size_t(chw) * p.Kt * p.N * kTcKT;
         const uint8_t* lat_img = q.lat_in + int64_t(i) * CHW;
         bool bad = false;
-        for (int g16 = int(blockIdx.x) * blockDim.x + tid; g16 < nk16; g16 += gridDim.x * blockDim.x) {
-          const int k0 = g16 * 16;
-          uint32_t limb[4][4] = {};
-          const int kyx = p.hwc ? k0 / p.Cp : 0, c0 = p.hwc ? k0 - kyx * p.Cp : 0;
-          int ev[16], pre[16];
-          float w0v[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            int e = -1, c = 0, ky = 0, kx = 0;
-            if (p.hwc) {
-              c = c0 + j;
-              ky = kyx / q.KW; kx = kyx - ky * q.KW;
-              if (c < q.C) e = c * KK + kyx;
-            } else if (k0 + j < R) {
-              e = k0 + j;
-              c = e / KK;
-              const int rr = e - c * KK;
-              ky = rr / q.KW; kx = rr - ky * q.KW;
-            }
-            ev[j] = e;
-            const int yy = y + ky - q.pad, xx = x + kx - q.pad;
-            const bool inb = e >= 0 && yy >= 0 && yy < q.H && xx >= 0 && xx < q.W;
-            pre[j] = inb ? int(__ldg(lat_img + (int64_t(c) * q.H + yy) * q.W + xx)) : int(kNoSpike);
-            w0v[j] = e >= 0 ? wf[e] : 0.0f;
-          }
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int e = ev[j];
-            if (e < 0) continue;
-            const float a = (pre[j] != kNoSpike && pre[j] <= post) ? ap : am;
-            const float w0 = w0v[j];
-            const float dw = q.stabilizer ? __fmul_rn(__fmul_rn(a, __fsub_rn(w0, q.lb)), __fsub_rn(q.ub, w0)) : a;
-            float w1 = __fadd_rn(w0, dw);
-            if (q.stabilizer != 2) {
-              w1 = w1 < q.lb ? q.lb : w1;
-              w1 = w1 > q.ub ? q.ub : w1;
-            }
-            wf[e] = w1;
-            const float sx = w1 * 2147483648.0f;
-            uint32_t qq = 0;
-            if (!(w1 >= 0.0f && w1 <= 1.0f) || sx != truncf(sx)) bad = true;
-            else qq = uint32_t(sx);
-#pragma unroll
-            for (int l = 0; l < 4; ++l) limb[l][j >> 2] |= ((qq >> (8 * l)) & 0xFFu) << (8 * (j & 3));
-          }
-#pragma unroll
-          for (int l = 0; l < 4; ++l)
-            *reinterpret_cast<uint4*>(base + tc_off(4 * fl + l, k0, p.N, p.Kt)) =
-                make_uint4(limb[l][0], limb[l][1], limb[l][2], limb[l][3]);
-        }
+        for (int g16 = int(blockIdx.x) * blockDim.x + tid; g16 < nk16; g16 += gridDim.x * blockDim.x)
+          bad |= rstdp_eq4_group(g16, f, y, x, ap, am, post, lat_img, q.C, q.H, q.W, q.KH, q.KW, q.pad, q.w, q.bq, p,
+                                 q.lb, q.ub, q.stabilizer);
         if (__any_sync(0xffffffffu, bad) && lane == 0) flag_error(q.err, kErrInexact);
         asm volatile("fence.proxy.async.global;" ::: "memory");  // the limbs are read by the next bulk copies
       }

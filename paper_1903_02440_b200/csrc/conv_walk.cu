@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(512) rf_sort_kernel(const WalkArgs a) {
       uint16_t* hdr = reinterpret_cast<uint16_t*>(rec);
       for (int t = gl; t <= a.T; t += LPP) hdr[t] = start[t];
       const int n4 = (((int(start[a.T]) & -a.pad_unit) + kIt - 1) / kIt) * (kIt / 4);  // uint4 per walk iteration
+      SNN_DCHECK(a.hdr + n4 * 16 <= a.rec && q < a.np);
       const uint4* src = reinterpret_cast<const uint4*>(list);
       uint4* dst = reinterpret_cast<uint4*>(rec + a.hdr);
       for (int k = gl; k < n4; k += LPP) dst[k] = src[k];

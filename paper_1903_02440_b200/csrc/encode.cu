@@ -531,7 +531,11 @@ __global__ void __launch_bounds__(kEncThreads) enc_assign2_kernel(const float* _
       const uint32_t v31 = 0x7FFFFFFFu - __float_as_uint(v);  // key bits 54..24
       const uint32_t d0 = v31 >> 19;                           // key bits 54..43
       c = int(ld8(d0));
-      if (c == 0xFF) c = int(ld8(2 * kEncBins + ld8(kEncBins + d0) * kEncL1Bins + ((v31 >> 11) & 0xFFu)));
+      SNN_DCHECK(d0 < uint32_t(kEncBins));
+      if (c == 0xFF) {
+        SNN_DCHECK(ld8(kEncBins + d0) < uint32_t(kEncL1MaxSlots));
+        c = int(ld8(2 * kEncBins + ld8(kEncBins + d0) * kEncL1Bins + ((v31 >> 11) & 0xFFu)));
+      }
       if (c == 0xFF) {
         enc_candidate(ws, g, enc_key(v, i));
         return kNoSpike;  // placeholder, rewritten by enc_finish_kernel
@@ -576,21 +580,26 @@ __global__ void __launch_bounds__(kEncThreads) enc_assign2_kernel(const float* _
   // warp's 32 positions), packs their latencies in one word and stores it to a tile row padded to an odd
   // word count (conflict-free); the tile then leaves as whole words.  Otherwise byte-wise, rows of C + 1.
   const int HW = eo.hw, C = eo.c;
-  const int ntiles = (HW + kEncTileP - 1) / kEncTileP;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const bool w4 = (C % 4 == 0) && (reinterpret_cast<uintptr_t>(lg) & 3) == 0;
+  // w4: a warp covers 128 positions of one 4-channel group; with fewer groups than warps the tile grows
+  // to 128 x (warps per group) positions so every warp has work (C4: C = 4, 1024-position tiles)
+  const int ncg4 = C / 4, nwarp4 = int(blockDim.x >> 5);
+  const int wpg = (w4 && ncg4 < nwarp4) ? nwarp4 / ncg4 : 1;
+  const int TP = kEncTileP * wpg;
+  const int ntiles = (HW + TP - 1) / TP;
   const int rw = w4 ? C / 4 + 1 : 0;                 // tile row stride in words (w4)
   uint32_t* tile32 = reinterpret_cast<uint32_t*>(tile);
   for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-    const int p0 = tl * kEncTileP;
-    const int np = min(kEncTileP, HW - p0);
+    const int p0 = tl * TP;
+    const int np = min(TP, HW - p0);
     if (w4) {
       const int ncg = C / 4, nwarp = blockDim.x >> 5;
       // one warp per 4-channel group: lane l takes positions 4l .. 4l + 3 of the tile, one float4 per
       // channel (vec) -- 16 elements from 4 loads, 4 packed words to the tile
       const bool v4 = vec && (HW % 4 == 0);
-      for (int cg = wid; cg < ncg; cg += nwarp) {
-        const int q = lane * 4;
+      for (int it = wid; it < ncg * wpg; it += nwarp) {
+        const int cg = it / wpg, q = (it - cg * wpg) * kEncTileP + lane * 4;
         if (q < np) {
           float v[4][4];  // [channel][position]
 #pragma unroll
@@ -678,6 +687,7 @@ __global__ void __launch_bounds__(kEncFinThreads) enc_finish_kernel(int T, int b
   }
   int np2 = 1;
   while (np2 < nc) np2 <<= 1;
+  SNN_DCHECK(np2 <= kEncCandCap);
   for (int i = tid; i < np2; i += blockDim.x) ck[i] = i < nc ? ws.cand[int64_t(g) * kEncCandCap + i] : ~uint64_t(0);
   __syncthreads();
   for (int k = 2; k <= np2; k <<= 1)
@@ -1075,9 +1085,11 @@ int encode_launch(const float* x, int B, int C, int H, int W, int T, int bins, u
     const int32_t* gate = nullptr;
     if (!all_levels) {
       // grid-stride pass 3: about 8 chunks (or tiles) per CTA, so the per-CTA table loads stay small
-      const int64_t units = eo.hw ? ceil_div(eo.hw, kEncTileP) : nchunks;
+      const int wpg = (eo.c % 4 == 0 && eo.c / 4 < kEncThreads / 32) ? (kEncThreads / 32) / (eo.c / 4) : 1;
+      const int64_t units = eo.hw ? ceil_div(eo.hw, int64_t(kEncTileP) * wpg) : nchunks;
       dim3 g3(unsigned(units < 8 ? 1 : units / 8), gn);
-      const int tile_bytes = eo.hw ? kEncTileP * (eo.c + 4) : 0;  // rows padded (see enc_assign2_kernel)
+      // the channels-last tile: rows padded (see enc_assign2_kernel), 128 x wpg positions when C % 4 == 0
+      const int tile_bytes = eo.hw ? (eo.c % 4 == 0 ? kEncTileP * wpg * (eo.c + 4) : kEncTileP * (eo.c + 1)) : 0;
       if (cudaFuncSetAttribute(enc_assign2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_bytes) != cudaSuccess)
         return check_launch("snn_encode(assign attr)");
       launch_k(enc_assign2_kernel, dim3(g3), dim3(kEncThreads), tile_bytes, s, xg, n, vec, T, bins, lg, ws, eo);

@@ -288,6 +288,37 @@ __global__ void __launch_bounds__(256) pool_nhwc2nhwc_kernel(const uint8_t* __re
   }
 }
 
+// Latencies only, channels-last in and out, F not a multiple of 4 (C2: F = 30 and 250): one warp per
+// output pixel, lanes over its F contiguous features (coalesced byte runs, no per-byte index
+// arithmetic), the min over the window's runs.  Windows inside the input (R10) or truncated (Eq. 3).
+__global__ void __launch_bounds__(256) pool_nhwc_lat_rows_kernel(const uint8_t* __restrict__ lat, int B, int F,
+                                                                 int H, int W, int PH, int PW, int SH, int SW, int DH,
+                                                                 int DW, int Ho, int Wo,
+                                                                 uint8_t* __restrict__ lat_out) {
+  pdl_begin();
+  const int lane = threadIdx.x & 31;
+  const int64_t npix = int64_t(B) * Ho * Wo;
+  const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t pix = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); pix < npix; pix += wstride) {
+    const int b = int(pix / (int64_t(Ho) * Wo));
+    const int rem = int(pix - int64_t(b) * Ho * Wo);
+    const int oy = rem / Wo, ox = rem - (rem / Wo) * Wo;
+    const int y0 = oy * SH - DH, x0 = ox * SW - DW;
+    const int ya = y0 < 0 ? 0 : y0, yb = (y0 + PH < H ? y0 + PH : H);
+    const int xa = x0 < 0 ? 0 : x0, xb = (x0 + PW < W ? x0 + PW : W);
+    const uint8_t* img = lat + int64_t(b) * H * W * F;
+    uint8_t* out = lat_out + pix * F;
+    for (int f = lane; f < F; f += 32) {
+      unsigned m = kNoSpike;
+      for (int yy = ya; yy < yb; ++yy) {
+        const uint8_t* row = img + (int64_t(yy) * W + xa) * F + f;
+        for (int xx = xa; xx < xb; ++xx, row += F) m = min(m, unsigned(__ldg(row)));
+      }
+      out[f] = uint8_t(m);
+    }
+  }
+}
+
 int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, int PH, int PW, int SH, int SW,
                 int DH, int DW, int flags, uint8_t* lat_out, float* v_out, cudaStream_t s) {
   // R10 (windows inside the padded input), or Eq. 3 literally (last window truncated at the edge)
@@ -306,6 +337,14 @@ int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, 
     const int vf = (flags & SNN_POOL_VFINAL) ? 1 : 0;
     if (flags & SNN_POOL_OUT_NHWC) {
       if (total >= (int64_t(1) << 32)) return set_error(SNN_ESHAPE, "snn_pool(NHWC output): B*Ho*Wo*F >= 2^32");
+      if (vec == 1 && !vin && !getenv("SNN_POOL_NOROWS")) {  // latencies only, F % 4 != 0: a warp per pixel
+        int64_t nb = ceil_div(int64_t(B) * Ho * Wo, 8);
+        if (nb > int64_t(num_sms()) * 16) nb = int64_t(num_sms()) * 16;
+        launch_k(pool_nhwc_lat_rows_kernel, dim3(unsigned(nb)), dim3(256), 0, s, lat, B, F, H, W, PH, PW, SH, SW, DH,
+                 DW, Ho, Wo, lat_out);
+        note_launch();
+        return check_launch("snn_pool(NHWC rows)");
+      }
       int64_t nb = ceil_div(total / vec, 256);
       if (nb > int64_t(num_sms()) * 16) nb = int64_t(num_sms()) * 16;
       if (vec == 4)
@@ -762,6 +801,7 @@ __global__ void __launch_bounds__(kKwtaThreads) kwta_rounds_kernel(const uint8_t
       const int qn = s_qn < kKwtaQueue ? s_qn : kKwtaQueue;
       for (int qi = wid; qi < qn; qi += nwarps) {
         const int p = queue[qi];
+        SNN_DCHECK(p >= 0 && p < HW);
         uint64_t key = ~uint64_t(0);
         for (int f0 = lane; f0 < F; f0 += 32 * 8) {  // 8 strided latency loads in flight per lane
           uint8_t l[8];

@@ -213,7 +213,11 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl
 #pragma unroll kSortUnroll
     for (int e = gl; e < R; e += LPP) {
       const int l = lat_of(e);
-      if (l <= tcut) list[atomicAdd(&cnt[l], 1u)] = uint32_t(e) * rb;
+      if (l <= tcut) {
+        const uint32_t slot = atomicAdd(&cnt[l], 1u);
+        SNN_DCHECK(slot < uint32_t(list_cap(R, T)));
+        list[slot] = uint32_t(e) * rb;
+      }
     }
 #endif
   }
@@ -608,6 +612,10 @@ __device__ __forceinline__ void walk_list(const WalkArgs& a, const unsigned char
       asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                    : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "r"(ebase + uint32_t((k + 4 * q) * 4)));
       off[4 * q] = c.x; off[4 * q + 1] = c.y; off[4 * q + 2] = c.z; off[4 * q + 3] = c.w;
+#ifdef SNN_CHECKED
+      for (int u = 0; u < 4; ++u)
+        SNN_DCHECK(off[4 * q + u] <= uint32_t(a.R) * uint32_t(a.row_bytes) && off[4 * q + u] % uint32_t(a.row_bytes) == 0);
+#endif
     }
   };
   // PRE, past the prefetched npre entries (a long walk): 16-byte groups from global memory
@@ -732,6 +740,7 @@ __device__ __forceinline__ void walk_list_lockstep(const WalkArgs& a, const unsi
         for (int u = 0; u < 2; ++u) {
           uint32_t e = zrow;
           if (k + u < n) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(lbase + uint32_t((b0 + k + u) * 4)));
+          SNN_DCHECK(e <= zrow && e % uint32_t(a.row_bytes) == 0);
           off[u] = e;
         }
         uint32_t w0[FPL], w1[FPL];

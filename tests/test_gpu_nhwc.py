@@ -153,7 +153,8 @@ def test_conv_in_nhwc_rejects_validation_paths(G, monkeypatch):
     ((2, 2), (2, 2), (0, 0), False, 30, 0), ((3, 3), (3, 3), (0, 0), False, 250, 0),
     ((2, 2), (2, 2), (0, 0), True, 256, 0), ((2, 2), (2, 2), (0, 0), False, 64, 0),
     ((7, 7), (6, 6), (0, 0), False, 20, 0), ((3, 2), (2, 1), (1, 1), True, 5, 0),
-    ((3, 3), (2, 2), (1, 1), True, 40, 1), ((2, 2), (2, 2), (0, 0), True, 64, 2)])
+    ((3, 3), (2, 2), (1, 1), True, 40, 1), ((2, 2), (2, 2), (0, 0), True, 64, 2),
+    ((3, 3), (2, 2), (1, 1), False, 30, 1), ((3, 2), (3, 3), (1, 0), False, 7, 0), ((1, 1), (1, 1), (0, 0), False, 33, 0)])
 def test_pool_nhwc_to_nhwc_vs_oracle(G, orc, win, stride, pad, with_v, F, flags):
     import synth
     rng = np.random.default_rng(F * 3 + flags + 1)

@@ -1,0 +1,6 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
+timeout 900 python -m pytest tests/test_gpu_f1.py tests/test_gpu_nhwc.py tests/test_gpu_kernels.py tests/test_gpu_configs.py -q -m gpu -x > gpurun_out/pytest_i9.log 2>&1; echo t=$?
+tail -2 gpurun_out/pytest_i9.log
+for w in c2 c4; do timeout 600 python bench.py --workload $w --no-cpu-baseline --no-e2e > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; echo $w=$?;
+python -c "import json; d=json.load(open('gpurun_out/bench_$w.json')); print(d['value'], d['stages_ms'], d['gpu_launches'])"; done
+timeout 300 python tools/rstdp_stamps.py 2>&1 | tail -4
