@@ -297,17 +297,18 @@ __global__ void __launch_bounds__(256) pool_nhwc_lat_rows_kernel(const uint8_t* 
                                                                  uint8_t* __restrict__ lat_out) {
   pdl_begin();
   const int lane = threadIdx.x & 31;
-  const int64_t npix = int64_t(B) * Ho * Wo;
-  const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t pix = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); pix < npix; pix += wstride) {
-    const int b = int(pix / (int64_t(Ho) * Wo));
-    const int rem = int(pix - int64_t(b) * Ho * Wo);
+  const uint32_t HoWo = uint32_t(Ho) * uint32_t(Wo);
+  const uint32_t npix = uint32_t(B) * HoWo;  // < 2^32 (checked by the launcher): 32-bit index math
+  const uint32_t wstride = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t pix = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); pix < npix; pix += wstride) {
+    const int b = int(pix / HoWo);
+    const int rem = int(pix - uint32_t(b) * HoWo);
     const int oy = rem / Wo, ox = rem - (rem / Wo) * Wo;
     const int y0 = oy * SH - DH, x0 = ox * SW - DW;
     const int ya = y0 < 0 ? 0 : y0, yb = (y0 + PH < H ? y0 + PH : H);
     const int xa = x0 < 0 ? 0 : x0, xb = (x0 + PW < W ? x0 + PW : W);
     const uint8_t* img = lat + int64_t(b) * H * W * F;
-    uint8_t* out = lat_out + pix * F;
+    uint8_t* out = lat_out + int64_t(pix) * F;
     for (int f = lane; f < F; f += 32) {
       unsigned m = kNoSpike;
       for (int yy = ya; yy < yb; ++yy) {
@@ -338,8 +339,8 @@ int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, 
     if (flags & SNN_POOL_OUT_NHWC) {
       if (total >= (int64_t(1) << 32)) return set_error(SNN_ESHAPE, "snn_pool(NHWC output): B*Ho*Wo*F >= 2^32");
       if (vec == 1 && !vin && !getenv("SNN_POOL_NOROWS")) {  // latencies only, F % 4 != 0: a warp per pixel
-        int64_t nb = ceil_div(int64_t(B) * Ho * Wo, 8);
-        if (nb > int64_t(num_sms()) * 16) nb = int64_t(num_sms()) * 16;
+        int64_t nb = ceil_div(int64_t(B) * Ho * Wo, 8);  // a warp per output pixel (8 per CTA)
+        if (nb > int64_t(num_sms()) * 64) nb = int64_t(num_sms()) * 64;
         launch_k(pool_nhwc_lat_rows_kernel, dim3(unsigned(nb)), dim3(256), 0, s, lat, B, F, H, W, PH, PW, SH, SW, DH,
                  DW, Ho, Wo, lat_out);
         note_launch();
