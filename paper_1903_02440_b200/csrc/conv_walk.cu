@@ -235,7 +235,78 @@ __device__ __forceinline__ void walk_positions(const WalkArgs& a, unsigned char*
   }
 }
 
-template <int FPL, int PPW, bool PRE, bool WCONV = false, bool BW = true, bool GW = false, bool LS = false>
+// K7: the fused schedule by row tiles (channels-last input).  A warp takes one tile -- output row y of
+// image b, output columns [x0, x0 + nxs) -- sorts its input halo once (rows_sort), then walks the tile's
+// positions PPW at a time in lockstep (walk_rows_lockstep) and stores their outputs as walk_positions
+// does.
+template <int FPL, int PPW, bool S28>
+__device__ __forceinline__ void walk_rows(const WalkArgs& a, unsigned char* smem) {
+  constexpr int LPP = 32 / PPW;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int grp = lane / LPP, gl = lane - grp * LPP;
+  unsigned char* wbase = smem + a.off_warps + warp * a.warp_bytes;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(wbase + a.cnt_off);
+  uint16_t* base = reinterpret_cast<uint16_t*>(wbase + a.start_off);
+  uint16_t* list = reinterpret_cast<uint16_t*>(wbase + a.list_off);
+  const uint8_t* colof = smem + a.off_eoff;
+  const int fbase = gl * FPL;
+  unsigned valid = 0;
+#pragma unroll
+  for (int j = 0; j < FPL; ++j) valid |= (fbase + j < a.F) ? (1u << j) : 0u;
+  const bool vec_out = a.nhwc && (a.F % FPL) == 0 && (reinterpret_cast<uintptr_t>(a.lat_out) % FPL) == 0 &&
+                       (reinterpret_cast<uintptr_t>(a.v_out) % (4 * FPL)) == 0;
+  const uint32_t wl = smem_u32(smem + gl * FPL * 4), lb = smem_u32(list);
+  const uint32_t rb = uint32_t(a.row_bytes), cstep = uint32_t(a.C) * rb;
+  const int HoWo = a.Ho * a.Wo, per_img = a.Ho * a.nseg;
+  const int64_t units = int64_t(a.B) * per_img;
+  for (int64_t u = int64_t(blockIdx.x) * nwarps + warp; u < units; u += int64_t(gridDim.x) * nwarps) {
+    const int b = int(u / per_img), rem = int(u - int64_t(b) * per_img);
+    const int y = rem / a.nseg, x0 = (rem - y * a.nseg) * a.nx;
+    const int nxs = min(a.nx, a.Wo - x0), ncol = nxs + a.KW - 1;
+    rows_sort(a, b, y, x0, ncol, colof, cnt, base, list, lane);
+    for (int q0 = 0; q0 < nxs; q0 += PPW) {
+      const int xr = q0 + grp;
+      const bool pv = xr < nxs;
+      uint32_t lo;
+      float vo[FPL];
+      walk_rows_lockstep<FPL, PPW, S28>(a, wl - uint32_t(xr) * cstep, uint32_t(a.R) * rb + uint32_t(xr) * cstep,
+                                        base + xr, ncol, lb, pv, valid, lo, vo);
+      if (pv) {
+        const int p = b * HoWo + y * a.Wo + x0 + xr;
+        int64_t o0 = int64_t(p) * a.F + fbase;
+        if (!a.nhwc) o0 = (int64_t(b) * a.F + fbase) * HoWo + (p - b * HoWo);
+        if (FPL > 1 && vec_out) {
+          if (valid == 0) {
+          } else if constexpr (FPL == 2) {
+            *reinterpret_cast<uint16_t*>(a.lat_out + o0) = uint16_t(lo);
+            if (a.v_out) __stcs(reinterpret_cast<float2*>(a.v_out + o0), make_float2(vo[0], vo[1]));
+          } else if constexpr (FPL == 4) {
+            *reinterpret_cast<uint32_t*>(a.lat_out + o0) = lo;
+            if (a.v_out) __stcs(reinterpret_cast<float4*>(a.v_out + o0), make_float4(vo[0], vo[1], vo[2], vo[3]));
+          }
+        } else {
+          const int64_t fs = a.nhwc ? 1 : HoWo;
+#pragma unroll
+          for (int j = 0; j < FPL; ++j) {
+            if (valid >> j & 1) {
+              a.lat_out[o0 + j * fs] = uint8_t(lo >> (8 * j));
+              if (a.v_out) a.v_out[o0 + j * fs] = vo[j];
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ void rows_tables(const WalkArgs& a, unsigned char* tabs) {
+  uint8_t* colof = tabs + a.off_eoff;
+  for (int j = threadIdx.x; j < (a.nx + a.KW - 1) * a.C; j += blockDim.x) colof[j] = uint8_t(j / a.C);
+}
+
+template <int FPL, int PPW, bool PRE, bool WCONV = false, bool BW = true, bool GW = false, bool LS = false,
+          bool RW = false>
 __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(const WalkArgs a) {
   pdl_wait();
   constexpr int LPP = 32 / PPW;
@@ -280,7 +351,8 @@ __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(
       ok28 &= ((v.x | v.y | v.z | v.w) & 7u) == 0;
       dst[i] = v;
     }
-    if (!PRE) rf_tables(a, smem);
+    if (RW) rows_tables(a, smem);
+    else if (!PRE) rf_tables(a, smem);
   }
   const bool s28 = __syncthreads_and(ok28) != 0;
   if (s28) {
@@ -291,9 +363,11 @@ __global__ void __launch_bounds__(WalkThreads<FPL, PRE>::v, 1) conv_walk_kernel(
       w4[i] = v;
     }
     __syncthreads();
-    walk_positions<FPL, PPW, PRE, true, BW, false, LS>(a, smem);
+    if constexpr (RW) walk_rows<FPL, PPW, true>(a, smem);
+    else walk_positions<FPL, PPW, PRE, true, BW, false, LS>(a, smem);
   } else {
-    walk_positions<FPL, PPW, PRE, false, BW, false, LS>(a, smem);
+    if constexpr (RW) walk_rows<FPL, PPW, false>(a, smem);
+    else walk_positions<FPL, PPW, PRE, false, BW, false, LS>(a, smem);
   }
 }
 
@@ -513,6 +587,47 @@ static int walk_go(const WalkPlan& pl, const WalkArgs& a, cudaStream_t s) {
   return check_launch("snn_conv_fire(walk)");
 }
 
+// K7 row-tile layout of a fused PPW = 4 / FPL = 4 plan (channels-last input): tiles of nx positions
+// (a multiple of 4, <= 32; nseg tiles per output row), per warp the (t, column) counters, the u16 bucket
+// bases and the u16 list; the CTA table colof (halo byte -> column).  False if the u16 weight-row byte
+// offsets or shared memory do not fit (the per-position fused walk runs instead).  SNN_WALK_ROWS=0 off.
+static bool rows_plan(WalkPlan& pl) {
+  if (const char* e = getenv("SNN_WALK_ROWS")) if (e[0] == '0') return false;
+  WalkArgs& a = pl.a;
+  if (pl.pre || pl.ppw != 4 || pl.fpl != 4 || !a.in_nhwc) return false;
+  a.nseg = int(ceil_div(a.Wo, 32));
+  a.nx = int(ceil_div(ceil_div(a.Wo, a.nseg), 4)) * 4;
+  const int ncolmax = a.nx + a.KW - 1;
+  if (ncolmax * a.C > 65535 || ncolmax > 255) return false;
+  if ((long((a.KH - 1) * a.KW * a.C + ncolmax * a.C) + a.R) * a.row_bytes >= 65536) return false;
+  if (long(a.T) * ncolmax >= 65535 || long(a.KH) * ncolmax * a.C >= 65535) return false;
+  a.cnt_off = 0;
+  a.start_off = al16(a.T * ncolmax * 4);
+  a.list_off = a.start_off + al16((a.T * ncolmax + 1) * 2);
+  a.warp_bytes = a.list_off + al16(a.KH * ncolmax * a.C * 2);
+  a.off_eoff = al16(int(long(a.R + 1) * pl.FGS * 4));
+  a.off_warps = a.off_eoff + al16(ncolmax * a.C);
+  int nw = int((kWalkSmemLimit - a.off_warps) / a.warp_bytes);
+  if (nw > 24) nw = 24;
+  if (const char* e = getenv("SNN_WALK_ROWS_WARPS")) { const int v = atoi(e); if (v >= 1 && v < nw) nw = v; }
+  if (nw < 8) return false;
+  pl.nwarps = nw;
+  pl.smem = a.off_warps + nw * a.warp_bytes;
+  return true;
+}
+
+static int rows_go(const WalkPlan& pl, const WalkArgs& a, cudaStream_t s) {
+  auto k = conv_walk_kernel<4, 4, false, false, false, false, false, true>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
+  if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_conv_fire(rows): %s", cudaGetErrorString(e));
+  const int64_t units = int64_t(a.B) * a.Ho * a.nseg;
+  const int64_t per = ceil_div(units, pl.nwarps);
+  const int64_t want = num_sms();
+  launch_k(k, dim3(int(per < want ? per : want)), dim3(pl.nwarps * 32), pl.smem, s, a);
+  note_launch();
+  return check_launch("snn_conv_fire(rows)");
+}
+
 template <int PPW>
 static int sort_go(const WalkPlan& pl, const WalkArgs& a, cudaStream_t s) {
   auto k = rf_sort_kernel<PPW>;
@@ -609,6 +724,15 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   if (rc) return rc;
   if (!pl.pre) {
     a.p0 = 0; a.np = npos;
+    {
+      WalkPlan rp = pl;
+      rp.a = a;
+      if (rows_plan(rp)) {
+        if (getenv("SNN_DEBUG_PLAN"))
+          fprintf(stderr, "walk rows: nx %d nseg %d warps %d smem %d\n", rp.a.nx, rp.a.nseg, rp.nwarps, rp.smem);
+        return rows_go(rp, rp.a, s);
+      }
+    }
     switch (pl.ppw * 10 + pl.fpl) {
       case 44: return walk_go<4, 4, false>(pl, a, s);
       case 24: return walk_go<4, 2, false>(pl, a, s);

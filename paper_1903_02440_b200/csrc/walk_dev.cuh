@@ -60,6 +60,9 @@ struct WalkArgs {
   int pad_unit;       // sorted buckets padded to a multiple of this many entries: 4 (bucket walk) or 2 (K3 blocks)
   int in_nhwc;        // input layout [B, H, W, C] (SNN_CONV_IN_NHWC): receptive-field entries are then
                       // ordered (ky, kx, c) -- e = (ky KW + kx) C + c -- and so are the weight rows
+  // row tiles (K7, walk_rows): a warp sorts the input halo of nx consecutive output positions of one
+  // output row once, by (spike time, halo column); nseg tiles per output row
+  int nx, nseg;
 };
 
 static inline int al16(int x) { return (x + 15) & ~15; }
@@ -769,6 +772,154 @@ __device__ __forceinline__ void walk_list_lockstep(const WalkArgs& a, const unsi
     }
     b0 = b1;
   }
+}
+
+// ------------------------------------------------------------------------------------- K7 row tiles
+// Walk of one position's buckets from a row tile's (t, column) sorted halo list (walk_rows): the same
+// lockstep loop as walk_list_lockstep (PPW positions per warp, a group gathers its own bucket, the warp
+// iterates to the largest; exact test at each bucket end, lat = t, v = P[t]), but bucket t of the
+// group's position is the contiguous list range [base[t ncol], base[t ncol + KW]) -- the entries of the
+// KW halo columns its receptive field covers -- and the entries are u16 weight-row byte offsets
+// relative to the tile's first position, so the group's gather base is shifted by its column
+// (wgb = slice - xr C row_bytes) and its zero-weight row is zrow = (R + xr C) row_bytes.
+template <int FPL, int PPW, bool S28>
+__device__ __forceinline__ void walk_rows_lockstep(const WalkArgs& a, uint32_t wgb, uint32_t zrow, const uint16_t* base,
+                                                   int ncol, uint32_t lbase, bool pv, unsigned valid, uint32_t& lo,
+                                                   float (&vo)[FPL]) {
+  const int T = a.T, KW = a.KW;
+  const int64_t thr = S28 ? a.thr28 : a.thr;
+  WSrcS wls;
+  wls.b = wgb;
+  uint64_t acc[FPL];
+  lo = 0xFFFFFFFFu;
+#pragma unroll
+  for (int j = 0; j < FPL; ++j) { acc[j] = (pv && (valid >> j & 1)) ? 0ull : kFiredAcc; vo[j] = 0.0f; }
+  auto alive = [&]() {
+    bool al = false;
+#pragma unroll
+    for (int j = 0; j < FPL; ++j) al |= int64_t(acc[j]) >= 0;
+    return al;
+  };
+  constexpr int LPP = 32 / PPW;
+  const int grp = int(threadIdx.x & 31) / LPP;
+  const unsigned gmask = (LPP == 32) ? 0xffffffffu : (((1u << LPP) - 1u) << (grp * LPP));
+  bool galive = (__ballot_sync(0xffffffffu, alive()) & gmask) != 0;
+  if (!__any_sync(0xffffffffu, galive)) return;
+  const uint16_t* bt = base;
+#pragma unroll 1
+  for (int t = 0; t < T; ++t, bt += ncol) {
+    const int b0 = pv ? int(bt[0]) : 0;
+    const int n = (pv && galive) ? int(bt[KW]) - b0 : 0;
+    const int nmax = __reduce_max_sync(0xffffffffu, n);
+    for (int c0 = 0; c0 < nmax; c0 += 14) {  // chunks of <= 14 entries (32-bit partial sums, S28)
+      const int c1 = min(nmax, c0 + 14);
+      uint32_t part[FPL];
+#pragma unroll
+      for (int j = 0; j < FPL; ++j) part[j] = 0;
+      for (int k = c0; k < c1; k += 2) {
+        uint32_t off[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          uint32_t e = zrow;
+          if (k + u < n) {
+            uint16_t h;
+            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(lbase + uint32_t((b0 + k + u) * 2)));
+            e = h;
+          }
+          off[u] = e;
+        }
+        uint32_t w0[FPL], w1[FPL];
+        wls.template g<FPL>(off[0], w0);
+        wls.template g<FPL>(off[1], w1);
+#pragma unroll
+        for (int j = 0; j < FPL; ++j) {
+          if constexpr (S28) part[j] += w0[j] + w1[j];
+          else acc[j] += uint64_t(w0[j]) + w1[j];
+        }
+      }
+      if constexpr (S28) {
+#pragma unroll
+        for (int j = 0; j < FPL; ++j) acc[j] += part[j];
+      }
+    }
+    if (n > 0 || t == 0) {  // the exact test at the end of bucket t (t = 0: a negative threshold)
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < FPL; ++j) any |= int64_t(acc[j]) > thr;
+      if (any) fire_at<FPL, S28>(acc, thr, t, lo, vo);
+    }
+    if (__any_sync(0xffffffffu, n > 0 || t == 0)) {
+      galive = (__ballot_sync(0xffffffffu, alive()) & gmask) != 0;
+      if (!__any_sync(0xffffffffu, galive)) break;
+    }
+  }
+}
+
+// Counting sort of one row tile's input halo (output row y of image b, output columns x0 .. x0+nxs-1;
+// channels-last input): KH halo rows of ncol = nxs + KW - 1 columns x C channels, each a contiguous
+// run of ncol C bytes.  Buckets are (t, column) in t-major order, so for every t the entries of KW
+// consecutive columns -- one position's receptive field at time t -- are one contiguous range.  Pass 1
+// counts with shared-memory atomics, a warp scan turns the counts into bucket bases (u16; base[nb] = the
+// total), pass 2 re-reads the latencies (L1) and places each spiking input's weight-row byte offset
+// (ky KW C + j) row_bytes -- j = column C + c inside the halo row -- relative to the tile's first
+// position; position xr reads row (ky KW + col - xr) C + c = that minus xr C, the (ky, kx, c) order of
+// the channels-last weight rows.  Every halo input is sorted once for the tile's nxs positions instead
+// of once per position (KH KW C entries each).
+__device__ __forceinline__ void rows_sort(const WalkArgs& a, int b, int y, int x0, int ncol, const uint8_t* colof,
+                                          uint32_t* cnt, uint16_t* base, uint16_t* list, int lane) {
+  const int T = a.T, C = a.C, KW = a.KW;
+  const int nb = T * ncol;
+  for (int i = lane; i < nb; i += 32) cnt[i] = 0;
+  __syncwarp();
+  const int ix0 = x0 - a.pad;
+  const int jlo = max(0, -ix0) * C, jhi = min(ncol, a.W - ix0) * C;  // the halo columns inside the input
+  for (int ky = 0; ky < a.KH; ++ky) {
+    const int iy = y - a.pad + ky;
+    if (iy < 0 || iy >= a.H) continue;  // warp-uniform
+    const uint8_t* rowp = a.lat_in + ((int64_t(b) * a.H + iy) * a.W + ix0) * C;
+#pragma unroll 4
+    for (int j = jlo + lane; j < jhi; j += 32) {
+      const int l = __ldg(rowp + j);
+      if (l < T) atomicAdd(&cnt[l * ncol + colof[j]], 1u);
+    }
+  }
+  __syncwarp();
+  const int per = (nb + 31) >> 5;
+  const int k0 = min(nb, lane * per), k1 = min(nb, k0 + per);
+  int sum = 0;
+  for (int k = k0; k < k1; ++k) sum += int(cnt[k]);
+  int inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  int run = inc - sum;
+  for (int k = k0; k < k1; ++k) {
+    const int c = int(cnt[k]);
+    base[k] = uint16_t(run);
+    cnt[k] = uint32_t(run);
+    run += c;
+  }
+  if (lane == 31) base[nb] = uint16_t(inc);
+  __syncwarp();
+  const uint32_t rb = uint32_t(a.row_bytes);
+  for (int ky = 0; ky < a.KH; ++ky) {
+    const int iy = y - a.pad + ky;
+    if (iy < 0 || iy >= a.H) continue;
+    const uint8_t* rowp = a.lat_in + ((int64_t(b) * a.H + iy) * a.W + ix0) * C;
+    const uint32_t eb = uint32_t(ky * KW * C);
+#pragma unroll 4
+    for (int j = jlo + lane; j < jhi; j += 32) {
+      const int l = __ldg(rowp + j);
+      if (l < T) {
+        const uint32_t slot = atomicAdd(&cnt[l * ncol + colof[j]], 1u);
+        SNN_DCHECK(slot < uint32_t(a.KH * ncol * C));
+        list[slot] = uint16_t((eb + uint32_t(j)) * rb);
+      }
+    }
+  }
+  __syncwarp();
 }
 
 }  // namespace snn

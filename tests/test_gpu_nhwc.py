@@ -187,3 +187,38 @@ def test_conv_fire_kstar_truncation(G, orc, case, monkeypatch):
     ol, ov = orc.conv_fire(lat_in, w, pad, T, theta)
     assert np.array_equal(host(lat), ol.transpose(0, 2, 3, 1))
     assert np.array_equal(host(v), ov.transpose(0, 2, 3, 1))
+
+
+# ------------------------------------------------- K7 row tiles (fused small-receptive-field layers, NHWC input)
+ROWS_CASES = [
+    # (B, C, H, W, pad, F, K, T, theta, p_spike, w_lo)
+    (8, 6, 28, 28, 2, 30, 5, 15, 15.0, 0.45, 2 ** -5),   # C2 L1 shape (one tile per output row), S28 slice
+    (8, 6, 28, 28, 2, 30, 5, 15, 15.0, 0.45, 2 ** -8),   # the same with an int64 (2^-31) slice
+    (3, 4, 40, 75, 0, 20, 5, 30, 15.0, 0.5, 2 ** -5),    # C4 L1-like: 3 tiles per row, ragged last tile
+    (4, 3, 33, 70, 1, 17, 3, 6, -0.5, 0.5, 2 ** -8),     # theta < 0 (fires at t = 0), F % 4 != 0
+    (5, 2, 30, 41, 2, 32, 5, 1, 1.0, 0.8, 2 ** -5),      # T = 1, F = 32
+    (6, 5, 25, 37, 1, 25, 3, 9, 3.0, 1.0, 2 ** -8),      # every input spikes, 2 tiles per row
+    (4, 4, 21, 130, 2, 9, 5, 12, 2.5, 0.3, 2 ** -5),     # 5 tiles per row, few features
+    (8, 6, 26, 29, 0, 30, 5, 15, 40.0, 0.5, 2 ** -5),    # threshold never reached (whole lists walked)
+]
+
+
+@pytest.mark.parametrize("out_nhwc", [True, False])
+@pytest.mark.parametrize("case", ROWS_CASES)
+def test_conv_fire_rows_vs_oracle(G, orc, case, out_nhwc, capfd, monkeypatch):
+    """K7: the fused walk by row tiles (each output row's input halo sorted once by (t, column)), bit-exact."""
+    monkeypatch.setenv("SNN_DEBUG_PLAN", "1")
+    B, C, H, W, pad, F, K, T, theta, p, lo = case
+    rng = np.random.default_rng(abs(hash(case)) % 2 ** 31)
+    import synth
+    lat_in = synth.random_latencies(rng, (B, C, H, W), T, p)
+    w = exact_weights(rng, (F, C, K, K), lo=lo)
+    lat, v = G.conv_fire(cu(np.ascontiguousarray(lat_in.transpose(0, 2, 3, 1))), cu(w), pad, T, theta,
+                         nhwc=out_nhwc, in_nhwc=True)
+    G.sync_status()
+    assert "walk rows:" in capfd.readouterr().err
+    ol, ov = orc.conv_fire(lat_in, w, pad, T, theta)
+    if out_nhwc:
+        ol, ov = ol.transpose(0, 2, 3, 1), ov.transpose(0, 2, 3, 1)
+    assert np.array_equal(host(lat), ol)
+    assert np.array_equal(host(v), ov)
