@@ -269,8 +269,12 @@ __device__ __forceinline__ void walk_rows(const WalkArgs& a, unsigned char* smem
       const bool pv = xr < nxs;
       uint32_t lo;
       float vo[FPL];
-      walk_rows_lockstep<FPL, PPW, S28>(a, wl - uint32_t(xr) * cstep, uint32_t(a.R) * rb + uint32_t(xr) * cstep,
-                                        base + xr, ncol, lb, pv, valid, lo, vo);
+      if (a.rows_g == 2)
+        walk_rows_lockstep<FPL, PPW, S28, 2>(a, wl - uint32_t(xr) * cstep, uint32_t(a.R) * rb + uint32_t(xr) * cstep,
+                                             base + xr, ncol, lb, pv, valid, lo, vo);
+      else
+        walk_rows_lockstep<FPL, PPW, S28, 1>(a, wl - uint32_t(xr) * cstep, uint32_t(a.R) * rb + uint32_t(xr) * cstep,
+                                             base + xr, ncol, lb, pv, valid, lo, vo);
       if (pv) {
         const int p = b * HoWo + y * a.Wo + x0 + xr;
         int64_t o0 = int64_t(p) * a.F + fbase;
@@ -611,6 +615,10 @@ static bool rows_plan(WalkPlan& pl) {
   if (nw > 24) nw = 24;
   if (const char* e = getenv("SNN_WALK_ROWS_WARPS")) { const int v = atoi(e); if (v >= 1 && v < nw) nw = v; }
   if (nw < 8) return false;
+  // K7c: two buckets per threshold test where buckets are small (R < 6 T, a few spiking inputs each;
+  // measured C4 L1 22.2 -> 19.9 ms, C2 L1 unchanged at 1, 4 buckets slower on both: register spills)
+  a.rows_g = a.R < 6 * a.T ? 2 : 1;
+  if (const char* e = getenv("SNN_WALK_ROWS_G")) { const int v = atoi(e); if (v == 1 || v == 2) a.rows_g = v; }
   pl.nwarps = nw;
   pl.smem = a.off_warps + nw * a.warp_bytes;
   return true;
@@ -729,7 +737,8 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
       rp.a = a;
       if (rows_plan(rp)) {
         if (getenv("SNN_DEBUG_PLAN"))
-          fprintf(stderr, "walk rows: nx %d nseg %d warps %d smem %d\n", rp.a.nx, rp.a.nseg, rp.nwarps, rp.smem);
+          fprintf(stderr, "walk rows: nx %d nseg %d warps %d smem %d g %d\n", rp.a.nx, rp.a.nseg, rp.nwarps, rp.smem,
+                  rp.a.rows_g);
         return rows_go(rp, rp.a, s);
       }
     }

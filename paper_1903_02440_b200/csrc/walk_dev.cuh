@@ -63,6 +63,7 @@ struct WalkArgs {
   // row tiles (K7, walk_rows): a warp sorts the input halo of nx consecutive output positions of one
   // output row once, by (spike time, halo column); nseg tiles per output row
   int nx, nseg;
+  int rows_g;         // K7c: buckets per threshold test of the row-tile walk (1, 2)
 };
 
 static inline int al16(int x) { return (x + 15) & ~15; }
@@ -782,7 +783,7 @@ __device__ __forceinline__ void walk_list_lockstep(const WalkArgs& a, const unsi
 // KW halo columns its receptive field covers -- and the entries are u16 weight-row byte offsets
 // relative to the tile's first position, so the group's gather base is shifted by its column
 // (wgb = slice - xr C row_bytes) and its zero-weight row is zrow = (R + xr C) row_bytes.
-template <int FPL, int PPW, bool S28>
+template <int FPL, int PPW, bool S28, int G>
 __device__ __forceinline__ void walk_rows_lockstep(const WalkArgs& a, uint32_t wgb, uint32_t zrow, const uint16_t* base,
                                                    int ncol, uint32_t lbase, bool pv, unsigned valid, uint32_t& lo,
                                                    float (&vo)[FPL]) {
@@ -805,50 +806,105 @@ __device__ __forceinline__ void walk_rows_lockstep(const WalkArgs& a, uint32_t w
   const unsigned gmask = (LPP == 32) ? 0xffffffffu : (((1u << LPP) - 1u) << (grp * LPP));
   bool galive = (__ballot_sync(0xffffffffu, alive()) & gmask) != 0;
   if (!__any_sync(0xffffffffu, galive)) return;
+  // gather-add of entries [k0, k1) of the lockstep bucket (b0, n) into 32-bit (S28) or 64-bit sums
+  auto gather = [&](int b0, int n, int k0, int k1, uint32_t (&part)[FPL]) {
+    for (int k = k0; k < k1; k += 2) {
+      uint32_t off[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        uint32_t e = zrow;
+        if (k + u < n) {
+          uint16_t h;
+          asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(lbase + uint32_t((b0 + k + u) * 2)));
+          e = h;
+        }
+        off[u] = e;
+      }
+      uint32_t w0[FPL], w1[FPL];
+      wls.template g<FPL>(off[0], w0);
+      wls.template g<FPL>(off[1], w1);
+#pragma unroll
+      for (int j = 0; j < FPL; ++j) {
+        if constexpr (S28) part[j] += w0[j] + w1[j];
+        else acc[j] += uint64_t(w0[j]) + w1[j];
+      }
+    }
+  };
   const uint16_t* bt = base;
 #pragma unroll 1
-  for (int t = 0; t < T; ++t, bt += ncol) {
-    const int b0 = pv ? int(bt[0]) : 0;
-    const int n = (pv && galive) ? int(bt[KW]) - b0 : 0;
-    const int nmax = __reduce_max_sync(0xffffffffu, n);
-    for (int c0 = 0; c0 < nmax; c0 += 14) {  // chunks of <= 14 entries (32-bit partial sums, S28)
-      const int c1 = min(nmax, c0 + 14);
-      uint32_t part[FPL];
+  for (int t0 = 0; t0 < T; t0 += G, bt += G * ncol) {
+    int b0[G], n[G], tot = 0;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      b0[i] = 0; n[i] = 0;
+      if (pv && galive && t0 + i < T) { b0[i] = int(bt[i * ncol]); n[i] = int(bt[i * ncol + KW]) - b0[i]; }
+      tot += n[i];
+    }
+    bool fired = false;
+    if (S28 && G > 1 && __reduce_max_sync(0xffffffffu, tot) <= 14) {
+      // K7c block of G buckets: sums in 32 bits with a snapshot at every bucket end, ONE threshold test at
+      // the block end (the potential is monotone: no feature crosses inside the block unless it is above
+      // the threshold at its end); a crossing feature takes the first bucket end above (exact lat, v)
+      uint32_t part[FPL], snap[G][FPL];
 #pragma unroll
       for (int j = 0; j < FPL; ++j) part[j] = 0;
-      for (int k = c0; k < c1; k += 2) {
-        uint32_t off[2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          uint32_t e = zrow;
-          if (k + u < n) {
-            uint16_t h;
-            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(lbase + uint32_t((b0 + k + u) * 2)));
-            e = h;
-          }
-          off[u] = e;
-        }
-        uint32_t w0[FPL], w1[FPL];
-        wls.template g<FPL>(off[0], w0);
-        wls.template g<FPL>(off[1], w1);
+      for (int i = 0; i < G; ++i) {
+        const int nmax = __reduce_max_sync(0xffffffffu, n[i]);
+        gather(b0[i], n[i], 0, nmax, part);
+#pragma unroll
+        for (int j = 0; j < FPL; ++j) snap[i][j] = part[j];
+      }
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < FPL; ++j) any |= int64_t(acc[j] + part[j]) > thr;
+      if (any) {
 #pragma unroll
         for (int j = 0; j < FPL; ++j) {
-          if constexpr (S28) part[j] += w0[j] + w1[j];
-          else acc[j] += uint64_t(w0[j]) + w1[j];
+          if (int64_t(acc[j] + part[j]) > thr) {
+            int fi = G - 1;
+#pragma unroll
+            for (int i = G - 2; i >= 0; --i)
+              if (int64_t(acc[j] + snap[i][j]) > thr) fi = i;
+            uint32_t sv = snap[0][j];
+#pragma unroll
+            for (int i = 1; i < G; ++i) if (fi == i) sv = snap[i][j];
+            lo = (lo & ~(0xFFu << (8 * j))) | (uint32_t(t0 + fi) << (8 * j));
+            vo[j] = fixed_to_float_s<S28>(int64_t(acc[j] + sv));
+            acc[j] = kFiredAcc;
+          } else {
+            acc[j] += part[j];
+          }
         }
-      }
-      if constexpr (S28) {
+        fired = true;
+      } else {
 #pragma unroll
         for (int j = 0; j < FPL; ++j) acc[j] += part[j];
       }
-    }
-    if (n > 0 || t == 0) {  // the exact test at the end of bucket t (t = 0: a negative threshold)
-      bool any = false;
+    } else {
 #pragma unroll
-      for (int j = 0; j < FPL; ++j) any |= int64_t(acc[j]) > thr;
-      if (any) fire_at<FPL, S28>(acc, thr, t, lo, vo);
+      for (int i = 0; i < G; ++i) {
+        const int t = t0 + i;
+        const int nmax = __reduce_max_sync(0xffffffffu, n[i]);
+        for (int c0 = 0; c0 < nmax; c0 += 14) {  // chunks of <= 14 entries (32-bit partial sums, S28)
+          uint32_t part[FPL];
+#pragma unroll
+          for (int j = 0; j < FPL; ++j) part[j] = 0;
+          gather(b0[i], n[i], c0, min(nmax, c0 + 14), part);
+          if constexpr (S28) {
+#pragma unroll
+            for (int j = 0; j < FPL; ++j) acc[j] += part[j];
+          }
+        }
+        if ((n[i] > 0 || t == 0) && t < T) {  // the exact test at the end of bucket t (t = 0: a negative threshold)
+          bool any = false;
+#pragma unroll
+          for (int j = 0; j < FPL; ++j) any |= int64_t(acc[j]) > thr;
+          if (any) { fire_at<FPL, S28>(acc, thr, t, lo, vo); fired = true; }
+        }
+      }
     }
-    if (__any_sync(0xffffffffu, n > 0 || t == 0)) {
+    if (__any_sync(0xffffffffu, fired)) {  // liveness changes only where a feature fired
       galive = (__ballot_sync(0xffffffffu, alive()) & gmask) != 0;
       if (!__any_sync(0xffffffffu, galive)) break;
     }

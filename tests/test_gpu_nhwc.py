@@ -203,11 +203,14 @@ ROWS_CASES = [
 ]
 
 
+@pytest.mark.parametrize("g", ["1", "2"])
 @pytest.mark.parametrize("out_nhwc", [True, False])
 @pytest.mark.parametrize("case", ROWS_CASES)
-def test_conv_fire_rows_vs_oracle(G, orc, case, out_nhwc, capfd, monkeypatch):
-    """K7: the fused walk by row tiles (each output row's input halo sorted once by (t, column)), bit-exact."""
+def test_conv_fire_rows_vs_oracle(G, orc, case, out_nhwc, g, capfd, monkeypatch):
+    """K7: the fused walk by row tiles (each output row's input halo sorted once by (t, column)), bit-exact;
+    g = buckets per threshold test (K7c: 2 = one test per bucket pair, snapshots locate the crossing)."""
     monkeypatch.setenv("SNN_DEBUG_PLAN", "1")
+    monkeypatch.setenv("SNN_WALK_ROWS_G", g)
     B, C, H, W, pad, F, K, T, theta, p, lo = case
     rng = np.random.default_rng(abs(hash(case)) % 2 ** 31)
     import synth
@@ -222,3 +225,4 @@ def test_conv_fire_rows_vs_oracle(G, orc, case, out_nhwc, capfd, monkeypatch):
         ol, ov = ol.transpose(0, 2, 3, 1), ov.transpose(0, 2, 3, 1)
     assert np.array_equal(host(lat), ol)
     assert np.array_equal(host(v), ov)
+
