@@ -15,6 +15,7 @@
 // allocator, warps 4..7 = epilogue (TMEM lane quadrant = warp % 4).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -289,26 +290,47 @@ __global__ void __launch_bounds__(256) tc_prep_a_hwc_kernel(const uint8_t* __res
 }
 
 // ------------------------------------------------------------------------------- the GEMM
-__global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* __restrict__ aq,
+// Implicit im2col (K8): with lat != nullptr the A operand is not read from aq but built in the CTA.  The
+// binary spike-wave S[T-1] of the input pixels the M tile's receptive fields touch -- per image of the
+// tile, the input rows its output rows need, full width, channels padded to Cp -- is staged once into
+// shared memory (the "band", foot bytes); then per pipeline stage the four epilogue warps (idle until the
+// accumulator is done) write the stage's A tile -- row r = position mt * 128 + r, 16-byte core-matrix rows
+// of 16 channels of one input pixel, (ky, kx, c) K order, zero outside the input -- in the canonical
+// K-major layout, fence the generic-proxy stores for the tensor core and arrive on the stage's full
+// barrier next to the producer's B bulk copy.  No A operand in HBM (tc_prep_a_hwc's write + the GEMM's
+// read of Mt x Kp x 128 bytes).
+struct TcImpl {
+  const uint8_t* lat;  // channels-last [B, H, W, C] latencies; nullptr = A prepared in aq
+  int C, H, W, pad, KH, KW, Wo, HoWo, T;
+  int foot;            // band bytes (the largest tile footprint, host-computed)
+};
+constexpr int kTcMaxImg = 128;  // images one M tile can touch (HoWo >= 1)
+
+__global__ void __launch_bounds__(kTcThreads + 128, 1) conv_tc_kernel(const uint8_t* __restrict__ aq,
                                                                  const uint8_t* __restrict__ bq, TcPlan p, int F,
                                                                  int HoWo, int T, uint32_t tmem_cols,
                                                                  uint8_t* __restrict__ lat_out,
                                                                  float* __restrict__ v_out,
-                                                                 unsigned long long* __restrict__ part, int nhwc) {
+                                                                 unsigned long long* __restrict__ part, int nhwc,
+                                                                 const TcImpl im) {
   pdl_begin();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t a_bytes = kTcM * kTcKT, b_bytes = uint32_t(p.N) * kTcKT, stage_bytes = a_bytes + b_bytes;
   __shared__ __align__(8) uint64_t full_bar[kTcStages], empty_bar[kTcStages], done_bar;
   __shared__ uint32_t tmem_base_sh;
+  __shared__ int img_off[kTcMaxImg + 1], img_r0[kTcMaxImg];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ksi = int(blockIdx.x % unsigned(p.KS)), tile = int(blockIdx.x / unsigned(p.KS));  // K slices fastest
   const int ch = tile % p.nch, mt = tile / p.nch;  // then feature chunks
   const int kt0 = int(int64_t(ksi) * p.Kt / p.KS), kt1 = int(int64_t(ksi + 1) * p.Kt / p.KS);
-
+  const bool impl = im.lat != nullptr;
+  uint8_t* band = smem + size_t(kTcStages) * stage_bytes;
+  const int m_first = mt * kTcM, m_last = min(p.M, m_first + kTcM) - 1;
+  const int b_first = impl ? m_first / im.HoWo : 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTcStages; ++s) {
-      mbar_init(smem_u32(&full_bar[s]), 1);
+      mbar_init(smem_u32(&full_bar[s]), impl ? 9 : 1);  // impl: + one arrival per A-writing warp
       mbar_init(smem_u32(&empty_bar[s]), 1);
     }
     mbar_init(smem_u32(&done_bar), 1);
@@ -326,18 +348,99 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
   const uint32_t tmem_base = tmem_base_sh;
 
   if (warp == 0 && lane == 0) {
-    // ---------------- producer: two bulk copies per stage ----------------
+    // ---------------- producer: two bulk copies per stage (impl: B only) ----------------
     const uint8_t* a_src = aq + size_t(mt) * p.Kt * a_bytes;
     const uint8_t* b_src = bq + size_t(ch) * p.Kt * b_bytes;
     for (int kt = kt0; kt < kt1; ++kt) {
       const int s = (kt - kt0) % kTcStages, u = (kt - kt0) / kTcStages;
       if (kt - kt0 >= kTcStages) mbar_wait(smem_u32(&empty_bar[s]), (u - 1) & 1);
       const uint32_t fb = smem_u32(&full_bar[s]);
-      mbar_expect_tx(fb, stage_bytes);
+      mbar_expect_tx(fb, impl ? b_bytes : stage_bytes);
       const uint32_t dst = smem_u32(smem + size_t(s) * stage_bytes);
-      bulk_g2s(dst, a_src + size_t(kt) * a_bytes, a_bytes, fb);
+      if (!impl) bulk_g2s(dst, a_src + size_t(kt) * a_bytes, a_bytes, fb);
       bulk_g2s(dst + a_bytes, b_src + size_t(kt) * b_bytes, b_bytes, fb);
     }
+  } else if (impl && warp >= 4) {
+    // ---------------- A writers (K8) ----------------
+    // stage the tile's binary S[T-1] footprint: per image, its input rows (full width), pixel stride
+    // PS = Cp + 16 bytes (16-byte loads of consecutive pixels fall in distinct bank groups); the B bulk
+    // copies of the first stages are already in flight
+    const int PS = p.Cp + 16, Ho = im.HoWo / im.Wo;
+    const int b_last = m_last / im.HoWo, nimg = b_last - b_first + 1;
+    const int wt = threadIdx.x - 128;  // 0..255: the 8 writer warps (4..11)
+    if (wt == 0) {
+      int off = 0;
+      for (int b = b_first, i = 0; b <= b_last; ++b, ++i) {
+        const int y0 = b == b_first ? (m_first - b * im.HoWo) / im.Wo : 0;
+        const int y1 = b == b_last ? (m_last - b * im.HoWo) / im.Wo : Ho - 1;
+        const int r0 = max(0, y0 - im.pad), r1 = min(im.H - 1, y1 - im.pad + im.KH - 1);
+        img_off[i] = off;
+        img_r0[i] = r0;
+        off += max(0, r1 - r0 + 1) * im.W * PS;
+      }
+      img_off[nimg] = off;
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    {
+      uint4* z = reinterpret_cast<uint4*>(band);
+      for (int i = wt; i < img_off[nimg] / 16; i += 256) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    for (int i = 0; i < nimg; ++i) {  // one warp per input pixel, lanes along its C contiguous channels
+      const int npx = (img_off[i + 1] - img_off[i]) / PS;
+      const uint8_t* src = im.lat + ((int64_t(b_first + i) * im.H + img_r0[i]) * im.W) * im.C;
+      uint8_t* dst = band + img_off[i];
+      for (int px = warp - 4; px < npx; px += 8)
+        for (int c = lane; c < im.C; c += 32) dst[px * PS + c] = __ldg(src + int64_t(px) * im.C + c) < im.T ? 1 : 0;
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    // then row r of every stage's A tile from the band: warps 4-7 the K bytes 0-63, warps 8-11 64-127
+    const int r = wt & 127, kh = wt >> 7, m = m_first + r;
+    const bool mv = m <= m_last;
+    const int b = mv ? m / im.HoWo : b_first, rem = m - b * im.HoWo;
+    const int y = mv ? rem / im.Wo : 0, x = mv ? rem - y * im.Wo : 0;
+    const uint8_t* bb = band + img_off[b - b_first];
+    const int r0 = img_r0[b - b_first], Cp = p.Cp, KK = im.KH * im.KW;
+    const uint32_t rofs = uint32_t(r >> 3) * 1024u + uint32_t(r & 7) * 16u;
+    // (ky, kx, c0) of the row's first 16-byte column of stage kt0, advanced incrementally
+    int k = kt0 * kTcKT + kh * (kTcKT / 2), kyx = k / Cp, c0 = k - kyx * Cp, ky = kyx / im.KW, kx = kyx - ky * im.KW;
+    for (int kt = kt0; kt < kt1; ++kt) {
+      const int s = (kt - kt0) % kTcStages, u = (kt - kt0) / kTcStages;
+      if (kt - kt0 >= kTcStages) mbar_wait(smem_u32(&empty_bar[s]), (u - 1) & 1);
+      uint8_t* at = smem + size_t(s) * stage_bytes;
+      if (Cp % kTcKT == 0) {  // the stage's 128 K bytes are 128 channels of ONE input pixel
+        const int kq = kt * kTcKT + kh * (kTcKT / 2), kq_yx = kq / Cp, cq = kq - kq_yx * Cp, kqy = kq_yx / im.KW, kqx = kq_yx - kqy * im.KW;
+        const int iy = y + kqy - im.pad, ix = x + kqx - im.pad;
+        const bool ok = mv && kq_yx < KK && iy >= 0 && iy < im.H && ix >= 0 && ix < im.W;
+        const uint4* src = reinterpret_cast<const uint4*>(bb + ((iy - r0) * im.W + ix) * (Cp + 16) + cq);
+        uint4 v[kTcKT / 32];
+#pragma unroll
+        for (int k16 = 0; k16 < kTcKT / 32; ++k16) v[k16] = ok ? src[k16] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int k16 = 0; k16 < kTcKT / 32; ++k16) *reinterpret_cast<uint4*>(at + rofs + (kh * 4 + k16) * 128) = v[k16];
+      } else {
+#pragma unroll
+      for (int k16 = kh * 4; k16 < kh * 4 + kTcKT / 32; ++k16) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        const int iy = y + ky - im.pad, ix = x + kx - im.pad;
+        if (mv && kyx < KK && iy >= 0 && iy < im.H && ix >= 0 && ix < im.W)
+          v = *reinterpret_cast<const uint4*>(bb + ((iy - r0) * im.W + ix) * (Cp + 16) + c0);
+        *reinterpret_cast<uint4*>(at + rofs + k16 * 128) = v;
+        c0 += 16;
+        if (c0 == Cp) { c0 = 0; ++kyx; if (++kx == im.KW) { kx = 0; ++ky; } }
+      }
+#pragma unroll
+      for (int k16 = 0; k16 < kTcKT / 32; ++k16) {  // skip the other writer half's 64 K bytes
+        c0 += 16;
+        if (c0 == Cp) { c0 = 0; ++kyx; if (++kx == im.KW) { kx = 0; ++ky; } }
+      }
+      }
+      fence_proxy_async_smem();  // the generic-proxy stores, visible to the tensor core's async proxy
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&full_bar[s]));
+    }
+  }
+  if (warp == 0 || (impl && warp >= 4)) {
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = (2u << 4)                       // D format: s32
@@ -359,7 +462,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const uint8_t* _
       umma_commit(smem_u32(&empty_bar[s]));  // frees the stage once these MMAs have read it
     }
     umma_commit(smem_u32(&done_bar));
-  } else if (warp >= 4) {
+  }
+  if (warp >= 4 && warp < 8) {
     // ---------------- epilogue: TMEM -> registers -> exact recombination -> (lat, v) ----------------
     mbar_wait(smem_u32(&done_bar), 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -466,7 +570,36 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
     launch_k(tc_prep_b16_kernel, dim3(int(blocks)), dim3(256), 0, s, w, F, R, KH * KW, p, bq, error_word_ptr(s));
     note_launch();
   }
-  if (aq_pre) {  // prepared by snn_conv_inf_prepare
+  // K8 implicit im2col: channels-last input on the (ky, kx, c) path, every tile's footprint (the input rows
+  // of its images' output rows, full width, Cp channels) fits next to the pipeline stages
+  TcImpl im{};
+  const int smem_stages = kTcStages * (kTcM * kTcKT + p.N * kTcKT) + 1024;
+  // Opt-in (SNN_TC_IMPLICIT=1): measured on C2's third layer 0.180 ms against 0.153 ms for the explicit
+  // prep + bulk-copy GEMM (8 A-writer warps; 4 warps: 0.216 ms) -- per stage the writers' 16-byte loads
+  // and stores add ~19 % shared-memory traffic to the MMA's reads and the bulk copies, and every feature
+  // chunk's CTA rebuilds the same A tile, which costs more than the prep kernel's HBM round trip saves.
+  if (!aq_pre && p.hwc && in_nhwc && p.Mt <= 65536 && getenv("SNN_TC_IMPLICIT") && getenv("SNN_TC_IMPLICIT")[0] == '1') {
+    const int HoWo = Ho * Wo;
+    long foot = 0;
+    for (int mt = 0; mt < p.Mt && foot >= 0; ++mt) {
+      const int m0 = mt * kTcM, m1 = (m0 + kTcM < p.M ? m0 + kTcM : p.M) - 1;
+      if (m1 / HoWo - m0 / HoWo + 1 > kTcMaxImg) { foot = -1; break; }
+      long f = 0;
+      for (int b = m0 / HoWo; b <= m1 / HoWo; ++b) {
+        const int y0 = b == m0 / HoWo ? (m0 - b * HoWo) / Wo : 0, y1 = b == m1 / HoWo ? (m1 - b * HoWo) / Wo : Ho - 1;
+        const int r0 = y0 - pad > 0 ? y0 - pad : 0, r1 = y1 - pad + KH - 1 < H - 1 ? y1 - pad + KH - 1 : H - 1;
+        f += long(r1 >= r0 ? r1 - r0 + 1 : 0) * W * (p.Cp + 16);
+      }
+      if (f > foot) foot = f;
+    }
+    foot = (foot + 15) & ~15L;
+    if (foot >= 0 && smem_stages + foot <= 227 * 1024) {
+      im.lat = lat_in; im.C = C; im.H = H; im.W = W; im.pad = pad; im.KH = KH; im.KW = KW; im.Wo = Wo;
+      im.HoWo = HoWo; im.T = T; im.foot = int(foot);
+    }
+  }
+  if (im.lat) {
+  } else if (aq_pre) {  // prepared by snn_conv_inf_prepare
     aq = const_cast<uint8_t*>(aq_pre);
   } else {
     if (p.hwc) {
@@ -486,11 +619,14 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
   }
   uint32_t cols = 32;
   while (cols < uint32_t(p.N)) cols <<= 1;
-  const int smem = kTcStages * (kTcM * kTcKT + p.N * kTcKT) + 1024;
+  const int smem = smem_stages + im.foot;
   cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_conv_fire(tc): %s", cudaGetErrorString(e));
-  launch_k(conv_tc_kernel, dim3(unsigned(int64_t(p.Mt) * p.nch * p.KS)), dim3(kTcThreads), smem, s, aq, bq, p, F, Ho * Wo, T, cols,
-                                                                               lat_out, v_out, part, nhwc);
+  if (getenv("SNN_DEBUG_PLAN"))
+    fprintf(stderr, "tc plan: Mt %d nch %d KS %d N %d Kt %d hwc %d implicit %d foot %d smem %d\n", p.Mt, p.nch, p.KS, p.N,
+            p.Kt, p.hwc, im.lat != nullptr, im.foot, smem);
+  launch_k(conv_tc_kernel, dim3(unsigned(int64_t(p.Mt) * p.nch * p.KS)), dim3(im.lat ? kTcThreads + 128 : kTcThreads), smem,
+           s, aq, bq, p, F, Ho * Wo, T, cols, lat_out, v_out, part, nhwc, im);
   note_launch();
   if (part) {
     const int64_t n = int64_t(p.M) * F;
@@ -973,7 +1109,7 @@ int rstdp_inf_sequence_launch(const void* prep, int b0, int N, int C, int H, int
   for (int i = 0; i < N; ++i) {
     const uint8_t* aq = static_cast<const uint8_t*>(prep) + size_t(b0 + i) * p.a_bytes;
     if (!(dbg & 2)) launch_k(conv_tc_kernel, dim3(unsigned(int64_t(p.Mt) * p.nch * p.KS)), dim3(kTcThreads), smem, s, aq,
-             (const uint8_t*)bq, p, F, Ho * Wo, T, cols, (uint8_t*)nullptr, (float*)nullptr, part, 0);
+             (const uint8_t*)bq, p, F, Ho * Wo, T, cols, (uint8_t*)nullptr, (float*)nullptr, part, 0, TcImpl{});
     launch_k(rstdp_inf_tail1_kernel, dim3(t1 > 0 ? t1 : 1), dim3(256), 0, s, part, Ho * Wo, Wo, F, T, labels, i,
              n_classes, stp, winners + 3 * i, count + i, decision ? decision + i : nullptr,
              reward ? reward + i : nullptr, dbg);

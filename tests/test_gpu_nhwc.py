@@ -226,3 +226,34 @@ def test_conv_fire_rows_vs_oracle(G, orc, case, out_nhwc, g, capfd, monkeypatch)
     assert np.array_equal(host(lat), ol)
     assert np.array_equal(host(v), ov)
 
+
+
+# ------------------------------------------------------- K8 implicit im2col (theta = inf, tcgen05 GEMM)
+IMPLICIT_CASES = [
+    # (B, C, H, W, pad, F, K, p_spike)
+    (320, 250, 4, 4, 2, 200, 5, 0.9),    # C2 L3 shape (8 images per M tile, 6 pad channels)
+    (300, 32, 9, 11, 1, 40, 3, 0.5),     # tiles cross image boundaries mid-row
+    (400, 16, 5, 7, 0, 24, 3, 0.7),      # 3 x 5 outputs: 9 images per tile, no padding
+    (300, 64, 12, 12, 2, 70, 5, 0.3),    # 2 feature chunks, partial rows at both tile ends
+]
+
+
+@pytest.mark.parametrize("case", IMPLICIT_CASES)
+def test_conv_inf_implicit_vs_oracle(G, orc, case, capfd, monkeypatch):
+    """K8 (opt-in): the A operand built in the GEMM CTA from the staged binary S[T-1] footprint (Eq. 5),
+    bit-exact."""
+    monkeypatch.setenv("SNN_DEBUG_PLAN", "1")
+    monkeypatch.setenv("SNN_TC_IMPLICIT", "1")
+    B, C, H, W, pad, F, K, p = case
+    T = 15
+    rng = np.random.default_rng(abs(hash(case)) % 2 ** 31)
+    import synth
+    lat_in = synth.random_latencies(rng, (B, C, H, W), T, p)
+    w = exact_weights(rng, (F, C, K, K))
+    lat, v = G.conv_fire(cu(np.ascontiguousarray(lat_in.transpose(0, 2, 3, 1))), cu(w), pad, T, math.inf,
+                         nhwc=True, in_nhwc=True)
+    G.sync_status()
+    assert "implicit 1" in capfd.readouterr().err
+    ol, ov = orc.conv_fire(lat_in, w, pad, T, math.inf)
+    assert np.array_equal(host(lat), ol.transpose(0, 2, 3, 1))
+    assert np.array_equal(host(v), ov.transpose(0, 2, 3, 1))
