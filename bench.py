@@ -168,8 +168,11 @@ class C2Step:
         mark(0)
         snn.filter_bank(self.raw if src is None else src, self.bank, fr["pad"], mode=fr["mode"], out=self.x); mark(1)
         n.encode(self.x); mark(2)         # channels-last maps from here to layer 3's input
-        n.l1.conv(n.lat0_buf); mark(3)    # no potentials: pool1 needs none
-        n.l1.pool(); mark(4)
+        if n.l1.fuse_pool:                # conv1 + its 2 x 2 pooling in one launch (K7, SNN_CONV_POOL2)
+            n.l1.conv_pool(n.lat0_buf); mark(3); mark(4)
+        else:
+            n.l1.conv(n.lat0_buf); mark(3)    # no potentials: pool1 needs none
+            n.l1.pool(); mark(4)
         n.l2.conv(n.l1.out_lat); mark(5)
         n.l2.pool(); mark(6)
         n.l3.conv(n.l2.out_lat); mark(7)
@@ -197,6 +200,7 @@ class C2Step:
         """(paper events per batch, necessary events per conv layer) -- off the clock."""
         n, snn, T = self.net, self.snn, self.wl.T
         self.run()
+        n.l1.conv(n.lat0_buf)             # the unpooled conv1 map (the fused step writes only its pooling)
         out = {}
         for name, lat_in, spec, lo in (("conv1", n.lat0, self.wl.convs[0], n.l1.lat),
                                        ("conv2", n.l1.plat, self.wl.convs[1], n.l2.lat),

@@ -156,6 +156,16 @@ SNN_API int snn_conv_fire(const uint8_t* lat_in, int B, int C, int H, int W, int
  * needs spike times, e.g. latency-only pooling).  Unknown flag bits: SNN_EINVAL. */
 #define SNN_CONV_OUT_NHWC 1
 #define SNN_CONV_IN_NHWC 2
+/*   SNN_CONV_POOL2     (with SNN_CONV_OUT_NHWC | SNN_CONV_IN_NHWC, a finite theta, v_out = pot_out = NULL):
+ *                      lat_out receives the 2 x 2 / stride 2 / unpadded latency pooling of the layer's
+ *                      spike times instead of the spike times themselves -- [B, Ho/2, Wo/2, F] channels-last
+ *                      (floor; the pooled map of snn_pool_ex(lat, NULL, ..., 2, 2, 2, 2, 0, 0,
+ *                      SNN_POOL_IN_NHWC | SNN_POOL_OUT_NHWC), Eq. 3 with A10/A11/A12), fused
+ *                      into the row-tile walk (the unpooled map never reaches memory).  SNN_EINVAL for the
+ *                      other options; SNN_ESHAPE (before any launch) when the row-tile walk does not apply
+ *                      (latency-sized batches, F > 32, receptive fields past its shared-memory budget) --
+ *                      the caller then runs snn_conv_fire_ex + snn_pool_ex. */
+#define SNN_CONV_POOL2 4
 SNN_API int snn_conv_fire_ex(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F,
                              int KH, int KW, int T, float theta, int flags, uint8_t* lat_out, float* v_out,
                              float* pot_out, void* ws, size_t ws_bytes, snn_stream_t s);

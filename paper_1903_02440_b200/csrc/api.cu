@@ -23,7 +23,7 @@ int conv_fire_plan(int B, int C, int H, int W, int pad, int F, int KH, int KW, i
                    int* launches, int* chunks);
 int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
                      int KW, int T, float theta, uint8_t* lat_out, float* v_out, float* pot_out, void* ws,
-                     size_t ws_bytes, cudaStream_t s, int nhwc, int in_nhwc);
+                     size_t ws_bytes, cudaStream_t s, int nhwc, int in_nhwc, int pool2 = 0);
 int pool_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, int PH, int PW, int SH, int SW,
                 int DH, int DW, int flags, uint8_t* lat_out, float* v_out, cudaStream_t s);
 int inhibit_launch(const uint8_t* lat, const float* v, int B, int F, int H, int W, uint8_t* lat_out, float* v_out,
@@ -329,12 +329,14 @@ int snn_conv_fire_ex(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
                      size_t ws_bytes, snn_stream_t s) {
   int rc = conv_checks(B, C, H, W, pad, F, KH, KW, T, theta);
   if (rc) return rc;
-  REQUIRE((flags & ~(SNN_CONV_OUT_NHWC | SNN_CONV_IN_NHWC)) == 0, SNN_EINVAL, "snn_conv_fire: unknown flags 0x%x", flags);
+  REQUIRE((flags & ~(SNN_CONV_OUT_NHWC | SNN_CONV_IN_NHWC | SNN_CONV_POOL2)) == 0, SNN_EINVAL,
+          "snn_conv_fire: unknown flags 0x%x", flags);
   if (B == 0 || F == 0) return SNN_OK;
   REQUIRE(lat_in && w && lat_out, SNN_EINVAL, "snn_conv_fire: NULL tensor");
   REQUIRE(ws, SNN_EWORKSPACE, "snn_conv_fire: NULL workspace");
   return conv_fire_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, theta, lat_out, v_out, pot_out, ws, ws_bytes,
-                          S(s), (flags & SNN_CONV_OUT_NHWC) ? 1 : 0, (flags & SNN_CONV_IN_NHWC) ? 1 : 0);
+                          S(s), (flags & SNN_CONV_OUT_NHWC) ? 1 : 0, (flags & SNN_CONV_IN_NHWC) ? 1 : 0,
+                          (flags & SNN_CONV_POOL2) ? 1 : 0);
 }
 
 int snn_conv_fire(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH, int KW,

@@ -442,7 +442,7 @@ static int conv_path_override() {
 }
 int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
                      int KW, int T, float theta, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes,
-                     cudaStream_t s, int nhwc, int in_nhwc);
+                     cudaStream_t s, int nhwc, int in_nhwc, int pool2 = 0);
 
 static int conv_path_override();
 int conv_walk_describe(int B, int C, int H, int W, int pad, int F, int KH, int KW, int T, int* pre, int* chunks,
@@ -503,7 +503,7 @@ size_t conv_fire_workspace(int B, int C, int H, int W, int pad, int F, int KH, i
 
 int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
                      int KW, int T, float theta, uint8_t* lat_out, float* v_out, float* pot_out, void* ws,
-                     size_t ws_bytes, cudaStream_t s, int nhwc, int in_nhwc) {
+                     size_t ws_bytes, cudaStream_t s, int nhwc, int in_nhwc, int pool2) {
   const bool inf = isinf(theta) && theta > 0;
   ConvPlan pl;
   make_plan(B, C, H, W, pad, F, KH, KW, T, inf, &pl);
@@ -517,6 +517,14 @@ int conv_fire_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   } else a.thr = INT64_MAX;
   const int64_t npos = int64_t(B) * a.Ho * a.Wo;
   if (npos == 0 || F == 0) return SNN_OK;
+  if (pool2) {  // SNN_CONV_POOL2: only the row-tile walk fuses the pooling (checked before any launch)
+    if (inf || pot_out || v_out || !nhwc || !in_nhwc || conv_path_override() != 1)
+      return set_error(SNN_EINVAL, "snn_conv_fire: SNN_CONV_POOL2 needs a finite threshold, channels-last input and "
+                                   "output, v_out = pot_out = NULL and the default path");
+    const int rc = conv_walk_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, theta, lat_out, v_out, ws, ws_bytes, s,
+                                    nhwc, in_nhwc, 1);
+    return rc == 1 ? set_error(SNN_ESHAPE, "snn_conv_fire: SNN_CONV_POOL2: the row-tile walk does not apply") : rc;
+  }
   if (inf && !pot_out)  // Eq. 5: dense contraction of S[T-1] on the tensor cores
     return conv_tc_launch(lat_in, B, C, H, W, pad, w, F, KH, KW, T, lat_out, v_out, ws, ws_bytes, s, nullptr, nhwc,
                           in_nhwc);

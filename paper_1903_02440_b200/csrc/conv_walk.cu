@@ -257,12 +257,18 @@ __device__ __forceinline__ void walk_rows(const WalkArgs& a, unsigned char* smem
                        (reinterpret_cast<uintptr_t>(a.v_out) % (4 * FPL)) == 0;
   const uint32_t wl = smem_u32(smem + gl * FPL * 4), lb = smem_u32(list);
   const uint32_t rb = uint32_t(a.row_bytes), cstep = uint32_t(a.C) * rb;
-  const int HoWo = a.Ho * a.Wo, per_img = a.Ho * a.nseg;
+  // pool2 (SNN_CONV_POOL2): a unit is the output row PAIR (2 py, 2 py + 1) of one tile; the pair's
+  // latencies stay in the warp's shared-memory row buffer and only the 2 x 2 / stride 2 minimum is stored
+  const int rpu = a.pool2 ? 2 : 1, ny = a.Ho / rpu;
+  uint32_t* rowbuf = reinterpret_cast<uint32_t*>(wbase + a.pool_off);  // [2][nx][LPP] latency words
+  const int HoWo = a.Ho * a.Wo, per_img = ny * a.nseg;
   const int64_t units = int64_t(a.B) * per_img;
   for (int64_t u = int64_t(blockIdx.x) * nwarps + warp; u < units; u += int64_t(gridDim.x) * nwarps) {
     const int b = int(u / per_img), rem = int(u - int64_t(b) * per_img);
-    const int y = rem / a.nseg, x0 = (rem - y * a.nseg) * a.nx;
+    const int yu = rem / a.nseg, x0 = (rem - yu * a.nseg) * a.nx;
     const int nxs = min(a.nx, a.Wo - x0), ncol = nxs + a.KW - 1;
+    for (int h = 0; h < rpu; ++h) {
+    const int y = yu * rpu + h;
     rows_sort(a, b, y, x0, ncol, colof, cnt, base, list, lane);
     for (int q0 = 0; q0 < nxs; q0 += PPW) {
       const int xr = q0 + grp;
@@ -275,7 +281,9 @@ __device__ __forceinline__ void walk_rows(const WalkArgs& a, unsigned char* smem
       else
         walk_rows_lockstep<FPL, PPW, S28, 1>(a, wl - uint32_t(xr) * cstep, uint32_t(a.R) * rb + uint32_t(xr) * cstep,
                                              base + xr, ncol, lb, pv, valid, lo, vo);
-      if (pv) {
+      if (a.pool2) {
+        if (pv) rowbuf[(h * a.nx + xr) * LPP + gl] = lo;
+      } else if (pv) {
         const int p = b * HoWo + y * a.Wo + x0 + xr;
         int64_t o0 = int64_t(p) * a.F + fbase;
         if (!a.nhwc) o0 = (int64_t(b) * a.F + fbase) * HoWo + (p - b * HoWo);
@@ -301,6 +309,30 @@ __device__ __forceinline__ void walk_rows(const WalkArgs& a, unsigned char* smem
       }
     }
     __syncwarp();
+    }
+    if (a.pool2) {  // lat_o = min over the 2 x 2 window (R: pool, latency-only), channels-last [B, Ho/2, Wo/2, F]
+      const int nx2 = nxs >> 1, PWo = a.Wo >> 1;
+      for (int i = lane; i < nx2 * LPP; i += 32) {
+        const int px = i / LPP, qd = i - px * LPP, f0 = qd * FPL;
+        if (f0 >= a.F) continue;
+        const uint32_t* r0 = rowbuf + (2 * px) * LPP + qd;
+        const uint32_t* r1 = r0 + a.nx * LPP;
+        const uint32_t m = __vminu4(__vminu4(r0[0], r0[LPP]), __vminu4(r1[0], r1[LPP]));
+        uint8_t* o = a.lat_out + ((int64_t(b) * ny + yu) * PWo + (x0 >> 1) + px) * a.F + f0;
+        const int nf = min(FPL, a.F - f0);
+        if (nf == 4 && (reinterpret_cast<uintptr_t>(o) & 3) == 0) {
+          *reinterpret_cast<uint32_t*>(o) = m;
+        } else if ((reinterpret_cast<uintptr_t>(o) & 1) == 0) {
+          if (nf >= 2) *reinterpret_cast<uint16_t*>(o) = uint16_t(m);
+          if (nf == 4) *reinterpret_cast<uint16_t*>(o + 2) = uint16_t(m >> 16);
+          else if (nf == 3) o[2] = uint8_t(m >> 16);
+          else if (nf == 1) o[0] = uint8_t(m);
+        } else {
+          for (int j = 0; j < nf; ++j) o[j] = uint8_t(m >> (8 * j));
+        }
+      }
+      __syncwarp();
+    }
   }
 }
 
@@ -599,6 +631,7 @@ static bool rows_plan(WalkPlan& pl) {
   if (const char* e = getenv("SNN_WALK_ROWS")) if (e[0] == '0') return false;
   WalkArgs& a = pl.a;
   if (pl.pre || pl.ppw != 4 || pl.fpl != 4 || !a.in_nhwc) return false;
+  if (a.pool2 && (a.Ho < 2 || a.Wo < 2 || !a.nhwc || a.v_out)) return false;
   a.nseg = int(ceil_div(a.Wo, 32));
   a.nx = int(ceil_div(ceil_div(a.Wo, a.nseg), 4)) * 4;
   const int ncolmax = a.nx + a.KW - 1;
@@ -608,7 +641,8 @@ static bool rows_plan(WalkPlan& pl) {
   a.cnt_off = 0;
   a.start_off = al16(a.T * ncolmax * 4);
   a.list_off = a.start_off + al16((a.T * ncolmax + 1) * 2);
-  a.warp_bytes = a.list_off + al16(a.KH * ncolmax * a.C * 2);
+  a.pool_off = a.list_off + al16(a.KH * ncolmax * a.C * 2);
+  a.warp_bytes = a.pool_off + (a.pool2 ? al16(2 * a.nx * 8 * 4) : 0);
   a.off_eoff = al16(int(long(a.R + 1) * pl.FGS * 4));
   a.off_warps = a.off_eoff + al16(ncolmax * a.C);
   int nw = int((kWalkSmemLimit - a.off_warps) / a.warp_bytes);
@@ -628,7 +662,7 @@ static int rows_go(const WalkPlan& pl, const WalkArgs& a, cudaStream_t s) {
   auto k = conv_walk_kernel<4, 4, false, false, false, false, false, true>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_conv_fire(rows): %s", cudaGetErrorString(e));
-  const int64_t units = int64_t(a.B) * a.Ho * a.nseg;
+  const int64_t units = int64_t(a.B) * (a.pool2 ? a.Ho / 2 : a.Ho) * a.nseg;
   const int64_t per = ceil_div(units, pl.nwarps);
   const int64_t want = num_sms();
   launch_k(k, dim3(int(per < want ? per : want)), dim3(pl.nwarps * 32), pl.smem, s, a);
@@ -689,7 +723,7 @@ int conv_walk_describe(int B, int C, int H, int W, int pad, int F, int KH, int K
 // Returns 1 if this path does not apply (caller falls back), else an SNN code.
 int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, const float* w, int F, int KH,
                      int KW, int T, float theta, uint8_t* lat_out, float* v_out, void* ws, size_t ws_bytes,
-                     cudaStream_t s, int nhwc, int in_nhwc) {
+                     cudaStream_t s, int nhwc, int in_nhwc, int pool2) {
   WalkPlan pl;
   if (!walk_plan(B, C, H, W, pad, F, KH, KW, T, &pl)) return 1;
   WalkArgs a = pl.a;
@@ -711,6 +745,12 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
             "warps %d smem %d | rec %d hdr %d chunk %lld npos %lld gw %d\n", int(pl.pre), pl.fpl, pl.ppw, pl.FGS,
             pl.n_groups, pl.nwarps, pl.smem, pl.sort_ppw, pl.sort_nwarps, pl.sort_smem, a.rec,
             a.hdr, (long long)pl.chunk, (long long)npos, int(pl.gw));
+  // K7 row tiles (decided before any launch: SNN_CONV_POOL2 needs them)
+  WalkPlan rp = pl;
+  rp.a = a;
+  rp.a.pool2 = pool2;
+  const bool rows = !pl.pre && rows_plan(rp);
+  if (pool2 && !rows) return 1;
   if (!pl.pre && pl.ppw == 1) {  // latency mode (few positions): the walk converts the weights itself
     a.wf32 = w;
     a.p0 = 0; a.np = npos;
@@ -732,15 +772,12 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   if (rc) return rc;
   if (!pl.pre) {
     a.p0 = 0; a.np = npos;
-    {
-      WalkPlan rp = pl;
-      rp.a = a;
-      if (rows_plan(rp)) {
-        if (getenv("SNN_DEBUG_PLAN"))
-          fprintf(stderr, "walk rows: nx %d nseg %d warps %d smem %d g %d\n", rp.a.nx, rp.a.nseg, rp.nwarps, rp.smem,
-                  rp.a.rows_g);
-        return rows_go(rp, rp.a, s);
-      }
+    if (rows) {
+      rp.a.wq = a.wq; rp.a.kstar = a.kstar;
+      if (getenv("SNN_DEBUG_PLAN"))
+        fprintf(stderr, "walk rows: nx %d nseg %d warps %d smem %d g %d pool2 %d\n", rp.a.nx, rp.a.nseg, rp.nwarps,
+                rp.smem, rp.a.rows_g, rp.a.pool2);
+      return rows_go(rp, rp.a, s);
     }
     switch (pl.ppw * 10 + pl.fpl) {
       case 44: return walk_go<4, 4, false>(pl, a, s);

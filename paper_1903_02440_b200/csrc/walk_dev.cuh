@@ -64,6 +64,7 @@ struct WalkArgs {
   // output row once, by (spike time, halo column); nseg tiles per output row
   int nx, nseg;
   int rows_g;         // K7c: buckets per threshold test of the row-tile walk (1, 2)
+  int pool2, pool_off; // SNN_CONV_POOL2: 2 x 2 / stride 2 latency pooling fused into the row-tile walk
 };
 
 static inline int al16(int x) { return (x + 15) & ~15; }

@@ -34,7 +34,7 @@ class Layer:
 
     def __init__(self, spec, w: torch.Tensor, B: int, C: int, H: int, W: int, T: int, pool_spec=None,
                  pool_v: bool = True, device="cuda", nhwc: bool = False, want_v: bool = True,
-                 in_nhwc: bool = False, pool_out_nhwc: bool = False):
+                 in_nhwc: bool = False, pool_out_nhwc: bool = False, fuse_pool: bool = False):
         self.spec, self.w, self.T = spec, w, T
         self.B, self.C, self.H, self.W = B, C, H, W
         self.Ho, self.Wo = snn.conv_out_hw(H, W, spec.KH, spec.KW, spec.pad)
@@ -56,6 +56,13 @@ class Layer:
             pshape = (B, self.PHo, self.PWo, F) if pool_out_nhwc else (B, F, self.PHo, self.PWo)
             self.plat_buf = torch.empty(pshape, dtype=torch.uint8, device=device)
             self.pv_buf = torch.empty(pshape, dtype=torch.float32, device=device) if pool_v else None
+        # fuse_pool: 2 x 2 / stride 2 latency-only pooling inside the conv (SNN_CONV_POOL2, K7 row tiles);
+        # the unpooled map (lat) is then not written.  The library declines (SNN_ESHAPE, before any launch)
+        # where the row-tile walk does not apply; the layer then runs conv + pool from then on.
+        self.fuse_pool = bool(fuse_pool and pool_spec is not None and not pool_v and not want_v and nhwc and in_nhwc
+                              and pool_out_nhwc and math.isfinite(spec.theta) and
+                              (pool_spec.PH, pool_spec.PW, pool_spec.SH, pool_spec.SW, pool_spec.DH, pool_spec.DW)
+                              == (2, 2, 2, 2, 0, 0))
 
     @staticmethod
     def _planar(t, nhwc):
@@ -102,10 +109,26 @@ class Layer:
         snn.pool(self.lat_buf, self.v_buf if self.pv_buf is not None else None, (p.PH, p.PW), (p.SH, p.SW),
                  (p.DH, p.DW), lat_out=self.plat_buf, v_out=self.pv_buf, flags=flags)
 
-    def __call__(self, lat_in: torch.Tensor, w: Optional[torch.Tensor] = None):
+    def conv_pool(self, lat_in: torch.Tensor, w: Optional[torch.Tensor] = None):
+        """conv + pool: fused into one launch when fuse_pool holds (plat only), else the two calls."""
+        if self.fuse_pool:
+            s = self.spec
+            try:
+                snn.conv_fire(lat_in, self.w if w is None else w, s.pad, self.T, s.theta, lat_out=self.plat_buf,
+                              ws=self.ws, nhwc=True, want_v=False, in_nhwc=True, pool2=True)
+                return
+            except snn.SNNError as e:
+                if e.code != snn.SNN_ESHAPE:
+                    raise
+                self.fuse_pool = False
         self.conv(lat_in, w)
+        self.pool()
+
+    def __call__(self, lat_in: torch.Tensor, w: Optional[torch.Tensor] = None):
         if self.pool_spec is not None:
-            self.pool()
+            self.conv_pool(lat_in, w)
+        else:
+            self.conv(lat_in, w)
         return self.out_lat
 
 
@@ -117,7 +140,7 @@ class C2Net:
     (encode -> conv1 -> pool1 -> conv2 -> pool2 -> conv3's input); conv_v False: layers 1 and 2 write
     no potentials (their latency-only pools need none).  Layer 3's output stays planar."""
 
-    def __init__(self, wl, B: int, device="cuda", nhwc: bool = True, conv_v: bool = False):
+    def __init__(self, wl, B: int, device="cuda", nhwc: bool = True, conv_v: bool = False, fuse_pool: bool = True):
         self.wl, self.B, self.T = wl, B, wl.T
         _, C, H, W = wl.X.shape
         self.nhwc = nhwc
@@ -126,7 +149,7 @@ class C2Net:
         self.w = [_dev(w, device) for w in wl.weights]
         s1, s2, s3 = wl.convs
         self.l1 = Layer(s1, self.w[0], B, C, H, W, wl.T, wl.pools[0], pool_v=False, device=device, nhwc=nhwc,
-                        want_v=conv_v, in_nhwc=nhwc, pool_out_nhwc=nhwc)
+                        want_v=conv_v, in_nhwc=nhwc, pool_out_nhwc=nhwc, fuse_pool=fuse_pool)
         self.l2 = Layer(s2, self.w[1], B, s1.F, self.l1.PHo, self.l1.PWo, wl.T, wl.pools[1], pool_v=False,
                         device=device, nhwc=nhwc, want_v=conv_v, in_nhwc=nhwc, pool_out_nhwc=nhwc)
         self.l3 = Layer(s3, self.w[2], B, s2.F, self.l2.PHo, self.l2.PWo, wl.T, None, device=device, in_nhwc=nhwc)

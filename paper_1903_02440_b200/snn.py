@@ -241,16 +241,17 @@ def conv_fire_workspace(B, C_, H, W, pad, F, KH, KW, T, theta) -> int:
     return int(lib().snn_conv_fire_workspace(B, C_, H, W, pad, F, KH, KW, T, float(theta)))
 
 
-CONV_OUT_NHWC, CONV_IN_NHWC = 1, 2  # snn_conv_fire_ex flags
+CONV_OUT_NHWC, CONV_IN_NHWC, CONV_POOL2 = 1, 2, 4  # snn_conv_fire_ex flags
 
 
 def conv_fire(lat_in: torch.Tensor, w: torch.Tensor, pad: int, T: int, theta: float, want_pot: bool = False,
               lat_out=None, v_out=None, ws=None, stream=None, nhwc: bool = False, want_v: bool = True,
-              in_nhwc: bool = False):
+              in_nhwc: bool = False, pool2: bool = False):
     """lat_in uint8 [B, C, H, W], w float32 [F, C, KH, KW] -> (lat uint8, v float32) [B, F, Ho, Wo]
     (+ pot float32 [B, T, F, Ho, Wo] when want_pot).  nhwc: outputs channels-last [B, Ho, Wo, F]
     (snn_conv_fire_ex SNN_CONV_OUT_NHWC); in_nhwc: lat_in is [B, H, W, C] (SNN_CONV_IN_NHWC);
-    want_v False: v is not written (None returned)."""
+    want_v False: v is not written (None returned).  pool2 (SNN_CONV_POOL2, with nhwc, in_nhwc and
+    want_v False): lat is the 2 x 2 / stride 2 latency pooling [B, Ho // 2, Wo // 2, F] of the spike times."""
     _req(lat_in, torch.uint8, "lat_in")
     _req(w, torch.float32, "w")
     if in_nhwc:
@@ -264,6 +265,8 @@ def conv_fire(lat_in: torch.Tensor, w: torch.Tensor, pad: int, T: int, theta: fl
     Ho, Wo = max(Ho, 0), max(Wo, 0)          # invalid shapes are rejected by the library (SNN_ESHAPE)
     dev = lat_in.device
     shape = (B, Ho, Wo, F) if nhwc else (B, F, Ho, Wo)
+    if pool2:
+        shape = (B, Ho // 2, Wo // 2, F)
     lat = lat_out if lat_out is not None else torch.empty(shape, dtype=torch.uint8, device=dev)
     v = None
     if want_v:
@@ -272,7 +275,8 @@ def conv_fire(lat_in: torch.Tensor, w: torch.Tensor, pad: int, T: int, theta: fl
     n = conv_fire_workspace(B, C_, H, W, pad, F, KH, KW, T, theta)
     buf = ws if ws is not None else _ws.get(n, dev, "conv", stream)
     _check(lib().snn_conv_fire_ex(_ptr(lat_in), B, C_, H, W, pad, _ptr(w), F, KH, KW, T, float(theta),
-                                  (CONV_OUT_NHWC if nhwc else 0) | (CONV_IN_NHWC if in_nhwc else 0), _ptr(lat),
+                                  (CONV_OUT_NHWC if nhwc else 0) | (CONV_IN_NHWC if in_nhwc else 0) |
+                                  (CONV_POOL2 if pool2 else 0), _ptr(lat),
                                   _ptr(v), _ptr(pot), _ptr(buf), buf.numel(),
                                   _stream(stream)))
     return (lat, v, pot) if want_pot else (lat, v)

@@ -61,17 +61,21 @@ def c2_ref(orc):
     return wl, flows.c2(wl)
 
 
-@pytest.mark.parametrize("nhwc,conv_v", [(True, False), (True, True), (False, True)])
-def test_c2_parity(G, c2_ref, nhwc, conv_v):
-    """(True, False) is the bench's configuration (channels-last layers 1-2, no unused potentials)."""
+@pytest.mark.parametrize("nhwc,conv_v,fuse", [(True, False, True), (True, False, False), (True, True, True),
+                                              (False, True, True)])
+def test_c2_parity(G, c2_ref, nhwc, conv_v, fuse):
+    """(True, False, True) is the bench's configuration (channels-last layers 1-2, no unused potentials,
+    layer 1's 2 x 2 pooling fused into its conv: SNN_CONV_POOL2)."""
     from paper_1903_02440_b200 import pipeline
     wl, ref = c2_ref
     n = wl.X.shape[0]
-    net = pipeline.C2Net(wl, n, nhwc=nhwc, conv_v=conv_v)
+    net = pipeline.C2Net(wl, n, nhwc=nhwc, conv_v=conv_v, fuse_pool=fuse)
     net.forward(cu(wl.X))
     G.sync_status()
+    assert net.l1.fuse_pool == (nhwc and not conv_v and fuse)
     assert np.array_equal(host(net.lat0), ref["lat0"])
-    assert np.array_equal(host(net.l1.lat), ref["l1"]["lat"])
+    if not net.l1.fuse_pool:  # the fused layer writes only the pooled map
+        assert np.array_equal(host(net.l1.lat), ref["l1"]["lat"])
     assert np.array_equal(host(net.l1.plat), ref["l1"]["pool_lat"])
     assert np.array_equal(host(net.l2.lat), ref["l2"]["lat"])
     if conv_v:

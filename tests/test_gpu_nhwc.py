@@ -257,3 +257,39 @@ def test_conv_inf_implicit_vs_oracle(G, orc, case, capfd, monkeypatch):
     ol, ov = orc.conv_fire(lat_in, w, pad, T, math.inf)
     assert np.array_equal(host(lat), ol.transpose(0, 2, 3, 1))
     assert np.array_equal(host(v), ov.transpose(0, 2, 3, 1))
+
+
+@pytest.mark.parametrize("case", ROWS_CASES)
+def test_conv_fire_pool2_vs_oracle(G, orc, case, capfd, monkeypatch):
+    """SNN_CONV_POOL2: the 2 x 2 / stride 2 latency pooling fused into the row-tile walk equals the oracle's
+    pooling (A10-A12) of the oracle's conv output; odd Ho / Wo drop the last row / column."""
+    monkeypatch.setenv("SNN_DEBUG_PLAN", "1")
+    B, C, H, W, pad, F, K, T, theta, p, lo = case
+    rng = np.random.default_rng(abs(hash(case)) % 2 ** 31)
+    import synth
+    lat_in = synth.random_latencies(rng, (B, C, H, W), T, p)
+    w = exact_weights(rng, (F, C, K, K), lo=lo)
+    lat, v = G.conv_fire(cu(np.ascontiguousarray(lat_in.transpose(0, 2, 3, 1))), cu(w), pad, T, theta,
+                         nhwc=True, in_nhwc=True, want_v=False, pool2=True)
+    G.sync_status()
+    assert v is None and "pool2 1" in capfd.readouterr().err
+    ol, ov = orc.conv_fire(lat_in, w, pad, T, theta)
+    pl, _ = orc.pool(ol, None, 2, 2, 2, 2, 0, 0, T)
+    assert np.array_equal(host(lat), pl.transpose(0, 2, 3, 1))
+
+
+def test_conv_fire_pool2_declined(G):
+    """SNN_CONV_POOL2 where the row-tile walk does not apply: SNN_ESHAPE before any launch; with potentials
+    or a planar output: SNN_EINVAL."""
+    lat_in = torch.zeros((1, 28, 28, 2), dtype=torch.uint8, device="cuda")   # one image: latency mode
+    w = torch.full((30, 2, 5, 5), 0.5, dtype=torch.float32, device="cuda")
+    with pytest.raises(G.SNNError) as e:
+        G.conv_fire(lat_in, w, 2, 15, 15.0, nhwc=True, in_nhwc=True, want_v=False, pool2=True)
+    assert e.value.code == G.SNN_ESHAPE
+    lat_in = torch.zeros((64, 28, 28, 2), dtype=torch.uint8, device="cuda")
+    with pytest.raises(G.SNNError) as e:
+        G.conv_fire(lat_in, w, 2, 15, 15.0, nhwc=True, in_nhwc=True, want_v=True, pool2=True)
+    assert e.value.code == G.SNN_EINVAL
+    with pytest.raises(G.SNNError) as e:
+        G.conv_fire(lat_in, w, 2, 15, math.inf, nhwc=True, in_nhwc=True, want_v=False, pool2=True)
+    assert e.value.code == G.SNN_EINVAL
