@@ -86,13 +86,28 @@ __global__ void __launch_bounds__(256) kstar_kernel(const float* __restrict__ w,
       }
     s_k = k;
   }
+  // kmin (K2e) = min over features of the smallest k such that the sum of f's k LARGEST weights exceeds
+  // the threshold: fewer than kmin spiking inputs cannot fire any feature, so the buckets of a sorted
+  // list that end below kmin entries need no threshold test.  out[1] = max over f of INT_MAX - k_f
+  // (zeroed before; a feature that can never fire contributes 0).
+  if (threadIdx.x == 32) {
+    int64_t acc = 0;
+    int k = 0x7FFFFFFF;
+    if (thr < 0) k = 0;
+    else
+      for (int i = R - 1; i >= 0; --i) {
+        acc += v[i];
+        if (acc > thr) { k = R - i; break; }
+      }
+    atomicMax(out + 1, 0x7FFFFFFF - k);
+  }
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(out, s_k);
   (void)in_nhwc_C; (void)KK;
 }
 
 int kstar_launch(const float* w, int F, int R, int64_t thr, int* out, cudaStream_t s) {
-  if (cudaMemsetAsync(out, 0, sizeof(int), s) != cudaSuccess) return check_launch("snn_conv_fire(K* memset)");
+  if (cudaMemsetAsync(out, 0, 2 * sizeof(int), s) != cudaSuccess) return check_launch("snn_conv_fire(K* memset)");
   launch_k(kstar_kernel, dim3(F), dim3(256), 0, s, w, R, thr, 0, 1, out);
   note_launch();
   return check_launch("snn_conv_fire(K*)");
@@ -765,9 +780,20 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   if (rc) return rc;
   // K* bound for the list truncation (K2b, opt-in with SNN_KSTAR=1: measured no faster -- C2 1.06 ->
   // 1.18 ms for conv1 + conv2, C5 unchanged -- the sort's first pass, not its placements, sets its time)
-  if (a.R <= 4096 && a.thr != INT64_MAX && getenv("SNN_KSTAR")) {
-    rc = kstar_launch(w, F, a.R, a.thr, kstar, s);
-    a.kstar = kstar;
+  // kmin bound for the test-free list prefix (K2e): on for the bucket walk where the threshold needs several
+  // average buckets of inputs (theta >= R / T: C5 conv 27.8 -> 26.1 ms; C2's second layer, whose kmin is about
+  // one bucket, measured 0.676 -> 0.691 ms with it); SNN_KMIN=0 / 1 overrides
+  {
+    const char* ek = getenv("SNN_KMIN");
+    const char* es = getenv("SNN_KSTAR");
+    const bool want_kstar = es && atoi(es) != 0;
+    bool want_kmin = a.pad_unit == 4 && double(theta) * a.T >= double(a.R);
+    if (ek) want_kmin = a.pad_unit == 4 && atoi(ek) != 0;
+    if (a.R <= 4096 && a.thr != INT64_MAX && (want_kstar || want_kmin)) {
+      rc = kstar_launch(w, F, a.R, a.thr, kstar, s);
+      if (want_kstar) a.kstar = kstar;
+      if (want_kmin) a.kmin = kstar + 1;
+    }
   }
   if (rc) return rc;
   if (!pl.pre) {

@@ -57,6 +57,9 @@ struct WalkArgs {
   int nhwc;           // output layout: 0 = [B, F, Ho, Wo], 1 = [B, Ho, Wo, F] (SNN_CONV_OUT_NHWC)
   const int* kstar;   // nullable: K* (kstar_kernel) -- any K* spiking inputs fire every feature, so a
                       // sorted list can end with the first bucket that brings its count to K* (K2b)
+  const int* kmin;    // nullable: word 1 of the K* pair = INT_MAX - kmin, kmin = the fewest spiking inputs that can
+                      // bring ANY feature above the threshold (kstar_kernel); buckets that end below kmin
+                      // entries are added without a threshold test (K2e)
   int pad_unit;       // sorted buckets padded to a multiple of this many entries: 4 (bucket walk) or 2 (K3 blocks)
   int in_nhwc;        // input layout [B, H, W, C] (SNN_CONV_IN_NHWC): receptive-field entries are then
                       // ordered (ky, kx, c) -- e = (ky KW + kx) C + c -- and so are the weight rows
@@ -591,15 +594,20 @@ __device__ __forceinline__ void walk_list(const WalkArgs& a, const unsigned char
       if (int64_t(acc[j]) >= 0) { lo &= ~(0xFFu << (8 * j)); acc[j] = kFiredAcc; }
   }
   if (__ballot_sync(gmask, alive()) == 0) return;
-  // the first non-empty bucket: the group's lanes test LPP buckets per vote
+  // the first bucket that can fire a feature: the first one whose padded end reaches kmin entries (K2e; no
+  // feature crosses the threshold with fewer than kmin inputs, and a padded end bounds the real count from
+  // above); without the bound (need = 1) the first non-empty bucket.  The group's lanes test LPP buckets per vote
   const int gl = int(threadIdx.x & 31) % LPP;
+  int need = 1;
+  if (a.kmin) { const int km = 0x7FFFFFFF - __ldg(a.kmin); need = km > 1 ? km : 1; }
   int t = T;
   for (int tb = 0; tb < T && t == T; tb += LPP) {
     const int tt = tb + gl;
-    const unsigned m = __ballot_sync(gmask, tt < T && int(start[tt + 1]) != 0) & gmask;
+    const unsigned m = __ballot_sync(gmask, tt < T && int(start[tt + 1] & ~3u) >= need) & gmask;
     if (m) t = tb + __ffs(m >> (__ffs(gmask) - 1)) - 1;
   }
-  int b0 = 0;                            // padded start of bucket t (all earlier buckets are empty)
+  int b0 = 0;                            // the first run walked is [0, end of bucket t): the earlier buckets (empty,
+                                         // or below kmin entries: no test needed, pads add 0) together with bucket t
   // header words through a 32-bit shared-window address kept in a register (start[t + 2] = hdr + 2 t + 4)
   uint32_t hdr_a;
   asm volatile("mov.u32 %0, %1;" : "=r"(hdr_a) : "r"(smem_u32(start)));

@@ -143,6 +143,62 @@ def test_conv_fire_vs_oracle(G, orc, case, path, monkeypatch):
     assert np.array_equal(host(v), ov)
 
 
+KMIN_CASES = [
+    # (B, C, H, W, pad, F, K, T, theta, p_spike, weights)   -- presorted bucket walk unless noted
+    (2, 32, 24, 24, 2, 256, 5, 32, 40.0, 0.5, "c5"),     # C5-like: kmin ~ 5 buckets of ~12 entries
+    (2, 32, 12, 12, 2, 100, 5, 2, 40.0, 0.6, "u"),       # 2 huge buckets: kmin inside bucket 0
+    (2, 30, 14, 14, 1, 250, 3, 15, 10.0, 0.9, "c2"),     # C2 L2 shape, FPL = 4 groups
+    (2, 30, 14, 14, 1, 250, 3, 15, 300.0, 0.9, "u"),     # no feature can ever fire (kmin = INT_MAX)
+    (2, 32, 16, 16, 2, 70, 5, 32, 60.0, 0.1, "c5"),      # most lists shorter than kmin: silent without a walk
+    (1, 32, 16, 16, 2, 64, 5, 32, 0.25, 0.5, "u"),       # kmin = 1 (the first non-empty bucket, as before)
+    (2, 32, 16, 16, 2, 64, 5, 32, -1.0, 0.5, "u"),       # theta < 0: kmin = 0
+    (2, 8, 10, 10, 1, 30, 3, 5, 6.0, 1.0, "u"),          # fused sort + bucket walk (one group, F < 32)
+    (3, 16, 20, 20, 1, 96, 3, 12, 25.0, 0.8, "s28"),     # weights on the 2^-28 grid (S28 block sums)
+]
+
+
+@pytest.mark.parametrize("nhwc,kstar", [(False, "0"), (True, "0"), (True, "1"), (False, "1")])
+@pytest.mark.parametrize("case", KMIN_CASES)
+def test_conv_kmin_prefix_vs_oracle(G, orc, case, nhwc, kstar, monkeypatch):
+    """K2e (SNN_KMIN=1 forces it on): buckets that end below kmin entries are added without a threshold
+    test; together with the K* list truncation (K2b, SNN_KSTAR=1) on maps whose spike density and timing
+    vary across positions.  Spike times and potentials stay those of Eq. 2 + R3 (oracle conv_fire)."""
+    monkeypatch.setenv("SNN_KMIN", "1")
+    monkeypatch.setenv("SNN_KSTAR", kstar)
+    B, C, H, W, pad, F, K, T, theta, p, wk = case
+    rng = np.random.default_rng(7000 + KMIN_CASES.index(case))
+    import synth
+    lat_in = synth.random_latencies(rng, (B, C, H, W), T, p)
+    if kstar == "1":                                     # a sparse, late-spiking band next to the dense map
+        band = lat_in[:, :, :, : W // 3]
+        band[rng.random(band.shape) < 0.8] = 255
+        late = lat_in[:, :, H // 2:, W // 3: 2 * W // 3]
+        late[(late != 255) & (late < T // 2)] = T - 1
+    if wk == "c5":
+        w = np.clip(rng.normal(0.5, 0.1, size=(F, C, K, K)), 2.0 ** -8, 1.0).astype(np.float32)
+    elif wk == "c2":
+        w = np.clip(rng.normal(0.8, 0.05, size=(F, C, K, K)), 2.0 ** -8, 1.0).astype(np.float32)
+    elif wk == "s28":
+        w = (rng.integers(2 ** 23, 2 ** 28, size=(F, C, K, K)) / 2.0 ** 28).astype(np.float32)
+        w = (np.round(w.astype(np.float64) * 2 ** 28) / 2 ** 28).astype(np.float32)
+    else:
+        w = exact_weights(rng, (F, C, K, K))
+    ol, ov = orc.conv_fire(lat_in, w, pad, T, theta)
+    if nhwc:
+        lin = cu(np.ascontiguousarray(lat_in.transpose(0, 2, 3, 1)))
+        lat, v = G.conv_fire(lin, cu(w), pad, T, theta, nhwc=True, in_nhwc=True)
+        lat, v = host(lat).transpose(0, 3, 1, 2), host(v).transpose(0, 3, 1, 2)
+    else:
+        lat, v = G.conv_fire(cu(lat_in), cu(w), pad, T, theta)
+        lat, v = host(lat), host(v)
+    G.sync_status()
+    assert np.array_equal(lat, ol)
+    assert np.array_equal(v, ov)
+    monkeypatch.setenv("SNN_KMIN", "0")                  # and the same call without the bound
+    lat0, v0 = G.conv_fire(cu(lat_in), cu(w), pad, T, theta)
+    assert np.array_equal(host(lat0), ol) and np.array_equal(host(v0), ov)
+
+
 @pytest.mark.parametrize("theta", [3.0, math.inf])
 def test_conv_pot_out_vs_oracle_potentials(G, orc, theta):
     rng = np.random.default_rng(5)
