@@ -192,6 +192,8 @@ __device__ __forceinline__ void walk_positions(const WalkArgs& a, unsigned char*
   // channels-last outputs with F % FPL == 0 and aligned pointers: a lane's FPL outputs are contiguous
   const bool vec_out = a.nhwc && (a.F % FPL) == 0 && (reinterpret_cast<uintptr_t>(a.lat_out) % FPL) == 0 &&
                        (reinterpret_cast<uintptr_t>(a.v_out) % (4 * FPL)) == 0;
+  int need = 1;  // K2e: max(kmin, 1), the entries a list needs before any feature can fire
+  if (a.kmin) { const int km = 0x7FFFFFFF - __ldg(a.kmin); need = km > 1 ? km : 1; }
   int npos_done = 0;
   for (int64_t wi = int64_t(blockIdx.x) * nwarps + warp; wi * PPW < a.np; wi += stride_w, ++npos_done) {
     const int64_t q = wi * PPW + grp;
@@ -217,7 +219,7 @@ __device__ __forceinline__ void walk_positions(const WalkArgs& a, unsigned char*
     uint32_t lo;
     float vo[FPL];
     if constexpr (LS) walk_list_lockstep<FPL, PPW, S28>(a, wl, start, list, pv, valid, lo, vo);
-    else walk_list<FPL, PPW, PRE, S28, BW, GW>(a, wl, start, sent, ent, list, pv, valid, gmask, lo, vo);
+    else walk_list<FPL, PPW, PRE, S28, BW, GW>(a, wl, start, sent, ent, list, pv, valid, gmask, lo, vo, need);
     if (pv) {
       // NHWC: the warp's features of one position are contiguous (one or two lines per store);
       // NCHW: every feature is a separate plane (a line per lane per store)
@@ -818,6 +820,7 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   WalkArgs sa = pl.sa;
   sa.in_nhwc = in_nhwc;
   sa.kstar = a.kstar;
+  sa.kmin = a.kmin;  // K2e: the sort leaves the test-free prefix unpadded for the same bound
   sa.lat_in = lat_in; sa.lists = a.lists; sa.hdr = a.hdr; sa.rec = a.rec;
   for (int64_t p0 = 0; p0 < npos; p0 += pl.chunk) {
     a.p0 = p0;

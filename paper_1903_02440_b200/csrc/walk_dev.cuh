@@ -186,12 +186,40 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl
       }
     }
   }
+  // K2e: with the kmin bound the walk adds the buckets before t0 -- the first bucket whose running count
+  // reaches kmin -- as one run together with bucket t0, so those buckets need no pads: they are laid out
+  // back to back (their header words hold the end rounded DOWN to 4 entries, which stays below kmin, pad
+  // bits 0) and bucket t0 is padded so that its END falls on a 4-entry boundary.  cum0 = entries before t0
+  int t0 = -1, cum0 = 0;
+  if (a.kmin && a.pad_unit == 4) {
+    const int km = 0x7FFFFFFF - *a.kmin, need = km > 1 ? km : 1;
+    t0 = 0x7FFFFFFF;
+    int carry_r = 0;
+    for (int tb = 0; tb < T; tb += LPP) {
+      const int t = tb + gl;
+      const int tot = (t < T && t <= tcut) ? int(cnt[t]) : 0;
+      int inc = tot;
+#pragma unroll
+      for (int o = 1; o < LPP; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o, LPP);
+        if (gl >= o) inc += v;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, t < T && carry_r + inc >= need);
+      const unsigned gm = (LPP == 32) ? m : (m >> ((threadIdx.x & 31) / LPP * LPP)) & ((1u << LPP) - 1u);
+      const int src = gm ? __ffs(gm) - 1 : 0;
+      const int before = carry_r + __shfl_sync(0xffffffffu, inc - tot, src, LPP);
+      if (t0 == 0x7FFFFFFF && gm) { t0 = tb + src; cum0 = before; }
+      carry_r += __shfl_sync(0xffffffffu, inc, LPP - 1, LPP);
+    }
+  }
   int carry = 0;
   if (gl == 0) start[0] = 0;
   for (int tb = 0; tb < T; tb += LPP) {
     const int t = tb + gl;
     const int tot = t <= tcut ? int(cnt[t]) : 0;
-    const int padded = (tot + a.pad_unit - 1) & -a.pad_unit;  // 4: buckets 16-byte aligned (bucket walk); 2: pairs
+    int padded = (tot + a.pad_unit - 1) & -a.pad_unit;  // 4: buckets 16-byte aligned (bucket walk); 2: pairs
+    if (t < t0) padded = tot;
+    else if (t == t0) padded = tot + ((-(cum0 + tot)) & 3);
     int inc = padded;
 #pragma unroll
     for (int o = 1; o < LPP; o <<= 1) {
@@ -200,7 +228,8 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl
     }
     const int st = carry + inc - padded;
     if (t < T) {
-      start[t + 1] = uint16_t((st + padded) | (padded - tot));  // padded end | this bucket's pad count
+      start[t + 1] = t < t0 ? uint16_t((st + tot) & ~3)         // K2e: an unpadded bucket of the test-free prefix
+                            : uint16_t((st + padded) | (padded - tot));  // padded end | this bucket's pad count
       cnt[t] = uint32_t(st);                                    // pass 2: running slot of the bucket
       for (int k = tot; k < padded; ++k) list[st + k] = uint32_t(R) * rb;  // pads: the zero-weight row
     }
@@ -561,7 +590,8 @@ __device__ __forceinline__ void walk_list_blocks(const WalkArgs& a, const unsign
 template <int FPL, int PPW, bool PRE, bool S28 = false, bool BW = true, bool GW = false>
 __device__ __forceinline__ void walk_list(const WalkArgs& a, const unsigned char* wl, const uint16_t* start,
                                           const unsigned char* sent, const unsigned char* ent, const uint32_t* list,
-                                          bool pv, unsigned valid, unsigned gmask, uint32_t& lo, float (&vo)[FPL]) {
+                                          bool pv, unsigned valid, unsigned gmask, uint32_t& lo, float (&vo)[FPL],
+                                          int need = 1) {
   if constexpr (!BW) {
     walk_list_blocks<FPL, PPW, PRE, S28, GW>(a, wl, start, sent, ent, list, pv, valid, gmask, lo, vo);
     return;
@@ -596,10 +626,9 @@ __device__ __forceinline__ void walk_list(const WalkArgs& a, const unsigned char
   if (__ballot_sync(gmask, alive()) == 0) return;
   // the first bucket that can fire a feature: the first one whose padded end reaches kmin entries (K2e; no
   // feature crosses the threshold with fewer than kmin inputs, and a padded end bounds the real count from
-  // above); without the bound (need = 1) the first non-empty bucket.  The group's lanes test LPP buckets per vote
+  // above; need = max(kmin, 1), read once per kernel by the caller); without the bound (need = 1) the first
+  // non-empty bucket.  The group's lanes test LPP buckets per vote
   const int gl = int(threadIdx.x & 31) % LPP;
-  int need = 1;
-  if (a.kmin) { const int km = 0x7FFFFFFF - __ldg(a.kmin); need = km > 1 ? km : 1; }
   int t = T;
   for (int tb = 0; tb < T && t == T; tb += LPP) {
     const int tt = tb + gl;
