@@ -44,6 +44,13 @@ struct TcPlan {
   // addition is order-free, so the result stays exact) and a finalize kernel writes (lat, v)
   int KS;
   size_t part_bytes;
+  // K9 (fcP > 0): the layer rewritten as a fully connected one -- a kernel larger than its input (H W < KH KW,
+  // C2's third layer: 5 x 5 on a 4 x 4 map) makes most of the im2col padding, so every output position p
+  // becomes fcF features of a "KH = H, KW = W, pad 0" layer with fcP fcF features, whose weights are the real
+  // kernel shifted by p (zero where the shifted tap leaves the kernel).  fcF = the real F, fcP = the real
+  // Ho Wo; fcW / fcWo / fcPad / fcKH / fcKW = the real geometry (B operand gather, output index).
+  int fcF, fcP, fcW, fcWo, fcPad, fcKH, fcKW;
+  size_t fc_l_bytes;  // K9: the real weights' limb rows L[F][4][KH KW][Cp]
 };
 
 static TcPlan tc_plan(int B, int C, int H, int W, int pad, int KH, int KW, int F, int sms) {
@@ -81,16 +88,43 @@ static TcPlan tc_plan(int B, int C, int H, int W, int pad, int KH, int KW, int F
     if (p.KS < 1) p.KS = 1;
   }
   p.part_bytes = p.KS > 1 ? size_t(p.M) * F * sizeof(int64_t) : 0;
+  p.fcF = p.fcP = p.fcW = p.fcWo = p.fcPad = p.fcKH = p.fcKW = 0;
+  p.fc_l_bytes = 0;
   return p;
 }
 
+// K9: the fully connected rewrite of a theta = inf layer whose kernel is larger than its input.  Returns
+// true and the rewritten plan (virtual layer: pad 0, KH = H, KW = W, Ho Wo F features, one position per
+// image) when it applies: fewer K columns than the im2col (H W < KH KW), the (ky, kx, c) K order (the B
+// gather below assumes it), and a feature count the chunking handles.  SNN_TC_FC=0 turns it off.
+static bool tc_fc_plan(int B, int C, int H, int W, int pad, int KH, int KW, int F, int sms, TcPlan* out) {
+  const int Ho = H + 2 * pad - KH + 1, Wo = W + 2 * pad - KW + 1;
+  if (const char* e = getenv("SNN_TC_FC")) if (e[0] == '0') return false;
+  if (Ho < 1 || Wo < 1 || H * W >= KH * KW || int64_t(Ho) * Wo * F > 32768) return false;
+  TcPlan p = tc_plan(B, C, H, W, 0, H, W, Ho * Wo * F, sms);
+  if (!p.hwc) return false;
+  p.fcF = F; p.fcP = Ho * Wo; p.fcW = W; p.fcWo = Wo; p.fcPad = pad; p.fcKH = KH; p.fcKW = KW;
+  p.fc_l_bytes = (size_t(F) * 4 * KH * KW * p.Cp + 1023) & ~size_t(1023);
+  *out = p;
+  return true;
+}
+
 int conv_tc_launches(int B, int C, int H, int W, int pad, int KH, int KW, int F) {
-  return tc_plan(B, C, H, W, pad, KH, KW, F, num_sms()).KS > 1 ? 4 : 3;  // prep B, prep A, GEMM (+ finalize)
+  TcPlan p = tc_plan(B, C, H, W, pad, KH, KW, F, num_sms()), q;
+  if (tc_fc_plan(B, C, H, W, pad, KH, KW, F, num_sms(), &q)) p = q;  // K9
+  return (p.KS > 1 ? 4 : 3) + (p.fcP ? 1 : 0);  // prep B (K9: two kernels), prep A, GEMM (+ finalize)
 }
 
 size_t conv_tc_workspace(int B, int C, int H, int W, int pad, int KH, int KW, int F) {
   TcPlan p = tc_plan(B, C, H, W, pad, KH, KW, F, num_sms());
-  return ((p.a_bytes + 1023) & ~size_t(1023)) + ((p.b_bytes + 1023) & ~size_t(1023)) + p.part_bytes + 1024;
+  size_t n = ((p.a_bytes + 1023) & ~size_t(1023)) + ((p.b_bytes + 1023) & ~size_t(1023)) + p.part_bytes + 1024;
+  TcPlan q;
+  if (tc_fc_plan(B, C, H, W, pad, KH, KW, F, num_sms(), &q)) {  // K9: either plan may run (prepared A: the first)
+    const size_t m = ((q.a_bytes + 1023) & ~size_t(1023)) + ((q.b_bytes + 1023) & ~size_t(1023)) + q.part_bytes +
+                     q.fc_l_bytes + 2048;
+    if (m > n) n = m;
+  }
+  return n;
 }
 
 // byte offset of element (row, k) inside a [row tiles][K tiles] blocked core-matrix array
@@ -184,6 +218,98 @@ __global__ void tc_prep_b16_kernel(const float* __restrict__ w, int F, int R, in
           make_uint4(limb[l][0], limb[l][1], limb[l][2], limb[l][3]);
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flag_error(err, kErrInexact);
+}
+
+// K9 B operand, stage 1: the real weights as limb rows L[f][limb][tap][Cp] (bytes; tap = ky KW + kx, channels
+// padded to Cp with zeros): one thread per (feature, tap, 16 channels), the arithmetic of tc_prep_b16_kernel.
+__global__ void tc_prep_limbs_kernel(const float* __restrict__ w, int F, int C, int KK, int Cp,
+                                     uint8_t* __restrict__ L, int* err) {
+  pdl_begin();
+  const int nc16 = Cp / 16;
+  const int64_t total = int64_t(F) * KK * nc16;
+  int bad = 0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int c16 = int(i % nc16);
+    const int64_t rest = i / nc16;
+    const int tap = int(rest % KK), f = int(rest / KK), c0 = c16 * 16;
+    float xs[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) xs[j] = c0 + j < C ? __ldg(w + (int64_t(f) * C + c0 + j) * KK + tap) : 0.0f;
+    uint32_t limb[4][4] = {};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float x = xs[j];
+      const float sx = x * 2147483648.0f;
+      if (!(x >= 0.0f && x <= 1.0f) || sx != truncf(sx)) { bad = 1; continue; }
+      const uint32_t q = uint32_t(sx);
+#pragma unroll
+      for (int l = 0; l < 4; ++l) limb[l][j >> 2] |= ((q >> (8 * l)) & 0xFFu) << (8 * (j & 3));
+    }
+#pragma unroll
+    for (int l = 0; l < 4; ++l)
+      *reinterpret_cast<uint4*>(L + ((int64_t(f) * 4 + l) * KK + tap) * Cp + c0) =
+          make_uint4(limb[l][0], limb[l][1], limb[l][2], limb[l][3]);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flag_error(err, kErrInexact);
+}
+
+// K9 B operand, stage 2: the virtual layer's limb rows are 16-byte pieces of L -- virtual feature
+// (position pp = (y, x), real feature fr), virtual tap = input pixel (iy, ix): the real tap
+// (iy - y + pad, ix - x + pad), or zeros where it leaves the kernel.  One thread per (chunk, virtual
+// feature, 16 consecutive k) as in tc_prep_b16_kernel; consecutive threads read consecutive 16-byte pieces.
+__global__ void tc_prep_b_fc_kernel(const uint8_t* __restrict__ L, int Fv, TcPlan p, uint8_t* __restrict__ bq) {
+  pdl_begin();
+  const int nk16 = p.Kp / 16, KK = p.fcKH * p.fcKW;
+  const int64_t total = int64_t(p.nch) * p.Fc * nk16;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int k16 = int(i % nk16);
+    const int64_t rest = i / nk16;
+    const int fl = int(rest % p.Fc), ch = int(rest / p.Fc);
+    const int f = ch * p.Fc + fl, k0 = k16 * 16;
+    const uint8_t* src = nullptr;
+    if (f < Fv && k0 < p.K) {
+      const int pix = k0 / p.Cp, c0 = k0 - pix * p.Cp;
+      const int pp = f / p.fcF, fr = f - pp * p.fcF, y = pp / p.fcWo, x = pp - y * p.fcWo;
+      const int iy = pix / p.fcW, ix = pix - iy * p.fcW;
+      const int ky = iy - y + p.fcPad, kx = ix - x + p.fcPad;
+      if (ky >= 0 && ky < p.fcKH && kx >= 0 && kx < p.fcKW)
+        src = L + (int64_t(fr) * 4 * KK + ky * p.fcKW + kx) * p.Cp + c0;
+    }
+    uint8_t* base = bq + size_t(ch) * p.Kt * p.N * kTcKT;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const uint4 v = src ? __ldg(reinterpret_cast<const uint4*>(src + int64_t(l) * KK * p.Cp)) : make_uint4(0u, 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(base + tc_off(4 * fl + l, k0, p.N, p.Kt)) = v;
+    }
+  }
+}
+
+// K9 A operand: row m = image m, K order (input pixel, channel padded to Cp) -- the binary S[T-1] of the
+// whole (small) input map, no im2col.  One thread per 16-byte core-matrix row (image, pixel, 16 channels),
+// consecutive threads = consecutive images (8 threads fill one 128-byte core matrix); rows M .. Mt * 128
+// and the K padding are zero-filled.
+__global__ void tc_prep_a_fc_kernel(const uint8_t* __restrict__ lat_in, int C, int HW, int T, TcPlan p,
+                                    uint8_t* __restrict__ aq, int in_nhwc) {
+  pdl_begin();
+  const int nk16 = p.Kp / 16, rows = p.Mt * kTcM;
+  const int64_t total = int64_t(rows) * nk16;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int m = int(i % rows), k0 = int(i / rows) * 16;
+    uint32_t wv[4] = {0u, 0u, 0u, 0u};
+    if (m < p.M && k0 < p.K) {
+      const int pix = k0 / p.Cp, c0 = k0 - pix * p.Cp;
+      const uint8_t* lb = lat_in + int64_t(m) * C * HW;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int c = c0 + j;
+        if (c < C) {
+          const uint8_t l = __ldg(lb + (in_nhwc ? int64_t(pix) * C + c : int64_t(c) * HW + pix));
+          wv[j >> 2] |= (l < T ? 1u : 0u) << (8 * (j & 3));
+        }
+      }
+    }
+    *reinterpret_cast<uint4*>(aq + tc_off(m, k0, kTcM, p.Kt)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+  }
 }
 
 // A operand from a shared-memory band: one CTA per (image, band of RB output rows) stages the binary
@@ -487,7 +613,11 @@ __global__ void __launch_bounds__(kTcThreads + 128, 1) conv_tc_kernel(const uint
               atomicAdd(part + int64_t(m) * F + f, (unsigned long long)acc);
               continue;
             }
-            const int64_t o = nhwc ? int64_t(m) * F + f : (int64_t(b) * F + f) * HoWo + rem;
+            int64_t o = nhwc ? int64_t(m) * F + f : (int64_t(b) * F + f) * HoWo + rem;
+            if (p.fcP) {  // K9: virtual feature f = (position pp, real feature fr) of image m
+              const int pp = f / p.fcF, fr = f - pp * p.fcF;
+              o = nhwc ? (int64_t(m) * p.fcP + pp) * p.fcF + fr : (int64_t(m) * p.fcF + fr) * p.fcP + pp;
+            }
             lat_out[o] = acc > 0 ? uint8_t(T - 1) : kNoSpike;
             if (v_out) v_out[o] = fixed_to_float(acc);
           }
@@ -505,14 +635,19 @@ __global__ void __launch_bounds__(kTcThreads + 128, 1) conv_tc_kernel(const uint
 
 // split-K finalize: the summed fixed-point potentials -> (lat, v) (Eq. 5).
 __global__ void conv_tc_finalize_kernel(const unsigned long long* __restrict__ part, int M, int F, int HoWo, int T,
-                                        uint8_t* __restrict__ lat_out, float* __restrict__ v_out, int nhwc) {
+                                        uint8_t* __restrict__ lat_out, float* __restrict__ v_out, int nhwc,
+                                        int fcF, int fcP) {
   pdl_begin();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < int64_t(M) * F;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int m = int(i / F), f = int(i - int64_t(m) * F);
     const int b = m / HoWo, rem = m - b * HoWo;
     const int64_t acc = int64_t(part[i]);
-    const int64_t o = nhwc ? i : (int64_t(b) * F + f) * HoWo + rem;
+    int64_t o = nhwc ? i : (int64_t(b) * F + f) * HoWo + rem;
+    if (fcP) {  // K9 (conv_tc_kernel's epilogue)
+      const int pp = f / fcF, fr = f - pp * fcF;
+      o = nhwc ? (int64_t(m) * fcP + pp) * fcF + fr : (int64_t(m) * fcF + fr) * fcP + pp;
+    }
     lat_out[o] = acc > 0 ? uint8_t(T - 1) : kNoSpike;
     if (v_out) v_out[o] = fixed_to_float(acc);
   }
@@ -555,15 +690,36 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
                    const uint8_t* aq_pre, int nhwc, int in_nhwc) {
   const int Ho = H + 2 * pad - KH + 1, Wo = W + 2 * pad - KW + 1, R = C * KH * KW;
   TcPlan p = tc_plan(B, C, H, W, pad, KH, KW, F, num_sms());
+  // K9: the geometry the A prep and the GEMM see (the fully connected rewrite: one position per image,
+  // Ho Wo F features); the B prep and the output index use the real geometry through p.fc*
+  int pad_v = pad, KH_v = KH, KW_v = KW, Ho_v = Ho, Wo_v = Wo, F_v = F;
+  {
+    TcPlan q;
+    if (!aq_pre && tc_fc_plan(B, C, H, W, pad, KH, KW, F, num_sms(), &q)) {
+      p = q; pad_v = 0; KH_v = H; KW_v = W; Ho_v = Wo_v = 1; F_v = Ho * Wo * F;
+    }
+  }
   const size_t a_off = 0, b_off = (p.a_bytes + 1023) & ~size_t(1023);
   const size_t part_off = b_off + ((p.b_bytes + 1023) & ~size_t(1023));
-  if (ws_bytes < part_off + p.part_bytes) return set_error(SNN_EWORKSPACE, "snn_conv_fire(tc): workspace too small");
+  const size_t l_off = (part_off + p.part_bytes + 1023) & ~size_t(1023);
+  if (ws_bytes < (p.fcP ? l_off + p.fc_l_bytes : part_off + p.part_bytes))
+    return set_error(SNN_EWORKSPACE, "snn_conv_fire(tc): workspace too small");
   unsigned long long* part =
       p.KS > 1 ? reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(ws) + part_off) : nullptr;
   if (part && cudaMemsetAsync(part, 0, p.part_bytes, s) != cudaSuccess) return check_launch("snn_conv_fire(tc) memset");
   uint8_t* aq = reinterpret_cast<uint8_t*>(ws) + a_off;
   uint8_t* bq = reinterpret_cast<uint8_t*>(ws) + b_off;
-  {
+  if (p.fcP) {  // K9: the real limb rows once, then the virtual layer's B as 16-byte pieces of them
+    uint8_t* L = reinterpret_cast<uint8_t*>(ws) + l_off;
+    int64_t blocks = ceil_div(int64_t(F) * KH * KW * (p.Cp / 16), 256);
+    if (blocks > int64_t(num_sms()) * 8) blocks = int64_t(num_sms()) * 8;
+    launch_k(tc_prep_limbs_kernel, dim3(int(blocks)), dim3(256), 0, s, w, F, C, KH * KW, p.Cp, L, error_word_ptr(s));
+    note_launch();
+    blocks = ceil_div(int64_t(p.nch) * p.Fc * (p.Kp / 16), 256);
+    if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
+    launch_k(tc_prep_b_fc_kernel, dim3(int(blocks)), dim3(256), 0, s, static_cast<const uint8_t*>(L), F_v, p, bq);
+    note_launch();
+  } else {
     const int64_t total = int64_t(p.nch) * p.Fc * (p.Kp / 16);
     int64_t blocks = ceil_div(total, 256);
     if (blocks > int64_t(num_sms()) * 8) blocks = int64_t(num_sms()) * 8;
@@ -578,7 +734,7 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
   // prep + bulk-copy GEMM (8 A-writer warps; 4 warps: 0.216 ms) -- per stage the writers' 16-byte loads
   // and stores add ~19 % shared-memory traffic to the MMA's reads and the bulk copies, and every feature
   // chunk's CTA rebuilds the same A tile, which costs more than the prep kernel's HBM round trip saves.
-  if (!aq_pre && p.hwc && in_nhwc && p.Mt <= 65536 && getenv("SNN_TC_IMPLICIT") && getenv("SNN_TC_IMPLICIT")[0] == '1') {
+  if (!aq_pre && !p.fcP && p.hwc && in_nhwc && p.Mt <= 65536 && getenv("SNN_TC_IMPLICIT") && getenv("SNN_TC_IMPLICIT")[0] == '1') {
     const int HoWo = Ho * Wo;
     long foot = 0;
     for (int mt = 0; mt < p.Mt && foot >= 0; ++mt) {
@@ -601,19 +757,24 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
   if (im.lat) {
   } else if (aq_pre) {  // prepared by snn_conv_inf_prepare
     aq = const_cast<uint8_t*>(aq_pre);
+  } else if (p.fcP) {  // K9: the input map itself (binary, channels padded), one row per image
+    int64_t blocks = ceil_div(int64_t(p.Mt) * kTcM * (p.Kp / 16), 256);
+    if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
+    launch_k(tc_prep_a_fc_kernel, dim3(int(blocks)), dim3(256), 0, s, lat_in, C, H * W, T, p, aq, in_nhwc);
+    note_launch();
   } else {
     if (p.hwc) {
-      launch_k(tc_prep_a_hwc_kernel, dim3(unsigned(int64_t(B) * p.nbands + 1)), dim3(256), p.band_smem, s, lat_in, C, H, W, pad, KH, KW,
-                                                                                      Ho, Wo, T, p, B, aq, in_nhwc);
+      launch_k(tc_prep_a_hwc_kernel, dim3(unsigned(int64_t(B) * p.nbands + 1)), dim3(256), p.band_smem, s, lat_in, C, H, W,
+               pad_v, KH_v, KW_v, Ho_v, Wo_v, T, p, B, aq, in_nhwc);
     } else if (p.band) {
       launch_k(tc_prep_a_band_kernel, dim3(unsigned(int64_t(B) * p.nbands + 1)), dim3(256), p.band_smem, s, 
-          lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p, p.RB, p.nbands, B, 1, aq, in_nhwc);
+          lat_in, C, H, W, pad_v, KH_v, KW_v, Ho_v, Wo_v, T, p, p.RB, p.nbands, B, 1, aq, in_nhwc);
     } else {
       const int64_t rows16 = int64_t(p.Mt) * kTcM * (p.Kp / 16);
       int64_t blocks = ceil_div(rows16, 256);
       if (blocks > int64_t(num_sms()) * 16) blocks = int64_t(num_sms()) * 16;
-      launch_k(tc_prep_a_kernel, dim3(int(blocks)), dim3(256), 0, s, lat_in, C, H, W, pad, KH, KW, Ho, Wo, T, p, aq,
-               size_t(0), in_nhwc);
+      launch_k(tc_prep_a_kernel, dim3(int(blocks)), dim3(256), 0, s, lat_in, C, H, W, pad_v, KH_v, KW_v, Ho_v, Wo_v, T, p,
+               aq, size_t(0), in_nhwc);
     }
     note_launch();
   }
@@ -623,16 +784,17 @@ int conv_tc_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad, c
   cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return set_error(SNN_ECUDA, "snn_conv_fire(tc): %s", cudaGetErrorString(e));
   if (getenv("SNN_DEBUG_PLAN"))
-    fprintf(stderr, "tc plan: Mt %d nch %d KS %d N %d Kt %d hwc %d implicit %d foot %d smem %d\n", p.Mt, p.nch, p.KS, p.N,
-            p.Kt, p.hwc, im.lat != nullptr, im.foot, smem);
+    fprintf(stderr, "tc plan: Mt %d nch %d KS %d N %d Kt %d hwc %d implicit %d foot %d smem %d fc %d\n", p.Mt, p.nch, p.KS,
+            p.N, p.Kt, p.hwc, im.lat != nullptr, im.foot, smem, p.fcP);
   launch_k(conv_tc_kernel, dim3(unsigned(int64_t(p.Mt) * p.nch * p.KS)), dim3(im.lat ? kTcThreads + 128 : kTcThreads), smem,
-           s, aq, bq, p, F, Ho * Wo, T, cols, lat_out, v_out, part, nhwc, im);
+           s, aq, bq, p, F_v, Ho_v * Wo_v, T, cols, lat_out, v_out, part, nhwc, im);
   note_launch();
   if (part) {
-    const int64_t n = int64_t(p.M) * F;
+    const int64_t n = int64_t(p.M) * F_v;
     int blocks = int(ceil_div(n, 256));
     if (blocks > num_sms() * 8) blocks = num_sms() * 8;
-    launch_k(conv_tc_finalize_kernel, dim3(blocks), dim3(256), 0, s, part, p.M, F, Ho * Wo, T, lat_out, v_out, nhwc);
+    launch_k(conv_tc_finalize_kernel, dim3(blocks), dim3(256), 0, s, part, p.M, F_v, Ho_v * Wo_v, T, lat_out, v_out, nhwc,
+             p.fcF, p.fcP);
     note_launch();
   }
   return check_launch("snn_conv_fire(tc)");

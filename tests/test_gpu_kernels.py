@@ -199,6 +199,47 @@ def test_conv_kmin_prefix_vs_oracle(G, orc, case, nhwc, kstar, monkeypatch):
     assert np.array_equal(host(lat0), ol) and np.array_equal(host(v0), ov)
 
 
+FC_CASES = [
+    # (B, C, H, W, pad, F, KH, KW, T, p_spike): theta = inf layers whose kernel is larger than the input (K9)
+    (300, 32, 4, 4, 2, 40, 5, 5, 15, 0.8),      # C2 L3-like (4 x 4 map, 5 x 5 kernel), one M tile row ragged
+    (300, 64, 3, 5, 2, 33, 5, 5, 7, 0.6),       # non-square map, F % 4 != 0
+    (310, 64, 2, 4, 2, 20, 3, 7, 9, 0.7),       # non-square kernel: Ho x Wo = 4 x 2 from a 2 x 4 map
+    (300, 250, 4, 4, 2, 200, 5, 5, 15, 0.9),    # C2 L3 shape (channels padded 250 -> 256, 3200 virtual features)
+    (300, 48, 2, 2, 1, 16, 3, 3, 5, 0.5),       # 2 x 2 map, 3 x 3 kernel, pad 1
+]
+
+
+@pytest.mark.parametrize("layout", ["planar", "nhwc_out", "nhwc_in_out"])
+@pytest.mark.parametrize("case", FC_CASES)
+def test_conv_tc_fc_rewrite_vs_oracle(G, orc, case, layout, monkeypatch):
+    """K9: Eq. 5 layers with H W < KH KW run as a fully connected tcgen05 GEMM (one row per image, Ho Wo F
+    virtual features); bit-exact vs the oracle conv_fire, and identical to the im2col plan (SNN_TC_FC=0)."""
+    monkeypatch.setenv("SNN_DEBUG_PLAN", "1")
+    B, C, H, W, pad, F, KH, KW, T, p = case
+    rng = np.random.default_rng(9100 + FC_CASES.index(case))
+    import synth
+    lat_in = synth.random_latencies(rng, (B, C, H, W), T, p)
+    lat_in[1] = 255                                      # an image with no input spike at all
+    w = exact_weights(rng, (F, C, KH, KW))
+    w[0, 0, 0, 0] = 0.0
+    ol, ov = orc.conv_fire(lat_in, w, pad, T, math.inf)
+    lin = cu(np.ascontiguousarray(lat_in.transpose(0, 2, 3, 1))) if layout == "nhwc_in_out" else cu(lat_in)
+    kw = dict(nhwc=layout != "planar", in_nhwc=layout == "nhwc_in_out")
+
+    def run():
+        lat, v = G.conv_fire(lin, cu(w), pad, T, math.inf, **kw)
+        G.sync_status()
+        lat, v = host(lat), host(v)
+        return (lat.transpose(0, 3, 1, 2), v.transpose(0, 3, 1, 2)) if kw["nhwc"] else (lat, v)
+
+    lat, v = run()
+    assert np.array_equal(lat, ol)
+    assert np.array_equal(v, ov)
+    monkeypatch.setenv("SNN_TC_FC", "0")
+    lat0, v0 = run()
+    assert np.array_equal(lat0, ol) and np.array_equal(v0, ov)
+
+
 @pytest.mark.parametrize("theta", [3.0, math.inf])
 def test_conv_pot_out_vs_oracle_potentials(G, orc, theta):
     rng = np.random.default_rng(5)

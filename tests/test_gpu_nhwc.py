@@ -244,6 +244,7 @@ def test_conv_inf_implicit_vs_oracle(G, orc, case, capfd, monkeypatch):
     bit-exact."""
     monkeypatch.setenv("SNN_DEBUG_PLAN", "1")
     monkeypatch.setenv("SNN_TC_IMPLICIT", "1")
+    monkeypatch.setenv("SNN_TC_FC", "0")                 # the im2col plan (K9 takes the C2 L3 shape otherwise)
     B, C, H, W, pad, F, K, p = case
     T = 15
     rng = np.random.default_rng(abs(hash(case)) % 2 ** 31)
