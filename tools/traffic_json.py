@@ -18,11 +18,11 @@ def launches(rep):
 
 
 out = {}
-k2 = launches("traffic_c2.ncu-rep")  # conv1 walk, conv2 sort + walk, conv3 prep_b + prep_a + tc
-assert len(k2) == 6, [x[0][:30] for x in k2]
+k2 = launches("traffic_c2.ncu-rep")  # conv1 walk, conv2 sort + walk, conv3 (K9) prep limbs + prep_b + prep_a + tc
+assert len(k2) == 7, [x[0][:30] for x in k2]
 out["c2:conv1"] = k2[0][1]
 out["c2:conv2"] = k2[1][1] + k2[2][1]
-out["c2:conv3"] = k2[3][1] + k2[4][1] + k2[5][1]
+out["c2:conv3"] = sum(x[1] for x in k2[3:])
 k5 = launches("traffic_c5.ncu-rep")  # 2 (sort, walk) chunk pairs of C5 conv1
 chunks = snn.conv_fire_plan(64, 32, 256, 256, 2, 256, 5, 5, 32, 40.0)["chunks"]
 out["c5:conv1"] = sum(x[1] for x in k5) / 2 * chunks
