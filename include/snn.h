@@ -131,7 +131,9 @@ SNN_API int snn_validate_lat(const uint8_t* lat, size_t n, int T, int32_t* n_bad
  *           mode, no early exit).
  * Workspace: snn_conv_fire_workspace(..., theta) bytes.  theta = +inf without pot_out runs the
  * tensor-core path (tcgen05 kind::i8, exact 4-limb split of the fixed-point weights); its workspace
- * holds the binary im2col of S[T-1] (positions x C*KH*KW bytes) and the weight limbs.
+ * holds the binary im2col of S[T-1] (positions x C*KH*KW bytes) and the weight limbs.  A kernel larger
+ * than the input map (H*W < KH*KW, e.g. 5 x 5 on a 4 x 4 map) runs as one fully connected contraction per
+ * image over the H*W*C input pixels instead (same Eq. 5 values, no im2col; K9).
  * Finite theta: any receptive field R = C*KH*KW up to ~65,000 entries (a sorted list's u16 bucket
  * starts); a layer whose weight slice does not fit shared memory (R above ~1,700 for 32 features)
  * walks from the prepared slice in global memory (L2).  With pot_out (validation mode) the weight

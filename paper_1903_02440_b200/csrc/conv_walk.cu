@@ -780,16 +780,19 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   int rc = weight_prep_launch(w, F, a.R, pl.FGS, pl.n_groups, reinterpret_cast<uint32_t*>(ws), s, in_nhwc ? C : 0,
                               KH * KW);
   if (rc) return rc;
-  // K* bound for the list truncation (K2b, opt-in with SNN_KSTAR=1: measured no faster -- C2 1.06 ->
-  // 1.18 ms for conv1 + conv2, C5 unchanged -- the sort's first pass, not its placements, sets its time)
+  // K* bound for the list truncation (K2b; on its own measured no faster -- C2 1.06 -> 1.18 ms for conv1 +
+  // conv2 -- the sort's first pass, not its placements, sets its time -- so it only rides along with kmin)
   // kmin bound for the test-free list prefix (K2e): on for the bucket walk where the threshold needs several
   // average buckets of inputs (theta >= R / T: C5 conv 27.8 -> 26.1 ms; C2's second layer, whose kmin is about
   // one bucket, measured 0.676 -> 0.691 ms with it); SNN_KMIN=0 / 1 overrides
   {
     const char* ek = getenv("SNN_KMIN");
     const char* es = getenv("SNN_KSTAR");
-    const bool want_kstar = es && atoi(es) != 0;
     bool want_kmin = a.pad_unit == 4 && double(theta) * a.T >= double(a.R);
+    // K2b list truncation at K*: free where the bound is computed anyway (presorted lists; C5 conv 24.83 ->
+    // 24.68 ms: fewer placements and shorter records to copy); SNN_KSTAR=0 / 1 overrides
+    bool want_kstar = want_kmin && pl.pre;
+    if (es) want_kstar = atoi(es) != 0;
     if (ek) want_kmin = a.pad_unit == 4 && atoi(ek) != 0;
     if (a.R <= 4096 && a.thr != INT64_MAX && (want_kstar || want_kmin)) {
       rc = kstar_launch(w, F, a.R, a.thr, kstar, s);
