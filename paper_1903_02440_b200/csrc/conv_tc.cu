@@ -285,16 +285,19 @@ __global__ void tc_prep_b_fc_kernel(const uint8_t* __restrict__ L, int Fv, TcPla
 }
 
 // K9 A operand: row m = image m, K order (input pixel, channel padded to Cp) -- the binary S[T-1] of the
-// whole (small) input map, no im2col.  One thread per 16-byte core-matrix row (image, pixel, 16 channels),
-// consecutive threads = consecutive images (8 threads fill one 128-byte core matrix); rows M .. Mt * 128
-// and the K padding are zero-filled.
+// whole (small) input map, no im2col.  One thread per 16-byte core-matrix row (image, pixel, 16 channels);
+// a warp takes 8 consecutive images x 4 consecutive 16-channel pieces, i.e. four whole 128-byte core
+// matrices per store and 64 contiguous input bytes per image per load step (channels-last input); rows
+// M .. Mt * 128 and the K padding are zero-filled.  (Kp is a multiple of 128, so nk16 is a multiple of 4.)
 __global__ void tc_prep_a_fc_kernel(const uint8_t* __restrict__ lat_in, int C, int HW, int T, TcPlan p,
                                     uint8_t* __restrict__ aq, int in_nhwc) {
   pdl_begin();
-  const int nk16 = p.Kp / 16, rows = p.Mt * kTcM;
+  const int nk16 = p.Kp / 16, rows = p.Mt * kTcM, mblocks = rows / 8;
   const int64_t total = int64_t(rows) * nk16;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int m = int(i % rows), k0 = int(i / rows) * 16;
+    const int lane = int(i & 31);
+    const int64_t wg = i >> 5;  // (8-image block, quad of 16-channel pieces); total is a multiple of 32
+    const int m = int(wg % mblocks) * 8 + (lane & 7), k0 = (int(wg / mblocks) * 4 + (lane >> 3)) * 16;
     uint32_t wv[4] = {0u, 0u, 0u, 0u};
     if (m < p.M && k0 < p.K) {
       const int pix = k0 / p.Cp, c0 = k0 - pix * p.Cp;
