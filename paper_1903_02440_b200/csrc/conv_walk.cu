@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(512) rf_sort_kernel(const WalkArgs a) {
   for (int64_t wi = int64_t(blockIdx.x) * nwarps + warp; wi * PPW < a.np; wi += int64_t(gridDim.x) * nwarps) {
     const int64_t q = wi * PPW + grp;  // chunk-relative position
     const bool pv = q < a.np;
-    rf_sort_warp<PPW>(a, smem, wbase, wi * PPW, lane, grp, gl, pv, cnt, start, list);
+    rf_sort_warp<PPW, true>(a, smem, wbase, wi * PPW, lane, grp, gl, pv, cnt, start, list);
     if (pv) {  // record = [header: T+1 u16 starts, 16-aligned][entries: u32, whole blocks]
       unsigned char* rec = a.lists + q * a.rec;
       uint16_t* hdr = reinterpret_cast<uint16_t*>(rec);
@@ -192,8 +192,10 @@ __device__ __forceinline__ void walk_positions(const WalkArgs& a, unsigned char*
   // channels-last outputs with F % FPL == 0 and aligned pointers: a lane's FPL outputs are contiguous
   const bool vec_out = a.nhwc && (a.F % FPL) == 0 && (reinterpret_cast<uintptr_t>(a.lat_out) % FPL) == 0 &&
                        (reinterpret_cast<uintptr_t>(a.v_out) % (4 * FPL)) == 0;
-  int need = 1;  // K2e: max(kmin, 1), the entries a list needs before any feature can fire
-  if (a.kmin) { const int km = 0x7FFFFFFF - __ldg(a.kmin); need = km > 1 ? km : 1; }
+  int need = 1;  // K2e (presorted lists): max(kmin, 1), the entries a list needs before any feature can fire
+  if constexpr (PRE) {
+    if (a.kmin) { const int km = 0x7FFFFFFF - __ldg(a.kmin); need = km > 1 ? km : 1; }
+  }
   int npos_done = 0;
   for (int64_t wi = int64_t(blockIdx.x) * nwarps + warp; wi * PPW < a.np; wi += stride_w, ++npos_done) {
     const int64_t q = wi * PPW + grp;
@@ -788,12 +790,12 @@ int conv_walk_launch(const uint8_t* lat_in, int B, int C, int H, int W, int pad,
   {
     const char* ek = getenv("SNN_KMIN");
     const char* es = getenv("SNN_KSTAR");
-    bool want_kmin = a.pad_unit == 4 && double(theta) * a.T >= double(a.R);
+    bool want_kmin = pl.pre && a.pad_unit == 4 && double(theta) * a.T >= double(a.R);
     // K2b list truncation at K*: free where the bound is computed anyway (presorted lists; C5 conv 24.83 ->
     // 24.68 ms: fewer placements and shorter records to copy); SNN_KSTAR=0 / 1 overrides
-    bool want_kstar = want_kmin && pl.pre;
+    bool want_kstar = want_kmin;
     if (es) want_kstar = atoi(es) != 0;
-    if (ek) want_kmin = a.pad_unit == 4 && atoi(ek) != 0;
+    if (ek) want_kmin = pl.pre && a.pad_unit == 4 && atoi(ek) != 0;
     if (a.R <= 4096 && a.thr != INT64_MAX && (want_kstar || want_kmin)) {
       rc = kstar_launch(w, F, a.R, a.thr, kstar, s);
       if (want_kstar) a.kstar = kstar;

@@ -134,7 +134,7 @@ __device__ __forceinline__ uint8_t rf_lat(const WalkArgs& a, const int32_t* eoff
 // bucket's running position.  Entries are weight-row byte offsets e * row_bytes; the tail is padded
 // to a whole walk iteration.  The order inside a bucket is whatever the atomics gave: it does
 // not change any result (the sum at a bucket end is exact and order-free).
-template <int LPP, class Lat>
+template <int LPP, bool KM = false, class Lat>
 __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl, uint32_t* cnt, uint16_t* start,
                                               uint32_t* list, Lat lat_of) {
   const int R = a.R, T = a.T;
@@ -190,8 +190,9 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl
   // reaches kmin -- as one run together with bucket t0, so those buckets need no pads: they are laid out
   // back to back (their header words hold the end rounded DOWN to 4 entries, which stays below kmin, pad
   // bits 0) and bucket t0 is padded so that its END falls on a 4-entry boundary.  cum0 = entries before t0
+  // (KM: only the presorted sort kernel compiles this in -- the fused kernels never get the bound)
   int t0 = -1, cum0 = 0;
-  if (a.kmin && a.pad_unit == 4) {
+  if (KM && a.kmin && a.pad_unit == 4) {
     const int km = 0x7FFFFFFF - *a.kmin, need = km > 1 ? km : 1;
     t0 = 0x7FFFFFFF;
     int carry_r = 0;
@@ -270,7 +271,7 @@ __device__ __forceinline__ void rf_sort_group(const WalkArgs& a, bool pv, int gl
 // fields is first staged once into the warp's shared-memory patch (one coalesced-ish byte gather,
 // bounds checked once per patch element); both sort passes then read latencies from the patch.
 // Otherwise (a warp straddling a row end) each group reads its latencies from global memory.
-template <int PPW>
+template <int PPW, bool KM = false>
 __device__ __forceinline__ void rf_sort_warp(const WalkArgs& a, const unsigned char* tabs, unsigned char* wbase,
                                              int64_t q0, int lane, int grp, int gl, bool pv, uint32_t* cnt,
                                              uint16_t* start, uint32_t* list) {
@@ -298,7 +299,7 @@ __device__ __forceinline__ void rf_sort_warp(const WalkArgs& a, const unsigned c
     }
     __syncwarp();
     const uint8_t* pg = patch + grp * (a.in_nhwc ? a.C : 1);  // the group's position is grp columns right
-    rf_sort_group<LPP>(a, pv, gl, cnt, start, list, [&](int e) { return int(pg[eoffp[e]]); });
+    rf_sort_group<LPP, KM>(a, pv, gl, cnt, start, list, [&](int e) { return int(pg[eoffp[e]]); });
   } else {
     const int32_t* eoff = reinterpret_cast<const int32_t*>(tabs + a.off_eoff);
     const uint16_t* ekk = reinterpret_cast<const uint16_t*>(tabs + a.off_ekk);
@@ -310,9 +311,9 @@ __device__ __forceinline__ void rf_sort_warp(const WalkArgs& a, const unsigned c
     const uint8_t* in = a.lat_in + int64_t(b) * CHW + (int64_t(y0) * a.W + x0) * (a.in_nhwc ? a.C : 1);
     const bool interior = y0 >= 0 && x0 >= 0 && y0 + a.KH <= a.H && x0 + a.KW <= a.W;
     if (PPW == 1 && interior)  // no bounds tests: the loads of an unrolled group issue back to back
-      rf_sort_group<LPP>(a, pv, gl, cnt, start, list, [&](int e) { return int(__ldg(in + eoff[e])); });
+      rf_sort_group<LPP, KM>(a, pv, gl, cnt, start, list, [&](int e) { return int(__ldg(in + eoff[e])); });
     else  // (PPW > 1 only reaches here for a warp straddling a row end: one lambda keeps its code small)
-      rf_sort_group<LPP>(a, pv, gl, cnt, start, list,
+      rf_sort_group<LPP, KM>(a, pv, gl, cnt, start, list,
                          [&](int e) { return int(rf_lat(a, eoff, ekk, in, interior, y0, x0, e)); });
   }
 }
