@@ -152,7 +152,7 @@ KMIN_CASES = [
     (2, 32, 16, 16, 2, 70, 5, 32, 60.0, 0.1, "c5"),      # most lists shorter than kmin: silent without a walk
     (1, 32, 16, 16, 2, 64, 5, 32, 0.25, 0.5, "u"),       # kmin = 1 (the first non-empty bucket, as before)
     (2, 32, 16, 16, 2, 64, 5, 32, -1.0, 0.5, "u"),       # theta < 0: kmin = 0
-    (2, 8, 10, 10, 1, 30, 3, 5, 6.0, 1.0, "u"),          # fused sort + bucket walk (one group, F < 32)
+    (2, 8, 10, 10, 1, 30, 3, 5, 6.0, 1.0, "u"),          # fused sort + bucket walk: the bound is not applied there
     (3, 16, 20, 20, 1, 96, 3, 12, 25.0, 0.8, "s28"),     # weights on the 2^-28 grid (S28 block sums)
 ]
 
